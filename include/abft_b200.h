@@ -1,0 +1,180 @@
+/*
+ * abft_b200.h — C-ABI of the B200-native ABFT-protected blocked factorization
+ * library (libabft_b200.so). Plain pointers and sizes only; no torch types.
+ *
+ * The reference (`slackwise`, pure Python/numpy) has no FFI; its "operator
+ * API" for this hot path is the set of Python names listed in SURVEY.md §8b.
+ * Each entry point below names the reference interface it replaces
+ * (file:line under /root/reference/pkg/src/slackwise/). The Python mirror in
+ * paper_2301_03166_b200/ binds these with ctypes (INTEGRATION.md shows the
+ * binding a maintainer would add to the reference).
+ *
+ * All matrices are column-major (Fortran order, as the reference's
+ * `np.asfortranarray` / `order="F"` working copy, linalg.py:78,180), float64.
+ * Return codes: 0 on success, negative on error (see ABFT_E_*); the message
+ * is available from abft_last_error() on the calling thread.
+ */
+#ifndef ABFT_B200_H
+#define ABFT_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define ABFT_API __attribute__((visibility("default")))
+#else
+#define ABFT_API
+#endif
+
+/* error codes -------------------------------------------------------------- */
+#define ABFT_OK 0
+#define ABFT_E_INVALID (-1)   /* ValueError (e.g. encode with scheme NONE, abft.py:97-98) */
+#define ABFT_E_DIM (-2)       /* InvalidDimensionError (linalg.py:37-38, :52-53, :313-316) */
+#define ABFT_E_BREAKDOWN (-3) /* NumericBreakdownError (linalg.py:41-43, :223-224, :234-235) */
+#define ABFT_E_RANGE (-4)     /* IndexError: fault outside matrix (abft.py:287-288) */
+#define ABFT_E_INCOMPLETE (-5)/* reconstruct before completion (linalg.py:341-342) */
+#define ABFT_E_OVERFLOW (-6)  /* event buffer too small */
+/* <= -1000: CUDA runtime error (-1000 - cudaError_t) */
+
+/* enums mirror DecompositionKind / ChecksumScheme / ErrorKind / TaskKind ---- */
+enum { ABFT_CHOLESKY = 0, ABFT_LU = 1, ABFT_QR = 2 };          /* linalg.py:24-27 */
+enum { ABFT_NONE = 0, ABFT_SINGLE = 1, ABFT_FULL = 2 };         /* abft.py:36-39 */
+enum { ABFT_D0 = 0, ABFT_D1 = 1, ABFT_D2 = 2 };                 /* abft.py:42-45 */
+enum { ABFT_TASK_PD = 0, ABFT_TASK_PU = 1, ABFT_TASK_TMU = 2 };  /* linalg.py:30-34 */
+
+/* One planned fault (InjectedFault, abft.py:48-57). Two magnitude forms:
+ *  absolute != 0: `magnitude` is applied as given (inject_faults, abft.py:283-307)
+ *  absolute == 0: magnitude = (u * 1e-3) * max(scale, 1), negated if `negate`,
+ *                 with scale = max|region| computed on the device after the
+ *                 trailing update — exactly sample_fault_plan's formula
+ *                 (abft.py:319-321, simulator.py:159-162); the host draws
+ *                 (row, col, u, negate) with the caller's numpy Generator. */
+typedef struct {
+  int32_t kind;        /* ABFT_D0/D1/D2 */
+  int32_t orientation; /* 0 = "col", 1 = "row" (1-D streak direction) */
+  int64_t row;         /* global row */
+  int64_t col;         /* global column */
+  int32_t extent;
+  int32_t absolute;
+  double u;
+  int32_t negate;
+  int32_t _pad;
+  double magnitude;
+} abft_fault;
+
+/* One CorrectionReport location (abft.py:60-84): (row, col, kind, flag). For a
+ * corrected 0-D element row/col are the element's global indices; otherwise
+ * the block's top-left corner. `detected_kind` is the ErrorKind counted in
+ * report.detected for this event; `corrected` says report.corrected was
+ * incremented; `uncorrectable` says report.uncorrectable was set. */
+typedef struct {
+  int64_t row;
+  int64_t col;
+  int32_t kind;
+  int32_t flag;
+  int32_t detected_kind;
+  int32_t corrected;
+  int32_t uncorrectable;
+  int32_t block_row; /* region-local block indices (ordering key) */
+  int32_t block_col;
+  int32_t seq;
+} abft_location;
+
+typedef struct {
+  int64_t detected[3];
+  int64_t corrected[3];
+  int32_t uncorrectable;
+  int32_t n_locations; /* events produced (may exceed the caller's buffer) */
+} abft_report;
+
+/* library ------------------------------------------------------------------ */
+ABFT_API int abft_version(void);
+ABFT_API const char* abft_last_error(void);
+ABFT_API int abft_device_count(int* count);
+
+/* device-pointer primitive (for integrators that own device memory):
+ * D = beta*C + alpha*op(A)*op(B) on `stream` (cudaStream_t, may be NULL). */
+ABFT_API int abft_dev_dgemm(void* stream, char transa, char transb, int64_t m, int64_t n,
+                            int64_t k, double alpha, const double* A, int64_t lda,
+                            const double* B, int64_t ldb, double beta, const double* C,
+                            int64_t ldc, double* D, int64_t ldd);
+
+/* factorization context: replaces Factorization (linalg.py:159-359) -------- */
+typedef struct abft_ctx abft_ctx;
+
+/* Factorization(kind, a0, b).__post_init__ (linalg.py:175-180). */
+ABFT_API int abft_create(abft_ctx** ctx, int kind, int64_t n, int64_t b, int device);
+ABFT_API int abft_destroy(abft_ctx* ctx);
+/* copy the host input (column-major, leading dim lda) into the device working matrix */
+ABFT_API int abft_set_matrix(abft_ctx* ctx, const double* a, int64_t lda);
+/* keep a device copy of the input for abft_residual(ctx, NULL, ...) */
+ABFT_API int abft_keep_input(abft_ctx* ctx, int keep);
+/* Factorization.m (host mirror): copy the device working matrix out */
+ABFT_API int abft_get_matrix(abft_ctx* ctx, double* m, int64_t ldm);
+/* Factorization.k_done */
+ABFT_API int64_t abft_k_done(abft_ctx* ctx);
+ABFT_API int abft_set_k_done(abft_ctx* ctx, int64_t k);
+/* task_pd / task_pu / task_tmu (linalg.py:192-258), unprotected */
+ABFT_API int abft_task(abft_ctx* ctx, int64_t k, int task);
+/* run_numeric_iteration (simulator.py:97-121): PD/PU + protected TMU with the
+ * fault plan injected between maintenance and verification. Synchronous;
+ * fills `rep` and up to `max_locs` locations in reference order. */
+ABFT_API int abft_iteration(abft_ctx* ctx, int64_t k, int scheme, const abft_fault* plan,
+                            int nplan, int correct, abft_report* rep, abft_location* locs,
+                            int max_locs);
+/* Whole remaining factorization in one call (no per-iteration host sync).
+ * schemes[k] per iteration (NULL: `scheme` for all); faults are given as a
+ * flat plan with plan_iter[i] = iteration of fault i (plans pre-drawn on the
+ * host in sample_fault_plan order). reports: n_blocks entries (may be NULL). */
+ABFT_API int abft_factorize(abft_ctx* ctx, int scheme, const int32_t* schemes,
+                            const abft_fault* plan, const int64_t* plan_iter, int nplan,
+                            int correct, abft_report* reports, abft_location* locs,
+                            int max_locs, int* n_locs);
+/* QR side data: qr_t[k] (w x w) and _qr_vs[k] (nk x w) (linalg.py:294-308) */
+ABFT_API int abft_qr_panels(abft_ctx* ctx);
+/* `del qr_t[n:]` / _qr_vs truncation in _Run._restore (simulator.py:431-435) */
+ABFT_API int abft_set_qr_panels(abft_ctx* ctx, int count);
+ABFT_API int abft_get_qr_panel(abft_ctx* ctx, int64_t k, double* V, int64_t ldv, double* T,
+                               int64_t ldt);
+/* in-device snapshot slots replacing _Run._snapshot/_restore (simulator.py:420-436) */
+ABFT_API int abft_snapshot(abft_ctx* ctx, int slot);
+ABFT_API int abft_restore(abft_ctx* ctx, int slot);
+/* residual(a, factors) (linalg.py:362-368); a0 == NULL uses the kept input */
+ABFT_API int abft_residual(abft_ctx* ctx, const double* a0, int64_t lda, double* out);
+/* Factorization.reconstruct() (linalg.py:340-359) into a host n x n array */
+ABFT_API int abft_reconstruct(abft_ctx* ctx, double* out, int64_t ldo);
+/* test/debug accessor for the device checksum arrays (see ctx.cu) */
+ABFT_API int abft_debug_array(abft_ctx* ctx, int which, double* out, int64_t* rows,
+                              int64_t* cols);
+/* column index of the last NumericBreakdownError */
+ABFT_API int64_t abft_breakdown_column(abft_ctx* ctx);
+/* synchronize the context stream and return accumulated device time (ms) of
+ * the last abft_factorize/abft_iteration call, measured with CUDA events */
+ABFT_API int abft_last_elapsed_ms(abft_ctx* ctx, double* ms);
+
+/* region ABFT on host arrays: encode / maintain_gemm / verify_correct /
+ * inject_faults (abft.py:118-307), executed on the device. Checksums are
+ * column-major arrays: col_plain/col_weighted (nbr x cols, ld nbr),
+ * row_plain/row_weighted (rows x nbc, ld rows), block_max (nbr x nbc). ------ */
+ABFT_API int abft_region_encode(const double* m, int64_t ldm, int64_t rows, int64_t cols,
+                                int64_t b, int scheme, double* col_plain, double* col_weighted,
+                                double* row_plain, double* row_weighted);
+ABFT_API int abft_region_maintain(int64_t rows, int64_t cols, int64_t kdim, int64_t b, int scheme,
+                                  const double* left, int64_t ldl, const double* right,
+                                  int64_t ldr, double* col_plain, double* col_weighted,
+                                  double* row_plain, double* row_weighted);
+ABFT_API int abft_region_verify(double* m, int64_t ldm, int64_t rows, int64_t cols, int64_t b,
+                                int scheme, int correct, int64_t r0, int64_t c0,
+                                const double* col_plain, const double* col_weighted,
+                                const double* row_plain, abft_report* rep, abft_location* locs,
+                                int max_locs);
+ABFT_API int abft_inject(double* m, int64_t ldm, int64_t n_rows, int64_t n_cols,
+                         const abft_fault* plan, int nplan, double scale);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ABFT_B200_H */

@@ -1,0 +1,544 @@
+// ABFT kernels: block checksums (K1), verify/classify/repair (K2), fault
+// injection (K7) and small element/reduction kernels.
+//
+// These restate, on the device, the reference's per-block Python loops in
+// /root/reference/pkg/src/slackwise/abft.py (encode :118-135, verify_correct
+// :174-205, _handle_single :216-238, _handle_full :241-276, inject_faults
+// :283-307). K1 is HBM-bound (one read of the region, no re-reads); K2 reads
+// only the O(n^2/b) checksum vectors plus the few blocks it repairs.
+#include "abft_kernels.cuh"
+
+#include <cfloat>
+
+namespace abft {
+
+namespace {
+
+constexpr int BS_THREADS = 256;  // 8 warps
+constexpr int BS_ROWS = 256;     // rows per chunk (8 per lane)
+
+// One CTA per block (grid-stride). Warp w takes columns w, w+8, ...; lane l
+// takes rows l + 32*i of the current 256-row chunk.
+__global__ void __launch_bounds__(BS_THREADS)
+    blocksum_kernel(Region reg, SumOut out, int64_t nbr, int64_t nbc, const int32_t* blocks,
+                    const int32_t* nblocks_dev, int64_t nlist_static) {
+  extern __shared__ double dsm[];
+  double* colacc_p = dsm;             // [b]
+  double* colacc_w = dsm + reg.b;     // [b]
+  __shared__ double srow[8][BS_ROWS];
+  __shared__ double srw[8][BS_ROWS];
+  __shared__ double smax[8];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t total = blocks ? (nblocks_dev ? (int64_t)*nblocks_dev : nlist_static) : nbr * nbc;
+  const bool want_rw = out.rw != nullptr;
+  const bool want_rp = out.rp != nullptr;
+
+  for (int64_t blk = blockIdx.x; blk < total; blk += gridDim.x) {
+    int64_t bi, bj;
+    if (blocks) {
+      bi = blocks[2 * blk];
+      bj = blocks[2 * blk + 1];
+    } else {
+      bi = blk % nbr;
+      bj = blk / nbr;
+    }
+    const int64_t r_lo = bi * reg.b, c_lo = bj * reg.b;
+    const int br = (int)min(reg.b, reg.rows - r_lo);
+    const int bc = (int)min(reg.b, reg.cols - c_lo);
+    const double* base = reg.ptr + r_lo + c_lo * reg.ld;
+    double mx = 0.0;
+    for (int c = threadIdx.x; c < bc; c += BS_THREADS) {
+      colacc_p[c] = 0.0;
+      colacc_w[c] = 0.0;
+    }
+    __syncthreads();
+    for (int r0 = 0; r0 < br; r0 += BS_ROWS) {
+      double racc[8], rwacc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) racc[i] = rwacc[i] = 0.0;
+      for (int c = warp; c < bc; c += 8) {
+        const double* col = base + (int64_t)c * reg.ld + r0;
+        double x[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = lane + 32 * i;
+          x[i] = (r0 + r < br) ? col[r] : 0.0;
+        }
+        double cs = 0.0, cw = 0.0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = lane + 32 * i;
+          cs += x[i];
+          cw += (double)(r0 + r) * x[i];
+          racc[i] += x[i];
+          if (want_rw) rwacc[i] += (double)c * x[i];
+          mx = fmax(mx, fabs(x[i]));
+        }
+        cs = warp_sum(cs);
+        cw = warp_sum(cw);
+        if (lane == 0) {
+          colacc_p[c] += cs;
+          colacc_w[c] += cw;
+        }
+      }
+      if (want_rp || want_rw) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          srow[warp][lane + 32 * i] = racc[i];
+          srw[warp][lane + 32 * i] = rwacc[i];
+        }
+        __syncthreads();
+        const int r = threadIdx.x;
+        if (r0 + r < br) {
+          double s = 0.0, sw = 0.0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) {
+            s += srow[w][r];
+            sw += srw[w][r];
+          }
+          if (want_rp) out.rp[r_lo + r0 + r + bj * out.rp_ld] = s;
+          if (want_rw) out.rw[r_lo + r0 + r + bj * out.rw_ld] = sw;
+        }
+        __syncthreads();
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < bc; c += BS_THREADS) {
+      if (out.cp) out.cp[out.cp_step * bi + (c_lo + c) * out.cp_ld] = colacc_p[c];
+      if (out.cw) out.cw[out.cw_step * bi + (c_lo + c) * out.cw_ld] = colacc_w[c];
+    }
+    mx = warp_max(mx);
+    if (lane == 0) smax[warp] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0 && out.bm) {
+      double m = smax[0];
+      for (int w = 1; w < 8; ++w) m = fmax(m, smax[w]);
+      out.bm[bi + bj * out.bm_ld] = m;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2
+// ---------------------------------------------------------------------------
+ABFT_DEVINL void emit(const EventSink& s, int bi, int bj, int seq, int kind, int64_t row,
+                      int64_t col, int flag, int det, int corr, int unc) {
+  const int slot = atomicAdd(s.count, 1);
+  if (slot < s.capacity) {
+    Event e;
+    e.bi = bi;
+    e.bj = bj;
+    e.seq = seq;
+    e.kind = kind;
+    e.row = row;
+    e.col = col;
+    e.flag = flag;
+    e.detected_kind = det;
+    e.corrected = corr;
+    e.uncorrectable = unc;
+    s.ev[slot] = e;
+  }
+}
+
+ABFT_DEVINL void mark_dirty(const EventSink& s, int bi, int bj) {
+  if (!s.dirty) return;
+  const int slot = atomicAdd(s.dirty_count, 1);
+  if (slot < s.dirty_capacity) {
+    s.dirty[2 * slot] = bi;
+    s.dirty[2 * slot + 1] = bj;
+  }
+}
+
+// Python's round() is round-half-to-even; rint() matches under the default
+// rounding mode (abft.py:208-213).
+ABFT_DEVINL bool recovered_index(double dw, double dp, int limit, int* idx) {
+  const double ratio = dw / dp;
+  const double r = rint(ratio);
+  if (fabs(ratio - r) <= 1e-2 && r >= 0.0 && r < (double)limit) {
+    *idx = (int)r;
+    return true;
+  }
+  return false;
+}
+
+__global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct, SumOut rec,
+                              Maintained mt, EventSink sink, int64_t nbr, int64_t nbc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
+  const bool full = (scheme == 2);
+  for (int64_t blk = wid; blk < nbr * nbc; blk += nw) {
+    const int bi = (int)(blk % nbr), bj = (int)(blk / nbr);
+    const int64_t r_lo = bi * reg.b, c_lo = bj * reg.b;
+    const int br = (int)min(reg.b, reg.rows - r_lo);
+    const int bc = (int)min(reg.b, reg.cols - c_lo);
+    const double bmax = rec.bm[bi + bj * rec.bm_ld];
+    const double tau = 50.0 * (double)b_nom * fmax(bmax, 1.0) * DBL_EPSILON;
+    int nbad_c = 0, nbad_r = 0;
+    for (int c = lane; c < bc; c += 32) {
+      const int64_t gc = c_lo + c;
+      const double d = rec.cp[rec.cp_step * bi + gc * rec.cp_ld] - mt.cp[mt.cp_step * bi + gc * mt.cp_ld];
+      nbad_c += (fabs(d) > tau) ? 1 : 0;
+    }
+    if (full) {
+      for (int r = lane; r < br; r += 32) {
+        const int64_t gr = r_lo + r;
+        const double d = rec.rp[gr + bj * rec.rp_ld] - mt.rp[gr + bj * mt.rp_ld];
+        nbad_r += (fabs(d) > tau) ? 1 : 0;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      nbad_c += __shfl_xor_sync(0xffffffffu, nbad_c, o);
+      nbad_r += __shfl_xor_sync(0xffffffffu, nbad_r, o);
+    }
+    if (nbad_c == 0 && nbad_r == 0) continue;
+    if (lane != 0) continue;
+    // ---- rare path: one lane classifies and repairs, in reference order ----
+    double* blkp = reg.ptr + r_lo + c_lo * reg.ld;
+    auto dcol = [&](int c) {
+      const int64_t gc = c_lo + c;
+      return rec.cp[rec.cp_step * bi + gc * rec.cp_ld] - mt.cp[mt.cp_step * bi + gc * mt.cp_ld];
+    };
+    auto drow = [&](int r) {
+      const int64_t gr = r_lo + r;
+      return rec.rp[gr + bj * rec.rp_ld] - mt.rp[gr + bj * mt.rp_ld];
+    };
+    if (!full) {
+      bool ok = true;
+      for (int c = 0; c < bc && ok; ++c) {
+        const double d = dcol(c);
+        if (!(fabs(d) > tau)) continue;
+        const int64_t gc = c_lo + c;
+        const double dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+        int idx;
+        if (!recovered_index(dw, d, br, &idx)) ok = false;
+      }
+      if (!ok) {
+        const int kind = (nbad_c == 1) ? 1 : 2;
+        emit(sink, bi, bj, 0, kind, r_lo, c_lo, 0, kind, 0, 1);
+        continue;
+      }
+      int seq = 0;
+      for (int c = 0; c < bc; ++c) {
+        const double d = dcol(c);
+        if (!(fabs(d) > tau)) continue;
+        const int64_t gc = c_lo + c;
+        const double dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+        int idx = 0;
+        recovered_index(dw, d, br, &idx);
+        if (correct) blkp[idx + (int64_t)c * reg.ld] -= d;
+        emit(sink, bi, bj, seq++, 0, r_lo + idx, c_lo + c, correct, 0, correct, 0);
+      }
+      if (correct) mark_dirty(sink, bi, bj);
+      continue;
+    }
+    // FULL (_classify, abft.py:166-171)
+    const int kind = (nbad_r <= 1 && nbad_c <= 1) ? 0 : ((nbad_r <= 1 || nbad_c <= 1) ? 1 : 2);
+    if (kind == 0) {
+      if (nbad_r == 0 || nbad_c == 0) {
+        emit(sink, bi, bj, 0, 0, r_lo, c_lo, 0, 0, 0, 1);
+        continue;
+      }
+      int i = 0, jc = 0;
+      while (!(fabs(drow(i)) > tau)) ++i;
+      while (!(fabs(dcol(jc)) > tau)) ++jc;
+      if (correct) {
+        blkp[i + (int64_t)jc * reg.ld] -= dcol(jc);
+        mark_dirty(sink, bi, bj);
+      }
+      emit(sink, bi, bj, 0, 0, r_lo + i, c_lo + jc, correct, 0, correct, 0);
+    } else if (kind == 1) {
+      if (nbad_c == 1) {
+        int jc = 0;
+        while (!(fabs(dcol(jc)) > tau)) ++jc;
+        if (correct) {
+          for (int r = 0; r < br; ++r) {
+            const double d = drow(r);
+            if (fabs(d) > tau) blkp[r + (int64_t)jc * reg.ld] -= d;
+          }
+          mark_dirty(sink, bi, bj);
+        }
+      } else {
+        if (nbad_r == 0) {
+          // reference: bad_rows[0] on an empty array raises IndexError
+          // (abft.py:267); surfaced to the host as kind -1.
+          emit(sink, bi, bj, 0, -1, r_lo, c_lo, 0, 1, 0, 1);
+          continue;
+        }
+        int i = 0;
+        while (!(fabs(drow(i)) > tau)) ++i;
+        if (correct) {
+          for (int c = 0; c < bc; ++c) {
+            const double d = dcol(c);
+            if (fabs(d) > tau) blkp[i + (int64_t)c * reg.ld] -= d;
+          }
+          mark_dirty(sink, bi, bj);
+        }
+      }
+      emit(sink, bi, bj, 0, 1, r_lo, c_lo, correct, 1, correct, 0);
+    } else {
+      emit(sink, bi, bj, 0, 2, r_lo, c_lo, 0, 2, 0, 1);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K7
+// ---------------------------------------------------------------------------
+__global__ void inject_kernel(double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+                              const DevFault* plan, int nplan, const double* ssrc, int64_t srows,
+                              int64_t scols, int64_t sld, double host_scale) {
+  __shared__ double sm[32];
+  double mx = 0.0;
+  if (ssrc) {
+    for (int64_t i = threadIdx.x; i < srows * scols; i += blockDim.x)
+      mx = fmax(mx, ssrc[(i % srows) + (i / srows) * sld]);
+  }
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  double scale = host_scale;
+  if (ssrc) {
+    scale = sm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) scale = fmax(scale, sm[w]);
+  }
+  for (int f = 0; f < nplan; ++f) {
+    const DevFault ft = plan[f];
+    double mag = ft.magnitude;
+    if (!ft.absolute) {
+      mag = (ft.u * 1e-3) * fmax(scale, 1.0);
+      if (ft.negate) mag = -mag;
+    }
+    if (ft.kind == 0) {
+      m[ft.row + ft.col * ld] += mag;
+    } else if (ft.kind == 1) {
+      const int ext = ft.extent > 2 ? ft.extent : 2;
+      if (ft.orientation == 0) {
+        const int64_t stop = min(ft.row + ext, n_rows);
+        for (int64_t i = 0; i < stop - ft.row; ++i)
+          m[ft.row + i + ft.col * ld] += mag * (1.0 + 0.1 * (double)i);
+      } else {
+        const int64_t stop = min(ft.col + ext, n_cols);
+        for (int64_t i = 0; i < stop - ft.col; ++i)
+          m[ft.row + (ft.col + i) * ld] += mag * (1.0 + 0.1 * (double)i);
+      }
+    } else {
+      const int ext = ft.extent > 2 ? ft.extent : 2;
+      const int64_t rstop = min(ft.row + ext, n_rows);
+      const int64_t cstop = min(ft.col + ext, n_cols);
+      for (int64_t i = 0; i < rstop - ft.row; ++i)
+        for (int64_t jj = 0; jj < cstop - ft.col; ++jj)
+          m[ft.row + i + (ft.col + jj) * ld] +=
+              mag * (((double)i * 0.1 + (double)jj * 0.07) + 1.0);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// reductions / element kernels
+// ---------------------------------------------------------------------------
+__global__ void sumsq_partial(const double* a, int64_t ld, int64_t rows, int64_t cols,
+                              double* part) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
+    const double* col = a + c * ld;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) s = fma(col[r], col[r], s);
+  }
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void sum_final(const double* part, int n, double* out) {
+  __shared__ double sm[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += part[i];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sm[w];
+    out[0] = t;
+  }
+}
+
+// y[r] -= sum_k A[r + k*lda] * x[k*incx]; CTA = 32 rows x 8 k-groups.
+__global__ void gemv_sub_kernel(int64_t rows, int64_t kdim, const double* A, int64_t lda,
+                                const double* x, int64_t incx, double* y) {
+  __shared__ double sm[8][33];
+  const int lane = threadIdx.x & 31, kg = threadIdx.x >> 5;
+  const int64_t r = blockIdx.x * 32 + lane;
+  double s = 0.0;
+  if (r < rows) {
+    for (int64_t k = kg; k < kdim; k += 8) s = fma(A[r + k * lda], x[k * incx], s);
+  }
+  sm[kg][lane] = s;
+  __syncthreads();
+  if (kg == 0 && r < rows) {
+    double t = 0.0;
+    for (int g2 = 0; g2 < 8; ++g2) t += sm[g2][lane];
+    y[r] -= t;
+  }
+}
+
+__global__ void fill_kernel(double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[(i % rows) + (i / rows) * ld] = v;
+}
+
+__global__ void copy_kernel(const double* s, int64_t lds, double* d, int64_t ldd, int64_t rows,
+                            int64_t cols, int mode) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % rows, c = i / rows;
+    double v = s[r + c * lds];
+    if (mode == 1) v = (r > c) ? v : (r == c ? 1.0 : 0.0);
+    else if (mode == 2) v = (r <= c) ? v : 0.0;
+    else if (mode == 3) v = (r >= c) ? v : 0.0;
+    d[r + c * ldd] = v;
+  }
+}
+
+__global__ void sub_kernel(const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+                           int64_t cols) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i % rows, c = i / rows;
+    d[r + c * ldd] -= x[r + c * ldx];
+  }
+}
+
+__global__ void add_diag_kernel(double* a, int64_t ld, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    a[i + i * ld] += v;
+}
+
+inline int grid_for(int64_t total, int threads) {
+  int64_t g = (total + threads - 1) / threads;
+  if (g > 148 * 32) g = 148 * 32;
+  return g < 1 ? 1 : (int)g;
+}
+
+}  // namespace
+
+int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_t* blocks,
+             const int32_t* nblocks_dev, int max_list) {
+  if (reg.rows <= 0 || reg.cols <= 0) return 0;
+  if (reg.b > 4096) {
+    set_last_error("block size %lld > 4096 not supported by the checksum kernels",
+                   (long long)reg.b);
+    return -1;
+  }
+  const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
+  const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
+  const size_t dyn = 2 * reg.b * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(blocksum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  2 * 4096 * 8));
+    attr = true;
+  }
+  int64_t nblk = blocks ? max_list : nbr * nbc;
+  if (nblk <= 0) return 0;
+  int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
+  blocksum_kernel<<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
+                                                  (int64_t)max_list);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
+                  const SumOut& rec, const Maintained& mt, const EventSink& sink) {
+  if (reg.rows <= 0 || reg.cols <= 0) return 0;
+  const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
+  const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
+  const int64_t warps = nbr * nbc;
+  int grid = (int)((warps + 7) / 8);
+  if (grid > 148 * 16) grid = 148 * 16;
+  verify_kernel<<<grid, 256, 0, st>>>(reg, b_nominal, scheme, correct, rec, mt, sink, nbr, nbc);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+           const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
+           int64_t scale_cols, int64_t scale_ld, double host_scale) {
+  if (nplan <= 0) return 0;
+  inject_kernel<<<1, 1024, 0, st>>>(m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows,
+                                    scale_cols, scale_ld, host_scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+          double* scratch) {
+  if (rows <= 0 || cols <= 0) {
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
+    return 0;
+  }
+  const int g = (int)(cols < 1024 ? cols : 1024);
+  sumsq_partial<<<g, 256, 0, st>>>(a, ld, rows, cols, scratch);
+  sum_final<<<1, 1024, 0, st>>>(scratch, g, out);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t lda,
+             const double* x, int64_t incx, double* y) {
+  if (rows <= 0 || k <= 0) return 0;
+  gemv_sub_kernel<<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(rows, k, A, lda, x, incx, y);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+  if (rows <= 0 || cols <= 0) return 0;
+  fill_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(a, ld, rows, cols, v);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
+                int64_t rows, int64_t cols, int mode) {
+  if (rows <= 0 || cols <= 0) return 0;
+  if (mode == 0) {
+    CUDA_TRY(cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, rows * 8, cols,
+                               cudaMemcpyDeviceToDevice, st));
+    return 0;
+  }
+  copy_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols, mode);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols) {
+  if (rows <= 0 || cols <= 0) return 0;
+  sub_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v) {
+  if (n <= 0) return 0;
+  add_diag_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, ld, n, v);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace abft

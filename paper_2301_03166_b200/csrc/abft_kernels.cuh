@@ -1,0 +1,105 @@
+#pragma once
+#include "common.cuh"
+
+namespace abft {
+
+// Output descriptor for per-block checksums of a region (all optional).
+//   col plain    : cp[cp_step*bi + c*cp_ld]        (nbr x cols)
+//   col weighted : cw[cw_step*bi + c*cw_ld]
+//   row plain    : rp[r + bj*rp_ld]                (rows x nbc)
+//   row weighted : rw[r + bj*rw_ld]
+//   block max|x| : bm[bi + bj*bm_ld]               (nbr x nbc)
+struct SumOut {
+  double* cp = nullptr;
+  int64_t cp_ld = 0, cp_step = 1;
+  double* cw = nullptr;
+  int64_t cw_ld = 0, cw_step = 1;
+  double* rp = nullptr;
+  int64_t rp_ld = 0;
+  double* rw = nullptr;
+  int64_t rw_ld = 0;
+  double* bm = nullptr;
+  int64_t bm_ld = 0;
+};
+
+// Region view: rows x cols at ptr (column-major, ld), b x b blocks on the
+// region-local grid (abft.py:108-112).
+struct Region {
+  double* ptr;
+  int64_t ld;
+  int64_t rows, cols;
+  int64_t b;
+};
+
+// K1: per-block plain/weighted column sums, row sums and max|x| of a region
+// (encode, abft.py:118-135; the recomputed side of verify_correct, :185-193).
+// `blocks`/`nblocks_dev`: optional device list of (bi, bj) int32 pairs to
+// restrict the pass to dirty blocks (count read on the device).
+int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_t* blocks = nullptr,
+             const int32_t* nblocks_dev = nullptr, int max_list = 0);
+
+// Maintained checksums handed to the verifier (maintain_gemm, abft.py:138-158).
+struct Maintained {
+  const double* cp;  // col plain    cp[cp_step*bi + c*cp_ld]
+  int64_t cp_ld, cp_step;
+  const double* cw;  // col weighted
+  int64_t cw_ld, cw_step;
+  const double* rp;  // row plain    rp[r + bj*rp_ld]  (FULL)
+  int64_t rp_ld;
+};
+
+// Device-side event record (one CorrectionReport location).
+struct Event {
+  int32_t bi, bj, seq, kind;
+  int64_t row, col;  // region-local
+  int32_t flag, detected_kind, corrected, uncorrectable;
+};
+
+struct EventSink {
+  Event* ev;
+  int32_t* count;
+  int32_t capacity;
+  int32_t* dirty;        // (bi, bj) pairs of repaired blocks
+  int32_t* dirty_count;
+  int32_t dirty_capacity;
+};
+
+// K2: threshold, classify and repair (verify_correct + _handle_single/_full,
+// abft.py:161-276). Reads recomputed sums `rec` (from K1) and maintained sums.
+int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
+                  const SumOut& rec, const Maintained& mt, const EventSink& sink);
+
+// K7: fault injection (inject_faults, abft.py:283-307). `scale_src`: device
+// block-max array of the region (nbr x nbc, ld) reduced to max|region| for the
+// sample_fault_plan magnitude; null when all faults are absolute.
+struct DevFault {
+  int32_t kind, orientation;
+  int64_t row, col;  // global
+  int32_t extent, absolute;
+  double u;
+  int32_t negate, pad;
+  double magnitude;
+};
+int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+           const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
+           int64_t scale_cols, int64_t scale_ld, double host_scale);
+
+// Sum of squares of (rows x cols) matrix into out[0] (deterministic).
+int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+          double* scratch /* >= 1024 doubles */);
+
+// y[r] -= A(r, :) . x   (GEMV for the Cholesky row-checksum maintenance)
+int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t lda,
+             const double* x, int64_t incx, double* y);
+
+// Element kernels
+int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v);
+// mode 0: copy; 1: strict-lower + unit diag (L of LU); 2: upper (U, R); 3: lower incl diag
+int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
+                int64_t rows, int64_t cols, int mode = 0);
+int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v);
+// d -= x
+int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols);
+
+}  // namespace abft

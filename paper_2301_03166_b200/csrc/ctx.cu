@@ -1,0 +1,1029 @@
+// Factorization context + protected-iteration driver (C-ABI).
+//
+// Restates, on one B200, the reference's numeric engine and protected
+// iteration (/root/reference/pkg/src/slackwise/):
+//   Factorization            linalg.py:159-359
+//   _tmu_region              simulator.py:86-94
+//   run_numeric_iteration    simulator.py:97-121
+//   _protected_tmu           simulator.py:124-167
+//   residual / reconstruct   linalg.py:340-368
+// Device data layout: the working matrix is column-major with
+// an even leading dimension (TMA stride rule); per-block checksums live on the
+// GLOBAL b-grid so the verify pass of iteration k is the encode of k+1 for LU
+// and QR (their next region is a block-aligned sub-grid untouched by PD/PU).
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "abft_b200.h"
+#include "abft_kernels.cuh"
+#include "gemm.cuh"
+#include "panel.cuh"
+
+using namespace abft;
+
+namespace {
+
+inline int64_t round_even(int64_t x) { return (x + 1) / 2 * 2; }
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct Snapshot {
+  double* m = nullptr;
+  int64_t k_done = 0;
+  int qr_count = 0;
+  bool used = false;
+};
+
+}  // namespace
+
+struct abft_ctx {
+  int kind = 0;
+  int64_t n = 0, b = 0, nb = 0, ld = 0;
+  int device = 0;
+  cudaStream_t st = nullptr;
+
+  double* m = nullptr;
+  double* a0 = nullptr;  // kept input (optional)
+  bool keep_input = false;
+
+  // checksums on the global block grid
+  double* gcsw = nullptr;  // (2nb) x n, ld_cs: row 2*gbi plain, 2*gbi+1 weighted
+  int64_t ld_cs = 0;
+  double* grs = nullptr;   // n x nb row sums, ld
+  double* gmax = nullptr;  // nb x nb, ld_max
+  int64_t ld_max = 0;
+  double* csm = nullptr;   // maintained col sums of the current region (2nb x n, ld_cs)
+  double* rsm = nullptr;   // maintained row sums (n x nb, ld)
+  double* el = nullptr;    // operand block-row sums (2nb x b, ld_cs)
+  double* er = nullptr;    // R * E_R (b x nb, ld_t)
+
+  // workspaces
+  int64_t ld_t = 0;     // leading dim of b x b / b x n buffers
+  double* lw = nullptr;    // n x b
+  double* uw = nullptr;    // b x n (ld_t)
+  double* linv = nullptr;  // b x b
+  double* uinv = nullptr;  // b x b
+  double* vstore = nullptr;  // QR V panels (n x n, ld)
+  double* tstore = nullptr;  // QR T factors (nb of b x b, ld_t)
+  double* betas = nullptr;
+  double* qr_part = nullptr;
+  int64_t qr_part_elems = 0;
+  double* qr_rowbuf = nullptr;
+  double* gram = nullptr;    // b x b
+  double* ww = nullptr;      // b x n
+  double* mid = nullptr;     // b x n
+  double* scratch = nullptr; // 4096 doubles
+  GemmWorkspace gws;
+
+  // events / lists
+  Event* ev = nullptr;
+  int32_t* counters = nullptr;  // [0] events, [1] dirty
+  int ev_cap = 0;
+  int32_t* dirty = nullptr;
+  int dirty_cap = 0;
+  DevFault* dplan = nullptr;
+  int dplan_cap = 0;
+  int32_t* dlist = nullptr;
+  int dlist_cap = 0;
+  int* info = nullptr;
+
+  // host state
+  int64_t k_done = 0;
+  bool sums_valid = false;
+  int64_t breakdown_col = -1;
+  int qr_count = 0;
+  std::vector<Snapshot> snaps;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool timed = false;
+};
+
+namespace {
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+bool poison_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("ABFT_POISON");
+    v = (e && e[0] == '1') ? 1 : 0;
+  }
+  return v == 1;
+}
+
+// Device allocation; with ABFT_POISON=1 every buffer starts as NaN so a read
+// of never-written memory shows up deterministically (debug aid).
+int dalloc(double** p, int64_t elems) {
+  CUDA_TRY(cudaMalloc(p, std::max<int64_t>(elems, 1) * sizeof(double)));
+  if (poison_enabled())
+    CUDA_TRY(cudaMemset(*p, 0xFF, std::max<int64_t>(elems, 1) * sizeof(double)));
+  return 0;
+}
+
+void region_of(const abft_ctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* rows,
+               int64_t* cols) {
+  // _tmu_region (simulator.py:86-94)
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n);
+  if (c->kind == ABFT_CHOLESKY) {
+    *r0 = p; *c0 = p; *rows = c->n - p; *cols = pe - p;
+  } else if (c->kind == ABFT_LU) {
+    *r0 = pe; *c0 = pe; *rows = c->n - pe; *cols = c->n - pe;
+  } else {
+    *r0 = p; *c0 = pe; *rows = c->n - p; *cols = c->n - pe;
+  }
+}
+
+// SumOut pointing into the global-grid checksum arrays for a b-aligned region.
+SumOut sums_for(abft_ctx* c, int64_t r0, int64_t c0, bool rows_too) {
+  SumOut o;
+  const int64_t gbi = r0 / c->b, gbj = c0 / c->b;
+  o.cp = c->gcsw + 2 * gbi + c0 * c->ld_cs;
+  o.cp_ld = c->ld_cs;
+  o.cp_step = 2;
+  o.cw = o.cp + 1;
+  o.cw_ld = c->ld_cs;
+  o.cw_step = 2;
+  if (rows_too) {
+    o.rp = c->grs + r0 + gbj * c->ld;
+    o.rp_ld = c->ld;
+  }
+  o.bm = c->gmax + gbi + gbj * c->ld_max;
+  o.bm_ld = c->ld_max;
+  return o;
+}
+
+int check_info(abft_ctx* c, int64_t p) {
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, c->info, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (h != 0) {
+    c->breakdown_col = p + h - 1;
+    if (c->kind == ABFT_CHOLESKY)
+      set_last_error("non-positive pivot at column %lld", (long long)c->breakdown_col);
+    else
+      set_last_error("zero pivot at column %lld", (long long)c->breakdown_col);
+    CUDA_TRY(cudaMemsetAsync(c->info, 0, sizeof(int), c->st));
+    return ABFT_E_BREAKDOWN;
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// tasks (linalg.py:192-258)
+// ---------------------------------------------------------------------------
+int task_pd(abft_ctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  double* D = c->m + p + p * c->ld;
+  if (c->kind == ABFT_LU) {
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info));
+    if (pe < n) {
+      // L21 = A21 U11^{-1}
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld,
+                    c->ld, c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
+      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w));
+    }
+  } else if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info));
+  } else {
+    double* V = c->vstore + p + p * c->ld;
+    ABFT_TRY(qr_panel(c->st, D, c->ld, n - p, (int)w, V, c->ld, c->betas, c->qr_part,
+                      c->qr_part_elems, c->qr_rowbuf));
+    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)w, (int)(n - p), 1.0, V, c->ld, V, c->ld, 0.0,
+                  nullptr, 0, c->gram, c->ld_t, &c->gws));
+    ABFT_TRY(larft(c->st, c->gram, c->ld_t, c->betas, (int)w, c->tstore + k * c->b * c->ld_t,
+                   c->ld_t));
+    c->qr_count = (int)(k + 1);
+  }
+  return 0;
+}
+
+int task_pu(abft_ctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (c->kind == ABFT_CHOLESKY) {
+    if (pe < n) {
+      // L21 = A21 L11^{-T}; zero the row block (linalg.py:251-252)
+      ABFT_TRY(gemm(c->st, 'N', 'T', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld,
+                    c->ld, c->linv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
+      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w));
+      ABFT_TRY(fill_matrix(c->st, c->m + p + pe * c->ld, c->ld, w, n - pe, 0.0));
+    }
+    // block-row checksums of the finished L panel (operand sums for later
+    // left-looking maintenance)
+    Region reg{c->m + p + p * c->ld, c->ld, n - p, w, c->b};
+    SumOut o = sums_for(c, p, p, false);
+    o.bm = nullptr;
+    ABFT_TRY(blocksum(c->st, reg, o));
+  } else if (c->kind == ABFT_LU) {
+    if (pe < n) {
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(n - pe), (int)w, 1.0, c->linv, c->ld_t,
+                    c->m + p + pe * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, &c->gws));
+      ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, c->m + p + pe * c->ld, c->ld, w, n - pe));
+    }
+  }
+  return 0;
+}
+
+// The trailing-update GEMM(s) of iteration k. Returns in *L/*R the operands
+// of `region -= L @ R` for checksum maintenance (simulator.py:135-157).
+int tmu_gemm(abft_ctx* c, int64_t k, bool* did) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  *did = false;
+  if (c->kind == ABFT_CHOLESKY) {
+    if (k == 0) return 0;
+    ABFT_TRY(gemm(c->st, 'N', 'T', (int)(n - p), (int)w, (int)p, -1.0, c->m + p, c->ld, c->m + p,
+                  c->ld, 1.0, c->m + p + p * c->ld, c->ld, c->m + p + p * c->ld, c->ld, &c->gws));
+  } else if (c->kind == ABFT_LU) {
+    if (pe >= n) return 0;
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)(n - pe), (int)w, -1.0,
+                  c->m + pe + p * c->ld, c->ld, c->m + p + pe * c->ld, c->ld, 1.0,
+                  c->m + pe + pe * c->ld, c->ld, c->m + pe + pe * c->ld, c->ld, &c->gws));
+  } else {
+    if (pe >= n || k >= c->qr_count) return 0;
+    const double* V = c->vstore + p + p * c->ld;
+    const double* T = c->tstore + k * c->b * c->ld_t;
+    double* C = c->m + p + pe * c->ld;
+    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)(n - p), 1.0, V, c->ld, C, c->ld,
+                  0.0, nullptr, 0, c->ww, c->ld_t, &c->gws));
+    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)w, 1.0, T, c->ld_t, c->ww, c->ld_t,
+                  0.0, nullptr, 0, c->mid, c->ld_t, &c->gws));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V, c->ld, c->mid,
+                  c->ld_t, 1.0, C, c->ld, C, c->ld, &c->gws));
+  }
+  *did = true;
+  return 0;
+}
+
+// maintain_gemm (abft.py:138-158) for the region of iteration k, from the
+// operands of the update. QR needs `mid`, so it runs after the first two QR
+// GEMMs (done inside tmu_gemm) -- callers order it accordingly.
+int maintain(abft_ctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t rows,
+             int64_t cols) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+  SumOut enc = sums_for(c, r0, c0, scheme == ABFT_FULL);
+  if (c->kind == ABFT_CHOLESKY) {
+    // col: CSm = CS - GCSW[2k:, 0:p] * m[p:pe, 0:p]^T   (K = p; K = 0 copies)
+    ABFT_TRY(gemm(c->st, 'N', 'T', (int)(2 * nbr), (int)w, (int)p, -1.0, c->gcsw + 2 * k, c->ld_cs,
+                  c->m + p, c->ld, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
+    if (scheme == ABFT_FULL) {
+      ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
+      // row: RSm -= L * rvec, rvec = block-row-k plain sums of L (= R e)
+      ABFT_TRY(gemv_sub(c->st, rows, p, c->m + p, c->ld, c->gcsw + 2 * k, c->ld_cs, c->rsm));
+    }
+    return 0;
+  }
+  const double* L;
+  int64_t ldl;
+  const double* R;
+  int64_t ldr;
+  if (c->kind == ABFT_LU) {
+    L = c->m + pe + p * c->ld;
+    ldl = c->ld;
+    R = c->m + p + pe * c->ld;
+    ldr = c->ld;
+  } else {
+    L = c->vstore + p + p * c->ld;
+    ldl = c->ld;
+    R = c->mid;
+    ldr = c->ld_t;
+  }
+  // E_L: plain/weighted block-row sums of L (rows x w), interleaved in el
+  {
+    Region rl{const_cast<double*>(L), ldl, rows, w, c->b};
+    SumOut o;
+    o.cp = c->el;
+    o.cp_ld = c->ld_cs;
+    o.cp_step = 2;
+    o.cw = c->el + 1;
+    o.cw_ld = c->ld_cs;
+    o.cw_step = 2;
+    ABFT_TRY(blocksum(c->st, rl, o));
+  }
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, c->el, c->ld_cs, R, ldr,
+                1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
+  if (scheme == ABFT_FULL) {
+    Region rr{const_cast<double*>(R), ldr, w, cols, c->b};
+    SumOut o;
+    o.rp = c->er;
+    o.rp_ld = c->ld_t;
+    ABFT_TRY(blocksum(c->st, rr, o));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbc, (int)w, -1.0, L, ldl, c->er, c->ld_t, 1.0,
+                  enc.rp, c->ld, c->rsm, c->ld, &c->gws));
+  }
+  return 0;
+}
+
+// Host-side list of region blocks touched by the planned faults.
+void touched_blocks(const abft_ctx* c, const abft_fault* plan, int nplan, int64_t r0, int64_t c0,
+                    int64_t rows, int64_t cols, std::vector<int32_t>* out) {
+  std::vector<std::pair<int32_t, int32_t>> blks;
+  for (int f = 0; f < nplan; ++f) {
+    const abft_fault& ft = plan[f];
+    int64_t er = 1, ec = 1;
+    const int64_t ext = std::max<int64_t>(2, ft.extent);
+    if (ft.kind == ABFT_D1) {
+      if (ft.orientation == 0) er = ext; else ec = ext;
+    } else if (ft.kind == ABFT_D2) {
+      er = ext;
+      ec = ext;
+    }
+    const int64_t rlo = std::max(ft.row, r0), rhi = std::min(std::min(ft.row + er, c->n), r0 + rows);
+    const int64_t clo = std::max(ft.col, c0), chi = std::min(std::min(ft.col + ec, c->n), c0 + cols);
+    for (int64_t r = rlo; r < rhi; ++r)
+      for (int64_t cc = clo; cc < chi; ++cc)
+        blks.emplace_back((int32_t)((r - r0) / c->b), (int32_t)((cc - c0) / c->b));
+  }
+  std::sort(blks.begin(), blks.end());
+  blks.erase(std::unique(blks.begin(), blks.end()), blks.end());
+  out->clear();
+  for (auto& pr : blks) {
+    out->push_back(pr.first);
+    out->push_back(pr.second);
+  }
+}
+
+int upload_plan(abft_ctx* c, const abft_fault* plan, int nplan) {
+  if (nplan > c->dplan_cap) {
+    if (c->dplan) cudaFree(c->dplan);
+    c->dplan_cap = std::max(nplan, 64);
+    CUDA_TRY(cudaMalloc(&c->dplan, c->dplan_cap * sizeof(DevFault)));
+  }
+  std::vector<DevFault> h(nplan);
+  for (int i = 0; i < nplan; ++i) {
+    h[i].kind = plan[i].kind;
+    h[i].orientation = plan[i].orientation;
+    h[i].row = plan[i].row;
+    h[i].col = plan[i].col;
+    h[i].extent = plan[i].extent;
+    h[i].absolute = plan[i].absolute;
+    h[i].u = plan[i].u;
+    h[i].negate = plan[i].negate;
+    h[i].pad = 0;
+    h[i].magnitude = plan[i].magnitude;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->dplan, h.data(), nplan * sizeof(DevFault), cudaMemcpyHostToDevice,
+                           c->st));
+  // the host vector dies at return: make the copy complete first
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int upload_list(abft_ctx* c, const std::vector<int32_t>& lst) {
+  const int n = (int)lst.size();
+  if (n == 0) return 0;
+  if (n > c->dlist_cap) {
+    if (c->dlist) cudaFree(c->dlist);
+    c->dlist_cap = std::max(n, 1024);
+    CUDA_TRY(cudaMalloc(&c->dlist, c->dlist_cap * sizeof(int32_t)));
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->dlist, lst.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+// _protected_tmu (simulator.py:124-167). Events are appended on the device.
+int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                  int correct) {
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  const bool has_region = rows > 0 && cols > 0;
+  const bool prot = scheme != ABFT_NONE && has_region;
+  Region reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  const bool full = scheme == ABFT_FULL;
+  if (prot) {
+    // encode (abft.py:118-135): reuse the previous verify's sums when the
+    // region is a sub-grid of the last verified region (LU/QR), else a pass
+    const bool reuse = c->sums_valid && c->kind != ABFT_CHOLESKY;
+    if (!reuse) ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
+  }
+  if (prot && c->kind != ABFT_QR) ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+  bool did = false;
+  if (prot && c->kind == ABFT_QR) {
+    // QR: maintenance needs mid = T^T (V^T C), computed by the first GEMMs
+    const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+    if (pe < n && k < c->qr_count) {
+      const double* V = c->vstore + p + p * c->ld;
+      const double* T = c->tstore + k * c->b * c->ld_t;
+      double* C = c->m + p + pe * c->ld;
+      ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)(n - p), 1.0, V, c->ld, C, c->ld,
+                    0.0, nullptr, 0, c->ww, c->ld_t, &c->gws));
+      ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)w, 1.0, T, c->ld_t, c->ww,
+                    c->ld_t, 0.0, nullptr, 0, c->mid, c->ld_t, &c->gws));
+      ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V, c->ld, c->mid,
+                    c->ld_t, 1.0, C, c->ld, C, c->ld, &c->gws));
+      did = true;
+    } else {
+      // no update: maintained == encoded
+      SumOut enc = sums_for(c, r0, c0, true);
+      const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+      ABFT_TRY(copy_matrix(c->st, enc.cp, c->ld_cs, c->csm, c->ld_cs, 2 * nbr, cols));
+      if (full) ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
+    }
+  } else {
+    ABFT_TRY(tmu_gemm(c, k, &did));
+  }
+  (void)did;
+  const bool faults = has_region && nplan > 0;
+  if (prot) {
+    // recomputed sums + block max of the updated region (verify's read)
+    ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
+  } else if (faults) {
+    SumOut o;
+    o.bm = c->gmax + (r0 / c->b) + (c0 / c->b) * c->ld_max;
+    o.bm_ld = c->ld_max;
+    ABFT_TRY(blocksum(c->st, reg, o));
+  }
+  if (faults) {
+    // sample_fault_plan magnitudes from scale = max|region| (simulator.py:159-163)
+    for (int f = 0; f < nplan; ++f) {
+      if (plan[f].row < 0 || plan[f].row >= c->n || plan[f].col < 0 || plan[f].col >= c->n) {
+        set_last_error("fault at (%lld, %lld) outside matrix", (long long)plan[f].row,
+                       (long long)plan[f].col);
+        return ABFT_E_RANGE;
+      }
+    }
+    ABFT_TRY(upload_plan(c, plan, nplan));
+    const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+    ABFT_TRY(inject(c->st, c->m, c->ld, c->n, c->n, c->dplan, nplan,
+                    c->gmax + (r0 / c->b) + (c0 / c->b) * c->ld_max, nbr, nbc, c->ld_max, 0.0));
+    if (prot) {
+      std::vector<int32_t> lst;
+      touched_blocks(c, plan, nplan, r0, c0, rows, cols, &lst);
+      if (!lst.empty()) {
+        ABFT_TRY(upload_list(c, lst));
+        ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true), c->dlist, nullptr,
+                          (int)(lst.size() / 2)));
+      }
+    }
+  }
+  if (prot) {
+    Maintained mt;
+    mt.cp = c->csm;
+    mt.cp_ld = c->ld_cs;
+    mt.cp_step = 2;
+    mt.cw = c->csm + 1;
+    mt.cw_ld = c->ld_cs;
+    mt.cw_step = 2;
+    mt.rp = c->rsm;
+    mt.rp_ld = c->ld;
+    EventSink sink{c->ev, c->counters, c->ev_cap, c->dirty, c->counters + 1, c->dirty_cap};
+    ABFT_TRY(verify_blocks(c->st, reg, c->b, scheme, correct, sums_for(c, r0, c0, true), mt, sink));
+    // refresh the sums of repaired blocks so they describe the current data
+    ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true), c->dirty, c->counters + 1,
+                      c->dirty_cap));
+    ABFT_TRY(cudaMemsetAsync(c->counters + 1, 0, sizeof(int32_t), c->st) == cudaSuccess ? 0 : -1);
+    c->sums_valid = true;
+  } else {
+    c->sums_valid = false;
+  }
+  return 0;
+}
+
+int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                         int correct) {
+  const int64_t p = k * c->b;
+  auto pd = [&]() -> int {
+    ABFT_TRY(task_pd(c, k));
+    return 0;
+  };
+  if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+    ABFT_TRY(pd());
+    ABFT_TRY(check_info(c, p));
+    ABFT_TRY(task_pu(c, k));
+  } else if (c->kind == ABFT_LU) {
+    ABFT_TRY(pd());
+    ABFT_TRY(check_info(c, p));
+    ABFT_TRY(task_pu(c, k));
+    ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+  } else {
+    ABFT_TRY(pd());
+    ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+  }
+  return 0;
+}
+
+// Pull device events, translate to reference locations, order like the
+// reference (block row, block col, column), fill the report.
+int collect_events(abft_ctx* c, const std::vector<int64_t>& r0s, const std::vector<int64_t>& c0s,
+                   const std::vector<int32_t>* iter_of_event, abft_report* rep, abft_location* locs,
+                   int max_locs, std::vector<Event>* raw_out) {
+  int32_t cnt[2];
+  CUDA_TRY(cudaMemcpyAsync(cnt, c->counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (cnt[0] > c->ev_cap) {
+    set_last_error("ABFT event buffer overflow (%d events)", cnt[0]);
+    return ABFT_E_OVERFLOW;
+  }
+  std::vector<Event> evs(cnt[0]);
+  if (cnt[0] > 0)
+    CUDA_TRY(cudaMemcpy(evs.data(), c->ev, cnt[0] * sizeof(Event), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  (void)iter_of_event;
+  if (raw_out) *raw_out = evs;
+  std::sort(evs.begin(), evs.end(), [](const Event& a, const Event& b) {
+    if (a.bi != b.bi) return a.bi < b.bi;
+    if (a.bj != b.bj) return a.bj < b.bj;
+    return a.seq < b.seq;
+  });
+  if (rep) {
+    memset(rep, 0, sizeof(*rep));
+    rep->n_locations = (int32_t)evs.size();
+  }
+  for (size_t i = 0; i < evs.size(); ++i) {
+    const Event& e = evs[i];
+    if (e.kind < 0) {
+      set_last_error("index 0 is out of bounds for axis 0 with size 0");
+      return ABFT_E_RANGE;
+    }
+    if (rep) {
+      rep->detected[e.detected_kind] += 1;
+      if (e.corrected) rep->corrected[e.detected_kind] += 1;
+      if (e.uncorrectable) rep->uncorrectable = 1;
+    }
+    if (locs && (int)i < max_locs) {
+      abft_location& L = locs[i];
+      L.row = e.row + (r0s.empty() ? 0 : r0s[0]);
+      L.col = e.col + (c0s.empty() ? 0 : c0s[0]);
+      L.kind = e.kind;
+      L.flag = e.flag;
+      L.detected_kind = e.detected_kind;
+      L.corrected = e.corrected;
+      L.uncorrectable = e.uncorrectable;
+      L.block_row = e.bi;
+      L.block_col = e.bj;
+      L.seq = e.seq;
+    }
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int device) {
+  *out = nullptr;
+  if (kind < 0 || kind > 2) {
+    set_last_error("unknown decomposition kind %d", kind);
+    return ABFT_E_INVALID;
+  }
+  if (n < 1) {
+    set_last_error("matrix order must be >= 1");
+    return ABFT_E_DIM;
+  }
+  if (!(1 <= b && b <= n)) {
+    set_last_error("block size %lld outside [1, %lld]", (long long)b, (long long)n);
+    return ABFT_E_DIM;
+  }
+  if (b > 256) {
+    set_last_error("block size %lld > 256 is not supported by the B200 panel kernels",
+                   (long long)b);
+    return ABFT_E_INVALID;
+  }
+  if (n > INT32_MAX / 2) {
+    set_last_error("matrix order too large");
+    return ABFT_E_INVALID;
+  }
+  DevGuard g(device);
+  abft_ctx* c = new abft_ctx();
+  c->kind = kind;
+  c->n = n;
+  c->b = b;
+  c->nb = (n + b - 1) / b;
+  c->ld = round_up(n, 16);
+  c->device = device;
+  c->ld_cs = round_even(2 * c->nb);
+  c->ld_max = round_even(c->nb);
+  c->ld_t = round_even(b);
+  int rc = 0;
+  auto fail = [&](int r) {
+    abft_destroy(c);
+    return r;
+  };
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+    set_last_error("cudaStreamCreate failed");
+    delete c;
+    return -1000;
+  }
+  const int64_t n_ = n, ld = c->ld;
+  if ((rc = dalloc(&c->m, ld * n_))) return fail(rc);
+  if ((rc = dalloc(&c->gcsw, c->ld_cs * n_))) return fail(rc);
+  if ((rc = dalloc(&c->csm, c->ld_cs * n_))) return fail(rc);
+  if ((rc = dalloc(&c->grs, ld * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->rsm, ld * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->gmax, c->ld_max * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->el, c->ld_cs * b))) return fail(rc);
+  if ((rc = dalloc(&c->er, c->ld_t * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->lw, ld * b))) return fail(rc);
+  if ((rc = dalloc(&c->uw, c->ld_t * n_))) return fail(rc);
+  if ((rc = dalloc(&c->linv, c->ld_t * b))) return fail(rc);
+  if ((rc = dalloc(&c->uinv, c->ld_t * b))) return fail(rc);
+  if ((rc = dalloc(&c->scratch, 4096))) return fail(rc);
+  if (kind == ABFT_QR) {
+    if ((rc = dalloc(&c->vstore, ld * n_))) return fail(rc);
+    if (cudaMemset(c->vstore, 0, ld * n_ * sizeof(double)) != cudaSuccess) return fail(-1000);
+    if ((rc = dalloc(&c->tstore, c->nb * b * c->ld_t))) return fail(rc);
+    if ((rc = dalloc(&c->betas, b))) return fail(rc);
+    c->qr_part_elems = 2 * 160 * (b + 1);
+    if ((rc = dalloc(&c->qr_part, c->qr_part_elems))) return fail(rc);
+    if ((rc = dalloc(&c->qr_rowbuf, 2 * (b + 1)))) return fail(rc);
+    if ((rc = dalloc(&c->gram, c->ld_t * b))) return fail(rc);
+    if ((rc = dalloc(&c->ww, c->ld_t * n_))) return fail(rc);
+    if ((rc = dalloc(&c->mid, c->ld_t * n_))) return fail(rc);
+  }
+  // split-K workspace: bounded (falls back to fewer splits when short)
+  c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
+  if ((rc = dalloc(&c->gws.ptr, c->gws.elems))) return fail(rc);
+  c->ev_cap = 1 << 16;
+  if (cudaMalloc(&c->ev, c->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&c->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  cudaMemset(c->counters, 0, 4 * sizeof(int32_t));
+  c->dirty_cap = 1 << 16;
+  if (cudaMalloc(&c->dirty, 2 * c->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&c->info, sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemset(c->info, 0, sizeof(int));
+  cudaEventCreate(&c->e0);
+  cudaEventCreate(&c->e1);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
+  *out = c;
+  return 0;
+}
+
+ABFT_API int abft_destroy(abft_ctx* c) {
+  if (!c) return 0;
+  DevGuard g(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  double* bufs[] = {c->m,     c->a0,     c->gcsw,   c->grs,     c->gmax,  c->csm,  c->rsm,
+                    c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
+                    c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
+                    c->scratch, c->gws.ptr};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  if (c->ev) cudaFree(c->ev);
+  if (c->counters) cudaFree(c->counters);
+  if (c->dirty) cudaFree(c->dirty);
+  if (c->dplan) cudaFree(c->dplan);
+  if (c->dlist) cudaFree(c->dlist);
+  if (c->info) cudaFree(c->info);
+  for (auto& s : c->snaps)
+    if (s.m) cudaFree(s.m);
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return 0;
+}
+
+ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
+  DevGuard g(c->device);
+  if (lda < c->n) {
+    set_last_error("lda < n");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(c->m, c->ld * 8, a, lda * 8, c->n * 8, c->n, cudaMemcpyHostToDevice,
+                             c->st));
+  if (c->keep_input) {
+    if (!c->a0) ABFT_TRY(dalloc(&c->a0, c->ld * c->n));
+    CUDA_TRY(cudaMemcpy2DAsync(c->a0, c->ld * 8, c->m, c->ld * 8, c->n * 8, c->n,
+                               cudaMemcpyDeviceToDevice, c->st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->k_done = 0;
+  c->sums_valid = false;
+  c->qr_count = 0;
+  c->breakdown_col = -1;
+  return 0;
+}
+
+ABFT_API int abft_keep_input(abft_ctx* c, int keep) {
+  c->keep_input = keep != 0;
+  return 0;
+}
+
+ABFT_API int abft_get_matrix(abft_ctx* c, double* mh, int64_t ldm) {
+  DevGuard g(c->device);
+  CUDA_TRY(cudaMemcpy2DAsync(mh, ldm * 8, c->m, c->ld * 8, c->n * 8, c->n, cudaMemcpyDeviceToHost,
+                             c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+ABFT_API int64_t abft_k_done(abft_ctx* c) { return c->k_done; }
+
+ABFT_API int abft_set_k_done(abft_ctx* c, int64_t k) {
+  c->k_done = k;
+  return 0;
+}
+
+ABFT_API int abft_task(abft_ctx* c, int64_t k, int task) {
+  DevGuard g(c->device);
+  if (k < 0 || k >= c->nb) {
+    set_last_error("iteration %lld out of range", (long long)k);
+    return ABFT_E_DIM;
+  }
+  if (task == ABFT_TASK_PD) {
+    ABFT_TRY(task_pd(c, k));
+    ABFT_TRY(check_info(c, k * c->b));
+  } else if (task == ABFT_TASK_PU) {
+    ABFT_TRY(task_pu(c, k));
+  } else if (task == ABFT_TASK_TMU) {
+    bool did;
+    ABFT_TRY(tmu_gemm(c, k, &did));
+    c->sums_valid = false;
+  } else {
+    set_last_error("unknown task %d", task);
+    return ABFT_E_INVALID;
+  }
+  return 0;
+}
+
+ABFT_API int abft_iteration(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                            int correct, abft_report* rep, abft_location* locs, int max_locs) {
+  DevGuard g(c->device);
+  if (k < 0 || k >= c->nb) {
+    set_last_error("iteration %lld out of range for %lld blocks", (long long)k, (long long)c->nb);
+    return ABFT_E_DIM;
+  }
+  if (scheme < 0 || scheme > 2) {
+    set_last_error("unknown checksum scheme %d", scheme);
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  CUDA_TRY(cudaEventRecord(c->e0, c->st));
+  int rc = run_iteration_device(c, k, scheme, plan, nplan, correct);
+  CUDA_TRY(cudaEventRecord(c->e1, c->st));
+  c->timed = true;
+  if (rc != 0) return rc;
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  ABFT_TRY(collect_events(c, {r0}, {c0}, nullptr, rep, locs, max_locs, nullptr));
+  c->k_done = k + 1;
+  return 0;
+}
+
+ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, const abft_fault* plan,
+                            const int64_t* plan_iter, int nplan, int correct, abft_report* reports,
+                            abft_location* locs, int max_locs, int* n_locs) {
+  DevGuard g(c->device);
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  if (n_locs) *n_locs = 0;
+  CUDA_TRY(cudaEventRecord(c->e0, c->st));
+  c->timed = true;
+  int total_locs = 0;
+  for (int64_t k = c->k_done; k < c->nb; ++k) {
+    const int sch = schemes ? schemes[k] : scheme;
+    // this iteration's slice of the flat plan
+    int f0 = 0, f1 = 0;
+    if (plan && plan_iter) {
+      while (f0 < nplan && plan_iter[f0] < k) ++f0;
+      f1 = f0;
+      while (f1 < nplan && plan_iter[f1] == k) ++f1;
+    }
+    int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct);
+    if (rc != 0) {
+      cudaEventRecord(c->e1, c->st);
+      return rc;
+    }
+    // events are only read when the iteration produced some: one 8-byte
+    // D2H of the counter per iteration, overlapped with the next launches
+    int32_t cnt = 0;
+    if (sch != ABFT_NONE) {
+      CUDA_TRY(cudaMemcpyAsync(&cnt, c->counters, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+      CUDA_TRY(cudaStreamSynchronize(c->st));
+    }
+    abft_report rep;
+    memset(&rep, 0, sizeof(rep));
+    if (cnt > 0) {
+      int64_t r0, c0, rows, cols;
+      region_of(c, k, &r0, &c0, &rows, &cols);
+      const int room = locs ? std::max(0, max_locs - total_locs) : 0;
+      ABFT_TRY(collect_events(c, {r0}, {c0}, nullptr, &rep, locs ? locs + total_locs : nullptr,
+                              room, nullptr));
+      total_locs += rep.n_locations;
+    }
+    if (reports) reports[k] = rep;
+    c->k_done = k + 1;
+  }
+  CUDA_TRY(cudaEventRecord(c->e1, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (n_locs) *n_locs = total_locs;
+  return 0;
+}
+
+ABFT_API int abft_last_elapsed_ms(abft_ctx* c, double* ms) {
+  DevGuard g(c->device);
+  if (!c->timed) {
+    *ms = 0.0;
+    return 0;
+  }
+  CUDA_TRY(cudaEventSynchronize(c->e1));
+  float f = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&f, c->e0, c->e1));
+  *ms = f;
+  return 0;
+}
+
+ABFT_API int abft_qr_panels(abft_ctx* c) { return c->qr_count; }
+
+ABFT_API int abft_get_qr_panel(abft_ctx* c, int64_t k, double* V, int64_t ldv, double* T,
+                               int64_t ldt) {
+  DevGuard g(c->device);
+  if (c->kind != ABFT_QR || k < 0 || k >= c->qr_count) {
+    set_last_error("no QR panel %lld", (long long)k);
+    return ABFT_E_INVALID;
+  }
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
+  if (V)
+    CUDA_TRY(cudaMemcpy2DAsync(V, ldv * 8, c->vstore + p + p * c->ld, c->ld * 8, (c->n - p) * 8, w,
+                               cudaMemcpyDeviceToHost, c->st));
+  if (T)
+    CUDA_TRY(cudaMemcpy2DAsync(T, ldt * 8, c->tstore + k * c->b * c->ld_t, c->ld_t * 8, w * 8, w,
+                               cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+ABFT_API int abft_snapshot(abft_ctx* c, int slot) {
+  DevGuard g(c->device);
+  if (slot < 0 || slot > 64) {
+    set_last_error("bad snapshot slot");
+    return ABFT_E_INVALID;
+  }
+  if ((int)c->snaps.size() <= slot) c->snaps.resize(slot + 1);
+  Snapshot& s = c->snaps[slot];
+  if (!s.m) ABFT_TRY(dalloc(&s.m, c->ld * c->n));
+  CUDA_TRY(cudaMemcpyAsync(s.m, c->m, c->ld * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  s.k_done = c->k_done;
+  s.qr_count = c->qr_count;
+  s.used = true;
+  return 0;
+}
+
+ABFT_API int abft_restore(abft_ctx* c, int slot) {
+  DevGuard g(c->device);
+  if (slot < 0 || slot >= (int)c->snaps.size() || !c->snaps[slot].used) {
+    set_last_error("empty snapshot slot %d", slot);
+    return ABFT_E_INVALID;
+  }
+  Snapshot& s = c->snaps[slot];
+  CUDA_TRY(cudaMemcpyAsync(c->m, s.m, c->ld * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  c->k_done = s.k_done;
+  c->qr_count = s.qr_count;
+  c->sums_valid = false;
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+ABFT_API int64_t abft_breakdown_column(abft_ctx* c) { return c->breakdown_col; }
+
+// Debug/test accessor for the device checksum state:
+// which = 0 gcsw (2nb x n), 1 csm (2nb x n), 2 grs (n x nb), 3 rsm (n x nb),
+// 4 gmax (nb x nb). Copies the full array into `out` (column-major).
+ABFT_API int abft_debug_array(abft_ctx* c, int which, double* out, int64_t* rows, int64_t* cols) {
+  DevGuard g(c->device);
+  const double* src;
+  int64_t r, cl, ld;
+  switch (which) {
+    case 0: src = c->gcsw; r = 2 * c->nb; cl = c->n; ld = c->ld_cs; break;
+    case 1: src = c->csm; r = 2 * c->nb; cl = c->n; ld = c->ld_cs; break;
+    case 2: src = c->grs; r = c->n; cl = c->nb; ld = c->ld; break;
+    case 3: src = c->rsm; r = c->n; cl = c->nb; ld = c->ld; break;
+    case 4: src = c->gmax; r = c->nb; cl = c->nb; ld = c->ld_max; break;
+    default: set_last_error("bad array id"); return ABFT_E_INVALID;
+  }
+  *rows = r;
+  *cols = cl;
+  if (out) {
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    CUDA_TRY(cudaMemcpy2D(out, r * 8, src, ld * 8, r * 8, cl, cudaMemcpyDeviceToHost));
+  }
+  return 0;
+}
+
+// reconstruct (linalg.py:340-359) into device buffer `out` (ld = c->ld);
+// `tmp` is an n x ld scratch buffer.
+static int reconstruct_device(abft_ctx* c, double* out, double* tmp) {
+  const int64_t n = c->n, ld = c->ld;
+  if (c->kind == ABFT_LU) {
+    ABFT_TRY(copy_matrix(c->st, c->m, ld, tmp, ld, n, n, 1));  // L (unit)
+    ABFT_TRY(copy_matrix(c->st, c->m, ld, out, ld, n, n, 2));  // U
+    // out = L U, computed in place from a copy of U
+    double* U = nullptr;
+    ABFT_TRY(dalloc(&U, ld * n));
+    int rc = copy_matrix(c->st, out, ld, U, ld, n, n, 0);
+    if (!rc)
+      rc = gemm(c->st, 'N', 'N', (int)n, (int)n, (int)n, 1.0, tmp, ld, U, ld, 0.0, nullptr, 0, out,
+                ld, &c->gws);
+    cudaStreamSynchronize(c->st);
+    cudaFree(U);
+    return rc;
+  }
+  if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(copy_matrix(c->st, c->m, ld, tmp, ld, n, n, 3));
+    return gemm(c->st, 'N', 'T', (int)n, (int)n, (int)n, 1.0, tmp, ld, tmp, ld, 0.0, nullptr, 0,
+                out, ld, &c->gws);
+  }
+  // out = triu(m); for k from last to 0: out[p:n,:] -= V (T (V^T out[p:n,:]))
+  ABFT_TRY(copy_matrix(c->st, c->m, ld, out, ld, n, n, 2));
+  for (int64_t k = c->qr_count - 1; k >= 0; --k) {
+    const int64_t p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+    const double* V = c->vstore + p + p * ld;
+    const double* T = c->tstore + k * c->b * c->ld_t;
+    double* blk = out + p;
+    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)n, (int)(n - p), 1.0, V, ld, blk, ld, 0.0, nullptr,
+                  0, c->ww, c->ld_t, &c->gws));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)n, (int)w, 1.0, T, c->ld_t, c->ww, c->ld_t, 0.0,
+                  nullptr, 0, c->mid, c->ld_t, &c->gws));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)n, (int)w, -1.0, V, ld, c->mid, c->ld_t, 1.0,
+                  blk, ld, blk, ld, &c->gws));
+  }
+  return 0;
+}
+
+ABFT_API int abft_reconstruct(abft_ctx* c, double* outh, int64_t ldo) {
+  DevGuard g(c->device);
+  if (c->k_done < c->nb) {
+    set_last_error("factorization incomplete");
+    return ABFT_E_INCOMPLETE;
+  }
+  const int64_t n = c->n, ld = c->ld;
+  double *X = nullptr, *T = nullptr;
+  int rc = dalloc(&X, ld * n);
+  if (!rc) rc = dalloc(&T, ld * n);
+  if (!rc) rc = reconstruct_device(c, X, T);
+  if (!rc && cudaMemcpy2DAsync(outh, ldo * 8, X, ld * 8, n * 8, n, cudaMemcpyDeviceToHost, c->st) !=
+                 cudaSuccess)
+    rc = -1000;
+  cudaStreamSynchronize(c->st);
+  if (X) cudaFree(X);
+  if (T) cudaFree(T);
+  return rc;
+}
+
+ABFT_API int abft_set_qr_panels(abft_ctx* c, int count) {
+  if (count < 0 || count > c->qr_count) {
+    set_last_error("cannot extend the QR panel list from the host");
+    return ABFT_E_INVALID;
+  }
+  c->qr_count = count;
+  return 0;
+}
+
+ABFT_API int abft_residual(abft_ctx* c, const double* a0h, int64_t lda, double* out) {
+  DevGuard g(c->device);
+  if (c->k_done < c->nb) {
+    set_last_error("factorization incomplete");
+    return ABFT_E_INCOMPLETE;
+  }
+  const int64_t n = c->n, ld = c->ld;
+  double *A = nullptr, *X = nullptr, *T = nullptr;
+  bool own_a = false;
+  int rc = 0;
+  if (a0h) {
+    rc = dalloc(&A, ld * n);
+    own_a = true;
+    if (!rc && cudaMemcpy2DAsync(A, ld * 8, a0h, lda * 8, n * 8, n, cudaMemcpyHostToDevice, c->st) !=
+                   cudaSuccess)
+      rc = -1000;
+  } else if (c->a0) {
+    A = c->a0;
+  } else {
+    set_last_error("no input matrix for the residual");
+    return ABFT_E_INVALID;
+  }
+  if (!rc) rc = dalloc(&X, ld * n);
+  if (!rc) rc = dalloc(&T, ld * n);
+  double* sq = c->scratch + 2048;
+  if (!rc) rc = sumsq(c->st, A, ld, n, n, sq, c->scratch);            // ||A||^2
+  if (!rc) rc = reconstruct_device(c, X, T);
+  if (!rc) rc = sub_matrix(c->st, A, ld, X, ld, n, n);                // X = rec - A
+  if (!rc) rc = sumsq(c->st, X, ld, n, n, sq + 1, c->scratch + 1024);  // ||A - rec||^2
+  double h[2] = {0, 0};
+  if (!rc && cudaMemcpyAsync(h, sq, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st) !=
+                 cudaSuccess)
+    rc = -1000;
+  cudaStreamSynchronize(c->st);
+  if (X) cudaFree(X);
+  if (T) cudaFree(T);
+  if (own_a && A) cudaFree(A);
+  if (rc) return rc;
+  const double na = sqrt(h[0]), nd = sqrt(h[1]);
+  *out = (na == 0.0) ? nd : nd / na;
+  return 0;
+}
+
+}  // extern "C"

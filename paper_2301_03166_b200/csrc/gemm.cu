@@ -1,0 +1,451 @@
+// FP64 GEMM for the trailing-matrix updates: D = beta*C + alpha*op(A)*op(B).
+//
+// B200 design (kernel K3):
+//  * FP64 tensor cores through DMMA (mma.sync m8n8k4 f64); tcgen05 has no f64
+//    kind on sm_100a, so this is the fastest FP64 datapath on the part
+//    (measured 37.1 TFLOP/s issue peak, profiles/fp64_peak_r01.txt).
+//  * Warp-specialised: one producer warp issues TMA (cp.async.bulk.tensor)
+//    loads into a 6-stage mbarrier ring; 8 consumer warps run DMMA out of
+//    shared memory with 64x32 register-blocked warp tiles (CTA tile 128x128).
+//  * Shared-memory layouts are chosen per operand orientation so every
+//    fragment read is a conflict-free ld.shared.v2.f64: m/n-contiguous tiles are
+//    dense, k-contiguous tiles use the TMA 128-byte swizzle.
+//  * Split-K (deterministic, ordered partial reduction) for the long-K /
+//    few-tile shapes of left-looking Cholesky and the QR V^T C product.
+// The reference computes these products with numpy/OpenBLAS dgemm:
+//   LU   m[pe:n,pe:n] -= l21 @ u12           (pkg/src/slackwise/simulator.py:148)
+//   Chol m[p:n,p:pe]  -= m[p:n,0:p] @ m[p:pe,0:p].T   (simulator.py:141)
+//   QR   mid = t.T @ (v.T @ c); c -= v @ mid  (simulator.py:154-157)
+#include "gemm.cuh"
+
+#include <cstdarg>
+#include <cstring>
+#include <mutex>
+
+#include <cudaTypedefs.h>
+
+namespace abft {
+
+// ---------------------------------------------------------------------------
+// error string (thread-local so concurrent contexts do not clobber each other)
+// ---------------------------------------------------------------------------
+static thread_local char g_last_error[1024] = "";
+
+void set_last_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_last_error, sizeof(g_last_error), fmt, ap);
+  va_end(ap);
+}
+const char* last_error() { return g_last_error; }
+
+// ---------------------------------------------------------------------------
+// TMA descriptor creation through the driver entry point (no -lcuda needed)
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int make_tma_map(CUtensorMap* map, const double* ptr, int64_t ld, int64_t inner, int64_t outer,
+                 int box_inner, int box_outer, bool swizzle128, int* shift) {
+  auto fn = get_encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return -20;
+  }
+  if (ld % 2 != 0) {
+    set_last_error("leading dimension %lld must be even for TMA", (long long)ld);
+    return -21;
+  }
+  uintptr_t addr = reinterpret_cast<uintptr_t>(ptr);
+  int sh = static_cast<int>((addr & 15u) / 8u);
+  const void* base = reinterpret_cast<const void*>(addr - sh * 8);
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(inner + sh),
+                        static_cast<cuuint64_t>(outer < 1 ? 1 : outer)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * 8)};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_inner), static_cast<cuuint32_t>(box_outer)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%dx%d",
+                   (int)r, (long long)inner, (long long)outer, (long long)ld, box_inner, box_outer);
+    return -22;
+  }
+  *shift = sh;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
+constexpr int NCONS = 8;  // consumer warps: 2 (M) x 4 (N), warp tile 64 x 32
+constexpr int THREADS = (NCONS + 4) * 32;  // + one producer warpgroup (1 active warp)
+constexpr int A_BYTES = BM * BK * 8;  // 16 KB
+constexpr int B_BYTES = BN * BK * 8;  // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+
+struct KParams {
+  int M, N, K;
+  int a_shift, b_shift;
+  int k_per_split;
+  const double* C;
+  int64_t ldc;
+  double* D;
+  int64_t ldd;
+  double alpha, beta;
+  int vec;          // 1 if C/D allow 16-byte row-pair accesses
+  int partial;      // 1: write raw acc to D (= split workspace slice z)
+  int64_t split_stride;  // elements between split slices in partial mode
+};
+
+// Row of accumulator row-fragment rf=(rp,e) for lane group g: wm+16rp+2g+e.
+// Column of (cf, c8): B-N: wn + 8cf + c8;  B-T: cf=(cp,f): wn + 16cp + 2c8 + f.
+template <bool BT>
+ABFT_DEVINL int col_of(int cf, int c8) {
+  if (BT) return 16 * (cf >> 1) + 2 * c8 + (cf & 1);
+  return 8 * cf + c8;
+}
+
+template <bool AT, bool BT>
+__global__ void __launch_bounds__(THREADS, 1)
+    dgemm_tma_dmma(const __grid_constant__ CUtensorMap mapA,
+                   const __grid_constant__ CUtensorMap mapB, KParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int kz = blockIdx.z;
+  const int kbeg = kz * p.k_per_split;
+  const int kend = min(p.K, kbeg + p.k_per_split);
+  const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCONS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp >= NCONS) {
+    // ===== TMA producer warpgroup: hand registers to the consumers =====
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
+    if (warp == NCONS && lane == 0) {
+      tma_prefetch_desc(&mapA);
+      tma_prefetch_desc(&mapB);
+      for (int kt = 0; kt < nkt; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        uint8_t* sb = sa + A_BYTES;
+        const int k0 = kbeg + kt * BK;
+        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+        if (AT)
+          tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
+        else
+          tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
+        if (BT)
+          tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
+        else
+          tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+      }
+    }
+    return;
+  }
+
+  // ===== DMMA consumers =====
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  const int g = lane >> 2, j = lane & 3;
+  const int wm = (warp & 1) * 64;
+  const int wn = (warp >> 1) * 32;
+
+  double acc[8][4][2];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  const uint32_t sbase = smem_u32(smem);
+
+  for (int kt = 0; kt < nkt; ++kt) {
+    const int s = kt % STAGES;
+    mbar_wait(&full[s], (kt / STAGES) & 1);
+    // lanes leave the spin loop independently; mma.sync.aligned needs the
+    // whole warp converged
+    __syncwarp();
+    const uint32_t sa = sbase + s * STAGE_BYTES;
+    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+    for (int ks = 0; ks < BK; ks += 8) {
+      // B fragments for both k-parities: b[cf][ss] = B(k = ks+2j+ss, col(cf, g))
+      double b[4][2];
+      if (!BT) {
+        // swizzled [n][16 k]: n = wn+8cf+g
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf) {
+          const int n = wn + 8 * cf + g;
+          double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
+          b[cf][0] = v.x;
+          b[cf][1] = v.y;
+        }
+      } else {
+        // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
+#pragma unroll
+        for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+          for (int ss = 0; ss < 2; ++ss) {
+            double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
+            b[2 * cp][ss] = v.x;
+            b[2 * cp + 1][ss] = v.y;
+          }
+      }
+#pragma unroll
+      for (int rp = 0; rp < 4; ++rp) {
+        // a[ss][e] = A(row = wm+16rp+2g+e, k = ks+2j+ss)
+        double a[2][2];
+        if (!AT) {
+          // dense [k][m], BM doubles per k row
+#pragma unroll
+          for (int ss = 0; ss < 2; ++ss) {
+            double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
+            a[ss][0] = v.x;
+            a[ss][1] = v.y;
+          }
+        } else {
+          // swizzled [m][16 k]
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int m = wm + 16 * rp + 2 * g + e;
+            double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
+            a[0][e] = v.x;
+            a[1][e] = v.y;
+          }
+        }
+#pragma unroll
+        for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+#pragma unroll
+            for (int cf = 0; cf < 4; ++cf)
+              dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
+      }
+    }
+    // Release the stage only after this warp's shared-memory reads have
+    // completed: SYNCS.ARRIVE is not ordered behind in-flight LDS, so without
+    // the fence the producer's TMA can overwrite the last fragments before
+    // they land in registers (write-after-read across the async proxy).
+    consumer_release(&empty[s], lane);
+  }
+
+  // ===== epilogue =====
+  double* D = p.partial ? p.D + (int64_t)kz * p.split_stride : p.D;
+  const bool use_c = !p.partial && p.beta != 0.0;
+#pragma unroll
+  for (int rp = 0; rp < 4; ++rp) {
+    const int row = m0 + wm + 16 * rp + 2 * g;
+    if (row >= p.M) continue;
+    const bool pair = row + 1 < p.M;
+#pragma unroll
+    for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const int col = n0 + wn + col_of<BT>(cf, 2 * j + t);
+        if (col >= p.N) continue;
+        double v0 = acc[2 * rp][cf][t], v1 = acc[2 * rp + 1][cf][t];
+        if (p.partial) {
+          double* d = D + row + (int64_t)col * p.ldd;
+          d[0] = v0;
+          if (pair) d[1] = v1;
+          continue;
+        }
+        double c0 = 0.0, c1 = 0.0;
+        const double* c = p.C + row + (int64_t)col * p.ldc;
+        double* d = D + row + (int64_t)col * p.ldd;
+        if (pair && p.vec) {
+          if (use_c) {
+            double2 cv = *reinterpret_cast<const double2*>(c);
+            c0 = cv.x;
+            c1 = cv.y;
+          }
+          double2 o;
+          o.x = fma(p.alpha, v0, p.beta * c0);
+          o.y = fma(p.alpha, v1, p.beta * c1);
+          *reinterpret_cast<double2*>(d) = o;
+        } else {
+          if (use_c) {
+            c0 = c[0];
+            if (pair) c1 = c[1];
+          }
+          d[0] = fma(p.alpha, v0, p.beta * c0);
+          if (pair) d[1] = fma(p.alpha, v1, p.beta * c1);
+        }
+      }
+  }
+}
+
+// D = beta*C + alpha * sum_z W[z]   (ordered, deterministic)
+__global__ void splitk_reduce(int M, int N, int splits, const double* __restrict__ W,
+                              int64_t ldw, int64_t stride, const double* C, int64_t ldc, double* D,
+                              int64_t ldd, double alpha, double beta) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int i = static_cast<int>(idx % M);
+    const int jcol = static_cast<int>(idx / M);
+    double s = 0.0;
+    for (int z = 0; z < splits; ++z) s += W[z * stride + i + jcol * ldw];
+    const double c = beta != 0.0 ? C[i + (int64_t)jcol * ldc] : 0.0;
+    D[i + (int64_t)jcol * ldd] = fma(alpha, s, beta * c);
+  }
+}
+
+template <bool AT, bool BT>
+int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& kp,
+                  int splits) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_dmma<AT, BT>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    attr_set = true;
+  }
+  dim3 grid((kp.M + BM - 1) / BM, (kp.N + BN - 1) / BN, splits);
+  dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, kp);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+int gemm_splits_for(int M, int N, int K, int num_sms) {
+  const int64_t tiles = (int64_t)((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  if (K <= 4 * BK * 8 || tiles >= 2 * num_sms) return 1;
+  int s = static_cast<int>((2 * num_sms + tiles - 1) / tiles);
+  const int maxs = K / (8 * BK);  // keep >= 128 of K per split
+  if (s > maxs) s = maxs;
+  if (s > 32) s = 32;
+  return s < 1 ? 1 : s;
+}
+
+int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
+         double* D, int64_t ldd, GemmWorkspace* ws, int splits) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) {
+    // D = beta*C (alpha*0)
+    if (beta == 0.0 && C == D) return 0;
+    splitk_reduce<<<256, 256, 0, st>>>(M, N, 0, nullptr, 1, 0, C, ldc, D, ldd, alpha, beta);
+    CUDA_TRY(cudaGetLastError());
+    return 0;
+  }
+  const bool AT = (ta == 'T' || ta == 't');
+  const bool BT = (tb == 'T' || tb == 't');
+  CUtensorMap ma, mb;
+  int sha = 0, shb = 0;
+  if (AT)
+    ABFT_TRY(make_tma_map(&ma, A, lda, K, M, BK, BM, true, &sha));
+  else
+    ABFT_TRY(make_tma_map(&ma, A, lda, M, K, BM, BK, false, &sha));
+  if (BT)
+    ABFT_TRY(make_tma_map(&mb, B, ldb, N, K, BN, BK, false, &shb));
+  else
+    ABFT_TRY(make_tma_map(&mb, B, ldb, K, N, BK, BN, true, &shb));
+
+  if (splits <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    splits = gemm_splits_for(M, N, K, sms);
+  }
+  int kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+  splits = (K + kps - 1) / kps;
+  const int64_t ldw = M;
+  const int64_t slice = ldw * N;
+  if (splits > 1) {
+    if (!ws || ws->ptr == nullptr || ws->elems < slice * splits) {
+      const int64_t cap = (ws && ws->ptr) ? ws->elems / slice : 0;
+      if (cap >= 2) {
+        splits = static_cast<int>(cap < splits ? cap : splits);
+        kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+        splits = (K + kps - 1) / kps;
+      } else {
+        splits = 1;
+        kps = K;
+      }
+    }
+  } else {
+    kps = K;
+  }
+
+  KParams kp;
+  kp.M = M;
+  kp.N = N;
+  kp.K = K;
+  kp.a_shift = sha;
+  kp.b_shift = shb;
+  kp.k_per_split = kps;
+  kp.alpha = alpha;
+  kp.beta = beta;
+  if (splits > 1) {
+    kp.C = nullptr;
+    kp.ldc = 0;
+    kp.D = ws->ptr;
+    kp.ldd = ldw;
+    kp.partial = 1;
+    kp.split_stride = slice;
+    kp.vec = 0;
+  } else {
+    kp.C = C;
+    kp.ldc = ldc;
+    kp.D = D;
+    kp.ldd = ldd;
+    kp.partial = 0;
+    kp.split_stride = 0;
+    const bool cv = (beta == 0.0) || ((reinterpret_cast<uintptr_t>(C) & 15) == 0 && ldc % 2 == 0);
+    const bool dv = (reinterpret_cast<uintptr_t>(D) & 15) == 0 && ldd % 2 == 0;
+    kp.vec = (cv && dv) ? 1 : 0;
+  }
+  int rc;
+  if (AT && BT)
+    rc = launch_kernel<true, true>(st, ma, mb, kp, splits);
+  else if (AT)
+    rc = launch_kernel<true, false>(st, ma, mb, kp, splits);
+  else if (BT)
+    rc = launch_kernel<false, true>(st, ma, mb, kp, splits);
+  else
+    rc = launch_kernel<false, false>(st, ma, mb, kp, splits);
+  if (rc) return rc;
+  if (splits > 1) {
+    int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    splitk_reduce<<<blocks, 256, 0, st>>>(M, N, splits, ws->ptr, ldw, slice, C, ldc, D, ldd, alpha,
+                                          beta);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return 0;
+}
+
+}  // namespace abft

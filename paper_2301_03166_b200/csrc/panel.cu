@@ -1,0 +1,418 @@
+// Panel kernels (K5/K6): diagonal-block factorization + triangular inverses.
+//
+// The reference's panel decompositions are Python column loops
+// (/root/reference/pkg/src/slackwise/linalg.py):
+//   LU  unpivoted dgetf2 on the nk x b panel   :230-238
+//   Chol Crout dpotf2 on the b x b block       :219-229
+// and its panel updates solve against the diagonal block with LAPACK dgesv
+//   Chol L21 = A21 L11^{-T}                     :246-252
+//   LU   U12 = L11^{-1} A12                     :253-257
+// B200 restatement: the w x w diagonal block is factored by ONE CTA with
+// 32-column sub-panels staged in shared memory (the block is L2-resident),
+// and the same CTA forms the triangular inverses. Everything tall-skinny
+// (L21 = A21 U11^{-1}, L21 = A21 L11^{-T}, U12 = L11^{-1} A12) then runs as a
+// DMMA GEMM over all SMs (gemm.cu), so the panel is GEMM-bound, not a
+// per-column loop. Breakdown detection follows the reference exactly: LU
+// pivot == 0 or non-finite (:234), Cholesky pivot <= 0 or non-finite (:223).
+#include "panel.cuh"
+
+#include <cooperative_groups.h>
+
+namespace abft {
+
+namespace {
+
+constexpr int DT = 512;   // threads of the diagonal kernel
+constexpr int NBK = 32;   // sub-panel width
+constexpr int PLD = 257;  // smem leading dim of the staged sub-panel (w <= 256)
+constexpr int DIAG_SMEM = 2 * 256 * 33 * 8 + 64;  // max over the phases
+
+// Accessor for a (possibly transposed) column-major matrix.
+struct Acc {
+  double* p;
+  int64_t ld;
+  bool t;
+  ABFT_DEVINL double& at(int r, int c) const { return t ? p[c + r * ld] : p[r + c * ld]; }
+};
+
+// X = L^{-1} for the w x w lower-triangular L (unit or not), X written through
+// `X` (lower part + explicit zeros above). Block-row sweep with 32-row blocks.
+ABFT_DEVINL void lower_inverse(const Acc& L, const Acc& X, int w, bool unit, double* smem) {
+  double* Ls = smem;             // [256][33]: Ls[l*33 + r] = L(r0 + r, l)
+  double* Ts = smem + 256 * 33;  // [256][33]: Ts[c*33 + r]
+  const int tid = threadIdx.x;
+  for (int r0 = 0; r0 < w; r0 += NBK) {
+    const int rh = min(NBK, w - r0);
+    const int ncol = r0 + rh;
+    for (int idx = tid; idx < rh * ncol; idx += DT) {
+      const int r = idx % rh, l = idx / rh;
+      Ls[l * 33 + r] = (l <= r0 + r) ? L.at(r0 + r, l) : 0.0;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < rh * ncol; idx += DT) {
+      const int r = idx % rh, c = idx / rh;
+      double acc = (r0 + r == c) ? 1.0 : 0.0;
+      for (int l = c; l < r0; ++l) acc -= Ls[l * 33 + r] * X.at(l, c);
+      Ts[c * 33 + r] = acc;
+    }
+    __syncthreads();
+    for (int c = tid; c < ncol; c += DT) {
+      for (int r = 0; r < rh; ++r) {
+        double x = Ts[c * 33 + r];
+        for (int l = 0; l < r; ++l) x -= Ls[(r0 + l) * 33 + r] * Ts[c * 33 + l];
+        if (!unit) x /= Ls[(r0 + r) * 33 + r];
+        Ts[c * 33 + r] = x;
+      }
+    }
+    __syncthreads();
+    for (int idx = tid; idx < rh * w; idx += DT) {
+      const int r = idx % rh, c = idx / rh;
+      X.at(r0 + r, c) = (c < ncol) ? Ts[c * 33 + r] : 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// mode 0: LU without pivoting (L unit lower \ U upper in place),
+//         Linv = L^{-1}, Uinv = U^{-1}.
+// mode 1: Cholesky, L lower in place with the strict upper part zeroed,
+//         Linv = L^{-1}.
+// info: 0, or 1 + local column of the first breakdown.
+__global__ void __launch_bounds__(DT, 1)
+    diag_factor_kernel(double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
+                       double* Uinv, int64_t ldu, int* info) {
+  extern __shared__ double sm[];
+  double* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
+  double* Rs = sm + NBK * PLD;     // [224][33]   Rs[c*33 + i]
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+
+  for (int jb = 0; jb < w; jb += NBK) {
+    const int jw = min(NBK, w - jb);
+    const int rem = w - jb;
+    for (int idx = tid; idx < rem * jw; idx += DT) {
+      const int r = idx % rem, c = idx / rem;
+      Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
+    }
+    __syncthreads();
+    for (int c = 0; c < jw; ++c) {
+      const double piv = Ps[c * PLD + c];
+      const bool bad = (mode == 0) ? (piv == 0.0 || !isfinite(piv)) : (!(piv > 0.0) || !isfinite(piv));
+      if (bad) {
+        if (tid == 0) {
+          s_bad = jb + c + 1;
+          *info = jb + c + 1;
+        }
+        break;  // uniform: every thread saw the same pivot
+      }
+      __syncthreads();
+      if (mode == 0) {
+        for (int r = c + 1 + tid; r < rem; r += DT) Ps[c * PLD + r] /= piv;
+        __syncthreads();
+        const int nr = rem - c - 1, ncc = jw - c - 1;
+        for (int idx = tid; idx < nr * ncc; idx += DT) {
+          const int r = c + 1 + idx % nr, cc = c + 1 + idx / nr;
+          Ps[cc * PLD + r] -= Ps[c * PLD + r] * Ps[cc * PLD + c];
+        }
+      } else {
+        const double d = sqrt(piv);
+        for (int r = c + tid; r < rem; r += DT) Ps[c * PLD + r] = (r == c) ? d : Ps[c * PLD + r] / d;
+        __syncthreads();
+        const int nr = rem - c - 1, ncc = jw - c - 1;
+        for (int idx = tid; idx < nr * ncc; idx += DT) {
+          const int r = c + 1 + idx % nr, cc = c + 1 + idx / nr;
+          if (r >= cc) Ps[cc * PLD + r] -= Ps[c * PLD + r] * Ps[c * PLD + cc];
+        }
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    if (s_bad) return;
+    for (int idx = tid; idx < rem * jw; idx += DT) {
+      const int r = idx % rem, c = idx / rem;
+      if (mode == 0 || r >= c) D[(jb + r) + (int64_t)(jb + c) * ld] = Ps[c * PLD + r];
+    }
+    __syncthreads();
+    const int ncols = w - jb - jw;
+    if (ncols > 0) {
+      if (mode == 0) {
+        for (int idx = tid; idx < jw * ncols; idx += DT) {
+          const int i = idx % jw, c = idx / jw;
+          Rs[c * 33 + i] = D[(jb + i) + (int64_t)(jb + jw + c) * ld];
+        }
+        __syncthreads();
+        for (int c = tid; c < ncols; c += DT) {
+          for (int i = 1; i < jw; ++i) {
+            double x = Rs[c * 33 + i];
+            for (int l = 0; l < i; ++l) x -= Ps[l * PLD + i] * Rs[c * 33 + l];
+            Rs[c * 33 + i] = x;
+          }
+        }
+        __syncthreads();
+        for (int idx = tid; idx < jw * ncols; idx += DT) {
+          const int i = idx % jw, c = idx / jw;
+          D[(jb + i) + (int64_t)(jb + jw + c) * ld] = Rs[c * 33 + i];
+        }
+        const int nr = rem - jw;
+        for (int idx = tid; idx < nr * ncols; idx += DT) {
+          const int r = idx % nr, c = idx / nr;
+          double acc = 0.0;
+          for (int l = 0; l < jw; ++l) acc += Ps[l * PLD + jw + r] * Rs[c * 33 + l];
+          D[(jb + jw + r) + (int64_t)(jb + jw + c) * ld] -= acc;
+        }
+      } else {
+        const int nr = rem - jw;
+        for (int idx = tid; idx < nr * ncols; idx += DT) {
+          const int r = idx % nr, c = idx / nr;
+          if (r < c) continue;
+          double acc = 0.0;
+          for (int l = 0; l < jw; ++l) acc += Ps[l * PLD + jw + r] * Ps[l * PLD + jw + c];
+          D[(jb + jw + r) + (int64_t)(jb + jw + c) * ld] -= acc;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (mode == 1) {
+    for (int idx = tid; idx < w * w; idx += DT) {
+      const int r = idx % w, c = idx / w;
+      if (r < c) D[r + (int64_t)c * ld] = 0.0;
+    }
+  }
+  __syncthreads();
+  // ---- inverses ----
+  if (Linv) lower_inverse(Acc{D, ld, false}, Acc{Linv, ldl, false}, w, mode == 0, sm);
+  if (Uinv) lower_inverse(Acc{D, ld, true}, Acc{Uinv, ldu, true}, w, false, sm);
+}
+
+}  // namespace
+
+int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
+                double* Uinv, int64_t ldu, int* info_dev) {
+  if (w <= 0) return 0;
+  if (w > 256) {
+    set_last_error("diag_factor: block width %d > 256 (host-level blocking required)", w);
+    return -1;
+  }
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(diag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  DIAG_SMEM));
+    attr = true;
+  }
+  diag_factor_kernel<<<1, DT, DIAG_SMEM, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+// ===========================================================================
+// QR panel (K5 geqr2 + larft)
+// ===========================================================================
+// Householder panel factorization with the reference's LAPACK sign
+// convention (linalg.py:260-300): alpha = -copysign(||x||, x0 or 1),
+// v scaled so v0 = 1, tau = beta * v0^2, R on/above the diagonal and zeros
+// below, V kept separately.
+//
+// One cooperative kernel over the whole panel with ONE grid-wide reduction
+// per column: each CTA owns a contiguous row slab and contributes, in one
+// pass, the partial sum of squares of x[1:] and the partial dot products
+// x[1:] . P[1:, c] for every trailing panel column c. After the grid sync
+// every CTA reduces the partials in a fixed order (deterministic), recovers
+// alpha/beta and w[c] = dots[c] + v0 * P[j, c] (v differs from x only in its
+// first entry), and applies the reflector to its own rows. The owner of row j
+// publishes row j through the partial buffer, so no second sync is needed.
+namespace {
+
+constexpr int QT = 256;
+
+__global__ void __launch_bounds__(QT)
+    qr_panel_kernel(double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
+                    double* betas, double* part, double* rowbuf) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double qsm[];
+  double* wv = qsm;        // [w]
+  double* rowj = qsm + w;  // [w]
+  const int G = gridDim.x, gi = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rpc = (nk + G - 1) / G;
+  const int64_t r_lo = min(nk, gi * rpc), r_hi = min(nk, r_lo + rpc);
+  const int W1 = w + 1;
+
+  for (int j = 0; j < w; ++j) {
+    double* buf = part + (int64_t)(j & 1) * G * W1;
+    double* rb = rowbuf + (j & 1) * W1;
+    // ---- phase A: partials over own rows i > j ----
+    const int64_t i0 = max(r_lo, (int64_t)j + 1);
+    for (int c = j + warp; c < w; c += QT / 32) {
+      double s = 0.0;
+      for (int64_t i = i0 + lane; i < r_hi; i += 32) s = fma(P[i + j * ld], P[i + c * ld], s);
+      s = warp_sum(s);
+      if (lane == 0) buf[(int64_t)gi * W1 + (c - j)] = s;
+    }
+    if (j >= r_lo && j < r_hi) {
+      for (int c = j + tid; c < w; c += QT) rb[c - j] = P[j + c * ld];
+    }
+    grid.sync();
+    // ---- phase B: reduce (fixed order), reflector, update own rows ----
+    for (int c = j + tid; c < w; c += QT) {
+      double s = 0.0;
+      for (int g2 = 0; g2 < G; ++g2) s += buf[(int64_t)g2 * W1 + (c - j)];
+      wv[c] = s;
+      rowj[c] = rb[c - j];
+    }
+    __syncthreads();
+    const double s1 = wv[j];
+    const double x0 = rowj[j];
+    const double normx = sqrt(s1 + x0 * x0);
+    const bool own_j = (j >= r_lo && j < r_hi);
+    if (normx == 0.0) {
+      if (tid == 0 && gi == 0) betas[j] = 0.0;
+      for (int64_t i = r_lo + tid; i < r_hi; i += QT)
+        if (i >= j) V[i + j * ldv] = (i == j) ? 1.0 : 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double alpha = -copysign(normx, x0 != 0.0 ? x0 : 1.0);
+    const double v0 = x0 - alpha;
+    const double vn2 = s1 + v0 * v0;
+    if (vn2 == 0.0) {
+      if (tid == 0 && gi == 0) betas[j] = 0.0;
+      if (own_j && tid == 0) P[j + j * ld] = alpha;
+      for (int64_t i = r_lo + tid; i < r_hi; i += QT)
+        if (i >= j) V[i + j * ldv] = (i == j) ? 1.0 : 0.0;
+      __syncthreads();
+      continue;
+    }
+    const double beta = 2.0 / vn2;
+    __syncthreads();
+    for (int c = j + 1 + tid; c < w; c += QT) wv[c] = wv[c] + v0 * rowj[c];
+    __syncthreads();
+    // rest -= beta * outer(v, w)  (linalg.py:287-288)
+    const int64_t nrows = r_hi - max(r_lo, (int64_t)j);
+    const int64_t rbeg = max(r_lo, (int64_t)j);
+    const int ncols = w - j - 1;
+    for (int64_t idx = tid; idx < nrows * ncols; idx += QT) {
+      const int64_t i = rbeg + idx % nrows;
+      const int c = j + 1 + (int)(idx / nrows);
+      const double vi = (i == j) ? v0 : P[i + j * ld];
+      P[i + c * ld] -= beta * (vi * wv[c]);
+    }
+    __syncthreads();
+    for (int64_t i = rbeg + tid; i < r_hi; i += QT) {
+      if (i == j) {
+        P[j + j * ld] = alpha;
+        V[j + j * ldv] = v0 / v0;
+      } else {
+        V[i + j * ldv] = P[i + j * ld] / v0;
+        P[i + j * ld] = 0.0;
+      }
+    }
+    if (tid == 0 && gi == 0) betas[j] = beta * v0 * v0;
+    __syncthreads();
+  }
+}
+
+// T (w x w, upper) from betas and Gm = V^T V (upper part used), forward
+// columnwise dlarft (linalg.py:294-298) in blocked form:
+//   diagonal 32x32 blocks by the column recurrence, then
+//   T[0:j0, jb] = -T[0:j0, 0:j0] * (Gm[0:j0, jb] * T[jb, jb]).
+__global__ void __launch_bounds__(512)
+    larft_kernel(const double* Gm, int64_t ldg, const double* betas, int w, double* T,
+                 int64_t ldt) {
+  extern __shared__ double lsm[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nblk = (w + 31) / 32;
+  // zero T
+  for (int64_t idx = tid; idx < (int64_t)w * w; idx += blockDim.x)
+    T[(idx % w) + (idx / w) * ldt] = 0.0;
+  __syncthreads();
+  // diagonal blocks: one warp per block (lane = row within block)
+  for (int bk = warp; bk < nblk; bk += blockDim.x / 32) {
+    const int j0 = bk * 32, jw = min(32, w - j0);
+    for (int jj = 0; jj < jw; ++jj) {
+      const int j = j0 + jj;
+      const double bj = betas[j];
+      if (lane < jj) {
+        const int i = j0 + lane;
+        double s = 0.0;
+        for (int l = i; l < j; ++l) s += T[i + l * ldt] * Gm[l + j * ldg];
+        T[i + j * ldt] = -bj * s;
+      }
+      if (lane == 0) T[j + j * ldt] = bj;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  double* Ys = lsm;  // [j0][32]
+  for (int bk = 1; bk < nblk; ++bk) {
+    const int j0 = bk * 32, jw = min(32, w - j0);
+    for (int idx = tid; idx < j0 * jw; idx += blockDim.x) {
+      const int i = idx % j0, c = idx / j0;
+      double s = 0.0;
+      for (int l = 0; l <= c; ++l) s += Gm[i + (j0 + l) * ldg] * T[(j0 + l) + (j0 + c) * ldt];
+      Ys[i + c * j0] = s;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < j0 * jw; idx += blockDim.x) {
+      const int i = idx % j0, c = idx / j0;
+      double s = 0.0;
+      for (int l = i; l < j0; ++l) s += T[i + l * ldt] * Ys[l + c * j0];
+      T[i + (j0 + c) * ldt] = -s;
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
+             double* betas, double* part, int64_t part_elems, double* rowbuf) {
+  if (w <= 0 || nk <= 0) return 0;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int G = (int)((nk + 63) / 64);
+  if (G > sms) G = sms;
+  const int64_t need = 2LL * G * (w + 1);
+  if (need > part_elems) {
+    G = (int)(part_elems / (2LL * (w + 1)));
+    if (G < 1) {
+      set_last_error("qr_panel: partial buffer too small");
+      return -1;
+    }
+  }
+  size_t smem = 2 * (size_t)w * sizeof(double);
+  int max_per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_per_sm, qr_panel_kernel, QT, smem));
+  if (max_per_sm < 1) {
+    set_last_error("qr_panel: kernel cannot be resident");
+    return -1;
+  }
+  void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf};
+  CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QT), args, smem, st));
+  return 0;
+}
+
+int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, int w, double* T,
+          int64_t ldt) {
+  if (w <= 0) return 0;
+  size_t smem = (size_t)w * 32 * sizeof(double);
+  if (smem > 200 * 1024) {
+    set_last_error("larft: panel width %d too large", w);
+    return -1;
+  }
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  200 * 1024));
+    attr = true;
+  }
+  larft_kernel<<<1, 512, smem, st>>>(Gm, ldg, betas, w, T, ldt);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace abft

@@ -1,0 +1,23 @@
+#pragma once
+#include "common.cuh"
+
+namespace abft {
+
+// Diagonal-block factorization (w <= 256) + triangular inverses on one CTA.
+// mode 0 = LU (no pivoting): Linv = L^{-1} (unit lower), Uinv = U^{-1}.
+// mode 1 = Cholesky: Linv = L^{-1}; strict upper of D zeroed. Uinv ignored.
+// *info_dev = 1 + local column of the first breakdown (left untouched if none).
+int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
+                double* Uinv, int64_t ldu, int* info_dev);
+
+// Householder panel (nk x w) in place: R above/on the diagonal, zeros below;
+// V (nk x w, unit diagonal, zeros above) and betas (tau) out. part: >= 2*148*(w+1)
+// doubles, rowbuf: >= 2*(w+1) doubles of device scratch.
+int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
+             double* betas, double* part, int64_t part_elems, double* rowbuf);
+
+// T factor (w x w upper) from Gm = V^T V and betas.
+int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, int w, double* T,
+          int64_t ldt);
+
+}  // namespace abft
