@@ -1,0 +1,470 @@
+#!/usr/bin/env python
+"""Benchmark: ABFT-protected blocked factorization TFLOP/s on B200.
+
+Headline (BASELINE.json metric "ABFT dpotrf/dgetrf/dgeqrf TFLOP/s at N=32768,
+1/2/4/8 GPU; ABFT overhead %; J"): one step = one complete ABFT-protected
+factorization of an N=32768 fp64 matrix (default: LU / dgetrf, b=256, FULL =
+col_ft+row_ft checksums as under the `bsr` mode flags, one seeded 0-D fault
+injected and corrected, criterion-5 protocol). TFLOP/s uses the LAPACK flop
+convention (2n^3/3 LU, n^3/3 Cholesky, 4n^3/3 QR), ABFT work not counted.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+  python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+
+N > 1: one independent factorization per GPU (weak scaling, "replicas");
+time is the max over ranks. --impl reference times the reference algorithm's
+CPU restatement (oracle/, numpy) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+FLOPS = {"cholesky": lambda n: n ** 3 / 3.0, "lu": lambda n: 2.0 * n ** 3 / 3.0,
+         "qr": lambda n: 4.0 * n ** 3 / 3.0}
+LAPACK = {"cholesky": "dpotrf", "lu": "dgetrf", "qr": "dgeqrf"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--kind", default="lu", choices=["lu", "cholesky", "qr"])
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=256)
+    ap.add_argument("--scheme", default="full", choices=["none", "single", "full"])
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-overhead", action="store_true", help="skip the scheme=none run")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-iters", type=int, default=1,
+                    help="oracle iterations timed for the CPU baseline sample")
+    ap.add_argument("--extra-kinds", default="", help="comma list of kinds also measured")
+    ap.add_argument("--profile-only", action="store_true", help="one step, for ncu")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# environment helpers
+# ---------------------------------------------------------------------------
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent sampling through NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.ok = True
+        except Exception:
+            return
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self.max_mhz = self.nv.nvmlDeviceGetMaxClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+
+    def energy_mj(self) -> float | None:
+        if not self.ok:
+            return None
+        try:
+            return float(self.nv.nvmlDeviceGetTotalEnergyConsumption(self.h))
+        except Exception:
+            return None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name not in ("gpu_idle",):
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def fault_plan(n: int, b: int, seed: int):
+    """Criterion-5 protocol (pkg/tests/test_acceptance.py:221-224): rng =
+    default_rng(seed); k_fault = rng.integers(0, nb-1); {0d: 1} at k_fault."""
+    rng = np.random.default_rng(seed)
+    nb = -(-n // b)
+    k_fault = int(rng.integers(0, nb - 1))
+    return k_fault, rng
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm (oracle restatement of the reference algorithm)
+# ---------------------------------------------------------------------------
+
+def cpu_sample(kind: str, n: int, b: int, scheme: str, seed: int, iters: int, a=None):
+    """Time the oracle's protected iterations 0..iters-1 of the same workload
+    (same matrix, block size, scheme and fault protocol) on the host cores.
+    Returns (TFLOP/s, seconds, flops, iterations)."""
+    import oracle as O
+    from paper_2301_03166_b200.linalg import compute_flops
+    if a is None:
+        a = O.generate_test_matrix(kind, n, seed)
+    k_fault, rng = fault_plan(n, b, seed)
+    f = O.OracleFactorization(kind, a, b)
+    nb = f.nb
+    iters = max(1, min(iters, nb))
+    flops = 0.0
+    t0 = time.perf_counter()
+    for k in range(iters):
+        O.protected_iteration(f, k, scheme, {"0d": 1} if k == k_fault else None, rng)
+        flops += sum(compute_flops(kind, t, n, b, k) for t in ("pd", "pu", "tmu"))
+    dt = time.perf_counter() - t0
+    return flops / dt / 1e12, dt, flops, iters
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    a = O.generate_test_matrix(args.kind, args.n, args.seed)
+    vals = []
+    for i in range(args.warmup + args.steps):
+        tf, dt, flops, iters = cpu_sample(args.kind, args.n, args.b, args.scheme, args.seed,
+                                          args.cpu_iters, a)
+        if i >= args.warmup:
+            vals.append((tf, dt))
+    value = statistics.median(v[0] for v in vals)
+    ms = statistics.median(v[1] for v in vals) * 1e3
+    sample = (f"oracle (numpy restatement of slackwise) protected {args.kind} N={args.n} "
+              f"b={args.b} scheme={args.scheme}: iterations 0..{args.cpu_iters - 1} of "
+              f"{-(-args.n // args.b)}, criterion-5 fault protocol")
+    line = {"impl": "reference", "metric": metric_name(args), "value": value, "unit": "TFLOP/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": config(args),
+            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(),
+                             "kind": "port", "sample": sample, "cpu": cpu_model()},
+            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def metric_name(args) -> str:
+    return (f"ABFT {LAPACK[args.kind]} TFLOP/s (fp64 N={args.n}, {args.scheme.upper()} "
+            f"checksums, 1 seeded fault)")
+
+
+def config(args) -> dict:
+    return {"workload": f"{args.kind} fp64 N={args.n} b={args.b} scheme={args.scheme} "
+                        f"(col_ft+row_ft as under mode=bsr), one 0-D fault at a seeded "
+                        f"iteration (criterion-5 protocol)",
+            "kind": args.kind, "n": args.n, "b": args.b, "scheme": args.scheme,
+            "seed": args.seed,
+            "l2": "working set 8.6 GB >> 126 MB L2; no flush needed",
+            "parallelism": "replicas" if args.gpus > 1 else "single"}
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+class Arm:
+    """One device-resident factorization context reused across steps."""
+
+    def __init__(self, kind, n, b, seed, device):
+        import paper_2301_03166_b200 as P
+        from paper_2301_03166_b200 import _lib
+        self.P, self.L = P, _lib
+        self.lib = _lib.load()
+        self.kind, self.n, self.b, self.seed = kind, n, b, seed
+        t0 = time.perf_counter()
+        if kind == "cholesky":
+            # host PCG64 uniform (bit-identical draws); SPD product on the GPU
+            host = np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n)))
+        else:
+            host = P.generate_test_matrix(kind, n, seed)
+        self.gen_s = time.perf_counter() - t0
+        self.f = P.Factorization(kind, host, b, device=device, keep_input=True)
+        if kind == "cholesky":
+            P.linalg.check(self.lib.abft_make_spd(self.f._ctx))
+            self.f._dirty()
+            host = self.f.m  # the SPD input, for the end-to-end leg
+        self.host = host
+        _GEN["s"] = self.gen_s
+        import torch
+        self.torch = torch
+        self.stream = torch.cuda.ExternalStream(self.lib.abft_stream(self.f._ctx))
+
+    def step(self, scheme):
+        k_fault, rng = fault_plan(self.n, self.b, self.seed)
+        self.P.linalg.check(self.lib.abft_reset(self.f._ctx))
+        sched = {k_fault: {"0d": 1}}
+        reps = self.P.run_protected(self.f, scheme, sched, rng)
+        return k_fault, reps
+
+    def timed(self, scheme, steps):
+        torch = self.torch
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(self.stream)
+        out = None
+        for _ in range(steps):
+            out = self.step(scheme)
+        e1.record(self.stream)
+        e1.synchronize()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), out
+
+    def profile(self, scheme):
+        lib = self.lib
+        lib.abft_profile(self.f._ctx, 1)
+        self.step(scheme)
+        ms = (ctypes.c_double * 4)()
+        lib.abft_profile_read(self.f._ctx, ms)
+        lib.abft_profile(self.f._ctx, 0)
+        return {"pd": ms[0], "pu": ms[1], "tmu_gemm": ms[2], "abft": ms[3]}
+
+    def residual(self):
+        out = ctypes.c_double(0.0)
+        self.P.linalg.check(self.lib.abft_residual(self.f._ctx, None, self.n, ctypes.byref(out)))
+        return out.value
+
+
+def tmu_flops(kind, n, b) -> float:
+    from paper_2301_03166_b200.linalg import compute_flops
+    return sum(compute_flops(kind, "tmu", n, b, k) for k in range(-(-n // b)))
+
+
+def verify_bytes(kind, n, b, scheme) -> float:
+    """Algorithmic bytes of the checksum verification per factorization: one
+    fp64 read of every protected region, plus the fresh encode
+    pass Cholesky needs (its region is a new panel each iteration)."""
+    if scheme == "none":
+        return 0.0
+    tot = 0.0
+    nb = -(-n // b)
+    for k in range(nb):
+        p, pe = k * b, min(k * b + b, n)
+        rows, cols = {"cholesky": (n - p, pe - p), "lu": (n - pe, n - pe)}.get(kind, (n - p, n - pe))
+        if rows > 0 and cols > 0:
+            tot += rows * cols * (2 if kind == "cholesky" else 1)
+    return 8.0 * tot
+
+
+def run_ours(args):
+    import torch
+    rank, world, local = dist_env()
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    P = __import__("paper_2301_03166_b200")
+    lib = P._lib.load()
+    peak = ctypes.c_double(0.0)
+    P.linalg.check(lib.abft_probe_dmma_peak(20000, ctypes.byref(peak)))
+    arm = Arm(args.kind, args.n, args.b, args.seed, local)
+    if args.profile_only:
+        arm.step(args.scheme)
+        torch.cuda.synchronize()
+        return
+    for _ in range(args.warmup):
+        arm.step(args.scheme)
+    launches0 = lib.abft_launch_count()
+    clk = ClockSampler(local)
+    en0 = clk.energy_mj()
+    if world > 1:
+        torch.distributed.barrier()
+    with clk:
+        ms, (k_fault, reps) = arm.timed(args.scheme, args.steps)
+    en1 = clk.energy_mj()
+    launches = (lib.abft_launch_count() - launches0) // max(1, args.steps)
+    res = arm.residual()
+    # the single planned 0-D fault must be located and corrected
+    locs = [loc for r in reps for loc in r.locations]
+    fixed = sum(r.corrected[P.ErrorKind.D0] for r in reps)
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
+    ms_step = ms_t.item() / args.steps
+    flops = FLOPS[args.kind](args.n)
+    value = world * flops / (ms_step * 1e-3) / 1e12
+
+    overhead = None
+    if not args.no_overhead and args.scheme != "none":
+        for _ in range(1):
+            arm.step("none")
+        ms_none, _ = arm.timed("none", args.steps)
+        overhead = 100.0 * (ms - ms_none) / ms_none
+    prof = arm.profile(args.scheme)
+    tflops_tmu = tmu_flops(args.kind, args.n, args.b)
+    achieved = tflops_tmu / (prof["tmu_gemm"] * 1e-3) / 1e12 if prof["tmu_gemm"] else None
+    vbytes = verify_bytes(args.kind, args.n, args.b, args.scheme)
+
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(arm, args)
+    extra = {}
+    for kind in [k for k in args.extra_kinds.split(",") if k and k != args.kind]:
+        extra[kind] = measure_kind(kind, args, local)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        a = arm.host if args.kind != "cholesky" else None
+        del arm
+        torch.cuda.empty_cache()
+        tf, dt, fl, it = cpu_sample(args.kind, args.n, args.b, args.scheme, args.seed,
+                                    args.cpu_iters, a)
+        cpu = {"value": tf, "unit": "TFLOP/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"oracle protected {args.kind} N={args.n} b={args.b} "
+                         f"scheme={args.scheme}, iterations 0..{it - 1} "
+                         f"({fl / 1e12:.3f} TFLOP in {dt:.1f} s)",
+               "cpu": cpu_model()}
+    if rank != 0:
+        return
+    line = {
+        "metric": metric_name(args), "value": value, "unit": "TFLOP/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": f"synthetic: generate_test_matrix({args.kind!r}, {args.n}, seed={args.seed}) "
+                "(PCG64 draws bit-identical to the reference)",
+        "config": config(args),
+        "abft_overhead_pct": overhead,
+        "energy_j_per_factorization": ((en1 - en0) / 1e3 / args.steps
+                                       if en0 is not None and en1 is not None else None),
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "tensor", "kernel": "dgemm_tma_dmma (trailing-matrix update)",
+                     "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                     "frac": (achieved / peak.value) if achieved else None, "traffic": None,
+                     "peak_source": "measured DMMA issue rate on this GPU "
+                                    "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"},
+        "abft_verify": {"bytes": vbytes, "ms": prof["abft"],
+                        "gbs": vbytes / (prof["abft"] * 1e-3) / 1e9 if prof["abft"] else None,
+                        "bound": "hbm"},
+        "profile_ms": prof,
+        "whole_step_frac_of_peak": value / world / peak.value,
+        "residual": res, "residual_over_n_eps": res / (args.n * 2.220446049250313e-16),
+        "fault": {"k_fault": k_fault, "locations": [[int(a), int(b), c.value, bool(d)]
+                                                    for a, b, c, d in locs],
+                  "corrected_0d": int(fixed)},
+        "cpu_baseline": cpu,
+        "input_generation_s": arm_gen_s(),
+    }
+    if extra:
+        line["extra_kinds"] = extra
+    print(json.dumps(line), flush=True)
+
+
+_GEN = {"s": None}
+
+
+def arm_gen_s():
+    return _GEN["s"]
+
+
+def measure_kind(kind, args, local):
+    import torch
+    arm = Arm(kind, args.n, args.b, args.seed, local)
+    arm.step(args.scheme)
+    ms, _ = arm.timed(args.scheme, max(1, args.steps))
+    ms_step = ms / max(1, args.steps)
+    ms_none, _ = arm.timed("none", 1)
+    prof = arm.profile(args.scheme)
+    out = {"value": FLOPS[kind](args.n) / (ms_step * 1e-3) / 1e12, "unit": "TFLOP/s",
+           "ms_per_step": ms_step, "abft_overhead_pct": 100.0 * (ms_step - ms_none) / ms_none,
+           "profile_ms": prof, "residual": arm.residual()}
+    del arm
+    torch.cuda.empty_cache()
+    return out
+
+
+def run_e2e(arm, args):
+    """Same metric through the public API with host buffers: pinned H2D of the
+    input, protected factorization, D2H of the factors, every step."""
+    import torch
+    P, lib, f = arm.P, arm.lib, arm.f
+    n = args.n
+    pinned_in = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+    pinned_in[...] = arm.host.T  # torch row-major storage holding the Fortran matrix
+    src = pinned_in.T           # Fortran-ordered view of the pinned buffer
+    pinned_out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy().T
+    torch.cuda.synchronize()
+    times = []
+    for i in range(1 + args.steps):
+        t0 = time.perf_counter()
+        P.linalg.check(lib.abft_set_matrix(f._ctx, P._lib.dptr(src), n))
+        k_fault, rng = fault_plan(n, args.b, args.seed)
+        P.run_protected(f, args.scheme, {k_fault: {"0d": 1}}, rng)
+        P.linalg.check(lib.abft_get_matrix(f._ctx, P._lib.dptr(pinned_out), n))
+        dt = time.perf_counter() - t0
+        if i:
+            times.append(dt)
+    sec = statistics.median(times)
+    return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
+            "ms_per_step": sec * 1e3, "api": "abft_set_matrix + run_protected + abft_get_matrix"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

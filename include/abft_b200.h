@@ -94,6 +94,8 @@ typedef struct {
 ABFT_API int abft_version(void);
 ABFT_API const char* abft_last_error(void);
 ABFT_API int abft_device_count(int* count);
+/* kernels launched by this library so far (process-wide counter) */
+ABFT_API long long abft_launch_count(void);
 
 /* device-pointer primitive (for integrators that own device memory):
  * D = beta*C + alpha*op(A)*op(B) on `stream` (cudaStream_t, may be NULL). */
@@ -112,6 +114,12 @@ ABFT_API int abft_destroy(abft_ctx* ctx);
 ABFT_API int abft_set_matrix(abft_ctx* ctx, const double* a, int64_t lda);
 /* keep a device copy of the input for abft_residual(ctx, NULL, ...) */
 ABFT_API int abft_keep_input(abft_ctx* ctx, int keep);
+/* restore the working matrix from the kept input (needs abft_keep_input) */
+ABFT_API int abft_reset(abft_ctx* ctx);
+/* the context's cudaStream_t (for timing with events on the launching stream) */
+ABFT_API void* abft_stream(abft_ctx* ctx);
+/* m <- m m^T + n I on the device (SPD construction of linalg.py:74-75) */
+ABFT_API int abft_make_spd(abft_ctx* ctx);
 /* Factorization.m (host mirror): copy the device working matrix out */
 ABFT_API int abft_get_matrix(abft_ctx* ctx, double* m, int64_t ldm);
 /* Factorization.k_done */
@@ -139,6 +147,12 @@ ABFT_API int abft_qr_panels(abft_ctx* ctx);
 ABFT_API int abft_set_qr_panels(abft_ctx* ctx, int count);
 ABFT_API int abft_get_qr_panel(abft_ctx* ctx, int64_t k, double* V, int64_t ldv, double* T,
                                int64_t ldt);
+/* per-task device timers (CUDA events): enable/reset, then read
+ * ms[0]=PD, ms[1]=PU, ms[2]=TMU GEMMs, ms[3]=ABFT encode/maintain/verify/inject */
+ABFT_API int abft_profile(abft_ctx* ctx, int enable);
+ABFT_API int abft_profile_read(abft_ctx* ctx, double* ms);
+/* FP64 DMMA issue-rate probe (TFLOP/s) over all SMs: the roofline denominator */
+ABFT_API int abft_probe_dmma_peak(int iters, double* tflops);
 /* in-device snapshot slots replacing _Run._snapshot/_restore (simulator.py:420-436) */
 ABFT_API int abft_snapshot(abft_ctx* ctx, int slot);
 ABFT_API int abft_restore(abft_ctx* ctx, int slot);

@@ -60,12 +60,16 @@ SIGNATURES = [
     ("abft_version", _I, []),
     ("abft_last_error", ctypes.c_char_p, []),
     ("abft_device_count", _I, [ctypes.POINTER(_I)]),
+    ("abft_launch_count", ctypes.c_longlong, []),
     ("abft_dev_dgemm", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, ctypes.c_double,
                             _P, _I64, _P, _I64, ctypes.c_double, _P, _I64, _P, _I64]),
     ("abft_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
     ("abft_destroy", _I, [_P]),
     ("abft_set_matrix", _I, [_P, _D, _I64]),
     ("abft_keep_input", _I, [_P, _I]),
+    ("abft_reset", _I, [_P]),
+    ("abft_stream", _P, [_P]),
+    ("abft_make_spd", _I, [_P]),
     ("abft_get_matrix", _I, [_P, _D, _I64]),
     ("abft_k_done", _I64, [_P]),
     ("abft_set_k_done", _I, [_P, _I64]),
@@ -78,6 +82,9 @@ SIGNATURES = [
     ("abft_qr_panels", _I, [_P]),
     ("abft_set_qr_panels", _I, [_P, _I]),
     ("abft_get_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
+    ("abft_profile", _I, [_P, _I]),
+    ("abft_profile_read", _I, [_P, _D]),
+    ("abft_probe_dmma_peak", _I, [_I, _D]),
     ("abft_snapshot", _I, [_P, _I]),
     ("abft_restore", _I, [_P, _I]),
     ("abft_residual", _I, [_P, _D, _I64, _D]),

@@ -138,6 +138,8 @@ ABFT_DEVINL void emit(const EventSink& s, int bi, int bj, int seq, int kind, int
     e.detected_kind = det;
     e.corrected = corr;
     e.uncorrectable = unc;
+    e.iter = s.iter;
+    e.pad = 0;
     s.ev[slot] = e;
   }
 }
@@ -456,6 +458,7 @@ int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_
   int64_t nblk = blocks ? max_list : nbr * nbc;
   if (nblk <= 0) return 0;
   int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
+  count_launch();
   blocksum_kernel<<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
                                                   (int64_t)max_list);
   CUDA_TRY(cudaGetLastError());
@@ -470,6 +473,7 @@ int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int sch
   const int64_t warps = nbr * nbc;
   int grid = (int)((warps + 7) / 8);
   if (grid > 148 * 16) grid = 148 * 16;
+  count_launch();
   verify_kernel<<<grid, 256, 0, st>>>(reg, b_nominal, scheme, correct, rec, mt, sink, nbr, nbc);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -479,6 +483,7 @@ int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_col
            const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
            int64_t scale_cols, int64_t scale_ld, double host_scale) {
   if (nplan <= 0) return 0;
+  count_launch();
   inject_kernel<<<1, 1024, 0, st>>>(m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows,
                                     scale_cols, scale_ld, host_scale);
   CUDA_TRY(cudaGetLastError());
@@ -492,7 +497,9 @@ int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t co
     return 0;
   }
   const int g = (int)(cols < 1024 ? cols : 1024);
+  count_launch();
   sumsq_partial<<<g, 256, 0, st>>>(a, ld, rows, cols, scratch);
+  count_launch();
   sum_final<<<1, 1024, 0, st>>>(scratch, g, out);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -501,6 +508,7 @@ int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t co
 int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t lda,
              const double* x, int64_t incx, double* y) {
   if (rows <= 0 || k <= 0) return 0;
+  count_launch();
   gemv_sub_kernel<<<(unsigned)((rows + 31) / 32), 256, 0, st>>>(rows, k, A, lda, x, incx, y);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -508,6 +516,7 @@ int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t 
 
 int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
   if (rows <= 0 || cols <= 0) return 0;
+  count_launch();
   fill_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(a, ld, rows, cols, v);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -521,6 +530,7 @@ int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, in
                                cudaMemcpyDeviceToDevice, st));
     return 0;
   }
+  count_launch();
   copy_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols, mode);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -529,6 +539,7 @@ int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, in
 int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
                int64_t cols) {
   if (rows <= 0 || cols <= 0) return 0;
+  count_launch();
   sub_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -536,6 +547,7 @@ int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t
 
 int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v) {
   if (n <= 0) return 0;
+  count_launch();
   add_diag_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, ld, n, v);
   CUDA_TRY(cudaGetLastError());
   return 0;

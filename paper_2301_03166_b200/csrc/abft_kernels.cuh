@@ -53,6 +53,7 @@ struct Event {
   int32_t bi, bj, seq, kind;
   int64_t row, col;  // region-local
   int32_t flag, detected_kind, corrected, uncorrectable;
+  int32_t iter, pad;  // iteration that produced the event
 };
 
 struct EventSink {
@@ -62,6 +63,7 @@ struct EventSink {
   int32_t* dirty;        // (bi, bj) pairs of repaired blocks
   int32_t* dirty_count;
   int32_t dirty_capacity;
+  int32_t iter;
 };
 
 // K2: threshold, classify and repair (verify_correct + _handle_single/_full,

@@ -4,14 +4,59 @@
 
 using namespace abft;
 
+namespace {
+// Register-resident DMMA loop: 8 independent accumulators per warp.
+__global__ void dmma_peak_kernel(double* out, int iters) {
+  double a = threadIdx.x * 1e-3, b = 1.0 + threadIdx.x * 1e-4;
+  double c[8][2];
+  for (int i = 0; i < 8; ++i) c[i][0] = c[i][1] = 0.0;
+  for (int it = 0; it < iters; ++it)
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dmma_8x8x4(c[i][0], c[i][1], a, b);
+  double s = 0.0;
+  for (int i = 0; i < 8; ++i) s += c[i][0] + c[i][1];
+  if (s == 1234.5678) out[0] = s;
+}
+}  // namespace
+
 extern "C" {
 
 ABFT_API int abft_version(void) { return 100; }
+
+ABFT_API long long abft_launch_count(void) { return launch_count(); }
 
 ABFT_API const char* abft_last_error(void) { return last_error(); }
 
 ABFT_API int abft_device_count(int* count) {
   CUDA_TRY(cudaGetDeviceCount(count));
+  return 0;
+}
+
+ABFT_API int abft_probe_dmma_peak(int iters, double* tflops) {
+  int dev = 0, sms = 148;
+  CUDA_TRY(cudaGetDevice(&dev));
+  CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  double* out = nullptr;
+  CUDA_TRY(cudaMalloc(&out, sizeof(double)));
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  const int warps = 16, blocks = 2 * sms;
+  count_launch();
+  dmma_peak_kernel<<<blocks, warps * 32>>>(out, iters / 10 + 1);  // warm-up
+  cudaEventRecord(e0);
+  count_launch();
+  dmma_peak_kernel<<<blocks, warps * 32>>>(out, iters);
+  cudaEventRecord(e1);
+  cudaError_t err = cudaEventSynchronize(e1);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  CUDA_TRY(err);
+  const double flops = 2.0 * 8 * 8 * 4 * 8.0 * iters * (double)blocks * warps;
+  *tflops = flops / (ms * 1e-3) / 1e12;
   return 0;
 }
 

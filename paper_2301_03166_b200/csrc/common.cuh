@@ -20,6 +20,9 @@ namespace abft {
 // ---------------------------------------------------------------------------
 void set_last_error(const char* fmt, ...);
 const char* last_error();
+// number of kernels this library has launched (bench.py's gpu_launches)
+void count_launch();
+long long launch_count();
 
 #define CUDA_TRY(expr)                                                          \
   do {                                                                          \

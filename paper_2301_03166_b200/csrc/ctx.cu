@@ -28,6 +28,8 @@ namespace {
 inline int64_t round_even(int64_t x) { return (x + 1) / 2 * 2; }
 inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
+enum { PROF_PD = 0, PROF_PU = 1, PROF_TMU = 2, PROF_ABFT = 3, PROF_N = 4 };
+
 struct Snapshot {
   double* m = nullptr;
   int64_t k_done = 0;
@@ -96,7 +98,45 @@ struct abft_ctx {
   std::vector<Snapshot> snaps;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool timed = false;
+  int32_t cur_iter = 0;
+  // profiling
+  struct ProfPair {
+    int cat;
+    cudaEvent_t e0, e1;
+  };
+  bool prof_on = false;
+  double prof_ms[4] = {0, 0, 0, 0};
+  std::vector<ProfPair> prof_pending;
+  std::vector<cudaEvent_t> prof_free;
+  cudaEvent_t prof_open[4] = {nullptr, nullptr, nullptr, nullptr};
 };
+
+namespace {
+
+cudaEvent_t prof_event(abft_ctx* c) {
+  if (!c->prof_free.empty()) {
+    cudaEvent_t e = c->prof_free.back();
+    c->prof_free.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+}  // namespace
+
+void prof_mark(abft_ctx* c, int cat, bool begin) {
+  if (!c->prof_on) return;
+  cudaEvent_t e = prof_event(c);
+  cudaEventRecord(e, c->st);
+  if (begin) {
+    c->prof_open[cat] = e;
+  } else {
+    c->prof_pending.push_back({cat, c->prof_open[cat], e});
+    c->prof_open[cat] = nullptr;
+  }
+}
 
 namespace {
 
@@ -161,12 +201,12 @@ SumOut sums_for(abft_ctx* c, int64_t r0, int64_t c0, bool rows_too) {
   return o;
 }
 
-int check_info(abft_ctx* c, int64_t p) {
+int check_info(abft_ctx* c) {
   int h = 0;
   CUDA_TRY(cudaMemcpyAsync(&h, c->info, sizeof(int), cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
   if (h != 0) {
-    c->breakdown_col = p + h - 1;
+    c->breakdown_col = h - 1;
     if (c->kind == ABFT_CHOLESKY)
       set_last_error("non-positive pivot at column %lld", (long long)c->breakdown_col);
     else
@@ -184,7 +224,7 @@ int task_pd(abft_ctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   double* D = c->m + p + p * c->ld;
   if (c->kind == ABFT_LU) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info));
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info, p));
     if (pe < n) {
       // L21 = A21 U11^{-1}
       ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld,
@@ -192,7 +232,7 @@ int task_pd(abft_ctx* c, int64_t k) {
       ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w));
     }
   } else if (c->kind == ABFT_CHOLESKY) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info));
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
     double* V = c->vstore + p + p * c->ld;
     ABFT_TRY(qr_panel(c->st, D, c->ld, n - p, (int)w, V, c->ld, c->betas, c->qr_part,
@@ -402,10 +442,12 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   if (prot) {
     // encode (abft.py:118-135): reuse the previous verify's sums when the
     // region is a sub-grid of the last verified region (LU/QR), else a pass
+    prof_mark(c, PROF_ABFT, true);
     const bool reuse = c->sums_valid && c->kind != ABFT_CHOLESKY;
     if (!reuse) ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
+    if (c->kind != ABFT_QR) ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+    prof_mark(c, PROF_ABFT, false);
   }
-  if (prot && c->kind != ABFT_QR) ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
   bool did = false;
   if (prot && c->kind == ABFT_QR) {
     // QR: maintenance needs mid = T^T (V^T C), computed by the first GEMMs
@@ -414,13 +456,19 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
       const double* V = c->vstore + p + p * c->ld;
       const double* T = c->tstore + k * c->b * c->ld_t;
       double* C = c->m + p + pe * c->ld;
+      prof_mark(c, PROF_TMU, true);
       ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)(n - p), 1.0, V, c->ld, C, c->ld,
                     0.0, nullptr, 0, c->ww, c->ld_t, &c->gws));
       ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)(n - pe), (int)w, 1.0, T, c->ld_t, c->ww,
                     c->ld_t, 0.0, nullptr, 0, c->mid, c->ld_t, &c->gws));
+      prof_mark(c, PROF_TMU, false);
+      prof_mark(c, PROF_ABFT, true);
       ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+      prof_mark(c, PROF_ABFT, false);
+      prof_mark(c, PROF_TMU, true);
       ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V, c->ld, c->mid,
                     c->ld_t, 1.0, C, c->ld, C, c->ld, &c->gws));
+      prof_mark(c, PROF_TMU, false);
       did = true;
     } else {
       // no update: maintained == encoded
@@ -430,9 +478,12 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
       if (full) ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
     }
   } else {
+    prof_mark(c, PROF_TMU, true);
     ABFT_TRY(tmu_gemm(c, k, &did));
+    prof_mark(c, PROF_TMU, false);
   }
   (void)did;
+  prof_mark(c, PROF_ABFT, true);
   const bool faults = has_region && nplan > 0;
   if (prot) {
     // recomputed sums + block max of the updated region (verify's read)
@@ -476,7 +527,8 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
     mt.cw_step = 2;
     mt.rp = c->rsm;
     mt.rp_ld = c->ld;
-    EventSink sink{c->ev, c->counters, c->ev_cap, c->dirty, c->counters + 1, c->dirty_cap};
+    EventSink sink{c->ev,    c->counters,     c->ev_cap,  c->dirty,
+                   c->counters + 1, c->dirty_cap, c->cur_iter};
     ABFT_TRY(verify_blocks(c->st, reg, c->b, scheme, correct, sums_for(c, r0, c0, true), mt, sink));
     // refresh the sums of repaired blocks so they describe the current data
     ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true), c->dirty, c->counters + 1,
@@ -486,25 +538,38 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   } else {
     c->sums_valid = false;
   }
+  prof_mark(c, PROF_ABFT, false);
   return 0;
 }
 
+// Per-task device timers (CUDA events on the context stream), enabled by
+// abft_profile(ctx, 1): PD, PU, TMU GEMM(s) and the ABFT work around them.
+
+// One iteration in the reference's task order. `sync_checks`: read the
+// breakdown flag right after PD (per-iteration API); otherwise it is checked
+// once at the end of abft_factorize.
 int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
-                         int correct) {
-  const int64_t p = k * c->b;
+                         int correct, bool sync_checks) {
   auto pd = [&]() -> int {
+    prof_mark(c, PROF_PD, true);
     ABFT_TRY(task_pd(c, k));
+    prof_mark(c, PROF_PD, false);
+    if (sync_checks) ABFT_TRY(check_info(c));
+    return 0;
+  };
+  auto pu = [&]() -> int {
+    prof_mark(c, PROF_PU, true);
+    ABFT_TRY(task_pu(c, k));
+    prof_mark(c, PROF_PU, false);
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
     ABFT_TRY(pd());
-    ABFT_TRY(check_info(c, p));
-    ABFT_TRY(task_pu(c, k));
+    ABFT_TRY(pu());
   } else if (c->kind == ABFT_LU) {
     ABFT_TRY(pd());
-    ABFT_TRY(check_info(c, p));
-    ABFT_TRY(task_pu(c, k));
+    ABFT_TRY(pu());
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
   } else {
     ABFT_TRY(pd());
@@ -681,6 +746,11 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   if (c->info) cudaFree(c->info);
   for (auto& s : c->snaps)
     if (s.m) cudaFree(s.m);
+  for (auto& pe : c->prof_pending) {
+    cudaEventDestroy(pe.e0);
+    cudaEventDestroy(pe.e1);
+  }
+  for (auto e : c->prof_free) cudaEventDestroy(e);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->st) cudaStreamDestroy(c->st);
@@ -707,6 +777,42 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   return 0;
+}
+
+// Restore the working matrix from the kept device copy of the input (a new
+// factorization of the same matrix without a host round trip).
+ABFT_API int abft_reset(abft_ctx* c) {
+  DevGuard g(c->device);
+  if (!c->a0) {
+    set_last_error("abft_reset needs abft_keep_input(ctx, 1) before abft_set_matrix");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(c->m, c->ld * 8, c->a0, c->ld * 8, c->n * 8, c->n,
+                             cudaMemcpyDeviceToDevice, c->st));
+  c->k_done = 0;
+  c->sums_valid = false;
+  c->qr_count = 0;
+  c->breakdown_col = -1;
+  return 0;
+}
+
+ABFT_API void* abft_stream(abft_ctx* c) { return reinterpret_cast<void*>(c->st); }
+
+// m <- m m^T + n I on the device (generate_test_matrix's SPD construction,
+// linalg.py:74-75, with the product on the DMMA GEMM instead of host BLAS);
+// the kept input copy (if any) is refreshed.
+ABFT_API int abft_make_spd(abft_ctx* c) {
+  DevGuard g(c->device);
+  double* T = nullptr;
+  ABFT_TRY(dalloc(&T, c->ld * c->n));
+  int rc = gemm(c->st, 'N', 'T', (int)c->n, (int)c->n, (int)c->n, 1.0, c->m, c->ld, c->m, c->ld,
+                0.0, nullptr, 0, T, c->ld, &c->gws);
+  if (!rc) rc = add_diag(c->st, T, c->ld, c->n, (double)c->n);
+  if (!rc) rc = copy_matrix(c->st, T, c->ld, c->m, c->ld, c->n, c->n, 0);
+  if (!rc && c->a0) rc = copy_matrix(c->st, T, c->ld, c->a0, c->ld, c->n, c->n, 0);
+  cudaStreamSynchronize(c->st);
+  cudaFree(T);
+  return rc;
 }
 
 ABFT_API int abft_keep_input(abft_ctx* c, int keep) {
@@ -737,7 +843,7 @@ ABFT_API int abft_task(abft_ctx* c, int64_t k, int task) {
   }
   if (task == ABFT_TASK_PD) {
     ABFT_TRY(task_pd(c, k));
-    ABFT_TRY(check_info(c, k * c->b));
+    ABFT_TRY(check_info(c));
   } else if (task == ABFT_TASK_PU) {
     ABFT_TRY(task_pu(c, k));
   } else if (task == ABFT_TASK_TMU) {
@@ -764,7 +870,8 @@ ABFT_API int abft_iteration(abft_ctx* c, int64_t k, int scheme, const abft_fault
   }
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
-  int rc = run_iteration_device(c, k, scheme, plan, nplan, correct);
+  c->cur_iter = (int32_t)k;
+  int rc = run_iteration_device(c, k, scheme, plan, nplan, correct, true);
   CUDA_TRY(cudaEventRecord(c->e1, c->st));
   c->timed = true;
   if (rc != 0) return rc;
@@ -781,46 +888,99 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
   DevGuard g(c->device);
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
   if (n_locs) *n_locs = 0;
+  const int64_t k0 = c->k_done;
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
-  int total_locs = 0;
-  for (int64_t k = c->k_done; k < c->nb; ++k) {
+  for (int64_t k = k0; k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
-    // this iteration's slice of the flat plan
     int f0 = 0, f1 = 0;
     if (plan && plan_iter) {
       while (f0 < nplan && plan_iter[f0] < k) ++f0;
       f1 = f0;
       while (f1 < nplan && plan_iter[f1] == k) ++f1;
     }
-    int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct);
+    c->cur_iter = (int32_t)k;
+    int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false);
     if (rc != 0) {
       cudaEventRecord(c->e1, c->st);
       return rc;
     }
-    // events are only read when the iteration produced some: one 8-byte
-    // D2H of the counter per iteration, overlapped with the next launches
-    int32_t cnt = 0;
-    if (sch != ABFT_NONE) {
-      CUDA_TRY(cudaMemcpyAsync(&cnt, c->counters, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
-      CUDA_TRY(cudaStreamSynchronize(c->st));
-    }
-    abft_report rep;
-    memset(&rep, 0, sizeof(rep));
-    if (cnt > 0) {
-      int64_t r0, c0, rows, cols;
-      region_of(c, k, &r0, &c0, &rows, &cols);
-      const int room = locs ? std::max(0, max_locs - total_locs) : 0;
-      ABFT_TRY(collect_events(c, {r0}, {c0}, nullptr, &rep, locs ? locs + total_locs : nullptr,
-                              room, nullptr));
-      total_locs += rep.n_locations;
-    }
-    if (reports) reports[k] = rep;
-    c->k_done = k + 1;
   }
   CUDA_TRY(cudaEventRecord(c->e1, c->st));
+  // one synchronisation for the whole factorization
+  int brk = check_info(c);
+  if (brk != 0) {
+    c->k_done = c->breakdown_col / c->b;
+    return brk;
+  }
+  // events of all iterations, split per iteration in reference order
+  std::vector<Event> evs;
+  ABFT_TRY(collect_events(c, {0}, {0}, nullptr, nullptr, nullptr, 0, &evs));
+  std::stable_sort(evs.begin(), evs.end(), [](const Event& a, const Event& b) {
+    if (a.iter != b.iter) return a.iter < b.iter;
+    if (a.bi != b.bi) return a.bi < b.bi;
+    if (a.bj != b.bj) return a.bj < b.bj;
+    return a.seq < b.seq;
+  });
+  if (reports)
+    for (int64_t k = k0; k < c->nb; ++k) memset(&reports[k], 0, sizeof(abft_report));
+  int total = 0;
+  for (const Event& e : evs) {
+    if (e.kind < 0) {
+      set_last_error("index 0 is out of bounds for axis 0 with size 0");
+      return ABFT_E_RANGE;
+    }
+    const int64_t k = e.iter;
+    int64_t r0, c0, rows, cols;
+    region_of(c, k, &r0, &c0, &rows, &cols);
+    if (reports) {
+      abft_report& rep = reports[k];
+      rep.detected[e.detected_kind] += 1;
+      if (e.corrected) rep.corrected[e.detected_kind] += 1;
+      if (e.uncorrectable) rep.uncorrectable = 1;
+      rep.n_locations += 1;
+    }
+    if (locs && total < max_locs) {
+      abft_location& L = locs[total];
+      L.row = e.row + r0;
+      L.col = e.col + c0;
+      L.kind = e.kind;
+      L.flag = e.flag;
+      L.detected_kind = e.detected_kind;
+      L.corrected = e.corrected;
+      L.uncorrectable = e.uncorrectable;
+      L.block_row = e.bi;
+      L.block_col = e.bj;
+      L.seq = e.seq;
+    }
+    ++total;
+  }
+  c->k_done = c->nb;
+  if (n_locs) *n_locs = total;
+  return 0;
+}
+
+ABFT_API int abft_profile(abft_ctx* c, int enable) {
+  c->prof_on = enable != 0;
+  for (int i = 0; i < PROF_N; ++i) c->prof_ms[i] = 0.0;
+  c->prof_pending.clear();
+  return 0;
+}
+
+// Accumulated per-task device time since abft_profile(ctx, 1):
+// ms[0] PD, ms[1] PU, ms[2] TMU GEMMs, ms[3] ABFT (encode/maintain/verify/inject)
+ABFT_API int abft_profile_read(abft_ctx* c, double* ms) {
+  DevGuard g(c->device);
   CUDA_TRY(cudaStreamSynchronize(c->st));
-  if (n_locs) *n_locs = total_locs;
+  for (auto& pe : c->prof_pending) {
+    float f = 0.f;
+    CUDA_TRY(cudaEventElapsedTime(&f, pe.e0, pe.e1));
+    c->prof_ms[pe.cat] += f;
+    c->prof_free.push_back(pe.e0);
+    c->prof_free.push_back(pe.e1);
+  }
+  c->prof_pending.clear();
+  for (int i = 0; i < PROF_N; ++i) ms[i] = c->prof_ms[i];
   return 0;
 }
 

@@ -20,6 +20,7 @@
 
 #include <cstdarg>
 #include <cstring>
+#include <atomic>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -38,6 +39,10 @@ void set_last_error(const char* fmt, ...) {
   va_end(ap);
 }
 const char* last_error() { return g_last_error; }
+
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(); }
 
 // ---------------------------------------------------------------------------
 // TMA descriptor creation through the driver entry point (no -lcuda needed)
@@ -333,6 +338,7 @@ int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
     attr_set = true;
   }
   dim3 grid((kp.M + BM - 1) / BM, (kp.N + BN - 1) / BN, splits);
+  count_launch();
   dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, kp);
   CUDA_TRY(cudaGetLastError());
   return 0;
@@ -357,6 +363,7 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
   if (K <= 0) {
     // D = beta*C (alpha*0)
     if (beta == 0.0 && C == D) return 0;
+    count_launch();
     splitk_reduce<<<256, 256, 0, st>>>(M, N, 0, nullptr, 1, 0, C, ldc, D, ldd, alpha, beta);
     CUDA_TRY(cudaGetLastError());
     return 0;
@@ -441,6 +448,7 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
   if (splits > 1) {
     int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
+    count_launch();
     splitk_reduce<<<blocks, 256, 0, st>>>(M, N, splits, ws->ptr, ldw, slice, C, ldc, D, ldd, alpha,
                                           beta);
     CUDA_TRY(cudaGetLastError());

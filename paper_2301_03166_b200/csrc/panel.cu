@@ -80,7 +80,7 @@ ABFT_DEVINL void lower_inverse(const Acc& L, const Acc& X, int w, bool unit, dou
 // info: 0, or 1 + local column of the first breakdown.
 __global__ void __launch_bounds__(DT, 1)
     diag_factor_kernel(double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                       double* Uinv, int64_t ldu, int* info) {
+                       double* Uinv, int64_t ldu, int* info, int64_t col_base) {
   extern __shared__ double sm[];
   double* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
   double* Rs = sm + NBK * PLD;     // [224][33]   Rs[c*33 + i]
@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(DT, 1)
       if (bad) {
         if (tid == 0) {
           s_bad = jb + c + 1;
-          *info = jb + c + 1;
+          // first breakdown wins: 1 + global column
+          atomicCAS(info, 0, (int)(col_base + jb + c + 1));
         }
         break;  // uniform: every thread saw the same pivot
       }
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(DT, 1)
 }  // namespace
 
 int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                double* Uinv, int64_t ldu, int* info_dev) {
+                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
   if (w <= 0) return 0;
   if (w > 256) {
     set_last_error("diag_factor: block width %d > 256 (host-level blocking required)", w);
@@ -202,7 +203,9 @@ int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double*
                                   DIAG_SMEM));
     attr = true;
   }
-  diag_factor_kernel<<<1, DT, DIAG_SMEM, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev);
+  count_launch();
+  diag_factor_kernel<<<1, DT, DIAG_SMEM, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
+                                                col_base);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -392,6 +395,7 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     return -1;
   }
   void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf};
+  count_launch();
   CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QT), args, smem, st));
   return 0;
 }
@@ -410,6 +414,7 @@ int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, i
                                   200 * 1024));
     attr = true;
   }
+  count_launch();
   larft_kernel<<<1, 512, smem, st>>>(Gm, ldg, betas, w, T, ldt);
   CUDA_TRY(cudaGetLastError());
   return 0;

@@ -6,9 +6,10 @@ namespace abft {
 // Diagonal-block factorization (w <= 256) + triangular inverses on one CTA.
 // mode 0 = LU (no pivoting): Linv = L^{-1} (unit lower), Uinv = U^{-1}.
 // mode 1 = Cholesky: Linv = L^{-1}; strict upper of D zeroed. Uinv ignored.
-// *info_dev = 1 + local column of the first breakdown (left untouched if none).
+// *info_dev = 1 + (col_base + local column) of the first breakdown; left
+// untouched (0) if none, and never overwritten once set.
 int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                double* Uinv, int64_t ldu, int* info_dev);
+                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base);
 
 // Householder panel (nk x w) in place: R above/on the diagonal, zeros below;
 // V (nk x w, unit diagonal, zeros above) and betas (tau) out. part: >= 2*148*(w+1)

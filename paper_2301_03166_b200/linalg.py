@@ -213,7 +213,8 @@ class Factorization:
     ones in libabft_b200.so.
     """
 
-    def __init__(self, kind, a0: np.ndarray, b: int, device: int | None = None):
+    def __init__(self, kind, a0: np.ndarray, b: int, device: int | None = None,
+                 keep_input: bool = False):
         self.kind = DecompositionKind(_value(kind))
         self.a0 = a0
         self.b = int(b)
@@ -228,6 +229,8 @@ class Factorization:
                               self.device))
         self._ctx = ctx
         self._lib = lib
+        if keep_input:  # device copy of the input for reset()/residual without a0
+            check(lib.abft_keep_input(ctx, 1))
         host = np.asfortranarray(np.asarray(a0, dtype=np.float64))
         check(lib.abft_set_matrix(ctx, _lib.dptr(host), n))
         self._m_cache: np.ndarray | None = None
