@@ -103,6 +103,14 @@ ABFT_DEVINL void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, i
       : "memory");
 }
 
+// Bulk prefetch of a 2-D tensor box into L2 (no shared-memory destination).
+ABFT_DEVINL void tma_prefetch_l2_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];\n" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
+}
+
 ABFT_DEVINL void tma_prefetch_desc(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

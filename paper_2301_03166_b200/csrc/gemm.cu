@@ -98,217 +98,284 @@ int make_tma_map(CUtensorMap* map, const double* ptr, int64_t ld, int64_t inner,
 // ---------------------------------------------------------------------------
 namespace {
 
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 6;
-constexpr int NCONS = 8;  // consumer warps: 2 (M) x 4 (N), warp tile 64 x 32
-constexpr int THREADS = (NCONS + 4) * 32;  // + one producer warpgroup (1 active warp)
-constexpr int A_BYTES = BM * BK * 8;  // 16 KB
-constexpr int B_BYTES = BN * BK * 8;  // 16 KB
+// Persistent ping-pong DMMA GEMM.
+//   * grid = #SMs CTAs; each CTA walks tiles t = blockIdx.x + i*gridDim.x.
+//   * two consumer warpgroups (WG0, WG1) own alternate tiles (i even / odd),
+//     each with its own TMA ring and its own producer warp; an mbarrier token
+//     makes their main loops strictly alternate, so one group's epilogue
+//     (C load, D store, checksum partials) runs under the other's DMMA loop.
+//   * warp tile 64x32 (128 fp64 accumulators / thread), WG tile 128x64.
+constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+constexpr int WG_THREADS = 128;
+constexpr int THREADS = 3 * WG_THREADS;  // WG0, WG1 consume; WG2 warps 8/9 produce
+constexpr int A_BYTES = BM * BK * 8;      // 16 KB
+constexpr int B_BYTES = BN * BK * 8;      // 8 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 2 * STAGES * 8;
+constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+constexpr int SMEM_BYTES = 2 * RING_BYTES + 1024 + (2 * 2 * STAGES + 2) * 8;
+constexpr int EPI_RP = 1;  // row-pair groups whose C loads are batched in the epilogue
 
 struct KParams {
   int M, N, K;
   int a_shift, b_shift;
   int k_per_split;
+  int tiles_m, tiles_n, splits;
   const double* C;
   int64_t ldc;
   double* D;
   int64_t ldd;
   double alpha, beta;
-  int vec;          // 1 if C/D allow 16-byte row-pair accesses
-  int partial;      // 1: write raw acc to D (= split workspace slice z)
+  int vec;               // 1 if C/D allow 16-byte row-pair accesses
+  int prefetch_c;        // 1: TMA-prefetch each C tile into L2 when its main loop starts
+  int c_shift;
+  int partial;           // 1: write raw acc to D (= split workspace slice z)
   int64_t split_stride;  // elements between split slices in partial mode
 };
 
-// Row of accumulator row-fragment rf=(rp,e) for lane group g: wm+16rp+2g+e.
-// Column of (cf, c8): B-N: wn + 8cf + c8;  B-T: cf=(cp,f): wn + 16cp + 2c8 + f.
+// Column of accumulator fragment (cf, c8) inside the warp tile.
+// B-N: wn + 8cf + c8;  B-T: cf=(cp,f): wn + 16cp + 2c8 + f.
 template <bool BT>
 ABFT_DEVINL int col_of(int cf, int c8) {
   if (BT) return 16 * (cf >> 1) + 2 * c8 + (cf & 1);
   return 8 * cf + c8;
 }
 
+ABFT_DEVINL void tile_coords(const KParams& p, int t, int* m0, int* n0, int* z) {
+  const int tm = t % p.tiles_m;
+  const int r = t / p.tiles_m;
+  *m0 = tm * BM;
+  *n0 = (r % p.tiles_n) * BN;
+  *z = r / p.tiles_n;
+}
+
 template <bool AT, bool BT>
 __global__ void __launch_bounds__(THREADS, 1)
     dgemm_tma_dmma(const __grid_constant__ CUtensorMap mapA,
-                   const __grid_constant__ CUtensorMap mapB, KParams p) {
+                   const __grid_constant__ CUtensorMap mapB,
+                   const __grid_constant__ CUtensorMap mapC, KParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  uint64_t* empty = full + STAGES;
-
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * RING_BYTES);
+  // bars[wg*2*STAGES + s] = full, bars[wg*2*STAGES + STAGES + s] = empty, bars[4*STAGES + wg] = token
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
-  const int kz = blockIdx.z;
-  const int kbeg = kz * p.k_per_split;
-  const int kend = min(p.K, kbeg + p.k_per_split);
-  const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  const int total = p.tiles_m * p.tiles_n * p.splits;
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NCONS);
-    }
+    for (int w = 0; w < 2; ++w)
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars[w * 2 * STAGES + s], 1);
+        mbar_init(&bars[w * 2 * STAGES + STAGES + s], 4);
+      }
+    mbar_init(&bars[4 * STAGES + 0], 4);
+    mbar_init(&bars[4 * STAGES + 1], 4);
     mbar_fence_init();
   }
   __syncthreads();
 
-  if (warp >= NCONS) {
-    // ===== TMA producer warpgroup: hand registers to the consumers =====
+  if (warp >= 8) {
+    // ===== producers: warp 8 feeds ring 0, warp 9 feeds ring 1 =====
     asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
-    if (warp == NCONS && lane == 0) {
+    const int w = warp - 8;
+    if (w < 2 && lane == 0) {
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
-      for (int kt = 0; kt < nkt; ++kt) {
-        const int s = kt % STAGES;
-        if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        uint8_t* sb = sa + A_BYTES;
-        const int k0 = kbeg + kt * BK;
-        mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-        if (AT)
-          tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
-        else
-          tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
-        if (BT)
-          tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
-        else
-          tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+      uint64_t* full = bars + w * 2 * STAGES;
+      uint64_t* empty = full + STAGES;
+      uint8_t* ring = smem + w * RING_BYTES;
+      uint32_t q = 0;
+      for (int i = w;; i += 2) {
+        const int t = blockIdx.x + i * gridDim.x;
+        if (t >= total) break;
+        int m0, n0, z;
+        tile_coords(p, t, &m0, &n0, &z);
+        const int kbeg = z * p.k_per_split;
+        const int kend = min(p.K, kbeg + p.k_per_split);
+        const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+        if (p.prefetch_c) tma_prefetch_l2_2d(&mapC, m0 + p.c_shift, n0);
+        for (int kt = 0; kt < nkt; ++kt, ++q) {
+          const int s = q % STAGES;
+          if (q >= STAGES) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
+          uint8_t* sa = ring + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const int k0 = kbeg + kt * BK;
+          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+          if (AT)
+            tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
+          else
+            tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
+          if (BT)
+            tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
+          else
+            tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+        }
       }
     }
     return;
   }
 
-  // ===== DMMA consumers =====
+  // ===== consumers =====
   asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  const int wg = warp >> 2;
+  const int wi = warp & 3;
   const int g = lane >> 2, j = lane & 3;
-  const int wm = (warp & 1) * 64;
-  const int wn = (warp >> 1) * 32;
+  const int wm = (wi & 1) * 64;
+  const int wn = (wi >> 1) * 32;
+  uint64_t* full = bars + wg * 2 * STAGES;
+  uint64_t* empty = full + STAGES;
+  uint64_t* my_tok = bars + 4 * STAGES + wg;
+  uint64_t* other_tok = bars + 4 * STAGES + (1 - wg);
+  const uint32_t ring = smem_u32(smem + wg * RING_BYTES);
+  uint32_t q = 0;
+  int jt = 0;  // local tile counter of this WG
 
-  double acc[8][4][2];
+  for (int i = wg;; i += 2, ++jt) {
+    const int t = blockIdx.x + i * gridDim.x;
+    if (t >= total) break;
+    int m0, n0, z;
+    tile_coords(p, t, &m0, &n0, &z);
+    const int kbeg = z * p.k_per_split;
+    const int kend = min(p.K, kbeg + p.k_per_split);
+    const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+    double acc[8][4][2];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+    for (int a = 0; a < 8; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-  const uint32_t sbase = smem_u32(smem);
-
-  for (int kt = 0; kt < nkt; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    // lanes leave the spin loop independently; mma.sync.aligned needs the
-    // whole warp converged
+    // Phase offset: WG1 starts its first main loop when WG0 finishes its
+    // first one; afterwards both run free, so their epilogues interleave
+    // with the other group's DMMA loop while main loops co-run (two warps
+    // per SM sub-partition keep the DMMA pipe saturated).
+    if (wg == 1 && jt == 0) mbar_wait(my_tok, 0);
     __syncwarp();
-    const uint32_t sa = sbase + s * STAGE_BYTES;
-    const uint32_t sb = sa + A_BYTES;
+
+    for (int kt = 0; kt < nkt; ++kt, ++q) {
+      const int s = q % STAGES;
+      mbar_wait(&full[s], (q / STAGES) & 1);
+      __syncwarp();  // mma.sync.aligned needs the whole warp converged
+      const uint32_t sa = ring + s * STAGE_BYTES;
+      const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-    for (int ks = 0; ks < BK; ks += 8) {
-      // B fragments for both k-parities: b[cf][ss] = B(k = ks+2j+ss, col(cf, g))
-      double b[4][2];
-      if (!BT) {
-        // swizzled [n][16 k]: n = wn+8cf+g
+      for (int ks = 0; ks < BK; ks += 8) {
+        double b[4][2];
+        if (!BT) {
+          // swizzled [n][16 k]: n = wn+8cf+g
 #pragma unroll
-        for (int cf = 0; cf < 4; ++cf) {
-          const int n = wn + 8 * cf + g;
-          double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
-          b[cf][0] = v.x;
-          b[cf][1] = v.y;
-        }
-      } else {
-        // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
-#pragma unroll
-        for (int cp = 0; cp < 2; ++cp)
-#pragma unroll
-          for (int ss = 0; ss < 2; ++ss) {
-            double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
-            b[2 * cp][ss] = v.x;
-            b[2 * cp + 1][ss] = v.y;
-          }
-      }
-#pragma unroll
-      for (int rp = 0; rp < 4; ++rp) {
-        // a[ss][e] = A(row = wm+16rp+2g+e, k = ks+2j+ss)
-        double a[2][2];
-        if (!AT) {
-          // dense [k][m], BM doubles per k row
-#pragma unroll
-          for (int ss = 0; ss < 2; ++ss) {
-            double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
-            a[ss][0] = v.x;
-            a[ss][1] = v.y;
+          for (int cf = 0; cf < 4; ++cf) {
+            const int n = wn + 8 * cf + g;
+            double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
+            b[cf][0] = v.x;
+            b[cf][1] = v.y;
           }
         } else {
-          // swizzled [m][16 k]
+          // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int m = wm + 16 * rp + 2 * g + e;
-            double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
-            a[0][e] = v.x;
-            a[1][e] = v.y;
-          }
+          for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+            for (int ss = 0; ss < 2; ++ss) {
+              double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
+              b[2 * cp][ss] = v.x;
+              b[2 * cp + 1][ss] = v.y;
+            }
         }
 #pragma unroll
-        for (int ss = 0; ss < 2; ++ss)
+        for (int rp = 0; rp < 4; ++rp) {
+          double a[2][2];
+          if (!AT) {
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
+            for (int ss = 0; ss < 2; ++ss) {
+              double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
+              a[ss][0] = v.x;
+              a[ss][1] = v.y;
+            }
+          } else {
 #pragma unroll
-            for (int cf = 0; cf < 4; ++cf)
-              dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
+            for (int e = 0; e < 2; ++e) {
+              const int m = wm + 16 * rp + 2 * g + e;
+              double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
+              a[0][e] = v.x;
+              a[1][e] = v.y;
+            }
+          }
+#pragma unroll
+          for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+              for (int cf = 0; cf < 4; ++cf)
+                dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
+        }
+      }
+      consumer_release(&empty[s], lane);
+    }
+    if (wg == 0 && jt == 0 && lane == 0) mbar_arrive(other_tok);
+
+    // ===== epilogue =====
+    // EPI_RP row-pair groups at a time: their C loads are all issued before
+    // any use, so the (L2-prefetched) reads overlap instead of serialising.
+    double* D = p.partial ? p.D + (int64_t)z * p.split_stride : p.D;
+    const bool use_c = !p.partial && p.beta != 0.0;
+#pragma unroll
+    for (int rq = 0; rq < 4; rq += EPI_RP) {
+      double cv[EPI_RP][4][2][2];
+      if (use_c) {
+#pragma unroll
+        for (int h = 0; h < EPI_RP; ++h) {
+          const int row = m0 + wm + 16 * (rq + h) + 2 * g;
+#pragma unroll
+          for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+              const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
+              cv[h][cf][tt][0] = cv[h][cf][tt][1] = 0.0;
+              if (row >= p.M || col >= p.N) continue;
+              const double* c = p.C + row + (int64_t)col * p.ldc;
+              if (row + 1 < p.M && p.vec) {
+                const double2 v = *reinterpret_cast<const double2*>(c);
+                cv[h][cf][tt][0] = v.x;
+                cv[h][cf][tt][1] = v.y;
+              } else {
+                cv[h][cf][tt][0] = c[0];
+                if (row + 1 < p.M) cv[h][cf][tt][1] = c[1];
+              }
+            }
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < EPI_RP; ++h) {
+        const int rp = rq + h;
+        const int row = m0 + wm + 16 * rp + 2 * g;
+        if (row >= p.M) continue;
+        const bool pair = row + 1 < p.M;
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
+            const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
+            if (col >= p.N) continue;
+            const double v0 = acc[2 * rp][cf][tt], v1 = acc[2 * rp + 1][cf][tt];
+            double* d = D + row + (int64_t)col * p.ldd;
+            if (p.partial) {
+              d[0] = v0;
+              if (pair) d[1] = v1;
+              continue;
+            }
+            const double c0 = use_c ? cv[h][cf][tt][0] : 0.0;
+            const double c1 = use_c ? cv[h][cf][tt][1] : 0.0;
+            const double o0 = fma(p.alpha, v0, p.beta * c0);
+            const double o1 = fma(p.alpha, v1, p.beta * c1);
+            if (pair && p.vec) {
+              *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+            } else {
+              d[0] = o0;
+              if (pair) d[1] = o1;
+            }
+          }
       }
     }
-    // Release the stage only after this warp's shared-memory reads have
-    // completed: SYNCS.ARRIVE is not ordered behind in-flight LDS, so without
-    // the fence the producer's TMA can overwrite the last fragments before
-    // they land in registers (write-after-read across the async proxy).
-    consumer_release(&empty[s], lane);
-  }
-
-  // ===== epilogue =====
-  double* D = p.partial ? p.D + (int64_t)kz * p.split_stride : p.D;
-  const bool use_c = !p.partial && p.beta != 0.0;
-#pragma unroll
-  for (int rp = 0; rp < 4; ++rp) {
-    const int row = m0 + wm + 16 * rp + 2 * g;
-    if (row >= p.M) continue;
-    const bool pair = row + 1 < p.M;
-#pragma unroll
-    for (int cf = 0; cf < 4; ++cf)
-#pragma unroll
-      for (int t = 0; t < 2; ++t) {
-        const int col = n0 + wn + col_of<BT>(cf, 2 * j + t);
-        if (col >= p.N) continue;
-        double v0 = acc[2 * rp][cf][t], v1 = acc[2 * rp + 1][cf][t];
-        if (p.partial) {
-          double* d = D + row + (int64_t)col * p.ldd;
-          d[0] = v0;
-          if (pair) d[1] = v1;
-          continue;
-        }
-        double c0 = 0.0, c1 = 0.0;
-        const double* c = p.C + row + (int64_t)col * p.ldc;
-        double* d = D + row + (int64_t)col * p.ldd;
-        if (pair && p.vec) {
-          if (use_c) {
-            double2 cv = *reinterpret_cast<const double2*>(c);
-            c0 = cv.x;
-            c1 = cv.y;
-          }
-          double2 o;
-          o.x = fma(p.alpha, v0, p.beta * c0);
-          o.y = fma(p.alpha, v1, p.beta * c1);
-          *reinterpret_cast<double2*>(d) = o;
-        } else {
-          if (use_c) {
-            c0 = c[0];
-            if (pair) c1 = c[1];
-          }
-          d[0] = fma(p.alpha, v0, p.beta * c0);
-          if (pair) d[1] = fma(p.alpha, v1, p.beta * c1);
-        }
-      }
   }
 }
 
@@ -329,7 +396,8 @@ __global__ void splitk_reduce(int M, int N, int splits, const double* __restrict
 }
 
 template <bool AT, bool BT>
-int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, const KParams& kp,
+int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
+                  const CUtensorMap& mc, const KParams& kp,
                   int splits) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -337,9 +405,13 @@ int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
                                   cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
     attr_set = true;
   }
-  dim3 grid((kp.M + BM - 1) / BM, (kp.N + BN - 1) / BN, splits);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int total = kp.tiles_m * kp.tiles_n * kp.splits;
+  const int grid = total < sms ? total : sms;
   count_launch();
-  dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, kp);
+  dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, mc, kp);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -416,6 +488,9 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
   kp.k_per_split = kps;
   kp.alpha = alpha;
   kp.beta = beta;
+  kp.tiles_m = (M + BM - 1) / BM;
+  kp.tiles_n = (N + BN - 1) / BN;
+  kp.splits = splits;
   if (splits > 1) {
     kp.C = nullptr;
     kp.ldc = 0;
@@ -435,15 +510,26 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
     const bool dv = (reinterpret_cast<uintptr_t>(D) & 15) == 0 && ldd % 2 == 0;
     kp.vec = (cv && dv) ? 1 : 0;
   }
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof(mc));
+  kp.prefetch_c = 0;
+  kp.c_shift = 0;
+  if (!kp.partial && beta != 0.0 && (ldc % 2) == 0) {
+    int shc = 0;
+    if (make_tma_map(&mc, C, ldc, M, N, BM, BN, false, &shc) == 0) {
+      kp.prefetch_c = 1;
+      kp.c_shift = shc;
+    }
+  }
   int rc;
   if (AT && BT)
-    rc = launch_kernel<true, true>(st, ma, mb, kp, splits);
+    rc = launch_kernel<true, true>(st, ma, mb, mc, kp, splits);
   else if (AT)
-    rc = launch_kernel<true, false>(st, ma, mb, kp, splits);
+    rc = launch_kernel<true, false>(st, ma, mb, mc, kp, splits);
   else if (BT)
-    rc = launch_kernel<false, true>(st, ma, mb, kp, splits);
+    rc = launch_kernel<false, true>(st, ma, mb, mc, kp, splits);
   else
-    rc = launch_kernel<false, false>(st, ma, mb, kp, splits);
+    rc = launch_kernel<false, false>(st, ma, mb, mc, kp, splits);
   if (rc) return rc;
   if (splits > 1) {
     int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
