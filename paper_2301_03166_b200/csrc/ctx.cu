@@ -99,6 +99,7 @@ struct abft_ctx {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool timed = false;
   int32_t cur_iter = 0;
+  bool fuse_enabled = true;  // ABFT_NO_FUSE=1 disables (A/B testing)
   // profiling
   struct ProfPair {
     int cat;
@@ -199,6 +200,22 @@ SumOut sums_for(abft_ctx* c, int64_t r0, int64_t c0, bool rows_too) {
   o.bm = c->gmax + gbi + gbj * c->ld_max;
   o.bm_ld = c->ld_max;
   return o;
+}
+
+FusedSums fused_for(abft_ctx* c, int64_t r0, int64_t c0) {
+  const SumOut o = sums_for(c, r0, c0, true);
+  FusedSums f;
+  f.cp = o.cp;
+  f.cp_ld = o.cp_ld;
+  f.cp_step = o.cp_step;
+  f.cw = o.cw;
+  f.cw_ld = o.cw_ld;
+  f.cw_step = o.cw_step;
+  f.rp = o.rp;
+  f.rp_ld = o.rp_ld;
+  f.bm = o.bm;
+  f.bm_ld = o.bm_ld;
+  return f;
 }
 
 int check_info(abft_ctx* c) {
@@ -439,6 +456,10 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   const bool prot = scheme != ABFT_NONE && has_region;
   Region reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
   const bool full = scheme == ABFT_FULL;
+  // LU / QR trailing updates produce the verify sums in the GEMM epilogue
+  // (b = 128 / 256); Cholesky's left-looking panel update keeps the pass.
+  const bool fuse = prot && c->fuse_enabled && c->kind != ABFT_CHOLESKY && gemm_can_fuse((int)c->b);
+  bool fused_done = false;
   if (prot) {
     // encode (abft.py:118-135): reuse the previous verify's sums when the
     // region is a sub-grid of the last verified region (LU/QR), else a pass
@@ -466,8 +487,15 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
       ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
       prof_mark(c, PROF_ABFT, false);
       prof_mark(c, PROF_TMU, true);
-      ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V, c->ld, c->mid,
-                    c->ld_t, 1.0, C, c->ld, C, c->ld, &c->gws));
+      if (fuse) {
+        ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V,
+                                 c->ld, c->mid, c->ld_t, 1.0, C, c->ld, C, c->ld, (int)c->b,
+                                 fused_for(c, r0, c0)));
+        fused_done = true;
+      } else {
+        ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - p), (int)(n - pe), (int)w, -1.0, V, c->ld,
+                      c->mid, c->ld_t, 1.0, C, c->ld, C, c->ld, &c->gws));
+      }
       prof_mark(c, PROF_TMU, false);
       did = true;
     } else {
@@ -477,6 +505,18 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
       ABFT_TRY(copy_matrix(c->st, enc.cp, c->ld_cs, c->csm, c->ld_cs, 2 * nbr, cols));
       if (full) ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
     }
+  } else if (prot && fuse && c->kind == ABFT_LU) {
+    // A22 -= L21 U12 with the verify-side block sums produced by the epilogue
+    const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+    prof_mark(c, PROF_TMU, true);
+    if (pe < n) {
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)(n - pe), (int)(n - pe), (int)w, -1.0,
+                               c->m + pe + p * c->ld, c->ld, c->m + p + pe * c->ld, c->ld, 1.0,
+                               c->m + pe + pe * c->ld, c->ld, c->m + pe + pe * c->ld, c->ld,
+                               (int)c->b, fused_for(c, r0, c0)));
+      fused_done = true;
+    }
+    prof_mark(c, PROF_TMU, false);
   } else {
     prof_mark(c, PROF_TMU, true);
     ABFT_TRY(tmu_gemm(c, k, &did));
@@ -485,10 +525,10 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   (void)did;
   prof_mark(c, PROF_ABFT, true);
   const bool faults = has_region && nplan > 0;
-  if (prot) {
+  if (prot && !fused_done) {
     // recomputed sums + block max of the updated region (verify's read)
     ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
-  } else if (faults) {
+  } else if (!prot && faults) {
     SumOut o;
     o.bm = c->gmax + (r0 / c->b) + (c0 / c->b) * c->ld_max;
     o.bm_ld = c->ld_max;
@@ -674,6 +714,10 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   c->ld_cs = round_even(2 * c->nb);
   c->ld_max = round_even(c->nb);
   c->ld_t = round_even(b);
+  {
+    const char* e = getenv("ABFT_NO_FUSE");
+    c->fuse_enabled = !(e && e[0] == '1');
+  }
   int rc = 0;
   auto fail = [&](int r) {
     abft_destroy(c);

@@ -112,7 +112,11 @@ constexpr int A_BYTES = BM * BK * 8;      // 16 KB
 constexpr int B_BYTES = BN * BK * 8;      // 8 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int RING_BYTES = STAGES * STAGE_BYTES;
-constexpr int SMEM_BYTES = 2 * RING_BYTES + 1024 + (2 * 2 * STAGES + 2) * 8;
+constexpr int MAXFB = 256;
+// per-WG fused-checksum accumulators: col plain/weighted [2 wm halves][fb][2],
+// row plain [2 wn halves][fb], warp max [4]
+constexpr int SUM_DOUBLES = 2 * MAXFB * 2 + 2 * MAXFB + 4;
+constexpr int SMEM_BYTES = 2 * RING_BYTES + 1024 + (2 * 2 * STAGES + 2) * 8 + 2 * SUM_DOUBLES * 8;
 constexpr int EPI_RP = 1;  // row-pair groups whose C loads are batched in the epilogue
 
 struct KParams {
@@ -128,6 +132,9 @@ struct KParams {
   int vec;               // 1 if C/D allow 16-byte row-pair accesses
   int prefetch_c;        // 1: TMA-prefetch each C tile into L2 when its main loop starts
   int c_shift;
+  // fused checksums: each warpgroup owns whole fb x fb blocks (fb = 128/256)
+  int fuse, fb, ntm_b, ntn_b, nbr_b, nbc_b;
+  FusedSums sums;
   int partial;           // 1: write raw acc to D (= split workspace slice z)
   int64_t split_stride;  // elements between split slices in partial mode
 };
@@ -138,6 +145,22 @@ template <bool BT>
 ABFT_DEVINL int col_of(int cf, int c8) {
   if (BT) return 16 * (cf >> 1) + 2 * c8 + (cf & 1);
   return 8 * cf + c8;
+}
+
+// Work unit u of a warpgroup: plain mode = one tile; fused mode = one
+// fb x fb block (ntm_b x ntn_b tiles). Returns the number of tiles in it.
+ABFT_DEVINL int unit_tiles(const KParams& p) { return p.fuse ? p.ntm_b * p.ntn_b : 1; }
+ABFT_DEVINL int total_units(const KParams& p) {
+  return p.fuse ? p.nbr_b * p.nbc_b : p.tiles_m * p.tiles_n * p.splits;
+}
+ABFT_DEVINL void fused_tile(const KParams& p, int unit, int u, int* m0, int* n0, int* bi, int* bj,
+                            int* tm, int* tn) {
+  *bi = unit % p.nbr_b;
+  *bj = unit / p.nbr_b;
+  *tm = u % p.ntm_b;
+  *tn = u / p.ntm_b;
+  *m0 = *bi * p.fb + *tm * BM;
+  *n0 = *bj * p.fb + *tn * BN;
 }
 
 ABFT_DEVINL void tile_coords(const KParams& p, int t, int* m0, int* n0, int* z) {
@@ -158,9 +181,11 @@ __global__ void __launch_bounds__(THREADS, 1)
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * RING_BYTES);
   // bars[wg*2*STAGES + s] = full, bars[wg*2*STAGES + STAGES + s] = empty, bars[4*STAGES + wg] = token
+  double* sums_base = reinterpret_cast<double*>(bars + 4 * STAGES + 2);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int total = p.tiles_m * p.tiles_n * p.splits;
+  const int units = total_units(p);
+  const int upt = unit_tiles(p);
 
   if (threadIdx.x == 0) {
     for (int w = 0; w < 2; ++w)
@@ -172,6 +197,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     mbar_init(&bars[4 * STAGES + 1], 4);
     mbar_fence_init();
   }
+  for (int i = threadIdx.x; i < 2 * SUM_DOUBLES; i += THREADS) sums_base[i] = 0.0;
   __syncthreads();
 
   if (warp >= 8) {
@@ -186,29 +212,37 @@ __global__ void __launch_bounds__(THREADS, 1)
       uint8_t* ring = smem + w * RING_BYTES;
       uint32_t q = 0;
       for (int i = w;; i += 2) {
-        const int t = blockIdx.x + i * gridDim.x;
-        if (t >= total) break;
-        int m0, n0, z;
-        tile_coords(p, t, &m0, &n0, &z);
-        const int kbeg = z * p.k_per_split;
-        const int kend = min(p.K, kbeg + p.k_per_split);
-        const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-        if (p.prefetch_c) tma_prefetch_l2_2d(&mapC, m0 + p.c_shift, n0);
-        for (int kt = 0; kt < nkt; ++kt, ++q) {
-          const int s = q % STAGES;
-          if (q >= STAGES) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
-          uint8_t* sa = ring + s * STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
-          const int k0 = kbeg + kt * BK;
-          mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-          if (AT)
-            tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
-          else
-            tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
-          if (BT)
-            tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
-          else
-            tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+        const int unit = blockIdx.x + i * gridDim.x;
+        if (unit >= units) break;
+        for (int u = 0; u < upt; ++u) {
+          int m0, n0, z = 0;
+          if (p.fuse) {
+            int bi, bj, tm, tn;
+            fused_tile(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
+          } else {
+            tile_coords(p, unit, &m0, &n0, &z);
+          }
+          if (m0 >= p.M || n0 >= p.N) continue;
+          const int kbeg = z * p.k_per_split;
+          const int kend = min(p.K, kbeg + p.k_per_split);
+          const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+          if (p.prefetch_c) tma_prefetch_l2_2d(&mapC, m0 + p.c_shift, n0);
+          for (int kt = 0; kt < nkt; ++kt, ++q) {
+            const int s = q % STAGES;
+            if (q >= STAGES) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
+            uint8_t* sa = ring + s * STAGE_BYTES;
+            uint8_t* sb = sa + A_BYTES;
+            const int k0 = kbeg + kt * BK;
+            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+            if (AT)
+              tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
+            else
+              tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
+            if (BT)
+              tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
+            else
+              tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+          }
         }
       }
     }
@@ -227,154 +261,230 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint64_t* my_tok = bars + 4 * STAGES + wg;
   uint64_t* other_tok = bars + 4 * STAGES + (1 - wg);
   const uint32_t ring = smem_u32(smem + wg * RING_BYTES);
+  // fused-checksum accumulators of this warpgroup
+  double* colacc = sums_base + wg * SUM_DOUBLES;   // [2][MAXFB][2]
+  double* rowacc = colacc + 2 * MAXFB * 2;         // [2][MAXFB]
+  double* wmax = rowacc + 2 * MAXFB;               // [4]
   uint32_t q = 0;
-  int jt = 0;  // local tile counter of this WG
+  int jt = 0;  // tiles processed by this WG
 
-  for (int i = wg;; i += 2, ++jt) {
-    const int t = blockIdx.x + i * gridDim.x;
-    if (t >= total) break;
-    int m0, n0, z;
-    tile_coords(p, t, &m0, &n0, &z);
-    const int kbeg = z * p.k_per_split;
-    const int kend = min(p.K, kbeg + p.k_per_split);
-    const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+  for (int i = wg;; i += 2) {
+    const int unit = blockIdx.x + i * gridDim.x;
+    if (unit >= units) break;
+    double mx = 0.0;
+    int bi = 0, bj = 0;
+    for (int u = 0; u < upt; ++u) {
+      int m0, n0, z = 0, tm = 0, tn = 0;
+      if (p.fuse)
+        fused_tile(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
+      else
+        tile_coords(p, unit, &m0, &n0, &z);
+      if (m0 >= p.M || n0 >= p.N) continue;
+      const int kbeg = z * p.k_per_split;
+      const int kend = min(p.K, kbeg + p.k_per_split);
+      const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
-    double acc[8][4][2];
+      double acc[8][4][2];
 #pragma unroll
-    for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 8; ++a)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+        for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-    // Phase offset: WG1 starts its first main loop when WG0 finishes its
-    // first one; afterwards both run free, so their epilogues interleave
-    // with the other group's DMMA loop while main loops co-run (two warps
-    // per SM sub-partition keep the DMMA pipe saturated).
-    if (wg == 1 && jt == 0) mbar_wait(my_tok, 0);
-    __syncwarp();
+      // Phase offset: WG1 starts its first main loop when WG0 finishes its
+      // first one; afterwards both run free, so their epilogues interleave
+      // with the other group's DMMA loop while main loops co-run (two warps
+      // per SM sub-partition keep the DMMA pipe saturated).
+      if (wg == 1 && jt == 0) mbar_wait(my_tok, 0);
+      __syncwarp();
 
-    for (int kt = 0; kt < nkt; ++kt, ++q) {
-      const int s = q % STAGES;
-      mbar_wait(&full[s], (q / STAGES) & 1);
-      __syncwarp();  // mma.sync.aligned needs the whole warp converged
-      const uint32_t sa = ring + s * STAGE_BYTES;
-      const uint32_t sb = sa + A_BYTES;
+      for (int kt = 0; kt < nkt; ++kt, ++q) {
+        const int s = q % STAGES;
+        mbar_wait(&full[s], (q / STAGES) & 1);
+        __syncwarp();  // mma.sync.aligned needs the whole warp converged
+        const uint32_t sa = ring + s * STAGE_BYTES;
+        const uint32_t sb = sa + A_BYTES;
 #pragma unroll
-      for (int ks = 0; ks < BK; ks += 8) {
-        double b[4][2];
-        if (!BT) {
-          // swizzled [n][16 k]: n = wn+8cf+g
+        for (int ks = 0; ks < BK; ks += 8) {
+          double b[4][2];
+          if (!BT) {
+            // swizzled [n][16 k]: n = wn+8cf+g
 #pragma unroll
-          for (int cf = 0; cf < 4; ++cf) {
-            const int n = wn + 8 * cf + g;
-            double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
-            b[cf][0] = v.x;
-            b[cf][1] = v.y;
-          }
-        } else {
-          // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
-#pragma unroll
-          for (int cp = 0; cp < 2; ++cp)
-#pragma unroll
-            for (int ss = 0; ss < 2; ++ss) {
-              double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
-              b[2 * cp][ss] = v.x;
-              b[2 * cp + 1][ss] = v.y;
-            }
-        }
-#pragma unroll
-        for (int rp = 0; rp < 4; ++rp) {
-          double a[2][2];
-          if (!AT) {
-#pragma unroll
-            for (int ss = 0; ss < 2; ++ss) {
-              double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
-              a[ss][0] = v.x;
-              a[ss][1] = v.y;
+            for (int cf = 0; cf < 4; ++cf) {
+              const int n = wn + 8 * cf + g;
+              double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
+              b[cf][0] = v.x;
+              b[cf][1] = v.y;
             }
           } else {
+            // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
 #pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int m = wm + 16 * rp + 2 * g + e;
-              double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
-              a[0][e] = v.x;
-              a[1][e] = v.y;
-            }
+            for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+              for (int ss = 0; ss < 2; ++ss) {
+                double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
+                b[2 * cp][ss] = v.x;
+                b[2 * cp + 1][ss] = v.y;
+              }
           }
 #pragma unroll
-          for (int ss = 0; ss < 2; ++ss)
+          for (int rp = 0; rp < 4; ++rp) {
+            double a[2][2];
+            if (!AT) {
 #pragma unroll
-            for (int e = 0; e < 2; ++e)
+              for (int ss = 0; ss < 2; ++ss) {
+                double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
+                a[ss][0] = v.x;
+                a[ss][1] = v.y;
+              }
+            } else {
 #pragma unroll
-              for (int cf = 0; cf < 4; ++cf)
-                dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
-        }
-      }
-      consumer_release(&empty[s], lane);
-    }
-    if (wg == 0 && jt == 0 && lane == 0) mbar_arrive(other_tok);
-
-    // ===== epilogue =====
-    // EPI_RP row-pair groups at a time: their C loads are all issued before
-    // any use, so the (L2-prefetched) reads overlap instead of serialising.
-    double* D = p.partial ? p.D + (int64_t)z * p.split_stride : p.D;
-    const bool use_c = !p.partial && p.beta != 0.0;
-#pragma unroll
-    for (int rq = 0; rq < 4; rq += EPI_RP) {
-      double cv[EPI_RP][4][2][2];
-      if (use_c) {
-#pragma unroll
-        for (int h = 0; h < EPI_RP; ++h) {
-          const int row = m0 + wm + 16 * (rq + h) + 2 * g;
-#pragma unroll
-          for (int cf = 0; cf < 4; ++cf)
-#pragma unroll
-            for (int tt = 0; tt < 2; ++tt) {
-              const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
-              cv[h][cf][tt][0] = cv[h][cf][tt][1] = 0.0;
-              if (row >= p.M || col >= p.N) continue;
-              const double* c = p.C + row + (int64_t)col * p.ldc;
-              if (row + 1 < p.M && p.vec) {
-                const double2 v = *reinterpret_cast<const double2*>(c);
-                cv[h][cf][tt][0] = v.x;
-                cv[h][cf][tt][1] = v.y;
-              } else {
-                cv[h][cf][tt][0] = c[0];
-                if (row + 1 < p.M) cv[h][cf][tt][1] = c[1];
+              for (int e = 0; e < 2; ++e) {
+                const int m = wm + 16 * rp + 2 * g + e;
+                double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
+                a[0][e] = v.x;
+                a[1][e] = v.y;
               }
             }
-        }
-      }
 #pragma unroll
-      for (int h = 0; h < EPI_RP; ++h) {
-        const int rp = rq + h;
+            for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+              for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int cf = 0; cf < 4; ++cf)
+                  dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
+          }
+        }
+        consumer_release(&empty[s], lane);
+      }
+      if (wg == 0 && jt == 0 && lane == 0) mbar_arrive(other_tok);
+      ++jt;
+
+      // ===== epilogue =====
+      // Pass 1 (per row-pair group, C loads batched): out = alpha*acc + beta*C,
+      // computed in place in the accumulator registers and stored.
+      double* D = p.partial ? p.D + (int64_t)z * p.split_stride : p.D;
+      const bool use_c = !p.partial && p.beta != 0.0;
+#pragma unroll
+      for (int rp = 0; rp < 4; ++rp) {
         const int row = m0 + wm + 16 * rp + 2 * g;
-        if (row >= p.M) continue;
-        const bool pair = row + 1 < p.M;
+        const bool rv0 = row < p.M, rv1 = row + 1 < p.M;
+        double cv[4][2][2];
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
+            cv[cf][tt][0] = cv[cf][tt][1] = 0.0;
+            const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
+            if (!use_c || !rv0 || col >= p.N) continue;
+            const double* c = p.C + row + (int64_t)col * p.ldc;
+            if (rv1 && p.vec) {
+              const double2 v = *reinterpret_cast<const double2*>(c);
+              cv[cf][tt][0] = v.x;
+              cv[cf][tt][1] = v.y;
+            } else {
+              cv[cf][tt][0] = c[0];
+              if (rv1) cv[cf][tt][1] = c[1];
+            }
+          }
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf)
 #pragma unroll
           for (int tt = 0; tt < 2; ++tt) {
             const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
-            if (col >= p.N) continue;
-            const double v0 = acc[2 * rp][cf][tt], v1 = acc[2 * rp + 1][cf][tt];
-            double* d = D + row + (int64_t)col * p.ldd;
-            if (p.partial) {
-              d[0] = v0;
-              if (pair) d[1] = v1;
-              continue;
+            const bool cvld = col < p.N;
+            double o0 = acc[2 * rp][cf][tt], o1 = acc[2 * rp + 1][cf][tt];
+            if (!p.partial) {
+              o0 = fma(p.alpha, o0, p.beta * cv[cf][tt][0]);
+              o1 = fma(p.alpha, o1, p.beta * cv[cf][tt][1]);
             }
-            const double c0 = use_c ? cv[h][cf][tt][0] : 0.0;
-            const double c1 = use_c ? cv[h][cf][tt][1] : 0.0;
-            const double o0 = fma(p.alpha, v0, p.beta * c0);
-            const double o1 = fma(p.alpha, v1, p.beta * c1);
-            if (pair && p.vec) {
+            // rows/cols outside D contribute nothing to the checksums
+            o0 = (rv0 && cvld) ? o0 : 0.0;
+            o1 = (rv1 && cvld) ? o1 : 0.0;
+            acc[2 * rp][cf][tt] = o0;
+            acc[2 * rp + 1][cf][tt] = o1;
+            if (!rv0 || !cvld) continue;
+            double* d = D + row + (int64_t)col * p.ldd;
+            if (rv1 && p.vec && !p.partial) {
               *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
             } else {
               d[0] = o0;
-              if (pair) d[1] = o1;
+              if (rv1) d[1] = o1;
             }
           }
       }
+      // Pass 2 (fused checksums) from the output registers.
+      if (p.fuse) {
+#pragma unroll
+        for (int rp = 0; rp < 4; ++rp) {
+          double rs0 = 0.0, rs1 = 0.0;
+#pragma unroll
+          for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+            for (int tt = 0; tt < 2; ++tt) {
+              rs0 += acc[2 * rp][cf][tt];
+              rs1 += acc[2 * rp + 1][cf][tt];
+              mx = fmax(mx, fmax(fabs(acc[2 * rp][cf][tt]), fabs(acc[2 * rp + 1][cf][tt])));
+            }
+          // row sums over this warp's 32 columns: reduce the 4 j-lanes
+          rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
+          rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
+          rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
+          rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
+          if (j == 0) {
+            const int r = tm * BM + wm + 16 * rp + 2 * g;
+            rowacc[(wn >> 5) * MAXFB + r] += rs0;
+            rowacc[(wn >> 5) * MAXFB + r + 1] += rs1;
+          }
+        }
+        // column plain / index-weighted sums over this warp's 64 rows
+        const double wbase = (double)(tm * BM + wm + 2 * g);
+#pragma unroll
+        for (int cf = 0; cf < 4; ++cf)
+#pragma unroll
+          for (int tt = 0; tt < 2; ++tt) {
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int rp = 0; rp < 4; ++rp) {
+              const double x0 = acc[2 * rp][cf][tt], x1 = acc[2 * rp + 1][cf][tt];
+              const double w0 = wbase + 16.0 * rp;
+              a0 += x0 + x1;
+              a1 += w0 * x0 + (w0 + 1.0) * x1;
+            }
+#pragma unroll
+            for (int o = 4; o < 32; o <<= 1) {
+              a0 += __shfl_xor_sync(0xffffffffu, a0, o);
+              a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+            }
+            if (g == 0) {
+              const int c = tn * BN + wn + col_of<BT>(cf, 2 * j + tt);
+              colacc[((wm >> 6) * MAXFB + c) * 2 + 0] += a0;
+              colacc[((wm >> 6) * MAXFB + c) * 2 + 1] += a1;
+            }
+          }
+      }
+    }
+    if (p.fuse) {
+      // block finished: combine the halves in a fixed order and publish
+      mx = warp_max(mx);
+      if (lane == 0) wmax[wi] = mx;
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
+      const int tid = threadIdx.x & 127;
+      const int rows_b = min(p.fb, p.M - bi * p.fb);
+      const int cols_b = min(p.fb, p.N - bj * p.fb);
+      const FusedSums& fs = p.sums;
+      for (int c = tid; c < cols_b; c += 128) {
+        const int64_t gc = (int64_t)bj * p.fb + c;
+        fs.cp[fs.cp_step * bi + gc * fs.cp_ld] = colacc[c * 2 + 0] + colacc[(MAXFB + c) * 2 + 0];
+        fs.cw[fs.cw_step * bi + gc * fs.cw_ld] = colacc[c * 2 + 1] + colacc[(MAXFB + c) * 2 + 1];
+      }
+      for (int r = tid; r < rows_b; r += 128)
+        fs.rp[(int64_t)bi * p.fb + r + (int64_t)bj * fs.rp_ld] = rowacc[r] + rowacc[MAXFB + r];
+      if (tid == 0)
+        fs.bm[bi + (int64_t)bj * fs.bm_ld] =
+            fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
+      for (int k2 = tid; k2 < SUM_DOUBLES; k2 += 128) colacc[k2] = 0.0;
+      asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
     }
   }
 }
@@ -408,7 +518,7 @@ int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const int total = kp.tiles_m * kp.tiles_n * kp.splits;
+  const int total = kp.fuse ? kp.nbr_b * kp.nbc_b : kp.tiles_m * kp.tiles_n * kp.splits;
   const int grid = total < sms ? total : sms;
   count_launch();
   dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, mc, kp);
@@ -428,9 +538,10 @@ int gemm_splits_for(int M, int N, int K, int num_sms) {
   return s < 1 ? 1 : s;
 }
 
-int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, const double* A,
-         int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
-         double* D, int64_t ldd, GemmWorkspace* ws, int splits) {
+static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                     const double* C, int64_t ldc, double* D, int64_t ldd, GemmWorkspace* ws,
+                     int splits, const FusedSums* fs, int fb) {
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0) {
     // D = beta*C (alpha*0)
@@ -453,6 +564,7 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
   else
     ABFT_TRY(make_tma_map(&mb, B, ldb, K, N, BK, BN, true, &shb));
 
+  if (fs) splits = 1;
   if (splits <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -491,6 +603,18 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
   kp.tiles_m = (M + BM - 1) / BM;
   kp.tiles_n = (N + BN - 1) / BN;
   kp.splits = splits;
+  kp.fuse = 0;
+  kp.fb = 0;
+  kp.ntm_b = kp.ntn_b = kp.nbr_b = kp.nbc_b = 0;
+  if (fs) {
+    kp.fuse = 1;
+    kp.fb = fb;
+    kp.ntm_b = fb / BM;
+    kp.ntn_b = fb / BN;
+    kp.nbr_b = (M + fb - 1) / fb;
+    kp.nbc_b = (N + fb - 1) / fb;
+    kp.sums = *fs;
+  }
   if (splits > 1) {
     kp.C = nullptr;
     kp.ldc = 0;
@@ -540,6 +664,31 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
     CUDA_TRY(cudaGetLastError());
   }
   return 0;
+}
+
+int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, const double* A,
+         int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
+         double* D, int64_t ldd, GemmWorkspace* ws, int splits) {
+  return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, ws, splits,
+                   nullptr, 0);
+}
+
+bool gemm_can_fuse(int fb) { return fb == 128 || fb == 256; }
+
+int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                    const double* C, int64_t ldc, double* D, int64_t ldd, int fb,
+                    const FusedSums& sums) {
+  if (!gemm_can_fuse(fb)) {
+    set_last_error("fused checksums need b = 128 or 256 (got %d)", fb);
+    return -1;
+  }
+  if (K <= 0) {
+    set_last_error("fused checksums need K > 0");
+    return -1;
+  }
+  return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, nullptr, 1,
+                   &sums, fb);
 }
 
 }  // namespace abft

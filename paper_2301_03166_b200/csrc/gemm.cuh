@@ -3,6 +3,21 @@
 
 namespace abft {
 
+// Checksum outputs of the fused epilogue for an fb x fb block grid over D:
+// col plain cp[cp_step*bi + col*cp_ld], col weighted cw[...], row plain
+// rp[row + bj*rp_ld], block max bm[bi + bj*bm_ld] (all block-local indexing
+// relative to D's origin).
+struct FusedSums {
+  double* cp = nullptr;
+  int64_t cp_ld = 0, cp_step = 1;
+  double* cw = nullptr;
+  int64_t cw_ld = 0, cw_step = 1;
+  double* rp = nullptr;
+  int64_t rp_ld = 0;
+  double* bm = nullptr;
+  int64_t bm_ld = 0;
+};
+
 struct GemmWorkspace {
   double* ptr = nullptr;
   int64_t elems = 0;
@@ -16,5 +31,14 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
          double* D, int64_t ldd, GemmWorkspace* ws, int splits = 0);
 
 int gemm_splits_for(int M, int N, int K, int num_sms);
+
+// As gemm() (no split-K) but the epilogue also produces the per-block
+// checksums of D on an fb x fb grid (fb = 128 or 256): the verify-side read
+// of encode/verify_correct without a separate pass over D.
+int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                    const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                    const double* C, int64_t ldc, double* D, int64_t ldd, int fb,
+                    const FusedSums& sums);
+bool gemm_can_fuse(int fb);
 
 }  // namespace abft

@@ -25,7 +25,8 @@ namespace {
 constexpr int DT = 512;   // threads of the diagonal kernel
 constexpr int NBK = 32;   // sub-panel width
 constexpr int PLD = 257;  // smem leading dim of the staged sub-panel (w <= 256)
-constexpr int DIAG_SMEM = 2 * 256 * 33 * 8 + 64;  // max over the phases
+constexpr int DIAG_SMEM = (NBK * PLD + 224 * 33) * 8 + 64;
+constexpr int INV_SMEM = (256 * 33 + 32 * 257) * 8;
 
 // Accessor for a (possibly transposed) column-major matrix.
 struct Acc {
@@ -34,44 +35,6 @@ struct Acc {
   bool t;
   ABFT_DEVINL double& at(int r, int c) const { return t ? p[c + r * ld] : p[r + c * ld]; }
 };
-
-// X = L^{-1} for the w x w lower-triangular L (unit or not), X written through
-// `X` (lower part + explicit zeros above). Block-row sweep with 32-row blocks.
-ABFT_DEVINL void lower_inverse(const Acc& L, const Acc& X, int w, bool unit, double* smem) {
-  double* Ls = smem;             // [256][33]: Ls[l*33 + r] = L(r0 + r, l)
-  double* Ts = smem + 256 * 33;  // [256][33]: Ts[c*33 + r]
-  const int tid = threadIdx.x;
-  for (int r0 = 0; r0 < w; r0 += NBK) {
-    const int rh = min(NBK, w - r0);
-    const int ncol = r0 + rh;
-    for (int idx = tid; idx < rh * ncol; idx += DT) {
-      const int r = idx % rh, l = idx / rh;
-      Ls[l * 33 + r] = (l <= r0 + r) ? L.at(r0 + r, l) : 0.0;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < rh * ncol; idx += DT) {
-      const int r = idx % rh, c = idx / rh;
-      double acc = (r0 + r == c) ? 1.0 : 0.0;
-      for (int l = c; l < r0; ++l) acc -= Ls[l * 33 + r] * X.at(l, c);
-      Ts[c * 33 + r] = acc;
-    }
-    __syncthreads();
-    for (int c = tid; c < ncol; c += DT) {
-      for (int r = 0; r < rh; ++r) {
-        double x = Ts[c * 33 + r];
-        for (int l = 0; l < r; ++l) x -= Ls[(r0 + l) * 33 + r] * Ts[c * 33 + l];
-        if (!unit) x /= Ls[(r0 + r) * 33 + r];
-        Ts[c * 33 + r] = x;
-      }
-    }
-    __syncthreads();
-    for (int idx = tid; idx < rh * w; idx += DT) {
-      const int r = idx % rh, c = idx / rh;
-      X.at(r0 + r, c) = (c < ncol) ? Ts[c * 33 + r] : 0.0;
-    }
-    __syncthreads();
-  }
-}
 
 // mode 0: LU without pivoting (L unit lower \ U upper in place),
 //         Linv = L^{-1}, Uinv = U^{-1}.
@@ -182,10 +145,68 @@ __global__ void __launch_bounds__(DT, 1)
       if (r < c) D[r + (int64_t)c * ld] = 0.0;
     }
   }
-  __syncthreads();
-  // ---- inverses ----
-  if (Linv) lower_inverse(Acc{D, ld, false}, Acc{Linv, ldl, false}, w, mode == 0, sm);
-  if (Uinv) lower_inverse(Acc{D, ld, true}, Acc{Uinv, ldu, true}, w, false, sm);
+}
+
+// Triangular inverses, one CTA per 32-column block of the result:
+// blockIdx.y = 0: X = L^{-1} (unit lower for LU, non-unit for Cholesky),
+// blockIdx.y = 1: X = U^{-1}, computed as ((U^T)^{-1})^T through transposed
+// accessors. Column block jb of X solves L X[:, jb] = E[:, jb] by block
+// forward substitution; the X column block and the L row-slab of each step
+// are staged in shared memory (no dependent global loads).
+__global__ void __launch_bounds__(DT)
+    tri_inverse_kernel(const double* D, int64_t ld, int w, int unit_l, double* Linv,
+                       int64_t ldl, double* Uinv, int64_t ldu, const int* info) {
+  extern __shared__ double sm[];
+  if (*info != 0) return;  // factorization broke down: nothing to invert
+  const bool upper = blockIdx.y == 1;
+  if (upper && !Uinv) return;
+  const Acc L{const_cast<double*>(D), ld, upper};
+  const Acc X{upper ? Uinv : Linv, upper ? ldu : ldl, upper};
+  const bool unit = upper ? false : (unit_l != 0);
+  const int jb = blockIdx.x;
+  const int c0 = jb * NBK;
+  if (c0 >= w) return;
+  const int cw = min(NBK, w - c0);
+  double* Xs = sm;                // [w][33]: Xs[r*33 + c] = X(r, c0 + c), rows r >= c0
+  double* Ls = sm + 256 * 33;     // [32][w+1]: Ls[r*257 + l] = L(r0 + r, l)
+  const int tid = threadIdx.x;
+  // rows above the diagonal block are zero
+  for (int idx = tid; idx < c0 * cw; idx += DT) {
+    const int r = idx / cw, c = idx % cw;
+    X.at(r, c0 + c) = 0.0;
+  }
+  for (int r0 = c0; r0 < w; r0 += NBK) {
+    const int rh = min(NBK, w - r0);
+    // stage L(r0.., c0 .. r0+rh)
+    const int lw = r0 + rh - c0;
+    for (int idx = tid; idx < rh * lw; idx += DT) {
+      const int r = idx % rh, l = c0 + idx / rh;
+      Ls[r * 257 + l - c0] = (l <= r0 + r) ? L.at(r0 + r, l) : 0.0;
+    }
+    __syncthreads();
+    // T = E - L(r0.., c0..r0) X(c0..r0, :)
+    for (int idx = tid; idx < rh * cw; idx += DT) {
+      const int r = idx / cw, c = idx % cw;
+      double acc = (r0 + r == c0 + c) ? 1.0 : 0.0;
+      for (int l = c0; l < r0; ++l) acc -= Ls[r * 257 + (l - c0)] * Xs[(l - c0) * 33 + c];
+      Xs[(r0 - c0 + r) * 33 + c] = acc;
+    }
+    __syncthreads();
+    // solve L(r0.., r0..) X(r0.., :) = T, one thread per column
+    for (int c = tid; c < cw; c += DT) {
+      for (int r = 0; r < rh; ++r) {
+        double x = Xs[(r0 - c0 + r) * 33 + c];
+        for (int l = 0; l < r; ++l) x -= Ls[r * 257 + (r0 + l - c0)] * Xs[(r0 - c0 + l) * 33 + c];
+        if (!unit) x /= Ls[r * 257 + (r0 + r - c0)];
+        Xs[(r0 - c0 + r) * 33 + c] = x;
+      }
+    }
+    __syncthreads();
+  }
+  for (int idx = tid; idx < (w - c0) * cw; idx += DT) {
+    const int r = c0 + idx / cw, c = idx % cw;
+    X.at(r, c0 + c) = Xs[(r - c0) * 33 + c];
+  }
 }
 
 }  // namespace
@@ -207,6 +228,19 @@ int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double*
   diag_factor_kernel<<<1, DT, DIAG_SMEM, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
                                                 col_base);
   CUDA_TRY(cudaGetLastError());
+  if (Linv || Uinv) {
+    static bool attr2 = false;
+    if (!attr2) {
+      CUDA_TRY(cudaFuncSetAttribute(tri_inverse_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, INV_SMEM));
+      attr2 = true;
+    }
+    dim3 grid((w + NBK - 1) / NBK, Uinv ? 2 : 1);
+    count_launch();
+    tri_inverse_kernel<<<grid, DT, INV_SMEM, st>>>(D, ld, w, mode == 0 ? 1 : 0, Linv, ldl, Uinv,
+                                                   ldu, info_dev);
+    CUDA_TRY(cudaGetLastError());
+  }
   return 0;
 }
 

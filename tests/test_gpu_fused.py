@@ -1,0 +1,77 @@
+"""GPU: the fused-checksum GEMM epilogue (b = 128 / 256, LU and QR) gives the
+same detection / correction as the CPU oracle and as the unfused path."""
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2301_03166_b200 as P
+from conftest import report_json
+
+pytestmark = pytest.mark.gpu
+
+COUNTS = {"0d": 2, "1d": 1, "2d": 1}
+
+
+def run_gpu(kind, n, b, seed, scheme, fault_iters, no_fuse=False):
+    old = os.environ.get("ABFT_NO_FUSE")
+    os.environ["ABFT_NO_FUSE"] = "1" if no_fuse else "0"
+    try:
+        a = P.generate_test_matrix(kind, n, seed)
+        f = P.Factorization(kind, a, b)
+    finally:
+        if old is None:
+            os.environ.pop("ABFT_NO_FUSE")
+        else:
+            os.environ["ABFT_NO_FUSE"] = old
+    rng = np.random.default_rng(seed)
+    reps = [report_json(P.run_numeric_iteration(f, k, scheme,
+                                                COUNTS if k in fault_iters else None, rng))
+            for k in range(f.layout.n_blocks)]
+    return reps, P.residual(a, f), f
+
+
+def run_oracle(kind, n, b, seed, scheme, fault_iters):
+    a = O.generate_test_matrix(kind, n, seed)
+    f = O.OracleFactorization(kind, a, b)
+    rng = np.random.default_rng(seed)
+    reps = [O.protected_iteration(f, k, scheme, COUNTS if k in fault_iters else None, rng).to_json()
+            for k in range(f.nb)]
+    return reps, O.residual(a, f)
+
+
+@pytest.mark.parametrize("kind", ["lu", "qr"])
+@pytest.mark.parametrize("n,b", [(1024, 128), (1000, 128), (1536, 256), (1300, 256)])
+@pytest.mark.parametrize("scheme", ["single", "full"])
+def test_fused_matches_oracle(kind, n, b, scheme):
+    fault_iters = {1, (-(-n // b)) - 2}
+    got, res, _ = run_gpu(kind, n, b, 11, scheme, fault_iters)
+    want, res_o = run_oracle(kind, n, b, 11, scheme, fault_iters)
+    assert got == want
+    if res_o <= 1e-8:
+        assert res <= res_o + 16 * n * 2.220446049250313e-16
+    else:
+        assert res == pytest.approx(res_o, rel=1e-3)
+
+
+@pytest.mark.parametrize("kind", ["lu", "qr"])
+def test_fused_equals_unfused(kind):
+    n, b = 1792, 256
+    r1, res1, f1 = run_gpu(kind, n, b, 5, "full", {2})
+    r2, res2, f2 = run_gpu(kind, n, b, 5, "full", {2}, no_fuse=True)
+    assert r1 == r2
+    np.testing.assert_allclose(f1.m, f2.m, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind", ["lu", "qr", "cholesky"])
+def test_clean_large_run_has_no_false_positives(kind):
+    """N = 4096, b = 256, no faults: no detections (SURVEY probe #5)."""
+    n, b = 4096, 256
+    a = P.generate_test_matrix("lu" if kind == "cholesky" else kind, n, 3)
+    if kind == "cholesky":
+        a = a @ a.T + n * np.eye(n)
+    f = P.Factorization(kind, np.asfortranarray(a), b)
+    reps = P.run_protected(f, "full", {}, np.random.default_rng(0))
+    assert all(r.clean for r in reps)
+    assert P.residual(a, f) < 64 * n * 2.220446049250313e-16
