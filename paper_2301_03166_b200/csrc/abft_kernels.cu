@@ -129,11 +129,11 @@ ABFT_DEVINL void emit(const EventSink& s, int bi, int bj, int seq, int kind, int
   if (slot < s.capacity) {
     Event e;
     e.bi = bi;
-    e.bj = bj;
+    e.bj = bj + s.bj_base;
     e.seq = seq;
     e.kind = kind;
     e.row = row;
-    e.col = col;
+    e.col = col + (int64_t)s.bj_base * s.b;
     e.flag = flag;
     e.detected_kind = det;
     e.corrected = corr;

@@ -64,6 +64,8 @@ struct EventSink {
   int32_t* dirty_count;
   int32_t dirty_capacity;
   int32_t iter;
+  int32_t bj_base = 0;  // block-column offset of a sub-region (event coordinates only)
+  int64_t b = 0;        // block size, for the column offset bj_base * b
 };
 
 // K2: threshold, classify and repair (verify_correct + _handle_single/_full,

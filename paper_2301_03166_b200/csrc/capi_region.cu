@@ -211,7 +211,7 @@ ABFT_API int abft_region_verify(double* m, int64_t ldm, int64_t rows, int64_t co
   CUDA_TRY(cudaMalloc(&ev, cap * sizeof(Event)));
   CUDA_TRY(cudaMalloc(&cnt, 2 * sizeof(int32_t)));
   CUDA_TRY(cudaMemset(cnt, 0, 2 * sizeof(int32_t)));
-  EventSink sink{ev, cnt, cap, nullptr, nullptr, 0, 0};
+  EventSink sink{ev, cnt, cap, nullptr, nullptr, 0, 0, 0, b};
   int rc = verify_blocks(nullptr, reg, b, scheme, correct, rec, mt, sink);
   int32_t h = 0;
   std::vector<Event> evs;

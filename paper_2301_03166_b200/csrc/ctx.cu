@@ -99,7 +99,11 @@ struct abft_ctx {
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool timed = false;
   int32_t cur_iter = 0;
-  bool fuse_enabled = true;  // ABFT_NO_FUSE=1 disables (A/B testing)
+  bool fuse_enabled = true;       // ABFT_NO_FUSE=1 disables (A/B testing)
+  bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
+  int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
+  cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // profiling
   struct ProfPair {
     int cat;
@@ -237,17 +241,28 @@ int check_info(abft_ctx* c) {
 // ---------------------------------------------------------------------------
 // tasks (linalg.py:192-258)
 // ---------------------------------------------------------------------------
+// LU panel, part 1: factor the diagonal block and form L11^{-1}, U11^{-1}.
+int lu_diag(abft_ctx* c, cudaStream_t st, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  return diag_factor(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv,
+                     c->ld_t, c->info, p);
+}
+
+// LU panel, part 2: L21 = A21 U11^{-1} (GEMM over all SMs).
+int lu_l21(abft_ctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (pe >= n) return 0;
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld, c->ld,
+                c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
+  return copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w);
+}
+
 int task_pd(abft_ctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   double* D = c->m + p + p * c->ld;
   if (c->kind == ABFT_LU) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info, p));
-    if (pe < n) {
-      // L21 = A21 U11^{-1}
-      ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld,
-                    c->ld, c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
-      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w));
-    }
+    ABFT_TRY(lu_diag(c, c->st, k));
+    ABFT_TRY(lu_l21(c, k));
   } else if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
@@ -582,6 +597,104 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   return 0;
 }
 
+// Verify (and refresh after repairs) the block columns [j0, j0 + ncb) of the
+// region of iteration k — a block-aligned sub-region with its own event
+// offsets, so the LU look-ahead can release the next panel early.
+int verify_sub(abft_ctx* c, int scheme, int correct, int64_t r0, int64_t c0, int64_t rows,
+               int64_t cols, int64_t j0, int64_t ncb) {
+  const int64_t cbeg = j0 * c->b;
+  const int64_t csub = std::min(cols - cbeg, ncb * c->b);
+  if (csub <= 0 || rows <= 0) return 0;
+  Region sub{c->m + r0 + (c0 + cbeg) * c->ld, c->ld, rows, csub, c->b};
+  SumOut rec = sums_for(c, r0, c0 + cbeg, true);
+  Maintained mt;
+  mt.cp = c->csm + cbeg * c->ld_cs;
+  mt.cp_ld = c->ld_cs;
+  mt.cp_step = 2;
+  mt.cw = mt.cp + 1;
+  mt.cw_ld = c->ld_cs;
+  mt.cw_step = 2;
+  mt.rp = c->rsm + j0 * c->ld;
+  mt.rp_ld = c->ld;
+  EventSink sink{c->ev,          c->counters,    c->ev_cap,  c->dirty,
+                 c->counters + 1, c->dirty_cap,  c->cur_iter, (int32_t)j0, c->b};
+  ABFT_TRY(verify_blocks(c->st, sub, c->b, scheme, correct, rec, mt, sink));
+  ABFT_TRY(blocksum(c->st, sub, rec, c->dirty, c->counters + 1, c->dirty_cap));
+  CUDA_TRY(cudaMemsetAsync(c->counters + 1, 0, sizeof(int32_t), c->st));
+  return 0;
+}
+
+// LU protected trailing update with look-ahead (fault-free iterations of the
+// one-call path): the next panel's block column is updated and verified
+// first, then its diagonal block is factored on a side stream (2 SMs left
+// free by the persistent GEMM) while the rest of the trailing matrix updates.
+// Same operations and ordering constraints as _protected_tmu
+// (simulator.py:124-167); only independent work overlaps.
+int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  Region reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  const bool prot = scheme != ABFT_NONE;
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    if (!c->sums_valid) ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
+    ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  const double* L21 = c->m + pe + p * c->ld;
+  const double* U12 = c->m + p + pe * c->ld;
+  double* A22 = c->m + pe + pe * c->ld;
+  const int64_t wa = std::min<int64_t>(c->b, cols);
+  // (a) next panel's block column, plain tiles over all SMs + checksum pass
+  prof_mark(c, PROF_TMU, true);
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, L21, c->ld, U12, c->ld, 1.0, A22,
+                c->ld, A22, c->ld, &c->gws));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    Region ra{A22, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, c0, true)));
+    ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  // side stream: diagonal block of panel k+1
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  ABFT_TRY(lu_diag(c, c->st2, k + 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  // (b) the rest of the trailing matrix with fused checksums
+  if (cols > wa) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    prof_mark(c, PROF_TMU, true);
+    if (prot) {
+      FusedSums fs = fused_for(c, r0, c0 + wa);
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
+                               c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
+                               A22 + wa * c->ld, c->ld, (int)c->b, fs, sms - 2));
+    } else {
+      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
+                             c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
+                             A22 + wa * c->ld, c->ld, sms - 2));
+    }
+    prof_mark(c, PROF_TMU, false);
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 1, (cols + c->b - 1) / c->b));
+      prof_mark(c, PROF_ABFT, false);
+    }
+  }
+  c->sums_valid = prot;
+  // join, then L21 of panel k+1 on the main stream
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  prof_mark(c, PROF_PD, true);
+  ABFT_TRY(lu_l21(c, k + 1));
+  prof_mark(c, PROF_PD, false);
+  c->pd_ready = k + 1;
+  return 0;
+}
+
 // Per-task device timers (CUDA events on the context stream), enabled by
 // abft_profile(ctx, 1): PD, PU, TMU GEMM(s) and the ABFT work around them.
 
@@ -589,8 +702,12 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
 // breakdown flag right after PD (per-iteration API); otherwise it is checked
 // once at the end of abft_factorize.
 int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
-                         int correct, bool sync_checks) {
+                         int correct, bool sync_checks, bool lookahead = false) {
   auto pd = [&]() -> int {
+    if (c->pd_ready == k) {  // produced by the previous iteration's look-ahead
+      c->pd_ready = -1;
+      return 0;
+    }
     prof_mark(c, PROF_PD, true);
     ABFT_TRY(task_pd(c, k));
     prof_mark(c, PROF_PD, false);
@@ -610,7 +727,13 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
   } else if (c->kind == ABFT_LU) {
     ABFT_TRY(pd());
     ABFT_TRY(pu());
-    ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+    const int64_t pe = std::min((k + 1) * c->b, c->n);
+    const bool la = lookahead && nplan == 0 && pe < c->n && c->fuse_enabled &&
+                    gemm_can_fuse((int)c->b);
+    if (la)
+      ABFT_TRY(protected_tmu_lu_lookahead(c, k, scheme, correct));
+    else
+      ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
   } else {
     ABFT_TRY(pd());
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
@@ -717,6 +840,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   {
     const char* e = getenv("ABFT_NO_FUSE");
     c->fuse_enabled = !(e && e[0] == '1');
+    const char* e2 = getenv("ABFT_NO_LOOKAHEAD");
+    c->lookahead_enabled = !(e2 && e2[0] == '1');
   }
   int rc = 0;
   auto fail = [&](int r) {
@@ -767,6 +892,9 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   cudaMemset(c->info, 0, sizeof(int));
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
+  cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
   *out = c;
   return 0;
@@ -795,6 +923,12 @@ ABFT_API int abft_destroy(abft_ctx* c) {
     cudaEventDestroy(pe.e1);
   }
   for (auto e : c->prof_free) cudaEventDestroy(e);
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamDestroy(c->st2);
+  }
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_p) cudaEventDestroy(c->ev_p);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->st) cudaStreamDestroy(c->st);
@@ -820,6 +954,7 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->sums_valid = false;
   c->qr_count = 0;
   c->breakdown_col = -1;
+  c->pd_ready = -1;
   return 0;
 }
 
@@ -837,6 +972,7 @@ ABFT_API int abft_reset(abft_ctx* c) {
   c->sums_valid = false;
   c->qr_count = 0;
   c->breakdown_col = -1;
+  c->pd_ready = -1;
   return 0;
 }
 
@@ -944,7 +1080,8 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
       while (f1 < nplan && plan_iter[f1] == k) ++f1;
     }
     c->cur_iter = (int32_t)k;
-    int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false);
+    int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false,
+                                  c->lookahead_enabled);
     if (rc != 0) {
       cudaEventRecord(c->e1, c->st);
       return rc;
@@ -1088,6 +1225,7 @@ ABFT_API int abft_restore(abft_ctx* c, int slot) {
   c->k_done = s.k_done;
   c->qr_count = s.qr_count;
   c->sums_valid = false;
+  c->pd_ready = -1;
   CUDA_TRY(cudaStreamSynchronize(c->st));
   return 0;
 }

@@ -507,7 +507,7 @@ __global__ void splitk_reduce(int M, int N, int splits, const double* __restrict
 
 template <bool AT, bool BT>
 int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
-                  const CUtensorMap& mc, const KParams& kp,
+                  const CUtensorMap& mc, const KParams& kp, int max_ctas,
                   int splits) {
   static bool attr_set = false;
   if (!attr_set) {
@@ -519,7 +519,8 @@ int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int total = kp.fuse ? kp.nbr_b * kp.nbc_b : kp.tiles_m * kp.tiles_n * kp.splits;
-  const int grid = total < sms ? total : sms;
+  const int cap = (max_ctas > 0 && max_ctas < sms) ? max_ctas : sms;
+  const int grid = total < cap ? total : cap;
   count_launch();
   dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, mc, kp);
   CUDA_TRY(cudaGetLastError());
@@ -541,7 +542,7 @@ int gemm_splits_for(int M, int N, int K, int num_sms) {
 static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                      const double* C, int64_t ldc, double* D, int64_t ldd, GemmWorkspace* ws,
-                     int splits, const FusedSums* fs, int fb) {
+                     int splits, const FusedSums* fs, int fb, int max_ctas) {
   if (M <= 0 || N <= 0) return 0;
   if (K <= 0) {
     // D = beta*C (alpha*0)
@@ -647,13 +648,13 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
   }
   int rc;
   if (AT && BT)
-    rc = launch_kernel<true, true>(st, ma, mb, mc, kp, splits);
+    rc = launch_kernel<true, true>(st, ma, mb, mc, kp, max_ctas, splits);
   else if (AT)
-    rc = launch_kernel<true, false>(st, ma, mb, mc, kp, splits);
+    rc = launch_kernel<true, false>(st, ma, mb, mc, kp, max_ctas, splits);
   else if (BT)
-    rc = launch_kernel<false, true>(st, ma, mb, mc, kp, splits);
+    rc = launch_kernel<false, true>(st, ma, mb, mc, kp, max_ctas, splits);
   else
-    rc = launch_kernel<false, false>(st, ma, mb, mc, kp, splits);
+    rc = launch_kernel<false, false>(st, ma, mb, mc, kp, max_ctas, splits);
   if (rc) return rc;
   if (splits > 1) {
     int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
@@ -670,15 +671,22 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
          int64_t lda, const double* B, int64_t ldb, double beta, const double* C, int64_t ldc,
          double* D, int64_t ldd, GemmWorkspace* ws, int splits) {
   return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, ws, splits,
-                   nullptr, 0);
+                   nullptr, 0, 0);
 }
 
 bool gemm_can_fuse(int fb) { return fb == 128 || fb == 256; }
 
+int gemm_reserved(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                  const double* C, int64_t ldc, double* D, int64_t ldd, int max_ctas) {
+  return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, nullptr, 1,
+                   nullptr, 0, max_ctas);
+}
+
 int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                     const double* C, int64_t ldc, double* D, int64_t ldd, int fb,
-                    const FusedSums& sums) {
+                    const FusedSums& sums, int max_ctas) {
   if (!gemm_can_fuse(fb)) {
     set_last_error("fused checksums need b = 128 or 256 (got %d)", fb);
     return -1;
@@ -688,7 +696,7 @@ int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, doub
     return -1;
   }
   return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, nullptr, 1,
-                   &sums, fb);
+                   &sums, fb, max_ctas);
 }
 
 }  // namespace abft

@@ -38,7 +38,13 @@ int gemm_splits_for(int M, int N, int K, int num_sms);
 int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
                     const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                     const double* C, int64_t ldc, double* D, int64_t ldd, int fb,
-                    const FusedSums& sums);
+                    const FusedSums& sums, int max_ctas = 0);
 bool gemm_can_fuse(int fb);
+
+// gemm() without split-K on at most max_ctas SMs (leaves SMs for a concurrent
+// side-stream kernel).
+int gemm_reserved(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                  const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                  const double* C, int64_t ldc, double* D, int64_t ldd, int max_ctas);
 
 }  // namespace abft

@@ -75,3 +75,25 @@ def test_clean_large_run_has_no_false_positives(kind):
     reps = P.run_protected(f, "full", {}, np.random.default_rng(0))
     assert all(r.clean for r in reps)
     assert P.residual(a, f) < 64 * n * 2.220446049250313e-16
+
+
+@pytest.mark.parametrize("n,b", [(2048, 256), (1408, 128), (1300, 256)])
+def test_lookahead_fast_path_equals_per_iteration(n, b):
+    """abft_factorize's LU look-ahead (next panel factored on a side stream
+    while the rest of the trailing matrix updates) gives the same reports as
+    run_numeric_iteration, faults at two iterations (those run serialised)."""
+    kind = "lu"
+    nb = -(-n // b)
+    sched = {1: {P.ErrorKind.D0: 2, P.ErrorKind.D1: 1}, nb - 2: {P.ErrorKind.D0: 1}}
+    a = P.generate_test_matrix(kind, n, 9)
+    f1 = P.Factorization(kind, a, b)
+    rng = np.random.default_rng(9)
+    per = [report_json(P.run_numeric_iteration(f1, k, "full", sched.get(k), rng)) for k in range(nb)]
+    f2 = P.Factorization(kind, a, b)
+    fast = [report_json(r) for r in P.run_protected(f2, "full", sched, np.random.default_rng(9))]
+    assert per == fast
+    np.testing.assert_allclose(f2.m, f1.m, rtol=0, atol=1e-12)
+    r1, r2 = P.residual(a, f1), P.residual(a, f2)
+    assert r2 == pytest.approx(r1, rel=1e-6, abs=1e-15)
+    if not any(r["uncorrectable"] for r in per):
+        assert r2 < 1e-14
