@@ -72,6 +72,8 @@ struct abft_ctx {
   double* qr_part = nullptr;
   int64_t qr_part_elems = 0;
   double* qr_rowbuf = nullptr;
+  double* qr_part2 = nullptr;  // 148 x 32 x b block-update partials
+  double* qr_wfin = nullptr;   // 32 x b
   double* gram = nullptr;    // b x b
   double* ww = nullptr;      // b x n
   double* mid = nullptr;     // b x n
@@ -268,7 +270,7 @@ int task_pd(abft_ctx* c, int64_t k) {
   } else {
     double* V = c->vstore + p + p * c->ld;
     ABFT_TRY(qr_panel(c->st, D, c->ld, n - p, (int)w, V, c->ld, c->betas, c->qr_part,
-                      c->qr_part_elems, c->qr_rowbuf));
+                      c->qr_part_elems, c->qr_rowbuf, c->qr_part2, c->qr_wfin));
     ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)w, (int)(n - p), 1.0, V, c->ld, V, c->ld, 0.0,
                   nullptr, 0, c->gram, c->ld_t, &c->gws));
     ABFT_TRY(larft(c->st, c->gram, c->ld_t, c->betas, (int)w, c->tstore + k * c->b * c->ld_t,
@@ -874,7 +876,9 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     if ((rc = dalloc(&c->betas, b))) return fail(rc);
     c->qr_part_elems = 2 * 160 * (b + 1);
     if ((rc = dalloc(&c->qr_part, c->qr_part_elems))) return fail(rc);
-    if ((rc = dalloc(&c->qr_rowbuf, 2 * (b + 1)))) return fail(rc);
+    if ((rc = dalloc(&c->qr_rowbuf, 2 * (b + 1) + 128))) return fail(rc);
+    if ((rc = dalloc(&c->qr_part2, 160LL * 32 * b))) return fail(rc);
+    if ((rc = dalloc(&c->qr_wfin, 32LL * b))) return fail(rc);
     if ((rc = dalloc(&c->gram, c->ld_t * b))) return fail(rc);
     if ((rc = dalloc(&c->ww, c->ld_t * n_))) return fail(rc);
     if ((rc = dalloc(&c->mid, c->ld_t * n_))) return fail(rc);
@@ -907,6 +911,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   double* bufs[] = {c->m,     c->a0,     c->gcsw,   c->grs,     c->gmax,  c->csm,  c->rsm,
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
+                    c->qr_part2, c->qr_wfin,
                     c->scratch, c->gws.ptr};
   for (double* p : bufs)
     if (p) cudaFree(p);

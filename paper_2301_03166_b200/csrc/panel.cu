@@ -403,11 +403,264 @@ __global__ void __launch_bounds__(512)
   }
 }
 
+
+// Householder panel v2: 32-column sub-panels resident in shared memory.
+// Every CTA owns a slab of <= QR_RMAX panel rows; for each sub-panel it keeps
+// the slab of P and V in shared memory, and each column costs ONE grid-wide
+// reduction of <= 32 values: the norm^2 of x[1:], the dots x[1:] . P[1:, c]
+// with the remaining sub-panel columns, and the dots V[1:, l] . x[1:] with the
+// sub-panel's previous reflectors (for its T). After the sub-panel, the
+// remaining panel columns receive the block reflector I - V_s T_s V_s^T
+// (two more grid syncs: reduce-scatter of V_s^T C, then gather).
+constexpr int QR_RMAX = 256;   // max rows per CTA
+constexpr int QR_RS = QR_RMAX + 1;
+constexpr int QR_SMEM = (3 * 32 * QR_RS + 32 * 33 + 4 * 32) * 8;
+
+__global__ void __launch_bounds__(QT, 1)
+    qr_panel2_kernel(double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
+                     double* betas, double* part, double* rowbuf, double* part2, double* wfin) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double qs[];
+  double* Ps = qs;                  // [32][QR_RS]  sub-panel slab, Ps[c*QR_RS + i]
+  double* Vs = Ps + 32 * QR_RS;     // [32][QR_RS]
+  double* Ws = Vs + 32 * QR_RS;     // [32][QR_RS]  W' = T_s^T V_s^T C, Ws[l*QR_RS + c]
+  double* Ts = Ws + 32 * QR_RS;     // [32][33]     T_s (upper)
+  double* red = Ts + 32 * 33;       // [32] reduced values
+  double* rowj = red + 32;          // [32] row j of the sub-panel
+  double* vrow = rowj + 32;         // [32] row j of V_s
+  double* tcol = vrow + 32;         // [32] V_s^T v_j
+  const int G = gridDim.x, gi = blockIdx.x;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t rpc = (nk + G - 1) / G;
+  const int64_t r_lo = min(nk, gi * rpc), r_hi = min(nk, r_lo + rpc);
+  const int nr = (int)(r_hi - r_lo);
+
+  for (int cs = 0; cs < w; cs += 32) {
+    const int cw = min(32, w - cs);
+    // ---- load the slab, zero V_s and T_s ----
+    for (int idx = tid; idx < cw * nr; idx += QT) {
+      const int c = idx / nr, i = idx % nr;
+      Ps[c * QR_RS + i] = P[(r_lo + i) + (int64_t)(cs + c) * ld];
+      Vs[c * QR_RS + i] = 0.0;
+    }
+    for (int idx = tid; idx < 32 * 33; idx += QT) Ts[idx] = 0.0;
+    __syncthreads();
+    for (int jj = 0; jj < cw; ++jj) {
+      const int64_t j = cs + jj;  // panel row/col of the pivot
+      double* buf = part + (int64_t)(j & 1) * G * 32;
+      double* rb = rowbuf + (j & 1) * 64;
+      // ---- phase A: partial reductions over own rows i > j ----
+      const int i0 = (int)max((int64_t)0, j + 1 - r_lo);
+      const int nv = cw;  // [0]: |x|^2, [1, cw-jj): dots with columns jj+1.., [cw-jj, cw): V dots
+      for (int v = warp; v < nv; v += QT / 32) {
+        double acc = 0.0;
+        if (v == 0) {
+          for (int i = i0 + lane; i < nr; i += 32) {
+            const double x = Ps[jj * QR_RS + i];
+            acc = fma(x, x, acc);
+          }
+        } else if (v < cw - jj) {
+          const int c = jj + v;
+          for (int i = i0 + lane; i < nr; i += 32) acc = fma(Ps[jj * QR_RS + i], Ps[c * QR_RS + i], acc);
+        } else {
+          const int l = v - (cw - jj);
+          for (int i = i0 + lane; i < nr; i += 32) acc = fma(Vs[l * QR_RS + i], Ps[jj * QR_RS + i], acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) buf[(int64_t)gi * 32 + v] = acc;
+      }
+      if (j >= r_lo && j < r_hi) {
+        const int il = (int)(j - r_lo);
+        for (int c = tid; c < 32; c += QT) {
+          rb[c] = (c >= jj && c < cw) ? Ps[c * QR_RS + il] : 0.0;
+          rb[32 + c] = (c < jj) ? Vs[c * QR_RS + il] : 0.0;
+        }
+      }
+      grid.sync();
+      // ---- phase B: fixed-order reduction over the G partials (all threads:
+      //      value = tid % 32, CTA subset = tid / 32; loads issued in parallel),
+      //      reflector, update own rows ----
+      {
+        const int v = tid & 31, grp = tid >> 5;
+        double acc = 0.0;
+        if (v < nv) {
+          double t[19];
+          int cnt = 0;
+#pragma unroll
+          for (int q2 = 0; q2 < 19; ++q2) {
+            const int g2 = grp + 8 * q2;
+            t[q2] = (g2 < G) ? buf[(int64_t)g2 * 32 + v] : 0.0;
+          }
+#pragma unroll
+          for (int q2 = 0; q2 < 19; ++q2) acc += t[q2];
+          (void)cnt;
+        }
+        Ws[grp * 32 + v] = acc;  // Ws is free during the column loop
+        __syncthreads();
+        if (tid < nv) {
+          double s = 0.0;
+#pragma unroll
+          for (int q2 = 0; q2 < 8; ++q2) s += Ws[q2 * 32 + tid];
+          red[tid] = s;
+        }
+      }
+      if (tid < 32) {
+        rowj[tid] = rb[tid];
+        vrow[tid] = rb[32 + tid];
+      }
+      __syncthreads();
+      const double s1 = red[0];
+      const double x0 = rowj[jj];
+      const double normx = sqrt(s1 + x0 * x0);
+      double alpha = 0.0, v0 = 1.0, beta = 0.0;
+      bool reflect = false;
+      if (normx != 0.0) {
+        alpha = -copysign(normx, x0 != 0.0 ? x0 : 1.0);
+        v0 = x0 - alpha;
+        const double vn2 = s1 + v0 * v0;
+        if (vn2 != 0.0) {
+          beta = 2.0 / vn2;
+          reflect = true;
+        }
+      }
+      const bool own_j = (j >= r_lo && j < r_hi);
+      const int il_j = (int)(j - r_lo);
+      if (!reflect) {
+        // reference: normx == 0 -> betas 0, v = e_j; vn2 == 0 -> also panel[j, j] = alpha
+        if (tid == 0 && gi == 0) betas[j] = 0.0;
+        if (own_j && tid == 0) {
+          Vs[jj * QR_RS + il_j] = 1.0;
+          if (normx != 0.0) Ps[jj * QR_RS + il_j] = alpha;
+        }
+        __syncthreads();
+        continue;  // T_s column jj stays zero (tau = 0)
+      }
+      const double tau = beta * v0 * v0;
+      // w[c] = dots[c] + v0 * P[j, c]  for c in (jj, cw)
+      if (tid > jj && tid < cw) red[tid - jj] = red[tid - jj] + v0 * rowj[tid];
+      // T_s recurrence: t[l] = V_s[:, l]^T v_j = V_s[j, l] + (sum_{i>j} V_s[i, l] x_i) / v0
+      if (tid < jj) tcol[tid] = vrow[tid] + red[(cw - jj) + tid] / v0;
+      __syncthreads();
+      if (tid < jj) {
+        double acc = 0.0;
+        for (int m = tid; m < jj; ++m) acc += Ts[tid * 33 + m] * tcol[m];
+        Ts[tid * 33 + jj] = -tau * acc;
+      }
+      if (tid == 0) Ts[jj * 33 + jj] = tau;
+      // rest -= beta * outer(v, w) over own rows i >= j
+      const int ib = (int)max((int64_t)0, j - r_lo);
+      const int ncc = cw - jj - 1;
+      for (int idx = tid; idx < (nr - ib) * ncc; idx += QT) {
+        const int i = ib + idx % (nr - ib);
+        const int c = jj + 1 + idx / (nr - ib);
+        const double vi = (r_lo + i == j) ? v0 : Ps[jj * QR_RS + i];
+        Ps[c * QR_RS + i] -= beta * (vi * red[c - jj]);
+      }
+      __syncthreads();
+      for (int i = ib + tid; i < nr; i += QT) {
+        if (r_lo + i == j) {
+          Ps[jj * QR_RS + i] = alpha;
+          Vs[jj * QR_RS + i] = v0 / v0;
+        } else {
+          Vs[jj * QR_RS + i] = Ps[jj * QR_RS + i] / v0;
+          Ps[jj * QR_RS + i] = 0.0;
+        }
+      }
+      if (tid == 0 && gi == 0) betas[j] = tau;
+      __syncthreads();
+    }
+    // ---- write the sub-panel and its V back ----
+    for (int idx = tid; idx < cw * nr; idx += QT) {
+      const int c = idx / nr, i = idx % nr;
+      P[(r_lo + i) + (int64_t)(cs + c) * ld] = Ps[c * QR_RS + i];
+      V[(r_lo + i) + (int64_t)(cs + c) * ldv] = Vs[c * QR_RS + i];
+    }
+    const int ce = cs + cw;
+    const int rem = w - ce;
+    if (rem <= 0) break;
+    // ---- block reflector on the remaining panel columns: C -= V_s T_s^T (V_s^T C) ----
+    // C is processed in 32-column chunks staged in shared memory (Ws), so every
+    // dot product runs out of shared memory.
+    const int ib = (int)max((int64_t)0, (int64_t)cs - r_lo);  // V_s is zero above row cs
+    const int nrr = nr - ib;
+    for (int cc0 = 0; cc0 < rem; cc0 += 32) {
+      const int ccw = min(32, rem - cc0);
+      for (int idx = tid; idx < ccw * nrr; idx += QT) {
+        const int c = idx / nrr, i = ib + idx % nrr;
+        Ws[c * QR_RS + i] = P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld];
+      }
+      __syncthreads();
+      for (int idx = tid; idx < cw * ccw; idx += QT) {
+        const int l = idx / ccw, c = idx % ccw;
+        double acc = 0.0;
+        for (int i = ib; i < nr; ++i) acc = fma(Vs[l * QR_RS + i], Ws[c * QR_RS + i], acc);
+        part2[((int64_t)gi * 32 + l) * rem + cc0 + c] = acc;
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    // reduce-scatter: CTA gi reduces a slice of the cw x rem entries (warp per entry)
+    const int tot = cw * rem;
+    const int per = (tot + G - 1) / G;
+    for (int e = gi * per + warp; e < min(tot, (gi + 1) * per); e += QT / 32) {
+      double acc = 0.0;
+      for (int g2 = lane; g2 < G; g2 += 32) acc += part2[(int64_t)g2 * 32 * rem + e];
+      acc = warp_sum(acc);
+      if (lane == 0) wfin[e] = acc;
+    }
+    grid.sync();
+    // W' = T_s^T W into Ps (the sub-panel slab is already written back)
+    for (int idx = tid; idx < cw * rem; idx += QT) Ws[(idx / rem) * QR_RS + idx % rem] = wfin[idx];
+    __syncthreads();
+    for (int idx = tid; idx < cw * rem; idx += QT) {
+      const int l = idx / rem, c = idx % rem;
+      double acc = 0.0;
+      for (int m = 0; m <= l; ++m) acc = fma(Ts[m * 33 + l], Ws[m * QR_RS + c], acc);
+      Ps[l * QR_RS + c] = acc;
+    }
+    __syncthreads();
+    // C(own rows) -= V_s W', chunk by chunk through shared memory
+    for (int cc0 = 0; cc0 < rem; cc0 += 32) {
+      const int ccw = min(32, rem - cc0);
+      for (int idx = tid; idx < ccw * nrr; idx += QT) {
+        const int c = idx / nrr, i = ib + idx % nrr;
+        double acc = 0.0;
+        for (int l = 0; l < cw; ++l) acc = fma(Vs[l * QR_RS + i], Ps[l * QR_RS + cc0 + c], acc);
+        P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld] -= acc;
+      }
+    }
+    grid.sync();  // the next sub-panel's slab load reads other CTAs' rows? no: own rows only,
+                  // but wfin / part2 are reused by the next block update
+  }
+}
+
 }  // namespace
 
 int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
-             double* betas, double* part, int64_t part_elems, double* rowbuf) {
+             double* betas, double* part, int64_t part_elems, double* rowbuf, double* part2,
+             double* wfin) {
   if (w <= 0 || nk <= 0) return 0;
+  if (part2 && wfin) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int G = (int)((nk + 63) / 64);
+    if (G > sms) G = sms;
+    if ((nk + G - 1) / G <= QR_RMAX && 2LL * G * 32 <= part_elems) {
+      static bool attr = false;
+      if (!attr) {
+        CUDA_TRY(cudaFuncSetAttribute(qr_panel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      QR_SMEM));
+        attr = true;
+      }
+      void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf, &part2, &wfin};
+      count_launch();
+      CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel2_kernel, dim3(G), dim3(QT), args,
+                                           (size_t)QR_SMEM, st));
+      return 0;
+    }
+  }
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
