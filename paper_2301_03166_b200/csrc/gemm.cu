@@ -21,6 +21,7 @@
 #include <cstdarg>
 #include <cstring>
 #include <atomic>
+#include <cstdlib>
 #include <mutex>
 
 #include <cudaTypedefs.h>
@@ -98,26 +99,49 @@ int make_tma_map(CUtensorMap* map, const double* ptr, int64_t ld, int64_t inner,
 // ---------------------------------------------------------------------------
 namespace {
 
-// Persistent ping-pong DMMA GEMM.
-//   * grid = #SMs CTAs; each CTA walks tiles t = blockIdx.x + i*gridDim.x.
-//   * two consumer warpgroups (WG0, WG1) own alternate tiles (i even / odd),
-//     each with its own TMA ring and its own producer warp; an mbarrier token
-//     makes their main loops strictly alternate, so one group's epilogue
-//     (C load, D store, checksum partials) runs under the other's DMMA loop.
-//   * warp tile 64x32 (128 fp64 accumulators / thread), WG tile 128x64.
-constexpr int BM = 128, BN = 64, BK = 16, STAGES = 4;
+// Persistent multi-warpgroup DMMA GEMM.
+//   * grid = #SMs CTAs; each CTA walks work units (tiles, or whole b x b
+//     checksum blocks in fused mode) u = blockIdx.x + i*gridDim.x.
+//   * NWG consumer warpgroups own units i = w (mod NWG), each with its own
+//     TMA ring fed by its own producer warp (the last warpgroup). Groups start
+//     one main loop apart and then run free: while one group runs its
+//     epilogue (C load, D store, checksum partials) the others keep the DMMA
+//     pipe busy. One warp per SM sub-partition reaches only ~83% of the DMMA
+//     issue rate with this instruction stream, so the trailing-update shapes
+//     (K = b) use three groups (32x32 warp tiles); long-K products use two
+//     (64x32 warp tiles, fewer shared-memory reads per DMMA).
+constexpr int BN = 64, BK = 16;
 constexpr int WG_THREADS = 128;
-constexpr int THREADS = 3 * WG_THREADS;  // WG0, WG1 consume; WG2 warps 8/9 produce
-constexpr int A_BYTES = BM * BK * 8;      // 16 KB
-constexpr int B_BYTES = BN * BK * 8;      // 8 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int RING_BYTES = STAGES * STAGE_BYTES;
 constexpr int MAXFB = 256;
 // per-WG fused-checksum accumulators: col plain/weighted [2 wm halves][fb][2],
 // row plain [2 wn halves][fb], warp max [4]
 constexpr int SUM_DOUBLES = 2 * MAXFB * 2 + 2 * MAXFB + 4;
-constexpr int SMEM_BYTES = 2 * RING_BYTES + 1024 + (2 * 2 * STAGES + 2) * 8 + 2 * SUM_DOUBLES * 8;
-constexpr int EPI_RP = 1;  // row-pair groups whose C loads are batched in the epilogue
+
+template <int NWG>
+struct Cfg;
+template <>
+struct Cfg<2> {
+  static constexpr int WTM = 64, BM = 128, STAGES = 4;
+};
+template <>
+struct Cfg<3> {
+  static constexpr int WTM = 32, BM = 64, STAGES = 3;
+};
+template <int NWG>
+struct Geo {
+  static constexpr int BM = Cfg<NWG>::BM, STAGES = Cfg<NWG>::STAGES, WTM = Cfg<NWG>::WTM;
+  static constexpr int RP = WTM / 16;  // 16-row fragment groups per warp
+  static constexpr int THREADS = (NWG + 1) * WG_THREADS;
+  static constexpr int A_BYTES = BM * BK * 8;
+  static constexpr int B_BYTES = BN * BK * 8;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int RING_BYTES = STAGES * STAGE_BYTES;
+  static constexpr int NBARS = NWG * 2 * STAGES + NWG;
+  static constexpr int SMEM_BYTES = NWG * RING_BYTES + 1024 + NBARS * 8 + NWG * SUM_DOUBLES * 8;
+  // registers: producer warpgroup drops to REG_P, consumers rise to REG_C
+  static constexpr int REG_P = NWG == 2 ? 40 : 32;
+  static constexpr int REG_C = NWG == 2 ? 232 : 160;
+};
 
 struct KParams {
   int M, N, K;
@@ -139,20 +163,38 @@ struct KParams {
   int64_t split_stride;  // elements between split slices in partial mode
 };
 
+// Shared-memory layouts (all TMA SWIZZLE_128B, 1024-byte aligned):
+//  * m/n-contiguous tiles (A-N, B-T): 16-row boxes [chunk][k][16] -- element
+//    (k, r) at chunk*2048 + k*128 + (((r%16)/2) ^ (k&7))*16 + (r&1)*8;
+//  * k-contiguous tiles (A-T, B-N): [r][16 k] -- (k, r) at
+//    r*128 + ((k/2) ^ (r&7))*16 + (k&1)*8.
+// A ld.shared.v2.f64 issued by a warp is served in four 8-lane phases; the
+// fragment -> row/column maps below make every phase touch 8 distinct 16-byte
+// chunks (conflict-free), which needs the permutation pm() on k-contiguous
+// tiles.
+ABFT_DEVINL int pm(int g) { return (g >> 1) + 4 * (g & 1); }
+
+// Row of accumulator fragment (rp, e) for lane group g inside the warp tile.
+template <bool AT>
+ABFT_DEVINL int row_of(int rp, int e, int g) {
+  if (AT) return 16 * rp + 8 * e + pm(g);
+  return 16 * rp + 2 * g + e;
+}
 // Column of accumulator fragment (cf, c8) inside the warp tile.
-// B-N: wn + 8cf + c8;  B-T: cf=(cp,f): wn + 16cp + 2c8 + f.
+// B-N: wn + 8cf + pm(c8);  B-T: cf=(cp,f): wn + 16cp + 2c8 + f.
 template <bool BT>
 ABFT_DEVINL int col_of(int cf, int c8) {
   if (BT) return 16 * (cf >> 1) + 2 * c8 + (cf & 1);
-  return 8 * cf + c8;
+  return 8 * cf + pm(c8);
 }
 
-// Work unit u of a warpgroup: plain mode = one tile; fused mode = one
-// fb x fb block (ntm_b x ntn_b tiles). Returns the number of tiles in it.
+// Work unit of a warpgroup: plain mode = one tile; fused mode = one fb x fb
+// block (ntm_b x ntn_b tiles).
 ABFT_DEVINL int unit_tiles(const KParams& p) { return p.fuse ? p.ntm_b * p.ntn_b : 1; }
 ABFT_DEVINL int total_units(const KParams& p) {
   return p.fuse ? p.nbr_b * p.nbc_b : p.tiles_m * p.tiles_n * p.splits;
 }
+template <int BM>
 ABFT_DEVINL void fused_tile(const KParams& p, int unit, int u, int* m0, int* n0, int* bi, int* bj,
                             int* tm, int* tn) {
   *bi = unit % p.nbr_b;
@@ -162,7 +204,7 @@ ABFT_DEVINL void fused_tile(const KParams& p, int unit, int u, int* m0, int* n0,
   *m0 = *bi * p.fb + *tm * BM;
   *n0 = *bj * p.fb + *tn * BN;
 }
-
+template <int BM>
 ABFT_DEVINL void tile_coords(const KParams& p, int t, int* m0, int* n0, int* z) {
   const int tm = t % p.tiles_m;
   const int r = t / p.tiles_m;
@@ -171,56 +213,59 @@ ABFT_DEVINL void tile_coords(const KParams& p, int t, int* m0, int* n0, int* z) 
   *z = r / p.tiles_n;
 }
 
-template <bool AT, bool BT>
-__global__ void __launch_bounds__(THREADS, 1)
+template <bool AT, bool BT, int NWG>
+__global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
     dgemm_tma_dmma(const __grid_constant__ CUtensorMap mapA,
                    const __grid_constant__ CUtensorMap mapB,
                    const __grid_constant__ CUtensorMap mapC, KParams p) {
+  using G = Geo<NWG>;
+  constexpr int BM = G::BM, STAGES = G::STAGES, RP = G::RP, WTM = G::WTM;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + 2 * RING_BYTES);
-  // bars[wg*2*STAGES + s] = full, bars[wg*2*STAGES + STAGES + s] = empty, bars[4*STAGES + wg] = token
-  double* sums_base = reinterpret_cast<double*>(bars + 4 * STAGES + 2);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NWG * G::RING_BYTES);
+  // bars[w*2*STAGES + s] = full, bars[w*2*STAGES + STAGES + s] = empty,
+  // bars[NWG*2*STAGES + w] = start token of warpgroup w
+  double* sums_base = reinterpret_cast<double*>(bars + G::NBARS);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int units = total_units(p);
   const int upt = unit_tiles(p);
 
   if (threadIdx.x == 0) {
-    for (int w = 0; w < 2; ++w)
+    for (int w = 0; w < NWG; ++w) {
       for (int s = 0; s < STAGES; ++s) {
         mbar_init(&bars[w * 2 * STAGES + s], 1);
         mbar_init(&bars[w * 2 * STAGES + STAGES + s], 4);
       }
-    mbar_init(&bars[4 * STAGES + 0], 4);
-    mbar_init(&bars[4 * STAGES + 1], 4);
+      mbar_init(&bars[NWG * 2 * STAGES + w], 4);
+    }
     mbar_fence_init();
   }
-  for (int i = threadIdx.x; i < 2 * SUM_DOUBLES; i += THREADS) sums_base[i] = 0.0;
+  for (int i = threadIdx.x; i < NWG * SUM_DOUBLES; i += G::THREADS) sums_base[i] = 0.0;
   __syncthreads();
 
-  if (warp >= 8) {
-    // ===== producers: warp 8 feeds ring 0, warp 9 feeds ring 1 =====
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n");
-    const int w = warp - 8;
-    if (w < 2 && lane == 0) {
+  if (warp >= 4 * NWG) {
+    // ===== producers: warp 4*NWG + w feeds ring w =====
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(G::REG_P));
+    const int w = warp - 4 * NWG;
+    if (w < NWG && lane == 0) {
       tma_prefetch_desc(&mapA);
       tma_prefetch_desc(&mapB);
       uint64_t* full = bars + w * 2 * STAGES;
       uint64_t* empty = full + STAGES;
-      uint8_t* ring = smem + w * RING_BYTES;
+      uint8_t* ring = smem + w * G::RING_BYTES;
       uint32_t q = 0;
-      for (int i = w;; i += 2) {
+      for (int i = w;; i += NWG) {
         const int unit = blockIdx.x + i * gridDim.x;
         if (unit >= units) break;
         for (int u = 0; u < upt; ++u) {
           int m0, n0, z = 0;
           if (p.fuse) {
             int bi, bj, tm, tn;
-            fused_tile(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
+            fused_tile<BM>(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
           } else {
-            tile_coords(p, unit, &m0, &n0, &z);
+            tile_coords<BM>(p, unit, &m0, &n0, &z);
           }
           if (m0 >= p.M || n0 >= p.N) continue;
           const int kbeg = z * p.k_per_split;
@@ -230,18 +275,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int kt = 0; kt < nkt; ++kt, ++q) {
             const int s = q % STAGES;
             if (q >= STAGES) mbar_wait(&empty[s], ((q / STAGES) - 1) & 1);
-            uint8_t* sa = ring + s * STAGE_BYTES;
-            uint8_t* sb = sa + A_BYTES;
+            uint8_t* sa = ring + s * G::STAGE_BYTES;
+            uint8_t* sb = sa + G::A_BYTES;
             const int k0 = kbeg + kt * BK;
-            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-            if (AT)
+            mbar_arrive_expect_tx(&full[s], G::STAGE_BYTES);
+            if (AT) {
               tma_load_2d(sa, &mapA, &full[s], k0 + p.a_shift, m0);
-            else
-              tma_load_2d(sa, &mapA, &full[s], m0 + p.a_shift, k0);
-            if (BT)
-              tma_load_2d(sb, &mapB, &full[s], n0 + p.b_shift, k0);
-            else
+            } else {
+#pragma unroll
+              for (int mc = 0; mc < BM / 16; ++mc)
+                tma_load_2d(sa + mc * 2048, &mapA, &full[s], m0 + 16 * mc + p.a_shift, k0);
+            }
+            if (BT) {
+#pragma unroll
+              for (int nc = 0; nc < BN / 16; ++nc)
+                tma_load_2d(sb + nc * 2048, &mapB, &full[s], n0 + 16 * nc + p.b_shift, k0);
+            } else {
               tma_load_2d(sb, &mapB, &full[s], k0 + p.b_shift, n0);
+            }
           }
         }
       }
@@ -250,17 +301,16 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 
   // ===== consumers =====
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 232;\n");
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(G::REG_C));
   const int wg = warp >> 2;
   const int wi = warp & 3;
   const int g = lane >> 2, j = lane & 3;
-  const int wm = (wi & 1) * 64;
+  const int wm = (wi & 1) * WTM;
   const int wn = (wi >> 1) * 32;
   uint64_t* full = bars + wg * 2 * STAGES;
   uint64_t* empty = full + STAGES;
-  uint64_t* my_tok = bars + 4 * STAGES + wg;
-  uint64_t* other_tok = bars + 4 * STAGES + (1 - wg);
-  const uint32_t ring = smem_u32(smem + wg * RING_BYTES);
+  uint64_t* tok = bars + NWG * 2 * STAGES;
+  const uint32_t ring = smem_u32(smem + wg * G::RING_BYTES);
   // fused-checksum accumulators of this warpgroup
   double* colacc = sums_base + wg * SUM_DOUBLES;   // [2][MAXFB][2]
   double* rowacc = colacc + 2 * MAXFB * 2;         // [2][MAXFB]
@@ -268,7 +318,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t q = 0;
   int jt = 0;  // tiles processed by this WG
 
-  for (int i = wg;; i += 2) {
+  for (int i = wg;; i += NWG) {
     const int unit = blockIdx.x + i * gridDim.x;
     if (unit >= units) break;
     double mx = 0.0;
@@ -276,87 +326,98 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int u = 0; u < upt; ++u) {
       int m0, n0, z = 0, tm = 0, tn = 0;
       if (p.fuse)
-        fused_tile(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
+        fused_tile<BM>(p, unit, u, &m0, &n0, &bi, &bj, &tm, &tn);
       else
-        tile_coords(p, unit, &m0, &n0, &z);
+        tile_coords<BM>(p, unit, &m0, &n0, &z);
       if (m0 >= p.M || n0 >= p.N) continue;
       const int kbeg = z * p.k_per_split;
       const int kend = min(p.K, kbeg + p.k_per_split);
       const int nkt = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
-      double acc[8][4][2];
+      double acc[2 * RP][4][2];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 2 * RP; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-      // Phase offset: WG1 starts its first main loop when WG0 finishes its
-      // first one; afterwards both run free, so their epilogues interleave
-      // with the other group's DMMA loop while main loops co-run (two warps
-      // per SM sub-partition keep the DMMA pipe saturated).
-      if (wg == 1 && jt == 0) mbar_wait(my_tok, 0);
+      // start offset: group w begins its first main loop when group w-1 has
+      // finished its first one
+      if (wg > 0 && jt == 0) mbar_wait(&tok[wg], 0);
       __syncwarp();
 
+      int prev_s = -1;
       for (int kt = 0; kt < nkt; ++kt, ++q) {
         const int s = q % STAGES;
         mbar_wait(&full[s], (q / STAGES) & 1);
         __syncwarp();  // mma.sync.aligned needs the whole warp converged
-        const uint32_t sa = ring + s * STAGE_BYTES;
-        const uint32_t sb = sa + A_BYTES;
+        // Release the previous stage one step late: its shared-memory reads
+        // fed DMMAs issued before this wait loop (a hard scheduling boundary),
+        // so they have completed -- no fence needed on the steady path.
+        if (prev_s >= 0 && lane == 0) mbar_arrive(&empty[prev_s]);
+        const uint32_t sa = ring + s * G::STAGE_BYTES;
+        const uint32_t sb = sa + G::A_BYTES;
 #pragma unroll
         for (int ks = 0; ks < BK; ks += 8) {
           double b[4][2];
           if (!BT) {
-            // swizzled [n][16 k]: n = wn+8cf+g
+            // [n][16 k]: n = wn + 8cf + pm(g), k = ks+2j (+ss in the pair)
 #pragma unroll
             for (int cf = 0; cf < 4; ++cf) {
-              const int n = wn + 8 * cf + g;
+              const int n = wn + 8 * cf + pm(g);
               double2 v = lds_f64x2(sb + n * 128 + ((((ks >> 1) + j) ^ (n & 7)) << 4));
               b[cf][0] = v.x;
               b[cf][1] = v.y;
             }
           } else {
-            // dense [k][n]: n = wn+16cp+2g+f, cf = 2cp+f
+            // [n/16][k][16 n]: n = wn + 16cp + 2g (+f in the pair), k = ks+2j+ss
 #pragma unroll
             for (int cp = 0; cp < 2; ++cp)
 #pragma unroll
               for (int ss = 0; ss < 2; ++ss) {
-                double2 v = lds_f64x2(sb + ((ks + 2 * j + ss) * BN + wn + 16 * cp + 2 * g) * 8);
+                const int k = ks + 2 * j + ss;
+                double2 v = lds_f64x2(sb + ((wn >> 4) + cp) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
                 b[2 * cp][ss] = v.x;
                 b[2 * cp + 1][ss] = v.y;
               }
           }
+          double a[RP][2][2];
 #pragma unroll
-          for (int rp = 0; rp < 4; ++rp) {
-            double a[2][2];
+          for (int rp = 0; rp < RP; ++rp) {
             if (!AT) {
+              // [m/16][k][16 m]: m = wm + 16rp + 2g (+e in the pair), k = ks+2j+ss
 #pragma unroll
               for (int ss = 0; ss < 2; ++ss) {
-                double2 v = lds_f64x2(sa + ((ks + 2 * j + ss) * BM + wm + 16 * rp + 2 * g) * 8);
-                a[ss][0] = v.x;
-                a[ss][1] = v.y;
+                const int k = ks + 2 * j + ss;
+                double2 v = lds_f64x2(sa + ((wm >> 4) + rp) * 2048 + k * 128 + ((g ^ (k & 7)) << 4));
+                a[rp][ss][0] = v.x;
+                a[rp][ss][1] = v.y;
               }
             } else {
+              // [m][16 k]: m = wm + 16rp + 8e + pm(g)
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
-                const int m = wm + 16 * rp + 2 * g + e;
+                const int m = wm + 16 * rp + 8 * e + pm(g);
                 double2 v = lds_f64x2(sa + m * 128 + ((((ks >> 1) + j) ^ (m & 7)) << 4));
-                a[0][e] = v.x;
-                a[1][e] = v.y;
+                a[rp][0][e] = v.x;
+                a[rp][1][e] = v.y;
               }
             }
+          }
 #pragma unroll
-            for (int ss = 0; ss < 2; ++ss)
+          for (int ss = 0; ss < 2; ++ss)
+#pragma unroll
+            for (int rp = 0; rp < RP; ++rp)
 #pragma unroll
               for (int e = 0; e < 2; ++e)
 #pragma unroll
                 for (int cf = 0; cf < 4; ++cf)
-                  dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[ss][e], b[cf][ss]);
-          }
+                  dmma_8x8x4(acc[2 * rp + e][cf][0], acc[2 * rp + e][cf][1], a[rp][ss][e], b[cf][ss]);
         }
-        consumer_release(&empty[s], lane);
+        prev_s = s;
       }
-      if (wg == 0 && jt == 0 && lane == 0) mbar_arrive(other_tok);
+      // last stage of the tile: fenced release (no later wait orders its reads)
+      if (prev_s >= 0) consumer_release(&empty[prev_s], lane);
+      if (wg + 1 < NWG && jt == 0 && lane == 0) mbar_arrive(&tok[wg + 1]);
       ++jt;
 
       // ===== epilogue =====
@@ -365,9 +426,12 @@ __global__ void __launch_bounds__(THREADS, 1)
       double* D = p.partial ? p.D + (int64_t)z * p.split_stride : p.D;
       const bool use_c = !p.partial && p.beta != 0.0;
 #pragma unroll
-      for (int rp = 0; rp < 4; ++rp) {
-        const int row = m0 + wm + 16 * rp + 2 * g;
-        const bool rv0 = row < p.M, rv1 = row + 1 < p.M;
+      for (int rp = 0; rp < RP; ++rp) {
+        // rows of fragments (rp, 0) / (rp, 1): adjacent for A-N, 8 apart for A-T
+        const int row0 = m0 + wm + row_of<AT>(rp, 0, g);
+        const int row1 = m0 + wm + row_of<AT>(rp, 1, g);
+        const bool rv0 = row0 < p.M, rv1 = row1 < p.M;
+        const bool pairv = !AT && p.vec && rv1;  // 16-byte row-pair access
         double cv[4][2][2];
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf)
@@ -375,15 +439,15 @@ __global__ void __launch_bounds__(THREADS, 1)
           for (int tt = 0; tt < 2; ++tt) {
             cv[cf][tt][0] = cv[cf][tt][1] = 0.0;
             const int col = n0 + wn + col_of<BT>(cf, 2 * j + tt);
-            if (!use_c || !rv0 || col >= p.N) continue;
-            const double* c = p.C + row + (int64_t)col * p.ldc;
-            if (rv1 && p.vec) {
-              const double2 v = *reinterpret_cast<const double2*>(c);
+            if (!use_c || col >= p.N) continue;
+            const double* c = p.C + (int64_t)col * p.ldc;
+            if (pairv) {
+              const double2 v = *reinterpret_cast<const double2*>(c + row0);
               cv[cf][tt][0] = v.x;
               cv[cf][tt][1] = v.y;
             } else {
-              cv[cf][tt][0] = c[0];
-              if (rv1) cv[cf][tt][1] = c[1];
+              if (rv0) cv[cf][tt][0] = c[row0];
+              if (rv1) cv[cf][tt][1] = c[row1];
             }
           }
 #pragma unroll
@@ -402,20 +466,20 @@ __global__ void __launch_bounds__(THREADS, 1)
             o1 = (rv1 && cvld) ? o1 : 0.0;
             acc[2 * rp][cf][tt] = o0;
             acc[2 * rp + 1][cf][tt] = o1;
-            if (!rv0 || !cvld) continue;
-            double* d = D + row + (int64_t)col * p.ldd;
-            if (rv1 && p.vec && !p.partial) {
-              *reinterpret_cast<double2*>(d) = make_double2(o0, o1);
+            if (!cvld) continue;
+            double* d = D + (int64_t)col * p.ldd;
+            if (pairv && !p.partial) {
+              *reinterpret_cast<double2*>(d + row0) = make_double2(o0, o1);
             } else {
-              d[0] = o0;
-              if (rv1) d[1] = o1;
+              if (rv0) d[row0] = o0;
+              if (rv1) d[row1] = o1;
             }
           }
       }
       // Pass 2 (fused checksums) from the output registers.
       if (p.fuse) {
 #pragma unroll
-        for (int rp = 0; rp < 4; ++rp) {
+        for (int rp = 0; rp < RP; ++rp) {
           double rs0 = 0.0, rs1 = 0.0;
 #pragma unroll
           for (int cf = 0; cf < 4; ++cf)
@@ -431,24 +495,26 @@ __global__ void __launch_bounds__(THREADS, 1)
           rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
           rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
           if (j == 0) {
-            const int r = tm * BM + wm + 16 * rp + 2 * g;
-            rowacc[(wn >> 5) * MAXFB + r] += rs0;
-            rowacc[(wn >> 5) * MAXFB + r + 1] += rs1;
+            const int r0b = tm * BM + wm + row_of<AT>(rp, 0, g);
+            const int r1b = tm * BM + wm + row_of<AT>(rp, 1, g);
+            rowacc[(wn >> 5) * MAXFB + r0b] += rs0;
+            rowacc[(wn >> 5) * MAXFB + r1b] += rs1;
           }
         }
-        // column plain / index-weighted sums over this warp's 64 rows
-        const double wbase = (double)(tm * BM + wm + 2 * g);
+        // column plain / index-weighted sums over this warp's WTM rows
+        const int wbase = tm * BM + wm;
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf)
 #pragma unroll
           for (int tt = 0; tt < 2; ++tt) {
             double a0 = 0.0, a1 = 0.0;
 #pragma unroll
-            for (int rp = 0; rp < 4; ++rp) {
+            for (int rp = 0; rp < RP; ++rp) {
               const double x0 = acc[2 * rp][cf][tt], x1 = acc[2 * rp + 1][cf][tt];
-              const double w0 = wbase + 16.0 * rp;
+              const double w0 = (double)(wbase + row_of<AT>(rp, 0, g));
+              const double w1 = (double)(wbase + row_of<AT>(rp, 1, g));
               a0 += x0 + x1;
-              a1 += w0 * x0 + (w0 + 1.0) * x1;
+              a1 += w0 * x0 + w1 * x1;
             }
 #pragma unroll
             for (int o = 4; o < 32; o <<= 1) {
@@ -457,8 +523,8 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             if (g == 0) {
               const int c = tn * BN + wn + col_of<BT>(cf, 2 * j + tt);
-              colacc[((wm >> 6) * MAXFB + c) * 2 + 0] += a0;
-              colacc[((wm >> 6) * MAXFB + c) * 2 + 1] += a1;
+              colacc[((wi & 1) * MAXFB + c) * 2 + 0] += a0;
+              colacc[((wi & 1) * MAXFB + c) * 2 + 1] += a1;
             }
           }
       }
@@ -505,14 +571,14 @@ __global__ void splitk_reduce(int M, int N, int splits, const double* __restrict
   }
 }
 
-template <bool AT, bool BT>
+template <bool AT, bool BT, int NWG>
 int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
-                  const CUtensorMap& mc, const KParams& kp, int max_ctas,
-                  int splits) {
+                  const CUtensorMap& mc, const KParams& kp, int max_ctas) {
+  using G = Geo<NWG>;
   static bool attr_set = false;
   if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_dmma<AT, BT>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES));
+    CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_dmma<AT, BT, NWG>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
     attr_set = true;
   }
   int dev = 0, sms = 148;
@@ -522,15 +588,24 @@ int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
   const int cap = (max_ctas > 0 && max_ctas < sms) ? max_ctas : sms;
   const int grid = total < cap ? total : cap;
   count_launch();
-  dgemm_tma_dmma<AT, BT><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, mc, kp);
+  dgemm_tma_dmma<AT, BT, NWG><<<grid, G::THREADS, G::SMEM_BYTES, st>>>(ma, mb, mc, kp);
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+
+template <int NWG>
+int launch_any(cudaStream_t st, bool AT, bool BT, const CUtensorMap& ma, const CUtensorMap& mb,
+               const CUtensorMap& mc, const KParams& kp, int max_ctas) {
+  if (AT && BT) return launch_kernel<true, true, NWG>(st, ma, mb, mc, kp, max_ctas);
+  if (AT) return launch_kernel<true, false, NWG>(st, ma, mb, mc, kp, max_ctas);
+  if (BT) return launch_kernel<false, true, NWG>(st, ma, mb, mc, kp, max_ctas);
+  return launch_kernel<false, false, NWG>(st, ma, mb, mc, kp, max_ctas);
 }
 
 }  // namespace
 
 int gemm_splits_for(int M, int N, int K, int num_sms) {
-  const int64_t tiles = (int64_t)((M + BM - 1) / BM) * ((N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + BN - 1) / BN);
   if (K <= 4 * BK * 8 || tiles >= 2 * num_sms) return 1;
   int s = static_cast<int>((2 * num_sms + tiles - 1) / tiles);
   const int maxs = K / (8 * BK);  // keep >= 128 of K per split
@@ -554,17 +629,6 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
   }
   const bool AT = (ta == 'T' || ta == 't');
   const bool BT = (tb == 'T' || tb == 't');
-  CUtensorMap ma, mb;
-  int sha = 0, shb = 0;
-  if (AT)
-    ABFT_TRY(make_tma_map(&ma, A, lda, K, M, BK, BM, true, &sha));
-  else
-    ABFT_TRY(make_tma_map(&ma, A, lda, M, K, BM, BK, false, &sha));
-  if (BT)
-    ABFT_TRY(make_tma_map(&mb, B, ldb, N, K, BN, BK, false, &shb));
-  else
-    ABFT_TRY(make_tma_map(&mb, B, ldb, K, N, BK, BN, true, &shb));
-
   if (fs) splits = 1;
   if (splits <= 0) {
     int dev = 0, sms = 148;
@@ -591,6 +655,21 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
   } else {
     kps = K;
   }
+
+  // three warpgroups (64x64 tiles) for short-K products such as the rank-b
+  // trailing updates, two (128x64 tiles) for long K
+  const int nwg = (kps <= 1024) ? 3 : 2;
+  const int BM = nwg == 3 ? Cfg<3>::BM : Cfg<2>::BM;
+  CUtensorMap ma, mb;
+  int sha = 0, shb = 0;
+  if (AT)
+    ABFT_TRY(make_tma_map(&ma, A, lda, K, M, BK, BM, true, &sha));
+  else
+    ABFT_TRY(make_tma_map(&ma, A, lda, M, K, 16, BK, true, &sha));
+  if (BT)
+    ABFT_TRY(make_tma_map(&mb, B, ldb, N, K, 16, BK, true, &shb));
+  else
+    ABFT_TRY(make_tma_map(&mb, B, ldb, K, N, BK, BN, true, &shb));
 
   KParams kp;
   kp.M = M;
@@ -646,15 +725,8 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
       kp.c_shift = shc;
     }
   }
-  int rc;
-  if (AT && BT)
-    rc = launch_kernel<true, true>(st, ma, mb, mc, kp, max_ctas, splits);
-  else if (AT)
-    rc = launch_kernel<true, false>(st, ma, mb, mc, kp, max_ctas, splits);
-  else if (BT)
-    rc = launch_kernel<false, true>(st, ma, mb, mc, kp, max_ctas, splits);
-  else
-    rc = launch_kernel<false, false>(st, ma, mb, mc, kp, max_ctas, splits);
+  int rc = nwg == 3 ? launch_any<3>(st, AT, BT, ma, mb, mc, kp, max_ctas)
+                    : launch_any<2>(st, AT, BT, ma, mb, mc, kp, max_ctas);
   if (rc) return rc;
   if (splits > 1) {
     int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
