@@ -424,6 +424,18 @@ __global__ void sub_kernel(const double* x, int64_t ldx, double* d, int64_t ldd,
   }
 }
 
+// dst[c + r*ldd] = src[r*row_step + c*lds]   (r < rows, c < cols): gathers
+// strided rows of src and transposes them.
+__global__ void gather_transpose_kernel(const double* src, int64_t row_step, int64_t lds,
+                                        int64_t rows, int64_t cols, double* dst, int64_t ldd) {
+  const int64_t total = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i % cols, r = i / cols;
+    dst[c + r * ldd] = src[r * row_step + c * lds];
+  }
+}
+
 __global__ void add_diag_kernel(double* a, int64_t ld, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
@@ -541,6 +553,16 @@ int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t
   if (rows <= 0 || cols <= 0) return 0;
   count_launch();
   sub_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,
+                     int64_t rows, int64_t cols, double* dst, int64_t ldd) {
+  if (rows <= 0 || cols <= 0) return 0;
+  count_launch();
+  gather_transpose_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, row_step, lds, rows,
+                                                                      cols, dst, ldd);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

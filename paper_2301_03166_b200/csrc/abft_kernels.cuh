@@ -102,6 +102,9 @@ int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t co
 int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
                 int64_t rows, int64_t cols, int mode = 0);
 int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v);
+// dst[c + r*ldd] = src[r*row_step + c*lds]
+int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,
+                     int64_t rows, int64_t cols, double* dst, int64_t ldd);
 // d -= x
 int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
                int64_t cols);

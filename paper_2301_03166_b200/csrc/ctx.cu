@@ -32,6 +32,8 @@ enum { PROF_PD = 0, PROF_PU = 1, PROF_TMU = 2, PROF_ABFT = 3, PROF_N = 4 };
 
 struct Snapshot {
   double* m = nullptr;
+  double* chol_rs = nullptr;
+  bool chol_rs_valid = false;
   int64_t k_done = 0;
   int qr_count = 0;
   bool used = false;
@@ -59,6 +61,8 @@ struct abft_ctx {
   double* rsm = nullptr;   // maintained row sums (n x nb, ld)
   double* el = nullptr;    // operand block-row sums (2nb x b, ld_cs)
   double* er = nullptr;    // R * E_R (b x nb, ld_t)
+  double* chol_rs = nullptr;  // Cholesky running row checksums of future panels (n x nb)
+  bool chol_rs_valid = false;
 
   // workspaces
   int64_t ld_t = 0;     // leading dim of b x b / b x n buffers
@@ -102,6 +106,7 @@ struct abft_ctx {
   bool timed = false;
   int32_t cur_iter = 0;
   bool fuse_enabled = true;       // ABFT_NO_FUSE=1 disables (A/B testing)
+  bool want_chol_rs = false;      // abft_factorize: a later iteration uses FULL
   bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
   int64_t pd_ready = -1;          // panel already factored by the look-ahead
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
@@ -243,6 +248,35 @@ int check_info(abft_ctx* c) {
 // ---------------------------------------------------------------------------
 // tasks (linalg.py:192-258)
 // ---------------------------------------------------------------------------
+// Cholesky FULL row checksums, maintained right-looking. chol_rs[r, j] holds,
+// for every future panel j, the row sums over panel j's columns of the
+// original matrix minus every rank-b update applied so far:
+//   after panel k is final, chol_rs[pe:n, j] -= L_k[pe:n, :] * (1^T L_k[block j, :])^T
+// for j > k. The reference maintains the same quantity from the operands at
+// TMU(j) (maintain_gemm, abft.py:157 with R = L[p:pe, 0:p]^T); accumulating
+// it panel by panel avoids re-reading all of L at every iteration.
+int chol_rs_encode(abft_ctx* c) {
+  Region all{c->m, c->ld, c->n, c->n, c->b};
+  SumOut o;
+  o.rp = c->chol_rs;
+  o.rp_ld = c->ld;
+  ABFT_TRY(blocksum(c->st, all, o));
+  c->chol_rs_valid = true;
+  return 0;
+}
+
+int chol_rs_update(abft_ctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t nj = c->nb - (k + 1);
+  if (nj <= 0 || pe >= n) return 0;
+  // Bc (w x nj): Bc[kk, j] = plain col sum of L over block row (k+1+j), column p+kk
+  ABFT_TRY(gather_transpose(c->st, c->gcsw + 2 * (k + 1) + p * c->ld_cs, 2, c->ld_cs, nj, w,
+                            c->er, c->ld_t));
+  return gemm(c->st, 'N', 'N', (int)(n - pe), (int)nj, (int)w, -1.0, c->m + pe + p * c->ld, c->ld,
+              c->er, c->ld_t, 1.0, c->chol_rs + pe + (k + 1) * c->ld, c->ld,
+              c->chol_rs + pe + (k + 1) * c->ld, c->ld, &c->gws);
+}
+
 // LU panel, part 1: factor the diagonal block and form L11^{-1}, U11^{-1}.
 int lu_diag(abft_ctx* c, cudaStream_t st, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
@@ -296,6 +330,7 @@ int task_pu(abft_ctx* c, int64_t k) {
     SumOut o = sums_for(c, p, p, false);
     o.bm = nullptr;
     ABFT_TRY(blocksum(c->st, reg, o));
+    if (c->chol_rs_valid) ABFT_TRY(chol_rs_update(c, k));
   } else if (c->kind == ABFT_LU) {
     if (pe < n) {
       ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(n - pe), (int)w, 1.0, c->linv, c->ld_t,
@@ -349,9 +384,15 @@ int maintain(abft_ctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t
     ABFT_TRY(gemm(c->st, 'N', 'T', (int)(2 * nbr), (int)w, (int)p, -1.0, c->gcsw + 2 * k, c->ld_cs,
                   c->m + p, c->ld, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
     if (scheme == ABFT_FULL) {
-      ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
-      // row: RSm -= L * rvec, rvec = block-row-k plain sums of L (= R e)
-      ABFT_TRY(gemv_sub(c->st, rows, p, c->m + p, c->ld, c->gcsw + 2 * k, c->ld_cs, c->rsm));
+      if (c->chol_rs_valid) {
+        // running right-looking maintenance (see chol_rs_update): the panel's
+        // row checksums already carry every earlier update
+        ABFT_TRY(copy_matrix(c->st, c->chol_rs + p + k * c->ld, c->ld, c->rsm, c->ld, rows, nbc));
+      } else {
+        ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
+        // row: RSm -= L * rvec, rvec = block-row-k plain sums of L (= R e)
+        ABFT_TRY(gemv_sub(c->st, rows, p, c->m + p, c->ld, c->gcsw + 2 * k, c->ld_cs, c->rsm));
+      }
     }
     return 0;
   }
@@ -477,6 +518,11 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   // (b = 128 / 256); Cholesky's left-looking panel update keeps the pass.
   const bool fuse = prot && c->fuse_enabled && c->kind != ABFT_CHOLESKY && gemm_can_fuse((int)c->b);
   bool fused_done = false;
+  if (c->kind == ABFT_CHOLESKY && k == 0 && (scheme == ABFT_FULL || c->want_chol_rs)) {
+    prof_mark(c, PROF_ABFT, true);
+    ABFT_TRY(chol_rs_encode(c));
+    prof_mark(c, PROF_ABFT, false);
+  }
   if (prot) {
     // encode (abft.py:118-135): reuse the previous verify's sums when the
     // region is a sub-grid of the last verified region (LU/QR), else a pass
@@ -863,7 +909,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   if ((rc = dalloc(&c->rsm, ld * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->gmax, c->ld_max * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->el, c->ld_cs * b))) return fail(rc);
-  if ((rc = dalloc(&c->er, c->ld_t * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->er, c->ld_t * std::max<int64_t>(c->nb, b)))) return fail(rc);
+  if (kind == ABFT_CHOLESKY && (rc = dalloc(&c->chol_rs, ld * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->lw, ld * b))) return fail(rc);
   if ((rc = dalloc(&c->uw, c->ld_t * n_))) return fail(rc);
   if ((rc = dalloc(&c->linv, c->ld_t * b))) return fail(rc);
@@ -909,6 +956,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   DevGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   double* bufs[] = {c->m,     c->a0,     c->gcsw,   c->grs,     c->gmax,  c->csm,  c->rsm,
+                    c->chol_rs,
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
                     c->qr_part2, c->qr_wfin,
@@ -921,8 +969,10 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   if (c->dplan) cudaFree(c->dplan);
   if (c->dlist) cudaFree(c->dlist);
   if (c->info) cudaFree(c->info);
-  for (auto& s : c->snaps)
+  for (auto& s : c->snaps) {
     if (s.m) cudaFree(s.m);
+    if (s.chol_rs) cudaFree(s.chol_rs);
+  }
   for (auto& pe : c->prof_pending) {
     cudaEventDestroy(pe.e0);
     cudaEventDestroy(pe.e1);
@@ -960,6 +1010,7 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->chol_rs_valid = false;
   return 0;
 }
 
@@ -978,6 +1029,7 @@ ABFT_API int abft_reset(abft_ctx* c) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->chol_rs_valid = false;
   return 0;
 }
 
@@ -1074,6 +1126,9 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
   if (n_locs) *n_locs = 0;
   const int64_t k0 = c->k_done;
+  c->want_chol_rs = false;
+  for (int64_t k = k0; k < c->nb; ++k)
+    if ((schemes ? schemes[k] : scheme) == ABFT_FULL) c->want_chol_rs = true;
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
   for (int64_t k = k0; k < c->nb; ++k) {
@@ -1213,6 +1268,12 @@ ABFT_API int abft_snapshot(abft_ctx* c, int slot) {
   Snapshot& s = c->snaps[slot];
   if (!s.m) ABFT_TRY(dalloc(&s.m, c->ld * c->n));
   CUDA_TRY(cudaMemcpyAsync(s.m, c->m, c->ld * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  if (c->chol_rs) {
+    if (!s.chol_rs) ABFT_TRY(dalloc(&s.chol_rs, c->ld * c->nb));
+    CUDA_TRY(cudaMemcpyAsync(s.chol_rs, c->chol_rs, c->ld * c->nb * 8, cudaMemcpyDeviceToDevice,
+                             c->st));
+  }
+  s.chol_rs_valid = c->chol_rs_valid;
   s.k_done = c->k_done;
   s.qr_count = c->qr_count;
   s.used = true;
@@ -1227,6 +1288,10 @@ ABFT_API int abft_restore(abft_ctx* c, int slot) {
   }
   Snapshot& s = c->snaps[slot];
   CUDA_TRY(cudaMemcpyAsync(c->m, s.m, c->ld * c->n * 8, cudaMemcpyDeviceToDevice, c->st));
+  if (c->chol_rs && s.chol_rs)
+    CUDA_TRY(cudaMemcpyAsync(c->chol_rs, s.chol_rs, c->ld * c->nb * 8, cudaMemcpyDeviceToDevice,
+                             c->st));
+  c->chol_rs_valid = s.chol_rs_valid && s.chol_rs != nullptr;
   c->k_done = s.k_done;
   c->qr_count = s.qr_count;
   c->sums_valid = false;
