@@ -37,10 +37,12 @@ struct Acc {
 };
 
 // mode 0: LU without pivoting (L unit lower \ U upper in place),
-//         Linv = L^{-1}, Uinv = U^{-1}.
-// mode 1: Cholesky, L lower in place with the strict upper part zeroed,
-//         Linv = L^{-1}.
-// info: 0, or 1 + local column of the first breakdown.
+//         Linv = L^{-1}, Uinv = U^{-1} (formed by tri_inverse_kernel).
+// mode 1: Cholesky, L lower in place with the strict upper part zeroed.
+// info: 1 + global column of the first breakdown (atomicCAS, first wins).
+// 512 threads viewed as 16 warps x 32 lanes: lanes walk rows, warps walk
+// columns (no integer division in the inner loops); the trailing update of
+// each 32-column sub-panel is register-blocked (7 rows x 2 columns / thread).
 __global__ void __launch_bounds__(DT, 1)
     diag_factor_kernel(double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
                        double* Uinv, int64_t ldu, int* info, int64_t col_base) {
@@ -48,17 +50,15 @@ __global__ void __launch_bounds__(DT, 1)
   double* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
   double* Rs = sm + NBK * PLD;     // [224][33]   Rs[c*33 + i]
   __shared__ int s_bad;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   if (tid == 0) s_bad = 0;
   __syncthreads();
 
   for (int jb = 0; jb < w; jb += NBK) {
     const int jw = min(NBK, w - jb);
     const int rem = w - jb;
-    for (int idx = tid; idx < rem * jw; idx += DT) {
-      const int r = idx % rem, c = idx / rem;
-      Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
-    }
+    for (int c = ty; c < jw; c += DT / 32)
+      for (int r = tx; r < rem; r += 32) Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
     __syncthreads();
     for (int c = 0; c < jw; ++c) {
       const double piv = Ps[c * PLD + c];
@@ -66,7 +66,6 @@ __global__ void __launch_bounds__(DT, 1)
       if (bad) {
         if (tid == 0) {
           s_bad = jb + c + 1;
-          // first breakdown wins: 1 + global column
           atomicCAS(info, 0, (int)(col_base + jb + c + 1));
         }
         break;  // uniform: every thread saw the same pivot
@@ -75,75 +74,88 @@ __global__ void __launch_bounds__(DT, 1)
       if (mode == 0) {
         for (int r = c + 1 + tid; r < rem; r += DT) Ps[c * PLD + r] /= piv;
         __syncthreads();
-        const int nr = rem - c - 1, ncc = jw - c - 1;
-        for (int idx = tid; idx < nr * ncc; idx += DT) {
-          const int r = c + 1 + idx % nr, cc = c + 1 + idx / nr;
-          Ps[cc * PLD + r] -= Ps[c * PLD + r] * Ps[cc * PLD + c];
+        for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
+          const double u = Ps[cc * PLD + c];
+          for (int r = c + 1 + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
         }
       } else {
         const double d = sqrt(piv);
         for (int r = c + tid; r < rem; r += DT) Ps[c * PLD + r] = (r == c) ? d : Ps[c * PLD + r] / d;
         __syncthreads();
-        const int nr = rem - c - 1, ncc = jw - c - 1;
-        for (int idx = tid; idx < nr * ncc; idx += DT) {
-          const int r = c + 1 + idx % nr, cc = c + 1 + idx / nr;
-          if (r >= cc) Ps[cc * PLD + r] -= Ps[c * PLD + r] * Ps[c * PLD + cc];
+        for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
+          const double u = Ps[c * PLD + cc];
+          for (int r = cc + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
         }
       }
       __syncthreads();
     }
     __syncthreads();
     if (s_bad) return;
-    for (int idx = tid; idx < rem * jw; idx += DT) {
-      const int r = idx % rem, c = idx / rem;
-      if (mode == 0 || r >= c) D[(jb + r) + (int64_t)(jb + c) * ld] = Ps[c * PLD + r];
-    }
+    for (int c = ty; c < jw; c += DT / 32)
+      for (int r = tx; r < rem; r += 32)
+        if (mode == 0 || r >= c) D[(jb + r) + (int64_t)(jb + c) * ld] = Ps[c * PLD + r];
     __syncthreads();
     const int ncols = w - jb - jw;
-    if (ncols > 0) {
-      if (mode == 0) {
-        for (int idx = tid; idx < jw * ncols; idx += DT) {
-          const int i = idx % jw, c = idx / jw;
-          Rs[c * 33 + i] = D[(jb + i) + (int64_t)(jb + jw + c) * ld];
+    if (ncols <= 0) continue;
+    const double* Rop;  // right operand of the trailing update: R[l][c] = Rop[c*ldr + l]
+    int ldr;
+    if (mode == 0) {
+      // U row block: R = L11^{-1} D[jb:jb+jw, jb+jw:w] (unit lower), one column per thread
+      for (int c = ty; c < ncols; c += DT / 32)
+        for (int i = tx; i < jw; i += 32) Rs[c * 33 + i] = D[(jb + i) + (int64_t)(jb + jw + c) * ld];
+      __syncthreads();
+      for (int c = tid; c < ncols; c += DT) {
+        for (int i = 1; i < jw; ++i) {
+          double x = Rs[c * 33 + i];
+          for (int l = 0; l < i; ++l) x -= Ps[l * PLD + i] * Rs[c * 33 + l];
+          Rs[c * 33 + i] = x;
         }
-        __syncthreads();
-        for (int c = tid; c < ncols; c += DT) {
-          for (int i = 1; i < jw; ++i) {
-            double x = Rs[c * 33 + i];
-            for (int l = 0; l < i; ++l) x -= Ps[l * PLD + i] * Rs[c * 33 + l];
-            Rs[c * 33 + i] = x;
-          }
+      }
+      __syncthreads();
+      for (int c = ty; c < ncols; c += DT / 32)
+        for (int i = tx; i < jw; i += 32) D[(jb + i) + (int64_t)(jb + jw + c) * ld] = Rs[c * 33 + i];
+      Rop = Rs;
+      ldr = 33;
+    } else {
+      // Cholesky: R[l][c] = L21[c][l] = Ps[l*PLD + jw + c]  -> stage transposed in Rs
+      for (int c = ty; c < ncols; c += DT / 32)
+        for (int i = tx; i < jw; i += 32) Rs[c * 33 + i] = Ps[i * PLD + jw + c];
+      __syncthreads();
+      Rop = Rs;
+      ldr = 33;
+    }
+    // trailing update D[jb+jw+r, jb+jw+c] -= sum_l P21[r][l] * R[l][c]
+    const int nr = rem - jw;
+    for (int c0 = 2 * ty; c0 < ncols; c0 += DT / 16) {
+      double acc[7][2];
+#pragma unroll
+      for (int i = 0; i < 7; ++i) acc[i][0] = acc[i][1] = 0.0;
+      const bool c1ok = c0 + 1 < ncols;
+      for (int l = 0; l < jw; ++l) {
+        const double r0v = Rop[c0 * ldr + l];
+        const double r1v = c1ok ? Rop[(c0 + 1) * ldr + l] : 0.0;
+#pragma unroll
+        for (int i = 0; i < 7; ++i) {
+          const int r = tx + 32 * i;
+          const double pv = (r < nr) ? Ps[l * PLD + jw + r] : 0.0;
+          acc[i][0] = fma(pv, r0v, acc[i][0]);
+          acc[i][1] = fma(pv, r1v, acc[i][1]);
         }
-        __syncthreads();
-        for (int idx = tid; idx < jw * ncols; idx += DT) {
-          const int i = idx % jw, c = idx / jw;
-          D[(jb + i) + (int64_t)(jb + jw + c) * ld] = Rs[c * 33 + i];
-        }
-        const int nr = rem - jw;
-        for (int idx = tid; idx < nr * ncols; idx += DT) {
-          const int r = idx % nr, c = idx / nr;
-          double acc = 0.0;
-          for (int l = 0; l < jw; ++l) acc += Ps[l * PLD + jw + r] * Rs[c * 33 + l];
-          D[(jb + jw + r) + (int64_t)(jb + jw + c) * ld] -= acc;
-        }
-      } else {
-        const int nr = rem - jw;
-        for (int idx = tid; idx < nr * ncols; idx += DT) {
-          const int r = idx % nr, c = idx / nr;
-          if (r < c) continue;
-          double acc = 0.0;
-          for (int l = 0; l < jw; ++l) acc += Ps[l * PLD + jw + r] * Ps[l * PLD + jw + c];
-          D[(jb + jw + r) + (int64_t)(jb + jw + c) * ld] -= acc;
-        }
+      }
+#pragma unroll
+      for (int i = 0; i < 7; ++i) {
+        const int r = tx + 32 * i;
+        if (r >= nr) continue;
+        if (mode == 0 || r >= c0) D[(jb + jw + r) + (int64_t)(jb + jw + c0) * ld] -= acc[i][0];
+        if (c1ok && (mode == 0 || r >= c0 + 1))
+          D[(jb + jw + r) + (int64_t)(jb + jw + c0 + 1) * ld] -= acc[i][1];
       }
     }
     __syncthreads();
   }
   if (mode == 1) {
-    for (int idx = tid; idx < w * w; idx += DT) {
-      const int r = idx % w, c = idx / w;
-      if (r < c) D[r + (int64_t)c * ld] = 0.0;
-    }
+    for (int c = ty; c < w; c += DT / 32)
+      for (int r = tx; r < c; r += 32) D[r + (int64_t)c * ld] = 0.0;
   }
 }
 
@@ -151,8 +163,8 @@ __global__ void __launch_bounds__(DT, 1)
 // blockIdx.y = 0: X = L^{-1} (unit lower for LU, non-unit for Cholesky),
 // blockIdx.y = 1: X = U^{-1}, computed as ((U^T)^{-1})^T through transposed
 // accessors. Column block jb of X solves L X[:, jb] = E[:, jb] by block
-// forward substitution; the X column block and the L row-slab of each step
-// are staged in shared memory (no dependent global loads).
+// forward substitution: T = E - L[r0.., c0..r0] X[c0..r0, :] from shared
+// memory (register-blocked), then a right-looking 32x32 solve in parallel.
 __global__ void __launch_bounds__(DT)
     tri_inverse_kernel(const double* D, int64_t ld, int w, int unit_l, double* Linv,
                        int64_t ldl, double* Uinv, int64_t ldu, const int* info) {
@@ -168,45 +180,49 @@ __global__ void __launch_bounds__(DT)
   if (c0 >= w) return;
   const int cw = min(NBK, w - c0);
   double* Xs = sm;                // [w][33]: Xs[r*33 + c] = X(r, c0 + c), rows r >= c0
-  double* Ls = sm + 256 * 33;     // [32][w+1]: Ls[r*257 + l] = L(r0 + r, l)
-  const int tid = threadIdx.x;
+  double* Ls = sm + 256 * 33;     // [32][257]: Ls[r*257 + l] = L(r0 + r, c0 + l)
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   // rows above the diagonal block are zero
-  for (int idx = tid; idx < c0 * cw; idx += DT) {
-    const int r = idx / cw, c = idx % cw;
-    X.at(r, c0 + c) = 0.0;
-  }
+  for (int r = ty; r < c0; r += DT / 32)
+    if (tx < cw) X.at(r, c0 + tx) = 0.0;
   for (int r0 = c0; r0 < w; r0 += NBK) {
     const int rh = min(NBK, w - r0);
-    // stage L(r0.., c0 .. r0+rh)
     const int lw = r0 + rh - c0;
-    for (int idx = tid; idx < rh * lw; idx += DT) {
-      const int r = idx % rh, l = c0 + idx / rh;
-      Ls[r * 257 + l - c0] = (l <= r0 + r) ? L.at(r0 + r, l) : 0.0;
-    }
+    for (int r = ty; r < rh; r += DT / 32)
+      for (int l = tx; l < lw; l += 32)
+        Ls[r * 257 + l] = (c0 + l <= r0 + r) ? L.at(r0 + r, c0 + l) : 0.0;
     __syncthreads();
-    // T = E - L(r0.., c0..r0) X(c0..r0, :)
-    for (int idx = tid; idx < rh * cw; idx += DT) {
-      const int r = idx / cw, c = idx % cw;
-      double acc = (r0 + r == c0 + c) ? 1.0 : 0.0;
-      for (int l = c0; l < r0; ++l) acc -= Ls[r * 257 + (l - c0)] * Xs[(l - c0) * 33 + c];
-      Xs[(r0 - c0 + r) * 33 + c] = acc;
-    }
-    __syncthreads();
-    // solve L(r0.., r0..) X(r0.., :) = T, one thread per column
-    for (int c = tid; c < cw; c += DT) {
-      for (int r = 0; r < rh; ++r) {
-        double x = Xs[(r0 - c0 + r) * 33 + c];
-        for (int l = 0; l < r; ++l) x -= Ls[r * 257 + (r0 + l - c0)] * Xs[(r0 - c0 + l) * 33 + c];
-        if (!unit) x /= Ls[r * 257 + (r0 + r - c0)];
-        Xs[(r0 - c0 + r) * 33 + c] = x;
+    // T = E - L(r0.., c0..r0) X(c0..r0, :): thread (row ty*2+{0,1}, col tx)
+    for (int rr = 2 * ty; rr < rh; rr += DT / 16) {
+      double a0 = (r0 + rr == c0 + tx) ? 1.0 : 0.0;
+      double a1 = (r0 + rr + 1 == c0 + tx) ? 1.0 : 0.0;
+      if (tx < cw) {
+        for (int l = 0; l < r0 - c0; ++l) {
+          const double xv = Xs[l * 33 + tx];
+          a0 -= Ls[rr * 257 + l] * xv;
+          if (rr + 1 < rh) a1 -= Ls[(rr + 1) * 257 + l] * xv;
+        }
+        Xs[(r0 - c0 + rr) * 33 + tx] = a0;
+        if (rr + 1 < rh) Xs[(r0 - c0 + rr + 1) * 33 + tx] = a1;
       }
     }
     __syncthreads();
+    // L(r0..,r0..) Y = T, right-looking: row i final, eliminate it below
+    for (int i = 0; i < rh; ++i) {
+      if (!unit) {
+        if (tid < cw) Xs[(r0 - c0 + i) * 33 + tid] /= Ls[i * 257 + (r0 + i - c0)];
+        __syncthreads();
+      }
+      for (int idx = tid; idx < (rh - i - 1) * 32; idx += DT) {
+        const int r = i + 1 + (idx >> 5), c = idx & 31;
+        if (c < cw)
+          Xs[(r0 - c0 + r) * 33 + c] -= Ls[r * 257 + (r0 + i - c0)] * Xs[(r0 - c0 + i) * 33 + c];
+      }
+      __syncthreads();
+    }
   }
-  for (int idx = tid; idx < (w - c0) * cw; idx += DT) {
-    const int r = c0 + idx / cw, c = idx % cw;
-    X.at(r, c0 + c) = Xs[(r - c0) * 33 + c];
-  }
+  for (int r = c0 + ty; r < w; r += DT / 32)
+    if (tx < cw) X.at(r, c0 + tx) = Xs[(r - c0) * 33 + tx];
 }
 
 }  // namespace
