@@ -73,16 +73,33 @@ def _blocked(x: np.ndarray, b: int) -> np.ndarray:
 def block_sums(x: np.ndarray, b: int):
     """Per-block plain / index-weighted column sums (nbr x cols), row sums
     (rows x nbc) and max|x| (nbr x nbc) of a region (abft.py:124-134, :162).
-    Weights restart at 0 in every block (abft.py:126, :132)."""
+    Weights restart at 0 in every block (abft.py:126, :132). Works one block
+    row at a time on strided views (no copy of the region), like the
+    reference's per-block loops but vectorised across the block row."""
     rows, cols = x.shape
-    t = _blocked(x, b)
-    nbr, _, nbc, _ = t.shape
-    w = np.arange(b, dtype=np.float64)
-    cp = t.sum(axis=1).reshape(nbr, nbc * b)[:, :cols]
-    cw = np.einsum("i,aibj->abj", w, t).reshape(nbr, nbc * b)[:, :cols]
-    rp = t.sum(axis=3).reshape(nbr * b, nbc)[:rows]
-    rw = np.einsum("j,aibj->aib", w, t).reshape(nbr * b, nbc)[:rows]
-    bmax = np.abs(t).max(axis=(1, 3))
+    nbr, nbc = -(-rows // b), -(-cols // b)
+    cp = np.zeros((nbr, cols))
+    cw = np.zeros((nbr, cols))
+    rp = np.zeros((rows, nbc))
+    rw = np.zeros((rows, nbc))
+    bmax = np.zeros((nbr, nbc))
+    wfull = np.arange(b, dtype=np.float64)
+    full_c = (cols // b) * b
+    for bi in range(nbr):
+        r0, r1 = bi * b, min(bi * b + b, rows)
+        blk = x[r0:r1, :]
+        cp[bi] = blk.sum(axis=0)
+        cw[bi] = wfull[:r1 - r0] @ blk
+        if full_c:
+            v3 = blk[:, :full_c].reshape(r1 - r0, full_c // b, b)
+            rp[r0:r1, :full_c // b] = v3.sum(axis=2)
+            rw[r0:r1, :full_c // b] = v3 @ wfull
+            bmax[bi, :full_c // b] = np.abs(v3).max(axis=(0, 2))
+        if full_c < cols:
+            tail = blk[:, full_c:]
+            rp[r0:r1, nbc - 1] = tail.sum(axis=1)
+            rw[r0:r1, nbc - 1] = tail @ wfull[:cols - full_c]
+            bmax[bi, nbc - 1] = np.abs(tail).max()
     return cp, cw, rp, rw, bmax
 
 
