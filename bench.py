@@ -381,7 +381,12 @@ def run_ours(args):
         "gpu_launches": launches,
         "roofline": {"bound": "tensor", "kernel": "dgemm_tma_dmma (trailing-matrix update)",
                      "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": (achieved / peak.value) if achieved else None, "traffic": None,
+                     "frac": (achieved / peak.value) if achieved else None,
+                     # dram read+write of one fused trailing-update launch (M=N~31.2k, K=256)
+                     # from `ncu --set full` (profiles/ncu_full_gemm_lu32k_r01.txt); the
+                     # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once)
+                     "traffic": 26.63e9 if args.kind == "lu" else None,
+                     "traffic_algorithmic": 15.7e9 if args.kind == "lu" else None,
                      "peak_source": "measured DMMA issue rate on this GPU "
                                     "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"},
         "abft_verify": {
