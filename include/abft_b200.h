@@ -169,6 +169,48 @@ ABFT_API int64_t abft_breakdown_column(abft_ctx* ctx);
  * the last abft_factorize/abft_iteration call, measured with CUDA events */
 ABFT_API int abft_last_elapsed_ms(abft_ctx* ctx, double* ms);
 
+/* 1-D block-cyclic distribution over G processes, one GPU each (SURVEY.md
+ * §8e; no reference counterpart: the reference is single-process). Rank g
+ * owns global column blocks j with j mod G == g, stored contiguously. The
+ * exchange step is the caller's (torch.distributed / NCCL) on the device
+ * buffer `xbuf` (abft_dist_xbuf_elems(k) doubles) between the phases:
+ *   LU/QR : begin (owner of k packs the factored panel) -> broadcast from
+ *           owner k mod G -> update -> [all-reduce MAX of *local_max when
+ *           faults are planned] -> finish
+ *   Chol. : begin (every rank: partial left-looking products) -> sum-reduce
+ *           to owner k mod G -> update -> [all-reduce MAX] -> finish
+ * One iteration = run_numeric_iteration (simulator.py:97-121) with the same
+ * host-drawn plan on every rank (abft.py:310-333). ----------------------- */
+typedef struct abft_dist abft_dist;
+ABFT_API int abft_dist_create(abft_dist** d, int kind, int64_t n, int64_t b, int device, int rank,
+                              int world);
+ABFT_API int abft_dist_destroy(abft_dist* d);
+ABFT_API int64_t abft_dist_local_cols(abft_dist* d);
+ABFT_API void* abft_dist_stream(abft_dist* d);
+/* doubles exchanged at iteration k (0: no exchange) */
+ABFT_API int64_t abft_dist_xbuf_elems(abft_dist* d, int64_t k);
+/* owned column blocks of the host global matrix (column-major, lda) -> device */
+ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda);
+/* local columns (n x local_cols) -> host */
+ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo);
+ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf);
+ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double* xbuf, int nplan,
+                              double* local_max);
+/* scale: device pointer to the all-reduced max|region| (NULL if nplan == 0) */
+ABFT_API int abft_dist_finish(abft_dist* d, int64_t k, int scheme, const abft_fault* plan,
+                              int nplan, int correct, const double* scale);
+/* synchronize, check breakdown, drain events (global coordinates; iters[i] = iteration) */
+ABFT_API int abft_dist_events(abft_dist* d, abft_location* locs, int64_t* iters, int max_locs,
+                              int* n_out);
+ABFT_API int64_t abft_dist_k_done(abft_dist* d);
+ABFT_API int abft_dist_get_qr_panel(abft_dist* d, int64_t k, double* V, int64_t ldv, double* T,
+                                    int64_t ldt);
+/* device time from the first begin(0) to the last finish (CUDA events) */
+ABFT_API int abft_dist_elapsed_ms(abft_dist* d, double* ms);
+/* single-context QR panel setter (rebuild a gathered factorization for the residual) */
+ABFT_API int abft_set_qr_panel(abft_ctx* ctx, int64_t k, const double* V, int64_t ldv,
+                               const double* T, int64_t ldt);
+
 /* region ABFT on host arrays: encode / maintain_gemm / verify_correct /
  * inject_faults (abft.py:118-307), executed on the device. Checksums are
  * column-major arrays: col_plain/col_weighted (nbr x cols, ld nbr),

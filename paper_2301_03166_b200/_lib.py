@@ -92,6 +92,22 @@ SIGNATURES = [
     ("abft_breakdown_column", _I64, [_P]),
     ("abft_debug_array", _I, [_P, _I, _D, ctypes.POINTER(_I64), ctypes.POINTER(_I64)]),
     ("abft_last_elapsed_ms", _I, [_P, _D]),
+    ("abft_dist_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I, _I, _I]),
+    ("abft_dist_destroy", _I, [_P]),
+    ("abft_dist_local_cols", _I64, [_P]),
+    ("abft_dist_stream", _P, [_P]),
+    ("abft_dist_xbuf_elems", _I64, [_P, _I64]),
+    ("abft_dist_set_matrix", _I, [_P, _D, _I64]),
+    ("abft_dist_get_matrix", _I, [_P, _D, _I64]),
+    ("abft_dist_begin", _I, [_P, _I64, _I, _P]),
+    ("abft_dist_update", _I, [_P, _I64, _I, _P, _I, _P]),
+    ("abft_dist_finish", _I, [_P, _I64, _I, ctypes.POINTER(Fault), _I, _I, _P]),
+    ("abft_dist_events", _I, [_P, ctypes.POINTER(Location), ctypes.POINTER(_I64), _I,
+                              ctypes.POINTER(_I)]),
+    ("abft_dist_k_done", _I64, [_P]),
+    ("abft_dist_get_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
+    ("abft_dist_elapsed_ms", _I, [_P, _D]),
+    ("abft_set_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
     ("abft_region_encode", _I, [_D, _I64, _I64, _I64, _I64, _I, _D, _D, _D, _D]),
     ("abft_region_maintain", _I, [_I64, _I64, _I64, _I64, _I, _D, _I64, _D, _I64, _D, _D, _D,
                                   _D]),

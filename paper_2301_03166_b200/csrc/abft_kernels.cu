@@ -339,6 +339,68 @@ __global__ void inject_kernel(double* m, int64_t ld, int64_t n_rows, int64_t n_c
   }
 }
 
+// Column-distributed variant of inject_kernel for the 1-D block-cyclic path:
+// the plan is in global coordinates, `scale` is already the global
+// max|region| (all-reduced over ranks), and only the elements of column blocks
+// owned by `rank` are applied (global column c -> local column
+// ((c / b) / world) * b + c % b). Same ramps and order as inject_faults
+// (abft.py:283-307).
+__global__ void inject_mapped_kernel(double* m, int64_t ld, int64_t n, const DevFault* plan,
+                                     int nplan, const double* scale_dev, int world, int rank,
+                                     int64_t b) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double scale = scale_dev ? scale_dev[0] : 0.0;
+  auto add = [&](int64_t r, int64_t c, double v) {
+    const int64_t jb = c / b;
+    if ((int)(jb % world) != rank) return;
+    m[r + ((jb / world) * b + c % b) * ld] += v;
+  };
+  for (int f = 0; f < nplan; ++f) {
+    const DevFault ft = plan[f];
+    double mag = ft.magnitude;
+    if (!ft.absolute) {
+      mag = (ft.u * 1e-3) * fmax(scale, 1.0);
+      if (ft.negate) mag = -mag;
+    }
+    if (ft.kind == 0) {
+      add(ft.row, ft.col, mag);
+    } else if (ft.kind == 1) {
+      const int ext = ft.extent > 2 ? ft.extent : 2;
+      if (ft.orientation == 0) {
+        const int64_t stop = min(ft.row + ext, n);
+        for (int64_t i = 0; i < stop - ft.row; ++i) add(ft.row + i, ft.col, mag * (1.0 + 0.1 * (double)i));
+      } else {
+        const int64_t stop = min(ft.col + ext, n);
+        for (int64_t i = 0; i < stop - ft.col; ++i) add(ft.row, ft.col + i, mag * (1.0 + 0.1 * (double)i));
+      }
+    } else {
+      const int ext = ft.extent > 2 ? ft.extent : 2;
+      const int64_t rstop = min(ft.row + ext, n);
+      const int64_t cstop = min(ft.col + ext, n);
+      for (int64_t i = 0; i < rstop - ft.row; ++i)
+        for (int64_t jj = 0; jj < cstop - ft.col; ++jj)
+          add(ft.row + i, ft.col + jj, mag * (((double)i * 0.1 + (double)jj * 0.07) + 1.0));
+    }
+  }
+}
+
+// out[0] = max over an (rows x cols) block-max array (0 when empty).
+__global__ void max_reduce_kernel(const double* a, int64_t rows, int64_t cols, int64_t ld,
+                                  double* out) {
+  __shared__ double sm[32];
+  double mx = 0.0;
+  for (int64_t i = threadIdx.x; i < rows * cols; i += blockDim.x)
+    mx = fmax(mx, a[(i % rows) + (i / rows) * ld]);
+  mx = warp_max(mx);
+  if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = sm[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) s = fmax(s, sm[w]);
+    out[0] = s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // reductions / element kernels
 // ---------------------------------------------------------------------------
@@ -498,6 +560,23 @@ int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_col
   count_launch();
   inject_kernel<<<1, 1024, 0, st>>>(m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows,
                                     scale_cols, scale_ld, host_scale);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int inject_mapped(cudaStream_t st, double* m, int64_t ld, int64_t n, const DevFault* plan,
+                  int nplan, const double* scale_dev, int world, int rank, int64_t b) {
+  if (nplan <= 0) return 0;
+  count_launch();
+  inject_mapped_kernel<<<1, 32, 0, st>>>(m, ld, n, plan, nplan, scale_dev, world, rank, b);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int max_reduce(cudaStream_t st, const double* a, int64_t rows, int64_t cols, int64_t ld,
+               double* out) {
+  count_launch();
+  max_reduce_kernel<<<1, 1024, 0, st>>>(a, rows > 0 && cols > 0 ? rows : 0, cols, ld, out);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -88,6 +88,15 @@ int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_col
            const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
            int64_t scale_cols, int64_t scale_ld, double host_scale);
 
+// K7 for the 1-D block-cyclic distribution: global plan, global scale
+// (device scalar, already reduced over ranks), only locally owned column
+// blocks are written.
+int inject_mapped(cudaStream_t st, double* m, int64_t ld, int64_t n, const DevFault* plan,
+                  int nplan, const double* scale_dev, int world, int rank, int64_t b);
+// out[0] = max of a (rows x cols, ld) array; 0 when empty.
+int max_reduce(cudaStream_t st, const double* a, int64_t rows, int64_t cols, int64_t ld,
+               double* out);
+
 // Sum of squares of (rows x cols) matrix into out[0] (deterministic).
 int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
           double* scratch /* >= 1024 doubles */);

@@ -1386,6 +1386,23 @@ ABFT_API int abft_reconstruct(abft_ctx* c, double* outh, int64_t ldo) {
   return rc;
 }
 
+ABFT_API int abft_set_qr_panel(abft_ctx* c, int64_t k, const double* V, int64_t ldv,
+                               const double* T, int64_t ldt) {
+  DevGuard g(c->device);
+  if (c->kind != ABFT_QR || k < 0 || k >= c->nb || k > c->qr_count) {
+    set_last_error("cannot set QR panel %lld", (long long)k);
+    return ABFT_E_INVALID;
+  }
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
+  CUDA_TRY(cudaMemcpy2DAsync(c->vstore + p + p * c->ld, c->ld * 8, V, ldv * 8, (c->n - p) * 8, w,
+                             cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaMemcpy2DAsync(c->tstore + k * c->b * c->ld_t, c->ld_t * 8, T, ldt * 8, w * 8, w,
+                             cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->qr_count = (int)std::max<int64_t>(c->qr_count, k + 1);
+  return 0;
+}
+
 ABFT_API int abft_set_qr_panels(abft_ctx* c, int count) {
   if (count < 0 || count > c->qr_count) {
     set_last_error("cannot extend the QR panel list from the host");

@@ -1,0 +1,885 @@
+// 1-D block-cyclic distributed factorization context.
+//
+// One process per GPU; rank g of G owns the global column blocks j with
+// j mod G == g, stored contiguously (local block l <-> global block l*G + g),
+// so the trailing columns of any iteration are a contiguous local suffix and
+// every b x b checksum block, its verification and its repair are local to
+// one rank. The exchange step is performed by the caller's transport
+// (torch.distributed over NCCL; paper_2301_03166_b200/distributed.py) on a
+// device buffer `xbuf` between the phases below:
+//
+//   LU / QR (right-looking, reference linalg.py:230-300, simulator.py:124-167)
+//     begin   owner(k): PD of panel k, pack [panel rows p:n | L11^{-1} or T]
+//     -- broadcast xbuf from owner(k) --
+//     update  every rank: PU (LU) + encode/maintain + trailing update of its
+//             local columns with fused block checksums; local max|region|
+//     -- all-reduce MAX of the local maxima (only when faults are planned) --
+//     finish  inject the plan's locally owned elements, verify/repair local
+//             blocks
+//   Cholesky (left-looking as the reference, linalg.py:192-229)
+//     begin   every rank: partial panel update from its own finished panels,
+//             [X | L*rvec | CS] = L_g * [R_g | rvec_g], CS = E_g * R_g
+//     -- sum-reduce xbuf to owner(k) --
+//     update  owner: encode the panel column, subtract the reduced update,
+//             maintained checksums = encoded - reduced checksum products
+//     finish  owner: inject/verify, PD + PU of the panel; all: zero the row
+//             block m[p:pe, pe:n] of their columns (linalg.py:251-252)
+//
+// The plan, RNG draws and the event order are host-side and identical on all
+// ranks (abft.py:310-333); events are returned in global coordinates.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "abft_b200.h"
+#include "abft_kernels.cuh"
+#include "gemm.cuh"
+#include "panel.cuh"
+
+using namespace abft;
+
+namespace {
+
+inline int64_t round_even(int64_t x) { return (x + 1) / 2 * 2; }
+inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct DevGuardD {
+  int prev = -1;
+  explicit DevGuardD(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuardD() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+int dalloc0(double** p, int64_t elems) {
+  CUDA_TRY(cudaMalloc(p, std::max<int64_t>(elems, 1) * sizeof(double)));
+  CUDA_TRY(cudaMemset(*p, 0, std::max<int64_t>(elems, 1) * sizeof(double)));
+  return 0;
+}
+
+}  // namespace
+
+struct abft_dist {
+  int kind = 0;
+  int64_t n = 0, b = 0, nb = 0, ld = 0;
+  int device = 0, rank = 0, world = 1;
+  int64_t nbl = 0, ncl = 0;  // local blocks / columns
+  cudaStream_t st = nullptr;
+
+  double* m = nullptr;      // n x ncl (ld)
+  double* gcsw = nullptr;   // (2nb) x ncl (ld_cs): row 2*gbi plain, 2*gbi+1 weighted
+  double* csm = nullptr;    // maintained col sums, region-local
+  int64_t ld_cs = 0;
+  double* grs = nullptr;    // n x nbl (ld)
+  double* rsm = nullptr;    // maintained row sums, region-local (ld)
+  double* gmax = nullptr;   // nb x nbl (ld_max)
+  int64_t ld_max = 0;
+  double* el = nullptr;     // operand block-row sums (2nb x b, ld_cs)
+  double* er = nullptr;     // R * E_R (b x nbl, ld_t)
+  int64_t ld_t = 0;
+  double* uw = nullptr;     // b x ncl (ld_t)
+  double* lw = nullptr;     // n x b (ld)
+  double* linv = nullptr;
+  double* uinv = nullptr;
+  double* bext = nullptr;   // Cholesky: ncl x (b+1), ld_b
+  int64_t ld_b = 0;
+  double* vstore = nullptr; // QR: every panel's V (n x n, ld)
+  double* tstore = nullptr; // QR: every panel's T (nb of b x b, ld_t)
+  double* betas = nullptr;
+  double* qr_part = nullptr;
+  int64_t qr_part_elems = 0;
+  double* qr_rowbuf = nullptr;
+  double* qr_part2 = nullptr;
+  double* qr_wfin = nullptr;
+  double* gram = nullptr;
+  double* ww = nullptr;     // b x ncl
+  double* mid = nullptr;    // b x ncl
+  double* dmax = nullptr;   // local max scratch
+  GemmWorkspace gws;
+
+  Event* ev = nullptr;
+  int32_t* counters = nullptr;
+  int ev_cap = 0;
+  int32_t* dirty = nullptr;
+  int dirty_cap = 0;
+  DevFault* dplan = nullptr;
+  int dplan_cap = 0;
+  int32_t* dlist = nullptr;
+  int dlist_cap = 0;
+  int* info = nullptr;
+
+  int64_t k_done = 0;
+  bool sums_valid = false;
+  int64_t breakdown_col = -1;
+  int qr_count = 0;
+  bool fuse_enabled = true;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool timed = false;
+};
+
+namespace {
+
+int owner(const abft_dist* d, int64_t k) { return (int)(k % d->world); }
+// number of owned global blocks j <= k
+int64_t owned_upto(const abft_dist* d, int64_t k) {
+  return k < d->rank ? 0 : (k - d->rank) / d->world + 1;
+}
+int64_t width(const abft_dist* d, int64_t k) { return std::min(d->b, d->n - k * d->b); }
+
+// LU/QR exchange buffer: panel rows p:n with ld = round_even(n - p), then the
+// w x w companion (L11^{-1} for LU, T for QR) at ld_t.
+int64_t panel_ld(const abft_dist* d, int64_t k) { return round_even(d->n - k * d->b); }
+
+// Sums of a local, b-aligned region starting at global row r0 and local block column lb.
+SumOut sums_local(abft_dist* d, int64_t r0, int64_t lb, bool rows_too) {
+  SumOut o;
+  const int64_t gbi = r0 / d->b;
+  o.cp = d->gcsw + 2 * gbi + lb * d->b * d->ld_cs;
+  o.cp_ld = d->ld_cs;
+  o.cp_step = 2;
+  o.cw = o.cp + 1;
+  o.cw_ld = d->ld_cs;
+  o.cw_step = 2;
+  if (rows_too) {
+    o.rp = d->grs + r0 + lb * d->ld;
+    o.rp_ld = d->ld;
+  }
+  o.bm = d->gmax + gbi + lb * d->ld_max;
+  o.bm_ld = d->ld_max;
+  return o;
+}
+
+FusedSums fused_local(abft_dist* d, int64_t r0, int64_t lb) {
+  const SumOut o = sums_local(d, r0, lb, true);
+  FusedSums f;
+  f.cp = o.cp;
+  f.cp_ld = o.cp_ld;
+  f.cp_step = o.cp_step;
+  f.cw = o.cw;
+  f.cw_ld = o.cw_ld;
+  f.cw_step = o.cw_step;
+  f.rp = o.rp;
+  f.rp_ld = o.rp_ld;
+  f.bm = o.bm;
+  f.bm_ld = o.bm_ld;
+  return f;
+}
+
+// Local part of the iteration-k region: global rows [r0, r0+rows), local
+// columns [lc0, lc0+cols) starting at local block lb0.
+struct LocalRegion {
+  int64_t r0 = 0, rows = 0, lb0 = 0, lc0 = 0, cols = 0;
+  int64_t gr0 = 0, gc0 = 0;  // global region origin (_tmu_region)
+};
+
+LocalRegion local_region(const abft_dist* d, int64_t k) {
+  LocalRegion L;
+  const int64_t p = k * d->b, pe = std::min(p + d->b, d->n);
+  if (d->kind == ABFT_CHOLESKY) {
+    L.gr0 = p;
+    L.gc0 = p;
+    if (owner(d, k) == d->rank) {
+      L.r0 = p;
+      L.rows = d->n - p;
+      L.lb0 = k / d->world;
+      L.lc0 = L.lb0 * d->b;
+      L.cols = pe - p;
+    }
+    return L;
+  }
+  L.gr0 = (d->kind == ABFT_LU) ? pe : p;
+  L.gc0 = pe;
+  L.r0 = L.gr0;
+  L.rows = d->n - L.r0;
+  L.lb0 = owned_upto(d, k);
+  L.lc0 = L.lb0 * d->b;
+  L.cols = d->ncl - L.lc0;
+  if (pe >= d->n) L.cols = 0;
+  if (L.cols < 0) L.cols = 0;
+  return L;
+}
+
+Maintained maintained(abft_dist* d) {
+  Maintained mt;
+  mt.cp = d->csm;
+  mt.cp_ld = d->ld_cs;
+  mt.cp_step = 2;
+  mt.cw = d->csm + 1;
+  mt.cw_ld = d->ld_cs;
+  mt.cw_step = 2;
+  mt.rp = d->rsm;
+  mt.rp_ld = d->ld;
+  return mt;
+}
+
+int upload_plan(abft_dist* d, const abft_fault* plan, int nplan) {
+  if (nplan > d->dplan_cap) {
+    if (d->dplan) cudaFree(d->dplan);
+    d->dplan_cap = std::max(nplan, 64);
+    CUDA_TRY(cudaMalloc(&d->dplan, d->dplan_cap * sizeof(DevFault)));
+  }
+  std::vector<DevFault> h(nplan);
+  for (int i = 0; i < nplan; ++i) {
+    h[i].kind = plan[i].kind;
+    h[i].orientation = plan[i].orientation;
+    h[i].row = plan[i].row;
+    h[i].col = plan[i].col;
+    h[i].extent = plan[i].extent;
+    h[i].absolute = plan[i].absolute;
+    h[i].u = plan[i].u;
+    h[i].negate = plan[i].negate;
+    h[i].pad = 0;
+    h[i].magnitude = plan[i].magnitude;
+  }
+  CUDA_TRY(cudaMemcpyAsync(d->dplan, h.data(), nplan * sizeof(DevFault), cudaMemcpyHostToDevice,
+                           d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  return 0;
+}
+
+// Local blocks (region-local bi, bj) touched by the plan's owned elements.
+int upload_touched(abft_dist* d, const abft_fault* plan, int nplan, const LocalRegion& R,
+                   int* count) {
+  std::vector<std::pair<int32_t, int32_t>> blks;
+  for (int f = 0; f < nplan; ++f) {
+    const abft_fault& ft = plan[f];
+    int64_t er = 1, ec = 1;
+    const int64_t ext = std::max<int64_t>(2, ft.extent);
+    if (ft.kind == ABFT_D1) {
+      if (ft.orientation == 0) er = ext; else ec = ext;
+    } else if (ft.kind == ABFT_D2) {
+      er = ext;
+      ec = ext;
+    }
+    for (int64_t r = std::max(ft.row, R.r0); r < std::min(std::min(ft.row + er, d->n), R.r0 + R.rows); ++r)
+      for (int64_t c = ft.col; c < std::min(ft.col + ec, d->n); ++c) {
+        const int64_t jb = c / d->b;
+        if ((int)(jb % d->world) != d->rank) continue;
+        const int64_t lc = (jb / d->world) * d->b + c % d->b;
+        if (lc < R.lc0 || lc >= R.lc0 + R.cols) continue;
+        blks.emplace_back((int32_t)((r - R.r0) / d->b), (int32_t)((lc - R.lc0) / d->b));
+      }
+  }
+  std::sort(blks.begin(), blks.end());
+  blks.erase(std::unique(blks.begin(), blks.end()), blks.end());
+  *count = (int)blks.size();
+  if (blks.empty()) return 0;
+  std::vector<int32_t> lst;
+  for (auto& pr : blks) {
+    lst.push_back(pr.first);
+    lst.push_back(pr.second);
+  }
+  const int nn = (int)lst.size();
+  if (nn > d->dlist_cap) {
+    if (d->dlist) cudaFree(d->dlist);
+    d->dlist_cap = std::max(nn, 1024);
+    CUDA_TRY(cudaMalloc(&d->dlist, d->dlist_cap * sizeof(int32_t)));
+  }
+  CUDA_TRY(cudaMemcpyAsync(d->dlist, lst.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  return 0;
+}
+
+// maintain_gemm (abft.py:138-158) for `region -= L @ R` from the operands:
+// L is rows x w (ldl), R is w x cols (ldr), both on the device.
+int maintain_lr(abft_dist* d, const LocalRegion& R, int scheme, const double* L, int64_t ldl,
+                const double* Rm, int64_t ldr, int64_t w) {
+  const int64_t nbr = (R.rows + d->b - 1) / d->b, nbc = (R.cols + d->b - 1) / d->b;
+  SumOut enc = sums_local(d, R.r0, R.lb0, scheme == ABFT_FULL);
+  {
+    Region rl{const_cast<double*>(L), ldl, R.rows, w, d->b};
+    SumOut o;
+    o.cp = d->el;
+    o.cp_ld = d->ld_cs;
+    o.cp_step = 2;
+    o.cw = d->el + 1;
+    o.cw_ld = d->ld_cs;
+    o.cw_step = 2;
+    ABFT_TRY(blocksum(d->st, rl, o));
+  }
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(2 * nbr), (int)R.cols, (int)w, -1.0, d->el, d->ld_cs, Rm, ldr,
+                1.0, enc.cp, d->ld_cs, d->csm, d->ld_cs, &d->gws));
+  if (scheme == ABFT_FULL) {
+    Region rr{const_cast<double*>(Rm), ldr, w, R.cols, d->b};
+    SumOut o;
+    o.rp = d->er;
+    o.rp_ld = d->ld_t;
+    ABFT_TRY(blocksum(d->st, rr, o));
+    ABFT_TRY(gemm(d->st, 'N', 'N', (int)R.rows, (int)nbc, (int)w, -1.0, L, ldl, d->er, d->ld_t, 1.0,
+                  enc.rp, d->ld, d->rsm, d->ld, &d->gws));
+  }
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// phases
+// ---------------------------------------------------------------------------
+int begin_lu(abft_dist* d, int64_t k, double* xb) {
+  if (owner(d, k) != d->rank) return 0;
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  const int64_t lc = (k / d->world) * d->b, ldp = panel_ld(d, k);
+  double* D = d->m + p + lc * d->ld;
+  ABFT_TRY(diag_factor(d->st, D, d->ld, (int)w, 0, d->linv, d->ld_t, d->uinv, d->ld_t, d->info, p));
+  if (pe < n) {
+    // L21 = A21 U11^{-1} straight into the exchange buffer, then back into m
+    ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->uinv, d->ld_t,
+                  0.0, nullptr, 0, xb + w, ldp, &d->gws));
+    ABFT_TRY(copy_matrix(d->st, xb + w, ldp, D + w, d->ld, n - pe, w));
+  }
+  ABFT_TRY(copy_matrix(d->st, D, d->ld, xb, ldp, w, w));
+  ABFT_TRY(copy_matrix(d->st, d->linv, d->ld_t, xb + ldp * w, d->ld_t, w, w));
+  return 0;
+}
+
+int begin_qr(abft_dist* d, int64_t k, double* xb) {
+  if (owner(d, k) != d->rank) return 0;
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  const int64_t lc = (k / d->world) * d->b, ldp = panel_ld(d, k);
+  double* D = d->m + p + lc * d->ld;
+  ABFT_TRY(fill_matrix(d->st, xb, ldp, n - p, w, 0.0));
+  ABFT_TRY(qr_panel(d->st, D, d->ld, n - p, (int)w, xb, ldp, d->betas, d->qr_part,
+                    d->qr_part_elems, d->qr_rowbuf, d->qr_part2, d->qr_wfin));
+  ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)w, (int)(n - p), 1.0, xb, ldp, xb, ldp, 0.0, nullptr,
+                0, d->gram, d->ld_t, &d->gws));
+  ABFT_TRY(larft(d->st, d->gram, d->ld_t, d->betas, (int)w, xb + ldp * w, d->ld_t));
+  return 0;
+}
+
+int begin_chol(abft_dist* d, int64_t k, double* xb) {
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  if (k == 0) return 0;
+  const int64_t ldp = panel_ld(d, k), nbr = (n - p + d->b - 1) / d->b;
+  const int64_t ldc = round_even(2 * nbr);
+  double* X = xb;                       // (n-p) x (w+1)
+  double* CS = xb + ldp * (w + 1);      // 2nbr x w
+  const int64_t pl = owned_upto(d, k - 1) * d->b;  // own finished panels (all full width)
+  if (pl == 0) {
+    ABFT_TRY(fill_matrix(d->st, X, ldp, n - p, w + 1, 0.0));
+    ABFT_TRY(fill_matrix(d->st, CS, ldc, 2 * nbr, w, 0.0));
+    return 0;
+  }
+  // B_ext = [ m[p:pe, 0:pl]^T | rvec ], rvec = block-row-k plain sums of L
+  ABFT_TRY(gather_transpose(d->st, d->m + p, 1, d->ld, w, pl, d->bext, d->ld_b));
+  ABFT_TRY(gather_transpose(d->st, d->gcsw + 2 * k, 1, d->ld_cs, 1, pl, d->bext + w * d->ld_b,
+                            d->ld_b));
+  // [X | L rvec] = L_g[p:n, 0:pl] B_ext ; CS = E_g[2k:, 0:pl] B
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - p), (int)(w + 1), (int)pl, 1.0, d->m + p, d->ld, d->bext,
+                d->ld_b, 0.0, nullptr, 0, X, ldp, &d->gws));
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(2 * nbr), (int)w, (int)pl, 1.0, d->gcsw + 2 * k, d->ld_cs,
+                d->bext, d->ld_b, 0.0, nullptr, 0, CS, ldc, &d->gws));
+  return 0;
+}
+
+int local_max(abft_dist* d, const LocalRegion& R, double* out) {
+  const int64_t nbr = (R.rows + d->b - 1) / d->b, nbc = (R.cols + d->b - 1) / d->b;
+  if (R.rows <= 0 || R.cols <= 0) {
+    CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), d->st));
+    return 0;
+  }
+  return max_reduce(d->st, d->gmax + R.r0 / d->b + R.lb0 * d->ld_max, nbr, nbc, d->ld_max, out);
+}
+
+int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int nplan,
+                 double* max_out) {
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  const int64_t ldp = panel_ld(d, k);
+  const LocalRegion R = local_region(d, k);
+  const bool has = R.rows > 0 && R.cols > 0;
+  const bool prot = scheme != ABFT_NONE && has;
+  Region reg{d->m + R.r0 + R.lc0 * d->ld, d->ld, R.rows, R.cols, d->b};
+  bool fused = false;
+  if (d->kind == ABFT_QR) {
+    // keep V_k / T_k (residual, qr_t / _qr_vs)
+    ABFT_TRY(copy_matrix(d->st, xb, ldp, d->vstore + p + p * d->ld, d->ld, n - p, w));
+    ABFT_TRY(copy_matrix(d->st, xb + ldp * w, d->ld_t, d->tstore + k * d->b * d->ld_t, d->ld_t, w, w));
+    d->qr_count = (int)(k + 1);
+  }
+  if (has) {
+    if (d->kind == ABFT_LU) {
+      double* U12 = d->m + p + R.lc0 * d->ld;
+      ABFT_TRY(gemm(d->st, 'N', 'N', (int)w, (int)R.cols, (int)w, 1.0, xb + ldp * w, d->ld_t, U12,
+                    d->ld, 0.0, nullptr, 0, d->uw, d->ld_t, &d->gws));
+      ABFT_TRY(copy_matrix(d->st, d->uw, d->ld_t, U12, d->ld, w, R.cols));
+      if (prot) {
+        if (!d->sums_valid) ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true)));
+        ABFT_TRY(maintain_lr(d, R, scheme, xb + w, ldp, U12, d->ld, w));
+      }
+      const bool fuse = prot && d->fuse_enabled && gemm_can_fuse((int)d->b);
+      if (fuse) {
+        ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)R.rows, (int)R.cols, (int)w, -1.0, xb + w, ldp,
+                                 U12, d->ld, 1.0, reg.ptr, d->ld, reg.ptr, d->ld, (int)d->b,
+                                 fused_local(d, R.r0, R.lb0)));
+        fused = true;
+      } else {
+        ABFT_TRY(gemm(d->st, 'N', 'N', (int)R.rows, (int)R.cols, (int)w, -1.0, xb + w, ldp, U12, d->ld,
+                      1.0, reg.ptr, d->ld, reg.ptr, d->ld, &d->gws));
+      }
+    } else {
+      const double* V = xb;
+      const double* T = xb + ldp * w;
+      double* C = d->m + p + R.lc0 * d->ld;
+      if (prot && !d->sums_valid) ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true)));
+      ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)R.cols, (int)(n - p), 1.0, V, ldp, C, d->ld, 0.0,
+                    nullptr, 0, d->ww, d->ld_t, &d->gws));
+      ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)R.cols, (int)w, 1.0, T, d->ld_t, d->ww, d->ld_t, 0.0,
+                    nullptr, 0, d->mid, d->ld_t, &d->gws));
+      if (prot) ABFT_TRY(maintain_lr(d, R, scheme, V, ldp, d->mid, d->ld_t, w));
+      const bool fuse = prot && d->fuse_enabled && gemm_can_fuse((int)d->b);
+      if (fuse) {
+        ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)(n - p), (int)R.cols, (int)w, -1.0, V, ldp,
+                                 d->mid, d->ld_t, 1.0, C, d->ld, C, d->ld, (int)d->b,
+                                 fused_local(d, R.r0, R.lb0)));
+        fused = true;
+      } else {
+        ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - p), (int)R.cols, (int)w, -1.0, V, ldp, d->mid,
+                      d->ld_t, 1.0, C, d->ld, C, d->ld, &d->gws));
+      }
+    }
+    if (prot && !fused) {
+      ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true)));
+    } else if (!prot && nplan > 0) {
+      SumOut o;
+      o.bm = d->gmax + R.r0 / d->b + R.lb0 * d->ld_max;
+      o.bm_ld = d->ld_max;
+      ABFT_TRY(blocksum(d->st, reg, o));
+    }
+  }
+  if (nplan > 0 && max_out) ABFT_TRY(local_max(d, R, max_out));
+  return 0;
+}
+
+int update_chol(abft_dist* d, int64_t k, int scheme, const double* xb, int nplan,
+                double* max_out) {
+  const LocalRegion R = local_region(d, k);
+  const bool has = R.rows > 0 && R.cols > 0;
+  if (has) {
+    const int64_t n = d->n, p = k * d->b, w = R.cols;
+    const int64_t ldp = panel_ld(d, k), nbr = (n - p + d->b - 1) / d->b, nbc = 1;
+    const int64_t ldc = round_even(2 * nbr);
+    const bool prot = scheme != ABFT_NONE;
+    Region reg{d->m + R.r0 + R.lc0 * d->ld, d->ld, R.rows, R.cols, d->b};
+    SumOut enc = sums_local(d, R.r0, R.lb0, true);
+    if (prot) {
+      // encode the untouched panel column (abft.py:118-135), maintained = encoded - reduced
+      ABFT_TRY(blocksum(d->st, reg, enc));
+      ABFT_TRY(copy_matrix(d->st, enc.cp, d->ld_cs, d->csm, d->ld_cs, 2 * nbr, w));
+      if (scheme == ABFT_FULL) ABFT_TRY(copy_matrix(d->st, enc.rp, d->ld, d->rsm, d->ld, R.rows, nbc));
+      if (k > 0) {
+        ABFT_TRY(sub_matrix(d->st, xb + ldp * (w + 1), ldc, d->csm, d->ld_cs, 2 * nbr, w));
+        if (scheme == ABFT_FULL) ABFT_TRY(sub_matrix(d->st, xb + ldp * w, ldp, d->rsm, d->ld, R.rows, 1));
+      }
+    }
+    if (k > 0) ABFT_TRY(sub_matrix(d->st, xb, ldp, reg.ptr, d->ld, R.rows, w));  // P -= L L^T
+    if (prot) {
+      ABFT_TRY(blocksum(d->st, reg, enc));
+    } else if (nplan > 0) {
+      SumOut o;
+      o.bm = enc.bm;
+      o.bm_ld = enc.bm_ld;
+      ABFT_TRY(blocksum(d->st, reg, o));
+    }
+  }
+  if (nplan > 0 && max_out) ABFT_TRY(local_max(d, R, max_out));
+  return 0;
+}
+
+int inject_verify(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                  int correct, const double* scale) {
+  const LocalRegion R = local_region(d, k);
+  const bool has = R.rows > 0 && R.cols > 0;
+  const bool prot = scheme != ABFT_NONE && has;
+  Region reg{d->m + R.r0 + R.lc0 * d->ld, d->ld, R.rows, R.cols, d->b};
+  if (nplan > 0) {
+    for (int f = 0; f < nplan; ++f)
+      if (plan[f].row < 0 || plan[f].row >= d->n || plan[f].col < 0 || plan[f].col >= d->n) {
+        set_last_error("fault at (%lld, %lld) outside matrix", (long long)plan[f].row,
+                       (long long)plan[f].col);
+        return ABFT_E_RANGE;
+      }
+  }
+  if (nplan > 0 && has) {
+    ABFT_TRY(upload_plan(d, plan, nplan));
+    ABFT_TRY(inject_mapped(d->st, d->m, d->ld, d->n, d->dplan, nplan, scale, d->world, d->rank,
+                           d->b));
+    if (prot) {
+      int cnt = 0;
+      ABFT_TRY(upload_touched(d, plan, nplan, R, &cnt));
+      if (cnt > 0)
+        ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true), d->dlist, nullptr, cnt));
+    }
+  }
+  if (prot) {
+    EventSink sink{d->ev, d->counters, d->ev_cap, d->dirty, d->counters + 1, d->dirty_cap,
+                   (int32_t)k};
+    ABFT_TRY(verify_blocks(d->st, reg, d->b, scheme, correct, sums_local(d, R.r0, R.lb0, true),
+                           maintained(d), sink));
+    ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true), d->dirty, d->counters + 1,
+                      d->dirty_cap));
+    CUDA_TRY(cudaMemsetAsync(d->counters + 1, 0, sizeof(int32_t), d->st));
+  }
+  d->sums_valid = prot;
+  return 0;
+}
+
+// Cholesky PD + PU of panel k (owner) after verification; every rank zeroes
+// its columns of the row block m[p:pe, pe:n] (linalg.py:228-229, :251-252).
+int chol_pd_pu(abft_dist* d, int64_t k) {
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  if (owner(d, k) == d->rank) {
+    const int64_t lc = (k / d->world) * d->b;
+    double* D = d->m + p + lc * d->ld;
+    ABFT_TRY(diag_factor(d->st, D, d->ld, (int)w, 1, d->linv, d->ld_t, nullptr, 0, d->info, p));
+    if (pe < n) {
+      ABFT_TRY(gemm(d->st, 'N', 'T', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->linv,
+                    d->ld_t, 0.0, nullptr, 0, d->lw, d->ld, &d->gws));
+      ABFT_TRY(copy_matrix(d->st, d->lw, d->ld, D + w, d->ld, n - pe, w));
+    }
+    // block-row checksums of the finished L panel (operand sums of later maintenance)
+    Region reg{D, d->ld, n - p, w, d->b};
+    SumOut o = sums_local(d, p, k / d->world, false);
+    o.bm = nullptr;
+    ABFT_TRY(blocksum(d->st, reg, o));
+  }
+  const int64_t tc0 = owned_upto(d, k) * d->b;
+  if (pe < n && d->ncl > tc0) ABFT_TRY(fill_matrix(d->st, d->m + p + tc0 * d->ld, d->ld, w, d->ncl - tc0, 0.0));
+  return 0;
+}
+
+int check_info(abft_dist* d) {
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, d->info, sizeof(int), cudaMemcpyDeviceToHost, d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  if (h != 0) {
+    d->breakdown_col = h - 1;
+    if (d->kind == ABFT_CHOLESKY)
+      set_last_error("non-positive pivot at column %lld", (long long)d->breakdown_col);
+    else
+      set_last_error("zero pivot at column %lld", (long long)d->breakdown_col);
+    CUDA_TRY(cudaMemsetAsync(d->info, 0, sizeof(int), d->st));
+    return ABFT_E_BREAKDOWN;
+  }
+  return 0;
+}
+
+int check_k(abft_dist* d, int64_t k, int scheme) {
+  if (k < 0 || k >= d->nb) {
+    set_last_error("iteration %lld out of range for %lld blocks", (long long)k, (long long)d->nb);
+    return ABFT_E_DIM;
+  }
+  if (scheme < 0 || scheme > 2) {
+    set_last_error("unknown checksum scheme %d", scheme);
+    return ABFT_E_INVALID;
+  }
+  return 0;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+ABFT_API int abft_dist_destroy(abft_dist* d);
+
+ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, int device, int rank,
+                              int world) {
+  *out = nullptr;
+  if (kind < 0 || kind > 2) {
+    set_last_error("unknown decomposition kind %d", kind);
+    return ABFT_E_INVALID;
+  }
+  if (n < 1 || !(1 <= b && b <= n)) {
+    set_last_error("block size %lld outside [1, %lld]", (long long)b, (long long)n);
+    return ABFT_E_DIM;
+  }
+  if (b > 256) {
+    set_last_error("block size %lld > 256 is not supported by the B200 panel kernels", (long long)b);
+    return ABFT_E_INVALID;
+  }
+  if (world < 1 || rank < 0 || rank >= world) {
+    set_last_error("rank %d outside world of %d", rank, world);
+    return ABFT_E_INVALID;
+  }
+  DevGuardD g(device);
+  abft_dist* d = new abft_dist();
+  d->kind = kind;
+  d->n = n;
+  d->b = b;
+  d->nb = (n + b - 1) / b;
+  d->ld = round_up(n, 16);
+  d->device = device;
+  d->rank = rank;
+  d->world = world;
+  d->nbl = d->nb > rank ? (d->nb - 1 - rank) / world + 1 : 0;
+  d->ncl = 0;
+  for (int64_t l = 0; l < d->nbl; ++l) d->ncl += width(d, l * world + rank);
+  d->ld_cs = round_even(2 * d->nb);
+  d->ld_max = round_even(d->nb);
+  d->ld_t = round_even(b);
+  d->ld_b = round_even(std::max<int64_t>(d->ncl, 1));
+  {
+    const char* e = getenv("ABFT_NO_FUSE");
+    d->fuse_enabled = !(e && e[0] == '1');
+  }
+  int rc = 0;
+  auto fail = [&](int r) {
+    abft_dist_destroy(d);
+    return r;
+  };
+  if (cudaStreamCreateWithFlags(&d->st, cudaStreamNonBlocking) != cudaSuccess) {
+    set_last_error("cudaStreamCreate failed");
+    delete d;
+    return -1000;
+  }
+  const int64_t ncl = std::max<int64_t>(d->ncl, 1), nbl = std::max<int64_t>(d->nbl, 1), ld = d->ld;
+  if ((rc = dalloc0(&d->m, ld * ncl))) return fail(rc);
+  if ((rc = dalloc0(&d->gcsw, d->ld_cs * ncl))) return fail(rc);
+  if ((rc = dalloc0(&d->csm, d->ld_cs * ncl))) return fail(rc);
+  if ((rc = dalloc0(&d->grs, ld * nbl))) return fail(rc);
+  if ((rc = dalloc0(&d->rsm, ld * nbl))) return fail(rc);
+  if ((rc = dalloc0(&d->gmax, d->ld_max * nbl))) return fail(rc);
+  if ((rc = dalloc0(&d->el, d->ld_cs * b))) return fail(rc);
+  if ((rc = dalloc0(&d->er, d->ld_t * std::max<int64_t>(nbl, b)))) return fail(rc);
+  if ((rc = dalloc0(&d->uw, d->ld_t * ncl))) return fail(rc);
+  if ((rc = dalloc0(&d->lw, ld * b))) return fail(rc);
+  if ((rc = dalloc0(&d->linv, d->ld_t * b))) return fail(rc);
+  if ((rc = dalloc0(&d->uinv, d->ld_t * b))) return fail(rc);
+  if ((rc = dalloc0(&d->dmax, 2))) return fail(rc);
+  if (kind == ABFT_CHOLESKY && (rc = dalloc0(&d->bext, d->ld_b * (b + 1)))) return fail(rc);
+  if (kind == ABFT_QR) {
+    if ((rc = dalloc0(&d->vstore, ld * n))) return fail(rc);
+    if ((rc = dalloc0(&d->tstore, d->nb * b * d->ld_t))) return fail(rc);
+    if ((rc = dalloc0(&d->betas, b))) return fail(rc);
+    d->qr_part_elems = 2 * 160 * (b + 1);
+    if ((rc = dalloc0(&d->qr_part, d->qr_part_elems))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_rowbuf, 2 * (b + 1) + 128))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_part2, 160LL * 32 * b))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_wfin, 32LL * b))) return fail(rc);
+    if ((rc = dalloc0(&d->gram, d->ld_t * b))) return fail(rc);
+    if ((rc = dalloc0(&d->ww, d->ld_t * ncl))) return fail(rc);
+    if ((rc = dalloc0(&d->mid, d->ld_t * ncl))) return fail(rc);
+  }
+  d->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
+  if ((rc = dalloc0(&d->gws.ptr, d->gws.elems))) return fail(rc);
+  d->ev_cap = 1 << 16;
+  if (cudaMalloc(&d->ev, d->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&d->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  cudaMemset(d->counters, 0, 4 * sizeof(int32_t));
+  d->dirty_cap = 1 << 16;
+  if (cudaMalloc(&d->dirty, 2 * d->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&d->info, sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemset(d->info, 0, sizeof(int));
+  cudaEventCreate(&d->e0);
+  cudaEventCreate(&d->e1);
+  if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
+  *out = d;
+  return 0;
+}
+
+ABFT_API int abft_dist_destroy(abft_dist* d) {
+  if (!d) return 0;
+  DevGuardD g(d->device);
+  if (d->st) cudaStreamSynchronize(d->st);
+  double* bufs[] = {d->m,      d->gcsw,   d->csm,    d->grs,       d->rsm,      d->gmax,
+                    d->el,     d->er,     d->uw,     d->lw,        d->linv,     d->uinv,
+                    d->bext,   d->vstore, d->tstore, d->betas,     d->qr_part,  d->qr_rowbuf,
+                    d->qr_part2, d->qr_wfin, d->gram, d->ww,       d->mid,      d->dmax,
+                    d->gws.ptr};
+  for (double* p : bufs)
+    if (p) cudaFree(p);
+  if (d->ev) cudaFree(d->ev);
+  if (d->counters) cudaFree(d->counters);
+  if (d->dirty) cudaFree(d->dirty);
+  if (d->dplan) cudaFree(d->dplan);
+  if (d->dlist) cudaFree(d->dlist);
+  if (d->info) cudaFree(d->info);
+  if (d->e0) cudaEventDestroy(d->e0);
+  if (d->e1) cudaEventDestroy(d->e1);
+  if (d->st) cudaStreamDestroy(d->st);
+  delete d;
+  return 0;
+}
+
+ABFT_API int64_t abft_dist_local_cols(abft_dist* d) { return d->ncl; }
+
+ABFT_API void* abft_dist_stream(abft_dist* d) { return reinterpret_cast<void*>(d->st); }
+
+ABFT_API int64_t abft_dist_xbuf_elems(abft_dist* d, int64_t k) {
+  if (k < 0 || k >= d->nb) return 0;
+  const int64_t p = k * d->b, w = width(d, k), ldp = panel_ld(d, k);
+  if (d->kind == ABFT_CHOLESKY) {
+    if (k == 0) return 0;
+    const int64_t nbr = (d->n - p + d->b - 1) / d->b;
+    return ldp * (w + 1) + round_even(2 * nbr) * w;
+  }
+  if (p + w >= d->n && d->kind == ABFT_LU) return 0;  // last LU panel: nothing to send
+  return ldp * w + d->ld_t * w;
+}
+
+ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda) {
+  DevGuardD g(d->device);
+  if (lda < d->n) {
+    set_last_error("lda < n");
+    return ABFT_E_INVALID;
+  }
+  for (int64_t l = 0; l < d->nbl; ++l) {
+    const int64_t j = l * d->world + d->rank;
+    CUDA_TRY(cudaMemcpy2DAsync(d->m + l * d->b * d->ld, d->ld * 8, a + j * d->b * lda, lda * 8,
+                               d->n * 8, width(d, j), cudaMemcpyHostToDevice, d->st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  d->k_done = 0;
+  d->sums_valid = false;
+  d->qr_count = 0;
+  d->breakdown_col = -1;
+  return 0;
+}
+
+ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo) {
+  DevGuardD g(d->device);
+  if (d->ncl > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(out, ldo * 8, d->m, d->ld * 8, d->n * 8, d->ncl,
+                               cudaMemcpyDeviceToHost, d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  return 0;
+}
+
+ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) {
+  DevGuardD g(d->device);
+  ABFT_TRY(check_k(d, k, scheme));
+  if (k != d->k_done) {
+    set_last_error("expected iteration %lld, got %lld", (long long)d->k_done, (long long)k);
+    return ABFT_E_DIM;
+  }
+  if (k == 0) {
+    CUDA_TRY(cudaMemsetAsync(d->counters, 0, 2 * sizeof(int32_t), d->st));
+    CUDA_TRY(cudaEventRecord(d->e0, d->st));
+    d->timed = false;
+  }
+  if (d->kind == ABFT_LU) {
+    // the last LU panel is factored in place; nothing is exchanged
+    const int64_t p = k * d->b, pe = std::min(p + d->b, d->n);
+    if (pe >= d->n) {
+      if (owner(d, k) == d->rank) {
+        const int64_t lc = (k / d->world) * d->b;
+        ABFT_TRY(diag_factor(d->st, d->m + p + lc * d->ld, d->ld, (int)(pe - p), 0, d->linv,
+                             d->ld_t, d->uinv, d->ld_t, d->info, p));
+      }
+      return 0;
+    }
+    return begin_lu(d, k, xbuf);
+  }
+  if (d->kind == ABFT_QR) return begin_qr(d, k, xbuf);
+  return begin_chol(d, k, xbuf);
+}
+
+ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double* xbuf, int nplan,
+                              double* local_max) {
+  DevGuardD g(d->device);
+  ABFT_TRY(check_k(d, k, scheme));
+  if (d->kind == ABFT_CHOLESKY) return update_chol(d, k, scheme, xbuf, nplan, local_max);
+  if (d->kind == ABFT_LU && std::min((k + 1) * d->b, d->n) >= d->n) {
+    if (nplan > 0 && local_max) CUDA_TRY(cudaMemsetAsync(local_max, 0, sizeof(double), d->st));
+    return 0;
+  }
+  return update_lu_qr(d, k, scheme, xbuf, nplan, local_max);
+}
+
+ABFT_API int abft_dist_finish(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                              int correct, const double* scale) {
+  DevGuardD g(d->device);
+  ABFT_TRY(check_k(d, k, scheme));
+  ABFT_TRY(inject_verify(d, k, scheme, plan, nplan, correct, scale));
+  if (d->kind == ABFT_CHOLESKY) ABFT_TRY(chol_pd_pu(d, k));
+  d->k_done = k + 1;
+  if (d->k_done == d->nb) {
+    CUDA_TRY(cudaEventRecord(d->e1, d->st));
+    d->timed = true;
+  }
+  return 0;
+}
+
+// Synchronize, check for a numeric breakdown and return every ABFT event
+// since the last call in global coordinates (row/col of the element or block
+// corner, block_row/block_col on the global region-local grid, iteration in
+// `iters`), unsorted; the host merges ranks and orders them like the
+// reference (iteration, block row, block column, column).
+ABFT_API int abft_dist_events(abft_dist* d, abft_location* locs, int64_t* iters, int max_locs,
+                              int* n_out) {
+  DevGuardD g(d->device);
+  *n_out = 0;
+  ABFT_TRY(check_info(d));
+  int32_t cnt[2];
+  CUDA_TRY(cudaMemcpyAsync(cnt, d->counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  if (cnt[0] > d->ev_cap) {
+    set_last_error("ABFT event buffer overflow (%d events)", cnt[0]);
+    return ABFT_E_OVERFLOW;
+  }
+  std::vector<Event> evs(cnt[0]);
+  if (cnt[0] > 0)
+    CUDA_TRY(cudaMemcpy(evs.data(), d->ev, cnt[0] * sizeof(Event), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemsetAsync(d->counters, 0, 2 * sizeof(int32_t), d->st));
+  *n_out = (int)evs.size();
+  for (size_t i = 0; i < evs.size(); ++i) {
+    const Event& e = evs[i];
+    if (e.kind < 0) {
+      set_last_error("index 0 is out of bounds for axis 0 with size 0");
+      return ABFT_E_RANGE;
+    }
+    if ((int)i >= max_locs) continue;
+    const LocalRegion R = local_region(d, e.iter);
+    const int64_t jg = (R.lb0 + e.bj) * d->world + d->rank;  // global block column
+    abft_location& L = locs[i];
+    L.row = R.r0 + e.row;
+    L.col = jg * d->b + (e.col - (int64_t)e.bj * d->b);
+    L.kind = e.kind;
+    L.flag = e.flag;
+    L.detected_kind = e.detected_kind;
+    L.corrected = e.corrected;
+    L.uncorrectable = e.uncorrectable;
+    L.block_row = e.bi;
+    L.block_col = (int32_t)(jg - R.gc0 / d->b);
+    L.seq = e.seq;
+    if (iters) iters[i] = e.iter;
+  }
+  return 0;
+}
+
+ABFT_API int64_t abft_dist_k_done(abft_dist* d) { return d->k_done; }
+
+ABFT_API int abft_dist_get_qr_panel(abft_dist* d, int64_t k, double* V, int64_t ldv, double* T,
+                                    int64_t ldt) {
+  DevGuardD g(d->device);
+  if (d->kind != ABFT_QR || k < 0 || k >= d->qr_count) {
+    set_last_error("no QR panel %lld", (long long)k);
+    return ABFT_E_INVALID;
+  }
+  const int64_t p = k * d->b, w = width(d, k);
+  if (V)
+    CUDA_TRY(cudaMemcpy2DAsync(V, ldv * 8, d->vstore + p + p * d->ld, d->ld * 8, (d->n - p) * 8, w,
+                               cudaMemcpyDeviceToHost, d->st));
+  if (T)
+    CUDA_TRY(cudaMemcpy2DAsync(T, ldt * 8, d->tstore + k * d->b * d->ld_t, d->ld_t * 8, w * 8, w,
+                               cudaMemcpyDeviceToHost, d->st));
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  return 0;
+}
+
+ABFT_API int abft_dist_elapsed_ms(abft_dist* d, double* ms) {
+  DevGuardD g(d->device);
+  *ms = 0.0;
+  if (!d->timed) return 0;
+  CUDA_TRY(cudaEventSynchronize(d->e1));
+  float f = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&f, d->e0, d->e1));
+  *ms = f;
+  return 0;
+}
+
+}  // extern "C"

@@ -1,0 +1,80 @@
+"""Worker processes for the multi-rank tests (spawned, one per rank).
+
+GPU mode: every rank drives the sm_100a library on cuda:0 (the test boxes
+have one GPU) with the gloo backend — the same DistributedFactorization code
+the NCCL path runs, with the exchange staged through host memory.
+CPU mode: only the host-side logic (event merge over all_gather_object).
+"""
+from __future__ import annotations
+
+import json
+import os
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+if str(ROOT) not in sys.path:
+    sys.path.insert(0, str(ROOT))
+
+
+def _init(rank: int, world: int, init_file: str):
+    import torch.distributed as dist
+    os.environ.setdefault("GLOO_SOCKET_IFNAME", "lo")
+    dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank,
+                            world_size=world)
+    return dist
+
+
+def gpu_cases(rank: int, world: int, init_file: str, cases: list, out: str) -> None:
+    import numpy as np
+    import torch
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, init_file)
+    import paper_2301_03166_b200 as P
+    from paper_2301_03166_b200.distributed import DistributedFactorization
+    results = []
+    for c in cases:
+        a = P.generate_test_matrix(c["kind"], c["n"], c["seed"])
+        f = DistributedFactorization(c["kind"], a, c["b"])
+        rng = np.random.default_rng(c["seed"])
+        sched = {int(k): v for k, v in c.get("schedule", {}).items()}
+        if c.get("per_iteration"):
+            reps = [f.run_numeric_iteration(k, c["scheme"], sched.get(k), rng)
+                    for k in range(f.layout.n_blocks)]
+        else:
+            reps = f.run_protected(c["scheme"], sched, rng)
+        locs = [[(int(r), int(cc), getattr(kk, "value", kk), bool(fl))
+                 for r, cc, kk, fl in rep.locations] for rep in reps]
+        res = f.residual(a)
+        full = f.gather(0)
+        if rank == 0:
+            np.save(os.path.join(out, f"{c['name']}.npy"), full)
+        results.append({"name": c["name"], "locations": locs, "residual": res,
+                        "detected": [{getattr(k, "value", k): v for k, v in r.detected.items()}
+                                     for r in reps],
+                        "uncorrectable": [bool(r.uncorrectable) for r in reps]})
+        del f
+    with open(os.path.join(out, f"rank{rank}.json"), "w") as fh:
+        json.dump(results, fh)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def cpu_merge(rank: int, world: int, init_file: str, out: str) -> None:
+    dist = _init(rank, world, init_file)
+    from paper_2301_03166_b200.distributed import merge_events, reports_from_events
+    # each rank owns different block columns of the same iterations
+    mine = [{"iter": k, "block_row": br, "block_col": bc, "seq": s, "row": 10 * br + s,
+             "col": 100 * bc + s, "kind": 0, "flag": 1, "detected_kind": 0, "corrected": 1,
+             "uncorrectable": 0}
+            for k in range(3) for br in range(2) for bc in range(rank, 4, world) for s in range(2)]
+    gathered = [None] * world
+    dist.all_gather_object(gathered, mine)
+    merged = merge_events(gathered)
+    reps = reports_from_events(merged, 0, 3)
+    with open(os.path.join(out, f"rank{rank}.json"), "w") as fh:
+        json.dump({"order": [(e["iter"], e["block_row"], e["block_col"], e["seq"]) for e in merged],
+                   "counts": [sum(r.detected.values()) for r in reps],
+                   "locations": [r.locations for r in reps]}, fh, default=str)
+    dist.barrier()
+    dist.destroy_process_group()
