@@ -44,7 +44,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kind", default="lu", choices=["lu", "cholesky", "qr"])
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--n", "--order", dest="n", type=int, default=32768)
     ap.add_argument("--b", type=int, default=256)
     ap.add_argument("--scheme", default="full", choices=["none", "single", "full"])
     ap.add_argument("--seed", type=int, default=0)
@@ -53,12 +53,26 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra-kinds", default="", help="comma list of kinds also measured")
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="N>1 transport (gloo: several ranks sharing one GPU, for testing)")
     return ap.parse_args()
 
 
 # ---------------------------------------------------------------------------
 # environment helpers
 # ---------------------------------------------------------------------------
+
+def all_max(x: float) -> float:
+    """Max over ranks (identity for a single process)."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(x)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
 
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
@@ -210,7 +224,9 @@ def config(args) -> dict:
             "kind": args.kind, "n": args.n, "b": args.b, "scheme": args.scheme,
             "seed": args.seed,
             "l2": "working set 8.6 GB >> 126 MB L2; no flush needed",
-            "parallelism": "replicas" if args.gpus > 1 else "single"}
+            "parallelism": (f"block-cyclic columns over {args.gpus} GPUs "
+                            f"({'panel broadcast' if args.kind != 'cholesky' else 'panel-update reduce'}"
+                            f" over {args.dist_backend})") if args.gpus > 1 else "single"}
 
 
 # ---------------------------------------------------------------------------
@@ -280,6 +296,51 @@ class Arm:
         return out.value
 
 
+class DistArm:
+    """Block-cyclic factorization over all ranks: every rank
+    holds its column blocks of the same global input, kept on the device."""
+
+    def __init__(self, kind, n, b, seed, device):
+        import paper_2301_03166_b200 as P
+        from paper_2301_03166_b200 import _lib
+        from paper_2301_03166_b200.distributed import DistributedFactorization
+        self.P, self.L = P, _lib
+        self.lib = _lib.load()
+        self.kind, self.n, self.b, self.seed = kind, n, b, seed
+        t0 = time.perf_counter()
+        if kind == "cholesky":
+            # uniform draws on the host, SPD product on this rank's GPU
+            host = np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n)))
+            tmp = P.Factorization(kind, host, b, device=device)
+            P.linalg.check(self.lib.abft_make_spd(tmp._ctx))
+            tmp._dirty()
+            host = tmp.m
+            del tmp
+        else:
+            host = P.generate_test_matrix(kind, n, seed)
+        self.gen_s = time.perf_counter() - t0
+        _GEN["s"] = self.gen_s
+        self.host = host
+        self.f = DistributedFactorization(kind, host, b, device=device, keep_input=True)
+        import torch
+        self.torch = torch
+        self.stream = torch.cuda.ExternalStream(self.f.stream_ptr())
+
+    def step(self, scheme):
+        k_fault, rng = fault_plan(self.n, self.b, self.seed)
+        self.f.reset()
+        reps = self.f.run_protected(scheme, {k_fault: {"0d": 1}}, rng)
+        return k_fault, reps
+
+    timed = Arm.timed
+
+    def profile(self, scheme):
+        return {"pd": None, "pu": None, "tmu_gemm": None, "abft": None}
+
+    def residual(self):
+        return self.f.residual(self.host)
+
+
 def tmu_flops(kind, n, b) -> float:
     from paper_2301_03166_b200.linalg import compute_flops
     return sum(compute_flops(kind, "tmu", n, b, k) for k in range(-(-n // b)))
@@ -306,13 +367,17 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        local = local % torch.cuda.device_count()  # gloo test mode: ranks may share a GPU
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(local)
     P = __import__("paper_2301_03166_b200")
     lib = P._lib.load()
     peak = ctypes.c_double(0.0)
     P.linalg.check(lib.abft_probe_dmma_peak(20000, ctypes.byref(peak)))
-    arm = Arm(args.kind, args.n, args.b, args.seed, local)
+    arm = (DistArm if world > 1 else Arm)(args.kind, args.n, args.b, args.seed, local)
     if args.profile_only:
         arm.step(args.scheme)
         torch.cuda.synchronize()
@@ -332,12 +397,11 @@ def run_ours(args):
     # the single planned 0-D fault must be located and corrected
     locs = [loc for r in reps for loc in r.locations]
     fixed = sum(r.corrected[P.ErrorKind.D0] for r in reps)
-    ms_t = torch.tensor([ms], device="cuda")
-    if world > 1:
-        torch.distributed.all_reduce(ms_t, op=torch.distributed.ReduceOp.MAX)
-    ms_step = ms_t.item() / args.steps
+    ms_max = all_max(ms)
+    ms_step = ms_max / args.steps
     flops = FLOPS[args.kind](args.n)
-    value = world * flops / (ms_step * 1e-3) / 1e12
+    # N > 1 factors ONE global matrix over all ranks (strong scaling)
+    value = flops / (ms_step * 1e-3) / 1e12
 
     overhead = None
     if not args.no_overhead and args.scheme != "none":
@@ -345,6 +409,9 @@ def run_ours(args):
             arm.step("none")
         ms_none, _ = arm.timed("none", args.steps)
         overhead = 100.0 * (ms - ms_none) / ms_none
+    if overhead is not None and world > 1:
+        ov = all_max(ms_none)
+        overhead = 100.0 * (ms_max - ov) / ov
     prof = arm.profile(args.scheme)
     tflops_tmu = tmu_flops(args.kind, args.n, args.b)
     achieved = tflops_tmu / (prof["tmu_gemm"] * 1e-3) / 1e12 if prof["tmu_gemm"] else None
@@ -352,7 +419,7 @@ def run_ours(args):
 
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(arm, args)
+        e2e = run_e2e(arm, args) if world == 1 else run_e2e_dist(arm, args)
     extra = {}
     for kind in [k for k in args.extra_kinds.split(",") if k and k != args.kind]:
         extra[kind] = measure_kind(kind, args, local)
@@ -369,7 +436,8 @@ def run_ours(args):
     line = {
         "metric": metric_name(args), "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: generate_test_matrix({args.kind!r}, {args.n}, seed={args.seed}) "
                 "(PCG64 draws bit-identical to the reference)",
         "config": config(args),
@@ -395,7 +463,8 @@ def run_ours(args):
                      "epilogue (no separate read of the region); 'ms' is all remaining ABFT work "
                      "(encode of the first region, operand sums, maintenance GEMMs, verify "
                      "kernel, Cholesky panel passes)"),
-            "ms": prof["abft"], "pct_of_step": 100.0 * prof["abft"] / ms_step},
+            "ms": prof["abft"],
+            "pct_of_step": 100.0 * prof["abft"] / ms_step if prof["abft"] is not None else None},
         "profile_ms": prof,
         "whole_step_frac_of_peak": value / world / peak.value,
         "residual": res, "residual_over_n_eps": res / (args.n * 2.220446049250313e-16),
@@ -458,6 +527,35 @@ def run_e2e(arm, args):
     return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
             "ms_per_step": sec * 1e3, "api": "abft_set_matrix + run_protected + abft_get_matrix"}
+
+
+def run_e2e_dist(arm, args):
+    """e2e at N>1: every rank copies its column blocks of the pinned host
+    input in, runs the distributed factorization and copies its columns out;
+    time = max over ranks."""
+    import torch
+    f, n = arm.f, args.n
+    pinned_in = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
+    pinned_in[...] = arm.host.T
+    src = pinned_in.T
+    pinned_out = torch.empty((f.ncl, n), dtype=torch.float64, pin_memory=True).numpy().T
+    times = []
+    for i in range(1 + args.steps):
+        torch.distributed.barrier()
+        t0 = time.perf_counter()
+        f.set_matrix(src)
+        k_fault, rng = fault_plan(n, args.b, args.seed)
+        f.run_protected(args.scheme, {k_fault: {"0d": 1}}, rng)
+        arm.P.linalg.check(arm.lib.abft_dist_get_matrix(f._ctx, arm.P._lib.dptr(pinned_out), n))
+        dt = all_max(time.perf_counter() - t0)
+        if i:
+            times.append(dt)
+    sec = statistics.median(times)
+    return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
+            "ms_per_step": sec * 1e3,
+            "api": "DistributedFactorization.set_matrix + run_protected + abft_dist_get_matrix "
+                   "(per rank, its column blocks; bytes summed over ranks)"}
 
 
 def main():

@@ -55,7 +55,9 @@ struct abft_ctx {
   double* gcsw = nullptr;  // (2nb) x n, ld_cs: row 2*gbi plain, 2*gbi+1 weighted
   int64_t ld_cs = 0;
   double* grs = nullptr;   // n x nb row sums, ld
-  double* gmax = nullptr;  // nb x nb, ld_max
+  double* gmax = nullptr;
+  double* fpart = nullptr;  // fused-epilogue per-strip row sums (ld x 4nb, region-local)
+  double* fmaxp = nullptr;  // fused-epilogue per-strip max (ld_max x 4nb)  // nb x nb, ld_max
   int64_t ld_max = 0;
   double* csm = nullptr;   // maintained col sums of the current region (2nb x n, ld_cs)
   double* rsm = nullptr;   // maintained row sums (n x nb, ld)
@@ -226,6 +228,10 @@ FusedSums fused_for(abft_ctx* c, int64_t r0, int64_t c0) {
   f.rp_ld = o.rp_ld;
   f.bm = o.bm;
   f.bm_ld = o.bm_ld;
+  f.rpp = c->fpart;
+  f.rpp_ld = c->ld;
+  f.bmp = c->fmaxp;
+  f.bmp_ld = c->ld_max;
   return f;
 }
 
@@ -908,6 +914,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   if ((rc = dalloc(&c->grs, ld * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->rsm, ld * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->gmax, c->ld_max * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->fpart, ld * 4 * c->nb))) return fail(rc);
+  if ((rc = dalloc(&c->fmaxp, c->ld_max * 4 * c->nb))) return fail(rc);
   if ((rc = dalloc(&c->el, c->ld_cs * b))) return fail(rc);
   if ((rc = dalloc(&c->er, c->ld_t * std::max<int64_t>(c->nb, b)))) return fail(rc);
   if (kind == ABFT_CHOLESKY && (rc = dalloc(&c->chol_rs, ld * c->nb))) return fail(rc);
@@ -956,6 +964,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   DevGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
   double* bufs[] = {c->m,     c->a0,     c->gcsw,   c->grs,     c->gmax,  c->csm,  c->rsm,
+                    c->fpart, c->fmaxp,
                     c->chol_rs,
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,

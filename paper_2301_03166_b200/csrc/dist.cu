@@ -71,12 +71,16 @@ struct abft_dist {
   cudaStream_t st = nullptr;
 
   double* m = nullptr;      // n x ncl (ld)
+  double* a0 = nullptr;     // kept local input (abft_dist_keep_input)
+  bool keep_input = false;
   double* gcsw = nullptr;   // (2nb) x ncl (ld_cs): row 2*gbi plain, 2*gbi+1 weighted
   double* csm = nullptr;    // maintained col sums, region-local
   int64_t ld_cs = 0;
   double* grs = nullptr;    // n x nbl (ld)
   double* rsm = nullptr;    // maintained row sums, region-local (ld)
-  double* gmax = nullptr;   // nb x nbl (ld_max)
+  double* gmax = nullptr;
+  double* fpart = nullptr;  // fused-epilogue per-strip row sums (ld x 4nb, region-local)
+  double* fmaxp = nullptr;  // fused-epilogue per-strip max (ld_max x 4nb)   // nb x nbl (ld_max)
   int64_t ld_max = 0;
   double* el = nullptr;     // operand block-row sums (2nb x b, ld_cs)
   double* er = nullptr;     // R * E_R (b x nbl, ld_t)
@@ -166,6 +170,10 @@ FusedSums fused_local(abft_dist* d, int64_t r0, int64_t lb) {
   f.rp_ld = o.rp_ld;
   f.bm = o.bm;
   f.bm_ld = o.bm_ld;
+  f.rpp = d->fpart;
+  f.rpp_ld = d->ld;
+  f.bmp = d->fmaxp;
+  f.bmp_ld = d->ld_max;
   return f;
 }
 
@@ -643,6 +651,8 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
   if ((rc = dalloc0(&d->grs, ld * nbl))) return fail(rc);
   if ((rc = dalloc0(&d->rsm, ld * nbl))) return fail(rc);
   if ((rc = dalloc0(&d->gmax, d->ld_max * nbl))) return fail(rc);
+  if ((rc = dalloc0(&d->fpart, ld * 4 * nbl))) return fail(rc);
+  if ((rc = dalloc0(&d->fmaxp, d->ld_max * 4 * nbl))) return fail(rc);
   if ((rc = dalloc0(&d->el, d->ld_cs * b))) return fail(rc);
   if ((rc = dalloc0(&d->er, d->ld_t * std::max<int64_t>(nbl, b)))) return fail(rc);
   if ((rc = dalloc0(&d->uw, d->ld_t * ncl))) return fail(rc);
@@ -685,7 +695,8 @@ ABFT_API int abft_dist_destroy(abft_dist* d) {
   if (!d) return 0;
   DevGuardD g(d->device);
   if (d->st) cudaStreamSynchronize(d->st);
-  double* bufs[] = {d->m,      d->gcsw,   d->csm,    d->grs,       d->rsm,      d->gmax,
+  double* bufs[] = {d->fpart,  d->fmaxp,
+                    d->m,      d->a0,     d->gcsw,   d->csm,    d->grs,       d->rsm,      d->gmax,
                     d->el,     d->er,     d->uw,     d->lw,        d->linv,     d->uinv,
                     d->bext,   d->vstore, d->tstore, d->betas,     d->qr_part,  d->qr_rowbuf,
                     d->qr_part2, d->qr_wfin, d->gram, d->ww,       d->mid,      d->dmax,
@@ -732,7 +743,32 @@ ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda) {
     CUDA_TRY(cudaMemcpy2DAsync(d->m + l * d->b * d->ld, d->ld * 8, a + j * d->b * lda, lda * 8,
                                d->n * 8, width(d, j), cudaMemcpyHostToDevice, d->st));
   }
+  if (d->keep_input) {
+    if (!d->a0) ABFT_TRY(dalloc0(&d->a0, d->ld * std::max<int64_t>(d->ncl, 1)));
+    CUDA_TRY(cudaMemcpyAsync(d->a0, d->m, d->ld * d->ncl * 8, cudaMemcpyDeviceToDevice, d->st));
+  }
   CUDA_TRY(cudaStreamSynchronize(d->st));
+  d->k_done = 0;
+  d->sums_valid = false;
+  d->qr_count = 0;
+  d->breakdown_col = -1;
+  return 0;
+}
+
+ABFT_API int abft_dist_keep_input(abft_dist* d, int keep) {
+  d->keep_input = keep != 0;
+  return 0;
+}
+
+// Restore the local columns from the kept input (a new factorization without
+// a host round trip); asynchronous on the context stream.
+ABFT_API int abft_dist_reset(abft_dist* d) {
+  DevGuardD g(d->device);
+  if (!d->a0) {
+    set_last_error("abft_dist_reset needs abft_dist_keep_input(d, 1) before abft_dist_set_matrix");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpyAsync(d->m, d->a0, d->ld * d->ncl * 8, cudaMemcpyDeviceToDevice, d->st));
   d->k_done = 0;
   d->sums_valid = false;
   d->qr_count = 0;

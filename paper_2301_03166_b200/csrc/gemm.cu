@@ -188,21 +188,24 @@ ABFT_DEVINL int col_of(int cf, int c8) {
   return 8 * cf + pm(c8);
 }
 
-// Work unit of a warpgroup: plain mode = one tile; fused mode = one fb x fb
-// block (ntm_b x ntn_b tiles).
-ABFT_DEVINL int unit_tiles(const KParams& p) { return p.fuse ? p.ntm_b * p.ntn_b : 1; }
+// Work unit of a warpgroup: plain mode = one tile; fused mode = one
+// fb x BN strip of a checksum block (ntm_b tiles stacked vertically): its
+// column sums are complete, its row sums / max are per-strip partials.
+// Strips (not whole blocks) keep the tail of each trailing update balanced.
+ABFT_DEVINL int unit_tiles(const KParams& p) { return p.fuse ? p.ntm_b : 1; }
 ABFT_DEVINL int total_units(const KParams& p) {
-  return p.fuse ? p.nbr_b * p.nbc_b : p.tiles_m * p.tiles_n * p.splits;
+  return p.fuse ? p.nbr_b * p.tiles_n : p.tiles_m * p.tiles_n * p.splits;
 }
 template <int BM>
 ABFT_DEVINL void fused_tile(const KParams& p, int unit, int u, int* m0, int* n0, int* bi, int* bj,
                             int* tm, int* tn) {
   *bi = unit % p.nbr_b;
-  *bj = unit / p.nbr_b;
-  *tm = u % p.ntm_b;
-  *tn = u / p.ntm_b;
-  *m0 = *bi * p.fb + *tm * BM;
-  *n0 = *bj * p.fb + *tn * BN;
+  const int tcol = unit / p.nbr_b;
+  *bj = tcol / p.ntn_b;
+  *tn = tcol % p.ntn_b;
+  *tm = u;
+  *m0 = *bi * p.fb + u * BM;
+  *n0 = tcol * BN;
 }
 template <int BM>
 ABFT_DEVINL void tile_coords(const KParams& p, int t, int* m0, int* n0, int* z) {
@@ -476,8 +479,13 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
             }
           }
       }
-      // Pass 2 (fused checksums) from the output registers.
+      // Pass 2 (fused checksums) from the output registers. Lane sums are
+      // combined with reduce-scatter butterflies (each exchange halves the
+      // values still carried), so every lane ends up owning complete sums.
       if (p.fuse) {
+        // row sums over this warp's 32 columns: 2*RP rows per lane group,
+        // reduced over the 4 j-lanes
+        double rv[2 * RP];
 #pragma unroll
         for (int rp = 0; rp < RP; ++rp) {
           double rs0 = 0.0, rs1 = 0.0;
@@ -489,20 +497,33 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
               rs1 += acc[2 * rp + 1][cf][tt];
               mx = fmax(mx, fmax(fabs(acc[2 * rp][cf][tt]), fabs(acc[2 * rp + 1][cf][tt])));
             }
-          // row sums over this warp's 32 columns: reduce the 4 j-lanes
-          rs0 += __shfl_xor_sync(0xffffffffu, rs0, 1);
-          rs0 += __shfl_xor_sync(0xffffffffu, rs0, 2);
-          rs1 += __shfl_xor_sync(0xffffffffu, rs1, 1);
-          rs1 += __shfl_xor_sync(0xffffffffu, rs1, 2);
-          if (j == 0) {
-            const int r0b = tm * BM + wm + row_of<AT>(rp, 0, g);
-            const int r1b = tm * BM + wm + row_of<AT>(rp, 1, g);
-            rowacc[(wn >> 5) * MAXFB + r0b] += rs0;
-            rowacc[(wn >> 5) * MAXFB + r1b] += rs1;
+          rv[2 * rp] = rs0;
+          rv[2 * rp + 1] = rs1;
+        }
+        {
+          constexpr int NR = 2 * RP;  // 4 (three warpgroups) or 8 (two)
+          const bool h1 = (j & 2) != 0, h0 = (j & 1) != 0;
+#pragma unroll
+          for (int i = 0; i < NR / 2; ++i) {
+            const double snd = h1 ? rv[i] : rv[i + NR / 2];
+            rv[i] = (h1 ? rv[i + NR / 2] : rv[i]) + __shfl_xor_sync(0xffffffffu, snd, 2);
+          }
+#pragma unroll
+          for (int i = 0; i < NR / 4; ++i) {
+            const double snd = h0 ? rv[i] : rv[i + NR / 4];
+            rv[i] = (h0 ? rv[i + NR / 4] : rv[i]) + __shfl_xor_sync(0xffffffffu, snd, 1);
+          }
+#pragma unroll
+          for (int i = 0; i < NR / 4; ++i) {
+            const int q = (h1 ? NR / 2 : 0) + (h0 ? NR / 4 : 0) + i;  // rv index = 2*rp + e
+            const int r = tm * BM + wm + row_of<AT>(q >> 1, q & 1, g);
+            rowacc[(wn >> 5) * MAXFB + r] += rv[i];
           }
         }
-        // column plain / index-weighted sums over this warp's WTM rows
+        // column plain / index-weighted sums over this warp's WTM rows:
+        // 16 values (cf, tt, plain|weighted) reduced over the 8 g-lanes
         const int wbase = tm * BM + wm;
+        double v[16];
 #pragma unroll
         for (int cf = 0; cf < 4; ++cf)
 #pragma unroll
@@ -516,41 +537,89 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
               a0 += x0 + x1;
               a1 += w0 * x0 + w1 * x1;
             }
-#pragma unroll
-            for (int o = 4; o < 32; o <<= 1) {
-              a0 += __shfl_xor_sync(0xffffffffu, a0, o);
-              a1 += __shfl_xor_sync(0xffffffffu, a1, o);
-            }
-            if (g == 0) {
-              const int c = tn * BN + wn + col_of<BT>(cf, 2 * j + tt);
-              colacc[((wi & 1) * MAXFB + c) * 2 + 0] += a0;
-              colacc[((wi & 1) * MAXFB + c) * 2 + 1] += a1;
-            }
+            v[(cf * 2 + tt) * 2 + 0] = a0;
+            v[(cf * 2 + tt) * 2 + 1] = a1;
           }
+        const bool g2 = (g & 4) != 0, g1 = (g & 2) != 0, g0 = (g & 1) != 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double snd = g2 ? v[i] : v[i + 8];
+          v[i] = (g2 ? v[i + 8] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const double snd = g1 ? v[i] : v[i + 4];
+          v[i] = (g1 ? v[i + 4] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 8);
+        }
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const double snd = g0 ? v[i] : v[i + 2];
+          v[i] = (g0 ? v[i + 2] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 4);
+        }
+        // this lane now owns (cf, tt) = (g >> 1, g & 1): plain v[0], weighted v[1]
+        const int c = tn * BN + wn + col_of<BT>(g >> 1, 2 * j + (g & 1));
+        colacc[((wi & 1) * MAXFB + c) * 2 + 0] += v[0];
+        colacc[((wi & 1) * MAXFB + c) * 2 + 1] += v[1];
       }
     }
     if (p.fuse) {
-      // block finished: combine the halves in a fixed order and publish
+      // strip finished: combine the halves in a fixed order and publish the
+      // complete column sums and the strip's partial row sums / max
+      const int tn = (unit / p.nbr_b) % p.ntn_b;
       mx = warp_max(mx);
       if (lane == 0) wmax[wi] = mx;
       asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
       const int tid = threadIdx.x & 127;
       const int rows_b = min(p.fb, p.M - bi * p.fb);
-      const int cols_b = min(p.fb, p.N - bj * p.fb);
+      const int c0s = tn * BN;
+      const int cols_s = min(BN, p.N - (bj * p.fb + c0s));
       const FusedSums& fs = p.sums;
-      for (int c = tid; c < cols_b; c += 128) {
-        const int64_t gc = (int64_t)bj * p.fb + c;
-        fs.cp[fs.cp_step * bi + gc * fs.cp_ld] = colacc[c * 2 + 0] + colacc[(MAXFB + c) * 2 + 0];
-        fs.cw[fs.cw_step * bi + gc * fs.cw_ld] = colacc[c * 2 + 1] + colacc[(MAXFB + c) * 2 + 1];
+      for (int c = tid; c < cols_s; c += 128) {
+        const int cc = c0s + c;
+        const int64_t gc = (int64_t)bj * p.fb + cc;
+        fs.cp[fs.cp_step * bi + gc * fs.cp_ld] = colacc[cc * 2 + 0] + colacc[(MAXFB + cc) * 2 + 0];
+        fs.cw[fs.cw_step * bi + gc * fs.cw_ld] = colacc[cc * 2 + 1] + colacc[(MAXFB + cc) * 2 + 1];
       }
+      const int64_t scol = (int64_t)bj * p.ntn_b + tn;
       for (int r = tid; r < rows_b; r += 128)
-        fs.rp[(int64_t)bi * p.fb + r + (int64_t)bj * fs.rp_ld] = rowacc[r] + rowacc[MAXFB + r];
+        fs.rpp[(int64_t)bi * p.fb + r + scol * fs.rpp_ld] = rowacc[r] + rowacc[MAXFB + r];
       if (tid == 0)
-        fs.bm[bi + (int64_t)bj * fs.bm_ld] =
-            fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
+        fs.bmp[bi + scol * fs.bmp_ld] = fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
       asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
-      for (int k2 = tid; k2 < SUM_DOUBLES; k2 += 128) colacc[k2] = 0.0;
+      for (int t = tid; t < 4 * BN; t += 128) {
+        const int half = t / (2 * BN), rem = t % (2 * BN);
+        colacc[(half * MAXFB + c0s + (rem >> 1)) * 2 + (rem & 1)] = 0.0;
+      }
+      for (int t = tid; t < 2 * MAXFB; t += 128) rowacc[t] = 0.0;
       asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
+    }
+  }
+}
+
+// Row sums and block max of the fused epilogue: fixed-order combination of
+// the per-strip partials (rows x nbc and nbr x nbc outputs).
+__global__ void fused_combine(int M, int N, int fb, int ntn, FusedSums s) {
+  const int nbr = (M + fb - 1) / fb, nbc = (N + fb - 1) / fb;
+  const int64_t nrow = (int64_t)M * nbc;
+  const int64_t total = nrow + (int64_t)nbr * nbc;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    if (idx < nrow) {
+      const int r = static_cast<int>(idx % M);
+      const int bj = static_cast<int>(idx / M);
+      const int ns = (min(fb, N - bj * fb) + BN - 1) / BN;
+      const double* src = s.rpp + r + (int64_t)bj * ntn * s.rpp_ld;
+      double v = 0.0;
+      for (int t = 0; t < ns; ++t) v += src[(int64_t)t * s.rpp_ld];
+      s.rp[r + (int64_t)bj * s.rp_ld] = v;
+    } else {
+      const int64_t t2 = idx - nrow;
+      const int bi = static_cast<int>(t2 % nbr);
+      const int bj = static_cast<int>(t2 / nbr);
+      const int ns = (min(fb, N - bj * fb) + BN - 1) / BN;
+      double m = 0.0;
+      for (int t = 0; t < ns; ++t) m = fmax(m, s.bmp[bi + ((int64_t)bj * ntn + t) * s.bmp_ld]);
+      s.bm[bi + (int64_t)bj * s.bm_ld] = m;
     }
   }
 }
@@ -728,6 +797,14 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
   int rc = nwg == 3 ? launch_any<3>(st, AT, BT, ma, mb, mc, kp, max_ctas)
                     : launch_any<2>(st, AT, BT, ma, mb, mc, kp, max_ctas);
   if (rc) return rc;
+  if (fs) {
+    const int64_t work = (int64_t)M * kp.nbc_b + (int64_t)kp.nbr_b * kp.nbc_b;
+    int blocks = static_cast<int>((work + 255) / 256);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    count_launch();
+    fused_combine<<<blocks, 256, 0, st>>>(M, N, fb, kp.ntn_b, *fs);
+    CUDA_TRY(cudaGetLastError());
+  }
   if (splits > 1) {
     int blocks = static_cast<int>(((int64_t)M * N + 255) / 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
@@ -765,6 +842,10 @@ int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, doub
   }
   if (K <= 0) {
     set_last_error("fused checksums need K > 0");
+    return -1;
+  }
+  if (!sums.rpp || !sums.bmp) {
+    set_last_error("fused checksums need the per-strip scratch arrays");
     return -1;
   }
   return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, nullptr, 1,

@@ -6,7 +6,10 @@ namespace abft {
 // Checksum outputs of the fused epilogue for an fb x fb block grid over D:
 // col plain cp[cp_step*bi + col*cp_ld], col weighted cw[...], row plain
 // rp[row + bj*rp_ld], block max bm[bi + bj*bm_ld] (all block-local indexing
-// relative to D's origin).
+// relative to D's origin). The GEMM's work unit is a 64-column strip of a
+// block, so row sums and the block max are first written per strip into the
+// scratch arrays rpp[row + (bj*fb/64 + s)*rpp_ld] and bmp[bi + (...)*bmp_ld]
+// (M x nbc*fb/64 and nbr x nbc*fb/64) and combined in a fixed order.
 struct FusedSums {
   double* cp = nullptr;
   int64_t cp_ld = 0, cp_step = 1;
@@ -16,6 +19,10 @@ struct FusedSums {
   int64_t rp_ld = 0;
   double* bm = nullptr;
   int64_t bm_ld = 0;
+  double* rpp = nullptr;  // per-strip row sums (scratch)
+  int64_t rpp_ld = 0;
+  double* bmp = nullptr;  // per-strip max|x| (scratch)
+  int64_t bmp_ld = 0;
 };
 
 struct GemmWorkspace {

@@ -166,7 +166,8 @@ class DistributedFactorization:
     column blocks on its GPU.
     """
 
-    def __init__(self, kind, a0: np.ndarray, b: int, group=None, device: int | None = None):
+    def __init__(self, kind, a0: np.ndarray, b: int, group=None, device: int | None = None,
+                 keep_input: bool = False):
         import torch
         import torch.distributed as dist
         self.kind = DecompositionKind(_value(kind))
@@ -185,6 +186,8 @@ class DistributedFactorization:
         check(lib.abft_dist_create(ctypes.byref(ctx), _lib.KIND_CODE[self.kind.value], n, self.b,
                                    self.device, self.rank, self.world))
         self._ctx = ctx
+        if keep_input:  # device copy of the local input for reset()
+            check(lib.abft_dist_keep_input(ctx, 1))
         host = np.asfortranarray(np.asarray(a0, dtype=np.float64))
         check(lib.abft_dist_set_matrix(ctx, _lib.dptr(host), n))
         self.ncl = int(lib.abft_dist_local_cols(ctx))
@@ -206,6 +209,18 @@ class DistributedFactorization:
     @property
     def k_done(self) -> int:
         return int(self._lib.abft_dist_k_done(self._ctx))
+
+    def set_matrix(self, a: np.ndarray) -> None:
+        """Load a new global input (owned column blocks are copied)."""
+        host = a if a.flags.f_contiguous else np.asfortranarray(a, dtype=np.float64)
+        check(self._lib.abft_dist_set_matrix(self._ctx, _lib.dptr(host), self.n))
+
+    def reset(self) -> None:
+        """Restore the kept input on the device (needs keep_input=True)."""
+        check(self._lib.abft_dist_reset(self._ctx))
+
+    def stream_ptr(self) -> int:
+        return int(self._lib.abft_dist_stream(self._ctx))
 
     @property
     def complete(self) -> bool:

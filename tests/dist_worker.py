@@ -35,7 +35,10 @@ def gpu_cases(rank: int, world: int, init_file: str, cases: list, out: str) -> N
     results = []
     for c in cases:
         a = P.generate_test_matrix(c["kind"], c["n"], c["seed"])
-        f = DistributedFactorization(c["kind"], a, c["b"])
+        f = DistributedFactorization(c["kind"], a, c["b"], keep_input=bool(c.get("reset")))
+        if c.get("reset"):  # a throw-away factorization, then restore the kept input
+            f.run_protected("none", {}, None)
+            f.reset()
         rng = np.random.default_rng(c["seed"])
         sched = {int(k): v for k, v in c.get("schedule", {}).items()}
         if c.get("per_iteration"):

@@ -80,6 +80,11 @@ CASES = [
      "schedule": {"0": {"1d": 1}, "4": {"0d": 1}}, "world": 3},
     {"name": "chol_w3", "kind": "cholesky", "n": 400, "b": 64, "scheme": "single", "seed": 8,
      "schedule": {"2": {"2d": 1}, "5": {"0d": 1}}, "world": 3, "per_iteration": True},
+    # b = 256 (the bench block size), device-side reset between factorizations
+    {"name": "lu_b256_reset", "kind": "lu", "n": 1024, "b": 256, "scheme": "full", "seed": 10,
+     "schedule": {"1": {"0d": 1}}, "world": 2, "reset": True},
+    {"name": "qr_b256", "kind": "qr", "n": 768, "b": 256, "scheme": "full", "seed": 11,
+     "schedule": {"0": {"0d": 1}}, "world": 2},
     # clean runs, no checksums
     {"name": "lu_none", "kind": "lu", "n": 512, "b": 128, "scheme": "none", "seed": 9,
      "schedule": {}, "world": 2},
