@@ -191,6 +191,9 @@ ABFT_API void* abft_dist_stream(abft_dist* d);
 ABFT_API int64_t abft_dist_xbuf_elems(abft_dist* d, int64_t k);
 /* owned column blocks of the host global matrix (column-major, lda) -> device */
 ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda);
+/* keep a device copy of the local input; abft_dist_reset restores it */
+ABFT_API int abft_dist_keep_input(abft_dist* d, int keep);
+ABFT_API int abft_dist_reset(abft_dist* d);
 /* local columns (n x local_cols) -> host */
 ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo);
 ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf);

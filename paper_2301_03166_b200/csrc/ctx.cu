@@ -180,6 +180,7 @@ int dalloc(double** p, int64_t elems) {
   CUDA_TRY(cudaMalloc(p, std::max<int64_t>(elems, 1) * sizeof(double)));
   if (poison_enabled())
     CUDA_TRY(cudaMemset(*p, 0xFF, std::max<int64_t>(elems, 1) * sizeof(double)));
+  if (poison_enabled()) CUDA_TRY(cudaDeviceSynchronize());  // order before non-blocking streams
   return 0;
 }
 

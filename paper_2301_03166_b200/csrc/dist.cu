@@ -55,9 +55,11 @@ struct DevGuardD {
   }
 };
 
-int dalloc0(double** p, int64_t elems) {
+// Zero-filled allocation, ordered on the context's (non-blocking) stream: a
+// legacy-stream cudaMemset could otherwise land after later work on `st`.
+int dalloc0(double** p, int64_t elems, cudaStream_t st) {
   CUDA_TRY(cudaMalloc(p, std::max<int64_t>(elems, 1) * sizeof(double)));
-  CUDA_TRY(cudaMemset(*p, 0, std::max<int64_t>(elems, 1) * sizeof(double)));
+  CUDA_TRY(cudaMemsetAsync(*p, 0, std::max<int64_t>(elems, 1) * sizeof(double), st));
   return 0;
 }
 
@@ -645,37 +647,37 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
     return -1000;
   }
   const int64_t ncl = std::max<int64_t>(d->ncl, 1), nbl = std::max<int64_t>(d->nbl, 1), ld = d->ld;
-  if ((rc = dalloc0(&d->m, ld * ncl))) return fail(rc);
-  if ((rc = dalloc0(&d->gcsw, d->ld_cs * ncl))) return fail(rc);
-  if ((rc = dalloc0(&d->csm, d->ld_cs * ncl))) return fail(rc);
-  if ((rc = dalloc0(&d->grs, ld * nbl))) return fail(rc);
-  if ((rc = dalloc0(&d->rsm, ld * nbl))) return fail(rc);
-  if ((rc = dalloc0(&d->gmax, d->ld_max * nbl))) return fail(rc);
-  if ((rc = dalloc0(&d->fpart, ld * 4 * nbl))) return fail(rc);
-  if ((rc = dalloc0(&d->fmaxp, d->ld_max * 4 * nbl))) return fail(rc);
-  if ((rc = dalloc0(&d->el, d->ld_cs * b))) return fail(rc);
-  if ((rc = dalloc0(&d->er, d->ld_t * std::max<int64_t>(nbl, b)))) return fail(rc);
-  if ((rc = dalloc0(&d->uw, d->ld_t * ncl))) return fail(rc);
-  if ((rc = dalloc0(&d->lw, ld * b))) return fail(rc);
-  if ((rc = dalloc0(&d->linv, d->ld_t * b))) return fail(rc);
-  if ((rc = dalloc0(&d->uinv, d->ld_t * b))) return fail(rc);
-  if ((rc = dalloc0(&d->dmax, 2))) return fail(rc);
-  if (kind == ABFT_CHOLESKY && (rc = dalloc0(&d->bext, d->ld_b * (b + 1)))) return fail(rc);
+  if ((rc = dalloc0(&d->m, ld * ncl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->gcsw, d->ld_cs * ncl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->csm, d->ld_cs * ncl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->grs, ld * nbl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->rsm, ld * nbl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->gmax, d->ld_max * nbl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->fpart, ld * 4 * nbl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->fmaxp, d->ld_max * 4 * nbl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->el, d->ld_cs * b, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->er, d->ld_t * std::max<int64_t>(nbl, b), d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->uw, d->ld_t * ncl, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->lw, ld * b, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->linv, d->ld_t * b, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->uinv, d->ld_t * b, d->st))) return fail(rc);
+  if ((rc = dalloc0(&d->dmax, 2, d->st))) return fail(rc);
+  if (kind == ABFT_CHOLESKY && (rc = dalloc0(&d->bext, d->ld_b * (b + 1), d->st))) return fail(rc);
   if (kind == ABFT_QR) {
-    if ((rc = dalloc0(&d->vstore, ld * n))) return fail(rc);
-    if ((rc = dalloc0(&d->tstore, d->nb * b * d->ld_t))) return fail(rc);
-    if ((rc = dalloc0(&d->betas, b))) return fail(rc);
+    if ((rc = dalloc0(&d->vstore, ld * n, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->tstore, d->nb * b * d->ld_t, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->betas, b, d->st))) return fail(rc);
     d->qr_part_elems = 2 * 160 * (b + 1);
-    if ((rc = dalloc0(&d->qr_part, d->qr_part_elems))) return fail(rc);
-    if ((rc = dalloc0(&d->qr_rowbuf, 2 * (b + 1) + 128))) return fail(rc);
-    if ((rc = dalloc0(&d->qr_part2, 160LL * 32 * b))) return fail(rc);
-    if ((rc = dalloc0(&d->qr_wfin, 32LL * b))) return fail(rc);
-    if ((rc = dalloc0(&d->gram, d->ld_t * b))) return fail(rc);
-    if ((rc = dalloc0(&d->ww, d->ld_t * ncl))) return fail(rc);
-    if ((rc = dalloc0(&d->mid, d->ld_t * ncl))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_part, d->qr_part_elems, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_rowbuf, 2 * (b + 1) + 128, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_part2, 160LL * 32 * b, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_wfin, 32LL * b, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->gram, d->ld_t * b, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->ww, d->ld_t * ncl, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->mid, d->ld_t * ncl, d->st))) return fail(rc);
   }
   d->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
-  if ((rc = dalloc0(&d->gws.ptr, d->gws.elems))) return fail(rc);
+  if ((rc = dalloc0(&d->gws.ptr, d->gws.elems, d->st))) return fail(rc);
   d->ev_cap = 1 << 16;
   if (cudaMalloc(&d->ev, d->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
   if (cudaMalloc(&d->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
@@ -744,7 +746,7 @@ ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda) {
                                d->n * 8, width(d, j), cudaMemcpyHostToDevice, d->st));
   }
   if (d->keep_input) {
-    if (!d->a0) ABFT_TRY(dalloc0(&d->a0, d->ld * std::max<int64_t>(d->ncl, 1)));
+    if (!d->a0) ABFT_TRY(dalloc0(&d->a0, d->ld * std::max<int64_t>(d->ncl, 1), d->st));
     CUDA_TRY(cudaMemcpyAsync(d->a0, d->m, d->ld * d->ncl * 8, cudaMemcpyDeviceToDevice, d->st));
   }
   CUDA_TRY(cudaStreamSynchronize(d->st));
