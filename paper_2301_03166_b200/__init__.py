@@ -16,5 +16,6 @@ from .linalg import (BlockLayout, DecompositionKind, Factorization,  # noqa: F40
 from .simulator import (CORRECTNESS_RESIDUAL, run_numeric_iteration,  # noqa: F401
                         run_protected)
 from .install import install, uninstall  # noqa: F401
+from . import governor  # noqa: F401  (run modes / adaptive ABFT / slack reclamation)
 
 __version__ = "0.1.0"

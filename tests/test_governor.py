@@ -1,0 +1,108 @@
+"""Run modes / adaptive ABFT / slack reclamation.
+
+CPU: the restated policy functions agree with the reference's own
+(coverage.py:137-230, scheduler.py:64-146) on a grid of inputs when the
+reference is importable, and with committed golden decisions otherwise.
+GPU: run_mode drives the B200 protected iteration with measured times.
+"""
+import json
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN
+from paper_2301_03166_b200 import governor as G
+
+GRID = [(f, t) for f in (1300.0, 1800.0, 1900.0, 2000.0, 2100.0, 2200.0)
+        for t in (1e-4, 1e-3, 1e-2, 0.1)]
+SIDES = [(tc, tg, r) for tc in (0.001, 0.01, 0.05) for tg in (0.002, 0.01, 0.04)
+         for r in (0.0, 0.3, 0.5, 1.0)]
+
+
+def _decisions():
+    table, cov = G.default_gpu_rate_table(), G.CoverageParams.for_matrix(8192, 256)
+    out = {"fc": [], "adaptive": [], "bsr": [], "sr": []}
+    for f, t in GRID:
+        out["fc"].append([G.fc_single(table, cov, f, t), G.fc_full(table, cov, f, t)])
+        d = G.adaptive_abft(cov, table, f, 1300.0, t, 300.0)
+        out["adaptive"].append([d.frequency, d.single_check, d.full_check])
+    for tc, tg, r in SIDES:
+        d = G.decide_bsr(G.panel_domain(), G.update_domain(), tc, tg, 0.0, r, cov, table)
+        out["bsr"].append([d.f_cpu_mhz, d.f_gpu_mhz, d.single_check, d.full_check, d.skipped])
+        d = G.decide_sr(G.panel_domain(), G.update_domain(), tc, tg, 0.0)
+        out["sr"].append([d.f_cpu_mhz, d.f_gpu_mhz])
+    return out
+
+
+def test_policy_matches_golden():
+    gold = json.loads((GOLDEN / "governor.json").read_text())
+    got = _decisions()
+    for key in ("adaptive", "bsr", "sr"):
+        assert got[key] == gold[key], key
+    np.testing.assert_allclose(np.array(got["fc"]), np.array(gold["fc"]), rtol=1e-12, atol=0)
+
+
+def test_policy_matches_reference_when_importable():
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import slackwise.coverage as RC
+        import slackwise.power as RP
+        import slackwise.scheduler as RS
+    except ImportError:
+        pytest.skip("reference not importable here")
+    table, cov = RC.default_gpu_rate_table(), RC.CoverageParams.for_matrix(8192, 256)
+    got = _decisions()
+    for i, (f, t) in enumerate(GRID):
+        assert got["fc"][i][0] == pytest.approx(RC.fc_single(table, cov, f, t), rel=1e-12, abs=0)
+        assert got["fc"][i][1] == pytest.approx(RC.fc_full(table, cov, f, t), rel=1e-12, abs=0)
+        d = RC.adaptive_abft(cov, table, f, 1300.0, t, 300.0)
+        assert got["adaptive"][i] == [d.frequency, d.single_check, d.full_check]
+    cpu, gpu = RP.default_cpu_model(), RP.default_gpu_model()
+    for i, (tc, tg, r) in enumerate(SIDES):
+        d = RS.decide_bsr(cpu, gpu, tc, tg, 0.0, r, cov, table)
+        assert got["bsr"][i] == [d.f_cpu_mhz, d.f_gpu_mhz, d.single_check, d.full_check, d.skipped]
+        d = RS.decide_sr(cpu, gpu, tc, tg, 0.0)
+        assert got["sr"][i] == [d.f_cpu_mhz, d.f_gpu_mhz]
+
+
+def test_mode_flags():
+    assert G.mode_from_flags(True, True, False) == "bsr"
+    assert G.mode_from_flags(False, False, True) == "r2h"
+    assert G.MODE_FLAGS["bsr"]["col_ft"] and G.MODE_FLAGS["bsr"]["row_ft"]
+    with pytest.raises(ValueError):
+        G.mode_from_flags(True, False, True)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
+def test_run_modes_on_b200(kind):
+    import paper_2301_03166_b200 as P
+    n, b = 1024, 128
+    a = P.generate_test_matrix(kind, n, 2)
+    out = {}
+    for mode in G.MODES:
+        s, recs = G.run_mode(kind, a, b, mode, r=1.0, seed=2)
+        assert s.correct and s.residual < 1e-12, (mode, s)
+        assert len(recs) == -(-n // b)
+        assert all(rc.t_update_ms >= 0 and rc.t_panel_ms >= 0 for rc in recs)
+        out[mode] = s
+    # unprotected modes inject nothing (base clocks are fault-free)
+    for mode in ("original", "r2h", "sr"):
+        assert out[mode].abft_ms == 0.0 and sum(out[mode].faults_injected.values()) == 0
+        assert set(out[mode].schemes) == {"none"}
+    # bsr: overclocked iterations run under adaptive checksums, every
+    # injected fault is detected and the factorization stays correct
+    s = out["bsr"]
+    assert s.faults_detected >= sum(s.faults_injected.values()) > 0 or s.schemes.get("none") == len(recs)
+    assert s.energy_j is None or s.energy_j > 0
+
+
+@pytest.mark.gpu
+def test_forced_full_scheme_overhead_is_measured():
+    import paper_2301_03166_b200 as P
+    a = P.generate_test_matrix("lu", 1024, 0)
+    s_full, _ = G.run_mode("lu", a, 128, "bsr", r=0.5, seed=0, forced_scheme="full")
+    s_none, _ = G.run_mode("lu", a, 128, "original", seed=0)
+    assert s_full.abft_ms > 0.0 and s_none.abft_ms == 0.0
+    assert s_full.schemes == {"full": 8}
