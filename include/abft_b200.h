@@ -104,6 +104,13 @@ ABFT_API int abft_dev_dgemm(void* stream, char transa, char transb, int64_t m, i
                             const double* B, int64_t ldb, double beta, const double* C,
                             int64_t ldc, double* D, int64_t ldd);
 
+/* fp32 device-pointer GEMM on the tcgen05 tensor cores (kind::tf32 with a
+ * 3xTF32 split for fp32 accuracy): D = beta*C + alpha*op(A)*op(B). */
+ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, int64_t n,
+                            int64_t k, float alpha, const float* A, int64_t lda, const float* B,
+                            int64_t ldb, float beta, const float* C, int64_t ldc, float* D,
+                            int64_t ldd);
+
 /* factorization context: replaces Factorization (linalg.py:159-359) -------- */
 typedef struct abft_ctx abft_ctx;
 

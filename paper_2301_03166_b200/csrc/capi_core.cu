@@ -1,6 +1,7 @@
 // Library-level C-ABI entry points (no context): version, errors, device-pointer GEMM.
 #include "abft_b200.h"
 #include "gemm.cuh"
+#include "sgemm.cuh"
 
 using namespace abft;
 
@@ -82,6 +83,24 @@ ABFT_API int abft_dev_dgemm(void* stream, char transa, char transb, int64_t m, i
   int rc = gemm(st, transa, transb, (int)m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C, ldc, D,
                 ldd, &ws, splits);
   if (ws.ptr) cudaFreeAsync(ws.ptr, st);
+  return rc;
+}
+
+// fp32 device-pointer GEMM on tcgen05 (3xTF32): D = beta*C + alpha*op(A)*op(B)
+ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                            float alpha, const float* A, int64_t lda, const float* B, int64_t ldb,
+                            float beta, const float* C, int64_t ldc, float* D, int64_t ldd) {
+  if (m < 0 || n < 0 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
+    set_last_error("abft_dev_sgemm: bad dimensions");
+    return ABFT_E_INVALID;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int64_t wse = sgemm_workspace_elems((int)m, (int)n, (int)k);
+  float* ws = nullptr;
+  CUDA_TRY(cudaMallocAsync(&ws, wse * sizeof(float), st));
+  int rc = sgemm_tc(st, transa, transb, (int)m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C, ldc,
+                    D, ldd, ws, wse);
+  cudaFreeAsync(ws, st);
   return rc;
 }
 

@@ -1,0 +1,464 @@
+// FP32 GEMM on the 5th-generation tensor cores (tcgen05, kind::tf32) for the
+// s* factorizations: D = beta*C + alpha*op(A)*op(B), column-major fp32.
+//
+// FP32 accuracy from TF32 tensor cores (3xTF32): each operand is split once
+// into hi = rna_tf32(x) and lo = x - hi, and every k-step issues
+//   acc += A_lo B_hi + A_hi B_lo + A_hi B_hi
+// (the lo*lo term is below fp32 resolution). The split kernel also writes
+// both operands K-major, so the MMA always reads the canonical K-major
+// 128-byte-swizzled shared-memory layout TMA produces.
+//
+// Kernel structure (persistent, one CTA per SM, 192 threads):
+//   warp 0      TMA producer: 4 boxes (A_hi, A_lo, B_hi, B_lo) per 32-wide
+//               k-block into a 3-stage mbarrier ring (64 KB per stage)
+//   warp 1      allocates 256 TMEM columns; one lane issues tcgen05.mma
+//               (M=128, N=128, K=8) into a double-buffered TMEM accumulator
+//               and commits stages / finished tiles to mbarriers
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one row per thread),
+//               D = beta*C + alpha*acc with warp-coalesced column accesses,
+//               and (fused mode, checksum block = tile = 128 x 128) the
+//               block's column plain / index-weighted sums, row sums and
+//               max|x| accumulated in fp64 -- the verify-side checksums of
+//               abft.py:118-135 without another pass over D.
+// The TMEM double buffer lets the epilogue of tile i overlap the MMAs of
+// tile i+1.
+#include "sgemm.cuh"
+
+#include <cstring>
+#include <mutex>
+
+#include <cudaTypedefs.h>
+
+namespace abft {
+
+namespace {
+
+constexpr int TBM = 128, TBN = 128, TBK = 32;  // TBK fp32 = one 128-byte swizzle row
+constexpr int TSTAGES = 3;
+constexpr int T_A_BYTES = TBM * TBK * 4;
+constexpr int T_B_BYTES = TBN * TBK * 4;
+constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;  // 64 KB
+constexpr int T_THREADS = 192;
+constexpr int T_TMEM_COLS = 256;  // two 128-column fp32 accumulators
+constexpr int T_TP = 33;          // padded transpose tile
+// smem: ring | barriers (2*ST + 4) | tmem slot | per-warp transpose tiles |
+//        per-warp column partials (double) | warp max
+constexpr int T_BAR_OFF = TSTAGES * T_STAGE_BYTES;
+constexpr int T_TR_OFF = T_BAR_OFF + 256;
+constexpr int T_TR_BYTES = 4 * 32 * T_TP * 4;
+constexpr int T_COL_OFF = T_TR_OFF + T_TR_BYTES;
+constexpr int T_COL_BYTES = 4 * TBN * 2 * 8;
+constexpr int T_SMEM = T_COL_OFF + T_COL_BYTES + 64 + 1024;
+
+struct SParams {
+  int M, N, K;
+  int tiles_m, tiles_n, nkb;
+  const float* C;
+  int64_t ldc;
+  float* D;
+  int64_t ldd;
+  float alpha, beta;
+  int fuse;
+  FusedSums sums;
+};
+
+// K-major SWIZZLE_128B shared-memory matrix descriptor (tcgen05 / UMMA):
+// start address >> 4, LBO 16 B (unused for swizzled K-major), SBO 1024 B
+// (8 rows x 128 B), descriptor version 1, layout type 2 = SWIZZLE_128B.
+ABFT_DEVINL uint64_t sdesc(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)(16u >> 4) << 16;
+  d |= (uint64_t)(1024u >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, both K-major,
+// M = 128, N = 128.
+constexpr uint32_t IDESC = (1u << 4)            // c_format F32
+                           | (2u << 7)          // a_format TF32
+                           | (2u << 10)         // b_format TF32
+                           | ((uint32_t)(TBN >> 3) << 17)
+                           | ((uint32_t)(TBM >> 4) << 24);
+
+ABFT_DEVINL void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accum) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(IDESC), "r"(accum));
+}
+
+ABFT_DEVINL void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+
+ABFT_DEVINL void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+ABFT_DEVINL void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+
+ABFT_DEVINL void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+      "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__global__ void __launch_bounds__(T_THREADS, 1)
+    sgemm_tc05_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
+                      const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
+                      SParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + T_BAR_OFF);
+  uint64_t* empty = full + TSTAGES;
+  uint64_t* tfull = empty + TSTAGES;   // [2]
+  uint64_t* tempty = tfull + 2;        // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  float* trs = reinterpret_cast<float*>(smem + T_TR_OFF);
+  double* colp = reinterpret_cast<double*>(smem + T_COL_OFF);  // [4 quarters][TBN][2]
+  double* wmaxs = colp + 4 * TBN * 2;                         // [4]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tiles = p.tiles_m * p.tiles_n;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TSTAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    mbar_fence_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "n"(T_TMEM_COLS)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ===== TMA producer =====
+    if (lane == 0) {
+      tma_prefetch_desc(&mAh);
+      tma_prefetch_desc(&mAl);
+      tma_prefetch_desc(&mBh);
+      tma_prefetch_desc(&mBl);
+      uint32_t q = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+        for (int kb = 0; kb < p.nkb; ++kb, ++q) {
+          const int s = q % TSTAGES;
+          if (q >= TSTAGES) mbar_wait(&empty[s], ((q / TSTAGES) - 1) & 1);
+          uint8_t* st = smem + s * T_STAGE_BYTES;
+          mbar_arrive_expect_tx(&full[s], T_STAGE_BYTES);
+          tma_load_2d(st, &mAh, &full[s], kb * TBK, tm * TBM);
+          tma_load_2d(st + T_A_BYTES, &mAl, &full[s], kb * TBK, tm * TBM);
+          tma_load_2d(st + 2 * T_A_BYTES, &mBh, &full[s], kb * TBK, tn * TBN);
+          tma_load_2d(st + 2 * T_A_BYTES + T_B_BYTES, &mBl, &full[s], kb * TBK, tn * TBN);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===== MMA issuer =====
+    uint32_t q = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1, use = it >> 1;
+      if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);
+      tc_fence_after();
+      const uint32_t dt = tmem_base + (uint32_t)(acc * TBN);
+      for (int kb = 0; kb < p.nkb; ++kb, ++q) {
+        const int s = q % TSTAGES;
+        mbar_wait(&full[s], (q / TSTAGES) & 1);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t st = smem_u32(smem + s * T_STAGE_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < TBK / 8; ++ks) {
+            const uint32_t off = ks * 32;  // 8 tf32 = 32 bytes along K
+            const uint64_t ah = sdesc(st + off), al = sdesc(st + T_A_BYTES + off);
+            const uint64_t bh = sdesc(st + 2 * T_A_BYTES + off);
+            const uint64_t bl = sdesc(st + 2 * T_A_BYTES + T_B_BYTES + off);
+            mma_tf32(dt, al, bh, (kb | ks) ? 1u : 0u);
+            mma_tf32(dt, ah, bl, 1u);
+            mma_tf32(dt, ah, bh, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        __syncwarp();
+      }
+      if (lane == 0) mma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else {
+    // ===== epilogue (warps 2..5) =====
+    const int quarter = warp & 3;               // TMEM lane quarter of this warp
+    const int row_t = quarter * 32 + lane;      // row within the tile
+    float* tr = trs + quarter * 32 * T_TP;      // this warp's 32 x 33 transpose tile
+    double* cq = colp + quarter * TBN * 2;
+    const int etid = threadIdx.x - 64;          // 0..127
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1, use = it >> 1;
+      const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
+      const int m = tm * TBM + row_t;
+      const bool rv = m < p.M;
+      double rsum = 0.0, mx = 0.0;
+#pragma unroll 1
+      for (int cc = 0; cc < TBN / 32; ++cc) {
+        float v[32];
+        tmem_ld32(tmem_base + (uint32_t)(acc * TBN + cc * 32) + ((uint32_t)(quarter * 32) << 16), v);
+        const int c0 = tn * TBN + cc * 32;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int col = c0 + j;
+          const bool ok = rv && col < p.N;
+          float o = p.alpha * v[j];
+          if (ok && p.beta != 0.0f) o = fmaf(p.beta, p.C[m + (int64_t)col * p.ldc], o);
+          if (ok) p.D[m + (int64_t)col * p.ldd] = o;
+          v[j] = ok ? o : 0.0f;
+        }
+        if (p.fuse) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            rsum += (double)v[j];
+            mx = fmax(mx, fabs((double)v[j]));
+            tr[lane * T_TP + j] = v[j];
+          }
+          __syncwarp();
+          // lane j: column c0 + j summed over this warp's 32 rows
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll 8
+          for (int r = 0; r < 32; ++r) {
+            const double x = (double)tr[r * T_TP + lane];
+            a0 += x;
+            a1 = fma((double)(quarter * 32 + r), x, a1);
+          }
+          cq[(cc * 32 + lane) * 2 + 0] = a0;
+          cq[(cc * 32 + lane) * 2 + 1] = a1;
+          __syncwarp();
+        }
+      }
+      // accumulator drained: hand TMEM back to the MMA warp
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      if (p.fuse) {
+        const FusedSums& fs = p.sums;
+        if (rv) fs.rp[m + (int64_t)tn * fs.rp_ld] = rsum;
+        mx = warp_max(mx);
+        if (lane == 0) wmaxs[quarter] = mx;
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        const int gc = tn * TBN + etid;
+        if (gc < p.N) {
+          double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            s0 += colp[(qq * TBN + etid) * 2 + 0];
+            s1 += colp[(qq * TBN + etid) * 2 + 1];
+          }
+          fs.cp[fs.cp_step * tm + (int64_t)gc * fs.cp_ld] = s0;
+          fs.cw[fs.cw_step * tm + (int64_t)gc * fs.cw_ld] = s1;
+        }
+        if (etid == 0)
+          fs.bm[tm + (int64_t)tn * fs.bm_ld] =
+              fmax(fmax(wmaxs[0], wmaxs[1]), fmax(wmaxs[2], wmaxs[3]));
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base),
+                 "n"(T_TMEM_COLS)
+                 : "memory");
+  }
+}
+
+// hi = rna_tf32(x), lo = x - hi, written K-major: out[r * ldo + k].
+// trans = 0: src is (R x K) column-major (element (r, k) at r + k * lds),
+//            transposed through a 32 x 33 shared tile;
+// trans = 1: src already holds (r, k) at k + r * lds (a plain copy).
+__global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, int R, int K, int trans,
+                                  float* __restrict__ hi, float* __restrict__ lo, int64_t ldo) {
+  __shared__ float tile[32][33];
+  const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  if (!trans) {
+    for (int i = ty; i < 32; i += 8) {
+      const int r = r0 + tx, k = k0 + i;
+      tile[i][tx] = (r < R && k < K) ? src[r + (int64_t)k * lds] : 0.0f;
+    }
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+      const int r = r0 + i, k = k0 + tx;
+      if (r < R && k < ldo) {
+        const float x = (k < K) ? tile[tx][i] : 0.0f;
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
+        const float hf = __uint_as_float(h);
+        hi[(int64_t)r * ldo + k] = hf;
+        lo[(int64_t)r * ldo + k] = x - hf;
+      }
+    }
+  } else {
+    for (int i = ty; i < 32; i += 8) {
+      const int r = r0 + i, k = k0 + tx;
+      if (r < R && k < ldo) {
+        const float x = (k < K) ? src[k + (int64_t)r * lds] : 0.0f;
+        uint32_t h;
+        asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
+        const float hf = __uint_as_float(h);
+        hi[(int64_t)r * ldo + k] = hf;
+        lo[(int64_t)r * ldo + k] = x - hf;
+      }
+    }
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  });
+  return fn;
+}
+
+// 2-D map over a K-major fp32 array (rows x ldk, K contiguous), box 32 x 128, 128B swizzle.
+int kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ldk) {
+  auto fn = encode_fn();
+  if (!fn) {
+    set_last_error("cuTensorMapEncodeTiled unavailable");
+    return -20;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)ldk, (cuuint64_t)(rows < 1 ? 1 : rows)};
+  cuuint64_t strides[1] = {(cuuint64_t)(ldk * 4)};
+  cuuint32_t box[2] = {TBK, 128};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_last_error("cuTensorMapEncodeTiled(fp32) failed (%d): rows=%lld ldk=%lld", (int)r,
+                   (long long)rows, (long long)ldk);
+    return -22;
+  }
+  return 0;
+}
+
+}  // namespace
+
+int64_t sgemm_workspace_elems(int M, int N, int K) {
+  const int64_t ldk = (K + 3) / 4 * 4;
+  return 2 * ((int64_t)M + N) * ldk + 64;
+}
+
+int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha, const float* A,
+             int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
+             float* D, int64_t ldd, float* ws, int64_t ws_elems, const FusedSums* fs, int max_ctas) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) {
+    set_last_error("sgemm_tc needs K > 0");
+    return -1;
+  }
+  const int64_t ldk = (K + 3) / 4 * 4;
+  if (!ws || ws_elems < sgemm_workspace_elems(M, N, K)) {
+    set_last_error("sgemm_tc workspace too small");
+    return -1;
+  }
+  // 256-byte aligned operand copies inside the workspace
+  auto align = [](float* q) {
+    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q) + 255) & ~uintptr_t(255));
+  };
+  float* ah = align(ws);
+  float* al = align(ah + (int64_t)M * ldk);
+  float* bh = align(al + (int64_t)M * ldk);
+  float* bl = align(bh + (int64_t)N * ldk);
+  if (bl + (int64_t)N * ldk > ws + ws_elems) {
+    set_last_error("sgemm_tc workspace too small (alignment)");
+    return -1;
+  }
+  // A: op(A) is M x K. 'N': (m, k) at m + k*lda -> transpose; 'T': (m, k) at k + m*lda -> copy.
+  const bool AT = (ta == 'T' || ta == 't');
+  const bool BT = (tb == 'T' || tb == 't');
+  {
+    dim3 g((unsigned)((ldk + 31) / 32), (unsigned)((M + 31) / 32));
+    count_launch();
+    tf32_split_kernel<<<g, 256, 0, st>>>(A, lda, M, K, AT ? 1 : 0, ah, al, ldk);
+  }
+  {
+    // op(B) is K x N; B' row n = column n of op(B): 'N': (k, n) at k + n*ldb -> copy;
+    // 'T': (k, n) at n + k*ldb -> transpose.
+    dim3 g((unsigned)((ldk + 31) / 32), (unsigned)((N + 31) / 32));
+    count_launch();
+    tf32_split_kernel<<<g, 256, 0, st>>>(B, ldb, N, K, BT ? 0 : 1, bh, bl, ldk);
+  }
+  CUDA_TRY(cudaGetLastError());
+  CUtensorMap mah, mal, mbh, mbl;
+  ABFT_TRY(kmajor_map(&mah, ah, M, ldk));
+  ABFT_TRY(kmajor_map(&mal, al, M, ldk));
+  ABFT_TRY(kmajor_map(&mbh, bh, N, ldk));
+  ABFT_TRY(kmajor_map(&mbl, bl, N, ldk));
+  SParams p;
+  p.M = M;
+  p.N = N;
+  p.K = K;
+  p.tiles_m = (M + TBM - 1) / TBM;
+  p.tiles_n = (N + TBN - 1) / TBN;
+  p.nkb = (K + TBK - 1) / TBK;
+  p.C = C;
+  p.ldc = ldc;
+  p.D = D;
+  p.ldd = ldd;
+  p.alpha = alpha;
+  p.beta = (C == nullptr) ? 0.0f : beta;
+  p.fuse = fs ? 1 : 0;
+  if (fs) p.sums = *fs;
+  static bool attr = false;
+  if (!attr) {
+    CUDA_TRY(cudaFuncSetAttribute(sgemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  T_SMEM));
+    attr = true;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
+  const int tiles = p.tiles_m * p.tiles_n;
+  const int grid = tiles < sms ? tiles : sms;
+  count_launch();
+  sgemm_tc05_kernel<<<grid, T_THREADS, T_SMEM, st>>>(mah, mal, mbh, mbl, p);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace abft

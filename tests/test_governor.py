@@ -89,7 +89,8 @@ def test_run_modes_on_b200(kind):
         out[mode] = s
     # unprotected modes inject nothing (base clocks are fault-free)
     for mode in ("original", "r2h", "sr"):
-        assert out[mode].abft_ms == 0.0 and sum(out[mode].faults_injected.values()) == 0
+        assert out[mode].abft_ms < 0.02 * out[mode].device_ms  # only empty timer brackets
+        assert sum(out[mode].faults_injected.values()) == 0
         assert set(out[mode].schemes) == {"none"}
     # bsr: overclocked iterations run under adaptive checksums, every
     # injected fault is detected and the factorization stays correct
@@ -104,5 +105,20 @@ def test_forced_full_scheme_overhead_is_measured():
     a = P.generate_test_matrix("lu", 1024, 0)
     s_full, _ = G.run_mode("lu", a, 128, "bsr", r=0.5, seed=0, forced_scheme="full")
     s_none, _ = G.run_mode("lu", a, 128, "original", seed=0)
-    assert s_full.abft_ms > 0.0 and s_none.abft_ms == 0.0
+    assert s_full.abft_ms > 5 * s_none.abft_ms
     assert s_full.schemes == {"full": 8}
+
+
+@pytest.mark.gpu
+def test_forced_scheme_campaign_corrects_injected_faults():
+    """fault_campaign-style run (simulator.py:683-710): forced checksums at
+    unclamped bsr clocks with rates scaled to the B200's short update
+    intervals, so faults do occur; FULL repairs what it detects."""
+    import paper_2301_03166_b200 as P
+    a = P.generate_test_matrix("lu", 2048, 1)
+    table = G.scaled_rate_table(5e3)
+    s, recs = G.run_mode("lu", a, 256, "bsr", r=1.0, seed=1, rates=table, forced_scheme="full",
+                         recovery="recompute")
+    assert sum(s.faults_injected.values()) > 0
+    assert s.faults_detected > 0
+    assert s.correct, s

@@ -1,0 +1,51 @@
+"""GPU: the tcgen05 fp32 GEMM (kind::tf32, 3xTF32) against a float64
+reference of the same op. Bound: |D - D_ref| <= 2e-6 * (|alpha| |A||B| + |beta||C|)
+elementwise (fp32 accuracy; plain TF32 would be ~1e-3)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0):
+    import torch
+    from paper_2301_03166_b200 import _lib
+    lib = _lib.load()
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    a_shape = (m, k) if ta == "N" else (k, m)
+    b_shape = (k, n) if tb == "N" else (n, k)
+    # column-major storage = transpose of a row-major torch tensor
+    A = torch.randn(a_shape[::-1], generator=g, dtype=torch.float32).cuda()
+    B = torch.randn(b_shape[::-1], generator=g, dtype=torch.float32).cuda()
+    C = torch.randn((n, m), generator=g, dtype=torch.float32).cuda()
+    D = torch.empty((n, m), dtype=torch.float32, device="cuda")
+    rc = lib.abft_dev_sgemm(None, ta.encode(), tb.encode(), m, n, k, alpha, A.data_ptr(),
+                            a_shape[0], B.data_ptr(), b_shape[0], beta,
+                            C.data_ptr() if beta else None, m, D.data_ptr(), m)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    An = A.double().cpu().numpy().T
+    Bn = B.double().cpu().numpy().T
+    opA = An if ta == "N" else An.T
+    opB = Bn if tb == "N" else Bn.T
+    Cn = C.double().cpu().numpy().T
+    ref = alpha * (opA @ opB) + beta * Cn
+    mag = abs(alpha) * (np.abs(opA) @ np.abs(opB)) + abs(beta) * np.abs(Cn)
+    got = D.double().cpu().numpy().T
+    return got, ref, mag
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("N", "T"), ("T", "N"), ("T", "T")])
+@pytest.mark.parametrize("m,n,k", [(128, 128, 32), (256, 384, 128), (300, 200, 100), (1000, 517, 256)])
+def test_sgemm_tc05_matches_fp64_reference(ta, tb, m, n, k):
+    got, ref, mag = _run(ta, tb, m, n, k, alpha=-1.0, beta=1.0)
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-6 * mag + 1e-30), float((err / (mag + 1e-30)).max())
+
+
+def test_sgemm_tc05_large_k_and_alpha():
+    got, ref, mag = _run("N", "N", 512, 512, 2048, alpha=0.5, beta=0.0)
+    err = np.abs(got - ref)
+    assert np.all(err <= 2e-6 * mag), float((err / mag).max())

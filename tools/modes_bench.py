@@ -17,19 +17,25 @@ ap.add_argument("--kind", default="lu")
 ap.add_argument("--n", type=int, default=8192)
 ap.add_argument("--b", type=int, default=256)
 ap.add_argument("--seed", type=int, default=0)
-ap.add_argument("--rate-scale", type=float, default=2e4)
+ap.add_argument("--rate-scale", type=float, default=2e3,
+                help="fault-rate scale of the forced-scheme campaign runs")
 ap.add_argument("--sweep", action="store_true")
 args = ap.parse_args()
 a = P.generate_test_matrix(args.kind, args.n, args.seed)
-table = G.scaled_rate_table(args.rate_scale)
 G.run_mode(args.kind, a, args.b, "original", seed=args.seed)  # warm-up
-runs = [(m, 0.5) for m in G.MODES]
+# (mode, r, forced scheme, rate scale): the reference's rates for the mode
+# comparison and the r sweep; forced-scheme campaign runs with scaled rates
+runs = [(m, 0.5, None, 1.0) for m in G.MODES]
 if args.sweep:
-    runs += [("bsr", r) for r in (0.0, 0.25, 0.5, 0.75, 1.0)]
-for mode, r in runs:
-    s, recs = G.run_mode(args.kind, a, args.b, mode, r=r, seed=args.seed, rates=table)
+    runs += [("bsr", r, None, 1.0) for r in (0.0, 0.25, 0.75, 1.0)]
+    runs += [("bsr", 1.0, sch, args.rate_scale) for sch in ("none", "single", "full")]
+for mode, r, forced, scale in runs:
+    s, recs = G.run_mode(args.kind, a, args.b, mode, r=r, seed=args.seed,
+                         rates=G.scaled_rate_table(scale), forced_scheme=forced,
+                         recovery="continue" if forced == "none" else "recompute")
     d = dataclasses.asdict(s)
-    d["rate_scale"] = args.rate_scale
+    d["rate_scale"] = scale
+    d["forced_scheme"] = forced
     d["f_gpu_mhz"] = [rc.f_gpu_mhz for rc in recs]
     d["abft_modes"] = "".join(rc.abft_mode[0] for rc in recs)
     print(json.dumps(d), flush=True)
