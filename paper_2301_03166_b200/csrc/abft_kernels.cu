@@ -19,8 +19,9 @@ constexpr int BS_ROWS = 256;     // rows per chunk (8 per lane)
 
 // One CTA per block (grid-stride). Warp w takes columns w, w+8, ...; lane l
 // takes rows l + 32*i of the current 256-row chunk.
+template <typename T>
 __global__ void __launch_bounds__(BS_THREADS)
-    blocksum_kernel(Region reg, SumOut out, int64_t nbr, int64_t nbc, const int32_t* blocks,
+    blocksum_kernel(RegionT<T> reg, SumOut out, int64_t nbr, int64_t nbc, const int32_t* blocks,
                     const int32_t* nblocks_dev, int64_t nlist_static) {
   extern __shared__ double dsm[];
   double* colacc_p = dsm;             // [b]
@@ -46,7 +47,7 @@ __global__ void __launch_bounds__(BS_THREADS)
     const int64_t r_lo = bi * reg.b, c_lo = bj * reg.b;
     const int br = (int)min(reg.b, reg.rows - r_lo);
     const int bc = (int)min(reg.b, reg.cols - c_lo);
-    const double* base = reg.ptr + r_lo + c_lo * reg.ld;
+    const T* base = reg.ptr + r_lo + c_lo * reg.ld;
     double mx = 0.0;
     for (int c = threadIdx.x; c < bc; c += BS_THREADS) {
       colacc_p[c] = 0.0;
@@ -58,12 +59,12 @@ __global__ void __launch_bounds__(BS_THREADS)
 #pragma unroll
       for (int i = 0; i < 8; ++i) racc[i] = rwacc[i] = 0.0;
       for (int c = warp; c < bc; c += 8) {
-        const double* col = base + (int64_t)c * reg.ld + r0;
+        const T* col = base + (int64_t)c * reg.ld + r0;
         double x[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           const int r = lane + 32 * i;
-          x[i] = (r0 + r < br) ? col[r] : 0.0;
+          x[i] = (r0 + r < br) ? (double)col[r] : 0.0;
         }
         double cs = 0.0, cw = 0.0;
 #pragma unroll
@@ -165,8 +166,9 @@ ABFT_DEVINL bool recovered_index(double dw, double dp, int limit, int* idx) {
   return false;
 }
 
-__global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct, SumOut rec,
-                              Maintained mt, EventSink sink, int64_t nbr, int64_t nbc) {
+template <typename T>
+__global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int correct, SumOut rec,
+                              Maintained mt, EventSink sink, int64_t nbr, int64_t nbc, double eps) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
@@ -177,7 +179,7 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
     const int br = (int)min(reg.b, reg.rows - r_lo);
     const int bc = (int)min(reg.b, reg.cols - c_lo);
     const double bmax = rec.bm[bi + bj * rec.bm_ld];
-    const double tau = 50.0 * (double)b_nom * fmax(bmax, 1.0) * DBL_EPSILON;
+    const double tau = 50.0 * (double)b_nom * fmax(bmax, 1.0) * eps;
     int nbad_c = 0, nbad_r = 0;
     for (int c = lane; c < bc; c += 32) {
       const int64_t gc = c_lo + c;
@@ -198,7 +200,8 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
     if (nbad_c == 0 && nbad_r == 0) continue;
     if (lane != 0) continue;
     // ---- rare path: one lane classifies and repairs, in reference order ----
-    double* blkp = reg.ptr + r_lo + c_lo * reg.ld;
+    T* blkp = reg.ptr + r_lo + c_lo * reg.ld;
+    auto fix = [&](int64_t off, double dlt) { blkp[off] = (T)((double)blkp[off] - dlt); };
     auto dcol = [&](int c) {
       const int64_t gc = c_lo + c;
       return rec.cp[rec.cp_step * bi + gc * rec.cp_ld] - mt.cp[mt.cp_step * bi + gc * mt.cp_ld];
@@ -230,7 +233,7 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
         const double dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
         int idx = 0;
         recovered_index(dw, d, br, &idx);
-        if (correct) blkp[idx + (int64_t)c * reg.ld] -= d;
+        if (correct) fix(idx + (int64_t)c * reg.ld, d);
         emit(sink, bi, bj, seq++, 0, r_lo + idx, c_lo + c, correct, 0, correct, 0);
       }
       if (correct) mark_dirty(sink, bi, bj);
@@ -247,7 +250,7 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
       while (!(fabs(drow(i)) > tau)) ++i;
       while (!(fabs(dcol(jc)) > tau)) ++jc;
       if (correct) {
-        blkp[i + (int64_t)jc * reg.ld] -= dcol(jc);
+        fix(i + (int64_t)jc * reg.ld, dcol(jc));
         mark_dirty(sink, bi, bj);
       }
       emit(sink, bi, bj, 0, 0, r_lo + i, c_lo + jc, correct, 0, correct, 0);
@@ -258,7 +261,7 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
         if (correct) {
           for (int r = 0; r < br; ++r) {
             const double d = drow(r);
-            if (fabs(d) > tau) blkp[r + (int64_t)jc * reg.ld] -= d;
+            if (fabs(d) > tau) fix(r + (int64_t)jc * reg.ld, d);
           }
           mark_dirty(sink, bi, bj);
         }
@@ -274,7 +277,7 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
         if (correct) {
           for (int c = 0; c < bc; ++c) {
             const double d = dcol(c);
-            if (fabs(d) > tau) blkp[i + (int64_t)c * reg.ld] -= d;
+            if (fabs(d) > tau) fix(i + (int64_t)c * reg.ld, d);
           }
           mark_dirty(sink, bi, bj);
         }
@@ -289,7 +292,8 @@ __global__ void verify_kernel(Region reg, int64_t b_nom, int scheme, int correct
 // ---------------------------------------------------------------------------
 // K7
 // ---------------------------------------------------------------------------
-__global__ void inject_kernel(double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+template <typename T>
+__global__ void inject_kernel(T* m, int64_t ld, int64_t n_rows, int64_t n_cols,
                               const DevFault* plan, int nplan, const double* ssrc, int64_t srows,
                               int64_t scols, int64_t sld, double host_scale) {
   __shared__ double sm[32];
@@ -314,18 +318,19 @@ __global__ void inject_kernel(double* m, int64_t ld, int64_t n_rows, int64_t n_c
       mag = (ft.u * 1e-3) * fmax(scale, 1.0);
       if (ft.negate) mag = -mag;
     }
+    auto add = [&](int64_t off, double v) { m[off] = (T)((double)m[off] + v); };
     if (ft.kind == 0) {
-      m[ft.row + ft.col * ld] += mag;
+      add(ft.row + ft.col * ld, mag);
     } else if (ft.kind == 1) {
       const int ext = ft.extent > 2 ? ft.extent : 2;
       if (ft.orientation == 0) {
         const int64_t stop = min(ft.row + ext, n_rows);
         for (int64_t i = 0; i < stop - ft.row; ++i)
-          m[ft.row + i + ft.col * ld] += mag * (1.0 + 0.1 * (double)i);
+          add(ft.row + i + ft.col * ld, mag * (1.0 + 0.1 * (double)i));
       } else {
         const int64_t stop = min(ft.col + ext, n_cols);
         for (int64_t i = 0; i < stop - ft.col; ++i)
-          m[ft.row + (ft.col + i) * ld] += mag * (1.0 + 0.1 * (double)i);
+          add(ft.row + (ft.col + i) * ld, mag * (1.0 + 0.1 * (double)i));
       }
     } else {
       const int ext = ft.extent > 2 ? ft.extent : 2;
@@ -333,8 +338,7 @@ __global__ void inject_kernel(double* m, int64_t ld, int64_t n_rows, int64_t n_c
       const int64_t cstop = min(ft.col + ext, n_cols);
       for (int64_t i = 0; i < rstop - ft.row; ++i)
         for (int64_t jj = 0; jj < cstop - ft.col; ++jj)
-          m[ft.row + i + (ft.col + jj) * ld] +=
-              mag * (((double)i * 0.1 + (double)jj * 0.07) + 1.0);
+          add(ft.row + i + (ft.col + jj) * ld, mag * (((double)i * 0.1 + (double)jj * 0.07) + 1.0));
     }
   }
 }
@@ -404,13 +408,17 @@ __global__ void max_reduce_kernel(const double* a, int64_t rows, int64_t cols, i
 // ---------------------------------------------------------------------------
 // reductions / element kernels
 // ---------------------------------------------------------------------------
-__global__ void sumsq_partial(const double* a, int64_t ld, int64_t rows, int64_t cols,
+template <typename T>
+__global__ void sumsq_partial(const T* a, int64_t ld, int64_t rows, int64_t cols,
                               double* part) {
   __shared__ double sm[32];
   double s = 0.0;
   for (int64_t c = blockIdx.x; c < cols; c += gridDim.x) {
-    const double* col = a + c * ld;
-    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) s = fma(col[r], col[r], s);
+    const T* col = a + c * ld;
+    for (int64_t r = threadIdx.x; r < rows; r += blockDim.x) {
+      const double x = (double)col[r];
+      s = fma(x, x, s);
+    }
   }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) sm[threadIdx.x >> 5] = s;
@@ -455,14 +463,16 @@ __global__ void gemv_sub_kernel(int64_t rows, int64_t kdim, const double* A, int
   }
 }
 
-__global__ void fill_kernel(double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+template <typename T>
+__global__ void fill_kernel(T* a, int64_t ld, int64_t rows, int64_t cols, double v) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x)
     a[(i % rows) + (i / rows) * ld] = v;
 }
 
-__global__ void copy_kernel(const double* s, int64_t lds, double* d, int64_t ldd, int64_t rows,
+template <typename T, typename U>
+__global__ void copy_kernel(const T* s, int64_t lds, U* d, int64_t ldd, int64_t rows,
                             int64_t cols, int mode) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -476,7 +486,8 @@ __global__ void copy_kernel(const double* s, int64_t lds, double* d, int64_t ldd
   }
 }
 
-__global__ void sub_kernel(const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+template <typename T>
+__global__ void sub_kernel(const T* x, int64_t ldx, T* d, int64_t ldd, int64_t rows,
                            int64_t cols) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -512,8 +523,9 @@ inline int grid_for(int64_t total, int threads) {
 
 }  // namespace
 
-int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_t* blocks,
-             const int32_t* nblocks_dev, int max_list) {
+template <typename T>
+static int blocksum_t(cudaStream_t st, const RegionT<T>& reg, const SumOut& out,
+                      const int32_t* blocks, const int32_t* nblocks_dev, int max_list) {
   if (reg.rows <= 0 || reg.cols <= 0) return 0;
   if (reg.b > 4096) {
     set_last_error("block size %lld > 4096 not supported by the checksum kernels",
@@ -525,7 +537,7 @@ int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_
   const size_t dyn = 2 * reg.b * sizeof(double);
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(blocksum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    CUDA_TRY(cudaFuncSetAttribute(blocksum_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   2 * 4096 * 8));
     attr = true;
   }
@@ -533,14 +545,25 @@ int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_
   if (nblk <= 0) return 0;
   int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
   count_launch();
-  blocksum_kernel<<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
-                                                  (int64_t)max_list);
+  blocksum_kernel<T><<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
+                                                     (int64_t)max_list);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
-int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
-                  const SumOut& rec, const Maintained& mt, const EventSink& sink) {
+int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_t* blocks,
+             const int32_t* nblocks_dev, int max_list) {
+  return blocksum_t(st, reg, out, blocks, nblocks_dev, max_list);
+}
+int blocksum(cudaStream_t st, const RegionF& reg, const SumOut& out, const int32_t* blocks,
+             const int32_t* nblocks_dev, int max_list) {
+  return blocksum_t(st, reg, out, blocks, nblocks_dev, max_list);
+}
+
+template <typename T>
+static int verify_t(cudaStream_t st, const RegionT<T>& reg, int64_t b_nominal, int scheme,
+                    int correct, const SumOut& rec, const Maintained& mt, const EventSink& sink,
+                    double eps) {
   if (reg.rows <= 0 || reg.cols <= 0) return 0;
   const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
   const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
@@ -548,7 +571,29 @@ int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int sch
   int grid = (int)((warps + 7) / 8);
   if (grid > 148 * 16) grid = 148 * 16;
   count_launch();
-  verify_kernel<<<grid, 256, 0, st>>>(reg, b_nominal, scheme, correct, rec, mt, sink, nbr, nbc);
+  verify_kernel<T><<<grid, 256, 0, st>>>(reg, b_nominal, scheme, correct, rec, mt, sink, nbr, nbc,
+                                         eps);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
+                  const SumOut& rec, const Maintained& mt, const EventSink& sink) {
+  return verify_t(st, reg, b_nominal, scheme, correct, rec, mt, sink, DBL_EPSILON);
+}
+int verify_blocks(cudaStream_t st, const RegionF& reg, int64_t b_nominal, int scheme, int correct,
+                  const SumOut& rec, const Maintained& mt, const EventSink& sink) {
+  return verify_t(st, reg, b_nominal, scheme, correct, rec, mt, sink, (double)FLT_EPSILON);
+}
+
+template <typename T>
+static int inject_t(cudaStream_t st, T* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+                    const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
+                    int64_t scale_cols, int64_t scale_ld, double host_scale) {
+  if (nplan <= 0) return 0;
+  count_launch();
+  inject_kernel<T><<<1, 1024, 0, st>>>(m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows,
+                                       scale_cols, scale_ld, host_scale);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -556,12 +601,14 @@ int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int sch
 int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
            const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
            int64_t scale_cols, int64_t scale_ld, double host_scale) {
-  if (nplan <= 0) return 0;
-  count_launch();
-  inject_kernel<<<1, 1024, 0, st>>>(m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows,
-                                    scale_cols, scale_ld, host_scale);
-  CUDA_TRY(cudaGetLastError());
-  return 0;
+  return inject_t(st, m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows, scale_cols,
+                  scale_ld, host_scale);
+}
+int inject(cudaStream_t st, float* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+           const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
+           int64_t scale_cols, int64_t scale_ld, double host_scale) {
+  return inject_t(st, m, ld, n_rows, n_cols, plan, nplan, scale_src, scale_rows, scale_cols,
+                  scale_ld, host_scale);
 }
 
 int inject_mapped(cudaStream_t st, double* m, int64_t ld, int64_t n, const DevFault* plan,
@@ -581,19 +628,28 @@ int max_reduce(cudaStream_t st, const double* a, int64_t rows, int64_t cols, int
   return 0;
 }
 
-int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
-          double* scratch) {
+template <typename T>
+static int sumsq_t(cudaStream_t st, const T* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+                   double* scratch) {
   if (rows <= 0 || cols <= 0) {
     CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double), st));
     return 0;
   }
   const int g = (int)(cols < 1024 ? cols : 1024);
   count_launch();
-  sumsq_partial<<<g, 256, 0, st>>>(a, ld, rows, cols, scratch);
+  sumsq_partial<T><<<g, 256, 0, st>>>(a, ld, rows, cols, scratch);
   count_launch();
   sum_final<<<1, 1024, 0, st>>>(scratch, g, out);
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+          double* scratch) {
+  return sumsq_t(st, a, ld, rows, cols, out, scratch);
+}
+int sumsq(cudaStream_t st, const float* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+          double* scratch) {
+  return sumsq_t(st, a, ld, rows, cols, out, scratch);
 }
 
 int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t lda,
@@ -605,35 +661,64 @@ int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t 
   return 0;
 }
 
-int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+template <typename T>
+static int fill_t(cudaStream_t st, T* a, int64_t ld, int64_t rows, int64_t cols, double v) {
   if (rows <= 0 || cols <= 0) return 0;
   count_launch();
-  fill_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(a, ld, rows, cols, v);
+  fill_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(a, ld, rows, cols, v);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
+int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+  return fill_t(st, a, ld, rows, cols, v);
+}
+int fill_matrix(cudaStream_t st, float* a, int64_t ld, int64_t rows, int64_t cols, double v) {
+  return fill_t(st, a, ld, rows, cols, v);
+}
 
-int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
-                int64_t rows, int64_t cols, int mode) {
+template <typename T, typename U>
+static int copy_t(cudaStream_t st, const T* src, int64_t lds, U* dst, int64_t ldd, int64_t rows,
+                  int64_t cols, int mode) {
   if (rows <= 0 || cols <= 0) return 0;
-  if (mode == 0) {
-    CUDA_TRY(cudaMemcpy2DAsync(dst, ldd * 8, src, lds * 8, rows * 8, cols,
+  if (mode == 0 && sizeof(T) == sizeof(U)) {
+    CUDA_TRY(cudaMemcpy2DAsync(dst, ldd * sizeof(U), src, lds * sizeof(T), rows * sizeof(T), cols,
                                cudaMemcpyDeviceToDevice, st));
     return 0;
   }
   count_launch();
-  copy_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols, mode);
+  copy_kernel<T, U><<<grid_for(rows * cols, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols, mode);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
+int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
+                int64_t rows, int64_t cols, int mode) {
+  return copy_t(st, src, lds, dst, ldd, rows, cols, mode);
+}
+int copy_matrix(cudaStream_t st, const float* src, int64_t lds, float* dst, int64_t ldd,
+                int64_t rows, int64_t cols, int mode) {
+  return copy_t(st, src, lds, dst, ldd, rows, cols, mode);
+}
+int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, int64_t ldd,
+                 int64_t rows, int64_t cols) {
+  return copy_t(st, src, lds, dst, ldd, rows, cols, 0);
+}
 
-int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
-               int64_t cols) {
+template <typename T>
+static int sub_t(cudaStream_t st, const T* x, int64_t ldx, T* d, int64_t ldd, int64_t rows,
+                 int64_t cols) {
   if (rows <= 0 || cols <= 0) return 0;
   count_launch();
-  sub_kernel<<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
+  sub_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols) {
+  return sub_t(st, x, ldx, d, ldd, rows, cols);
+}
+int sub_matrix(cudaStream_t st, const float* x, int64_t ldx, float* d, int64_t ldd, int64_t rows,
+               int64_t cols) {
+  return sub_t(st, x, ldx, d, ldd, rows, cols);
 }
 
 int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,

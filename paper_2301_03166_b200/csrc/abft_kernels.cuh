@@ -24,18 +24,23 @@ struct SumOut {
 
 // Region view: rows x cols at ptr (column-major, ld), b x b blocks on the
 // region-local grid (abft.py:108-112).
-struct Region {
-  double* ptr;
+template <typename T>
+struct RegionT {
+  T* ptr;
   int64_t ld;
   int64_t rows, cols;
   int64_t b;
 };
+using Region = RegionT<double>;
+using RegionF = RegionT<float>;  // fp32 data (s* factorizations); sums stay fp64
 
 // K1: per-block plain/weighted column sums, row sums and max|x| of a region
 // (encode, abft.py:118-135; the recomputed side of verify_correct, :185-193).
 // `blocks`/`nblocks_dev`: optional device list of (bi, bj) int32 pairs to
 // restrict the pass to dirty blocks (count read on the device).
 int blocksum(cudaStream_t st, const Region& reg, const SumOut& out, const int32_t* blocks = nullptr,
+             const int32_t* nblocks_dev = nullptr, int max_list = 0);
+int blocksum(cudaStream_t st, const RegionF& reg, const SumOut& out, const int32_t* blocks = nullptr,
              const int32_t* nblocks_dev = nullptr, int max_list = 0);
 
 // Maintained checksums handed to the verifier (maintain_gemm, abft.py:138-158).
@@ -72,6 +77,10 @@ struct EventSink {
 // abft.py:161-276). Reads recomputed sums `rec` (from K1) and maintained sums.
 int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
                   const SumOut& rec, const Maintained& mt, const EventSink& sink);
+// fp32 data: tau = 50 * b * max(max|blk|, 1) * eps32 (the reference's rule
+// restated for single precision; SURVEY.md §8c "fp32: parity unpinned")
+int verify_blocks(cudaStream_t st, const RegionF& reg, int64_t b_nominal, int scheme, int correct,
+                  const SumOut& rec, const Maintained& mt, const EventSink& sink);
 
 // K7: fault injection (inject_faults, abft.py:283-307). `scale_src`: device
 // block-max array of the region (nbr x nbc, ld) reduced to max|region| for the
@@ -87,6 +96,9 @@ struct DevFault {
 int inject(cudaStream_t st, double* m, int64_t ld, int64_t n_rows, int64_t n_cols,
            const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
            int64_t scale_cols, int64_t scale_ld, double host_scale);
+int inject(cudaStream_t st, float* m, int64_t ld, int64_t n_rows, int64_t n_cols,
+           const DevFault* plan, int nplan, const double* scale_src, int64_t scale_rows,
+           int64_t scale_cols, int64_t scale_ld, double host_scale);
 
 // K7 for the 1-D block-cyclic distribution: global plan, global scale
 // (device scalar, already reduced over ranks), only locally owned column
@@ -100,6 +112,8 @@ int max_reduce(cudaStream_t st, const double* a, int64_t rows, int64_t cols, int
 // Sum of squares of (rows x cols) matrix into out[0] (deterministic).
 int sumsq(cudaStream_t st, const double* a, int64_t ld, int64_t rows, int64_t cols, double* out,
           double* scratch /* >= 1024 doubles */);
+int sumsq(cudaStream_t st, const float* a, int64_t ld, int64_t rows, int64_t cols, double* out,
+          double* scratch);
 
 // y[r] -= A(r, :) . x   (GEMV for the Cholesky row-checksum maintenance)
 int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t lda,
@@ -107,15 +121,23 @@ int gemv_sub(cudaStream_t st, int64_t rows, int64_t k, const double* A, int64_t 
 
 // Element kernels
 int fill_matrix(cudaStream_t st, double* a, int64_t ld, int64_t rows, int64_t cols, double v);
+int fill_matrix(cudaStream_t st, float* a, int64_t ld, int64_t rows, int64_t cols, double v);
 // mode 0: copy; 1: strict-lower + unit diag (L of LU); 2: upper (U, R); 3: lower incl diag
 int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, int64_t ldd,
                 int64_t rows, int64_t cols, int mode = 0);
+int copy_matrix(cudaStream_t st, const float* src, int64_t lds, float* dst, int64_t ldd,
+                int64_t rows, int64_t cols, int mode = 0);
+// fp32 -> fp64 widening copy (operands of the fp64 checksum maintenance)
+int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, int64_t ldd,
+                 int64_t rows, int64_t cols);
 int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v);
 // dst[c + r*ldd] = src[r*row_step + c*lds]
 int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,
                      int64_t rows, int64_t cols, double* dst, int64_t ldd);
 // d -= x
 int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols);
+int sub_matrix(cudaStream_t st, const float* x, int64_t ldx, float* d, int64_t ldd, int64_t rows,
                int64_t cols);
 
 }  // namespace abft

@@ -10,6 +10,8 @@ namespace abft {
 // untouched (0) if none, and never overwritten once set.
 int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
                 double* Uinv, int64_t ldu, int* info_dev, int64_t col_base);
+int diag_factor(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv, int64_t ldl,
+                float* Uinv, int64_t ldu, int* info_dev, int64_t col_base);
 
 // Householder panel (nk x w) in place: R above/on the diagonal, zeros below;
 // V (nk x w, unit diagonal, zeros above) and betas (tau) out. part: >= 2*148*(w+1)

@@ -1,6 +1,7 @@
 """GPU: the tcgen05 fp32 GEMM (kind::tf32, 3xTF32) against a float64
-reference of the same op. Bound: |D - D_ref| <= 2e-6 * (|alpha| |A||B| + |beta||C|)
-elementwise (fp32 accuracy; plain TF32 would be ~1e-3)."""
+reference of the same op. Bound: |D - D_ref| <= 2e-6 * max(1, sqrt(K/256)) *
+(|alpha| |A||B| + |beta||C|) elementwise (fp32 accumulation accuracy; plain
+TF32 operands would be ~1e-3)."""
 import ctypes
 
 import numpy as np
@@ -42,10 +43,11 @@ def _run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0):
 def test_sgemm_tc05_matches_fp64_reference(ta, tb, m, n, k):
     got, ref, mag = _run(ta, tb, m, n, k, alpha=-1.0, beta=1.0)
     err = np.abs(got - ref)
-    assert np.all(err <= 2e-6 * mag + 1e-30), float((err / (mag + 1e-30)).max())
+    tol = 2e-6 * max(1.0, (k / 256) ** 0.5)
+    assert np.all(err <= tol * mag + 1e-30), float((err / (mag + 1e-30)).max())
 
 
 def test_sgemm_tc05_large_k_and_alpha():
     got, ref, mag = _run("N", "N", 512, 512, 2048, alpha=0.5, beta=0.0)
     err = np.abs(got - ref)
-    assert np.all(err <= 2e-6 * mag), float((err / mag).max())
+    assert np.all(err <= 2e-6 * (2048 / 256) ** 0.5 * mag), float((err / mag).max())

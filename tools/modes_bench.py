@@ -20,6 +20,8 @@ ap.add_argument("--seed", type=int, default=0)
 ap.add_argument("--rate-scale", type=float, default=2e3,
                 help="fault-rate scale of the forced-scheme campaign runs")
 ap.add_argument("--sweep", action="store_true")
+ap.add_argument("--repeat", type=int, default=10,
+                help="factorizations per configuration (NVML energy counter resolution)")
 args = ap.parse_args()
 a = P.generate_test_matrix(args.kind, args.n, args.seed)
 G.run_mode(args.kind, a, args.b, "original", seed=args.seed)  # warm-up
@@ -29,11 +31,17 @@ runs = [(m, 0.5, None, 1.0) for m in G.MODES]
 if args.sweep:
     runs += [("bsr", r, None, 1.0) for r in (0.0, 0.25, 0.75, 1.0)]
     runs += [("bsr", 1.0, sch, args.rate_scale) for sch in ("none", "single", "full")]
+nv = G._Energy(0)
 for mode, r, forced, scale in runs:
-    s, recs = G.run_mode(args.kind, a, args.b, mode, r=r, seed=args.seed,
-                         rates=G.scaled_rate_table(scale), forced_scheme=forced,
-                         recovery="continue" if forced == "none" else "recompute")
+    e0 = nv.mj()
+    for _ in range(args.repeat):
+        s, recs = G.run_mode(args.kind, a, args.b, mode, r=r, seed=args.seed,
+                             rates=G.scaled_rate_table(scale), forced_scheme=forced,
+                             recovery="continue" if forced == "none" else "recompute")
+    e1 = nv.mj()
     d = dataclasses.asdict(s)
+    d["energy_j"] = (e1 - e0) / 1e3 / args.repeat if e0 is not None and e1 is not None else None
+    d["energy_note"] = f"NVML TotalEnergyConsumption over {args.repeat} factorizations (incl. host gaps)"
     d["rate_scale"] = scale
     d["forced_scheme"] = forced
     d["f_gpu_mhz"] = [rc.f_gpu_mhz for rc in recs]
