@@ -221,6 +221,34 @@ ABFT_API int abft_dist_elapsed_ms(abft_dist* d, double* ms);
 ABFT_API int abft_set_qr_panel(abft_ctx* ctx, int64_t k, const double* V, int64_t ldv,
                                const double* T, int64_t ldt);
 
+/* single precision (the s* variants: sgetrf / spotrf) ---------------------
+ * Same task order, regions, fault plan semantics, events and error codes as
+ * the fp64 context above; fp32 data (tcgen05 kind::tf32 GEMMs with a 3xTF32
+ * split), fp64 block checksums, tau = 50 * b * max(max|blk|, 1) * eps32.
+ * The reference has no fp32 path (parity unpinned). */
+typedef struct abft_sctx abft_sctx;
+ABFT_API int abft_s_create(abft_sctx** ctx, int kind, int64_t n, int64_t b, int device);
+ABFT_API int abft_s_destroy(abft_sctx* ctx);
+ABFT_API void* abft_s_stream(abft_sctx* ctx);
+ABFT_API int64_t abft_s_k_done(abft_sctx* ctx);
+ABFT_API int abft_s_keep_input(abft_sctx* ctx, int keep);
+ABFT_API int abft_s_set_matrix(abft_sctx* ctx, const float* a, int64_t lda);
+ABFT_API int abft_s_reset(abft_sctx* ctx);
+ABFT_API int abft_s_make_spd(abft_sctx* ctx);
+ABFT_API int abft_s_get_matrix(abft_sctx* ctx, float* m, int64_t ldm);
+ABFT_API int abft_s_iteration(abft_sctx* ctx, int64_t k, int scheme, const abft_fault* plan,
+                              int nplan, int correct, abft_report* rep, abft_location* locs,
+                              int max_locs);
+ABFT_API int abft_s_factorize(abft_sctx* ctx, int scheme, const int32_t* schemes,
+                              const abft_fault* plan, const int64_t* plan_iter, int nplan,
+                              int correct, abft_report* reports, abft_location* locs,
+                              int max_locs, int* n_locs);
+ABFT_API int abft_s_last_elapsed_ms(abft_sctx* ctx, double* ms);
+ABFT_API int abft_s_profile(abft_sctx* ctx, int enable);
+ABFT_API int abft_s_profile_read(abft_sctx* ctx, double* ms);
+ABFT_API int abft_s_residual(abft_sctx* ctx, const float* a0, int64_t lda, double* out);
+ABFT_API int64_t abft_s_breakdown_column(abft_sctx* ctx);
+
 /* region ABFT on host arrays: encode / maintain_gemm / verify_correct /
  * inject_faults (abft.py:118-307), executed on the device. Checksums are
  * column-major arrays: col_plain/col_weighted (nbr x cols, ld nbr),

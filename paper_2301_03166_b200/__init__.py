@@ -16,6 +16,7 @@ from .linalg import (BlockLayout, DecompositionKind, Factorization,  # noqa: F40
 from .simulator import (CORRECTNESS_RESIDUAL, run_numeric_iteration,  # noqa: F401
                         run_protected)
 from .install import install, uninstall  # noqa: F401
+from .single import SFactorization  # noqa: F401  (fp32 s* variants on tcgen05)
 from . import governor  # noqa: F401  (run modes / adaptive ABFT / slack reclamation)
 
 __version__ = "0.1.0"

@@ -52,6 +52,7 @@ class Report(ctypes.Structure):
 
 _P = ctypes.c_void_p
 _D = ctypes.POINTER(ctypes.c_double)
+_F = ctypes.POINTER(ctypes.c_float)
 _I64 = ctypes.c_int64
 _I = ctypes.c_int
 
@@ -112,6 +113,25 @@ SIGNATURES = [
     ("abft_dist_get_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
     ("abft_dist_elapsed_ms", _I, [_P, _D]),
     ("abft_set_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
+    ("abft_s_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
+    ("abft_s_destroy", _I, [_P]),
+    ("abft_s_stream", _P, [_P]),
+    ("abft_s_k_done", _I64, [_P]),
+    ("abft_s_keep_input", _I, [_P, _I]),
+    ("abft_s_set_matrix", _I, [_P, _F, _I64]),
+    ("abft_s_reset", _I, [_P]),
+    ("abft_s_make_spd", _I, [_P]),
+    ("abft_s_get_matrix", _I, [_P, _F, _I64]),
+    ("abft_s_iteration", _I, [_P, _I64, _I, ctypes.POINTER(Fault), _I, _I, ctypes.POINTER(Report),
+                              ctypes.POINTER(Location), _I]),
+    ("abft_s_factorize", _I, [_P, _I, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(Fault),
+                              ctypes.POINTER(ctypes.c_int64), _I, _I, ctypes.POINTER(Report),
+                              ctypes.POINTER(Location), _I, ctypes.POINTER(_I)]),
+    ("abft_s_last_elapsed_ms", _I, [_P, _D]),
+    ("abft_s_profile", _I, [_P, _I]),
+    ("abft_s_profile_read", _I, [_P, _D]),
+    ("abft_s_residual", _I, [_P, _F, _I64, _D]),
+    ("abft_s_breakdown_column", _I64, [_P]),
     ("abft_region_encode", _I, [_D, _I64, _I64, _I64, _I64, _I, _D, _D, _D, _D]),
     ("abft_region_maintain", _I, [_I64, _I64, _I64, _I64, _I, _D, _I64, _D, _I64, _D, _D, _D,
                                   _D]),
@@ -156,3 +176,7 @@ def last_error() -> str:
 
 def dptr(a) -> "ctypes._Pointer":
     return a.ctypes.data_as(_D)
+
+
+def fptr(a) -> "ctypes._Pointer":
+    return a.ctypes.data_as(_F)

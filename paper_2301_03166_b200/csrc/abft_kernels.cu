@@ -509,7 +509,8 @@ __global__ void gather_transpose_kernel(const double* src, int64_t row_step, int
   }
 }
 
-__global__ void add_diag_kernel(double* a, int64_t ld, int64_t n, double v) {
+template <typename T>
+__global__ void add_diag_kernel(T* a, int64_t ld, int64_t n, double v) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x)
     a[i + i * ld] += v;
@@ -731,12 +732,19 @@ int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64
   return 0;
 }
 
-int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v) {
+template <typename T>
+static int add_diag_t(cudaStream_t st, T* a, int64_t ld, int64_t n, double v) {
   if (n <= 0) return 0;
   count_launch();
-  add_diag_kernel<<<grid_for(n, 256), 256, 0, st>>>(a, ld, n, v);
+  add_diag_kernel<T><<<grid_for(n, 256), 256, 0, st>>>(a, ld, n, v);
   CUDA_TRY(cudaGetLastError());
   return 0;
+}
+int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v) {
+  return add_diag_t(st, a, ld, n, v);
+}
+int add_diag(cudaStream_t st, float* a, int64_t ld, int64_t n, double v) {
+  return add_diag_t(st, a, ld, n, v);
 }
 
 }  // namespace abft

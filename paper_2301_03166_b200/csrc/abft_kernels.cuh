@@ -131,6 +131,7 @@ int copy_matrix(cudaStream_t st, const float* src, int64_t lds, float* dst, int6
 int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, int64_t ldd,
                  int64_t rows, int64_t cols);
 int add_diag(cudaStream_t st, double* a, int64_t ld, int64_t n, double v);
+int add_diag(cudaStream_t st, float* a, int64_t ld, int64_t n, double v);
 // dst[c + r*ldd] = src[r*row_step + c*lds]
 int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,
                      int64_t rows, int64_t cols, double* dst, int64_t ldd);

@@ -1,0 +1,826 @@
+// Single-precision factorization context (the s* variants of the north star:
+// sgetrf / spotrf) on the tcgen05 fp32 GEMM (sgemm_tc05.cu).
+//
+// Same algorithm, task order, regions, fault semantics and event order as
+// the fp64 context (ctx.cu, restating linalg.py:159-359 and
+// simulator.py:86-167); the data is fp32, the block checksums, their
+// maintenance and verification stay fp64 (abft.py:118-276 with tau on eps32,
+// the reference has no fp32 path, so parity is unpinned and
+// checked against the fp64 oracle's fault outcomes).
+//   LU       right-looking: PD = diag factor + L21 = A21 U11^{-1} (tcgen05),
+//            PU = L11^{-1} A12 (tcgen05), TMU = A22 -= L21 U12 with the block
+//            checksums produced in the GEMM epilogue (b = 128).
+//   Cholesky left-looking like the reference: TMU = panel -= L L^T (tcgen05),
+//            PD = diag factor, PU = L21 = A21 L11^{-T} (tcgen05).
+// The maintenance products run on the fp64 DMMA GEMM from widened operands.
+#include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "abft_b200.h"
+#include "abft_kernels.cuh"
+#include "gemm.cuh"
+#include "panel.cuh"
+#include "sgemm.cuh"
+
+using namespace abft;
+
+namespace {
+
+inline int64_t s_round_even(int64_t x) { return (x + 1) / 2 * 2; }
+inline int64_t s_round_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+struct SGuard {
+  int prev = -1;
+  explicit SGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~SGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <typename T>
+int salloc(T** p, int64_t elems, cudaStream_t st) {
+  CUDA_TRY(cudaMalloc(p, std::max<int64_t>(elems, 1) * sizeof(T)));
+  CUDA_TRY(cudaMemsetAsync(*p, 0, std::max<int64_t>(elems, 1) * sizeof(T), st));
+  return 0;
+}
+
+enum { SP_PD = 0, SP_PU = 1, SP_TMU = 2, SP_ABFT = 3 };
+
+}  // namespace
+
+struct abft_sctx {
+  int kind = 0;
+  int64_t n = 0, b = 0, nb = 0, ld = 0;
+  int device = 0;
+  cudaStream_t st = nullptr;
+  float* m = nullptr;
+  float* a0 = nullptr;
+  bool keep_input = false;
+  // fp64 checksums on the global block grid (as ctx.cu)
+  double* gcsw = nullptr;
+  int64_t ld_cs = 0;
+  double* grs = nullptr;
+  double* gmax = nullptr;
+  int64_t ld_max = 0;
+  double* csm = nullptr;
+  double* rsm = nullptr;
+  double* el = nullptr;
+  double* er = nullptr;
+  int64_t ld_t = 0;
+  double* lwd = nullptr;  // widened left operand (n x b, or n x n for Cholesky's L)
+  double* uwd = nullptr;  // widened right operand (b x n)
+  // fp32 workspaces
+  float* lw = nullptr;    // n x b
+  float* uw = nullptr;    // b x n
+  float* linv = nullptr;
+  float* uinv = nullptr;
+  float* sws = nullptr;   // sgemm split-operand workspace
+  int64_t sws_elems = 0;
+  double* scratch = nullptr;
+  GemmWorkspace gws;
+  Event* ev = nullptr;
+  int32_t* counters = nullptr;
+  int ev_cap = 0;
+  int32_t* dirty = nullptr;
+  int dirty_cap = 0;
+  DevFault* dplan = nullptr;
+  int dplan_cap = 0;
+  int32_t* dlist = nullptr;
+  int dlist_cap = 0;
+  int* info = nullptr;
+  int64_t k_done = 0;
+  bool sums_valid = false;
+  int64_t breakdown_col = -1;
+  bool fuse_enabled = true;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  bool timed = false;
+  bool prof_on = false;
+  double prof_ms[4] = {0, 0, 0, 0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> prof_pending;
+  cudaEvent_t prof_open[4] = {nullptr, nullptr, nullptr, nullptr};
+};
+
+namespace {
+
+void smark(abft_sctx* c, int cat, bool begin) {
+  if (!c->prof_on) return;
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  cudaEventRecord(e, c->st);
+  if (begin) {
+    c->prof_open[cat] = e;
+  } else {
+    c->prof_pending.push_back({cat, {c->prof_open[cat], e}});
+    c->prof_open[cat] = nullptr;
+  }
+}
+
+void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* rows, int64_t* cols) {
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n);
+  if (c->kind == ABFT_CHOLESKY) {
+    *r0 = p; *c0 = p; *rows = c->n - p; *cols = pe - p;
+  } else {
+    *r0 = pe; *c0 = pe; *rows = c->n - pe; *cols = c->n - pe;
+  }
+}
+
+SumOut s_sums(abft_sctx* c, int64_t r0, int64_t c0, bool rows_too) {
+  SumOut o;
+  const int64_t gbi = r0 / c->b, gbj = c0 / c->b;
+  o.cp = c->gcsw + 2 * gbi + c0 * c->ld_cs;
+  o.cp_ld = c->ld_cs;
+  o.cp_step = 2;
+  o.cw = o.cp + 1;
+  o.cw_ld = c->ld_cs;
+  o.cw_step = 2;
+  if (rows_too) {
+    o.rp = c->grs + r0 + gbj * c->ld;
+    o.rp_ld = c->ld;
+  }
+  o.bm = c->gmax + gbi + gbj * c->ld_max;
+  o.bm_ld = c->ld_max;
+  return o;
+}
+
+int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, float alpha,
+           const float* A, int64_t lda, const float* B, int64_t ldb, float beta, const float* C,
+           int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  const int64_t need = sgemm_workspace_elems((int)M, (int)N, (int)K);
+  if (need > c->sws_elems) {
+    if (c->sws) cudaFreeAsync(c->sws, c->st);
+    c->sws_elems = need;
+    CUDA_TRY(cudaMallocAsync(&c->sws, need * sizeof(float), c->st));
+  }
+  return sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C, ldc, D,
+                  ldd, c->sws, c->sws_elems, fs);
+}
+
+int s_check_info(abft_sctx* c) {
+  int h = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h, c->info, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (h != 0) {
+    c->breakdown_col = h - 1;
+    set_last_error(c->kind == ABFT_CHOLESKY ? "non-positive pivot at column %lld"
+                                            : "zero pivot at column %lld",
+                   (long long)c->breakdown_col);
+    CUDA_TRY(cudaMemsetAsync(c->info, 0, sizeof(int), c->st));
+    return ABFT_E_BREAKDOWN;
+  }
+  return 0;
+}
+
+// ---- tasks -------------------------------------------------------------------
+int s_pd(abft_sctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  float* D = c->m + p + p * c->ld;
+  if (c->kind == ABFT_LU) {
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info, p));
+    if (pe < n) {
+      ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, w, w, 1.0f, D + w, c->ld, c->uinv, c->ld_t, 0.0f, nullptr,
+                      0, c->lw, c->ld));
+      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, D + w, c->ld, n - pe, w));
+    }
+  } else {
+    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+  }
+  return 0;
+}
+
+int s_pu(abft_sctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (c->kind == ABFT_LU) {
+    if (pe < n) {
+      float* U12 = c->m + p + pe * c->ld;
+      ABFT_TRY(s_gemm(c, 'N', 'N', w, n - pe, w, 1.0f, c->linv, c->ld_t, U12, c->ld, 0.0f, nullptr, 0,
+                      c->uw, c->ld_t));
+      ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, U12, c->ld, w, n - pe));
+    }
+  } else {
+    if (pe < n) {
+      float* A21 = c->m + pe + p * c->ld;
+      ABFT_TRY(s_gemm(c, 'N', 'T', n - pe, w, w, 1.0f, A21, c->ld, c->linv, c->ld_t, 0.0f, nullptr, 0,
+                      c->lw, c->ld));
+      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, A21, c->ld, n - pe, w));
+      ABFT_TRY(fill_matrix(c->st, c->m + p + pe * c->ld, c->ld, w, n - pe, 0.0));
+    }
+    // block-row sums of the finished panel: operand sums of later maintenance
+    RegionF reg{c->m + p + p * c->ld, c->ld, n - p, w, c->b};
+    SumOut o = s_sums(c, p, p, false);
+    o.bm = nullptr;
+    ABFT_TRY(blocksum(c->st, reg, o));
+  }
+  return 0;
+}
+
+// maintain_gemm (abft.py:138-158) in fp64 from widened operands.
+int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t rows,
+               int64_t cols) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+  SumOut enc = s_sums(c, r0, c0, scheme == ABFT_FULL);
+  if (c->kind == ABFT_CHOLESKY) {
+    // col: CSm = CS - GCSW[2k:, 0:p] * m[p:pe, 0:p]^T ; row: RSm = RS - L * rvec
+    ABFT_TRY(widen_matrix(c->st, c->m + p, c->ld, c->uwd, c->ld_t, w, p));  // R^T rows (w x p)
+    ABFT_TRY(gemm(c->st, 'N', 'T', (int)(2 * nbr), (int)w, (int)p, -1.0, c->gcsw + 2 * k, c->ld_cs,
+                  c->uwd, c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
+    if (scheme == ABFT_FULL) {
+      ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
+      if (p > 0) {
+        ABFT_TRY(widen_matrix(c->st, c->m + p, c->ld, c->lwd, c->ld, rows, p));
+        ABFT_TRY(gemv_sub(c->st, rows, p, c->lwd, c->ld, c->gcsw + 2 * k, c->ld_cs, c->rsm));
+      }
+    }
+    return 0;
+  }
+  const float* L = c->m + pe + p * c->ld;
+  const float* R = c->m + p + pe * c->ld;
+  {
+    RegionF rl{const_cast<float*>(L), c->ld, rows, w, c->b};
+    SumOut o;
+    o.cp = c->el;
+    o.cp_ld = c->ld_cs;
+    o.cp_step = 2;
+    o.cw = c->el + 1;
+    o.cw_ld = c->ld_cs;
+    o.cw_step = 2;
+    ABFT_TRY(blocksum(c->st, rl, o));
+  }
+  ABFT_TRY(widen_matrix(c->st, R, c->ld, c->uwd, c->ld_t, w, cols));
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, c->el, c->ld_cs, c->uwd,
+                c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
+  if (scheme == ABFT_FULL) {
+    RegionF rr{const_cast<float*>(R), c->ld, w, cols, c->b};
+    SumOut o;
+    o.rp = c->er;
+    o.rp_ld = c->ld_t;
+    ABFT_TRY(blocksum(c->st, rr, o));
+    ABFT_TRY(widen_matrix(c->st, L, c->ld, c->lwd, c->ld, rows, w));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbc, (int)w, -1.0, c->lwd, c->ld, c->er, c->ld_t,
+                  1.0, enc.rp, c->ld, c->rsm, c->ld, &c->gws));
+  }
+  return 0;
+}
+
+int s_upload_plan(abft_sctx* c, const abft_fault* plan, int nplan) {
+  if (nplan > c->dplan_cap) {
+    if (c->dplan) cudaFree(c->dplan);
+    c->dplan_cap = std::max(nplan, 64);
+    CUDA_TRY(cudaMalloc(&c->dplan, c->dplan_cap * sizeof(DevFault)));
+  }
+  std::vector<DevFault> h(nplan);
+  for (int i = 0; i < nplan; ++i) {
+    h[i].kind = plan[i].kind;
+    h[i].orientation = plan[i].orientation;
+    h[i].row = plan[i].row;
+    h[i].col = plan[i].col;
+    h[i].extent = plan[i].extent;
+    h[i].absolute = plan[i].absolute;
+    h[i].u = plan[i].u;
+    h[i].negate = plan[i].negate;
+    h[i].pad = 0;
+    h[i].magnitude = plan[i].magnitude;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->dplan, h.data(), nplan * sizeof(DevFault), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+int s_touched(abft_sctx* c, const abft_fault* plan, int nplan, int64_t r0, int64_t c0, int64_t rows,
+              int64_t cols, int* count) {
+  std::vector<std::pair<int32_t, int32_t>> blks;
+  for (int f = 0; f < nplan; ++f) {
+    const abft_fault& ft = plan[f];
+    int64_t er = 1, ec = 1;
+    const int64_t ext = std::max<int64_t>(2, ft.extent);
+    if (ft.kind == ABFT_D1) {
+      if (ft.orientation == 0) er = ext; else ec = ext;
+    } else if (ft.kind == ABFT_D2) {
+      er = ext;
+      ec = ext;
+    }
+    for (int64_t r = std::max(ft.row, r0); r < std::min(std::min(ft.row + er, c->n), r0 + rows); ++r)
+      for (int64_t cc = std::max(ft.col, c0); cc < std::min(std::min(ft.col + ec, c->n), c0 + cols); ++cc)
+        blks.emplace_back((int32_t)((r - r0) / c->b), (int32_t)((cc - c0) / c->b));
+  }
+  std::sort(blks.begin(), blks.end());
+  blks.erase(std::unique(blks.begin(), blks.end()), blks.end());
+  *count = (int)blks.size();
+  if (blks.empty()) return 0;
+  std::vector<int32_t> lst;
+  for (auto& pr : blks) {
+    lst.push_back(pr.first);
+    lst.push_back(pr.second);
+  }
+  const int nn = (int)lst.size();
+  if (nn > c->dlist_cap) {
+    if (c->dlist) cudaFree(c->dlist);
+    c->dlist_cap = std::max(nn, 1024);
+    CUDA_TRY(cudaMalloc(&c->dlist, c->dlist_cap * sizeof(int32_t)));
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->dlist, lst.data(), nn * sizeof(int32_t), cudaMemcpyHostToDevice, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+// _protected_tmu (simulator.py:124-167) in fp32 data / fp64 checksums.
+int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                    int correct) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  s_region(c, k, &r0, &c0, &rows, &cols);
+  const bool has = rows > 0 && cols > 0;
+  const bool prot = scheme != ABFT_NONE && has;
+  RegionF reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  bool fused = false;
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    const bool reuse = c->sums_valid && c->kind == ABFT_LU;
+    if (!reuse) ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
+    ABFT_TRY(s_maintain(c, k, scheme, r0, c0, rows, cols));
+    smark(c, SP_ABFT, false);
+  }
+  smark(c, SP_TMU, true);
+  if (c->kind == ABFT_LU) {
+    if (pe < n) {
+      FusedSums fs;
+      const bool fuse = prot && c->fuse_enabled && c->b == 128;
+      if (fuse) {
+        const SumOut o = s_sums(c, r0, c0, true);
+        fs.cp = o.cp;
+        fs.cp_ld = o.cp_ld;
+        fs.cp_step = o.cp_step;
+        fs.cw = o.cw;
+        fs.cw_ld = o.cw_ld;
+        fs.cw_step = o.cw_step;
+        fs.rp = o.rp;
+        fs.rp_ld = o.rp_ld;
+        fs.bm = o.bm;
+        fs.bm_ld = o.bm_ld;
+      }
+      float* A22 = c->m + pe + pe * c->ld;
+      ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, n - pe, w, -1.0f, c->m + pe + p * c->ld, c->ld,
+                      c->m + p + pe * c->ld, c->ld, 1.0f, A22, c->ld, A22, c->ld,
+                      fuse ? &fs : nullptr));
+      fused = fuse;
+    }
+  } else if (k > 0) {
+    float* P = c->m + p + p * c->ld;
+    ABFT_TRY(s_gemm(c, 'N', 'T', n - p, w, p, -1.0f, c->m + p, c->ld, c->m + p, c->ld, 1.0f, P, c->ld,
+                    P, c->ld));
+  }
+  smark(c, SP_TMU, false);
+  smark(c, SP_ABFT, true);
+  const bool faults = has && nplan > 0;
+  if (prot && !fused) {
+    ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
+  } else if (!prot && faults) {
+    SumOut o;
+    o.bm = c->gmax + (r0 / c->b) + (c0 / c->b) * c->ld_max;
+    o.bm_ld = c->ld_max;
+    ABFT_TRY(blocksum(c->st, reg, o));
+  }
+  if (faults) {
+    for (int f = 0; f < nplan; ++f)
+      if (plan[f].row < 0 || plan[f].row >= n || plan[f].col < 0 || plan[f].col >= n) {
+        set_last_error("fault at (%lld, %lld) outside matrix", (long long)plan[f].row,
+                       (long long)plan[f].col);
+        return ABFT_E_RANGE;
+      }
+    ABFT_TRY(s_upload_plan(c, plan, nplan));
+    const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+    ABFT_TRY(inject(c->st, c->m, c->ld, n, n, c->dplan, nplan,
+                    c->gmax + (r0 / c->b) + (c0 / c->b) * c->ld_max, nbr, nbc, c->ld_max, 0.0));
+    if (prot) {
+      int cnt = 0;
+      ABFT_TRY(s_touched(c, plan, nplan, r0, c0, rows, cols, &cnt));
+      if (cnt > 0) ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true), c->dlist, nullptr, cnt));
+    }
+  }
+  if (prot) {
+    Maintained mt;
+    mt.cp = c->csm;
+    mt.cp_ld = c->ld_cs;
+    mt.cp_step = 2;
+    mt.cw = c->csm + 1;
+    mt.cw_ld = c->ld_cs;
+    mt.cw_step = 2;
+    mt.rp = c->rsm;
+    mt.rp_ld = c->ld;
+    EventSink sink{c->ev, c->counters, c->ev_cap, c->dirty, c->counters + 1, c->dirty_cap, (int32_t)k};
+    ABFT_TRY(verify_blocks(c->st, reg, c->b, scheme, correct, s_sums(c, r0, c0, true), mt, sink));
+    ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true), c->dirty, c->counters + 1, c->dirty_cap));
+    CUDA_TRY(cudaMemsetAsync(c->counters + 1, 0, sizeof(int32_t), c->st));
+  }
+  c->sums_valid = prot;
+  smark(c, SP_ABFT, false);
+  return 0;
+}
+
+int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan, int correct,
+                bool sync_checks) {
+  auto pd = [&]() -> int {
+    smark(c, SP_PD, true);
+    ABFT_TRY(s_pd(c, k));
+    smark(c, SP_PD, false);
+    if (sync_checks) ABFT_TRY(s_check_info(c));
+    return 0;
+  };
+  auto pu = [&]() -> int {
+    smark(c, SP_PU, true);
+    ABFT_TRY(s_pu(c, k));
+    smark(c, SP_PU, false);
+    return 0;
+  };
+  if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
+    ABFT_TRY(pd());
+    ABFT_TRY(pu());
+  } else {
+    ABFT_TRY(pd());
+    ABFT_TRY(pu());
+    ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
+  }
+  return 0;
+}
+
+int s_collect(abft_sctx* c, std::vector<Event>* out) {
+  int32_t cnt[2];
+  CUDA_TRY(cudaMemcpyAsync(cnt, c->counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  if (cnt[0] > c->ev_cap) {
+    set_last_error("ABFT event buffer overflow (%d events)", cnt[0]);
+    return ABFT_E_OVERFLOW;
+  }
+  out->resize(cnt[0]);
+  if (cnt[0] > 0) CUDA_TRY(cudaMemcpy(out->data(), c->ev, cnt[0] * sizeof(Event), cudaMemcpyDeviceToHost));
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  std::stable_sort(out->begin(), out->end(), [](const Event& a, const Event& b) {
+    if (a.iter != b.iter) return a.iter < b.iter;
+    if (a.bi != b.bi) return a.bi < b.bi;
+    if (a.bj != b.bj) return a.bj < b.bj;
+    return a.seq < b.seq;
+  });
+  for (const Event& e : *out)
+    if (e.kind < 0) {
+      set_last_error("index 0 is out of bounds for axis 0 with size 0");
+      return ABFT_E_RANGE;
+    }
+  return 0;
+}
+
+void s_fill(abft_sctx* c, const std::vector<Event>& evs, int64_t k0, abft_report* reports,
+            abft_location* locs, int max_locs, int* n_locs) {
+  if (reports)
+    for (int64_t k = k0; k < c->nb; ++k) memset(&reports[k], 0, sizeof(abft_report));
+  int total = 0;
+  for (const Event& e : evs) {
+    int64_t r0, c0, rows, cols;
+    s_region(c, e.iter, &r0, &c0, &rows, &cols);
+    if (reports) {
+      abft_report& rep = reports[e.iter];
+      rep.detected[e.detected_kind] += 1;
+      if (e.corrected) rep.corrected[e.detected_kind] += 1;
+      if (e.uncorrectable) rep.uncorrectable = 1;
+      rep.n_locations += 1;
+    }
+    if (locs && total < max_locs) {
+      abft_location& L = locs[total];
+      L.row = e.row + r0;
+      L.col = e.col + c0;
+      L.kind = e.kind;
+      L.flag = e.flag;
+      L.detected_kind = e.detected_kind;
+      L.corrected = e.corrected;
+      L.uncorrectable = e.uncorrectable;
+      L.block_row = e.bi;
+      L.block_col = e.bj;
+      L.seq = e.seq;
+    }
+    ++total;
+  }
+  if (n_locs) *n_locs = total;
+}
+
+}  // namespace
+
+extern "C" {
+
+ABFT_API int abft_s_destroy(abft_sctx* c);
+
+ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int device) {
+  *out = nullptr;
+  if (kind != ABFT_LU && kind != ABFT_CHOLESKY) {
+    set_last_error("fp32 contexts support LU (sgetrf) and Cholesky (spotrf); got kind %d", kind);
+    return ABFT_E_INVALID;
+  }
+  if (n < 1 || !(1 <= b && b <= n)) {
+    set_last_error("block size %lld outside [1, %lld]", (long long)b, (long long)n);
+    return ABFT_E_DIM;
+  }
+  if (b > 256) {
+    set_last_error("block size %lld > 256 is not supported by the B200 panel kernels", (long long)b);
+    return ABFT_E_INVALID;
+  }
+  SGuard g(device);
+  abft_sctx* c = new abft_sctx();
+  c->kind = kind;
+  c->n = n;
+  c->b = b;
+  c->nb = (n + b - 1) / b;
+  c->ld = s_round_up(n, 16);
+  c->device = device;
+  c->ld_cs = s_round_even(2 * c->nb);
+  c->ld_max = s_round_even(c->nb);
+  c->ld_t = s_round_up(b, 4);
+  {
+    const char* e = getenv("ABFT_NO_FUSE");
+    c->fuse_enabled = !(e && e[0] == '1');
+  }
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
+    set_last_error("cudaStreamCreate failed");
+    delete c;
+    return -1000;
+  }
+  int rc = 0;
+  auto fail = [&](int r) {
+    abft_s_destroy(c);
+    return r;
+  };
+  const int64_t ld = c->ld;
+  if ((rc = salloc(&c->m, ld * n, c->st))) return fail(rc);
+  if ((rc = salloc(&c->gcsw, c->ld_cs * n, c->st))) return fail(rc);
+  if ((rc = salloc(&c->csm, c->ld_cs * n, c->st))) return fail(rc);
+  if ((rc = salloc(&c->grs, ld * c->nb, c->st))) return fail(rc);
+  if ((rc = salloc(&c->rsm, ld * c->nb, c->st))) return fail(rc);
+  if ((rc = salloc(&c->gmax, c->ld_max * c->nb, c->st))) return fail(rc);
+  if ((rc = salloc(&c->el, c->ld_cs * b, c->st))) return fail(rc);
+  if ((rc = salloc(&c->er, c->ld_t * std::max<int64_t>(c->nb, b), c->st))) return fail(rc);
+  if ((rc = salloc(&c->lwd, ld * (kind == ABFT_CHOLESKY ? n : b), c->st))) return fail(rc);
+  if ((rc = salloc(&c->uwd, c->ld_t * n, c->st))) return fail(rc);
+  if ((rc = salloc(&c->lw, ld * b, c->st))) return fail(rc);
+  if ((rc = salloc(&c->uw, c->ld_t * n, c->st))) return fail(rc);
+  if ((rc = salloc(&c->linv, c->ld_t * b, c->st))) return fail(rc);
+  if ((rc = salloc(&c->uinv, c->ld_t * b, c->st))) return fail(rc);
+  if ((rc = salloc(&c->scratch, 4096, c->st))) return fail(rc);
+  c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
+  if ((rc = salloc(&c->gws.ptr, c->gws.elems, c->st))) return fail(rc);
+  c->sws_elems = sgemm_workspace_elems((int)n, (int)n, (int)b);
+  if ((rc = salloc(&c->sws, c->sws_elems, c->st))) return fail(rc);
+  c->ev_cap = 1 << 16;
+  if (cudaMalloc(&c->ev, c->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&c->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  cudaMemsetAsync(c->counters, 0, 4 * sizeof(int32_t), c->st);
+  c->dirty_cap = 1 << 16;
+  if (cudaMalloc(&c->dirty, 2 * c->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
+  if (cudaMalloc(&c->info, sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemsetAsync(c->info, 0, sizeof(int), c->st);
+  cudaEventCreate(&c->e0);
+  cudaEventCreate(&c->e1);
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(-1000);
+  *out = c;
+  return 0;
+}
+
+ABFT_API int abft_s_destroy(abft_sctx* c) {
+  if (!c) return 0;
+  SGuard g(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  void* bufs[] = {c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
+                  c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
+                  c->uinv, c->sws, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
+                  c->dplan, c->dlist, c->info};
+  for (void* p : bufs)
+    if (p) cudaFree(p);
+  for (auto& pe : c->prof_pending) {
+    cudaEventDestroy(pe.second.first);
+    cudaEventDestroy(pe.second.second);
+  }
+  if (c->e0) cudaEventDestroy(c->e0);
+  if (c->e1) cudaEventDestroy(c->e1);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return 0;
+}
+
+ABFT_API void* abft_s_stream(abft_sctx* c) { return reinterpret_cast<void*>(c->st); }
+ABFT_API int64_t abft_s_k_done(abft_sctx* c) { return c->k_done; }
+
+ABFT_API int abft_s_keep_input(abft_sctx* c, int keep) {
+  c->keep_input = keep != 0;
+  return 0;
+}
+
+static void s_reset_state(abft_sctx* c) {
+  c->k_done = 0;
+  c->sums_valid = false;
+  c->breakdown_col = -1;
+}
+
+ABFT_API int abft_s_set_matrix(abft_sctx* c, const float* a, int64_t lda) {
+  SGuard g(c->device);
+  if (lda < c->n) {
+    set_last_error("lda < n");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpy2DAsync(c->m, c->ld * 4, a, lda * 4, c->n * 4, c->n, cudaMemcpyHostToDevice, c->st));
+  if (c->keep_input) {
+    if (!c->a0) ABFT_TRY(salloc(&c->a0, c->ld * c->n, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->a0, c->m, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  s_reset_state(c);
+  return 0;
+}
+
+ABFT_API int abft_s_reset(abft_sctx* c) {
+  SGuard g(c->device);
+  if (!c->a0) {
+    set_last_error("abft_s_reset needs abft_s_keep_input(ctx, 1) before abft_s_set_matrix");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->m, c->a0, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
+  s_reset_state(c);
+  return 0;
+}
+
+// m <- m m^T + n I (generate_test_matrix's SPD construction, linalg.py:74-75)
+ABFT_API int abft_s_make_spd(abft_sctx* c) {
+  SGuard g(c->device);
+  float* T = nullptr;
+  ABFT_TRY(salloc(&T, c->ld * c->n, c->st));
+  int rc = s_gemm(c, 'N', 'T', c->n, c->n, c->n, 1.0f, c->m, c->ld, c->m, c->ld, 0.0f, nullptr, 0, T,
+                  c->ld);
+  if (!rc) rc = add_diag(c->st, T, c->ld, c->n, (double)c->n);
+  if (!rc) rc = copy_matrix(c->st, T, c->ld, c->m, c->ld, c->n, c->n, 0);
+  if (!rc && c->a0) rc = copy_matrix(c->st, T, c->ld, c->a0, c->ld, c->n, c->n, 0);
+  cudaStreamSynchronize(c->st);
+  cudaFree(T);
+  return rc;
+}
+
+ABFT_API int abft_s_get_matrix(abft_sctx* c, float* mh, int64_t ldm) {
+  SGuard g(c->device);
+  CUDA_TRY(cudaMemcpy2DAsync(mh, ldm * 4, c->m, c->ld * 4, c->n * 4, c->n, cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
+
+ABFT_API int abft_s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                              int correct, abft_report* rep, abft_location* locs, int max_locs) {
+  SGuard g(c->device);
+  if (k != c->k_done || k < 0 || k >= c->nb) {
+    set_last_error("expected iteration %lld, got %lld", (long long)c->k_done, (long long)k);
+    return ABFT_E_DIM;
+  }
+  if (scheme < 0 || scheme > 2) {
+    set_last_error("unknown checksum scheme %d", scheme);
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  CUDA_TRY(cudaEventRecord(c->e0, c->st));
+  int rc = s_iteration(c, k, scheme, plan, nplan, correct, true);
+  CUDA_TRY(cudaEventRecord(c->e1, c->st));
+  c->timed = true;
+  if (rc) return rc;
+  std::vector<Event> evs;
+  ABFT_TRY(s_collect(c, &evs));
+  std::vector<abft_report> reps(c->nb);
+  int nl = 0;
+  s_fill(c, evs, k, reps.data(), locs, max_locs, &nl);
+  if (rep) *rep = reps[k];
+  c->k_done = k + 1;
+  return 0;
+}
+
+ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, const abft_fault* plan,
+                              const int64_t* plan_iter, int nplan, int correct, abft_report* reports,
+                              abft_location* locs, int max_locs, int* n_locs) {
+  SGuard g(c->device);
+  CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
+  if (n_locs) *n_locs = 0;
+  const int64_t k0 = c->k_done;
+  CUDA_TRY(cudaEventRecord(c->e0, c->st));
+  c->timed = true;
+  for (int64_t k = k0; k < c->nb; ++k) {
+    const int sch = schemes ? schemes[k] : scheme;
+    int f0 = 0, f1 = 0;
+    if (plan && plan_iter) {
+      while (f0 < nplan && plan_iter[f0] < k) ++f0;
+      f1 = f0;
+      while (f1 < nplan && plan_iter[f1] == k) ++f1;
+    }
+    int rc = s_iteration(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false);
+    if (rc) {
+      cudaEventRecord(c->e1, c->st);
+      return rc;
+    }
+  }
+  CUDA_TRY(cudaEventRecord(c->e1, c->st));
+  int brk = s_check_info(c);
+  if (brk) {
+    c->k_done = c->breakdown_col / c->b;
+    return brk;
+  }
+  std::vector<Event> evs;
+  ABFT_TRY(s_collect(c, &evs));
+  s_fill(c, evs, k0, reports, locs, max_locs, n_locs);
+  c->k_done = c->nb;
+  return 0;
+}
+
+ABFT_API int abft_s_last_elapsed_ms(abft_sctx* c, double* ms) {
+  SGuard g(c->device);
+  *ms = 0.0;
+  if (!c->timed) return 0;
+  CUDA_TRY(cudaEventSynchronize(c->e1));
+  float f = 0.f;
+  CUDA_TRY(cudaEventElapsedTime(&f, c->e0, c->e1));
+  *ms = f;
+  return 0;
+}
+
+ABFT_API int abft_s_profile(abft_sctx* c, int enable) {
+  c->prof_on = enable != 0;
+  for (double& x : c->prof_ms) x = 0.0;
+  return 0;
+}
+
+ABFT_API int abft_s_profile_read(abft_sctx* c, double* ms) {
+  SGuard g(c->device);
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  for (auto& pe : c->prof_pending) {
+    float f = 0.f;
+    cudaEventElapsedTime(&f, pe.second.first, pe.second.second);
+    c->prof_ms[pe.first] += f;
+    cudaEventDestroy(pe.second.first);
+    cudaEventDestroy(pe.second.second);
+  }
+  c->prof_pending.clear();
+  for (int i = 0; i < 4; ++i) ms[i] = c->prof_ms[i];
+  return 0;
+}
+
+// residual(a, factors) (linalg.py:362-368) with the reconstruction on the
+// tcgen05 GEMM (fp32 accuracy) and fp64 Frobenius sums. a0 == NULL: kept input.
+ABFT_API int abft_s_residual(abft_sctx* c, const float* a0h, int64_t lda, double* out) {
+  SGuard g(c->device);
+  if (c->k_done < c->nb) {
+    set_last_error("factorization incomplete");
+    return ABFT_E_INCOMPLETE;
+  }
+  const int64_t n = c->n, ld = c->ld;
+  float *A = nullptr, *L = nullptr, *U = nullptr, *X = nullptr;
+  bool own = false;
+  int rc = 0;
+  if (a0h) {
+    rc = salloc(&A, ld * n, c->st);
+    own = true;
+    if (!rc && cudaMemcpy2DAsync(A, ld * 4, a0h, lda * 4, n * 4, n, cudaMemcpyHostToDevice, c->st) !=
+                   cudaSuccess)
+      rc = -1000;
+  } else if (c->a0) {
+    A = c->a0;
+  } else {
+    set_last_error("no input matrix for the residual");
+    return ABFT_E_INVALID;
+  }
+  if (!rc) rc = salloc(&L, ld * n, c->st);
+  if (!rc) rc = salloc(&U, ld * n, c->st);
+  if (!rc) rc = salloc(&X, ld * n, c->st);
+  if (!rc) {
+    if (c->kind == ABFT_LU) {
+      rc = copy_matrix(c->st, c->m, ld, L, ld, n, n, 1);
+      if (!rc) rc = copy_matrix(c->st, c->m, ld, U, ld, n, n, 2);
+      if (!rc) rc = s_gemm(c, 'N', 'N', n, n, n, 1.0f, L, ld, U, ld, 0.0f, nullptr, 0, X, ld);
+    } else {
+      rc = copy_matrix(c->st, c->m, ld, L, ld, n, n, 3);
+      if (!rc) rc = s_gemm(c, 'N', 'T', n, n, n, 1.0f, L, ld, L, ld, 0.0f, nullptr, 0, X, ld);
+    }
+  }
+  double* sq = c->scratch + 2048;
+  if (!rc) rc = sumsq(c->st, A, ld, n, n, sq, c->scratch);
+  if (!rc) rc = sub_matrix(c->st, A, ld, X, ld, n, n);
+  if (!rc) rc = sumsq(c->st, X, ld, n, n, sq + 1, c->scratch + 1024);
+  double h[2] = {0, 0};
+  if (!rc && cudaMemcpyAsync(h, sq, 2 * sizeof(double), cudaMemcpyDeviceToHost, c->st) != cudaSuccess)
+    rc = -1000;
+  cudaStreamSynchronize(c->st);
+  for (float* p : {L, U, X})
+    if (p) cudaFree(p);
+  if (own && A) cudaFree(A);
+  if (rc) return rc;
+  const double na = sqrt(h[0]), nd = sqrt(h[1]);
+  *out = (na == 0.0) ? nd : nd / na;
+  return 0;
+}
+
+ABFT_API int64_t abft_s_breakdown_column(abft_sctx* c) { return c->breakdown_col; }
+
+}  // extern "C"

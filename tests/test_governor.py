@@ -117,7 +117,9 @@ def test_forced_scheme_campaign_corrects_injected_faults():
     intervals, so faults do occur; FULL repairs what it detects."""
     import paper_2301_03166_b200 as P
     a = P.generate_test_matrix("lu", 2048, 1)
-    table = G.scaled_rate_table(5e3)
+    # rates that are non-zero at every clock this (panel-bound) size reaches
+    table = G.ErrorRateTable({"0d": [(100.0, 0.0), (2200.0, 2e4)],
+                              "1d": [(100.0, 0.0), (2200.0, 2e3)]})
     s, recs = G.run_mode("lu", a, 256, "bsr", r=1.0, seed=1, rates=table, forced_scheme="full",
                          recovery="recompute")
     assert sum(s.faults_injected.values()) > 0

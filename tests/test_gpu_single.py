@@ -1,0 +1,61 @@
+"""GPU: the fp32 (s*) factorizations on the tcgen05 path.
+
+The reference is fp64-only (parity unpinned); the fp32 run
+must (a) reconstruct A to fp32 accuracy (residual <= 64 * n * eps32 stated
+bound; typically ~1e-7), and (b) report exactly the fault locations the
+fp64 oracle reports for the same seeded plan, since the reference's fault
+magnitudes (1e-3 * max|region|) sit far above the eps32 threshold.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_2301_03166_b200 as P
+
+pytestmark = pytest.mark.gpu
+EPS32 = float(np.finfo(np.float32).eps)
+
+
+@pytest.mark.parametrize("kind", ["lu", "cholesky"])
+@pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64)])
+@pytest.mark.parametrize("scheme", ["full", "single"])
+def test_fp32_fault_locations_match_fp64_oracle(kind, n, b, scheme):
+    seed = 5
+    a = P.generate_test_matrix(kind, n, seed)
+    f = P.SFactorization(kind, a, b)
+    nb = f.layout.n_blocks
+    sched = {1: {"0d": 1}, 2: {"0d": 2}, nb - 2: {"1d": 1}}
+    reps = f.run_protected(scheme, sched, np.random.default_rng(seed))
+    fo = O.OracleFactorization(kind, a, b)
+    rng_o = np.random.default_rng(seed)
+    for k in range(nb):
+        ro = O.protected_iteration(fo, k, scheme, sched.get(k), rng_o)
+        got = [(r, c, kk.value, fl) for r, c, kk, fl in reps[k].locations]
+        assert got == ro.locations, (k, got, ro.locations)
+    res = f.residual(a)
+    assert res <= 64 * n * EPS32, res
+
+
+@pytest.mark.parametrize("kind", ["lu", "cholesky"])
+def test_fp32_per_iteration_equals_one_call(kind):
+    n, b, seed = 640, 128, 9
+    a = P.generate_test_matrix(kind, n, seed)
+    f1 = P.SFactorization(kind, a, b)
+    sched = {2: {"0d": 1}}
+    r1 = f1.run_protected("full", sched, np.random.default_rng(seed))
+    f2 = P.SFactorization(kind, a, b)
+    rng = np.random.default_rng(seed)
+    r2 = [f2.run_numeric_iteration(k, "full", sched.get(k), rng) for k in range(f2.layout.n_blocks)]
+    assert [r.locations for r in r1] == [r.locations for r in r2]
+    np.testing.assert_array_equal(f1.m, f2.m)
+
+
+def test_fp32_clean_run_reports_nothing_and_breakdown_raises():
+    a = P.generate_test_matrix("lu", 512, 1)
+    f = P.SFactorization("lu", a, 128)
+    reps = f.run_protected("full")
+    assert all(r.clean for r in reps)
+    bad = P.generate_test_matrix("cholesky", 256, 0)
+    bad[0, 0] = -1.0
+    with pytest.raises(P.NumericBreakdownError):
+        P.SFactorization("cholesky", bad, 64).run_protected("none")
