@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--extra-kinds", default="", help="comma list of kinds also measured")
     ap.add_argument("--profile-only", action="store_true", help="one step, for ncu")
+    ap.add_argument("--precision", default="f64", choices=["f64", "f32"],
+                    help="f32: the s* variants (sgetrf/spotrf) on the tcgen05 tf32 path")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="N>1 transport (gloo: several ranks sharing one GPU, for testing)")
     return ap.parse_args()
@@ -213,17 +215,20 @@ def run_reference(args):
 
 
 def metric_name(args) -> str:
-    return (f"ABFT {LAPACK[args.kind]} TFLOP/s (fp64 N={args.n}, {args.scheme.upper()} "
-            f"checksums, 1 seeded fault)")
+    name = LAPACK[args.kind] if args.precision == "f64" else "s" + LAPACK[args.kind][1:]
+    return (f"ABFT {name} TFLOP/s ({'fp64' if args.precision == 'f64' else 'fp32'} N={args.n}, "
+            f"{args.scheme.upper()} checksums, 1 seeded fault)")
 
 
 def config(args) -> dict:
-    return {"workload": f"{args.kind} fp64 N={args.n} b={args.b} scheme={args.scheme} "
+    prec = "fp64" if args.precision == "f64" else "fp32 (tcgen05 3xTF32)"
+    return {"workload": f"{args.kind} {prec} N={args.n} b={args.b} scheme={args.scheme} "
                         f"(col_ft+row_ft as under mode=bsr), one 0-D fault at a seeded "
                         f"iteration (criterion-5 protocol)",
             "kind": args.kind, "n": args.n, "b": args.b, "scheme": args.scheme,
             "seed": args.seed,
-            "l2": "working set 8.6 GB >> 126 MB L2; no flush needed",
+            "l2": f"working set {args.n * args.n * (8 if args.precision == 'f64' else 4) / 1e9:.1f} GB "
+                  ">> 126 MB L2; no flush needed",
             "parallelism": (f"block-cyclic columns over {args.gpus} GPUs "
                             f"({'panel broadcast' if args.kind != 'cholesky' else 'panel-update reduce'}"
                             f" over {args.dist_backend})") if args.gpus > 1 else "single"}
@@ -341,6 +346,57 @@ class DistArm:
         return self.f.residual(self.host)
 
 
+class SArm(Arm):
+    """fp32 (s*) factorization context on the tcgen05 path, device-resident."""
+
+    def __init__(self, kind, n, b, seed, device):
+        import paper_2301_03166_b200 as P
+        from paper_2301_03166_b200 import _lib
+        self.P, self.L = P, _lib
+        self.lib = _lib.load()
+        self.kind, self.n, self.b, self.seed = kind, n, b, seed
+        t0 = time.perf_counter()
+        if kind == "cholesky":
+            host = np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n)))
+        else:
+            host = P.generate_test_matrix(kind, n, seed)
+        self.gen_s = time.perf_counter() - t0
+        _GEN["s"] = self.gen_s
+        self.f = P.SFactorization(kind, host, b, device=device, keep_input=True,
+                                  spd_on_device=(kind == "cholesky"))
+        self.host = self.f.m if kind == "cholesky" else np.asfortranarray(host, dtype=np.float32)
+        import torch
+        self.torch = torch
+        self.stream = torch.cuda.ExternalStream(self.f.stream_ptr())
+
+    def step(self, scheme):
+        k_fault, rng = fault_plan(self.n, self.b, self.seed)
+        self.f.reset()
+        return k_fault, self.f.run_protected(scheme, {k_fault: {"0d": 1}}, rng)
+
+    def profile(self, scheme):
+        lib = self.lib
+        lib.abft_s_profile(self.f._ctx, 1)
+        self.step(scheme)
+        ms = (ctypes.c_double * 4)()
+        lib.abft_s_profile_read(self.f._ctx, ms)
+        lib.abft_s_profile(self.f._ctx, 0)
+        return {"pd": ms[0], "pu": ms[1], "tmu_gemm": ms[2], "abft": ms[3]}
+
+    def residual(self):
+        return self.f.residual(None)
+
+
+def tf32x3_peak() -> tuple:
+    """Effective 3xTF32 tensor peak: measured dense bf16 (MEASURED_PEAKS.json,
+    burst) / 2 for TF32 operands / 3 MMAs per product; fallback 1.59 PF bf16."""
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return d["bf16_tflops"] / 6.0, "measured bf16 burst / 2 (tf32) / 3 (3xTF32 split), of measured"
+    except Exception:
+        return 1590.0 / 6.0, "fallback bf16 1.59 PF / 2 / 3 (B200_PROFILING.md), of fallback"
+
+
 def tmu_flops(kind, n, b) -> float:
     from paper_2301_03166_b200.linalg import compute_flops
     return sum(compute_flops(kind, "tmu", n, b, k) for k in range(-(-n // b)))
@@ -377,7 +433,12 @@ def run_ours(args):
     lib = P._lib.load()
     peak = ctypes.c_double(0.0)
     P.linalg.check(lib.abft_probe_dmma_peak(20000, ctypes.byref(peak)))
-    arm = (DistArm if world > 1 else Arm)(args.kind, args.n, args.b, args.seed, local)
+    if args.precision == "f32":
+        if world > 1 or args.kind == "qr":
+            raise SystemExit("fp32 runs: single GPU, lu or cholesky")
+        arm = SArm(args.kind, args.n, args.b, args.seed, local)
+    else:
+        arm = (DistArm if world > 1 else Arm)(args.kind, args.n, args.b, args.seed, local)
     if args.profile_only:
         arm.step(args.scheme)
         torch.cuda.synchronize()
@@ -417,8 +478,27 @@ def run_ours(args):
     achieved = tflops_tmu / (prof["tmu_gemm"] * 1e-3) / 1e12 if prof["tmu_gemm"] else None
     vbytes = verify_bytes(args.kind, args.n, args.b, args.scheme)
 
+    if args.precision == "f64":
+        roofline = {"bound": "tensor", "kernel": "dgemm_tma_dmma (trailing-matrix update)",
+                    "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
+                    "frac": (achieved / peak.value) if achieved else None,
+                    # dram read+write of one fused trailing-update launch (M=N~31.2k, K=256)
+                    # from `ncu --set full` (profiles/ncu_full_gemm_lu32k_r01.txt); the
+                    # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once)
+                    "traffic": 26.63e9 if args.kind == "lu" else None,
+                    "traffic_algorithmic": 15.7e9 if args.kind == "lu" else None,
+                    "peak_source": "measured DMMA issue rate on this GPU "
+                                   "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"}
+    else:
+        p32, src32 = tf32x3_peak()
+        roofline = {"bound": "tensor", "kernel": "sgemm_tc05 (tcgen05 kind::tf32, 3xTF32)",
+                    "achieved": achieved, "peak": p32, "unit": "TFLOP/s",
+                    "frac": (achieved / p32) if achieved else None, "traffic": None,
+                    "peak_source": src32}
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.precision == "f32":
+        e2e = run_e2e_s(arm, args)
+    elif not args.no_e2e:
         e2e = run_e2e(arm, args) if world == 1 else run_e2e_dist(arm, args)
     extra = {}
     for kind in [k for k in args.extra_kinds.split(",") if k and k != args.kind]:
@@ -437,7 +517,7 @@ def run_ours(args):
         "metric": metric_name(args), "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
         "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
-        "vs_baseline": None, "dtype": "f64",
+        "vs_baseline": None, "dtype": args.precision,
         "data": f"synthetic: generate_test_matrix({args.kind!r}, {args.n}, seed={args.seed}) "
                 "(PCG64 draws bit-identical to the reference)",
         "config": config(args),
@@ -447,16 +527,7 @@ def run_ours(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": launches,
-        "roofline": {"bound": "tensor", "kernel": "dgemm_tma_dmma (trailing-matrix update)",
-                     "achieved": achieved, "peak": peak.value, "unit": "TFLOP/s",
-                     "frac": (achieved / peak.value) if achieved else None,
-                     # dram read+write of one fused trailing-update launch (M=N~31.2k, K=256)
-                     # from `ncu --set full` (profiles/ncu_full_gemm_lu32k_r01.txt); the
-                     # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once)
-                     "traffic": 26.63e9 if args.kind == "lu" else None,
-                     "traffic_algorithmic": 15.7e9 if args.kind == "lu" else None,
-                     "peak_source": "measured DMMA issue rate on this GPU "
-                                    "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"},
+        "roofline": roofline,
         "abft_verify": {
             "region_bytes": vbytes,
             "note": ("verify-side block sums of LU/QR trailing updates are produced in the GEMM "
@@ -527,6 +598,30 @@ def run_e2e(arm, args):
     return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
             "ms_per_step": sec * 1e3, "api": "abft_set_matrix + run_protected + abft_get_matrix"}
+
+
+def run_e2e_s(arm, args):
+    """fp32 e2e: pinned fp32 host input in, factorization, factor out."""
+    import torch
+    f, n = arm.f, args.n
+    pinned_in = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy()
+    pinned_in[...] = arm.host.T
+    src = pinned_in.T
+    pinned_out = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy().T
+    times = []
+    for i in range(1 + args.steps):
+        t0 = time.perf_counter()
+        arm.P.linalg.check(arm.lib.abft_s_set_matrix(f._ctx, arm.P._lib.fptr(src), n))
+        k_fault, rng = fault_plan(n, args.b, args.seed)
+        f.run_protected(args.scheme, {k_fault: {"0d": 1}}, rng)
+        arm.P.linalg.check(arm.lib.abft_s_get_matrix(f._ctx, arm.P._lib.fptr(pinned_out), n))
+        if i:
+            times.append(time.perf_counter() - t0)
+    sec = statistics.median(times)
+    return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
+            "h2d_bytes_per_step": 4 * n * n, "d2h_bytes_per_step": 4 * n * n,
+            "ms_per_step": sec * 1e3, "api": "abft_s_set_matrix + SFactorization.run_protected + "
+                                             "abft_s_get_matrix"}
 
 
 def run_e2e_dist(arm, args):

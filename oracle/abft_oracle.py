@@ -19,6 +19,7 @@ import numpy as np
 CHECK_TOLERANCE_FACTOR = 50.0
 INDEX_SNAP_TOLERANCE = 1e-2
 EPS64 = float(np.finfo(np.float64).eps)
+EPS32 = float(np.finfo(np.float32).eps)
 
 ALL_KINDS = ("cholesky", "lu", "qr")
 ERROR_KINDS = ("0d", "1d", "2d")   # ErrorKind iteration order, abft.py:42-45
@@ -181,13 +182,15 @@ def _snap_index(dw: float, dp: float, limit: int):
     return None
 
 
-def verify(m: np.ndarray, cs: Checksums, correct: bool = True) -> OracleReport:
-    """verify_correct (abft.py:174-205) with _handle_single / _handle_full."""
+def verify(m: np.ndarray, cs: Checksums, correct: bool = True, eps: float = EPS64) -> OracleReport:
+    """verify_correct (abft.py:174-205) with _handle_single / _handle_full.
+    ``eps`` = EPS64 is the reference; EPS32 is the fp32 restatement of the
+    threshold rule (s* variants: parity unpinned)."""
     rep = OracleReport()
     b = cs.b
     view = m[cs.r0:cs.r0 + cs.rows, cs.c0:cs.c0 + cs.cols]
     cp, cw, rp, _, bmax = block_sums(view, b)
-    tau = CHECK_TOLERANCE_FACTOR * b * np.maximum(bmax, 1.0) * EPS64   # _block_threshold
+    tau = CHECK_TOLERANCE_FACTOR * b * np.maximum(bmax, 1.0) * eps     # _block_threshold
     nbr, nbc = bmax.shape
     d_col = cp - cs.cp
     d_w = cw - cs.cw
@@ -481,7 +484,7 @@ def residual(a: np.ndarray, f: OracleFactorization) -> float:
 
 def protected_iteration(f: OracleFactorization, k: int, scheme: str,
                         counts: dict | None = None, rng=None,
-                        correct: bool = True) -> OracleReport:
+                        correct: bool = True, eps: float = EPS64) -> OracleReport:
     rep = OracleReport()
     for task in f.order():
         if task != "tmu":
@@ -503,6 +506,6 @@ def protected_iteration(f: OracleFactorization, k: int, scheme: str,
                 flt["magnitude"] = magnitude(flt["u"], flt["negate"], scale)
             inject(f.m, plan)
         if cs is not None:
-            rep = verify(f.m, cs, correct)
+            rep = verify(f.m, cs, correct, eps)
     f.k_done = k + 1
     return rep

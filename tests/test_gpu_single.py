@@ -2,9 +2,12 @@
 
 The reference is fp64-only (parity unpinned); the fp32 run
 must (a) reconstruct A to fp32 accuracy (residual <= 64 * n * eps32 stated
-bound; typically ~1e-7), and (b) report exactly the fault locations the
-fp64 oracle reports for the same seeded plan, since the reference's fault
-magnitudes (1e-3 * max|region|) sit far above the eps32 threshold.
+bound; typically ~1e-7), and (b) report exactly the fault locations of the
+oracle restated for fp32 (same algorithm, tau on eps32). The reference's
+fault magnitude (u * 1e-3 * max|region|) can sit within 2x of tau32 in the
+dominant diagonal blocks, where fp32 rounding decides detection; the test
+uses the first seed whose oracle outcome is identical for tau32 / 2 and
+2 * tau32, so every compared decision has a margin of 2x.
 """
 import numpy as np
 import pytest
@@ -19,19 +22,31 @@ EPS32 = float(np.finfo(np.float32).eps)
 @pytest.mark.parametrize("kind", ["lu", "cholesky"])
 @pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64)])
 @pytest.mark.parametrize("scheme", ["full", "single"])
-def test_fp32_fault_locations_match_fp64_oracle(kind, n, b, scheme):
-    seed = 5
-    a = P.generate_test_matrix(kind, n, seed)
-    f = P.SFactorization(kind, a, b)
-    nb = f.layout.n_blocks
+def test_fp32_fault_locations_match_fp32_oracle(kind, n, b, scheme):
+    nb = -(-n // b)
     sched = {1: {"0d": 1}, 2: {"0d": 2}, nb - 2: {"1d": 1}}
+
+    def oracle(seed, eps):
+        a = O.generate_test_matrix(kind, n, seed)
+        fo = O.OracleFactorization(kind, a, b)
+        rng = np.random.default_rng(seed)
+        return [O.protected_iteration(fo, k, scheme, sched.get(k), rng, eps=eps).locations
+                for k in range(nb)], fo, a
+
+    for seed in range(5, 40):
+        lo, _, _ = oracle(seed, EPS32 / 2)
+        hi, _, _ = oracle(seed, EPS32 * 2)
+        ref, fo, a = oracle(seed, EPS32)
+        if lo == ref == hi:
+            break
+    else:
+        pytest.skip("no seed with a 2x detection margin")
+    assert sum(len(x) for x in ref) > 0
+    f = P.SFactorization(kind, a, b)
     reps = f.run_protected(scheme, sched, np.random.default_rng(seed))
-    fo = O.OracleFactorization(kind, a, b)
-    rng_o = np.random.default_rng(seed)
     for k in range(nb):
-        ro = O.protected_iteration(fo, k, scheme, sched.get(k), rng_o)
         got = [(r, c, kk.value, fl) for r, c, kk, fl in reps[k].locations]
-        assert got == ro.locations, (k, got, ro.locations)
+        assert got == ref[k], (seed, k, got, ref[k])
     res = f.residual(a)
     assert res <= 64 * n * EPS32, res
 
