@@ -72,7 +72,10 @@ struct abft_sctx {
   double* el = nullptr;
   double* er = nullptr;
   int64_t ld_t = 0;
-  double* lwd = nullptr;  // widened left operand (n x b, or n x n for Cholesky's L)
+  double* lwd = nullptr;  // widened left operand (n x b)
+  double* chol_rs = nullptr;  // Cholesky running row checksums of future panels (n x nb)
+  bool chol_rs_valid = false;
+  bool want_chol_rs = false;
   double* uwd = nullptr;  // widened right operand (b x n)
   // fp32 workspaces
   float* lw = nullptr;    // n x b
@@ -215,6 +218,16 @@ int s_pu(abft_sctx* c, int64_t k) {
     SumOut o = s_sums(c, p, p, false);
     o.bm = nullptr;
     ABFT_TRY(blocksum(c->st, reg, o));
+    // chol_rs[pe:n, j] -= L_k[pe:n, :] (1^T L_k[block j, :])^T for j > k
+    const int64_t nj = c->nb - (k + 1);
+    if (c->chol_rs_valid && nj > 0 && pe < n) {
+      ABFT_TRY(gather_transpose(c->st, c->gcsw + 2 * (k + 1) + p * c->ld_cs, 2, c->ld_cs, nj, w, c->er,
+                                c->ld_t));
+      ABFT_TRY(widen_matrix(c->st, c->m + pe + p * c->ld, c->ld, c->lwd, c->ld, n - pe, w));
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)nj, (int)w, -1.0, c->lwd, c->ld, c->er,
+                    c->ld_t, 1.0, c->chol_rs + pe + (k + 1) * c->ld, c->ld,
+                    c->chol_rs + pe + (k + 1) * c->ld, c->ld, &c->gws));
+    }
   }
   return 0;
 }
@@ -231,11 +244,13 @@ int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int6
     ABFT_TRY(gemm(c->st, 'N', 'T', (int)(2 * nbr), (int)w, (int)p, -1.0, c->gcsw + 2 * k, c->ld_cs,
                   c->uwd, c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
     if (scheme == ABFT_FULL) {
-      ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
-      if (p > 0) {
-        ABFT_TRY(widen_matrix(c->st, c->m + p, c->ld, c->lwd, c->ld, rows, p));
-        ABFT_TRY(gemv_sub(c->st, rows, p, c->lwd, c->ld, c->gcsw + 2 * k, c->ld_cs, c->rsm));
+      if (!c->chol_rs_valid) {
+        set_last_error("fp32 Cholesky FULL checksums need FULL from the first iteration");
+        return ABFT_E_INVALID;
       }
+      // running right-looking maintenance (as ctx.cu): the panel's row
+      // checksums already carry every earlier update
+      ABFT_TRY(copy_matrix(c->st, c->chol_rs + p + k * c->ld, c->ld, c->rsm, c->ld, rows, nbc));
     }
     return 0;
   }
@@ -339,6 +354,14 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   const bool prot = scheme != ABFT_NONE && has;
   RegionF reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
   bool fused = false;
+  if (c->kind == ABFT_CHOLESKY && k == 0 && (scheme == ABFT_FULL || c->want_chol_rs)) {
+    RegionF all{c->m, c->ld, n, n, c->b};
+    SumOut o;
+    o.rp = c->chol_rs;
+    o.rp_ld = c->ld;
+    ABFT_TRY(blocksum(c->st, all, o));
+    c->chol_rs_valid = true;
+  }
   if (prot) {
     smark(c, SP_ABFT, true);
     const bool reuse = c->sums_valid && c->kind == ABFT_LU;
@@ -562,7 +585,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   if ((rc = salloc(&c->gmax, c->ld_max * c->nb, c->st))) return fail(rc);
   if ((rc = salloc(&c->el, c->ld_cs * b, c->st))) return fail(rc);
   if ((rc = salloc(&c->er, c->ld_t * std::max<int64_t>(c->nb, b), c->st))) return fail(rc);
-  if ((rc = salloc(&c->lwd, ld * (kind == ABFT_CHOLESKY ? n : b), c->st))) return fail(rc);
+  if ((rc = salloc(&c->lwd, ld * b, c->st))) return fail(rc);
+  if (kind == ABFT_CHOLESKY && (rc = salloc(&c->chol_rs, ld * c->nb, c->st))) return fail(rc);
   if ((rc = salloc(&c->uwd, c->ld_t * n, c->st))) return fail(rc);
   if ((rc = salloc(&c->lw, ld * b, c->st))) return fail(rc);
   if ((rc = salloc(&c->uw, c->ld_t * n, c->st))) return fail(rc);
@@ -592,7 +616,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
   if (!c) return 0;
   SGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  void* bufs[] = {c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
+  void* bufs[] = {c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
                   c->uinv, c->sws, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
                   c->dplan, c->dlist, c->info};
@@ -618,6 +642,7 @@ ABFT_API int abft_s_keep_input(abft_sctx* c, int keep) {
 }
 
 static void s_reset_state(abft_sctx* c) {
+  c->chol_rs_valid = false;
   c->k_done = 0;
   c->sums_valid = false;
   c->breakdown_col = -1;
@@ -685,6 +710,7 @@ ABFT_API int abft_s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fa
   }
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
+  if (k == 0) c->want_chol_rs = true;  // a later iteration may ask for FULL
   int rc = s_iteration(c, k, scheme, plan, nplan, correct, true);
   CUDA_TRY(cudaEventRecord(c->e1, c->st));
   c->timed = true;
@@ -706,6 +732,9 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
   CUDA_TRY(cudaMemsetAsync(c->counters, 0, 2 * sizeof(int32_t), c->st));
   if (n_locs) *n_locs = 0;
   const int64_t k0 = c->k_done;
+  c->want_chol_rs = false;
+  for (int64_t k = k0; k < c->nb; ++k)
+    if ((schemes ? schemes[k] : scheme) == ABFT_FULL) c->want_chol_rs = true;
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
   for (int64_t k = k0; k < c->nb; ++k) {

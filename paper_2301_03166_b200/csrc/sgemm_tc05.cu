@@ -220,12 +220,22 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int acc = it & 1, use = it >> 1;
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
-      mbar_wait(&tfull[acc], use & 1);
-      tc_fence_after();
       const int m = tm * TBM + row_t;
       const bool rv = m < p.M;
+      // The whole C row segment (128 values) is loaded before waiting for the
+      // accumulator: 128 independent coalesced loads per thread overlap this
+      // tile's MMAs (memory-level parallelism is what bounds this epilogue).
+      float cv[TBN];
+      const bool use_c = p.beta != 0.0f;
+#pragma unroll
+      for (int j = 0; j < TBN; ++j) {
+        const int col = tn * TBN + j;
+        cv[j] = (use_c && rv && col < p.N) ? p.C[m + (int64_t)col * p.ldc] : 0.0f;
+      }
+      mbar_wait(&tfull[acc], use & 1);
+      tc_fence_after();
       double rsum = 0.0, mx = 0.0;
-#pragma unroll 1
+#pragma unroll
       for (int cc = 0; cc < TBN / 32; ++cc) {
         float v[32];
         tmem_ld32(tmem_base + (uint32_t)(acc * TBN + cc * 32) + ((uint32_t)(quarter * 32) << 16), v);
@@ -234,8 +244,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
         for (int j = 0; j < 32; ++j) {
           const int col = c0 + j;
           const bool ok = rv && col < p.N;
-          float o = p.alpha * v[j];
-          if (ok && p.beta != 0.0f) o = fmaf(p.beta, p.C[m + (int64_t)col * p.ldc], o);
+          const float o = fmaf(p.beta, cv[cc * 32 + j], p.alpha * v[j]);
           if (ok) p.D[m + (int64_t)col * p.ldd] = o;
           v[j] = ok ? o : 0.0f;
         }
