@@ -100,6 +100,10 @@ struct abft_sctx {
   bool sums_valid = false;
   int64_t breakdown_col = -1;
   bool fuse_enabled = true;
+  bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
+  int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  cudaStream_t st2 = nullptr;     // side stream for the look-ahead diagonal block
+  cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool timed = false;
   bool prof_on = false;
@@ -152,7 +156,7 @@ SumOut s_sums(abft_sctx* c, int64_t r0, int64_t c0, bool rows_too) {
 
 int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, float alpha,
            const float* A, int64_t lda, const float* B, int64_t ldb, float beta, const float* C,
-           int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr) {
+           int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr, int max_ctas = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   const int64_t need = sgemm_workspace_elems((int)M, (int)N, (int)K);
   if (need > c->sws_elems) {
@@ -161,7 +165,7 @@ int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, floa
     CUDA_TRY(cudaMallocAsync(&c->sws, need * sizeof(float), c->st));
   }
   return sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C, ldc, D,
-                  ldd, c->sws, c->sws_elems, fs);
+                  ldd, c->sws, c->sws_elems, fs, max_ctas);
 }
 
 int s_check_info(abft_sctx* c) {
@@ -180,16 +184,27 @@ int s_check_info(abft_sctx* c) {
 }
 
 // ---- tasks -------------------------------------------------------------------
+int s_lu_diag(abft_sctx* c, cudaStream_t st, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  return diag_factor(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t,
+                     c->info, p);
+}
+
+int s_lu_l21(abft_sctx* c, int64_t k) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (pe >= n) return 0;
+  float* D = c->m + p + p * c->ld;
+  ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, w, w, 1.0f, D + w, c->ld, c->uinv, c->ld_t, 0.0f, nullptr, 0,
+                  c->lw, c->ld));
+  return copy_matrix(c->st, c->lw, c->ld, D + w, c->ld, n - pe, w);
+}
+
 int s_pd(abft_sctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   float* D = c->m + p + p * c->ld;
   if (c->kind == ABFT_LU) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t, c->info, p));
-    if (pe < n) {
-      ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, w, w, 1.0f, D + w, c->ld, c->uinv, c->ld_t, 0.0f, nullptr,
-                      0, c->lw, c->ld));
-      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, D + w, c->ld, n - pe, w));
-    }
+    ABFT_TRY(s_lu_diag(c, c->st, k));
+    ABFT_TRY(s_lu_l21(c, k));
   } else {
     ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   }
@@ -446,9 +461,119 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   return 0;
 }
 
+FusedSums s_fused(abft_sctx* c, int64_t r0, int64_t c0) {
+  const SumOut o = s_sums(c, r0, c0, true);
+  FusedSums fs;
+  fs.cp = o.cp;
+  fs.cp_ld = o.cp_ld;
+  fs.cp_step = o.cp_step;
+  fs.cw = o.cw;
+  fs.cw_ld = o.cw_ld;
+  fs.cw_step = o.cw_step;
+  fs.rp = o.rp;
+  fs.rp_ld = o.rp_ld;
+  fs.bm = o.bm;
+  fs.bm_ld = o.bm_ld;
+  return fs;
+}
+
+// Verify (and refresh after repairs) block columns [j0, j0 + ncb) of the
+// region of iteration k, with event coordinates relative to the region.
+int s_verify_sub(abft_sctx* c, int64_t k, int scheme, int correct, int64_t r0, int64_t c0,
+                 int64_t rows, int64_t cols, int64_t j0, int64_t ncb) {
+  const int64_t cbeg = j0 * c->b;
+  const int64_t csub = std::min(cols - cbeg, ncb * c->b);
+  if (csub <= 0 || rows <= 0) return 0;
+  RegionF sub{c->m + r0 + (c0 + cbeg) * c->ld, c->ld, rows, csub, c->b};
+  SumOut rec = s_sums(c, r0, c0 + cbeg, true);
+  Maintained mt;
+  mt.cp = c->csm + cbeg * c->ld_cs;
+  mt.cp_ld = c->ld_cs;
+  mt.cp_step = 2;
+  mt.cw = mt.cp + 1;
+  mt.cw_ld = c->ld_cs;
+  mt.cw_step = 2;
+  mt.rp = c->rsm + j0 * c->ld;
+  mt.rp_ld = c->ld;
+  EventSink sink{c->ev,          c->counters,  c->ev_cap, c->dirty, c->counters + 1,
+                 c->dirty_cap,   (int32_t)k,   (int32_t)j0, c->b};
+  ABFT_TRY(verify_blocks(c->st, sub, c->b, scheme, correct, rec, mt, sink));
+  ABFT_TRY(blocksum(c->st, sub, rec, c->dirty, c->counters + 1, c->dirty_cap));
+  CUDA_TRY(cudaMemsetAsync(c->counters + 1, 0, sizeof(int32_t), c->st));
+  return 0;
+}
+
+// LU trailing update with look-ahead (fault-free iterations of the one-call
+// path, as ctx.cu): the next panel's block column is updated and verified
+// first, its diagonal block is factored on a side stream while the rest of
+// the trailing matrix updates on the remaining SMs.
+int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  s_region(c, k, &r0, &c0, &rows, &cols);
+  RegionF reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  const bool prot = scheme != ABFT_NONE;
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    if (!c->sums_valid) ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
+    ABFT_TRY(s_maintain(c, k, scheme, r0, c0, rows, cols));
+    smark(c, SP_ABFT, false);
+  }
+  const float* L21 = c->m + pe + p * c->ld;
+  const float* U12 = c->m + p + pe * c->ld;
+  float* A22 = c->m + pe + pe * c->ld;
+  const int64_t wa = std::min<int64_t>(c->b, cols);
+  smark(c, SP_TMU, true);
+  ABFT_TRY(s_gemm(c, 'N', 'N', rows, wa, w, -1.0f, L21, c->ld, U12, c->ld, 1.0f, A22, c->ld, A22,
+                  c->ld));
+  smark(c, SP_TMU, false);
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    RegionF ra{A22, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, c0, true)));
+    ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 0, 1));
+    smark(c, SP_ABFT, false);
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  ABFT_TRY(s_lu_diag(c, c->st2, k + 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  if (cols > wa) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    const bool fuse = prot && c->fuse_enabled && c->b == 128;
+    FusedSums fs;
+    if (fuse) fs = s_fused(c, r0, c0 + wa);
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, cols - wa, w, -1.0f, L21, c->ld, U12 + wa * c->ld, c->ld, 1.0f,
+                    A22 + wa * c->ld, c->ld, A22 + wa * c->ld, c->ld, fuse ? &fs : nullptr, sms - 2));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      if (!fuse) {
+        RegionF rb{A22 + wa * c->ld, c->ld, rows, cols - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, s_sums(c, r0, c0 + wa, true)));
+      }
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 1, (cols + c->b - 1) / c->b));
+      smark(c, SP_ABFT, false);
+    }
+  }
+  c->sums_valid = prot;
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  smark(c, SP_PD, true);
+  ABFT_TRY(s_lu_l21(c, k + 1));
+  smark(c, SP_PD, false);
+  c->pd_ready = k + 1;
+  return 0;
+}
+
 int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan, int correct,
-                bool sync_checks) {
+                bool sync_checks, bool lookahead = false) {
   auto pd = [&]() -> int {
+    if (c->pd_ready == k) {  // produced by the previous iteration's look-ahead
+      c->pd_ready = -1;
+      return 0;
+    }
     smark(c, SP_PD, true);
     ABFT_TRY(s_pd(c, k));
     smark(c, SP_PD, false);
@@ -468,7 +593,11 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
   } else {
     ABFT_TRY(pd());
     ABFT_TRY(pu());
-    ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
+    const int64_t pe = std::min((k + 1) * c->b, c->n);
+    if (lookahead && nplan == 0 && pe < c->n && c->lookahead_enabled)
+      ABFT_TRY(s_tmu_lu_lookahead(c, k, scheme, correct));
+    else
+      ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
   }
   return 0;
 }
@@ -607,6 +736,13 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   cudaMemsetAsync(c->info, 0, sizeof(int), c->st);
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
+  cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
+  {
+    const char* e2 = getenv("ABFT_NO_LOOKAHEAD");
+    c->lookahead_enabled = !(e2 && e2[0] == '1');
+  }
   if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(-1000);
   *out = c;
   return 0;
@@ -626,6 +762,12 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
     cudaEventDestroy(pe.second.first);
     cudaEventDestroy(pe.second.second);
   }
+  if (c->st2) {
+    cudaStreamSynchronize(c->st2);
+    cudaStreamDestroy(c->st2);
+  }
+  if (c->ev_a) cudaEventDestroy(c->ev_a);
+  if (c->ev_p) cudaEventDestroy(c->ev_p);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->st) cudaStreamDestroy(c->st);
@@ -643,6 +785,7 @@ ABFT_API int abft_s_keep_input(abft_sctx* c, int keep) {
 
 static void s_reset_state(abft_sctx* c) {
   c->chol_rs_valid = false;
+  c->pd_ready = -1;
   c->k_done = 0;
   c->sums_valid = false;
   c->breakdown_col = -1;
@@ -745,7 +888,7 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
       f1 = f0;
       while (f1 < nplan && plan_iter[f1] == k) ++f1;
     }
-    int rc = s_iteration(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false);
+    int rc = s_iteration(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false, true);
     if (rc) {
       cudaEventRecord(c->e1, c->st);
       return rc;
