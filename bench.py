@@ -434,8 +434,8 @@ def run_ours(args):
     peak = ctypes.c_double(0.0)
     P.linalg.check(lib.abft_probe_dmma_peak(20000, ctypes.byref(peak)))
     if args.precision == "f32":
-        if world > 1 or args.kind == "qr":
-            raise SystemExit("fp32 runs: single GPU, lu or cholesky")
+        if world > 1:
+            raise SystemExit("fp32 runs: single GPU")
         arm = SArm(args.kind, args.n, args.b, args.seed, local)
     else:
         arm = (DistArm if world > 1 else Arm)(args.kind, args.n, args.b, args.seed, local)

@@ -221,10 +221,11 @@ ABFT_API int abft_dist_elapsed_ms(abft_dist* d, double* ms);
 ABFT_API int abft_set_qr_panel(abft_ctx* ctx, int64_t k, const double* V, int64_t ldv,
                                const double* T, int64_t ldt);
 
-/* single precision (the s* variants: sgetrf / spotrf) ---------------------
+/* single precision (the s* variants: sgetrf / spotrf / sgeqrf) ------------
  * Same task order, regions, fault plan semantics, events and error codes as
  * the fp64 context above; fp32 data (tcgen05 kind::tf32 GEMMs with a 3xTF32
- * split), fp64 block checksums, tau = 50 * b * max(max|blk|, 1) * eps32.
+ * split), fp64 block checksums, tau = 50 * b * max(max|blk|, 1) * eps32;
+ * the QR Householder panel is factored in fp64 from the widened fp32 panel.
  * The reference has no fp32 path (parity unpinned). */
 typedef struct abft_sctx abft_sctx;
 ABFT_API int abft_s_create(abft_sctx** ctx, int kind, int64_t n, int64_t b, int device);

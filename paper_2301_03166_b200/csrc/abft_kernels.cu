@@ -699,6 +699,10 @@ int copy_matrix(cudaStream_t st, const float* src, int64_t lds, float* dst, int6
                 int64_t rows, int64_t cols, int mode) {
   return copy_t(st, src, lds, dst, ldd, rows, cols, mode);
 }
+int narrow_matrix(cudaStream_t st, const double* src, int64_t lds, float* dst, int64_t ldd,
+                  int64_t rows, int64_t cols) {
+  return copy_t(st, src, lds, dst, ldd, rows, cols, 0);
+}
 int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, int64_t ldd,
                  int64_t rows, int64_t cols) {
   return copy_t(st, src, lds, dst, ldd, rows, cols, 0);

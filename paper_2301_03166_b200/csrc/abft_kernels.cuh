@@ -127,6 +127,9 @@ int copy_matrix(cudaStream_t st, const double* src, int64_t lds, double* dst, in
                 int64_t rows, int64_t cols, int mode = 0);
 int copy_matrix(cudaStream_t st, const float* src, int64_t lds, float* dst, int64_t ldd,
                 int64_t rows, int64_t cols, int mode = 0);
+// fp64 -> fp32 narrowing copy (the mixed-precision QR panel)
+int narrow_matrix(cudaStream_t st, const double* src, int64_t lds, float* dst, int64_t ldd,
+                  int64_t rows, int64_t cols);
 // fp32 -> fp64 widening copy (operands of the fp64 checksum maintenance)
 int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, int64_t ldd,
                  int64_t rows, int64_t cols);

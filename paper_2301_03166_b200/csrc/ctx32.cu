@@ -12,6 +12,11 @@
 //            checksums produced in the GEMM epilogue (b = 128).
 //   Cholesky left-looking like the reference: TMU = panel -= L L^T (tcgen05),
 //            PD = diag factor, PU = L21 = A21 L11^{-T} (tcgen05).
+//   QR       compact-WY: the Householder panel is factored in fp64 from the
+//            widened fp32 panel (the fp64 cooperative panel kernel + larft,
+//            a mixed-precision panel), V / T / R are stored back in fp32, and
+//            the trailing update C -= V (T^T (V^T C)) runs on tcgen05 with the
+//            fused checksums.
 // The maintenance products run on the fp64 DMMA GEMM from widened operands.
 #include <algorithm>
 #include <cstdlib>
@@ -73,6 +78,22 @@ struct abft_sctx {
   double* er = nullptr;
   int64_t ld_t = 0;
   double* lwd = nullptr;  // widened left operand (n x b)
+  // QR: fp32 V / T of every panel, fp64 panel workspaces
+  float* vstore = nullptr;   // n x n (ld)
+  float* tstore = nullptr;   // nb of b x b (ld_t)
+  float* ww = nullptr;       // b x n (ld_t)
+  float* mid = nullptr;      // b x n (ld_t)
+  double* pan64 = nullptr;   // n x b (ld)
+  double* v64 = nullptr;     // n x b (ld)
+  double* t64 = nullptr;     // b x b (ld_t)
+  double* gram = nullptr;    // b x b
+  double* betas = nullptr;
+  double* qr_part = nullptr;
+  int64_t qr_part_elems = 0;
+  double* qr_rowbuf = nullptr;
+  double* qr_part2 = nullptr;
+  double* qr_wfin = nullptr;
+  int qr_count = 0;
   double* chol_rs = nullptr;  // Cholesky running row checksums of future panels (n x nb)
   bool chol_rs_valid = false;
   bool want_chol_rs = false;
@@ -131,8 +152,10 @@ void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
   const int64_t p = k * c->b, pe = std::min(p + c->b, c->n);
   if (c->kind == ABFT_CHOLESKY) {
     *r0 = p; *c0 = p; *rows = c->n - p; *cols = pe - p;
-  } else {
+  } else if (c->kind == ABFT_LU) {
     *r0 = pe; *c0 = pe; *rows = c->n - pe; *cols = c->n - pe;
+  } else {
+    *r0 = p; *c0 = pe; *rows = c->n - p; *cols = c->n - pe;
   }
 }
 
@@ -205,8 +228,22 @@ int s_pd(abft_sctx* c, int64_t k) {
   if (c->kind == ABFT_LU) {
     ABFT_TRY(s_lu_diag(c, c->st, k));
     ABFT_TRY(s_lu_l21(c, k));
-  } else {
+  } else if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+  } else {
+    // mixed-precision Householder panel: widen, factor in fp64, narrow back
+    const int64_t nk = n - p;
+    ABFT_TRY(widen_matrix(c->st, D, c->ld, c->pan64, c->ld, nk, w));
+    ABFT_TRY(fill_matrix(c->st, c->v64, c->ld, nk, w, 0.0));
+    ABFT_TRY(qr_panel(c->st, c->pan64, c->ld, nk, (int)w, c->v64, c->ld, c->betas, c->qr_part,
+                      c->qr_part_elems, c->qr_rowbuf, c->qr_part2, c->qr_wfin));
+    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)w, (int)nk, 1.0, c->v64, c->ld, c->v64, c->ld, 0.0,
+                  nullptr, 0, c->gram, c->ld_t, &c->gws));
+    ABFT_TRY(larft(c->st, c->gram, c->ld_t, c->betas, (int)w, c->t64, c->ld_t));
+    ABFT_TRY(narrow_matrix(c->st, c->pan64, c->ld, D, c->ld, nk, w));
+    ABFT_TRY(narrow_matrix(c->st, c->v64, c->ld, c->vstore + p + p * c->ld, c->ld, nk, w));
+    ABFT_TRY(narrow_matrix(c->st, c->t64, c->ld_t, c->tstore + k * c->b * c->ld_t, c->ld_t, w, w));
+    c->qr_count = (int)(k + 1);
   }
   return 0;
 }
@@ -269,8 +306,9 @@ int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int6
     }
     return 0;
   }
-  const float* L = c->m + pe + p * c->ld;
-  const float* R = c->m + p + pe * c->ld;
+  const float* L = c->kind == ABFT_LU ? c->m + pe + p * c->ld : c->vstore + p + p * c->ld;
+  const float* R = c->kind == ABFT_LU ? c->m + p + pe * c->ld : c->mid;
+  const int64_t ldr = c->kind == ABFT_LU ? c->ld : c->ld_t;
   {
     RegionF rl{const_cast<float*>(L), c->ld, rows, w, c->b};
     SumOut o;
@@ -282,11 +320,11 @@ int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int6
     o.cw_step = 2;
     ABFT_TRY(blocksum(c->st, rl, o));
   }
-  ABFT_TRY(widen_matrix(c->st, R, c->ld, c->uwd, c->ld_t, w, cols));
+  ABFT_TRY(widen_matrix(c->st, R, ldr, c->uwd, c->ld_t, w, cols));
   ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, c->el, c->ld_cs, c->uwd,
                 c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
   if (scheme == ABFT_FULL) {
-    RegionF rr{const_cast<float*>(R), c->ld, w, cols, c->b};
+    RegionF rr{const_cast<float*>(R), ldr, w, cols, c->b};
     SumOut o;
     o.rp = c->er;
     o.rp_ld = c->ld_t;
@@ -359,6 +397,22 @@ int s_touched(abft_sctx* c, const abft_fault* plan, int nplan, int64_t r0, int64
   return 0;
 }
 
+FusedSums s_fused(abft_sctx* c, int64_t r0, int64_t c0) {
+  const SumOut o = s_sums(c, r0, c0, true);
+  FusedSums fs;
+  fs.cp = o.cp;
+  fs.cp_ld = o.cp_ld;
+  fs.cp_step = o.cp_step;
+  fs.cw = o.cw;
+  fs.cw_ld = o.cw_ld;
+  fs.cw_step = o.cw_step;
+  fs.rp = o.rp;
+  fs.rp_ld = o.rp_ld;
+  fs.bm = o.bm;
+  fs.bm_ld = o.bm_ld;
+  return fs;
+}
+
 // _protected_tmu (simulator.py:124-167) in fp32 data / fp64 checksums.
 int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
                     int correct) {
@@ -377,15 +431,50 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
     ABFT_TRY(blocksum(c->st, all, o));
     c->chol_rs_valid = true;
   }
+  const bool qr_live = c->kind == ABFT_QR && pe < n && k < c->qr_count;
   if (prot) {
     smark(c, SP_ABFT, true);
-    const bool reuse = c->sums_valid && c->kind == ABFT_LU;
+    const bool reuse = c->sums_valid && c->kind != ABFT_CHOLESKY;
     if (!reuse) ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
-    ABFT_TRY(s_maintain(c, k, scheme, r0, c0, rows, cols));
+    smark(c, SP_ABFT, false);
+  }
+  if (c->kind == ABFT_QR && qr_live) {
+    // W = V^T C, mid = T^T W (maintenance needs mid)
+    const float* V = c->vstore + p + p * c->ld;
+    const float* T = c->tstore + k * c->b * c->ld_t;
+    float* C = c->m + p + pe * c->ld;
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'T', 'N', w, n - pe, n - p, 1.0f, V, c->ld, C, c->ld, 0.0f, nullptr, 0, c->ww,
+                    c->ld_t));
+    ABFT_TRY(s_gemm(c, 'T', 'N', w, n - pe, w, 1.0f, T, c->ld_t, c->ww, c->ld_t, 0.0f, nullptr, 0,
+                    c->mid, c->ld_t));
+    smark(c, SP_TMU, false);
+  }
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    if (c->kind != ABFT_QR || qr_live) {
+      ABFT_TRY(s_maintain(c, k, scheme, r0, c0, rows, cols));
+    } else {
+      // no update: maintained == encoded
+      SumOut enc = s_sums(c, r0, c0, true);
+      const int64_t nbr = (rows + c->b - 1) / c->b, nbc = (cols + c->b - 1) / c->b;
+      ABFT_TRY(copy_matrix(c->st, enc.cp, c->ld_cs, c->csm, c->ld_cs, 2 * nbr, cols));
+      if (scheme == ABFT_FULL) ABFT_TRY(copy_matrix(c->st, enc.rp, c->ld, c->rsm, c->ld, rows, nbc));
+    }
     smark(c, SP_ABFT, false);
   }
   smark(c, SP_TMU, true);
-  if (c->kind == ABFT_LU) {
+  if (c->kind == ABFT_QR) {
+    if (qr_live) {
+      const bool fuse = prot && c->fuse_enabled && c->b == 128;
+      FusedSums fs;
+      if (fuse) fs = s_fused(c, r0, c0);
+      float* C = c->m + p + pe * c->ld;
+      ABFT_TRY(s_gemm(c, 'N', 'N', n - p, n - pe, w, -1.0f, c->vstore + p + p * c->ld, c->ld, c->mid,
+                      c->ld_t, 1.0f, C, c->ld, C, c->ld, fuse ? &fs : nullptr));
+      fused = fuse;
+    }
+  } else if (c->kind == ABFT_LU) {
     if (pe < n) {
       FusedSums fs;
       const bool fuse = prot && c->fuse_enabled && c->b == 128;
@@ -461,21 +550,6 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   return 0;
 }
 
-FusedSums s_fused(abft_sctx* c, int64_t r0, int64_t c0) {
-  const SumOut o = s_sums(c, r0, c0, true);
-  FusedSums fs;
-  fs.cp = o.cp;
-  fs.cp_ld = o.cp_ld;
-  fs.cp_step = o.cp_step;
-  fs.cw = o.cw;
-  fs.cw_ld = o.cw_ld;
-  fs.cw_step = o.cw_step;
-  fs.rp = o.rp;
-  fs.rp_ld = o.rp_ld;
-  fs.bm = o.bm;
-  fs.bm_ld = o.bm_ld;
-  return fs;
-}
 
 // Verify (and refresh after repairs) block columns [j0, j0 + ncb) of the
 // region of iteration k, with event coordinates relative to the region.
@@ -590,6 +664,9 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
     ABFT_TRY(pd());
     ABFT_TRY(pu());
+  } else if (c->kind == ABFT_QR) {
+    ABFT_TRY(pd());
+    ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
   } else {
     ABFT_TRY(pd());
     ABFT_TRY(pu());
@@ -668,8 +745,8 @@ ABFT_API int abft_s_destroy(abft_sctx* c);
 
 ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int device) {
   *out = nullptr;
-  if (kind != ABFT_LU && kind != ABFT_CHOLESKY) {
-    set_last_error("fp32 contexts support LU (sgetrf) and Cholesky (spotrf); got kind %d", kind);
+  if (kind < 0 || kind > 2) {
+    set_last_error("unknown decomposition kind %d", kind);
     return ABFT_E_INVALID;
   }
   if (n < 1 || !(1 <= b && b <= n)) {
@@ -716,6 +793,22 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   if ((rc = salloc(&c->er, c->ld_t * std::max<int64_t>(c->nb, b), c->st))) return fail(rc);
   if ((rc = salloc(&c->lwd, ld * b, c->st))) return fail(rc);
   if (kind == ABFT_CHOLESKY && (rc = salloc(&c->chol_rs, ld * c->nb, c->st))) return fail(rc);
+  if (kind == ABFT_QR) {
+    if ((rc = salloc(&c->vstore, ld * n, c->st))) return fail(rc);
+    if ((rc = salloc(&c->tstore, c->nb * b * c->ld_t, c->st))) return fail(rc);
+    if ((rc = salloc(&c->ww, c->ld_t * n, c->st))) return fail(rc);
+    if ((rc = salloc(&c->mid, c->ld_t * n, c->st))) return fail(rc);
+    if ((rc = salloc(&c->pan64, ld * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->v64, ld * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->t64, c->ld_t * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->gram, c->ld_t * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->betas, b, c->st))) return fail(rc);
+    c->qr_part_elems = 2 * 160 * (b + 1);
+    if ((rc = salloc(&c->qr_part, c->qr_part_elems, c->st))) return fail(rc);
+    if ((rc = salloc(&c->qr_rowbuf, 2 * (b + 1) + 128, c->st))) return fail(rc);
+    if ((rc = salloc(&c->qr_part2, 160LL * 32 * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->qr_wfin, 32LL * b, c->st))) return fail(rc);
+  }
   if ((rc = salloc(&c->uwd, c->ld_t * n, c->st))) return fail(rc);
   if ((rc = salloc(&c->lw, ld * b, c->st))) return fail(rc);
   if ((rc = salloc(&c->uw, c->ld_t * n, c->st))) return fail(rc);
@@ -752,7 +845,9 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
   if (!c) return 0;
   SGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  void* bufs[] = {c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
+  void* bufs[] = {c->vstore, c->tstore, c->ww, c->mid, c->pan64, c->v64, c->t64, c->gram,
+                  c->betas, c->qr_part, c->qr_rowbuf, c->qr_part2, c->qr_wfin,
+                  c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
                   c->uinv, c->sws, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
                   c->dplan, c->dlist, c->info};
@@ -785,6 +880,7 @@ ABFT_API int abft_s_keep_input(abft_sctx* c, int keep) {
 
 static void s_reset_state(abft_sctx* c) {
   c->chol_rs_valid = false;
+  c->qr_count = 0;
   c->pd_ready = -1;
   c->k_done = 0;
   c->sums_valid = false;
@@ -971,9 +1067,23 @@ ABFT_API int abft_s_residual(abft_sctx* c, const float* a0h, int64_t lda, double
       rc = copy_matrix(c->st, c->m, ld, L, ld, n, n, 1);
       if (!rc) rc = copy_matrix(c->st, c->m, ld, U, ld, n, n, 2);
       if (!rc) rc = s_gemm(c, 'N', 'N', n, n, n, 1.0f, L, ld, U, ld, 0.0f, nullptr, 0, X, ld);
-    } else {
+    } else if (c->kind == ABFT_CHOLESKY) {
       rc = copy_matrix(c->st, c->m, ld, L, ld, n, n, 3);
       if (!rc) rc = s_gemm(c, 'N', 'T', n, n, n, 1.0f, L, ld, L, ld, 0.0f, nullptr, 0, X, ld);
+    } else {
+      // X = triu(m); for k from last to 0: X[p:n, :] -= V (T (V^T X[p:n, :]))  (linalg.py:351-359)
+      rc = copy_matrix(c->st, c->m, ld, X, ld, n, n, 2);
+      for (int64_t k = c->qr_count - 1; k >= 0 && !rc; --k) {
+        const int64_t p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+        const float* V = c->vstore + p + p * ld;
+        const float* T = c->tstore + k * c->b * c->ld_t;
+        float* blk = X + p;
+        rc = s_gemm(c, 'T', 'N', w, n, n - p, 1.0f, V, ld, blk, ld, 0.0f, nullptr, 0, c->ww, c->ld_t);
+        if (!rc) rc = s_gemm(c, 'N', 'N', w, n, w, 1.0f, T, c->ld_t, c->ww, c->ld_t, 0.0f, nullptr, 0,
+                             c->mid, c->ld_t);
+        if (!rc) rc = s_gemm(c, 'N', 'N', n - p, n, w, -1.0f, V, ld, c->mid, c->ld_t, 1.0f, blk, ld,
+                             blk, ld);
+      }
     }
   }
   double* sq = c->scratch + 2048;

@@ -1,5 +1,5 @@
 """Single-precision factorizations (the s* variants of the north star:
-sgetrf, spotrf) on the B200.
+sgetrf, spotrf, sgeqrf) on the B200.
 
 Same Python surface and semantics as the fp64 drop-in (Factorization,
 run_numeric_iteration, run_protected, residual; linalg.py:159-368,
@@ -24,13 +24,12 @@ from .simulator import _plan_structs, _tmu_region
 
 class SFactorization:
     """fp32 Factorization (LU = sgetrf without pivoting, Cholesky = spotrf,
-    left-looking as the reference)."""
+    left-looking as the reference, QR = sgeqrf compact-WY with the
+    Householder panel factored in fp64 from the widened fp32 panel)."""
 
     def __init__(self, kind, a0: np.ndarray, b: int, device: int | None = None,
                  keep_input: bool = False, spd_on_device: bool = False):
         self.kind = DecompositionKind(_value(kind))
-        if self.kind == DecompositionKind.QR:
-            raise ValueError("fp32 QR (sgeqrf) is not provided by the B200 library yet")
         n = a0.shape[0]
         if a0.ndim != 2 or a0.shape != (n, n):
             raise ERRORS["dim"]("square input required")

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 EPS32 = float(np.finfo(np.float32).eps)
 
 
-@pytest.mark.parametrize("kind", ["lu", "cholesky"])
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
 @pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64)])
 @pytest.mark.parametrize("scheme", ["full", "single"])
 def test_fp32_fault_locations_match_fp32_oracle(kind, n, b, scheme):
@@ -51,7 +51,7 @@ def test_fp32_fault_locations_match_fp32_oracle(kind, n, b, scheme):
     assert res <= 64 * n * EPS32, res
 
 
-@pytest.mark.parametrize("kind", ["lu", "cholesky"])
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
 def test_fp32_per_iteration_equals_one_call(kind):
     n, b, seed = 640, 128, 9
     a = P.generate_test_matrix(kind, n, seed)
