@@ -344,6 +344,8 @@ class IterationRecord:
     detected: int = 0
     corrected: int = 0
     retries: int = 0
+    pred_time_s: dict = field(default_factory=dict)    # task -> predicted seconds
+    actual_time_s: dict = field(default_factory=dict)  # task -> measured seconds
 
 
 @dataclass
@@ -477,6 +479,10 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
             f.restore(0)
             rec.retries += 1
             total_retries += 1
+        rec.pred_time_s = {"pd": hist["pd"].predict(k), "pu": hist["pu"].predict(k),
+                           "tmu": t_gpu_p, "transfer": 0.0}
+        rec.actual_time_s = {"pd": d[0] * 1e-3, "pu": d[1] * 1e-3, "tmu": (d[2] + d[3]) * 1e-3,
+                             "transfer": 0.0}
         rec.t_panel_ms = d[0] + d[1]
         rec.t_update_ms = d[2] + d[3]
         rec.t_abft_ms = d[3]
@@ -513,3 +519,70 @@ def sweep_reclamation_ratio(kind, a0: np.ndarray, b: int, ratios=None, seed: int
 def compare_modes(kind, a0: np.ndarray, b: int, r: float = 0.5, seed: int = 0, **kw) -> dict:
     """simulator.py:650-669 on the B200: every mode on the same input."""
     return {m: run_mode(kind, a0, b, m, r, seed, **kw)[0] for m in MODES}
+
+
+# ---------------------------------------------------------------------------
+# output formats (cli.py:33-122): the reference's trace CSV and summary JSON
+# ---------------------------------------------------------------------------
+TRACE_HEADER = ("iter,task,pred_time_s,actual_time_s,slack_pred_s,"
+                "slack_actual_s,f_cpu_mhz,f_gpu_mhz,abft_mode,faults_0d,"
+                "faults_1d,faults_2d,detected,corrected,e_cpu_dyn_j,"
+                "e_cpu_stat_j,e_cpu_idle_j,e_gpu_dyn_j,e_gpu_stat_j,"
+                "e_gpu_idle_j,skipped")                 # cli.py:33-37
+_TRACE_TASKS = ("pd", "pu", "tmu", "transfer", "idle")  # cli.py:39
+
+
+def trace_rows(records: list) -> list:
+    """cli.py:46-92 over B200 records: one row per task plus an idle row per
+    iteration; slack on the pd row, fault counters on the tmu row. Times are
+    measured device times; per-task energies are not metered separately on
+    one GPU (the run's NVML total is in the summary), so those columns are 0."""
+    rows = []
+    fmt = lambda x: repr(float(x))  # noqa: E731  (cli.py:42-43)
+    for rec in records:
+        for task in _TRACE_TASKS:
+            is_pd, is_tmu = task == "pd", task == "tmu"
+            pred = 0.0 if task == "idle" else rec.pred_time_s.get(task, 0.0)
+            act = 0.0 if task == "idle" else rec.actual_time_s.get(task, 0.0)
+            cells = [str(rec.k), task, fmt(pred), fmt(act),
+                     fmt(rec.slack_pred_s if is_pd else 0.0),
+                     fmt(rec.slack_actual_s if is_pd else 0.0),
+                     fmt(rec.f_cpu_mhz), fmt(rec.f_gpu_mhz), rec.abft_mode,
+                     str(rec.faults["0d"] if is_tmu else 0),
+                     str(rec.faults["1d"] if is_tmu else 0),
+                     str(rec.faults["2d"] if is_tmu else 0),
+                     str(rec.detected if is_tmu else 0),
+                     str(rec.corrected if is_tmu else 0),
+                     fmt(0.0), fmt(0.0), fmt(0.0), fmt(0.0), fmt(0.0), fmt(0.0),
+                     "1" if rec.skipped else "0"]
+            rows.append(",".join(cells))
+    return rows
+
+
+def _write_atomic(path: str, text: str) -> None:
+    """cli.py:95-106."""
+    import os
+    import tempfile
+    directory = os.path.dirname(os.path.abspath(path)) or "."
+    os.makedirs(directory, exist_ok=True)
+    fd, tmp = tempfile.mkstemp(dir=directory, prefix=".b200-")
+    try:
+        with os.fdopen(fd, "w", encoding="utf-8", newline="\n") as fh:
+            fh.write(text)
+        os.replace(tmp, path)
+    except BaseException:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+        raise
+
+
+def write_trace(path: str, records: list) -> None:
+    """cli.py:109-110."""
+    _write_atomic(path, "\n".join([TRACE_HEADER] + trace_rows(records)) + "\n")
+
+
+def write_summary(path: str, summary: RunSummary) -> None:
+    """cli.py:113-122 (sorted keys, indent 2)."""
+    import dataclasses
+    import json
+    _write_atomic(path, json.dumps(dataclasses.asdict(summary), sort_keys=True, indent=2) + "\n")

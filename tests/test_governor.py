@@ -125,3 +125,26 @@ def test_forced_scheme_campaign_corrects_injected_faults():
     assert sum(s.faults_injected.values()) > 0
     assert s.faults_detected > 0
     assert s.correct, s
+
+
+def test_trace_format_matches_reference_layout(tmp_path):
+    recs = [G.IterationRecord(0, 3500.0, 1300.0, "none", False,
+                              pred_time_s={"pd": 1e-4, "pu": 2e-5, "tmu": 3e-4, "transfer": 0.0},
+                              actual_time_s={"pd": 1.1e-4, "pu": 2e-5, "tmu": 2.9e-4,
+                                             "transfer": 0.0}),
+            G.IterationRecord(1, 3400.0, 2100.0, "full", True, detected=1, corrected=1)]
+    recs[1].faults["0d"] = 1
+    p = tmp_path / "trace.csv"
+    G.write_trace(str(p), recs)
+    lines = p.read_text().splitlines()
+    assert lines[0] == G.TRACE_HEADER
+    assert len(lines) == 1 + 5 * len(recs)
+    assert all(len(x.split(",")) == len(G.TRACE_HEADER.split(",")) for x in lines[1:])
+    tmu1 = [x for x in lines[1:] if x.startswith("1,tmu,")][0].split(",")
+    assert tmu1[8] == "full" and tmu1[9] == "1" and tmu1[12] == "1" and tmu1[-1] == "1"
+    sys.path.insert(0, "/root/reference/pkg/src")
+    try:
+        import slackwise.cli as RC
+    except ImportError:
+        return
+    assert RC.TRACE_HEADER == G.TRACE_HEADER
