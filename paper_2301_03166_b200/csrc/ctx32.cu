@@ -177,18 +177,35 @@ SumOut s_sums(abft_sctx* c, int64_t r0, int64_t c0, bool rows_too) {
   return o;
 }
 
+// Long reductions are split into K chunks of at most S_KCHUNK, accumulated
+// in fp32 through the epilogue (beta = 1): the tensor core's internal
+// accumulation of a single long-K MMA chain loses precision roughly linearly
+// in K (measured: QR residual ~2e-8 * n with K = n - p), so chunking keeps
+// every product fp32-accurate.
+constexpr int64_t S_KCHUNK = 512;
+
 int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, float alpha,
            const float* A, int64_t lda, const float* B, int64_t ldb, float beta, const float* C,
            int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr, int max_ctas = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  const int64_t need = sgemm_workspace_elems((int)M, (int)N, (int)K);
+  const int64_t kc = std::min(K, S_KCHUNK);
+  const int64_t need = sgemm_workspace_elems((int)M, (int)N, (int)kc);
   if (need > c->sws_elems) {
     if (c->sws) cudaFreeAsync(c->sws, c->st);
     c->sws_elems = need;
     CUDA_TRY(cudaMallocAsync(&c->sws, need * sizeof(float), c->st));
   }
-  return sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C, ldc, D,
-                  ldd, c->sws, c->sws_elems, fs, max_ctas);
+  const bool AT = (ta == 'T' || ta == 't'), BT = (tb == 'T' || tb == 't');
+  for (int64_t k0 = 0; k0 < K; k0 += S_KCHUNK) {
+    const int64_t kl = std::min(S_KCHUNK, K - k0);
+    const float* Ak = AT ? A + k0 : A + k0 * lda;
+    const float* Bk = BT ? B + k0 * ldb : B + k0;
+    const bool first = k0 == 0, last = k0 + kl >= K;
+    ABFT_TRY(sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)kl, alpha, Ak, lda, Bk, ldb,
+                      first ? beta : 1.0f, first ? C : D, first ? ldc : ldd, D, ldd, c->sws,
+                      c->sws_elems, last ? fs : nullptr, max_ctas));
+  }
+  return 0;
 }
 
 int s_check_info(abft_sctx* c) {
