@@ -215,6 +215,13 @@ ABFT_API int abft_dist_events(abft_dist* d, abft_location* locs, int64_t* iters,
 ABFT_API int64_t abft_dist_k_done(abft_dist* d);
 ABFT_API int abft_dist_get_qr_panel(abft_dist* d, int64_t k, double* V, int64_t ldv, double* T,
                                     int64_t ldt);
+/* LU look-ahead across ranks: before update(k), hand the buffer for panel
+ * k+1; its owner factors and packs it mid-update, then the caller broadcasts
+ * it from rank (k+1) mod G on abft_dist_comm_stream() and calls
+ * abft_dist_comm_done(); begin(k+1) waits for that broadcast. */
+ABFT_API int abft_dist_lookahead(abft_dist* d, int64_t k, double* xnext);
+ABFT_API void* abft_dist_comm_stream(abft_dist* d);
+ABFT_API int abft_dist_comm_done(abft_dist* d);
 /* device time from the first begin(0) to the last finish (CUDA events) */
 ABFT_API int abft_dist_elapsed_ms(abft_dist* d, double* ms);
 /* single-context QR panel setter (rebuild a gathered factorization for the residual) */

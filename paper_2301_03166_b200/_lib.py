@@ -112,6 +112,9 @@ SIGNATURES = [
     ("abft_dist_k_done", _I64, [_P]),
     ("abft_dist_get_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
     ("abft_dist_elapsed_ms", _I, [_P, _D]),
+    ("abft_dist_lookahead", _I, [_P, _I64, _P]),
+    ("abft_dist_comm_stream", _P, [_P]),
+    ("abft_dist_comm_done", _I, [_P]),
     ("abft_set_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),
     ("abft_s_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
     ("abft_s_destroy", _I, [_P]),

@@ -125,6 +125,16 @@ struct abft_dist {
   bool fuse_enabled = true;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   bool timed = false;
+  // LU look-ahead across ranks: the owner of panel k+1 factors and packs it
+  // in the middle of update(k); the caller broadcasts it on the comm stream
+  // (st2) while the trailing update of k still runs on the main stream.
+  cudaStream_t st2 = nullptr;
+  cudaEvent_t ev_free = nullptr, ev_pack = nullptr, ev_comm = nullptr;
+  double* la_buf = nullptr;      // set by abft_dist_lookahead for the next update
+  int64_t panel_ready = -1;      // panel already factored + packed by the look-ahead
+  bool comm_pending = false;     // main stream must wait on ev_comm before the next begin
+  bool verified_in_update = false;
+  int reserve_sms = 8;           // SMs left to the collective kernels during the big GEMM
 };
 
 namespace {
@@ -393,6 +403,76 @@ int local_max(abft_dist* d, const LocalRegion& R, double* out) {
   return max_reduce(d->st, d->gmax + R.r0 / d->b + R.lb0 * d->ld_max, nbr, nbc, d->ld_max, out);
 }
 
+// Verify (and refresh after repairs) local block columns [j0, j0 + ncb) of
+// the iteration-k region (events keep region-local block coordinates).
+int verify_sub_local(abft_dist* d, int64_t k, int scheme, int correct, const LocalRegion& R,
+                     int64_t j0, int64_t ncb) {
+  const int64_t cbeg = j0 * d->b;
+  const int64_t csub = std::min(R.cols - cbeg, ncb * d->b);
+  if (csub <= 0 || R.rows <= 0) return 0;
+  Region sub{d->m + R.r0 + (R.lc0 + cbeg) * d->ld, d->ld, R.rows, csub, d->b};
+  SumOut rec = sums_local(d, R.r0, R.lb0 + j0, true);
+  Maintained mt = maintained(d);
+  mt.cp = d->csm + cbeg * d->ld_cs;
+  mt.cw = mt.cp + 1;
+  mt.rp = d->rsm + j0 * d->ld;
+  EventSink sink{d->ev,          d->counters,  d->ev_cap,  d->dirty, d->counters + 1,
+                 d->dirty_cap,   (int32_t)k,   (int32_t)j0, d->b};
+  ABFT_TRY(verify_blocks(d->st, sub, d->b, scheme, correct, rec, mt, sink));
+  ABFT_TRY(blocksum(d->st, sub, rec, d->dirty, d->counters + 1, d->dirty_cap));
+  CUDA_TRY(cudaMemsetAsync(d->counters + 1, 0, sizeof(int32_t), d->st));
+  return 0;
+}
+
+// LU update of iteration k on the owner of panel k+1 (fault-free k): the
+// panel's block column is updated and verified first, panel k+1 is factored
+// and packed into the look-ahead buffer (ev_pack releases the comm stream),
+// then the rest of the trailing matrix is updated on all but reserve_sms SMs.
+int update_lu_lookahead(abft_dist* d, int64_t k, int scheme, const double* xb, const LocalRegion& R,
+                        double* U12, int64_t w) {
+  const int64_t n = d->n, ldp = panel_ld(d, k);
+  const bool prot = scheme != ABFT_NONE;
+  const double* L21 = xb + w;
+  double* A22 = d->m + R.r0 + R.lc0 * d->ld;
+  const int64_t wa = std::min<int64_t>(d->b, R.cols);
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)R.rows, (int)wa, (int)w, -1.0, L21, ldp, U12, d->ld, 1.0, A22,
+                d->ld, A22, d->ld, &d->gws));
+  if (prot) {
+    Region ra{A22, d->ld, R.rows, wa, d->b};
+    ABFT_TRY(blocksum(d->st, ra, sums_local(d, R.r0, R.lb0, true)));
+    ABFT_TRY(verify_sub_local(d, k, scheme, 1, R, 0, 1));
+  }
+  // panel k+1 (global block k+1 = local block R.lb0 on this rank)
+  ABFT_TRY(begin_lu(d, k + 1, d->la_buf));
+  CUDA_TRY(cudaEventRecord(d->ev_pack, d->st));
+  CUDA_TRY(cudaStreamWaitEvent(d->st2, d->ev_pack, 0));
+  d->panel_ready = k + 1;
+  if (R.cols > wa) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+    const int cap = std::max(1, sms - d->reserve_sms);
+    if (prot && d->fuse_enabled && gemm_can_fuse((int)d->b)) {
+      ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)R.rows, (int)(R.cols - wa), (int)w, -1.0, L21,
+                               ldp, U12 + wa * d->ld, d->ld, 1.0, A22 + wa * d->ld, d->ld,
+                               A22 + wa * d->ld, d->ld, (int)d->b, fused_local(d, R.r0, R.lb0 + 1),
+                               cap));
+    } else {
+      ABFT_TRY(gemm_reserved(d->st, 'N', 'N', (int)R.rows, (int)(R.cols - wa), (int)w, -1.0, L21, ldp,
+                             U12 + wa * d->ld, d->ld, 1.0, A22 + wa * d->ld, d->ld, A22 + wa * d->ld,
+                             d->ld, cap));
+      if (prot) {
+        Region rb{A22 + wa * d->ld, d->ld, R.rows, R.cols - wa, d->b};
+        ABFT_TRY(blocksum(d->st, rb, sums_local(d, R.r0, R.lb0 + 1, true)));
+      }
+    }
+    if (prot) ABFT_TRY(verify_sub_local(d, k, scheme, 1, R, 1, (R.cols + d->b - 1) / d->b));
+  }
+  (void)n;
+  d->verified_in_update = true;
+  d->sums_valid = prot;
+  return 0;
+}
+
 int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int nplan,
                  double* max_out) {
   const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
@@ -418,12 +498,24 @@ int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int npla
         if (!d->sums_valid) ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true)));
         ABFT_TRY(maintain_lr(d, R, scheme, xb + w, ldp, U12, d->ld, w));
       }
+      const bool la = d->la_buf != nullptr && nplan == 0;
+      if (la && owner(d, k + 1) == d->rank)
+        return update_lu_lookahead(d, k, scheme, xb, R, U12, w);
+      int cap = 0;  // leave SMs to the collective receiving panel k+1 meanwhile
+      if (la) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+        cap = std::max(1, sms - d->reserve_sms);
+      }
       const bool fuse = prot && d->fuse_enabled && gemm_can_fuse((int)d->b);
       if (fuse) {
         ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)R.rows, (int)R.cols, (int)w, -1.0, xb + w, ldp,
                                  U12, d->ld, 1.0, reg.ptr, d->ld, reg.ptr, d->ld, (int)d->b,
-                                 fused_local(d, R.r0, R.lb0)));
+                                 fused_local(d, R.r0, R.lb0), cap));
         fused = true;
+      } else if (cap > 0) {
+        ABFT_TRY(gemm_reserved(d->st, 'N', 'N', (int)R.rows, (int)R.cols, (int)w, -1.0, xb + w, ldp,
+                               U12, d->ld, 1.0, reg.ptr, d->ld, reg.ptr, d->ld, cap));
       } else {
         ABFT_TRY(gemm(d->st, 'N', 'N', (int)R.rows, (int)R.cols, (int)w, -1.0, xb + w, ldp, U12, d->ld,
                       1.0, reg.ptr, d->ld, reg.ptr, d->ld, &d->gws));
@@ -521,6 +613,10 @@ int inject_verify(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, i
       if (cnt > 0)
         ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true), d->dlist, nullptr, cnt));
     }
+  }
+  if (d->verified_in_update) {  // look-ahead owner: verified block column by block column
+    d->verified_in_update = false;
+    return 0;
   }
   if (prot) {
     EventSink sink{d->ev, d->counters, d->ev_cap, d->dirty, d->counters + 1, d->dirty_cap,
@@ -688,6 +784,14 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
   cudaMemset(d->info, 0, sizeof(int));
   cudaEventCreate(&d->e0);
   cudaEventCreate(&d->e1);
+  cudaStreamCreateWithFlags(&d->st2, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&d->ev_free, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&d->ev_pack, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&d->ev_comm, cudaEventDisableTiming);
+  {
+    const char* e = getenv("ABFT_DIST_RESERVE_SMS");
+    if (e) d->reserve_sms = std::max(0, atoi(e));
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
   *out = d;
   return 0;
@@ -713,6 +817,12 @@ ABFT_API int abft_dist_destroy(abft_dist* d) {
   if (d->info) cudaFree(d->info);
   if (d->e0) cudaEventDestroy(d->e0);
   if (d->e1) cudaEventDestroy(d->e1);
+  if (d->st2) {
+    cudaStreamSynchronize(d->st2);
+    cudaStreamDestroy(d->st2);
+  }
+  for (cudaEvent_t e : {d->ev_free, d->ev_pack, d->ev_comm})
+    if (e) cudaEventDestroy(e);
   if (d->st) cudaStreamDestroy(d->st);
   delete d;
   return 0;
@@ -754,6 +864,10 @@ ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda) {
   d->sums_valid = false;
   d->qr_count = 0;
   d->breakdown_col = -1;
+  d->panel_ready = -1;
+  d->comm_pending = false;
+  d->la_buf = nullptr;
+  d->verified_in_update = false;
   return 0;
 }
 
@@ -775,6 +889,10 @@ ABFT_API int abft_dist_reset(abft_dist* d) {
   d->sums_valid = false;
   d->qr_count = 0;
   d->breakdown_col = -1;
+  d->panel_ready = -1;
+  d->comm_pending = false;
+  d->la_buf = nullptr;
+  d->verified_in_update = false;
   return 0;
 }
 
@@ -799,6 +917,14 @@ ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) 
     CUDA_TRY(cudaEventRecord(d->e0, d->st));
     d->timed = false;
   }
+  if (d->comm_pending) {  // the look-ahead broadcast of this panel ran on the comm stream
+    CUDA_TRY(cudaStreamWaitEvent(d->st, d->ev_comm, 0));
+    d->comm_pending = false;
+  }
+  if (d->kind == ABFT_LU && d->panel_ready == k) {  // factored + packed by the look-ahead
+    d->panel_ready = -1;
+    return 0;
+  }
   if (d->kind == ABFT_LU) {
     // the last LU panel is factored in place; nothing is exchanged
     const int64_t p = k * d->b, pe = std::min(p + d->b, d->n);
@@ -822,10 +948,42 @@ ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double*
   ABFT_TRY(check_k(d, k, scheme));
   if (d->kind == ABFT_CHOLESKY) return update_chol(d, k, scheme, xbuf, nplan, local_max);
   if (d->kind == ABFT_LU && std::min((k + 1) * d->b, d->n) >= d->n) {
+    d->la_buf = nullptr;
     if (nplan > 0 && local_max) CUDA_TRY(cudaMemsetAsync(local_max, 0, sizeof(double), d->st));
     return 0;
   }
-  return update_lu_qr(d, k, scheme, xbuf, nplan, local_max);
+  if (d->la_buf) {
+    // the comm stream may overwrite the look-ahead buffer only after every
+    // earlier reader on the main stream (update(k-1)) is done
+    CUDA_TRY(cudaEventRecord(d->ev_free, d->st));
+    CUDA_TRY(cudaStreamWaitEvent(d->st2, d->ev_free, 0));
+  }
+  const int rc = update_lu_qr(d, k, scheme, xbuf, nplan, local_max);
+  d->la_buf = nullptr;
+  return rc;
+}
+
+// LU look-ahead for the next abft_dist_update(k): the owner of panel k+1
+// factors it mid-update into `xnext` (abft_dist_xbuf_elems(k+1) doubles);
+// the caller then broadcasts `xnext` from rank (k+1) mod G on the comm stream
+// (abft_dist_comm_stream) and calls abft_dist_comm_done; begin(k+1) makes the
+// main stream wait for that broadcast.
+ABFT_API int abft_dist_lookahead(abft_dist* d, int64_t k, double* xnext) {
+  if (d->kind != ABFT_LU || k + 1 >= d->nb || abft_dist_xbuf_elems(d, k + 1) == 0) {
+    set_last_error("no look-ahead panel after iteration %lld", (long long)k);
+    return ABFT_E_INVALID;
+  }
+  d->la_buf = xnext;
+  return 0;
+}
+
+ABFT_API void* abft_dist_comm_stream(abft_dist* d) { return reinterpret_cast<void*>(d->st2); }
+
+ABFT_API int abft_dist_comm_done(abft_dist* d) {
+  DevGuardD g(d->device);
+  CUDA_TRY(cudaEventRecord(d->ev_comm, d->st2));
+  d->comm_pending = true;
+  return 0;
 }
 
 ABFT_API int abft_dist_finish(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, int nplan,

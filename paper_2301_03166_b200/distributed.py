@@ -29,6 +29,7 @@ way; there is no CPU compute path.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -121,19 +122,21 @@ class _Transport:
     """torch.distributed collectives on the context stream (NCCL: device
     buffers; other backends: staged through host memory)."""
 
-    def __init__(self, group, stream_ptr: int, device: int):
+    def __init__(self, group, stream_ptr: int, device: int, comm_ptr: int | None = None):
         import torch
         import torch.distributed as dist
         self.torch, self.dist, self.group = torch, dist, group
         self.native = dist.get_backend(group) == "nccl"
-        self.stream = torch.cuda.ExternalStream(stream_ptr, device=torch.device("cuda", device))
+        dev = torch.device("cuda", device)
+        self.stream = torch.cuda.ExternalStream(stream_ptr, device=dev)
+        self.comm = torch.cuda.ExternalStream(comm_ptr, device=dev) if comm_ptr else self.stream
 
     def _global(self, r: int) -> int:
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
 
-    def _run(self, t, fn):
+    def _run(self, t, fn, comm: bool = False):
         torch = self.torch
-        with torch.cuda.stream(self.stream):
+        with torch.cuda.stream(self.comm if comm else self.stream):
             if self.native:
                 fn(t)
             else:
@@ -141,8 +144,8 @@ class _Transport:
                 fn(h)
                 t.copy_(h)
 
-    def broadcast(self, t, src: int) -> None:
-        self._run(t, lambda x: self.dist.broadcast(x, self._global(src), group=self.group))
+    def broadcast(self, t, src: int, comm: bool = False) -> None:
+        self._run(t, lambda x: self.dist.broadcast(x, self._global(src), group=self.group), comm)
 
     def reduce_sum(self, t, dst: int) -> None:
         if self.native:
@@ -193,9 +196,14 @@ class DistributedFactorization:
         self.ncl = int(lib.abft_dist_local_cols(ctx))
         dev = torch.device("cuda", self.device)
         cap = max(int(lib.abft_dist_xbuf_elems(ctx, k)) for k in range(self.layout.n_blocks))
-        self._xbuf = torch.zeros(max(cap, 1), dtype=torch.float64, device=dev)
+        # two exchange buffers: panel k is consumed while panel k+1 is broadcast
+        self._bufs = [torch.zeros(max(cap, 1), dtype=torch.float64, device=dev) for _ in range(2)]
+        self._xbuf = self._bufs[0]
         self._scale = torch.zeros(2, dtype=torch.float64, device=dev)
-        self._tx = _Transport(group, lib.abft_dist_stream(ctx), self.device)
+        self._tx = _Transport(group, lib.abft_dist_stream(ctx), self.device,
+                              lib.abft_dist_comm_stream(ctx))
+        self.lookahead = os.environ.get("ABFT_NO_LOOKAHEAD") != "1"
+        self._prefetched = set()
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
@@ -213,10 +221,12 @@ class DistributedFactorization:
     def set_matrix(self, a: np.ndarray) -> None:
         """Load a new global input (owned column blocks are copied)."""
         host = a if a.flags.f_contiguous else np.asfortranarray(a, dtype=np.float64)
+        self._prefetched.clear()
         check(self._lib.abft_dist_set_matrix(self._ctx, _lib.dptr(host), self.n))
 
     def reset(self) -> None:
         """Restore the kept input on the device (needs keep_input=True)."""
+        self._prefetched.clear()
         check(self._lib.abft_dist_reset(self._ctx))
 
     def stream_ptr(self) -> int:
@@ -231,18 +241,33 @@ class DistributedFactorization:
         lib, ctx = self._lib, self._ctx
         code = _lib.SCHEME_CODE[scheme]
         xe = int(lib.abft_dist_xbuf_elems(ctx, k))
-        xptr = self._xbuf.data_ptr()
+        buf = self._bufs[k % 2]
+        xptr = buf.data_ptr()
         check(lib.abft_dist_begin(ctx, k, code, ctypes.c_void_p(xptr)))
-        if xe > 0:
-            view = self._xbuf[:xe]
+        if xe > 0 and k not in self._prefetched:
+            view = buf[:xe]
             if self.kind == DecompositionKind.CHOLESKY:
                 self._tx.reduce_sum(view, owner_of(k, self.world))
             else:
                 self._tx.broadcast(view, owner_of(k, self.world))
+        self._prefetched.discard(k)
         nplan = len(plan)
+        # LU look-ahead: panel k+1 is factored mid-update by its owner and
+        # broadcast on the comm stream while the trailing update of k runs
+        nb = self.layout.n_blocks
+        xe1 = int(lib.abft_dist_xbuf_elems(ctx, k + 1)) if k + 1 < nb else 0
+        la = (self.lookahead and self.world > 1 and self.kind == DecompositionKind.LU
+              and nplan == 0 and xe1 > 0)
+        nxt = self._bufs[(k + 1) % 2]
+        if la:
+            check(lib.abft_dist_lookahead(ctx, k, ctypes.c_void_p(nxt.data_ptr())))
         sptr = ctypes.c_void_p(self._scale.data_ptr())
         check(lib.abft_dist_update(ctx, k, code, ctypes.c_void_p(xptr), nplan,
                                    sptr if nplan else None))
+        if la:
+            self._tx.broadcast(nxt[:xe1], owner_of(k + 1, self.world), comm=True)
+            check(lib.abft_dist_comm_done(ctx))
+            self._prefetched.add(k + 1)
         if nplan:
             self._tx.allreduce_max(self._scale[:1])
         arr = _plan_structs(plan)
@@ -293,6 +318,7 @@ class DistributedFactorization:
         CorrectionReport per iteration, identical on every rank. The host
         loop only enqueues work; it synchronizes once at the end."""
         nb, k0 = self.layout.n_blocks, self.k_done
+        self._prefetched.clear()
         for k in range(k0, nb):
             sch = ChecksumScheme(_value(schemes[k] if schemes is not None else scheme)).value
             counts = (fault_schedule or {}).get(k)

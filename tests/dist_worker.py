@@ -36,6 +36,7 @@ def gpu_cases(rank: int, world: int, init_file: str, cases: list, out: str) -> N
     for c in cases:
         a = P.generate_test_matrix(c["kind"], c["n"], c["seed"])
         f = DistributedFactorization(c["kind"], a, c["b"], keep_input=bool(c.get("reset")))
+        f.lookahead = not c.get("no_lookahead", False)
         if c.get("reset"):  # a throw-away factorization, then restore the kept input
             f.run_protected("none", {}, None)
             f.reset()

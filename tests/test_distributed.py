@@ -85,6 +85,11 @@ CASES = [
      "schedule": {"1": {"0d": 1}}, "world": 2, "reset": True},
     {"name": "qr_b256", "kind": "qr", "n": 768, "b": 256, "scheme": "full", "seed": 11,
      "schedule": {"0": {"0d": 1}}, "world": 2},
+    # look-ahead off (ABFT_NO_LOOKAHEAD path) must give the same answers
+    {"name": "lu_w3_nola", "kind": "lu", "n": 768, "b": 128, "scheme": "full", "seed": 12,
+     "schedule": {"2": {"0d": 1}}, "world": 3, "no_lookahead": True},
+    {"name": "lu_w3_la", "kind": "lu", "n": 768, "b": 128, "scheme": "full", "seed": 12,
+     "schedule": {"2": {"0d": 1}}, "world": 3},
     # clean runs, no checksums
     {"name": "lu_none", "kind": "lu", "n": 512, "b": 128, "scheme": "none", "seed": 9,
      "schedule": {}, "world": 2},
