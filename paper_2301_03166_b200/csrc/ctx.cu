@@ -111,6 +111,10 @@ struct abft_ctx {
   bool want_chol_rs = false;      // abft_factorize: a later iteration uses FULL
   bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
   int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  int64_t chol_part = -1;         // Cholesky: panel whose update from panels 0..k-2 is done
+  bool chol_enc_ahead = false;    // ... and whose encode ran with it
+  int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
+  GemmWorkspace gws2;             // split-K workspace of the side stream
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // profiling
@@ -355,8 +359,15 @@ int tmu_gemm(abft_ctx* c, int64_t k, bool* did) {
   *did = false;
   if (c->kind == ABFT_CHOLESKY) {
     if (k == 0) return 0;
-    ABFT_TRY(gemm(c->st, 'N', 'T', (int)(n - p), (int)w, (int)p, -1.0, c->m + p, c->ld, c->m + p,
-                  c->ld, 1.0, c->m + p + p * c->ld, c->ld, c->m + p + p * c->ld, c->ld, &c->gws));
+    if (c->chol_part == k) {
+      // the look-ahead already applied panels 0..k-2: only panel k-1 is left (K = b)
+      const double* Lk = c->m + p + (p - c->b) * c->ld;
+      ABFT_TRY(gemm(c->st, 'N', 'T', (int)(n - p), (int)w, (int)c->b, -1.0, Lk, c->ld, Lk, c->ld, 1.0,
+                    c->m + p + p * c->ld, c->ld, c->m + p + p * c->ld, c->ld, &c->gws));
+    } else {
+      ABFT_TRY(gemm(c->st, 'N', 'T', (int)(n - p), (int)w, (int)p, -1.0, c->m + p, c->ld, c->m + p,
+                    c->ld, 1.0, c->m + p + p * c->ld, c->ld, c->m + p + p * c->ld, c->ld, &c->gws));
+    }
   } else if (c->kind == ABFT_LU) {
     if (pe >= n) return 0;
     ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)(n - pe), (int)w, -1.0,
@@ -534,7 +545,8 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
     // encode (abft.py:118-135): reuse the previous verify's sums when the
     // region is a sub-grid of the last verified region (LU/QR), else a pass
     prof_mark(c, PROF_ABFT, true);
-    const bool reuse = c->sums_valid && c->kind != ABFT_CHOLESKY;
+    const bool reuse = (c->sums_valid && c->kind != ABFT_CHOLESKY) ||
+                       (c->kind == ABFT_CHOLESKY && c->chol_part == k && c->chol_enc_ahead);
     if (!reuse) ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
     if (c->kind != ABFT_QR) ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
     prof_mark(c, PROF_ABFT, false);
@@ -649,6 +661,37 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
     c->sums_valid = false;
   }
   prof_mark(c, PROF_ABFT, false);
+  if (c->chol_part == k) {
+    c->chol_part = -1;
+    c->chol_enc_ahead = false;
+  }
+  return 0;
+}
+
+// Cholesky look-ahead (left-looking, fast path): right after TMU(k), the
+// update of panel k+1 by panels 0..k-1 -- final since their PU -- runs on the
+// side stream on all SMs but one, while the one-CTA diagonal factorization
+// PD(k) runs on the main stream; the panel-(k+1) encode goes with it. PU(k)
+// waits for the side stream (it needs the whole GPU), TMU(k+1) then only
+// applies panel k (K = b). Same operations as simulator.py:135-167, split.
+int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next) {
+  const int64_t n = c->n, pk = k * c->b, p1 = (k + 1) * c->b;
+  const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  c->chol_enc_ahead = false;
+  if (scheme_next != ABFT_NONE) {
+    Region reg1{c->m + p1 + p1 * c->ld, c->ld, n - p1, w1, c->b};
+    ABFT_TRY(blocksum(c->st2, reg1, sums_for(c, p1, p1, true)));
+    c->chol_enc_ahead = true;
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  double* P1 = c->m + p1 + p1 * c->ld;
+  ABFT_TRY(gemm_capped(c->st2, 'N', 'T', (int)(n - p1), (int)w1, (int)pk, -1.0, c->m + p1, c->ld,
+                       c->m + p1, c->ld, 1.0, P1, c->ld, P1, c->ld, &c->gws2, sms - 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  c->chol_part = k + 1;
   return 0;
 }
 
@@ -777,7 +820,10 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
   };
   if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+    const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb;
+    if (la) ABFT_TRY(chol_lookahead(c, k, c->next_scheme));
     ABFT_TRY(pd());
+    if (la) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
     ABFT_TRY(pu());
   } else if (c->kind == ABFT_LU) {
     ABFT_TRY(pd());
@@ -942,6 +988,10 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   // split-K workspace: bounded (falls back to fewer splits when short)
   c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
   if ((rc = dalloc(&c->gws.ptr, c->gws.elems))) return fail(rc);
+  if (kind == ABFT_CHOLESKY) {
+    c->gws2.elems = c->gws.elems;
+    if ((rc = dalloc(&c->gws2.ptr, c->gws2.elems))) return fail(rc);
+  }
   c->ev_cap = 1 << 16;
   if (cudaMalloc(&c->ev, c->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
   if (cudaMalloc(&c->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
@@ -970,7 +1020,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
                     c->qr_part2, c->qr_wfin,
-                    c->scratch, c->gws.ptr};
+                    c->scratch, c->gws.ptr, c->gws2.ptr};
   for (double* p : bufs)
     if (p) cudaFree(p);
   if (c->ev) cudaFree(c->ev);
@@ -1020,6 +1070,8 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
   return 0;
 }
@@ -1039,6 +1091,8 @@ ABFT_API int abft_reset(abft_ctx* c) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
   return 0;
 }
@@ -1150,6 +1204,7 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
       while (f1 < nplan && plan_iter[f1] == k) ++f1;
     }
     c->cur_iter = (int32_t)k;
+    c->next_scheme = (k + 1 < c->nb) ? (schemes ? schemes[k + 1] : scheme) : ABFT_NONE;
     int rc = run_iteration_device(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false,
                                   c->lookahead_enabled);
     if (rc != 0) {
@@ -1306,6 +1361,8 @@ ABFT_API int abft_restore(abft_ctx* c, int slot) {
   c->qr_count = s.qr_count;
   c->sums_valid = false;
   c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
   CUDA_TRY(cudaStreamSynchronize(c->st));
   return 0;
 }

@@ -825,6 +825,14 @@ int gemm(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha, c
 
 bool gemm_can_fuse(int fb) { return fb == 128 || fb == 256; }
 
+int gemm_capped(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                const double* C, int64_t ldc, double* D, int64_t ldd, GemmWorkspace* ws,
+                int max_ctas) {
+  return gemm_impl(st, ta, tb, M, N, K, alpha, A, lda, B, ldb, beta, C, ldc, D, ldd, ws, 0,
+                   nullptr, 0, max_ctas);
+}
+
 int gemm_reserved(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
                   const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                   const double* C, int64_t ldc, double* D, int64_t ldd, int max_ctas) {

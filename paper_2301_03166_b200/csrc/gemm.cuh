@@ -48,6 +48,12 @@ int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, doub
                     const FusedSums& sums, int max_ctas = 0);
 bool gemm_can_fuse(int fb);
 
+// gemm() (split-K allowed) on at most max_ctas SMs per launch
+int gemm_capped(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
+                const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                const double* C, int64_t ldc, double* D, int64_t ldd, GemmWorkspace* ws,
+                int max_ctas);
+
 // gemm() without split-K on at most max_ctas SMs (leaves SMs for a concurrent
 // side-stream kernel).
 int gemm_reserved(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
