@@ -59,6 +59,7 @@ struct SParams {
   int64_t ldd;
   float alpha, beta;
   int fuse;
+  int prefetch_c;  // 1: TMA-prefetch each tile's C box into L2 ahead of its epilogue
   FusedSums sums;
 };
 
@@ -117,7 +118,7 @@ ABFT_DEVINL void tmem_ld32(uint32_t taddr, float* v) {
 __global__ void __launch_bounds__(T_THREADS, 1)
     sgemm_tc05_kernel(const __grid_constant__ CUtensorMap mAh, const __grid_constant__ CUtensorMap mAl,
                       const __grid_constant__ CUtensorMap mBh, const __grid_constant__ CUtensorMap mBl,
-                      SParams p) {
+                      const __grid_constant__ CUtensorMap mC, SParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -165,6 +166,9 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       uint32_t q = 0;
       for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
         const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+        // the epilogue of this tile reads C long after its operands stream in:
+        // pull the C box into L2 now so those loads do not pay DRAM latency
+        if (p.prefetch_c) tma_prefetch_l2_2d(&mC, tm * TBM, tn * TBN);
         for (int kb = 0; kb < p.nkb; ++kb, ++q) {
           const int s = q % TSTAGES;
           if (q >= TSTAGES) mbar_wait(&empty[s], ((q / TSTAGES) - 1) & 1);
@@ -474,6 +478,20 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   p.beta = (C == nullptr) ? 0.0f : beta;
   p.fuse = fs ? 1 : 0;
   if (fs) p.sums = *fs;
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof(mc));
+  p.prefetch_c = 0;
+  if (p.beta != 0.0f && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc % 4) == 0) {
+    auto fn = encode_fn();
+    cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
+    cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
+    cuuint32_t box[2] = {TBM, TBN};
+    cuuint32_t estr[2] = {1, 1};
+    if (fn && fn(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(C), dims, strides, box,
+                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+      p.prefetch_c = 1;
+  }
   static bool attr = false;
   if (!attr) {
     CUDA_TRY(cudaFuncSetAttribute(sgemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -487,7 +505,7 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   const int tiles = p.tiles_m * p.tiles_n;
   const int grid = tiles < sms ? tiles : sms;
   count_launch();
-  sgemm_tc05_kernel<<<grid, T_THREADS, T_SMEM, st>>>(mah, mal, mbh, mbl, p);
+  sgemm_tc05_kernel<<<grid, T_THREADS, T_SMEM, st>>>(mah, mal, mbh, mbl, mc, p);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
