@@ -8,13 +8,14 @@
 // both operands K-major, so the MMA always reads the canonical K-major
 // 128-byte-swizzled shared-memory layout TMA produces.
 //
-// Kernel structure (persistent, one CTA per SM, 192 threads):
+// Kernel structure (persistent, one CTA per SM, 320 threads):
 //   warp 0      TMA producer: 4 boxes (A_hi, A_lo, B_hi, B_lo) per 32-wide
 //               k-block into a 3-stage mbarrier ring (64 KB per stage)
 //   warp 1      allocates 256 TMEM columns; one lane issues tcgen05.mma
 //               (M=128, N=128, K=8) into a double-buffered TMEM accumulator
 //               and commits stages / finished tiles to mbarriers
-//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 (one row per thread),
+//   warps 2..9  epilogue, two warps per TMEM lane quarter (each owns half
+//               the tile's columns): tcgen05.ld 32x32b.x32 (one row per thread),
 //               D = beta*C + alpha*acc with warp-coalesced column accesses,
 //               and (fused mode, checksum block = tile = 128 x 128) the
 //               block's column plain / index-weighted sums, row sums and
@@ -38,17 +39,19 @@ constexpr int TSTAGES = 3;
 constexpr int T_A_BYTES = TBM * TBK * 4;
 constexpr int T_B_BYTES = TBN * TBK * 4;
 constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;  // 64 KB
-constexpr int T_THREADS = 192;
+constexpr int T_THREADS = 320;  // producer, MMA issuer, 8 epilogue warps
 constexpr int T_TMEM_COLS = 256;  // two 128-column fp32 accumulators
-constexpr int T_TP = 33;          // padded transpose tile
+constexpr int T_TP = 17;          // padded 32 x 16 transpose tile
 // smem: ring | barriers (2*ST + 4) | tmem slot | per-warp transpose tiles |
 //        per-warp column partials (double) | warp max
 constexpr int T_BAR_OFF = TSTAGES * T_STAGE_BYTES;
 constexpr int T_TR_OFF = T_BAR_OFF + 256;
-constexpr int T_TR_BYTES = 4 * 32 * T_TP * 4;
+constexpr int T_TR_BYTES = 8 * 32 * T_TP * 4;
 constexpr int T_COL_OFF = T_TR_OFF + T_TR_BYTES;
 constexpr int T_COL_BYTES = 4 * TBN * 2 * 8;
-constexpr int T_SMEM = T_COL_OFF + T_COL_BYTES + 64 + 1024;
+constexpr int T_ROW_OFF = T_COL_OFF + T_COL_BYTES + 64;   // after 8 warp maxima
+constexpr int T_ROW_BYTES = 2 * TBM * 4;
+constexpr int T_SMEM = T_ROW_OFF + T_ROW_BYTES + 1024;
 
 struct SParams {
   int M, N, K;
@@ -129,7 +132,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* trs = reinterpret_cast<float*>(smem + T_TR_OFF);
   double* colp = reinterpret_cast<double*>(smem + T_COL_OFF);  // [4 quarters][TBN][2]
-  double* wmaxs = colp + 4 * TBN * 2;                         // [4]
+  double* wmaxs = colp + 4 * TBN * 2;                         // [8]
+  float* rowp = reinterpret_cast<float*>(smem + T_ROW_OFF);    // [2 halves][TBM]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = p.tiles_m * p.tiles_n;
 
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], 8);
     }
     mbar_fence_init();
   }
@@ -214,12 +218,14 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       __syncwarp();
     }
   } else {
-    // ===== epilogue (warps 2..5) =====
+    // ===== epilogue (warps 2..9): two warps per TMEM lane quarter, each
+    // owning half of the tile's columns =====
     const int quarter = warp & 3;               // TMEM lane quarter of this warp
+    const int half = (warp - 2) >> 2;           // column half of the tile
     const int row_t = quarter * 32 + lane;      // row within the tile
-    float* tr = trs + quarter * 32 * T_TP;      // this warp's 32 x 33 transpose tile
+    float* tr = trs + (warp - 2) * 32 * T_TP;   // this warp's 32 x 17 transpose tile
     double* cq = colp + quarter * TBN * 2;
-    const int etid = threadIdx.x - 64;          // 0..127
+    const int etid = threadIdx.x - 64;          // 0..255
     // kernel parameters hoisted into registers once
     const float* Cg = p.C;  // may alias D (in-place update): every element is read before it is written
     float* Dg = p.D;
@@ -227,26 +233,26 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const float alpha = p.alpha, beta = p.beta;
     const int M = p.M, N = p.N;
     const bool use_c = beta != 0.0f, fuse = p.fuse != 0;
+    constexpr int HN = TBN / 2;  // columns per warp
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int acc = it & 1, use = it >> 1;
       const int tm = t % p.tiles_m, tn = t / p.tiles_m;
       const int m = tm * TBM + row_t;
       const bool rv = m < M;
-      const int c_base = tn * TBN;
+      const int c_base = tn * TBN + half * HN;
       // interior tiles take an unpredicated path (no per-element bounds)
-      const bool interior = (tm + 1) * TBM <= M && c_base + TBN <= N;
-      // The whole C row segment (128 values) is loaded before waiting for the
-      // accumulator: 128 independent coalesced loads per thread overlap this
-      // tile's MMAs (memory-level parallelism is what bounds this epilogue).
-      float cv[TBN];
+      const bool interior = (tm + 1) * TBM <= M && tn * TBN + TBN <= N;
+      // the thread's C row segment (64 values, L2-resident thanks to the
+      // producer's prefetch) is loaded before waiting for the accumulator
+      float cv[HN];
       const float* crow = Cg + m + (int64_t)c_base * ldc;
       if (use_c && interior) {
 #pragma unroll
-        for (int j = 0; j < TBN; ++j) cv[j] = __ldg(crow + (int64_t)j * ldc);
+        for (int j = 0; j < HN; ++j) cv[j] = __ldg(crow + (int64_t)j * ldc);
       } else {
 #pragma unroll
-        for (int j = 0; j < TBN; ++j)
+        for (int j = 0; j < HN; ++j)
           cv[j] = (use_c && rv && c_base + j < N) ? __ldg(crow + (int64_t)j * ldc) : 0.0f;
       }
       mbar_wait(&tfull[acc], use & 1);
@@ -256,9 +262,11 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       float rsum = 0.0f, mx = 0.0f;
       float* drow = Dg + m + (int64_t)c_base * ldd;
 #pragma unroll
-      for (int cc = 0; cc < TBN / 32; ++cc) {
+      for (int cc = 0; cc < HN / 32; ++cc) {
         float v[32];
-        tmem_ld32(tmem_base + (uint32_t)(acc * TBN + cc * 32) + ((uint32_t)(quarter * 32) << 16), v);
+        tmem_ld32(tmem_base + (uint32_t)(acc * TBN + half * HN + cc * 32) +
+                      ((uint32_t)(quarter * 32) << 16),
+                  v);
         if (interior) {
 #pragma unroll
           for (int j = 0; j < 32; ++j) {
@@ -279,20 +287,27 @@ __global__ void __launch_bounds__(T_THREADS, 1)
           for (int j = 0; j < 32; ++j) {
             rsum += v[j];
             mx = fmaxf(mx, fabsf(v[j]));
-            tr[lane * T_TP + j] = v[j];
           }
-          __syncwarp();
-          // lane j: column c_base + cc*32 + j summed over this warp's 32 rows
-          float a0 = 0.0f, a1 = 0.0f;
+          // column sums over this warp's 32 rows, 16 columns per transpose
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) tr[lane * T_TP + j] = v[hh * 16 + j];
+            __syncwarp();
+            if (lane < 16) {
+              float a0 = 0.0f, a1 = 0.0f;
 #pragma unroll 8
-          for (int r = 0; r < 32; ++r) {
-            const float x = tr[r * T_TP + lane];
-            a0 += x;
-            a1 = fmaf((float)(quarter * 32 + r), x, a1);
+              for (int r = 0; r < 32; ++r) {
+                const float x = tr[r * T_TP + lane];
+                a0 += x;
+                a1 = fmaf((float)(quarter * 32 + r), x, a1);
+              }
+              const int col = half * HN + cc * 32 + hh * 16 + lane;
+              cq[col * 2 + 0] = a0;
+              cq[col * 2 + 1] = a1;
+            }
+            __syncwarp();
           }
-          cq[(cc * 32 + lane) * 2 + 0] = a0;
-          cq[(cc * 32 + lane) * 2 + 1] = a1;
-          __syncwarp();
         }
       }
       // accumulator drained: hand TMEM back to the MMA warp
@@ -301,25 +316,33 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (fuse) {
         const FusedSums& fs = p.sums;
-        if (rv) fs.rp[m + (int64_t)tn * fs.rp_ld] = (double)rsum;
+        rowp[half * TBM + row_t] = rsum;
         mx = warp_max(mx);
-        if (lane == 0) wmaxs[quarter] = mx;
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
-        const int gc = tn * TBN + etid;
-        if (gc < N) {
-          double s0 = 0.0, s1 = 0.0;
+        if (lane == 0) wmaxs[warp - 2] = mx;
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
+        if (etid < TBN) {
+          const int gc = tn * TBN + etid;
+          if (gc < N) {
+            double s0 = 0.0, s1 = 0.0;
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            s0 += colp[(qq * TBN + etid) * 2 + 0];
-            s1 += colp[(qq * TBN + etid) * 2 + 1];
+            for (int qq = 0; qq < 4; ++qq) {
+              s0 += colp[(qq * TBN + etid) * 2 + 0];
+              s1 += colp[(qq * TBN + etid) * 2 + 1];
+            }
+            fs.cp[fs.cp_step * tm + (int64_t)gc * fs.cp_ld] = s0;
+            fs.cw[fs.cw_step * tm + (int64_t)gc * fs.cw_ld] = s1;
           }
-          fs.cp[fs.cp_step * tm + (int64_t)gc * fs.cp_ld] = s0;
-          fs.cw[fs.cw_step * tm + (int64_t)gc * fs.cw_ld] = s1;
+          // row etid of the tile: the two column halves in a fixed order
+          const int mr = tm * TBM + etid;
+          if (mr < M)
+            fs.rp[mr + (int64_t)tn * fs.rp_ld] = (double)rowp[etid] + (double)rowp[TBM + etid];
         }
-        if (etid == 0)
-          fs.bm[tm + (int64_t)tn * fs.bm_ld] =
-              fmax(fmax(wmaxs[0], wmaxs[1]), fmax(wmaxs[2], wmaxs[3]));
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        if (etid == 0) {
+          double bmx = 0.0;
+          for (int w8 = 0; w8 < 8; ++w8) bmx = fmax(bmx, wmaxs[w8]);
+          fs.bm[tm + (int64_t)tn * fs.bm_ld] = bmx;
+        }
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
       }
     }
   }
