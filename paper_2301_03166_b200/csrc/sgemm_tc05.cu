@@ -504,7 +504,10 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   CUtensorMap mc;
   memset(&mc, 0, sizeof(mc));
   p.prefetch_c = 0;
-  if (p.beta != 0.0f && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc % 4) == 0) {
+  // only worth a descriptor when CTAs run several tiles (the prefetch for
+  // tile i+1 overlaps tile i); tiny launches stay host-cheap
+  if (p.beta != 0.0f && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc % 4) == 0 &&
+      (int64_t)p.tiles_m * p.tiles_n > 148) {
     auto fn = encode_fn();
     cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
     cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
