@@ -490,8 +490,9 @@ def run_ours(args):
                     "frac": (achieved / peak.value) if achieved else None,
                     # dram read+write of one fused trailing-update launch (M=N~31.2k, K=256)
                     # from `ncu --set full` (profiles/ncu_full_gemm_lu32k_r01.txt); the
-                    # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once)
-                    "traffic": 26.63e9 if args.kind == "lu" else None,
+                    # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once);
+                    # 26.63e9 before the grouped unit order
+                    "traffic": 16.25e9 if args.kind == "lu" else None,
                     "traffic_algorithmic": 15.7e9 if args.kind == "lu" else None,
                     "peak_source": "measured DMMA issue rate on this GPU "
                                    "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"}

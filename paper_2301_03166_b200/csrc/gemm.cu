@@ -158,6 +158,7 @@ struct KParams {
   int c_shift;
   // fused checksums: each warpgroup owns whole fb x fb blocks (fb = 128/256)
   int fuse, fb, ntm_b, ntn_b, nbr_b, nbc_b;
+  int unit_group;        // block rows per unit group (fused mode rasterization)
   FusedSums sums;
   int partial;           // 1: write raw acc to D (= split workspace slice z)
   int64_t split_stride;  // elements between split slices in partial mode
@@ -201,12 +202,12 @@ ABFT_DEVINL int total_units(const KParams& p) {
 // panels (GROUP x fb rows) and B strips stay L2-resident and are reused
 // instead of re-read from DRAM (plain column-major order re-read the whole
 // L21 panel per strip column: 1.7x the algorithmic DRAM traffic).
-constexpr int UNIT_GROUP = 16;
 ABFT_DEVINL void unit_coords(const KParams& p, int unit, int* bi, int* tcol) {
-  const int per_group = UNIT_GROUP * p.tiles_n;
+  const int G = p.unit_group;
+  const int per_group = G * p.tiles_n;
   const int g = unit / per_group, r = unit - g * per_group;
-  const int rows_g = min(UNIT_GROUP, p.nbr_b - g * UNIT_GROUP);
-  *bi = g * UNIT_GROUP + r % rows_g;
+  const int rows_g = min(G, p.nbr_b - g * G);
+  *bi = g * G + r % rows_g;
   *tcol = r / rows_g;
 }
 template <int BM>
@@ -778,6 +779,12 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
     kp.nbr_b = (M + fb - 1) / fb;
     kp.nbc_b = (N + fb - 1) / fb;
     kp.sums = *fs;
+    static int ug = [] {
+      const char* e = getenv("ABFT_UNIT_GROUP");
+      const int v = e ? atoi(e) : 0;
+      return v > 0 ? v : 16;  // ABFT_UNIT_GROUP=100000 restores plain column-major strips
+    }();
+    kp.unit_group = ug;
   }
   if (splits > 1) {
     kp.C = nullptr;
