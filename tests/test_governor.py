@@ -148,3 +148,27 @@ def test_trace_format_matches_reference_layout(tmp_path):
     except ImportError:
         return
     assert RC.TRACE_HEADER == G.TRACE_HEADER
+
+
+@pytest.mark.gpu
+def test_recovery_policies_on_b200():
+    """_Run recovery (simulator.py:456-481): SINGLE flags 1-D faults as
+    uncorrectable; 'abort' stops, 'continue' keeps going, 'recompute'
+    restores the device snapshot and retries."""
+    import paper_2301_03166_b200 as P
+    a = P.generate_test_matrix("lu", 1024, 3)
+    table = G.ErrorRateTable({"1d": [(100.0, 0.0), (2200.0, 3e3)]})
+    out = {}
+    for policy in ("abort", "continue", "recompute"):
+        out[policy] = G.run_mode("lu", a, 128, "bsr", r=1.0, seed=3, rates=table,
+                                 forced_scheme="single", recovery=policy)
+    s_abort, r_abort = out["abort"]
+    s_cont, r_cont = out["continue"]
+    s_rec, r_rec = out["recompute"]
+    assert sum(s_cont.faults_injected.values()) > 0
+    assert len(r_cont) == 8 and not s_cont.unrecoverable
+    if s_cont.faults_detected:  # some 1-D fault was flagged: abort must stop there
+        assert s_abort.unrecoverable and len(r_abort) < 8
+    assert s_rec.retries > 0 or s_rec.faults_detected == 0
+    if not s_rec.unrecoverable:
+        assert s_rec.correct
