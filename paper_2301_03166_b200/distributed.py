@@ -203,6 +203,7 @@ class DistributedFactorization:
         self._tx = _Transport(group, lib.abft_dist_stream(ctx), self.device,
                               lib.abft_dist_comm_stream(ctx))
         self.lookahead = os.environ.get("ABFT_NO_LOOKAHEAD") != "1"
+        self.force_lookahead = False  # exercise the look-ahead machinery on one rank (tests)
         self._prefetched = set()
 
     def __del__(self):
@@ -256,8 +257,8 @@ class DistributedFactorization:
         # broadcast on the comm stream while the trailing update of k runs
         nb = self.layout.n_blocks
         xe1 = int(lib.abft_dist_xbuf_elems(ctx, k + 1)) if k + 1 < nb else 0
-        la = (self.lookahead and self.world > 1 and self.kind == DecompositionKind.LU
-              and nplan == 0 and xe1 > 0)
+        la = (self.lookahead and (self.world > 1 or self.force_lookahead)
+              and self.kind == DecompositionKind.LU and nplan == 0 and xe1 > 0)
         nxt = self._bufs[(k + 1) % 2]
         if la:
             check(lib.abft_dist_lookahead(ctx, k, ctypes.c_void_p(nxt.data_ptr())))

@@ -82,3 +82,39 @@ def cpu_merge(rank: int, world: int, init_file: str, out: str) -> None:
                    "locations": [r.locations for r in reps]}, fh, default=str)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def nccl_single(rank: int, world: int, init_file: str, out: str) -> None:
+    """World-size-1 NCCL group: the native transport (device tensors on the
+    context / comm streams) and the look-ahead machinery against the
+    single-GPU path, bit for bit."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"file://{init_file}", rank=rank,
+                            world_size=world, device_id=torch.device("cuda", 0))
+    import paper_2301_03166_b200 as P
+    from paper_2301_03166_b200.distributed import DistributedFactorization
+    res = {}
+    for kind in ("lu", "qr", "cholesky"):
+        n, b, seed = 768, 128, 13
+        a = P.generate_test_matrix(kind, n, seed)
+        sched = {1: {"0d": 1}, 3: {"0d": 1}}
+        f = DistributedFactorization(kind, a, b)
+        f.force_lookahead = True
+        reps = f.run_protected("full", sched, np.random.default_rng(seed))
+        full = f.gather(0)
+        f1 = P.Factorization(kind, a, b)
+        reps1 = P.run_protected(f1, "full", sched, np.random.default_rng(seed))
+        res[kind] = {
+            "same_reports": [r.locations for r in reps] == [r.locations for r in reps1],
+            "max_diff": float(np.max(np.abs(full - f1.m))),
+            "residual": f.residual(a),
+            "residual1": P.residual(a, f1),
+        }
+    import json
+    with open(os.path.join(out, "nccl.json"), "w") as fh:
+        json.dump(res, fh, default=str)
+    dist.barrier()
+    dist.destroy_process_group()

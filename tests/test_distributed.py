@@ -133,3 +133,16 @@ def test_distributed_matches_oracle(tmp_path, world):
         sched = {int(k): v for k, v in c["schedule"].items()}
         P.run_protected(f1, c["scheme"], sched, rng)
         np.testing.assert_allclose(full, f1.m, rtol=1e-9, atol=1e-9)
+
+
+@pytest.mark.gpu
+def test_nccl_transport_and_lookahead_on_one_rank(tmp_path):
+    from dist_worker import nccl_single
+    _spawn(nccl_single, 1, str(tmp_path / "init"), str(tmp_path))
+    res = json.loads((tmp_path / "nccl.json").read_text())
+    for kind, r in res.items():
+        assert r["same_reports"], kind
+        # LU and QR: identical kernels, identical results; Cholesky's
+        # distributed form sums its panel products in another order
+        assert r["max_diff"] <= (0.0 if kind != "cholesky" else 1e-10), (kind, r)
+        assert r["residual"] < 1e-12 and r["residual1"] < 1e-12, (kind, r)
