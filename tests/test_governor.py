@@ -157,7 +157,7 @@ def test_recovery_policies_on_b200():
     restores the device snapshot and retries."""
     import paper_2301_03166_b200 as P
     a = P.generate_test_matrix("lu", 1024, 3)
-    table = G.ErrorRateTable({"1d": [(100.0, 0.0), (2200.0, 3e3)]})
+    table = G.ErrorRateTable({"1d": [(100.0, 0.0), (2200.0, 5e4)]})
     out = {}
     for policy in ("abort", "continue", "recompute"):
         out[policy] = G.run_mode("lu", a, 128, "bsr", r=1.0, seed=3, rates=table,
