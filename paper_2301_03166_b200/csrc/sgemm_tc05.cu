@@ -48,10 +48,12 @@ constexpr int T_BAR_OFF = TSTAGES * T_STAGE_BYTES;
 constexpr int T_TR_OFF = T_BAR_OFF + 256;
 constexpr int T_TR_BYTES = 8 * 32 * T_TP * 4;
 constexpr int T_COL_OFF = T_TR_OFF + T_TR_BYTES;
-constexpr int T_COL_BYTES = 4 * TBN * 2 * 8;
-constexpr int T_ROW_OFF = T_COL_OFF + T_COL_BYTES + 64;   // after 8 warp maxima
-constexpr int T_ROW_BYTES = 2 * TBM * 4;
-constexpr int T_SMEM = T_ROW_OFF + T_ROW_BYTES + 1024;
+// per-tile cross-warp partials, double-buffered by tile parity so one
+// named barrier per tile suffices: column sums [4 quarters][TBN][2] fp32,
+// row sums [2 halves][TBM] fp32, warp maxima [8] fp32
+constexpr int T_PART_FLOATS = 4 * TBN * 2 + 2 * TBM + 8;
+constexpr int T_COL_BYTES = 2 * T_PART_FLOATS * 4;
+constexpr int T_SMEM = T_COL_OFF + T_COL_BYTES + 1024;
 
 struct SParams {
   int M, N, K;
@@ -131,9 +133,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   uint64_t* tempty = tfull + 2;        // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   float* trs = reinterpret_cast<float*>(smem + T_TR_OFF);
-  double* colp = reinterpret_cast<double*>(smem + T_COL_OFF);  // [4 quarters][TBN][2]
-  double* wmaxs = colp + 4 * TBN * 2;                         // [8]
-  float* rowp = reinterpret_cast<float*>(smem + T_ROW_OFF);    // [2 halves][TBM]
+  float* parts = reinterpret_cast<float*>(smem + T_COL_OFF);   // [2 parities][T_PART_FLOATS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = p.tiles_m * p.tiles_n;
 
@@ -224,7 +224,6 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const int half = (warp - 2) >> 2;           // column half of the tile
     const int row_t = quarter * 32 + lane;      // row within the tile
     float* tr = trs + (warp - 2) * 32 * T_TP;   // this warp's 32 x 17 transpose tile
-    double* cq = colp + quarter * TBN * 2;
     const int etid = threadIdx.x - 64;          // 0..255
     // kernel parameters hoisted into registers once
     const float* Cg = p.C;  // may alias D (in-place update): every element is read before it is written
@@ -234,6 +233,22 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const int M = p.M, N = p.N;
     const bool use_c = beta != 0.0f, fuse = p.fuse != 0;
     constexpr int HN = TBN / 2;  // columns per warp
+    float cv[HN];
+    auto load_c = [&](int tt, float* dst) {
+      const int tm2 = tt % p.tiles_m, tn2 = tt / p.tiles_m;
+      const int m2 = tm2 * TBM + row_t;
+      const int cb2 = tn2 * TBN + half * HN;
+      const bool int2 = (tm2 + 1) * TBM <= M && tn2 * TBN + TBN <= N;
+      const float* crow = Cg + m2 + (int64_t)cb2 * ldc;
+      if (use_c && int2) {
+#pragma unroll
+        for (int j = 0; j < HN; ++j) dst[j] = __ldg(crow + (int64_t)j * ldc);
+      } else {
+#pragma unroll
+        for (int j = 0; j < HN; ++j)
+          dst[j] = (use_c && m2 < M && cb2 + j < N) ? __ldg(crow + (int64_t)j * ldc) : 0.0f;
+      }
+    };
     int it = 0;
     for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
       const int acc = it & 1, use = it >> 1;
@@ -244,17 +259,9 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       // interior tiles take an unpredicated path (no per-element bounds)
       const bool interior = (tm + 1) * TBM <= M && tn * TBN + TBN <= N;
       // the thread's C row segment (64 values, L2-resident thanks to the
-      // producer's prefetch) is loaded before waiting for the accumulator
-      float cv[HN];
-      const float* crow = Cg + m + (int64_t)c_base * ldc;
-      if (use_c && interior) {
-#pragma unroll
-        for (int j = 0; j < HN; ++j) cv[j] = __ldg(crow + (int64_t)j * ldc);
-      } else {
-#pragma unroll
-        for (int j = 0; j < HN; ++j)
-          cv[j] = (use_c && rv && c_base + j < N) ? __ldg(crow + (int64_t)j * ldc) : 0.0f;
-      }
+      // producer's prefetch): loaded at the end of the previous tile's
+      // epilogue (software pipelining across tiles), or here for the first
+      if (it == 0) load_c(t, cv);
       mbar_wait(&tfull[acc], use & 1);
       tc_fence_after();
       // in-tile sums in fp32 (<= 128 terms: error <= ~128 eps32 max|x|, 50x
@@ -303,6 +310,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
                 a1 = fmaf((float)(quarter * 32 + r), x, a1);
               }
               const int col = half * HN + cc * 32 + hh * 16 + lane;
+              float* cq = parts + acc * T_PART_FLOATS + quarter * TBN * 2;
               cq[col * 2 + 0] = a0;
               cq[col * 2 + 1] = a1;
             }
@@ -314,11 +322,20 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
+      // next tile's C loads go out now; their latency hides behind the
+      // cross-warp combine below and the next accumulator wait
+      if (t + (int)gridDim.x < tiles) load_c(t + gridDim.x, cv);
       if (fuse) {
         const FusedSums& fs = p.sums;
+        float* pp = parts + acc * T_PART_FLOATS;
+        float* rowp = pp + 4 * TBN * 2;
+        float* wmx = rowp + 2 * TBM;
         rowp[half * TBM + row_t] = rsum;
         mx = warp_max(mx);
-        if (lane == 0) wmaxs[warp - 2] = mx;
+        if (lane == 0) wmx[warp - 2] = mx;
+        // one barrier per tile: the partials are double-buffered by parity,
+        // and the barrier of tile i+1 orders this combine before tile i+2
+        // overwrites the buffer
         asm volatile("bar.sync 1, 256;\n" ::: "memory");
         if (etid < TBN) {
           const int gc = tn * TBN + etid;
@@ -326,8 +343,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
             double s0 = 0.0, s1 = 0.0;
 #pragma unroll
             for (int qq = 0; qq < 4; ++qq) {
-              s0 += colp[(qq * TBN + etid) * 2 + 0];
-              s1 += colp[(qq * TBN + etid) * 2 + 1];
+              s0 += (double)pp[(qq * TBN + etid) * 2 + 0];
+              s1 += (double)pp[(qq * TBN + etid) * 2 + 1];
             }
             fs.cp[fs.cp_step * tm + (int64_t)gc * fs.cp_ld] = s0;
             fs.cw[fs.cw_step * tm + (int64_t)gc * fs.cw_ld] = s1;
@@ -338,11 +355,10 @@ __global__ void __launch_bounds__(T_THREADS, 1)
             fs.rp[mr + (int64_t)tn * fs.rp_ld] = (double)rowp[etid] + (double)rowp[TBM + etid];
         }
         if (etid == 0) {
-          double bmx = 0.0;
-          for (int w8 = 0; w8 < 8; ++w8) bmx = fmax(bmx, wmaxs[w8]);
-          fs.bm[tm + (int64_t)tn * fs.bm_ld] = bmx;
+          float bmx = 0.0f;
+          for (int w8 = 0; w8 < 8; ++w8) bmx = fmaxf(bmx, wmx[w8]);
+          fs.bm[tm + (int64_t)tn * fs.bm_ld] = (double)bmx;
         }
-        asm volatile("bar.sync 1, 256;\n" ::: "memory");
       }
     }
   }
