@@ -117,6 +117,8 @@ struct abft_sctx {
   int32_t* dlist = nullptr;
   int dlist_cap = 0;
   int* info = nullptr;
+  int64_t el_for = -1;  // iteration whose operand sums E_L / R E_R came out of the
+  int64_t er_for = -1;  // PD / PU GEMM epilogues (no separate checksum pass)
   int64_t k_done = 0;
   bool sums_valid = false;
   int64_t breakdown_col = -1;
@@ -239,8 +241,25 @@ int s_lu_l21(abft_sctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   if (pe >= n) return 0;
   float* D = c->m + p + p * c->ld;
+  // b = 128: the GEMM epilogue also emits the block column sums of L21 =
+  // the operand sums E_L of the maintenance of iteration k (abft.py:147-152)
+  FusedSums fs;
+  const bool fuse = c->fuse_enabled && c->b == 128 && w == 128;
+  if (fuse) {
+    fs.cp = c->el;
+    fs.cp_ld = c->ld_cs;
+    fs.cp_step = 2;
+    fs.cw = c->el + 1;
+    fs.cw_ld = c->ld_cs;
+    fs.cw_step = 2;
+    fs.rp = c->lwd;  // row sums / maxima are not needed: scratch
+    fs.rp_ld = c->ld;
+    fs.bm = c->scratch;
+    fs.bm_ld = 1;
+  }
   ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, w, w, 1.0f, D + w, c->ld, c->uinv, c->ld_t, 0.0f, nullptr, 0,
-                  c->lw, c->ld));
+                  c->lw, c->ld, fuse ? &fs : nullptr));
+  c->el_for = fuse ? k : -1;
   return copy_matrix(c->st, c->lw, c->ld, D + w, c->ld, n - pe, w);
 }
 
@@ -275,8 +294,24 @@ int s_pu(abft_sctx* c, int64_t k) {
   if (c->kind == ABFT_LU) {
     if (pe < n) {
       float* U12 = c->m + p + pe * c->ld;
+      // b = 128: the epilogue also emits the block row sums of U12 = R E_R
+      FusedSums fs;
+      const bool fuse = c->fuse_enabled && c->b == 128 && w == 128;
+      if (fuse) {
+        fs.cp = c->uwd;  // column sums are not needed: scratch
+        fs.cp_ld = c->ld_t;
+        fs.cp_step = 1;
+        fs.cw = c->uwd + 1;
+        fs.cw_ld = c->ld_t;
+        fs.cw_step = 1;
+        fs.rp = c->er;
+        fs.rp_ld = c->ld_t;
+        fs.bm = c->scratch + 2048;
+        fs.bm_ld = 1;
+      }
       ABFT_TRY(s_gemm(c, 'N', 'N', w, n - pe, w, 1.0f, c->linv, c->ld_t, U12, c->ld, 0.0f, nullptr, 0,
-                      c->uw, c->ld_t));
+                      c->uw, c->ld_t, fuse ? &fs : nullptr));
+      c->er_for = fuse ? k : -1;
       ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, U12, c->ld, w, n - pe));
     }
   } else {
@@ -331,7 +366,7 @@ int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int6
   const float* L = c->kind == ABFT_LU ? c->m + pe + p * c->ld : c->vstore + p + p * c->ld;
   const float* R = c->kind == ABFT_LU ? c->m + p + pe * c->ld : c->mid;
   const int64_t ldr = c->kind == ABFT_LU ? c->ld : c->ld_t;
-  {
+  if (!(c->kind == ABFT_LU && c->el_for == k)) {
     RegionF rl{const_cast<float*>(L), c->ld, rows, w, c->b};
     SumOut o;
     o.cp = c->el;
@@ -346,11 +381,13 @@ int s_maintain(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int6
   ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, c->el, c->ld_cs, c->uwd,
                 c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
   if (scheme == ABFT_FULL) {
-    RegionF rr{const_cast<float*>(R), ldr, w, cols, c->b};
-    SumOut o;
-    o.rp = c->er;
-    o.rp_ld = c->ld_t;
-    ABFT_TRY(blocksum(c->st, rr, o));
+    if (!(c->kind == ABFT_LU && c->er_for == k)) {
+      RegionF rr{const_cast<float*>(R), ldr, w, cols, c->b};
+      SumOut o;
+      o.rp = c->er;
+      o.rp_ld = c->ld_t;
+      ABFT_TRY(blocksum(c->st, rr, o));
+    }
     ABFT_TRY(widen_matrix(c->st, L, c->ld, c->lwd, c->ld, rows, w));
     ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbc, (int)w, -1.0, c->lwd, c->ld, c->er, c->ld_t,
                   1.0, enc.rp, c->ld, c->rsm, c->ld, &c->gws));
@@ -619,14 +656,19 @@ int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
   const float* U12 = c->m + p + pe * c->ld;
   float* A22 = c->m + pe + pe * c->ld;
   const int64_t wa = std::min<int64_t>(c->b, cols);
+  const bool fuse_a = prot && c->fuse_enabled && c->b == 128;
+  FusedSums fsa;
+  if (fuse_a) fsa = s_fused(c, r0, c0);
   smark(c, SP_TMU, true);
   ABFT_TRY(s_gemm(c, 'N', 'N', rows, wa, w, -1.0f, L21, c->ld, U12, c->ld, 1.0f, A22, c->ld, A22,
-                  c->ld));
+                  c->ld, fuse_a ? &fsa : nullptr));
   smark(c, SP_TMU, false);
   if (prot) {
     smark(c, SP_ABFT, true);
-    RegionF ra{A22, c->ld, rows, wa, c->b};
-    ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, c0, true)));
+    if (!fuse_a) {
+      RegionF ra{A22, c->ld, rows, wa, c->b};
+      ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, c0, true)));
+    }
     ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 0, 1));
     smark(c, SP_ABFT, false);
   }
@@ -901,6 +943,8 @@ ABFT_API int abft_s_keep_input(abft_sctx* c, int keep) {
 }
 
 static void s_reset_state(abft_sctx* c) {
+  c->el_for = -1;
+  c->er_for = -1;
   c->chol_rs_valid = false;
   c->qr_count = 0;
   c->pd_ready = -1;
