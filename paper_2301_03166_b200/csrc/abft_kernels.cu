@@ -545,6 +545,9 @@ static int blocksum_t(cudaStream_t st, const RegionT<T>& reg, const SumOut& out,
   int64_t nblk = blocks ? max_list : nbr * nbc;
   if (nblk <= 0) return 0;
   int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
+  // device-counted lists (dirty blocks after repairs) are almost always
+  // empty: a one-wave grid keeps the no-op launch cheap
+  if (nblocks_dev && grid > 148) grid = 148;
   count_launch();
   blocksum_kernel<T><<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
                                                      (int64_t)max_list);
