@@ -114,8 +114,6 @@ struct abft_ctx {
   int64_t chol_part = -1;         // Cholesky: panel whose update from panels 0..k-2 is done
   bool chol_enc_ahead = false;    // ... and whose encode ran with it
   int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
-  int64_t el_for = -1;            // iteration whose E_L / R E_R came out of the PD / PU
-  int64_t er_for = -1;            // GEMM epilogues (no separate checksum pass)
   GemmWorkspace gws2;             // split-K workspace of the side stream
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
@@ -298,42 +296,11 @@ int lu_diag(abft_ctx* c, cudaStream_t st, int64_t k) {
 }
 
 // LU panel, part 2: L21 = A21 U11^{-1} (GEMM over all SMs).
-// Fused-epilogue outputs that only feed scratch (row sums / maxima nobody reads).
-FusedSums scratch_sums(abft_ctx* c) {
-  FusedSums f;
-  f.rpp = c->fpart;
-  f.rpp_ld = c->ld;
-  f.bmp = c->fmaxp;
-  f.bmp_ld = c->ld_max;
-  f.bm = c->scratch;
-  f.bm_ld = 1;
-  return f;
-}
-
 int lu_l21(abft_ctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   if (pe >= n) return 0;
-  if (c->fuse_enabled && gemm_can_fuse((int)c->b) && w == c->b) {
-    // the epilogue also emits the block column sums of L21: the operand
-    // sums E_L of iteration k's maintenance (abft.py:147-152), no extra pass
-    FusedSums f = scratch_sums(c);
-    f.cp = c->el;
-    f.cp_ld = c->ld_cs;
-    f.cp_step = 2;
-    f.cw = c->el + 1;
-    f.cw_ld = c->ld_cs;
-    f.cw_step = 2;
-    f.rp = c->rsm;  // scratch until maintain(k) rewrites it
-    f.rp_ld = c->ld;
-    ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0,
-                             c->m + pe + p * c->ld, c->ld, c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw,
-                             c->ld, (int)c->b, f));
-    c->el_for = k;
-  } else {
-    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld, c->ld,
-                  c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
-    c->el_for = -1;
-  }
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, c->m + pe + p * c->ld, c->ld,
+                c->uinv, c->ld_t, 0.0, nullptr, 0, c->lw, c->ld, &c->gws));
   return copy_matrix(c->st, c->lw, c->ld, c->m + pe + p * c->ld, c->ld, n - pe, w);
 }
 
@@ -377,26 +344,8 @@ int task_pu(abft_ctx* c, int64_t k) {
     if (c->chol_rs_valid) ABFT_TRY(chol_rs_update(c, k));
   } else if (c->kind == ABFT_LU) {
     if (pe < n) {
-      if (c->fuse_enabled && gemm_can_fuse((int)c->b) && w == c->b) {
-        // the epilogue also emits the block row sums of U12 = R E_R
-        FusedSums f = scratch_sums(c);
-        f.cp = c->csm;  // scratch until maintain(k) rewrites it
-        f.cp_ld = c->ld_cs;
-        f.cp_step = 2;
-        f.cw = c->csm + 1;
-        f.cw_ld = c->ld_cs;
-        f.cw_step = 2;
-        f.rp = c->er;
-        f.rp_ld = c->ld_t;
-        ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)w, (int)(n - pe), (int)w, 1.0, c->linv,
-                                 c->ld_t, c->m + p + pe * c->ld, c->ld, 0.0, nullptr, 0, c->uw,
-                                 c->ld_t, (int)c->b, f));
-        c->er_for = k;
-      } else {
-        ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(n - pe), (int)w, 1.0, c->linv, c->ld_t,
-                      c->m + p + pe * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, &c->gws));
-        c->er_for = -1;
-      }
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(n - pe), (int)w, 1.0, c->linv, c->ld_t,
+                    c->m + p + pe * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, &c->gws));
       ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, c->m + p + pe * c->ld, c->ld, w, n - pe));
     }
   }
@@ -481,7 +430,7 @@ int maintain(abft_ctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t
     ldr = c->ld_t;
   }
   // E_L: plain/weighted block-row sums of L (rows x w), interleaved in el
-  if (!(c->kind == ABFT_LU && c->el_for == k)) {
+  {
     Region rl{const_cast<double*>(L), ldl, rows, w, c->b};
     SumOut o;
     o.cp = c->el;
@@ -495,13 +444,11 @@ int maintain(abft_ctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t
   ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, c->el, c->ld_cs, R, ldr,
                 1.0, enc.cp, c->ld_cs, c->csm, c->ld_cs, &c->gws));
   if (scheme == ABFT_FULL) {
-    if (!(c->kind == ABFT_LU && c->er_for == k)) {
-      Region rr{const_cast<double*>(R), ldr, w, cols, c->b};
-      SumOut o;
-      o.rp = c->er;
-      o.rp_ld = c->ld_t;
-      ABFT_TRY(blocksum(c->st, rr, o));
-    }
+    Region rr{const_cast<double*>(R), ldr, w, cols, c->b};
+    SumOut o;
+    o.rp = c->er;
+    o.rp_ld = c->ld_t;
+    ABFT_TRY(blocksum(c->st, rr, o));
     ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbc, (int)w, -1.0, L, ldl, c->er, c->ld_t, 1.0,
                   enc.rp, c->ld, c->rsm, c->ld, &c->gws));
   }
@@ -799,20 +746,13 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   const int64_t wa = std::min<int64_t>(c->b, cols);
   // (a) next panel's block column, plain tiles over all SMs + checksum pass
   prof_mark(c, PROF_TMU, true);
-  if (prot && wa == c->b) {  // block column with its checksums from the epilogue
-    ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, L21, c->ld, U12,
-                             c->ld, 1.0, A22, c->ld, A22, c->ld, (int)c->b, fused_for(c, r0, c0)));
-  } else {
-    ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, L21, c->ld, U12, c->ld, 1.0,
-                  A22, c->ld, A22, c->ld, &c->gws));
-  }
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, L21, c->ld, U12, c->ld, 1.0, A22,
+                c->ld, A22, c->ld, &c->gws));
   prof_mark(c, PROF_TMU, false);
   if (prot) {
     prof_mark(c, PROF_ABFT, true);
-    if (wa != c->b) {
-      Region ra{A22, c->ld, rows, wa, c->b};
-      ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, c0, true)));
-    }
+    Region ra{A22, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, c0, true)));
     ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
     prof_mark(c, PROF_ABFT, false);
   }
@@ -1130,8 +1070,6 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
-  c->el_for = -1;
-  c->er_for = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
@@ -1153,8 +1091,6 @@ ABFT_API int abft_reset(abft_ctx* c) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
-  c->el_for = -1;
-  c->er_for = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
@@ -1427,8 +1363,6 @@ ABFT_API int abft_restore(abft_ctx* c, int slot) {
   c->pd_ready = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
-  c->el_for = -1;
-  c->er_for = -1;
   CUDA_TRY(cudaStreamSynchronize(c->st));
   return 0;
 }
