@@ -58,29 +58,42 @@ __global__ void __launch_bounds__(BS_THREADS)
       double racc[8], rwacc[8];
 #pragma unroll
       for (int i = 0; i < 8; ++i) racc[i] = rwacc[i] = 0.0;
-      for (int c = warp; c < bc; c += 8) {
-        const T* col = base + (int64_t)c * reg.ld + r0;
-        double x[8];
+      // each warp takes 4 adjacent columns per step and issues all 32 of its
+      // loads per lane before reducing: 4x the memory-level parallelism of a
+      // column-at-a-time loop (panel-shaped regions have few blocks, so
+      // per-CTA bandwidth is what bounds this pass)
+      constexpr int C4 = 4;
+      for (int cb = warp * C4; cb < bc; cb += 8 * C4) {
+        double x[C4][8];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = lane + 32 * i;
-          x[i] = (r0 + r < br) ? (double)col[r] : 0.0;
-        }
-        double cs = 0.0, cw = 0.0;
+        for (int q = 0; q < C4; ++q) {
+          const int c = cb + q;
+          const T* col = base + (int64_t)c * reg.ld + r0;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = lane + 32 * i;
-          cs += x[i];
-          cw += (double)(r0 + r) * x[i];
-          racc[i] += x[i];
-          if (want_rw) rwacc[i] += (double)c * x[i];
-          mx = fmax(mx, fabs(x[i]));
+          for (int i = 0; i < 8; ++i) {
+            const int r = lane + 32 * i;
+            x[q][i] = (c < bc && r0 + r < br) ? (double)col[r] : 0.0;
+          }
         }
-        cs = warp_sum(cs);
-        cw = warp_sum(cw);
-        if (lane == 0) {
-          colacc_p[c] += cs;
-          colacc_w[c] += cw;
+#pragma unroll
+        for (int q = 0; q < C4; ++q) {
+          const int c = cb + q;
+          double cs = 0.0, cw = 0.0;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = lane + 32 * i;
+            cs += x[q][i];
+            cw += (double)(r0 + r) * x[q][i];
+            racc[i] += x[q][i];
+            if (want_rw) rwacc[i] += (double)c * x[q][i];
+            mx = fmax(mx, fabs(x[q][i]));
+          }
+          cs = warp_sum(cs);
+          cw = warp_sum(cw);
+          if (lane == 0 && c < bc) {
+            colacc_p[c] += cs;
+            colacc_w[c] += cw;
+          }
         }
       }
       if (want_rp || want_rw) {
