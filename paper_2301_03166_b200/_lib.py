@@ -157,7 +157,8 @@ def load(path: str | os.PathLike | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        # ABFT_LIB: an alternative build of the same library (A/B measurements)
+        p = Path(path) if path else Path(os.environ.get("ABFT_LIB", str(LIB_PATH)))
         if not p.exists():
             raise LibraryUnavailable(
                 f"{p} not found: build it with `python -m paper_2301_03166_b200.build` "

@@ -115,9 +115,7 @@ constexpr int WG_THREADS = 128;
 constexpr int MAXFB = 256;
 // per-WG fused-checksum accumulators: col plain/weighted [2 wm halves][fb][2],
 // row plain [2 wn halves][fb], warp max [4]
-// strip-local column accumulators [2 wm halves][BN][2], block-row row
-// accumulators [2 wn halves][MAXFB], warp maxima [4]
-constexpr int SUM_DOUBLES = 2 * 64 * 2 + 2 * MAXFB + 4;
+constexpr int SUM_DOUBLES = 2 * MAXFB * 2 + 2 * MAXFB + 4;
 
 template <int NWG>
 struct Cfg;
@@ -127,7 +125,7 @@ struct Cfg<2> {
 };
 template <>
 struct Cfg<3> {
-  static constexpr int WTM = 32, BM = 64, STAGES = 4;
+  static constexpr int WTM = 32, BM = 64, STAGES = 3;
 };
 template <int NWG>
 struct Geo {
@@ -331,8 +329,8 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
   uint64_t* tok = bars + NWG * 2 * STAGES;
   const uint32_t ring = smem_u32(smem + wg * G::RING_BYTES);
   // fused-checksum accumulators of this warpgroup
-  double* colacc = sums_base + wg * SUM_DOUBLES;   // [2][BN][2] (strip-local columns)
-  double* rowacc = colacc + 2 * BN * 2;            // [2][MAXFB]
+  double* colacc = sums_base + wg * SUM_DOUBLES;   // [2][MAXFB][2]
+  double* rowacc = colacc + 2 * MAXFB * 2;         // [2][MAXFB]
   double* wmax = rowacc + 2 * MAXFB;               // [4]
   uint32_t q = 0;
   int jt = 0;  // tiles processed by this WG
@@ -573,9 +571,9 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
           v[i] = (g0 ? v[i + 2] : v[i]) + __shfl_xor_sync(0xffffffffu, snd, 4);
         }
         // this lane now owns (cf, tt) = (g >> 1, g & 1): plain v[0], weighted v[1]
-        const int c = wn + col_of<BT>(g >> 1, 2 * j + (g & 1));  // strip-local column
-        colacc[((wi & 1) * BN + c) * 2 + 0] += v[0];
-        colacc[((wi & 1) * BN + c) * 2 + 1] += v[1];
+        const int c = tn * BN + wn + col_of<BT>(g >> 1, 2 * j + (g & 1));
+        colacc[((wi & 1) * MAXFB + c) * 2 + 0] += v[0];
+        colacc[((wi & 1) * MAXFB + c) * 2 + 1] += v[1];
       }
     }
     if (p.fuse) {
@@ -593,9 +591,10 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
       const int cols_s = min(BN, p.N - (bj * p.fb + c0s));
       const FusedSums& fs = p.sums;
       for (int c = tid; c < cols_s; c += 128) {
-        const int64_t gc = (int64_t)bj * p.fb + c0s + c;
-        fs.cp[fs.cp_step * bi + gc * fs.cp_ld] = colacc[c * 2 + 0] + colacc[(BN + c) * 2 + 0];
-        fs.cw[fs.cw_step * bi + gc * fs.cw_ld] = colacc[c * 2 + 1] + colacc[(BN + c) * 2 + 1];
+        const int cc = c0s + c;
+        const int64_t gc = (int64_t)bj * p.fb + cc;
+        fs.cp[fs.cp_step * bi + gc * fs.cp_ld] = colacc[cc * 2 + 0] + colacc[(MAXFB + cc) * 2 + 0];
+        fs.cw[fs.cw_step * bi + gc * fs.cw_ld] = colacc[cc * 2 + 1] + colacc[(MAXFB + cc) * 2 + 1];
       }
       const int64_t scol = (int64_t)bj * p.ntn_b + tn;
       for (int r = tid; r < rows_b; r += 128)
@@ -603,7 +602,10 @@ __global__ void __launch_bounds__(Geo<NWG>::THREADS, 1)
       if (tid == 0)
         fs.bmp[bi + scol * fs.bmp_ld] = fmax(fmax(wmax[0], wmax[1]), fmax(wmax[2], wmax[3]));
       asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
-      for (int t = tid; t < 4 * BN; t += 128) colacc[t] = 0.0;
+      for (int t = tid; t < 4 * BN; t += 128) {
+        const int half = t / (2 * BN), rem = t % (2 * BN);
+        colacc[(half * MAXFB + c0s + (rem >> 1)) * 2 + (rem & 1)] = 0.0;
+      }
       for (int t = tid; t < 2 * MAXFB; t += 128) rowacc[t] = 0.0;
       asm volatile("bar.sync %0, 128;\n" ::"r"(1 + wg) : "memory");
     }
