@@ -632,20 +632,24 @@ def run_e2e_s(arm, args):
 
 
 def run_e2e_dist(arm, args):
-    """e2e at N>1: every rank copies its column blocks of the pinned host
-    input in, runs the distributed factorization and copies its columns out;
-    time = max over ranks."""
+    """e2e at N>1: every rank copies its column blocks (pinned host, n x
+    local columns: 1/N of the matrix per rank) in, runs the distributed
+    factorization and copies its columns out; time = max over ranks."""
     import torch
+    from paper_2301_03166_b200.distributed import scatter_columns
     f, n = arm.f, args.n
-    pinned_in = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy()
-    pinned_in[...] = arm.host.T
+    rank = torch.distributed.get_rank()
+    local = scatter_columns(arm.host, args.b, rank, f.world)
+    pinned_in = torch.empty((max(f.ncl, 1), n), dtype=torch.float64, pin_memory=True).numpy()
+    pinned_in[:f.ncl] = local.T
     src = pinned_in.T
-    pinned_out = torch.empty((f.ncl, n), dtype=torch.float64, pin_memory=True).numpy().T
+    pinned_out = torch.empty((max(f.ncl, 1), n), dtype=torch.float64, pin_memory=True).numpy().T
     times = []
     for i in range(1 + args.steps):
         torch.distributed.barrier()
         t0 = time.perf_counter()
-        f.set_matrix(src)
+        f._prefetched.clear()
+        arm.P.linalg.check(arm.lib.abft_dist_set_local(f._ctx, arm.P._lib.dptr(src), n))
         k_fault, rng = fault_plan(n, args.b, args.seed)
         f.run_protected(args.scheme, {k_fault: {"0d": 1}}, rng)
         arm.P.linalg.check(arm.lib.abft_dist_get_matrix(f._ctx, arm.P._lib.dptr(pinned_out), n))

@@ -201,6 +201,8 @@ ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda);
 /* keep a device copy of the local input; abft_dist_reset restores it */
 ABFT_API int abft_dist_keep_input(abft_dist* d, int keep);
 ABFT_API int abft_dist_reset(abft_dist* d);
+/* the rank's own column blocks (n x local_cols, ldl) -> device */
+ABFT_API int abft_dist_set_local(abft_dist* d, const double* local, int64_t ldl);
 /* local columns (n x local_cols) -> host */
 ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo);
 ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf);

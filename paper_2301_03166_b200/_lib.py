@@ -102,6 +102,7 @@ SIGNATURES = [
     ("abft_dist_xbuf_elems", _I64, [_P, _I64]),
     ("abft_dist_set_matrix", _I, [_P, _D, _I64]),
     ("abft_dist_get_matrix", _I, [_P, _D, _I64]),
+    ("abft_dist_set_local", _I, [_P, _D, _I64]),
     ("abft_dist_keep_input", _I, [_P, _I]),
     ("abft_dist_reset", _I, [_P]),
     ("abft_dist_begin", _I, [_P, _I64, _I, _P]),

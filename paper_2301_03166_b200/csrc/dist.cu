@@ -896,6 +896,32 @@ ABFT_API int abft_dist_reset(abft_dist* d) {
   return 0;
 }
 
+// The rank's own column blocks (n x local_cols, ldl), already scattered.
+ABFT_API int abft_dist_set_local(abft_dist* d, const double* local, int64_t ldl) {
+  DevGuardD g(d->device);
+  if (ldl < d->n) {
+    set_last_error("ldl < n");
+    return ABFT_E_INVALID;
+  }
+  if (d->ncl > 0)
+    CUDA_TRY(cudaMemcpy2DAsync(d->m, d->ld * 8, local, ldl * 8, d->n * 8, d->ncl,
+                               cudaMemcpyHostToDevice, d->st));
+  if (d->keep_input) {
+    if (!d->a0) ABFT_TRY(dalloc0(&d->a0, d->ld * std::max<int64_t>(d->ncl, 1), d->st));
+    CUDA_TRY(cudaMemcpyAsync(d->a0, d->m, d->ld * d->ncl * 8, cudaMemcpyDeviceToDevice, d->st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(d->st));
+  d->k_done = 0;
+  d->sums_valid = false;
+  d->qr_count = 0;
+  d->breakdown_col = -1;
+  d->panel_ready = -1;
+  d->comm_pending = false;
+  d->la_buf = nullptr;
+  d->verified_in_update = false;
+  return 0;
+}
+
 ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo) {
   DevGuardD g(d->device);
   if (d->ncl > 0)
