@@ -596,15 +596,17 @@ def run_e2e(arm, args):
         t0 = time.perf_counter()
         P.linalg.check(lib.abft_set_matrix(f._ctx, P._lib.dptr(src), n))
         k_fault, rng = fault_plan(n, args.b, args.seed)
-        P.run_protected(f, args.scheme, {k_fault: {"0d": 1}}, rng)
-        P.linalg.check(lib.abft_get_matrix(f._ctx, P._lib.dptr(pinned_out), n))
+        # the factor streams to the pinned host buffer as column blocks finish
+        P.run_protected(f, args.scheme, {k_fault: {"0d": 1}}, rng, out=pinned_out)
         dt = time.perf_counter() - t0
         if i:
             times.append(dt)
     sec = statistics.median(times)
     return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": 8 * n * n, "d2h_bytes_per_step": 8 * n * n,
-            "ms_per_step": sec * 1e3, "api": "abft_set_matrix + run_protected + abft_get_matrix"}
+            "ms_per_step": sec * 1e3,
+            "api": "abft_set_matrix + run_protected(out=pinned host; finished column blocks "
+                   "stream D2H on a copy stream during the factorization)"}
 
 
 def run_e2e_s(arm, args):

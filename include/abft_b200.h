@@ -148,6 +148,10 @@ ABFT_API int abft_factorize(abft_ctx* ctx, int scheme, const int32_t* schemes,
                             const abft_fault* plan, const int64_t* plan_iter, int nplan,
                             int correct, abft_report* reports, abft_location* locs,
                             int max_locs, int* n_locs);
+/* stream the finished factor to `host` (ldh) during the next abft_factorize
+ * calls: each column block is copied on a copy stream as soon as it is final,
+ * overlapping the rest of the factorization (NULL: off) */
+ABFT_API int abft_stream_out(abft_ctx* ctx, double* host, int64_t ldh);
 /* QR side data: qr_t[k] (w x w) and _qr_vs[k] (nk x w) (linalg.py:294-308) */
 ABFT_API int abft_qr_panels(abft_ctx* ctx);
 /* `del qr_t[n:]` / _qr_vs truncation in _Run._restore (simulator.py:431-435) */

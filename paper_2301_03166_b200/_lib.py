@@ -82,6 +82,7 @@ SIGNATURES = [
     ("abft_factorize", _I, [_P, _I, ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(Fault),
                             ctypes.POINTER(ctypes.c_int64), _I, _I, ctypes.POINTER(Report),
                             ctypes.POINTER(Location), _I, ctypes.POINTER(_I)]),
+    ("abft_stream_out", _I, [_P, _D, _I64]),
     ("abft_qr_panels", _I, [_P]),
     ("abft_set_qr_panels", _I, [_P, _I]),
     ("abft_get_qr_panel", _I, [_P, _I64, _D, _I64, _D, _I64]),

@@ -115,6 +115,12 @@ struct abft_ctx {
   bool chol_enc_ahead = false;    // ... and whose encode ran with it
   int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
   GemmWorkspace gws2;             // split-K workspace of the side stream
+  // streamed result (abft_stream_out): finished column blocks are copied to
+  // this host buffer on a copy stream while the factorization continues
+  double* out_host = nullptr;
+  int64_t out_ld = 0;
+  cudaStream_t st_out = nullptr;
+  cudaEvent_t ev_out = nullptr;
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   // profiling
@@ -199,6 +205,18 @@ void region_of(const abft_ctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
   } else {
     *r0 = p; *c0 = pe; *rows = c->n - p; *cols = c->n - pe;
   }
+}
+
+// Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
+// its device-to-host copy on the copy stream behind the main stream's work.
+int emit_column(abft_ctx* c, int64_t k) {
+  if (!c->out_host) return 0;
+  const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
+  CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p * c->out_ld, c->out_ld * 8, c->m + p * c->ld, c->ld * 8,
+                             c->n * 8, w, cudaMemcpyDeviceToHost, c->st_out));
+  return 0;
 }
 
 // SumOut pointing into the global-grid checksum arrays for a b-aligned region.
@@ -789,6 +807,7 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   prof_mark(c, PROF_PD, true);
   ABFT_TRY(lu_l21(c, k + 1));
   prof_mark(c, PROF_PD, false);
+  ABFT_TRY(emit_column(c, k + 1));
   c->pd_ready = k + 1;
   return 0;
 }
@@ -810,12 +829,14 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
     ABFT_TRY(task_pd(c, k));
     prof_mark(c, PROF_PD, false);
     if (sync_checks) ABFT_TRY(check_info(c));
+    if (c->kind != ABFT_CHOLESKY) ABFT_TRY(emit_column(c, k));
     return 0;
   };
   auto pu = [&]() -> int {
     prof_mark(c, PROF_PU, true);
     ABFT_TRY(task_pu(c, k));
     prof_mark(c, PROF_PU, false);
+    if (c->kind == ABFT_CHOLESKY) ABFT_TRY(emit_column(c, k));
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
@@ -1003,6 +1024,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
@@ -1042,6 +1065,11 @@ ABFT_API int abft_destroy(abft_ctx* c) {
     cudaStreamSynchronize(c->st2);
     cudaStreamDestroy(c->st2);
   }
+  if (c->st_out) {
+    cudaStreamSynchronize(c->st_out);
+    cudaStreamDestroy(c->st_out);
+  }
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
   if (c->e0) cudaEventDestroy(c->e0);
@@ -1212,6 +1240,10 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
       return rc;
     }
   }
+  if (c->out_host) {  // the streamed result is part of the call
+    CUDA_TRY(cudaEventRecord(c->ev_out, c->st_out));
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_out, 0));
+  }
   CUDA_TRY(cudaEventRecord(c->e1, c->st));
   // one synchronisation for the whole factorization
   int brk = check_info(c);
@@ -1263,6 +1295,19 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
   }
   c->k_done = c->nb;
   if (n_locs) *n_locs = total;
+  return 0;
+}
+
+// Stream the finished factor into `host` (column-major, ldh; pinned memory
+// makes the copies asynchronous) during the next abft_factorize calls;
+// NULL turns streaming off. Replaces the abft_get_matrix round trip.
+ABFT_API int abft_stream_out(abft_ctx* c, double* host, int64_t ldh) {
+  if (host && ldh < c->n) {
+    set_last_error("ldh < n");
+    return ABFT_E_INVALID;
+  }
+  c->out_host = host;
+  c->out_ld = ldh;
   return 0;
 }
 

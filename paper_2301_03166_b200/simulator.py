@@ -69,8 +69,9 @@ def run_numeric_iteration(factors: Factorization, k: int, scheme,
 
 def run_protected(factors: Factorization, scheme, fault_schedule: dict | None = None,
                   rng: np.random.Generator | None = None, correct: bool = True,
-                  schemes: list | None = None) -> list:
-    """All remaining iterations in one device call.
+                  schemes: list | None = None, out: np.ndarray | None = None) -> list:
+    """All remaining iterations in one device call (``out``: stream the
+    finished factor into this host array during the call).
 
     ``fault_schedule``: {k: counts} — equivalent to calling
     run_numeric_iteration(factors, k, scheme, fault_schedule.get(k), rng) for
@@ -98,9 +99,19 @@ def run_protected(factors: Factorization, scheme, fault_schedule: dict | None = 
     locs = (_lib.Location * cap)()
     nloc = ctypes.c_int(0)
     factors._dirty()
-    check(factors._lib.abft_factorize(factors._ctx, _lib.SCHEME_CODE[sch.value], sarr, arr, it,
-                                      len(flat), int(bool(correct)), reports, locs, cap,
-                                      ctypes.byref(nloc)))
+    if out is not None:
+        # the finished factor streams into `out` (n x n, Fortran order; pinned
+        # memory overlaps the copies with the factorization)
+        if out.shape != (n, n) or out.dtype != np.float64 or not out.flags.f_contiguous:
+            raise ValueError("out must be an n x n float64 Fortran-ordered array")
+        check(factors._lib.abft_stream_out(factors._ctx, _lib.dptr(out), n))
+    try:
+        check(factors._lib.abft_factorize(factors._ctx, _lib.SCHEME_CODE[sch.value], sarr, arr, it,
+                                          len(flat), int(bool(correct)), reports, locs, cap,
+                                          ctypes.byref(nloc)))
+    finally:
+        if out is not None:
+            factors._lib.abft_stream_out(factors._ctx, None, 0)
     out, pos = [], 0
     for k in range(k0, nb):
         r = reports[k]

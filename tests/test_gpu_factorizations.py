@@ -176,3 +176,16 @@ def test_snapshot_restore_roundtrip():
     np.testing.assert_array_equal(f.m, m0)
     f.run_all()
     assert P.residual(a, f) < 1e-12
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_streamed_result_equals_device_factor(kind):
+    """run_protected(out=...) copies each finished column block to the host
+    during the factorization: the streamed array is the final factor."""
+    n, b, seed = 640, 128, 2
+    a = P.generate_test_matrix(kind, n, seed)
+    f = P.Factorization(kind, a, b)
+    out = np.full((n, n), np.nan, order="F")
+    reps = P.run_protected(f, "full", {2: {P.ErrorKind.D0: 1}}, np.random.default_rng(seed), out=out)
+    np.testing.assert_array_equal(out, f.m)
+    assert any(r.locations for r in reps)
