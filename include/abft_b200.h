@@ -258,6 +258,8 @@ ABFT_API int abft_s_factorize(abft_sctx* ctx, int scheme, const int32_t* schemes
                               int correct, abft_report* reports, abft_location* locs,
                               int max_locs, int* n_locs);
 ABFT_API int abft_s_last_elapsed_ms(abft_sctx* ctx, double* ms);
+/* stream the finished factor to `host` during the next abft_s_factorize calls */
+ABFT_API int abft_s_stream_out(abft_sctx* ctx, float* host, int64_t ldh);
 ABFT_API int abft_s_profile(abft_sctx* ctx, int enable);
 ABFT_API int abft_s_profile_read(abft_sctx* ctx, double* ms);
 ABFT_API int abft_s_residual(abft_sctx* ctx, const float* a0, int64_t lda, double* out);

@@ -117,6 +117,10 @@ struct abft_sctx {
   int32_t* dlist = nullptr;
   int dlist_cap = 0;
   int* info = nullptr;
+  float* out_host = nullptr;  // streamed result (abft_s_stream_out)
+  int64_t out_ld = 0;
+  cudaStream_t st_out = nullptr;
+  cudaEvent_t ev_out = nullptr;
   int64_t el_for = -1;  // iteration whose operand sums E_L / R E_R came out of the
   int64_t er_for = -1;  // PD / PU GEMM epilogues (no separate checksum pass)
   int64_t k_done = 0;
@@ -159,6 +163,18 @@ void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
   } else {
     *r0 = p; *c0 = pe; *rows = c->n - p; *cols = c->n - pe;
   }
+}
+
+// Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
+// its device-to-host copy on the copy stream (as ctx.cu).
+int s_emit_column(abft_sctx* c, int64_t k) {
+  if (!c->out_host) return 0;
+  const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
+  CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p * c->out_ld, c->out_ld * 4, c->m + p * c->ld, c->ld * 4,
+                             c->n * 4, w, cudaMemcpyDeviceToHost, c->st_out));
+  return 0;
 }
 
 SumOut s_sums(abft_sctx* c, int64_t r0, int64_t c0, bool rows_too) {
@@ -701,6 +717,7 @@ int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
   smark(c, SP_PD, true);
   ABFT_TRY(s_lu_l21(c, k + 1));
   smark(c, SP_PD, false);
+  ABFT_TRY(s_emit_column(c, k + 1));
   c->pd_ready = k + 1;
   return 0;
 }
@@ -716,12 +733,14 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     ABFT_TRY(s_pd(c, k));
     smark(c, SP_PD, false);
     if (sync_checks) ABFT_TRY(s_check_info(c));
+    if (c->kind != ABFT_CHOLESKY) ABFT_TRY(s_emit_column(c, k));
     return 0;
   };
   auto pu = [&]() -> int {
     smark(c, SP_PU, true);
     ABFT_TRY(s_pu(c, k));
     smark(c, SP_PU, false);
+    if (c->kind == ABFT_CHOLESKY) ABFT_TRY(s_emit_column(c, k));
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
@@ -894,6 +913,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking);
+  cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
   {
@@ -925,6 +946,11 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
     cudaStreamSynchronize(c->st2);
     cudaStreamDestroy(c->st2);
   }
+  if (c->st_out) {
+    cudaStreamSynchronize(c->st_out);
+    cudaStreamDestroy(c->st_out);
+  }
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
   if (c->e0) cudaEventDestroy(c->e0);
@@ -1056,6 +1082,10 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
       return rc;
     }
   }
+  if (c->out_host) {
+    CUDA_TRY(cudaEventRecord(c->ev_out, c->st_out));
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_out, 0));
+  }
   CUDA_TRY(cudaEventRecord(c->e1, c->st));
   int brk = s_check_info(c);
   if (brk) {
@@ -1066,6 +1096,16 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
   ABFT_TRY(s_collect(c, &evs));
   s_fill(c, evs, k0, reports, locs, max_locs, n_locs);
   c->k_done = c->nb;
+  return 0;
+}
+
+ABFT_API int abft_s_stream_out(abft_sctx* c, float* host, int64_t ldh) {
+  if (host && ldh < c->n) {
+    set_last_error("ldh < n");
+    return ABFT_E_INVALID;
+  }
+  c->out_host = host;
+  c->out_ld = ldh;
   return 0;
 }
 

@@ -98,8 +98,10 @@ class SFactorization:
 
     def run_protected(self, scheme, fault_schedule: dict | None = None,
                       rng: np.random.Generator | None = None, correct: bool = True,
-                      schemes: list | None = None) -> list:
-        """All remaining iterations in one device call (run_protected)."""
+                      schemes: list | None = None, out: np.ndarray | None = None) -> list:
+        """All remaining iterations in one device call (run_protected);
+        ``out`` (n x n float32, Fortran order) receives the finished factor,
+        streamed column block by column block during the call."""
         nb, k0 = self.layout.n_blocks, self.k_done
         flat, iters = [], []
         for k in range(k0, nb):
@@ -119,9 +121,17 @@ class SFactorization:
         cap = 1 << 16
         locs = (_lib.Location * cap)()
         nloc = ctypes.c_int(0)
-        check(self._lib.abft_s_factorize(self._ctx, _lib.SCHEME_CODE[sch.value], sarr, arr, it,
-                                         len(flat), int(bool(correct)), reports, locs, cap,
-                                         ctypes.byref(nloc)))
+        if out is not None:
+            if out.shape != (self.n, self.n) or out.dtype != np.float32 or not out.flags.f_contiguous:
+                raise ValueError("out must be an n x n float32 Fortran-ordered array")
+            check(self._lib.abft_s_stream_out(self._ctx, _lib.fptr(out), self.n))
+        try:
+            check(self._lib.abft_s_factorize(self._ctx, _lib.SCHEME_CODE[sch.value], sarr, arr, it,
+                                             len(flat), int(bool(correct)), reports, locs, cap,
+                                             ctypes.byref(nloc)))
+        finally:
+            if out is not None:
+                self._lib.abft_s_stream_out(self._ctx, None, 0)
         out, pos = [], 0
         for k in range(k0, nb):
             r = reports[k]

@@ -80,3 +80,13 @@ def test_fp32_clean_run_reports_nothing_and_breakdown_raises():
     bad[0, 0] = -1.0
     with pytest.raises(P.NumericBreakdownError):
         P.SFactorization("cholesky", bad, 64).run_protected("none")
+
+
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
+def test_fp32_streamed_result_equals_device_factor(kind):
+    n, b, seed = 640, 128, 4
+    a = P.generate_test_matrix(kind, n, seed)
+    f = P.SFactorization(kind, a, b)
+    out = np.full((n, n), np.nan, dtype=np.float32, order="F")
+    f.run_protected("full", {1: {"0d": 1}}, np.random.default_rng(seed), out=out)
+    np.testing.assert_array_equal(out, f.m)
