@@ -118,3 +118,28 @@ def nccl_single(rank: int, world: int, init_file: str, out: str) -> None:
         json.dump(res, fh, default=str)
     dist.barrier()
     dist.destroy_process_group()
+
+
+def breakdown(rank: int, world: int, init_file: str, out: str) -> None:
+    """A zero pivot in a panel owned by rank 1 surfaces as the reference's
+    NumericBreakdownError on every rank (linalg.py:234-235)."""
+    import torch
+    torch.cuda.set_device(0)
+    dist = _init(rank, world, init_file)
+    import paper_2301_03166_b200 as P
+    from paper_2301_03166_b200.distributed import DistributedFactorization
+    a = P.generate_test_matrix("lu", 256, 0)
+    a[70, 70] = 0.0
+    a[70, :] = 0.0  # row 70 identically zero: the pivot of column 70 (panel 1) is 0
+    f = DistributedFactorization("lu", a, 64)
+    try:
+        f.run_protected("full")
+        res = "no error"
+    except P.NumericBreakdownError as e:
+        res = f"NumericBreakdownError: {e}"
+    except Exception as e:  # noqa: BLE001
+        res = f"{type(e).__name__}: {e}"
+    with open(os.path.join(out, f"brk{rank}.txt"), "w") as fh:
+        fh.write(res)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -85,6 +85,11 @@ CASES = [
      "schedule": {"1": {"0d": 1}}, "world": 2, "reset": True},
     {"name": "qr_b256", "kind": "qr", "n": 768, "b": 256, "scheme": "full", "seed": 11,
      "schedule": {"0": {"0d": 1}}, "world": 2},
+    # ragged last block with b = 256 (fused epilogue) for QR / Cholesky
+    {"name": "qr_rag256", "kind": "qr", "n": 900, "b": 256, "scheme": "full", "seed": 14,
+     "schedule": {"1": {"0d": 1, "1d": 1}}, "world": 2},
+    {"name": "chol_rag256", "kind": "cholesky", "n": 900, "b": 256, "scheme": "full", "seed": 15,
+     "schedule": {"2": {"0d": 1}}, "world": 2},
     # look-ahead off (ABFT_NO_LOOKAHEAD path) must give the same answers
     {"name": "lu_w3_nola", "kind": "lu", "n": 768, "b": 128, "scheme": "full", "seed": 12,
      "schedule": {"2": {"0d": 1}}, "world": 3, "no_lookahead": True},
@@ -146,3 +151,16 @@ def test_nccl_transport_and_lookahead_on_one_rank(tmp_path):
         # distributed form sums its panel products in another order
         assert r["max_diff"] <= (0.0 if kind != "cholesky" else 1e-10), (kind, r)
         assert r["residual"] < 1e-12 and r["residual1"] < 1e-12, (kind, r)
+
+
+def test_breakdown_worker_case_registered():
+    # the GPU breakdown case lives in dist_worker.breakdown (spawned below)
+    from dist_worker import breakdown  # noqa: F401
+
+
+@pytest.mark.gpu
+def test_distributed_breakdown_raises_on_every_rank(tmp_path):
+    from dist_worker import breakdown
+    _spawn(breakdown, 2, str(tmp_path / "init"), str(tmp_path))
+    for r in range(2):
+        assert (tmp_path / f"brk{r}.txt").read_text().startswith("NumericBreakdownError")
