@@ -63,7 +63,47 @@ __global__ void __launch_bounds__(DT, 1)
     for (int c = ty; c < jw; c += DT / 32)
       for (int r = tx; r < rem; r += 32) Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
     __syncthreads();
-    for (int c = 0; c < jw; ++c) {
+    if (mode == 0) {
+      // LU: the sub-panel lives in registers, one row per thread; per pivot
+      // the owner of row c publishes it (double-buffered) and ONE barrier
+      // separates the pivots (the shared-memory form needed three)
+      T a[NBK];
+      const bool own = tid < rem;
+#pragma unroll
+      for (int c = 0; c < NBK; ++c) a[c] = (own && c < jw) ? Ps[c * PLD + tid] : T(0);
+      T* prow = Rs;  // [2][NBK] pivot rows (Rs is free during the panel phase)
+      bool badf = false;
+#pragma unroll
+      for (int c = 0; c < NBK; ++c) {
+        if (c < jw && !badf) {  // uniform across the CTA
+          T* pr = prow + (c & 1) * NBK;
+          if (tid == c) {
+#pragma unroll
+            for (int cc = c; cc < NBK; ++cc) pr[cc] = a[cc];
+          }
+          __syncthreads();
+          const T piv = pr[c];
+          if (piv == T(0) || !isfinite(piv)) {
+            badf = true;
+            if (tid == 0) {
+              s_bad = jb + c + 1;
+              atomicCAS(info, 0, (int)(col_base + jb + c + 1));
+            }
+          } else if (own && tid > c) {
+            const T l = a[c] / piv;
+            a[c] = l;
+#pragma unroll
+            for (int cc = c + 1; cc < NBK; ++cc) a[cc] = fma(-l, pr[cc], a[cc]);
+          }
+        }
+      }
+      if (own && !badf) {
+#pragma unroll
+        for (int c = 0; c < NBK; ++c)
+          if (c < jw) Ps[c * PLD + tid] = a[c];
+      }
+    }
+    for (int c = 0; c < jw && mode != 0; ++c) {
       const T piv = Ps[c * PLD + c];
       const bool bad = (mode == 0) ? (piv == 0.0 || !isfinite(piv)) : (!(piv > 0.0) || !isfinite(piv));
       if (bad) {
