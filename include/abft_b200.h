@@ -258,6 +258,9 @@ ABFT_API int abft_s_factorize(abft_sctx* ctx, int scheme, const int32_t* schemes
                               int correct, abft_report* reports, abft_location* locs,
                               int max_locs, int* n_locs);
 ABFT_API int abft_s_last_elapsed_ms(abft_sctx* ctx, double* ms);
+/* one in-device snapshot slot (the recompute recovery policy) */
+ABFT_API int abft_s_snapshot(abft_sctx* ctx);
+ABFT_API int abft_s_restore(abft_sctx* ctx);
 /* stream the finished factor to `host` during the next abft_s_factorize calls */
 ABFT_API int abft_s_stream_out(abft_sctx* ctx, float* host, int64_t ldh);
 ABFT_API int abft_s_profile(abft_sctx* ctx, int enable);

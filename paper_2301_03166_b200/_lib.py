@@ -134,6 +134,8 @@ SIGNATURES = [
                               ctypes.POINTER(Location), _I, ctypes.POINTER(_I)]),
     ("abft_s_last_elapsed_ms", _I, [_P, _D]),
     ("abft_s_stream_out", _I, [_P, _F, _I64]),
+    ("abft_s_snapshot", _I, [_P]),
+    ("abft_s_restore", _I, [_P]),
     ("abft_s_profile", _I, [_P, _I]),
     ("abft_s_profile_read", _I, [_P, _D]),
     ("abft_s_residual", _I, [_P, _F, _I64, _D]),

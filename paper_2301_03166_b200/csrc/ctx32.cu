@@ -121,6 +121,12 @@ struct abft_sctx {
   int64_t out_ld = 0;
   cudaStream_t st_out = nullptr;
   cudaEvent_t ev_out = nullptr;
+  // device snapshot slot (replaces _Run._snapshot/_restore, simulator.py:420-436)
+  float* snap_m = nullptr;
+  double* snap_rs = nullptr;
+  bool snap_used = false, snap_rs_valid = false;
+  int64_t snap_k = 0;
+  int snap_qr = 0;
   int64_t el_for = -1;  // iteration whose operand sums E_L / R E_R came out of the
   int64_t er_for = -1;  // PD / PU GEMM epilogues (no separate checksum pass)
   int64_t k_done = 0;
@@ -930,7 +936,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
   if (!c) return 0;
   SGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  void* bufs[] = {c->vstore, c->tstore, c->ww, c->mid, c->pan64, c->v64, c->t64, c->gram,
+  void* bufs[] = {c->snap_m, c->snap_rs, c->vstore, c->tstore, c->ww, c->mid, c->pan64, c->v64, c->t64, c->gram,
                   c->betas, c->qr_part, c->qr_rowbuf, c->qr_part2, c->qr_wfin,
                   c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
@@ -1210,5 +1216,44 @@ ABFT_API int abft_s_residual(abft_sctx* c, const float* a0h, int64_t lda, double
 }
 
 ABFT_API int64_t abft_s_breakdown_column(abft_sctx* c) { return c->breakdown_col; }
+
+// One in-device snapshot slot of the working matrix (and Cholesky's running
+// row checksums) for the recompute recovery policy.
+ABFT_API int abft_s_snapshot(abft_sctx* c) {
+  SGuard g(c->device);
+  if (!c->snap_m) ABFT_TRY(salloc(&c->snap_m, c->ld * c->n, c->st));
+  CUDA_TRY(cudaMemcpyAsync(c->snap_m, c->m, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
+  if (c->chol_rs) {
+    if (!c->snap_rs) ABFT_TRY(salloc(&c->snap_rs, c->ld * c->nb, c->st));
+    CUDA_TRY(cudaMemcpyAsync(c->snap_rs, c->chol_rs, c->ld * c->nb * 8, cudaMemcpyDeviceToDevice,
+                             c->st));
+  }
+  c->snap_rs_valid = c->chol_rs_valid;
+  c->snap_k = c->k_done;
+  c->snap_qr = c->qr_count;
+  c->snap_used = true;
+  return 0;
+}
+
+ABFT_API int abft_s_restore(abft_sctx* c) {
+  SGuard g(c->device);
+  if (!c->snap_used) {
+    set_last_error("empty snapshot slot");
+    return ABFT_E_INVALID;
+  }
+  CUDA_TRY(cudaMemcpyAsync(c->m, c->snap_m, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
+  if (c->chol_rs && c->snap_rs)
+    CUDA_TRY(cudaMemcpyAsync(c->chol_rs, c->snap_rs, c->ld * c->nb * 8, cudaMemcpyDeviceToDevice,
+                             c->st));
+  c->chol_rs_valid = c->snap_rs_valid && c->snap_rs != nullptr;
+  c->k_done = c->snap_k;
+  c->qr_count = c->snap_qr;
+  c->sums_valid = false;
+  c->pd_ready = -1;
+  c->el_for = -1;
+  c->er_for = -1;
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  return 0;
+}
 
 }  // extern "C"

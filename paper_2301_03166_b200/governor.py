@@ -387,16 +387,27 @@ class _Energy:
             return None
 
 
+def _is_single(f) -> bool:
+    return f.__class__.__name__ == "SFactorization"
+
+
 def _profile(f) -> list:
     ms = (ctypes.c_double * 4)()
-    check(f._lib.abft_profile_read(f._ctx, ms))
+    read = f._lib.abft_s_profile_read if _is_single(f) else f._lib.abft_profile_read
+    check(read(f._ctx, ms))
     return [ms[i] for i in range(4)]
+
+
+def _profile_enable(f, on: bool) -> None:
+    fn = f._lib.abft_s_profile if _is_single(f) else f._lib.abft_profile
+    check(fn(f._ctx, 1 if on else 0))
 
 
 def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, seed: int = 0,
              rates: ErrorRateTable | None = None, recovery: str = "recompute",
              fc_desired: float = 0.999999, forced_scheme=None, device: int | None = None,
-             cpu: ClockDomain | None = None, gpu: ClockDomain | None = None):
+             cpu: ClockDomain | None = None, gpu: ClockDomain | None = None,
+             precision: str = "f64"):
     """One factorization under a run mode (simulate_run(engine="numeric"),
     simulator.py:440-492) with measured B200 task times. Returns
     (RunSummary, [IterationRecord])."""
@@ -410,7 +421,11 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
     gpu = gpu or update_domain()
     table = rates or default_gpu_rate_table()
     n = a0.shape[0]
-    f = Factorization(kind, a0, b, device=device)
+    if precision == "f32":
+        from .single import SFactorization
+        f = SFactorization(kind, a0, b, device=device)
+    else:
+        f = Factorization(kind, a0, b, device=device)
     nb = f.layout.n_blocks
     coverage = CoverageParams.for_matrix(n, b, fc_desired)
     _, fault_seed = np.random.SeedSequence(seed).spawn(2)   # simulator.py:212-215
@@ -424,7 +439,7 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
     unrecoverable = False
     e0 = energy.mj()
     total_ms = abft_ms = 0.0
-    check(f._lib.abft_profile(f._ctx, 1))
+    _profile_enable(f, True)
     for k in range(nb):
         # -- decide (simulator.py:274-305) --
         if mode == "original":
@@ -459,7 +474,8 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
             t_tmu = (t_gpu_p if t_gpu_p > 0 else 0.0) * gpu.f_base_mhz / dec.f_gpu_mhz
             lam = table.rates(dec.f_gpu_mhz)
             counts = {kk: int(rng_fault.poisson(l * t_tmu)) for kk, l in zip(ErrorKind, lam)}
-            rep = run_numeric_iteration(f, k, scheme, counts, rng_fault)
+            rep = (f.run_numeric_iteration(k, scheme, counts, rng_fault) if _is_single(f)
+                   else run_numeric_iteration(f, k, scheme, counts, rng_fault))
             after = _profile(f)
             d = [x - y for x, y in zip(after, before)]
             total_ms += sum(d)
@@ -497,15 +513,19 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
         records.append(rec)
         if unrecoverable:
             break
-    check(f._lib.abft_profile(f._ctx, 0))
+    _profile_enable(f, False)
     e1 = energy.mj()
-    res = residual(a0, f) if f.complete else float("inf")
+    if not f.complete:
+        res = float("inf")
+    else:
+        res = f.residual(a0) if _is_single(f) else residual(a0, f)
+    tol = 1e-3 if _is_single(f) else 1e-8  # simulator.py:33 (fp64); fp32 restated
     schemes = {}
     for rec in records:
         schemes[rec.abft_mode] = schemes.get(rec.abft_mode, 0) + 1
     summary = RunSummary(mode, r, kind.value, n, b, total_ms, abft_ms,
                          (e1 - e0) / 1e3 if e0 is not None and e1 is not None else None,
-                         res, res <= 1e-8 and not unrecoverable, injected, detected, corrected,
+                         res, res <= tol and not unrecoverable, injected, detected, corrected,
                          unrecoverable, total_retries, schemes)
     return summary, records
 

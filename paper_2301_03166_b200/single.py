@@ -77,6 +77,13 @@ class SFactorization:
         check(self._lib.abft_s_get_matrix(self._ctx, _lib.fptr(out), self.n))
         return out
 
+    def snapshot(self, slot: int = 0) -> None:
+        """Device snapshot (one slot) for the recompute recovery policy."""
+        check(self._lib.abft_s_snapshot(self._ctx))
+
+    def restore(self, slot: int = 0) -> None:
+        check(self._lib.abft_s_restore(self._ctx))
+
     def stream_ptr(self) -> int:
         return int(self._lib.abft_s_stream(self._ctx))
 

@@ -172,3 +172,17 @@ def test_recovery_policies_on_b200():
     assert s_rec.retries > 0 or s_rec.faults_detected == 0
     if not s_rec.unrecoverable:
         assert s_rec.correct
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
+def test_fp32_run_modes_and_campaign(kind):
+    """C5: the s* variants under run modes, with a forced-FULL fault campaign."""
+    import paper_2301_03166_b200 as P
+    a = P.generate_test_matrix(kind, 1024, 4)
+    s, recs = G.run_mode(kind, a, 128, "bsr", r=0.5, seed=4, precision="f32")
+    assert s.correct and len(recs) == 8
+    table = G.ErrorRateTable({"0d": [(100.0, 0.0), (2200.0, 2e4)]})
+    s2, _ = G.run_mode(kind, a, 128, "bsr", r=1.0, seed=4, rates=table, forced_scheme="full",
+                       recovery="recompute", precision="f32")
+    assert sum(s2.faults_injected.values()) > 0 and s2.faults_detected > 0
