@@ -519,7 +519,7 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
         res = float("inf")
     else:
         res = f.residual(a0) if _is_single(f) else residual(a0, f)
-    tol = 1e-3 if _is_single(f) else 1e-8  # simulator.py:33 (fp64); fp32 restated
+    tol = 1e-4 if _is_single(f) else 1e-8  # simulator.py:33 (fp64); fp32 restated (typical 1e-7..2e-5)
     schemes = {}
     for rec in records:
         schemes[rec.abft_mode] = schemes.get(rec.abft_mode, 0) + 1
