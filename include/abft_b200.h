@@ -111,6 +111,14 @@ ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, i
                             int64_t ldb, float beta, const float* C, int64_t ldc, float* D,
                             int64_t ldd);
 
+/* the same with an explicit split-K factor: `splits` K-slices accumulate in
+ * separate tensor-core chains, reduced in a fixed order (the s* Cholesky /
+ * QR deep-K updates use this internally). */
+ABFT_API int abft_dev_sgemm_splitk(void* stream, char transa, char transb, int64_t m, int64_t n,
+                                   int64_t k, float alpha, const float* A, int64_t lda,
+                                   const float* B, int64_t ldb, float beta, const float* C,
+                                   int64_t ldc, float* D, int64_t ldd, int splits);
+
 /* factorization context: replaces Factorization (linalg.py:159-359) -------- */
 typedef struct abft_ctx abft_ctx;
 

@@ -66,6 +66,9 @@ SIGNATURES = [
                             _P, _I64, _P, _I64, ctypes.c_double, _P, _I64, _P, _I64]),
     ("abft_dev_sgemm", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, ctypes.c_float,
                             _P, _I64, _P, _I64, ctypes.c_float, _P, _I64, _P, _I64]),
+    ("abft_dev_sgemm_splitk", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64,
+                                   ctypes.c_float, _P, _I64, _P, _I64, ctypes.c_float, _P, _I64,
+                                   _P, _I64, _I]),
     ("abft_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
     ("abft_destroy", _I, [_P]),
     ("abft_set_matrix", _I, [_P, _D, _I64]),

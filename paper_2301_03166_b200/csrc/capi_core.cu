@@ -87,21 +87,29 @@ ABFT_API int abft_dev_dgemm(void* stream, char transa, char transb, int64_t m, i
 }
 
 // fp32 device-pointer GEMM on tcgen05 (3xTF32): D = beta*C + alpha*op(A)*op(B)
-ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, int64_t n, int64_t k,
-                            float alpha, const float* A, int64_t lda, const float* B, int64_t ldb,
-                            float beta, const float* C, int64_t ldc, float* D, int64_t ldd) {
-  if (m < 0 || n < 0 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
+ABFT_API int abft_dev_sgemm_splitk(void* stream, char transa, char transb, int64_t m, int64_t n,
+                                   int64_t k, float alpha, const float* A, int64_t lda,
+                                   const float* B, int64_t ldb, float beta, const float* C,
+                                   int64_t ldc, float* D, int64_t ldd, int splits) {
+  if (m < 0 || n < 0 || k < 1 || m > INT32_MAX || n > INT32_MAX || k > INT32_MAX || splits < 1) {
     set_last_error("abft_dev_sgemm: bad dimensions");
     return ABFT_E_INVALID;
   }
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  const int64_t wse = sgemm_workspace_elems((int)m, (int)n, (int)k);
+  const int64_t wse = sgemm_workspace_elems((int)m, (int)n, (int)k, splits);
   float* ws = nullptr;
   CUDA_TRY(cudaMallocAsync(&ws, wse * sizeof(float), st));
   int rc = sgemm_tc(st, transa, transb, (int)m, (int)n, (int)k, alpha, A, lda, B, ldb, beta, C, ldc,
-                    D, ldd, ws, wse);
+                    D, ldd, ws, wse, nullptr, 0, splits);
   cudaFreeAsync(ws, st);
   return rc;
+}
+
+ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, int64_t n, int64_t k,
+                            float alpha, const float* A, int64_t lda, const float* B, int64_t ldb,
+                            float beta, const float* C, int64_t ldc, float* D, int64_t ldd) {
+  return abft_dev_sgemm_splitk(stream, transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
+                               D, ldd, 1);
 }
 
 }  // extern "C"

@@ -105,6 +105,13 @@ struct abft_sctx {
   float* uinv = nullptr;
   float* sws = nullptr;   // sgemm split-operand workspace
   int64_t sws_elems = 0;
+  int sms = 148;
+  // Cholesky: finished L columns kept pre-split for the tensor cores
+  // (lsh/lsl[r * ldk + c] = hi/lo of L(r, c)), written once per panel, so
+  // the left-looking update reads both operands with no per-iteration split
+  float* lsh = nullptr;
+  float* lsl = nullptr;
+  int64_t ldk = 0;
   double* scratch = nullptr;
   GemmWorkspace gws;
   Event* ev = nullptr;
@@ -212,18 +219,47 @@ constexpr int64_t S_KCHUNK = 512;
 // residual 2.4e-7 at N = 16384)
 constexpr int64_t S_KCHUNK_CHOL = 2048;
 
+// Split-K plan of one s_gemm. Narrow outputs with deep K (Cholesky's
+// left-looking panel update, QR's V^T C: fewer tiles than SMs) run as one
+// split-K launch -- at least ceil(K / kchunk) slices for the chain-depth
+// bound, more for parallelism (up to two units per SM). Wide outputs, and
+// GEMMs whose epilogue produces the checksums, run the K chunks as
+// sequential launches accumulating through beta = 1 (no partial buffers).
+void s_gemm_plan(int sms, int64_t M, int64_t N, int64_t K, int64_t kchunk, bool fused, int* splits,
+                 int64_t* need) {
+  const int64_t tiles = ((M + 127) / 128) * ((N + 127) / 128);
+  int64_t S = (K + kchunk - 1) / kchunk;
+  if (fused || tiles >= sms) {
+    *splits = 1;
+    *need = sgemm_workspace_elems((int)M, (int)N, (int)std::min(K, kchunk), 1);
+    return;
+  }
+  if (tiles < sms && K >= 512)
+    S = std::max<int64_t>(S, std::min<int64_t>((2 * sms + tiles - 1) / tiles, K / 256));
+  S = std::min<int64_t>(S, (K + 31) / 32);
+  *splits = (int)std::max<int64_t>(S, 1);
+  *need = sgemm_workspace_elems((int)M, (int)N, (int)K, *splits);
+}
+
 int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, float alpha,
            const float* A, int64_t lda, const float* B, int64_t ldb, float beta, const float* C,
            int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr, int max_ctas = 0,
            int64_t kchunk = S_KCHUNK) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
-  const int64_t kc = std::min(K, kchunk);
-  const int64_t need = sgemm_workspace_elems((int)M, (int)N, (int)kc);
+  int splits;
+  int64_t need;
+  s_gemm_plan(max_ctas > 0 ? std::min(max_ctas, c->sms) : c->sms, M, N, K, kchunk, fs != nullptr,
+              &splits, &need);
   if (need > c->sws_elems) {
-    if (c->sws) cudaFreeAsync(c->sws, c->st);
-    c->sws_elems = need;
-    CUDA_TRY(cudaMallocAsync(&c->sws, need * sizeof(float), c->st));
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    if (c->sws) cudaFree(c->sws);
+    c->sws = nullptr;
+    c->sws_elems = need + need / 4;
+    CUDA_TRY(cudaMalloc(&c->sws, c->sws_elems * sizeof(float)));
   }
+  if (splits > 1 || K <= kchunk)
+    return sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)K, alpha, A, lda, B, ldb, beta, C, ldc, D,
+                    ldd, c->sws, c->sws_elems, fs, max_ctas, splits);
   const bool AT = (ta == 'T' || ta == 't'), BT = (tb == 'T' || tb == 't');
   for (int64_t k0 = 0; k0 < K; k0 += kchunk) {
     const int64_t kl = std::min(kchunk, K - k0);
@@ -233,6 +269,40 @@ int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, floa
     ABFT_TRY(sgemm_tc(c->st, ta, tb, (int)M, (int)N, (int)kl, alpha, Ak, lda, Bk, ldb,
                       first ? beta : 1.0f, first ? C : D, first ? ldc : ldd, D, ldd, c->sws,
                       c->sws_elems, last ? fs : nullptr, max_ctas));
+  }
+  return 0;
+}
+
+// Cholesky left-looking panel update P(p:n, p:pe) -= L(p:n, 0:p) L(p:pe, 0:p)^T
+// from the cached operand splits (split-K, one launch + reduction).
+int s_chol_update(abft_sctx* c, int64_t k, int max_ctas) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (p == 0) return 0;
+  int splits;
+  int64_t need;
+  s_gemm_plan(max_ctas > 0 ? std::min(max_ctas, c->sms) : c->sms, n - p, w, p, S_KCHUNK_CHOL, false,
+              &splits, &need);
+  need = sgemm_partial_elems((int)(n - p), (int)w, splits) + 128;
+  if (need > c->sws_elems) {
+    CUDA_TRY(cudaStreamSynchronize(c->st));
+    if (c->sws) cudaFree(c->sws);
+    c->sws = nullptr;
+    c->sws_elems = need;
+    CUDA_TRY(cudaMalloc(&c->sws, c->sws_elems * sizeof(float)));
+  }
+  float* P = c->m + p + p * c->ld;
+  const float* ah = c->lsh + p * c->ldk;
+  const float* al = c->lsl + p * c->ldk;
+  if (splits > 1)
+    return sgemm_tc_presplit(c->st, (int)(n - p), (int)w, (int)p, -1.0f, ah, al, c->ldk, ah, al,
+                             c->ldk, 1.0f, P, c->ld, P, c->ld, c->sws, c->sws_elems, max_ctas, splits);
+  // wide enough for the SMs: the chain-depth bound runs as sequential
+  // K chunks accumulating through beta = 1
+  for (int64_t k0 = 0; k0 < p; k0 += S_KCHUNK_CHOL) {
+    const int64_t kl = std::min<int64_t>(S_KCHUNK_CHOL, p - k0);
+    ABFT_TRY(sgemm_tc_presplit(c->st, (int)(n - p), (int)w, (int)kl, -1.0f, ah + k0, al + k0, c->ldk,
+                               ah + k0, al + k0, c->ldk, 1.0f, P, c->ld, P, c->ld, nullptr, 0, max_ctas,
+                               1));
   }
   return 0;
 }
@@ -344,6 +414,9 @@ int s_pu(abft_sctx* c, int64_t k) {
       ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, A21, c->ld, n - pe, w));
       ABFT_TRY(fill_matrix(c->st, c->m + p + pe * c->ld, c->ld, w, n - pe, 0.0));
     }
+    // panel k is final: keep its hi/lo split for the later panel updates
+    if (c->lsh) ABFT_TRY(sgemm_split_operand(c->st, c->m + p + p * c->ld, c->ld, (int)(n - p), (int)w, (int)w, 0,
+                                 c->lsh + p * c->ldk + p, c->lsl + p * c->ldk + p, c->ldk));
     // block-row sums of the finished panel: operand sums of later maintenance
     RegionF reg{c->m + p + p * c->ld, c->ld, n - p, w, c->b};
     SumOut o = s_sums(c, p, p, false);
@@ -579,9 +652,7 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
       fused = fuse;
     }
   } else if (k > 0) {
-    float* P = c->m + p + p * c->ld;
-    ABFT_TRY(s_gemm(c, 'N', 'T', n - p, w, p, -1.0f, c->m + p, c->ld, c->m + p, c->ld, 1.0f, P, c->ld,
-                    P, c->ld, nullptr, 0, S_KCHUNK_CHOL));
+    ABFT_TRY(s_chol_update(c, k, 0));
   }
   smark(c, SP_TMU, false);
   smark(c, SP_ABFT, true);
@@ -906,8 +977,28 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   if ((rc = salloc(&c->scratch, 4096, c->st))) return fail(rc);
   c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
   if ((rc = salloc(&c->gws.ptr, c->gws.elems, c->st))) return fail(rc);
+  // split-operand workspace sized once for the deepest s_gemm of the kind
+  // (regrowing inside the per-iteration path costs allocator round trips)
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
   c->sws_elems = sgemm_workspace_elems((int)n, (int)n, (int)b);
+  for (int64_t k = 0; k < c->nb; ++k) {  // the deep-K GEMMs of the kind
+    const int64_t p = k * b, pe = std::min(p + b, n);
+    int sp;
+    int64_t need = 0;
+    if (kind == ABFT_CHOLESKY && k > 0) {  // pre-split operands: partials only
+      s_gemm_plan(c->sms, n - p, pe - p, p, S_KCHUNK_CHOL, false, &sp, &need);
+      need = sgemm_partial_elems((int)(n - p), (int)(pe - p), sp) + 128;
+    }
+    else if (kind == ABFT_QR && pe < n)
+      s_gemm_plan(c->sms, pe - p, n - pe, n - p, S_KCHUNK, false, &sp, &need);
+    c->sws_elems = std::max(c->sws_elems, need);
+  }
   if ((rc = salloc(&c->sws, c->sws_elems, c->st))) return fail(rc);
+  if (kind == ABFT_CHOLESKY) {
+    c->ldk = (n + 3) / 4 * 4;
+    if ((rc = salloc(&c->lsh, c->ldk * n, c->st))) return fail(rc);
+    if ((rc = salloc(&c->lsl, c->ldk * n, c->st))) return fail(rc);
+  }
   c->ev_cap = 1 << 16;
   if (cudaMalloc(&c->ev, c->ev_cap * sizeof(Event)) != cudaSuccess) return fail(-1000);
   if (cudaMalloc(&c->counters, 4 * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
@@ -940,7 +1031,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
                   c->betas, c->qr_part, c->qr_rowbuf, c->qr_part2, c->qr_wfin,
                   c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
-                  c->uinv, c->sws, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
+                  c->uinv, c->sws, c->lsh, c->lsl, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
                   c->dplan, c->dlist, c->info};
   for (void* p : bufs)
     if (p) cudaFree(p);

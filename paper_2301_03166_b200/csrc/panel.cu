@@ -63,15 +63,20 @@ __global__ void __launch_bounds__(DT, 1)
     for (int c = ty; c < jw; c += DT / 32)
       for (int r = tx; r < rem; r += 32) Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
     __syncthreads();
-    if (mode == 0) {
-      // LU: the sub-panel lives in registers, one row per thread; per pivot
-      // the owner of row c publishes it (double-buffered) and ONE barrier
-      // separates the pivots (the shared-memory form needed three)
+    {
+      // The sub-panel lives in registers, one row per thread; per pivot the
+      // owner of row c publishes it (double-buffered) and ONE barrier
+      // separates the pivots (the shared-memory form needed three).
+      // Cholesky runs the same elimination: its sub-panel's diagonal part is
+      // kept symmetric (the trailing updates below write both triangles), so
+      // pivot row c equals column c and the unpivoted LU multipliers give
+      // L(r, c) = l(r, c) * sqrt(piv_c), L(c, c) = sqrt(piv_c).
       T a[NBK];
       const bool own = tid < rem;
 #pragma unroll
       for (int c = 0; c < NBK; ++c) a[c] = (own && c < jw) ? Ps[c * PLD + tid] : T(0);
-      T* prow = Rs;  // [2][NBK] pivot rows (Rs is free during the panel phase)
+      T* prow = Rs;            // [2][NBK] pivot rows (Rs is free during the panel phase)
+      T* dsq = Rs + 2 * NBK;   // [NBK] sqrt of the Cholesky pivots
       bool badf = false;
 #pragma unroll
       for (int c = 0; c < NBK; ++c) {
@@ -80,10 +85,12 @@ __global__ void __launch_bounds__(DT, 1)
           if (tid == c) {
 #pragma unroll
             for (int cc = c; cc < NBK; ++cc) pr[cc] = a[cc];
+            if (mode == 1) dsq[c] = sqrt(a[c]);
           }
           __syncthreads();
           const T piv = pr[c];
-          if (piv == T(0) || !isfinite(piv)) {
+          const bool bad = mode == 0 ? (piv == T(0) || !isfinite(piv)) : (!(piv > T(0)) || !isfinite(piv));
+          if (bad) {
             badf = true;
             if (tid == 0) {
               s_bad = jb + c + 1;
@@ -97,40 +104,16 @@ __global__ void __launch_bounds__(DT, 1)
           }
         }
       }
+      __syncthreads();
       if (own && !badf) {
 #pragma unroll
         for (int c = 0; c < NBK; ++c)
-          if (c < jw) Ps[c * PLD + tid] = a[c];
+          if (c < jw) {
+            T v = a[c];
+            if (mode == 1) v = tid > c ? v * dsq[c] : (tid == c ? dsq[c] : T(0));
+            Ps[c * PLD + tid] = v;
+          }
       }
-    }
-    for (int c = 0; c < jw && mode != 0; ++c) {
-      const T piv = Ps[c * PLD + c];
-      const bool bad = (mode == 0) ? (piv == 0.0 || !isfinite(piv)) : (!(piv > 0.0) || !isfinite(piv));
-      if (bad) {
-        if (tid == 0) {
-          s_bad = jb + c + 1;
-          atomicCAS(info, 0, (int)(col_base + jb + c + 1));
-        }
-        break;  // uniform: every thread saw the same pivot
-      }
-      __syncthreads();
-      if (mode == 0) {
-        for (int r = c + 1 + tid; r < rem; r += DT) Ps[c * PLD + r] /= piv;
-        __syncthreads();
-        for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
-          const T u = Ps[cc * PLD + c];
-          for (int r = c + 1 + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
-        }
-      } else {
-        const T d = sqrt(piv);
-        for (int r = c + tid; r < rem; r += DT) Ps[c * PLD + r] = (r == c) ? d : Ps[c * PLD + r] / d;
-        __syncthreads();
-        for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
-          const T u = Ps[c * PLD + cc];
-          for (int r = cc + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
-        }
-      }
-      __syncthreads();
     }
     __syncthreads();
     if (s_bad) return;
@@ -189,9 +172,10 @@ __global__ void __launch_bounds__(DT, 1)
       for (int i = 0; i < 7; ++i) {
         const int r = tx + 32 * i;
         if (r >= nr) continue;
-        if (mode == 0 || r >= c0) D[(jb + jw + r) + (int64_t)(jb + jw + c0) * ld] -= acc[i][0];
-        if (c1ok && (mode == 0 || r >= c0 + 1))
-          D[(jb + jw + r) + (int64_t)(jb + jw + c0 + 1) * ld] -= acc[i][1];
+        // both triangles (Cholesky too: the next sub-panel's elimination
+        // reads its diagonal part as a symmetric block)
+        D[(jb + jw + r) + (int64_t)(jb + jw + c0) * ld] -= acc[i][0];
+        if (c1ok) D[(jb + jw + r) + (int64_t)(jb + jw + c0 + 1) * ld] -= acc[i][1];
       }
     }
     __syncthreads();

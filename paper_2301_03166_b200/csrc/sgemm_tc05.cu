@@ -65,6 +65,11 @@ struct SParams {
   float alpha, beta;
   int fuse;
   int prefetch_c;  // 1: TMA-prefetch each tile's C box into L2 ahead of its epilogue
+  // split-K: unit u = (tile u % tiles, split u / tiles) runs k-blocks
+  // [split * kbs, min(nkb, (split + 1) * kbs)) and writes alpha * acc to
+  // D + split * dstride (a partial; beta = 0, no fused sums)
+  int splits, kbs;
+  int64_t dstride;
   FusedSums sums;
 };
 
@@ -136,6 +141,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   float* parts = reinterpret_cast<float*>(smem + T_COL_OFF);   // [2 parities][T_PART_FLOATS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tiles = p.tiles_m * p.tiles_n;
+  const int units = tiles * p.splits;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < TSTAGES; ++s) {
@@ -168,12 +174,14 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       tma_prefetch_desc(&mBh);
       tma_prefetch_desc(&mBl);
       uint32_t q = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const int tt = t % tiles, sp = t / tiles;
+        const int tm = tt % p.tiles_m, tn = tt / p.tiles_m;
+        const int kb0 = sp * p.kbs, kb1 = min(p.nkb, kb0 + p.kbs);
         // the epilogue of this tile reads C long after its operands stream in:
         // pull the C box into L2 now so those loads do not pay DRAM latency
         if (p.prefetch_c) tma_prefetch_l2_2d(&mC, tm * TBM, tn * TBN);
-        for (int kb = 0; kb < p.nkb; ++kb, ++q) {
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
           const int s = q % TSTAGES;
           if (q >= TSTAGES) mbar_wait(&empty[s], ((q / TSTAGES) - 1) & 1);
           uint8_t* st = smem + s * T_STAGE_BYTES;
@@ -189,12 +197,13 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     // ===== MMA issuer =====
     uint32_t q = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int t = blockIdx.x; t < units; t += gridDim.x, ++it) {
       const int acc = it & 1, use = it >> 1;
+      const int kb0 = (t / tiles) * p.kbs, kb1 = min(p.nkb, kb0 + p.kbs);
       if (use >= 1) mbar_wait(&tempty[acc], (use - 1) & 1);
       tc_fence_after();
       const uint32_t dt = tmem_base + (uint32_t)(acc * TBN);
-      for (int kb = 0; kb < p.nkb; ++kb, ++q) {
+      for (int kb = kb0; kb < kb1; ++kb, ++q) {
         const int s = q % TSTAGES;
         mbar_wait(&full[s], (q / TSTAGES) & 1);
         tc_fence_after();
@@ -206,7 +215,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
             const uint64_t ah = sdesc(st + off), al = sdesc(st + T_A_BYTES + off);
             const uint64_t bh = sdesc(st + 2 * T_A_BYTES + off);
             const uint64_t bl = sdesc(st + 2 * T_A_BYTES + T_B_BYTES + off);
-            mma_tf32(dt, al, bh, (kb | ks) ? 1u : 0u);
+            mma_tf32(dt, al, bh, (kb > kb0 || ks) ? 1u : 0u);
             mma_tf32(dt, ah, bl, 1u);
             mma_tf32(dt, ah, bh, 1u);
           }
@@ -227,14 +236,14 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     const int etid = threadIdx.x - 64;          // 0..255
     // kernel parameters hoisted into registers once
     const float* Cg = p.C;  // may alias D (in-place update): every element is read before it is written
-    float* Dg = p.D;
     const int64_t ldc = p.ldc, ldd = p.ldd;
     const float alpha = p.alpha, beta = p.beta;
     const int M = p.M, N = p.N;
     const bool use_c = beta != 0.0f, fuse = p.fuse != 0;
     constexpr int HN = TBN / 2;  // columns per warp
     float cv[HN];
-    auto load_c = [&](int tt, float* dst) {
+    auto load_c = [&](int tu, float* dst) {
+      const int tt = tu % tiles;
       const int tm2 = tt % p.tiles_m, tn2 = tt / p.tiles_m;
       const int m2 = tm2 * TBM + row_t;
       const int cb2 = tn2 * TBN + half * HN;
@@ -250,9 +259,11 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       }
     };
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int t = blockIdx.x; t < units; t += gridDim.x, ++it) {
       const int acc = it & 1, use = it >> 1;
-      const int tm = t % p.tiles_m, tn = t / p.tiles_m;
+      const int tt = t % tiles;
+      const int tm = tt % p.tiles_m, tn = tt / p.tiles_m;
+
       const int m = tm * TBM + row_t;
       const bool rv = m < M;
       const int c_base = tn * TBN + half * HN;
@@ -267,7 +278,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       // in-tile sums in fp32 (<= 128 terms: error <= ~128 eps32 max|x|, 50x
       // below tau32), converted to fp64 once per published checksum
       float rsum = 0.0f, mx = 0.0f;
-      float* drow = Dg + m + (int64_t)c_base * ldd;
+      float* drow = p.D + (p.dstride ? (int64_t)(t / tiles) * p.dstride : 0) + m + (int64_t)c_base * ldd;
 #pragma unroll
       for (int cc = 0; cc < HN / 32; ++cc) {
         float v[32];
@@ -324,7 +335,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       // next tile's C loads go out now; their latency hides behind the
       // cross-warp combine below and the next accumulator wait
-      if (t + (int)gridDim.x < tiles) load_c(t + gridDim.x, cv);
+      if (t + (int)gridDim.x < units) load_c(t + gridDim.x, cv);
       if (fuse) {
         const FusedSums& fs = p.sums;
         float* pp = parts + acc * T_PART_FLOATS;
@@ -376,8 +387,10 @@ __global__ void __launch_bounds__(T_THREADS, 1)
 // trans = 0: src is (R x K) column-major (element (r, k) at r + k * lds),
 //            transposed through a 32 x 33 shared tile;
 // trans = 1: src already holds (r, k) at k + r * lds (a plain copy).
-__global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, int R, int K, int trans,
-                                  float* __restrict__ hi, float* __restrict__ lo, int64_t ldo) {
+// Columns K..kpad-1 are written as zeros.
+__global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, int R, int K, int kpad,
+                                  int trans, float* __restrict__ hi, float* __restrict__ lo,
+                                  int64_t ldo) {
   __shared__ float tile[32][33];
   const int k0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
@@ -389,7 +402,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, in
     __syncthreads();
     for (int i = ty; i < 32; i += 8) {
       const int r = r0 + i, k = k0 + tx;
-      if (r < R && k < ldo) {
+      if (r < R && k < kpad) {
         const float x = (k < K) ? tile[tx][i] : 0.0f;
         uint32_t h;
         asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
@@ -401,7 +414,7 @@ __global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, in
   } else {
     for (int i = ty; i < 32; i += 8) {
       const int r = r0 + i, k = k0 + tx;
-      if (r < R && k < ldo) {
+      if (r < R && k < kpad) {
         const float x = (k < K) ? src[k + (int64_t)r * lds] : 0.0f;
         uint32_t h;
         asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(h) : "f"(x));
@@ -410,6 +423,21 @@ __global__ void tf32_split_kernel(const float* __restrict__ src, int64_t lds, in
         lo[(int64_t)r * ldo + k] = x - hf;
       }
     }
+  }
+}
+
+// split-K reduction: D = beta*C + sum_s P_s (fixed order, column-major M x N,
+// partials at ldp = M). C may alias D.
+__global__ void splitk_reduce_f32(int M, int N, int S, const float* __restrict__ P, int64_t pstride,
+                                  float beta, const float* C, int64_t ldc, float* D, int64_t ldd) {
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = e / M, i = e - j * M;
+    float acc = 0.0f;
+    for (int s2 = 0; s2 < S; ++s2) acc += __ldg(P + s2 * pstride + e);
+    if (beta != 0.0f) acc = fmaf(beta, C[i + j * ldc], acc);
+    D[i + j * ldd] = acc;
   }
 }
 
@@ -428,13 +456,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 // 2-D map over a K-major fp32 array (rows x ldk, K contiguous), box 32 x 128, 128B swizzle.
-int kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ldk) {
+int kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t K, int64_t ldk) {
   auto fn = encode_fn();
   if (!fn) {
     set_last_error("cuTensorMapEncodeTiled unavailable");
     return -20;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)ldk, (cuuint64_t)(rows < 1 ? 1 : rows)};
+  // K extent = the operand's own K (columns past it are zero-filled by TMA)
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)(rows < 1 ? 1 : rows)};
   cuuint64_t strides[1] = {(cuuint64_t)(ldk * 4)};
   cuuint32_t box[2] = {TBK, 128};
   cuuint32_t estr[2] = {1, 1};
@@ -451,57 +480,43 @@ int kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t ldk) {
 
 }  // namespace
 
-int64_t sgemm_workspace_elems(int M, int N, int K) {
+int64_t sgemm_workspace_elems(int M, int N, int K, int splits) {
   const int64_t ldk = (K + 3) / 4 * 4;
-  return 2 * ((int64_t)M + N) * ldk + 64;
+  return 2 * ((int64_t)M + N) * ldk + 64 + sgemm_partial_elems(M, N, splits);
 }
 
-int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha, const float* A,
-             int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
-             float* D, int64_t ldd, float* ws, int64_t ws_elems, const FusedSums* fs, int max_ctas) {
-  if (M <= 0 || N <= 0) return 0;
-  if (K <= 0) {
-    set_last_error("sgemm_tc needs K > 0");
-    return -1;
-  }
-  const int64_t ldk = (K + 3) / 4 * 4;
-  if (!ws || ws_elems < sgemm_workspace_elems(M, N, K)) {
-    set_last_error("sgemm_tc workspace too small");
-    return -1;
-  }
-  // 256-byte aligned operand copies inside the workspace
-  auto align = [](float* q) {
-    return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q) + 255) & ~uintptr_t(255));
-  };
-  float* ah = align(ws);
-  float* al = align(ah + (int64_t)M * ldk);
-  float* bh = align(al + (int64_t)M * ldk);
-  float* bl = align(bh + (int64_t)N * ldk);
-  if (bl + (int64_t)N * ldk > ws + ws_elems) {
-    set_last_error("sgemm_tc workspace too small (alignment)");
-    return -1;
-  }
-  // A: op(A) is M x K. 'N': (m, k) at m + k*lda -> transpose; 'T': (m, k) at k + m*lda -> copy.
-  const bool AT = (ta == 'T' || ta == 't');
-  const bool BT = (tb == 'T' || tb == 't');
-  {
-    dim3 g((unsigned)((ldk + 31) / 32), (unsigned)((M + 31) / 32));
-    count_launch();
-    tf32_split_kernel<<<g, 256, 0, st>>>(A, lda, M, K, AT ? 1 : 0, ah, al, ldk);
-  }
-  {
-    // op(B) is K x N; B' row n = column n of op(B): 'N': (k, n) at k + n*ldb -> copy;
-    // 'T': (k, n) at n + k*ldb -> transpose.
-    dim3 g((unsigned)((ldk + 31) / 32), (unsigned)((N + 31) / 32));
-    count_launch();
-    tf32_split_kernel<<<g, 256, 0, st>>>(B, ldb, N, K, BT ? 0 : 1, bh, bl, ldk);
-  }
+int64_t sgemm_partial_elems(int M, int N, int splits) {
+  return splits > 1 ? (int64_t)splits * M * N + 64 : 0;
+}
+
+int sgemm_split_operand(cudaStream_t st, const float* src, int64_t lds, int R, int K, int kpad,
+                        int trans, float* hi, float* lo, int64_t ldo) {
+  if (R <= 0 || K <= 0) return 0;
+  if (kpad < K) kpad = K;
+  dim3 g((unsigned)((kpad + 31) / 32), (unsigned)((R + 31) / 32));
+  count_launch();
+  tf32_split_kernel<<<g, 256, 0, st>>>(src, lds, R, K, kpad, trans, hi, lo, ldo);
   CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
+namespace {
+
+float* align256(float* q) {
+  return reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(q) + 255) & ~uintptr_t(255));
+}
+
+// the tcgen05 launch over K-major split operands (A' row m = row m of op(A),
+// B' row n = column n of op(B), both ld elements apart, K contiguous)
+int launch_tc(cudaStream_t st, int M, int N, int K, float alpha, const float* ah, const float* al,
+              int64_t lda_k, const float* bh, const float* bl, int64_t ldb_k, float beta, const float* C,
+              int64_t ldc, float* D, int64_t ldd, float* part, int64_t part_elems, const FusedSums* fs,
+              int max_ctas, int splits) {
   CUtensorMap mah, mal, mbh, mbl;
-  ABFT_TRY(kmajor_map(&mah, ah, M, ldk));
-  ABFT_TRY(kmajor_map(&mal, al, M, ldk));
-  ABFT_TRY(kmajor_map(&mbh, bh, N, ldk));
-  ABFT_TRY(kmajor_map(&mbl, bl, N, ldk));
+  ABFT_TRY(kmajor_map(&mah, ah, M, K, lda_k));
+  ABFT_TRY(kmajor_map(&mal, al, M, K, lda_k));
+  ABFT_TRY(kmajor_map(&mbh, bh, N, K, ldb_k));
+  ABFT_TRY(kmajor_map(&mbl, bl, N, K, ldb_k));
   SParams p;
   p.M = M;
   p.N = N;
@@ -509,30 +524,56 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   p.tiles_m = (M + TBM - 1) / TBM;
   p.tiles_n = (N + TBN - 1) / TBN;
   p.nkb = (K + TBK - 1) / TBK;
-  p.C = C;
-  p.ldc = ldc;
-  p.D = D;
-  p.ldd = ldd;
+  if (splits > p.nkb) splits = p.nkb;
+  if (splits < 1) splits = 1;
+  p.kbs = (p.nkb + splits - 1) / splits;
+  splits = (p.nkb + p.kbs - 1) / p.kbs;  // no empty splits
+  p.splits = splits;
   p.alpha = alpha;
-  p.beta = (C == nullptr) ? 0.0f : beta;
-  p.fuse = fs ? 1 : 0;
-  if (fs) p.sums = *fs;
+  p.fuse = 0;
+  p.prefetch_c = 0;
   CUtensorMap mc;
   memset(&mc, 0, sizeof(mc));
-  p.prefetch_c = 0;
-  // only worth a descriptor when CTAs run several tiles (the prefetch for
-  // tile i+1 overlaps tile i); tiny launches stay host-cheap
-  if (p.beta != 0.0f && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc % 4) == 0 &&
-      (int64_t)p.tiles_m * p.tiles_n > 148) {
-    auto fn = encode_fn();
-    cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
-    cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
-    cuuint32_t box[2] = {TBM, TBN};
-    cuuint32_t estr[2] = {1, 1};
-    if (fn && fn(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(C), dims, strides, box,
-                 estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-      p.prefetch_c = 1;
+  float* pbase = nullptr;
+  if (splits > 1) {
+    if (fs) {
+      set_last_error("sgemm_tc: fused sums need splits == 1");
+      return -1;
+    }
+    pbase = align256(part);
+    if (!part || pbase + (int64_t)splits * M * N > part + part_elems) {
+      set_last_error("sgemm_tc: split-K partial workspace too small");
+      return -1;
+    }
+    p.C = nullptr;
+    p.ldc = M;
+    p.D = pbase;
+    p.ldd = M;
+    p.beta = 0.0f;
+    p.dstride = (int64_t)M * N;
+  } else {
+    p.C = C;
+    p.ldc = ldc;
+    p.D = D;
+    p.ldd = ldd;
+    p.beta = (C == nullptr) ? 0.0f : beta;
+    p.dstride = 0;
+    p.fuse = fs ? 1 : 0;
+    if (fs) p.sums = *fs;
+    // only worth a descriptor when CTAs run several tiles (the prefetch for
+    // tile i+1 overlaps tile i); tiny launches stay host-cheap
+    if (p.beta != 0.0f && (reinterpret_cast<uintptr_t>(C) & 15) == 0 && (ldc % 4) == 0 &&
+        (int64_t)p.tiles_m * p.tiles_n > 148) {
+      auto fn = encode_fn();
+      cuuint64_t dims[2] = {(cuuint64_t)M, (cuuint64_t)N};
+      cuuint64_t strides[1] = {(cuuint64_t)(ldc * 4)};
+      cuuint32_t box[2] = {TBM, TBN};
+      cuuint32_t estr[2] = {1, 1};
+      if (fn && fn(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(C), dims, strides, box,
+                   estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+        p.prefetch_c = 1;
+    }
   }
   static bool attr = false;
   if (!attr) {
@@ -544,12 +585,72 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
-  const int tiles = p.tiles_m * p.tiles_n;
-  const int grid = tiles < sms ? tiles : sms;
+  const int units = p.tiles_m * p.tiles_n * splits;
+  const int grid = units < sms ? units : sms;
   count_launch();
   sgemm_tc05_kernel<<<grid, T_THREADS, T_SMEM, st>>>(mah, mal, mbh, mbl, mc, p);
   CUDA_TRY(cudaGetLastError());
+  if (splits > 1) {
+    const int64_t total = (int64_t)M * N;
+    const int blocks = (int)std::min<int64_t>((total + 255) / 256, 4 * (int64_t)sms);
+    count_launch();
+    splitk_reduce_f32<<<blocks, 256, 0, st>>>(M, N, splits, pbase, (int64_t)M * N,
+                                              C ? beta : 0.0f, C, ldc, D, ldd);
+    CUDA_TRY(cudaGetLastError());
+  }
   return 0;
+}
+
+}  // namespace
+
+int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha, const float* A,
+             int64_t lda, const float* B, int64_t ldb, float beta, const float* C, int64_t ldc,
+             float* D, int64_t ldd, float* ws, int64_t ws_elems, const FusedSums* fs, int max_ctas,
+             int splits) {
+  if (M <= 0 || N <= 0) return 0;
+  if (K <= 0) {
+    set_last_error("sgemm_tc needs K > 0");
+    return -1;
+  }
+  const int64_t ldk = (K + 3) / 4 * 4;
+  if (!ws || ws_elems < sgemm_workspace_elems(M, N, K, splits)) {
+    set_last_error("sgemm_tc workspace too small");
+    return -1;
+  }
+  // 256-byte aligned operand copies inside the workspace
+  float* ah = align256(ws);
+  float* al = align256(ah + (int64_t)M * ldk);
+  float* bh = align256(al + (int64_t)M * ldk);
+  float* bl = align256(bh + (int64_t)N * ldk);
+  float* part = bl + (int64_t)N * ldk;
+  if (part > ws + ws_elems) {
+    set_last_error("sgemm_tc workspace too small (alignment)");
+    return -1;
+  }
+  // A: op(A) is M x K. 'N': (m, k) at m + k*lda -> transpose; 'T': (m, k) at k + m*lda -> copy.
+  const bool AT = (ta == 'T' || ta == 't');
+  const bool BT = (tb == 'T' || tb == 't');
+  ABFT_TRY(sgemm_split_operand(st, A, lda, M, K, (int)ldk, AT ? 1 : 0, ah, al, ldk));
+  // op(B) is K x N; B' row n = column n of op(B): 'N': (k, n) at k + n*ldb -> copy;
+  // 'T': (k, n) at n + k*ldb -> transpose.
+  ABFT_TRY(sgemm_split_operand(st, B, ldb, N, K, (int)ldk, BT ? 0 : 1, bh, bl, ldk));
+  return launch_tc(st, M, N, K, alpha, ah, al, ldk, bh, bl, ldk, beta, C, ldc, D, ldd, part,
+                   ws + ws_elems - part, fs, max_ctas, splits);
+}
+
+int sgemm_tc_presplit(cudaStream_t st, int M, int N, int K, float alpha, const float* ah,
+                      const float* al, int64_t lda_k, const float* bh, const float* bl, int64_t ldb_k,
+                      float beta, const float* C, int64_t ldc, float* D, int64_t ldd, float* part,
+                      int64_t part_elems, int max_ctas, int splits) {
+  if (M <= 0 || N <= 0 || K <= 0) return 0;
+  if ((lda_k % 4) || (ldb_k % 4) || (reinterpret_cast<uintptr_t>(ah) & 15) ||
+      (reinterpret_cast<uintptr_t>(al) & 15) || (reinterpret_cast<uintptr_t>(bh) & 15) ||
+      (reinterpret_cast<uintptr_t>(bl) & 15)) {
+    set_last_error("sgemm_tc_presplit: operands must be 16-byte aligned with ld % 4 == 0");
+    return -1;
+  }
+  return launch_tc(st, M, N, K, alpha, ah, al, lda_k, bh, bl, ldb_k, beta, C, ldc, D, ldd, part,
+                   part_elems, nullptr, max_ctas, splits);
 }
 
 }  // namespace abft

@@ -10,7 +10,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0):
+def _run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0, splits=1):
     import torch
     from paper_2301_03166_b200 import _lib
     lib = _lib.load()
@@ -22,9 +22,9 @@ def _run(ta, tb, m, n, k, alpha=1.0, beta=0.0, seed=0):
     B = torch.randn(b_shape[::-1], generator=g, dtype=torch.float32).cuda()
     C = torch.randn((n, m), generator=g, dtype=torch.float32).cuda()
     D = torch.empty((n, m), dtype=torch.float32, device="cuda")
-    rc = lib.abft_dev_sgemm(None, ta.encode(), tb.encode(), m, n, k, alpha, A.data_ptr(),
-                            a_shape[0], B.data_ptr(), b_shape[0], beta,
-                            C.data_ptr() if beta else None, m, D.data_ptr(), m)
+    rc = lib.abft_dev_sgemm_splitk(None, ta.encode(), tb.encode(), m, n, k, alpha, A.data_ptr(),
+                                   a_shape[0], B.data_ptr(), b_shape[0], beta,
+                                   C.data_ptr() if beta else None, m, D.data_ptr(), m, splits)
     assert rc == 0, _lib.last_error()
     torch.cuda.synchronize()
     An = A.double().cpu().numpy().T
@@ -51,3 +51,21 @@ def test_sgemm_tc05_large_k_and_alpha():
     got, ref, mag = _run("N", "N", 512, 512, 2048, alpha=0.5, beta=0.0)
     err = np.abs(got - ref)
     assert np.all(err <= 2e-6 * (2048 / 256) ** 0.5 * mag), float((err / mag).max())
+
+
+@pytest.mark.parametrize("ta,tb", [("N", "N"), ("N", "T"), ("T", "N")])
+@pytest.mark.parametrize("m,n,k,splits", [(1000, 128, 4096, 7), (128, 517, 3000, 16),
+                                          (300, 200, 100, 3), (256, 256, 64, 5)])
+def test_sgemm_tc05_split_k(ta, tb, m, n, k, splits):
+    """split-K: K-slices in separate tensor-core chains + fixed-order
+    reduction (beta*C added once); splits beyond the k-block count clamp."""
+    got, ref, mag = _run(ta, tb, m, n, k, alpha=-1.0, beta=1.0, splits=splits)
+    err = np.abs(got - ref)
+    tol = 2e-6 * max(1.0, (k / 256) ** 0.5)
+    assert np.all(err <= tol * mag + 1e-30), float((err / (mag + 1e-30)).max())
+
+
+def test_sgemm_tc05_split_k_is_deterministic():
+    a = _run("N", "T", 640, 128, 8192, alpha=-1.0, beta=1.0, splits=12)[0]
+    b = _run("N", "T", 640, 128, 8192, alpha=-1.0, beta=1.0, splits=12)[0]
+    assert np.array_equal(a, b)
