@@ -25,15 +25,16 @@ namespace {
 constexpr int DT = 512;   // threads of the diagonal kernel
 constexpr int NBK = 32;   // sub-panel width
 constexpr int PLD = 257;  // smem leading dim of the staged sub-panel (w <= 256)
-constexpr int DIAG_SMEM = (NBK * PLD + 224 * 33) * 8 + 64;
+constexpr int DIAG_SMEM = (NBK * PLD + 224 * 33) * 8 + 64;   // bytes for fp64 (fp32 uses half)
 constexpr int INV_SMEM = (256 * 33 + 32 * 257) * 8;
 
 // Accessor for a (possibly transposed) column-major matrix.
+template <typename T>
 struct Acc {
-  double* p;
+  T* p;
   int64_t ld;
   bool t;
-  ABFT_DEVINL double& at(int r, int c) const { return t ? p[c + r * ld] : p[r + c * ld]; }
+  ABFT_DEVINL T& at(int r, int c) const { return t ? p[c + r * ld] : p[r + c * ld]; }
 };
 
 // mode 0: LU without pivoting (L unit lower \ U upper in place),
@@ -43,12 +44,14 @@ struct Acc {
 // 512 threads viewed as 16 warps x 32 lanes: lanes walk rows, warps walk
 // columns (no integer division in the inner loops); the trailing update of
 // each 32-column sub-panel is register-blocked (7 rows x 2 columns / thread).
+template <typename T>
 __global__ void __launch_bounds__(DT, 1)
-    diag_factor_kernel(double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                       double* Uinv, int64_t ldu, int* info, int64_t col_base) {
-  extern __shared__ double sm[];
-  double* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
-  double* Rs = sm + NBK * PLD;     // [224][33]   Rs[c*33 + i]
+    diag_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
+                       T* Uinv, int64_t ldu, int* info, int64_t col_base) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T* sm = reinterpret_cast<T*>(sm_raw);
+  T* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
+  T* Rs = sm + NBK * PLD;     // [224][33]   Rs[c*33 + i]
   __shared__ int s_bad;
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   if (tid == 0) s_bad = 0;
@@ -60,8 +63,48 @@ __global__ void __launch_bounds__(DT, 1)
     for (int c = ty; c < jw; c += DT / 32)
       for (int r = tx; r < rem; r += 32) Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
     __syncthreads();
-    for (int c = 0; c < jw; ++c) {
-      const double piv = Ps[c * PLD + c];
+    if (mode == 0) {
+      // LU: the sub-panel lives in registers, one row per thread; per pivot
+      // the owner of row c publishes it (double-buffered) and ONE barrier
+      // separates the pivots (the shared-memory form needed three)
+      T a[NBK];
+      const bool own = tid < rem;
+#pragma unroll
+      for (int c = 0; c < NBK; ++c) a[c] = (own && c < jw) ? Ps[c * PLD + tid] : T(0);
+      T* prow = Rs;  // [2][NBK] pivot rows (Rs is free during the panel phase)
+      bool badf = false;
+#pragma unroll
+      for (int c = 0; c < NBK; ++c) {
+        if (c < jw && !badf) {  // uniform across the CTA
+          T* pr = prow + (c & 1) * NBK;
+          if (tid == c) {
+#pragma unroll
+            for (int cc = c; cc < NBK; ++cc) pr[cc] = a[cc];
+          }
+          __syncthreads();
+          const T piv = pr[c];
+          if (piv == T(0) || !isfinite(piv)) {
+            badf = true;
+            if (tid == 0) {
+              s_bad = jb + c + 1;
+              atomicCAS(info, 0, (int)(col_base + jb + c + 1));
+            }
+          } else if (own && tid > c) {
+            const T l = a[c] / piv;
+            a[c] = l;
+#pragma unroll
+            for (int cc = c + 1; cc < NBK; ++cc) a[cc] = fma(-l, pr[cc], a[cc]);
+          }
+        }
+      }
+      if (own && !badf) {
+#pragma unroll
+        for (int c = 0; c < NBK; ++c)
+          if (c < jw) Ps[c * PLD + tid] = a[c];
+      }
+    }
+    for (int c = 0; c < jw && mode != 0; ++c) {
+      const T piv = Ps[c * PLD + c];
       const bool bad = (mode == 0) ? (piv == 0.0 || !isfinite(piv)) : (!(piv > 0.0) || !isfinite(piv));
       if (bad) {
         if (tid == 0) {
@@ -75,15 +118,15 @@ __global__ void __launch_bounds__(DT, 1)
         for (int r = c + 1 + tid; r < rem; r += DT) Ps[c * PLD + r] /= piv;
         __syncthreads();
         for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
-          const double u = Ps[cc * PLD + c];
+          const T u = Ps[cc * PLD + c];
           for (int r = c + 1 + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
         }
       } else {
-        const double d = sqrt(piv);
+        const T d = sqrt(piv);
         for (int r = c + tid; r < rem; r += DT) Ps[c * PLD + r] = (r == c) ? d : Ps[c * PLD + r] / d;
         __syncthreads();
         for (int cc = c + 1 + ty; cc < jw; cc += DT / 32) {
-          const double u = Ps[c * PLD + cc];
+          const T u = Ps[c * PLD + cc];
           for (int r = cc + tx; r < rem; r += 32) Ps[cc * PLD + r] -= Ps[c * PLD + r] * u;
         }
       }
@@ -97,7 +140,7 @@ __global__ void __launch_bounds__(DT, 1)
     __syncthreads();
     const int ncols = w - jb - jw;
     if (ncols <= 0) continue;
-    const double* Rop;  // right operand of the trailing update: R[l][c] = Rop[c*ldr + l]
+    const T* Rop;  // right operand of the trailing update: R[l][c] = Rop[c*ldr + l]
     int ldr;
     if (mode == 0) {
       // U row block: R = L11^{-1} D[jb:jb+jw, jb+jw:w] (unit lower), one column per thread
@@ -106,7 +149,7 @@ __global__ void __launch_bounds__(DT, 1)
       __syncthreads();
       for (int c = tid; c < ncols; c += DT) {
         for (int i = 1; i < jw; ++i) {
-          double x = Rs[c * 33 + i];
+          T x = Rs[c * 33 + i];
           for (int l = 0; l < i; ++l) x -= Ps[l * PLD + i] * Rs[c * 33 + l];
           Rs[c * 33 + i] = x;
         }
@@ -127,17 +170,17 @@ __global__ void __launch_bounds__(DT, 1)
     // trailing update D[jb+jw+r, jb+jw+c] -= sum_l P21[r][l] * R[l][c]
     const int nr = rem - jw;
     for (int c0 = 2 * ty; c0 < ncols; c0 += DT / 16) {
-      double acc[7][2];
+      T acc[7][2];
 #pragma unroll
       for (int i = 0; i < 7; ++i) acc[i][0] = acc[i][1] = 0.0;
       const bool c1ok = c0 + 1 < ncols;
       for (int l = 0; l < jw; ++l) {
-        const double r0v = Rop[c0 * ldr + l];
-        const double r1v = c1ok ? Rop[(c0 + 1) * ldr + l] : 0.0;
+        const T r0v = Rop[c0 * ldr + l];
+        const T r1v = c1ok ? Rop[(c0 + 1) * ldr + l] : 0.0;
 #pragma unroll
         for (int i = 0; i < 7; ++i) {
           const int r = tx + 32 * i;
-          const double pv = (r < nr) ? Ps[l * PLD + jw + r] : 0.0;
+          const T pv = (r < nr) ? Ps[l * PLD + jw + r] : 0.0;
           acc[i][0] = fma(pv, r0v, acc[i][0]);
           acc[i][1] = fma(pv, r1v, acc[i][1]);
         }
@@ -165,22 +208,24 @@ __global__ void __launch_bounds__(DT, 1)
 // accessors. Column block jb of X solves L X[:, jb] = E[:, jb] by block
 // forward substitution: T = E - L[r0.., c0..r0] X[c0..r0, :] from shared
 // memory (register-blocked), then a right-looking 32x32 solve in parallel.
+template <typename T>
 __global__ void __launch_bounds__(DT)
-    tri_inverse_kernel(const double* D, int64_t ld, int w, int unit_l, double* Linv,
-                       int64_t ldl, double* Uinv, int64_t ldu, const int* info) {
-  extern __shared__ double sm[];
+    tri_inverse_kernel(const T* D, int64_t ld, int w, int unit_l, T* Linv,
+                       int64_t ldl, T* Uinv, int64_t ldu, const int* info) {
+  extern __shared__ __align__(16) unsigned char sm_raw[];
+  T* sm = reinterpret_cast<T*>(sm_raw);
   if (*info != 0) return;  // factorization broke down: nothing to invert
   const bool upper = blockIdx.y == 1;
   if (upper && !Uinv) return;
-  const Acc L{const_cast<double*>(D), ld, upper};
-  const Acc X{upper ? Uinv : Linv, upper ? ldu : ldl, upper};
+  const Acc<T> L{const_cast<T*>(D), ld, upper};
+  const Acc<T> X{upper ? Uinv : Linv, upper ? ldu : ldl, upper};
   const bool unit = upper ? false : (unit_l != 0);
   const int jb = blockIdx.x;
   const int c0 = jb * NBK;
   if (c0 >= w) return;
   const int cw = min(NBK, w - c0);
-  double* Xs = sm;                // [w][33]: Xs[r*33 + c] = X(r, c0 + c), rows r >= c0
-  double* Ls = sm + 256 * 33;     // [32][257]: Ls[r*257 + l] = L(r0 + r, c0 + l)
+  T* Xs = sm;                // [w][33]: Xs[r*33 + c] = X(r, c0 + c), rows r >= c0
+  T* Ls = sm + 256 * 33;     // [32][257]: Ls[r*257 + l] = L(r0 + r, c0 + l)
   const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
   // rows above the diagonal block are zero
   for (int r = ty; r < c0; r += DT / 32)
@@ -194,11 +239,11 @@ __global__ void __launch_bounds__(DT)
     __syncthreads();
     // T = E - L(r0.., c0..r0) X(c0..r0, :): thread (row ty*2+{0,1}, col tx)
     for (int rr = 2 * ty; rr < rh; rr += DT / 16) {
-      double a0 = (r0 + rr == c0 + tx) ? 1.0 : 0.0;
-      double a1 = (r0 + rr + 1 == c0 + tx) ? 1.0 : 0.0;
+      T a0 = (r0 + rr == c0 + tx) ? 1.0 : 0.0;
+      T a1 = (r0 + rr + 1 == c0 + tx) ? 1.0 : 0.0;
       if (tx < cw) {
         for (int l = 0; l < r0 - c0; ++l) {
-          const double xv = Xs[l * 33 + tx];
+          const T xv = Xs[l * 33 + tx];
           a0 -= Ls[rr * 257 + l] * xv;
           if (rr + 1 < rh) a1 -= Ls[(rr + 1) * 257 + l] * xv;
         }
@@ -227,37 +272,49 @@ __global__ void __launch_bounds__(DT)
 
 }  // namespace
 
-int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
+template <typename T>
+static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
+                         T* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
   if (w <= 0) return 0;
   if (w > 256) {
     set_last_error("diag_factor: block width %d > 256 (host-level blocking required)", w);
     return -1;
   }
+  const int dsm = DIAG_SMEM / 8 * (int)sizeof(T) + 64;
+  const int ism = INV_SMEM / 8 * (int)sizeof(T);
   static bool attr = false;
   if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(diag_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  DIAG_SMEM));
+    CUDA_TRY(cudaFuncSetAttribute(diag_factor_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  dsm));
     attr = true;
   }
   count_launch();
-  diag_factor_kernel<<<1, DT, DIAG_SMEM, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
-                                                col_base);
+  diag_factor_kernel<T><<<1, DT, dsm, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
+                                            col_base);
   CUDA_TRY(cudaGetLastError());
   if (Linv || Uinv) {
     static bool attr2 = false;
     if (!attr2) {
-      CUDA_TRY(cudaFuncSetAttribute(tri_inverse_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, INV_SMEM));
+      CUDA_TRY(cudaFuncSetAttribute(tri_inverse_kernel<T>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ism));
       attr2 = true;
     }
     dim3 grid((w + NBK - 1) / NBK, Uinv ? 2 : 1);
     count_launch();
-    tri_inverse_kernel<<<grid, DT, INV_SMEM, st>>>(D, ld, w, mode == 0 ? 1 : 0, Linv, ldl, Uinv,
-                                                   ldu, info_dev);
+    tri_inverse_kernel<T><<<grid, DT, ism, st>>>(D, ld, w, mode == 0 ? 1 : 0, Linv, ldl, Uinv,
+                                                 ldu, info_dev);
     CUDA_TRY(cudaGetLastError());
   }
   return 0;
+}
+
+int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
+                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
+  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base);
+}
+int diag_factor(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv, int64_t ldl,
+                float* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
+  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base);
 }
 
 // ===========================================================================
