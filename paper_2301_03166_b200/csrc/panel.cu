@@ -624,11 +624,14 @@ __global__ void __launch_bounds__(QT, 1)
       // rest -= beta * outer(v, w) over own rows i >= j
       const int ib = (int)max((int64_t)0, j - r_lo);
       const int ncc = cw - jj - 1;
-      for (int idx = tid; idx < (nr - ib) * ncc; idx += QT) {
-        const int i = ib + idx % (nr - ib);
-        const int c = jj + 1 + idx / (nr - ib);
-        const double vi = (r_lo + i == j) ? v0 : Ps[jj * QR_RS + i];
-        Ps[c * QR_RS + i] -= beta * (vi * red[c - jj]);
+      // warp per column, lanes over rows (no per-element div/mod)
+      for (int cq = warp; cq < ncc; cq += QT / 32) {
+        const int c = jj + 1 + cq;
+        const double bw = red[c - jj];
+        for (int i = ib + lane; i < nr; i += 32) {
+          const double vi = (r_lo + i == j) ? v0 : Ps[jj * QR_RS + i];
+          Ps[c * QR_RS + i] -= beta * (vi * bw);
+        }
       }
       __syncthreads();
       for (int i = ib + tid; i < nr; i += QT) {
@@ -656,13 +659,11 @@ __global__ void __launch_bounds__(QT, 1)
     // C is processed in 32-column chunks staged in shared memory (Ws), so every
     // dot product runs out of shared memory.
     const int ib = (int)max((int64_t)0, (int64_t)cs - r_lo);  // V_s is zero above row cs
-    const int nrr = nr - ib;
     for (int cc0 = 0; cc0 < rem; cc0 += 32) {
       const int ccw = min(32, rem - cc0);
-      for (int idx = tid; idx < ccw * nrr; idx += QT) {
-        const int c = idx / nrr, i = ib + idx % nrr;
-        Ws[c * QR_RS + i] = P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld];
-      }
+      for (int c = warp; c < ccw; c += QT / 32)
+        for (int i = ib + lane; i < nr; i += 32)
+          Ws[c * QR_RS + i] = P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld];
       __syncthreads();
       for (int idx = tid; idx < cw * ccw; idx += QT) {
         const int l = idx / ccw, c = idx % ccw;
@@ -696,12 +697,12 @@ __global__ void __launch_bounds__(QT, 1)
     // C(own rows) -= V_s W', chunk by chunk through shared memory
     for (int cc0 = 0; cc0 < rem; cc0 += 32) {
       const int ccw = min(32, rem - cc0);
-      for (int idx = tid; idx < ccw * nrr; idx += QT) {
-        const int c = idx / nrr, i = ib + idx % nrr;
-        double acc = 0.0;
-        for (int l = 0; l < cw; ++l) acc = fma(Vs[l * QR_RS + i], Ps[l * QR_RS + cc0 + c], acc);
-        P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld] -= acc;
-      }
+      for (int c = warp; c < ccw; c += QT / 32)
+        for (int i = ib + lane; i < nr; i += 32) {
+          double acc = 0.0;
+          for (int l = 0; l < cw; ++l) acc = fma(Vs[l * QR_RS + i], Ps[l * QR_RS + cc0 + c], acc);
+          P[(r_lo + i) + (int64_t)(ce + cc0 + c) * ld] -= acc;
+        }
     }
     grid.sync();  // the next sub-panel's slab load reads other CTAs' rows? no: own rows only,
                   // but wfin / part2 are reused by the next block update
