@@ -89,7 +89,8 @@ def test_run_modes_on_b200(kind):
         out[mode] = s
     # unprotected modes inject nothing (base clocks are fault-free)
     for mode in ("original", "r2h", "sr"):
-        assert out[mode].abft_ms < 0.02 * out[mode].device_ms  # only empty timer brackets
+        # only empty timer brackets (each <= ~10 us of event resolution/noise)
+        assert out[mode].abft_ms < 0.01 * -(-n // b) + 0.02 * out[mode].device_ms
         assert sum(out[mode].faults_injected.values()) == 0
         assert set(out[mode].schemes) == {"none"}
     # bsr: overclocked iterations run under adaptive checksums, every

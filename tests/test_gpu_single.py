@@ -90,3 +90,18 @@ def test_fp32_streamed_result_equals_device_factor(kind):
     out = np.full((n, n), np.nan, dtype=np.float32, order="F")
     f.run_protected("full", {1: {"0d": 1}}, np.random.default_rng(seed), out=out)
     np.testing.assert_array_equal(out, f.m)
+
+
+@pytest.mark.parametrize("kind,bound", [("lu", 1.5e-6), ("cholesky", 1.5e-6), ("qr", 6e-5)])
+def test_fp32_large_residual_bound(kind, bound):
+    """N = 12288, b = 256: deep-K updates take both GEMM regimes (split-K for
+    narrow outputs, sequential K chunks for wide ones); every tensor-core
+    chain must stay within the chunk depth. Measured clean residuals are
+    ~3e-7 (LU / Cholesky) and ~2e-5 (QR); a single unchunked chain of depth
+    ~10^4 raises LU / Cholesky by ~10x."""
+    n, b = 12288, 256
+    a = P.generate_test_matrix(kind, n, 3)
+    f = P.SFactorization(kind, a, b)
+    f.run_protected("none")
+    res = f.residual(a)
+    assert res <= bound, res
