@@ -25,6 +25,7 @@
 // tile i+1.
 #include "sgemm.cuh"
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -39,7 +40,7 @@ constexpr int TSTAGES = 3;
 constexpr int T_A_BYTES = TBM * TBK * 4;
 constexpr int T_B_BYTES = TBN * TBK * 4;
 constexpr int T_STAGE_BYTES = 2 * T_A_BYTES + 2 * T_B_BYTES;  // 64 KB
-constexpr int T_THREADS = 320;  // producer, MMA issuer, 8 epilogue warps
+constexpr int T_THREADS = 384;  // producer, MMA issuer, 8 epilogue warps, 2 converter warps
 constexpr int T_TMEM_COLS = 256;  // two 128-column fp32 accumulators
 constexpr int T_TP = 17;          // padded 32 x 16 transpose tile
 // smem: ring | barriers (2*ST + 4) | tmem slot | per-warp transpose tiles |
@@ -70,6 +71,10 @@ struct SParams {
   // D + split * dstride (a partial; beta = 0, no fused sums)
   int splits, kbs;
   int64_t dstride;
+  // raw operands: TMA brings the unsplit fp32 box into the hi slot and the
+  // converter warps form hi = rna_tf32(x) / lo = x - hi in shared memory
+  // (elementwise, so the 128-byte swizzle is preserved) -- no split pass
+  int raw_a, raw_b;
   FusedSums sums;
 };
 
@@ -136,7 +141,8 @@ __global__ void __launch_bounds__(T_THREADS, 1)
   uint64_t* empty = full + TSTAGES;
   uint64_t* tfull = empty + TSTAGES;   // [2]
   uint64_t* tempty = tfull + 2;        // [2]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* conv = tempty + 2;         // [TSTAGES] raw operands converted
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(conv + TSTAGES);
   float* trs = reinterpret_cast<float*>(smem + T_TR_OFF);
   float* parts = reinterpret_cast<float*>(smem + T_COL_OFF);   // [2 parities][T_PART_FLOATS]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -147,6 +153,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
     for (int s = 0; s < TSTAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
+      mbar_init(&conv[s], 2);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -185,11 +192,12 @@ __global__ void __launch_bounds__(T_THREADS, 1)
           const int s = q % TSTAGES;
           if (q >= TSTAGES) mbar_wait(&empty[s], ((q / TSTAGES) - 1) & 1);
           uint8_t* st = smem + s * T_STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[s], T_STAGE_BYTES);
+          mbar_arrive_expect_tx(&full[s], T_STAGE_BYTES - (p.raw_a ? T_A_BYTES : 0) -
+                                              (p.raw_b ? T_B_BYTES : 0));
           tma_load_2d(st, &mAh, &full[s], kb * TBK, tm * TBM);
-          tma_load_2d(st + T_A_BYTES, &mAl, &full[s], kb * TBK, tm * TBM);
+          if (!p.raw_a) tma_load_2d(st + T_A_BYTES, &mAl, &full[s], kb * TBK, tm * TBM);
           tma_load_2d(st + 2 * T_A_BYTES, &mBh, &full[s], kb * TBK, tn * TBN);
-          tma_load_2d(st + 2 * T_A_BYTES + T_B_BYTES, &mBl, &full[s], kb * TBK, tn * TBN);
+          if (!p.raw_b) tma_load_2d(st + 2 * T_A_BYTES + T_B_BYTES, &mBl, &full[s], kb * TBK, tn * TBN);
         }
       }
     }
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       const uint32_t dt = tmem_base + (uint32_t)(acc * TBN);
       for (int kb = kb0; kb < kb1; ++kb, ++q) {
         const int s = q % TSTAGES;
-        mbar_wait(&full[s], (q / TSTAGES) & 1);
+        mbar_wait((p.raw_a | p.raw_b) ? &conv[s] : &full[s], (q / TSTAGES) & 1);
         tc_fence_after();
         if (lane == 0) {
           const uint32_t st = smem_u32(smem + s * T_STAGE_BYTES);
@@ -225,6 +233,51 @@ __global__ void __launch_bounds__(T_THREADS, 1)
       }
       if (lane == 0) mma_commit(&tfull[acc]);
       __syncwarp();
+    }
+  } else if (warp >= 10) {
+    // ===== converters (warps 10, 11): raw fp32 -> hi (in place) + lo =====
+    if (p.raw_a | p.raw_b) {
+      const int ct = threadIdx.x - 320;  // 0..63
+      uint32_t q = 0;
+      for (int t = blockIdx.x; t < units; t += gridDim.x) {
+        const int kb0 = (t / tiles) * p.kbs, kb1 = min(p.nkb, kb0 + p.kbs);
+        for (int kb = kb0; kb < kb1; ++kb, ++q) {
+          const int s = q % TSTAGES;
+          mbar_wait(&full[s], (q / TSTAGES) & 1);
+          uint8_t* st = smem + s * T_STAGE_BYTES;
+#pragma unroll
+          for (int op = 0; op < 2; ++op) {
+            if (op == 0 ? !p.raw_a : !p.raw_b) continue;
+            float4* hi = reinterpret_cast<float4*>(st + (op == 0 ? 0 : 2 * T_A_BYTES));
+            float4* lo = reinterpret_cast<float4*>(st + (op == 0 ? T_A_BYTES : 2 * T_A_BYTES + T_B_BYTES));
+#pragma unroll 4
+            for (int j = ct; j < T_A_BYTES / 16; j += 64) {
+              float4 x = hi[j], h, l;
+              uint32_t u;
+              asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(u) : "f"(x.x));
+              h.x = __uint_as_float(u);
+              asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(u) : "f"(x.y));
+              h.y = __uint_as_float(u);
+              asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(u) : "f"(x.z));
+              h.z = __uint_as_float(u);
+              asm("cvt.rna.tf32.f32 %0, %1;\n" : "=r"(u) : "f"(x.w));
+              h.w = __uint_as_float(u);
+              l.x = x.x - h.x;
+              l.y = x.y - h.y;
+              l.z = x.z - h.z;
+              l.w = x.w - h.w;
+              hi[j] = h;
+              lo[j] = l;
+            }
+          }
+          // generic-proxy stores -> visible to the tensor core's async proxy
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0)
+            asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&conv[s]))
+                         : "memory");
+        }
+      }
     }
   } else {
     // ===== epilogue (warps 2..9): two warps per TMEM lane quarter, each
@@ -511,7 +564,7 @@ float* align256(float* q) {
 int launch_tc(cudaStream_t st, int M, int N, int K, float alpha, const float* ah, const float* al,
               int64_t lda_k, const float* bh, const float* bl, int64_t ldb_k, float beta, const float* C,
               int64_t ldc, float* D, int64_t ldd, float* part, int64_t part_elems, const FusedSums* fs,
-              int max_ctas, int splits) {
+              int max_ctas, int splits, int raw_a = 0, int raw_b = 0) {
   CUtensorMap mah, mal, mbh, mbl;
   ABFT_TRY(kmajor_map(&mah, ah, M, K, lda_k));
   ABFT_TRY(kmajor_map(&mal, al, M, K, lda_k));
@@ -529,6 +582,8 @@ int launch_tc(cudaStream_t st, int M, int N, int K, float alpha, const float* ah
   p.kbs = (p.nkb + splits - 1) / splits;
   splits = (p.nkb + p.kbs - 1) / p.kbs;  // no empty splits
   p.splits = splits;
+  p.raw_a = raw_a;
+  p.raw_b = raw_b;
   p.alpha = alpha;
   p.fuse = 0;
   p.prefetch_c = 0;
@@ -617,6 +672,15 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
     set_last_error("sgemm_tc workspace too small");
     return -1;
   }
+  // K-major sources ('T' A, 'N' B) go to the kernel raw (split in shared
+  // memory) when TMA can address them directly
+  static const bool raw_ok = [] {
+    const char* e = getenv("ABFT_SGEMM_RAW");
+    return !(e && e[0] == '0');
+  }();
+  auto tma_ok = [](const float* q, int64_t ld) {
+    return (reinterpret_cast<uintptr_t>(q) & 15) == 0 && (ld % 4) == 0;
+  };
   // 256-byte aligned operand copies inside the workspace
   float* ah = align256(ws);
   float* al = align256(ah + (int64_t)M * ldk);
@@ -630,12 +694,19 @@ int sgemm_tc(cudaStream_t st, char ta, char tb, int M, int N, int K, float alpha
   // A: op(A) is M x K. 'N': (m, k) at m + k*lda -> transpose; 'T': (m, k) at k + m*lda -> copy.
   const bool AT = (ta == 'T' || ta == 't');
   const bool BT = (tb == 'T' || tb == 't');
-  ABFT_TRY(sgemm_split_operand(st, A, lda, M, K, (int)ldk, AT ? 1 : 0, ah, al, ldk));
+  // the converter re-splits an operand box for every tile that reads it:
+  // worth it only while the operand is read by at most two tile rows /
+  // columns (else the one-time split pass is cheaper)
+  const int tiles_m = (M + TBM - 1) / TBM, tiles_n = (N + TBN - 1) / TBN;
+  const bool raw_a = raw_ok && AT && tiles_n <= 2 && tma_ok(A, lda);
+  const bool raw_b = raw_ok && !BT && tiles_m <= 2 && tma_ok(B, ldb);
+  if (!raw_a) ABFT_TRY(sgemm_split_operand(st, A, lda, M, K, (int)ldk, AT ? 1 : 0, ah, al, ldk));
   // op(B) is K x N; B' row n = column n of op(B): 'N': (k, n) at k + n*ldb -> copy;
   // 'T': (k, n) at n + k*ldb -> transpose.
-  ABFT_TRY(sgemm_split_operand(st, B, ldb, N, K, (int)ldk, BT ? 0 : 1, bh, bl, ldk));
-  return launch_tc(st, M, N, K, alpha, ah, al, ldk, bh, bl, ldk, beta, C, ldc, D, ldd, part,
-                   ws + ws_elems - part, fs, max_ctas, splits);
+  if (!raw_b) ABFT_TRY(sgemm_split_operand(st, B, ldb, N, K, (int)ldk, BT ? 0 : 1, bh, bl, ldk));
+  return launch_tc(st, M, N, K, alpha, raw_a ? A : ah, raw_a ? A : al, raw_a ? lda : ldk,
+                   raw_b ? B : bh, raw_b ? B : bl, raw_b ? ldb : ldk, beta, C, ldc, D, ldd, part,
+                   ws + ws_elems - part, fs, max_ctas, splits, raw_a, raw_b);
 }
 
 int sgemm_tc_presplit(cudaStream_t st, int M, int N, int K, float alpha, const float* ah,

@@ -69,3 +69,33 @@ def test_sgemm_tc05_split_k_is_deterministic():
     a = _run("N", "T", 640, 128, 8192, alpha=-1.0, beta=1.0, splits=12)[0]
     b = _run("N", "T", 640, 128, 8192, alpha=-1.0, beta=1.0, splits=12)[0]
     assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("splits", [1, 3])
+def test_sgemm_tc05_raw_operands_with_k_tail(splits):
+    """'T' A and 'N' B with 16-byte aligned leading dimensions are split in
+    shared memory (raw TMA boxes); K = 77 leaves a partial k-block whose
+    tail the TMA must zero-fill. Checked against fp64."""
+    import torch
+    from paper_2301_03166_b200 import _lib
+    lib = _lib.load()
+    m, n, k, ld = 200, 130, 77, 80
+    g = torch.Generator(device="cpu").manual_seed(5)
+    At = torch.randn((m, ld), generator=g, dtype=torch.float32)   # column-major k x m, ld 80
+    Bt = torch.randn((n, ld), generator=g, dtype=torch.float32)   # column-major k x n, ld 80
+    At[:, k:] = float("nan")  # must never be read
+    Bt[:, k:] = float("nan")
+    C = torch.randn((n, m), generator=g, dtype=torch.float32)
+    A, B, Cd = At.cuda(), Bt.cuda(), C.cuda()
+    D = torch.empty((n, m), dtype=torch.float32, device="cuda")
+    rc = lib.abft_dev_sgemm_splitk(None, b"T", b"N", m, n, k, -1.0, A.data_ptr(), ld, B.data_ptr(),
+                                   ld, 1.0, Cd.data_ptr(), m, D.data_ptr(), m, splits)
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    opA = At[:, :k].double().numpy()          # m x k
+    opB = Bt[:, :k].double().numpy().T        # k x n
+    ref = -(opA @ opB) + C.double().numpy().T
+    mag = np.abs(opA) @ np.abs(opB) + np.abs(C.double().numpy().T)
+    got = D.double().cpu().numpy().T
+    assert np.all(np.isfinite(got))
+    assert np.all(np.abs(got - ref) <= 2e-6 * mag), float((np.abs(got - ref) / mag).max())
