@@ -439,21 +439,29 @@ __global__ void __launch_bounds__(512)
   for (int64_t idx = tid; idx < (int64_t)w * w; idx += blockDim.x)
     T[(idx % w) + (idx / w) * ldt] = 0.0;
   __syncthreads();
-  // diagonal blocks: one warp per block (lane = row within block)
+  // diagonal blocks: one warp per block (lane = row within block), the
+  // block of Gm and the T block staged in shared memory
   for (int bk = warp; bk < nblk; bk += blockDim.x / 32) {
     const int j0 = bk * 32, jw = min(32, w - j0);
+    double* Gs = lsm + (int64_t)bk * 2 * 32 * 33;  // Gs[r*33 + c] = Gm(j0 + r, j0 + c)
+    double* Ts = Gs + 32 * 33;                     // Ts[r*33 + c] = T(j0 + r, j0 + c)
+    for (int c = 0; c < 32; ++c) {
+      Gs[lane * 33 + c] = (lane < jw && c < jw) ? Gm[(j0 + lane) + (int64_t)(j0 + c) * ldg] : 0.0;
+      Ts[lane * 33 + c] = 0.0;
+    }
+    __syncwarp();
     for (int jj = 0; jj < jw; ++jj) {
-      const int j = j0 + jj;
-      const double bj = betas[j];
+      const double bj = betas[j0 + jj];
       if (lane < jj) {
-        const int i = j0 + lane;
         double s = 0.0;
-        for (int l = i; l < j; ++l) s += T[i + l * ldt] * Gm[l + j * ldg];
-        T[i + j * ldt] = -bj * s;
+        for (int l = lane; l < jj; ++l) s = fma(Ts[lane * 33 + l], Gs[l * 33 + jj], s);
+        Ts[lane * 33 + jj] = -bj * s;
       }
-      if (lane == 0) T[j + j * ldt] = bj;
+      if (lane == 0) Ts[jj * 33 + jj] = bj;
       __syncwarp();
     }
+    if (lane < jw)
+      for (int c = lane; c < jw; ++c) T[(j0 + lane) + (int64_t)(j0 + c) * ldt] = Ts[lane * 33 + c];
   }
   __syncthreads();
   double* Ys = lsm;  // [j0][32]
@@ -764,7 +772,8 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
 int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, int w, double* T,
           int64_t ldt) {
   if (w <= 0) return 0;
-  size_t smem = (size_t)w * 32 * sizeof(double);
+  const size_t nblk = (size_t)(w + 31) / 32;
+  size_t smem = std::max((size_t)w * 32, nblk * 2 * 32 * 33) * sizeof(double);
   if (smem > 200 * 1024) {
     set_last_error("larft: panel width %d too large", w);
     return -1;
