@@ -689,14 +689,32 @@ int launch_any(cudaStream_t st, bool AT, bool BT, const CUtensorMap& ma, const C
 
 }  // namespace
 
+// Split-K factor from a wave model of the persistent kernel: units are
+// handed out round-robin, so a launch takes ceil(units / SMs) unit-times;
+// a unit costs (K-slice + fixed prologue/epilogue) DMMA steps on a
+// BM x 64 tile, and every extra slice adds a partial write + read-back.
+// Short-K products (the rank-b trailing updates) never split.
 int gemm_splits_for(int M, int N, int K, int num_sms) {
-  const int64_t tiles = (int64_t)((M + 127) / 128) * ((N + BN - 1) / BN);
-  if (K <= 4 * BK * 8 || tiles >= 2 * num_sms) return 1;
-  int s = static_cast<int>((2 * num_sms + tiles - 1) / tiles);
-  const int maxs = K / (8 * BK);  // keep >= 128 of K per split
-  if (s > maxs) s = maxs;
-  if (s > 32) s = 32;
-  return s < 1 ? 1 : s;
+  if (K <= 4 * BK * 8) return 1;
+  const int maxs = std::min(32, K / (8 * BK));  // keep >= 128 of K per split
+  const double step_s = 2.0 * 64 / 0.25e12;  // seconds per k per tile row (64-wide tile, one SM)
+  int best = 1;
+  double best_t = 0.0;
+  for (int s = 1; s <= std::max(1, maxs); ++s) {
+    const int kps = ((K + s - 1) / s + BK - 1) / BK * BK;
+    const int se = (K + kps - 1) / kps;
+    if (se != s) continue;
+    const int bm = kps <= 1024 ? 64 : 128;
+    const int64_t units = (int64_t)((M + bm - 1) / bm) * ((N + BN - 1) / BN) * se;
+    const int64_t waves = (units + num_sms - 1) / num_sms;
+    double t = (double)waves * (kps + 256) * bm * step_s;
+    if (se > 1) t += (double)se * M * N * 16.0 / 6.0e12 + 5e-6;
+    if (s == 1 || t < 0.98 * best_t) {
+      best = s;
+      best_t = t;
+    }
+  }
+  return best;
 }
 
 static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
