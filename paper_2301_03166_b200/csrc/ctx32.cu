@@ -234,10 +234,25 @@ void s_gemm_plan(int sms, int64_t M, int64_t N, int64_t K, int64_t kchunk, bool 
     *need = sgemm_workspace_elems((int)M, (int)N, (int)std::min(K, kchunk), 1);
     return;
   }
-  if (tiles < sms && K >= 512)
-    S = std::max<int64_t>(S, std::min<int64_t>((2 * sms + tiles - 1) / tiles, K / 256));
-  S = std::min<int64_t>(S, (K + 31) / 32);
-  *splits = (int)std::max<int64_t>(S, 1);
+  // wave model (as gemm_splits_for): units run round-robin over the SMs,
+  // each costs its K-slice plus a fixed ~128-deep prologue/epilogue, and
+  // every slice adds a partial write + read-back
+  const int64_t s_min = std::max<int64_t>(S, 1), s_max = std::max<int64_t>(s_min, std::min<int64_t>(64, K / 128));
+  double best_t = 0.0;
+  int64_t best = s_min;
+  for (int64_t sc = s_min; sc <= s_max; ++sc) {
+    const int64_t kps = ((K + sc - 1) / sc + 31) / 32 * 32;
+    if ((K + kps - 1) / kps != sc) continue;
+    const int64_t waves = (tiles * sc + sms - 1) / sms;
+    // seconds: one 128 x 128 x 32 3xTF32 k-block ~ 0.4 us per SM
+    double t = (double)waves * ((double)kps / 32.0 + 4.0) * 0.4e-6;
+    if (sc > 1) t += (double)sc * M * N * 8.0 / 6.0e12 + 4e-6;
+    if (sc == s_min || t < 0.98 * best_t) {
+      best = sc;
+      best_t = t;
+    }
+  }
+  *splits = (int)best;
   *need = sgemm_workspace_elems((int)M, (int)N, (int)K, *splits);
 }
 
