@@ -727,7 +727,14 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    int G = (int)((nk + 63) / 64);
+    // rows per CTA target (ABFT_QR_ROWS, default 64): more rows per CTA
+    // means fewer CTAs in each per-column grid barrier and reduction
+    static const int rows_t = [] {
+      const char* e = getenv("ABFT_QR_ROWS");
+      const int v = e ? atoi(e) : 0;
+      return v >= 16 && v <= QR_RMAX ? v : 64;
+    }();
+    int G = (int)((nk + rows_t - 1) / rows_t);
     if (G > sms) G = sms;
     if ((nk + G - 1) / G <= QR_RMAX && 2LL * G * 32 <= part_elems) {
       static bool attr = false;
