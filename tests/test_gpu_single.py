@@ -20,7 +20,7 @@ EPS32 = float(np.finfo(np.float32).eps)
 
 
 @pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
-@pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64)])
+@pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64), (700, 50)])
 @pytest.mark.parametrize("scheme", ["full", "single"])
 def test_fp32_fault_locations_match_fp32_oracle(kind, n, b, scheme):
     if kind == "qr" and scheme == "single":
