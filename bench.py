@@ -492,8 +492,10 @@ def run_ours(args):
                     # from `ncu --set full` (profiles/ncu_full_gemm_lu32k_r01.txt); the
                     # algorithmic bytes of that launch are 15.7e9 (C in, D out, panels once);
                     # 26.63e9 before the grouped unit order
-                    "traffic": 16.16e9 if args.kind == "lu" else None,
-                    "traffic_algorithmic": 15.7e9 if args.kind == "lu" else None,
+                    # QR: the fused C -= V (T^T W) launch of an early iteration
+                    # (profiles/ncu_full_gemm_qr32k_r01.txt)
+                    "traffic": {"lu": 16.16e9, "qr": 15.36e9}.get(args.kind),
+                    "traffic_algorithmic": {"lu": 15.7e9, "qr": 15.4e9}.get(args.kind),
                     "peak_source": "measured DMMA issue rate on this GPU "
                                    "(abft_probe_dmma_peak; MEASURED_PEAKS.json has no fp64)"}
     else:
