@@ -737,6 +737,8 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // a capped launch (look-ahead side streams) deals its units over fewer CTAs
+    if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
     splits = gemm_splits_for(M, N, K, sms);
   }
   int kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
@@ -761,7 +763,12 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
 
   // three warpgroups (64x64 tiles) for short-K products such as the rank-b
   // trailing updates, two (128x64 tiles) for long K
-  const int nwg = (kps <= 1024) ? 3 : 2;
+  static const int nwg_env = [] {
+    const char* e = getenv("ABFT_GEMM_NWG");  // A/B knob: force 2 or 3 consumer warpgroups
+    const int v = e ? atoi(e) : 0;
+    return (v == 2 || v == 3) ? v : 0;
+  }();
+  const int nwg = nwg_env ? nwg_env : ((kps <= 1024) ? 3 : 2);
   const int BM = nwg == 3 ? Cfg<3>::BM : Cfg<2>::BM;
   CUtensorMap ma, mb;
   int sha = 0, shb = 0;
