@@ -142,6 +142,9 @@ struct abft_sctx {
   bool fuse_enabled = true;
   bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
   int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  int64_t chol_part = -1;         // Cholesky: panel already updated by panels 0..k-2
+  bool chol_enc_ahead = false;    // ... and encoded before that update
+  int next_scheme = 0;            // scheme of the next iteration (abft_s_factorize)
   cudaStream_t st2 = nullptr;     // side stream for the look-ahead diagonal block
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -288,37 +291,61 @@ int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, floa
   return 0;
 }
 
-// Cholesky left-looking panel update P(p:n, p:pe) -= L(p:n, 0:p) L(p:pe, 0:p)^T
-// from the cached operand splits (split-K, one launch + reduction).
-int s_chol_update(abft_sctx* c, int64_t k, int max_ctas) {
+// Cholesky left-looking panel update P(p:n, p:pe) -= L(p:n, K0:K1) L(p:pe, K0:K1)^T
+// from the cached operand splits (split-K, one launch + reduction), on `st`.
+// K0:K1 = 0:p normally; the look-ahead applies 0:p-b on the side stream
+// and leaves p-b:p (the newest panel) to the main stream.
+int s_chol_update(abft_sctx* c, cudaStream_t st, int64_t k, int64_t K0, int64_t K1, int max_ctas) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
-  if (p == 0) return 0;
+  const int64_t K = K1 - K0;
+  if (K <= 0) return 0;
   int splits;
   int64_t need;
-  s_gemm_plan(max_ctas > 0 ? std::min(max_ctas, c->sms) : c->sms, n - p, w, p, S_KCHUNK_CHOL, false,
+  s_gemm_plan(max_ctas > 0 ? std::min(max_ctas, c->sms) : c->sms, n - p, w, K, S_KCHUNK_CHOL, false,
               &splits, &need);
   need = sgemm_partial_elems((int)(n - p), (int)w, splits) + 128;
   if (need > c->sws_elems) {
-    CUDA_TRY(cudaStreamSynchronize(c->st));
+    CUDA_TRY(cudaDeviceSynchronize());
     if (c->sws) cudaFree(c->sws);
     c->sws = nullptr;
     c->sws_elems = need;
     CUDA_TRY(cudaMalloc(&c->sws, c->sws_elems * sizeof(float)));
   }
   float* P = c->m + p + p * c->ld;
-  const float* ah = c->lsh + p * c->ldk;
-  const float* al = c->lsl + p * c->ldk;
+  const float* ah = c->lsh + p * c->ldk + K0;
+  const float* al = c->lsl + p * c->ldk + K0;
   if (splits > 1)
-    return sgemm_tc_presplit(c->st, (int)(n - p), (int)w, (int)p, -1.0f, ah, al, c->ldk, ah, al,
-                             c->ldk, 1.0f, P, c->ld, P, c->ld, c->sws, c->sws_elems, max_ctas, splits);
+    return sgemm_tc_presplit(st, (int)(n - p), (int)w, (int)K, -1.0f, ah, al, c->ldk, ah, al, c->ldk,
+                             1.0f, P, c->ld, P, c->ld, c->sws, c->sws_elems, max_ctas, splits);
   // wide enough for the SMs: the chain-depth bound runs as sequential
   // K chunks accumulating through beta = 1
-  for (int64_t k0 = 0; k0 < p; k0 += S_KCHUNK_CHOL) {
-    const int64_t kl = std::min<int64_t>(S_KCHUNK_CHOL, p - k0);
-    ABFT_TRY(sgemm_tc_presplit(c->st, (int)(n - p), (int)w, (int)kl, -1.0f, ah + k0, al + k0, c->ldk,
+  for (int64_t k0 = 0; k0 < K; k0 += S_KCHUNK_CHOL) {
+    const int64_t kl = std::min<int64_t>(S_KCHUNK_CHOL, K - k0);
+    ABFT_TRY(sgemm_tc_presplit(st, (int)(n - p), (int)w, (int)kl, -1.0f, ah + k0, al + k0, c->ldk,
                                ah + k0, al + k0, c->ldk, 1.0f, P, c->ld, P, c->ld, nullptr, 0, max_ctas,
                                1));
   }
+  return 0;
+}
+
+// Cholesky look-ahead (as ctx.cu): right after TMU(k) the update of panel
+// k+1 by panels 0..k-1 -- final since their PU -- runs on the side stream
+// (encode of panel k+1 first, when its iteration is protected) while the
+// main stream factors panel k; TMU(k+1) then applies panel k alone.
+int s_chol_lookahead(abft_sctx* c, int64_t k, int scheme_next) {
+  const int64_t n = c->n, pk = k * c->b, p1 = (k + 1) * c->b;
+  const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  c->chol_enc_ahead = false;
+  if (scheme_next != ABFT_NONE) {
+    RegionF reg1{c->m + p1 + p1 * c->ld, c->ld, n - p1, w1, c->b};
+    ABFT_TRY(blocksum(c->st2, reg1, s_sums(c, p1, p1, true)));
+    c->chol_enc_ahead = true;
+  }
+  ABFT_TRY(s_chol_update(c, c->st2, k + 1, 0, pk, c->sms - 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  c->chol_part = k + 1;
   return 0;
 }
 
@@ -603,7 +630,8 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   const bool qr_live = c->kind == ABFT_QR && pe < n && k < c->qr_count;
   if (prot) {
     smark(c, SP_ABFT, true);
-    const bool reuse = c->sums_valid && c->kind != ABFT_CHOLESKY;
+    const bool reuse = (c->sums_valid && c->kind != ABFT_CHOLESKY) ||
+                       (c->kind == ABFT_CHOLESKY && c->chol_part == k && c->chol_enc_ahead);
     if (!reuse) ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
     smark(c, SP_ABFT, false);
   }
@@ -667,7 +695,8 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
       fused = fuse;
     }
   } else if (k > 0) {
-    ABFT_TRY(s_chol_update(c, k, 0));
+    // after the look-ahead only the newest panel (k-1) is left
+    ABFT_TRY(s_chol_update(c, c->st, k, c->chol_part == k ? p - c->b : 0, p, 0));
   }
   smark(c, SP_TMU, false);
   smark(c, SP_ABFT, true);
@@ -714,6 +743,10 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   }
   c->sums_valid = prot;
   smark(c, SP_ABFT, false);
+  if (c->chol_part == k) {
+    c->chol_part = -1;
+    c->chol_enc_ahead = false;
+  }
   return 0;
 }
 
@@ -837,7 +870,11 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
   };
   if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
+    // (b % 4: the newest panel's K offset must keep the pre-split rows TMA-aligned)
+    const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb && c->b % 4 == 0;
+    if (la) ABFT_TRY(s_chol_lookahead(c, k, c->next_scheme));
     ABFT_TRY(pd());
+    if (la) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
     ABFT_TRY(pu());
   } else if (c->kind == ABFT_QR) {
     ABFT_TRY(pd());
@@ -1086,6 +1123,8 @@ static void s_reset_state(abft_sctx* c) {
   c->chol_rs_valid = false;
   c->qr_count = 0;
   c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
   c->k_done = 0;
   c->sums_valid = false;
   c->breakdown_col = -1;
@@ -1182,6 +1221,7 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
   c->timed = true;
   for (int64_t k = k0; k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
+    c->next_scheme = (k + 1 < c->nb) ? (schemes ? schemes[k + 1] : scheme) : ABFT_NONE;
     int f0 = 0, f1 = 0;
     if (plan && plan_iter) {
       while (f0 < nplan && plan_iter[f0] < k) ++f0;
@@ -1356,6 +1396,8 @@ ABFT_API int abft_s_restore(abft_sctx* c) {
   c->qr_count = c->snap_qr;
   c->sums_valid = false;
   c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
   c->el_for = -1;
   c->er_for = -1;
   CUDA_TRY(cudaStreamSynchronize(c->st));

@@ -68,7 +68,13 @@ def test_fp32_per_iteration_equals_one_call(kind):
     rng = np.random.default_rng(seed)
     r2 = [f2.run_numeric_iteration(k, "full", sched.get(k), rng) for k in range(f2.layout.n_blocks)]
     assert [r.locations for r in r1] == [r.locations for r in r2]
-    np.testing.assert_array_equal(f1.m, f2.m)
+    if kind == "cholesky":
+        # the one-call look-ahead applies panels 0..k-2 on a side stream and
+        # panel k-1 on the main stream: a different fp32 summation order
+        scale = float(np.abs(f2.m).max())
+        np.testing.assert_allclose(f1.m, f2.m, rtol=0, atol=1e-5 * scale)
+    else:
+        np.testing.assert_array_equal(f1.m, f2.m)
 
 
 def test_fp32_clean_run_reports_nothing_and_breakdown_raises():
