@@ -391,10 +391,12 @@ int s_lu_l21(abft_sctx* c, int64_t k) {
     fs.bm = c->scratch;
     fs.bm_ld = 1;
   }
+  // in place: sgemm_tc splits A (= the output block) into its workspace
+  // before the tensor-core launch reads anything, so D may alias A
   ABFT_TRY(s_gemm(c, 'N', 'N', n - pe, w, w, 1.0f, D + w, c->ld, c->uinv, c->ld_t, 0.0f, nullptr, 0,
-                  c->lw, c->ld, fuse ? &fs : nullptr));
+                  D + w, c->ld, fuse ? &fs : nullptr));
   c->el_for = fuse ? k : -1;
-  return copy_matrix(c->st, c->lw, c->ld, D + w, c->ld, n - pe, w);
+  return 0;
 }
 
 int s_pd(abft_sctx* c, int64_t k) {
@@ -451,9 +453,9 @@ int s_pu(abft_sctx* c, int64_t k) {
   } else {
     if (pe < n) {
       float* A21 = c->m + pe + p * c->ld;
+      // in place (A is split into the workspace before the launch, as s_lu_l21)
       ABFT_TRY(s_gemm(c, 'N', 'T', n - pe, w, w, 1.0f, A21, c->ld, c->linv, c->ld_t, 0.0f, nullptr, 0,
-                      c->lw, c->ld));
-      ABFT_TRY(copy_matrix(c->st, c->lw, c->ld, A21, c->ld, n - pe, w));
+                      A21, c->ld));
       ABFT_TRY(fill_matrix(c->st, c->m + p + pe * c->ld, c->ld, w, n - pe, 0.0));
     }
     // panel k is final: keep its hi/lo split for the later panel updates
