@@ -566,8 +566,7 @@ __global__ void __launch_bounds__(QT, 1)
         const int v = tid & 31, grp = tid >> 5;
         double acc = 0.0;
         if (v < nv) {
-          double t[19];
-          int cnt = 0;
+          double t[19];  // G <= 152 (148 SMs)
 #pragma unroll
           for (int q2 = 0; q2 < 19; ++q2) {
             const int g2 = grp + 8 * q2;
@@ -575,7 +574,6 @@ __global__ void __launch_bounds__(QT, 1)
           }
 #pragma unroll
           for (int q2 = 0; q2 < 19; ++q2) acc += t[q2];
-          (void)cnt;
         }
         Ws[grp * 32 + v] = acc;  // Ws is free during the column loop
         __syncthreads();
@@ -736,6 +734,7 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     }();
     int G = (int)((nk + rows_t - 1) / rows_t);
     if (G > sms) G = sms;
+    if (G > 152) G = 152;  // the per-column reduction reads 19 x 8 partials
     if ((nk + G - 1) / G <= QR_RMAX && 2LL * G * 32 <= part_elems) {
       static bool attr = false;
       if (!attr) {
