@@ -1040,10 +1040,13 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     int sp;
     int64_t need = 0;
     if (kind == ABFT_CHOLESKY && k > 0) {  // pre-split operands: partials only
-      s_gemm_plan(c->sms, n - p, pe - p, p, S_KCHUNK_CHOL, false, &sp, &need);
-      need = sgemm_partial_elems((int)(n - p), (int)(pe - p), sp) + 128;
-    }
-    else if (kind == ABFT_QR && pe < n)
+      // main-stream updates (all SMs) and the look-ahead's (one SM fewer)
+      for (int cap : {c->sms, c->sms - 1}) {
+        int64_t unused;
+        s_gemm_plan(cap, n - p, pe - p, p, S_KCHUNK_CHOL, false, &sp, &unused);
+        need = std::max(need, sgemm_partial_elems((int)(n - p), (int)(pe - p), sp) + 128);
+      }
+    } else if (kind == ABFT_QR && pe < n)
       s_gemm_plan(c->sms, pe - p, n - pe, n - p, S_KCHUNK, false, &sp, &need);
     c->sws_elems = std::max(c->sws_elems, need);
   }
