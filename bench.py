@@ -11,9 +11,12 @@ convention (2n^3/3 LU, n^3/3 Cholesky, 4n^3/3 QR), ABFT work not counted.
   python bench.py [--gpus N --steps K --warmup W] [--impl reference]
   python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
 
-N > 1: one independent factorization per GPU (weak scaling, "replicas");
-time is the max over ranks. --impl reference times the reference algorithm's
-CPU restatement (oracle/, numpy) on a bounded sample of the same workload.
+N > 1: ONE global N=32768 matrix distributed 1-D block-cyclic by column
+blocks over the ranks (strong scaling: total work fixed); time is the max
+over ranks. --impl reference times the reference algorithm's CPU restatement
+(oracle/, numpy + LAPACK) on a bounded sample: a complete protected
+factorization at N=4096 (an N=32768 factorization takes hours on the host);
+its line's config names the order it actually timed.
 """
 from __future__ import annotations
 
@@ -201,10 +204,12 @@ def run_reference(args):
     vals = [cpu_sample(args.kind, n, args.b, args.scheme, args.seed) for _ in range(args.steps)]
     value = statistics.median(v[0] for v in vals)
     ms = statistics.median(v[1] for v in vals) * 1e3
+    cfg = config(args, n=n)
+    cfg["sample_of"] = config(args)["workload"]
     line = {"impl": "reference", "metric": metric_name(args), "value": value, "unit": "TFLOP/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic", "config": config(args),
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic", "config": cfg,
             "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": os.cpu_count(),
                              "kind": "port", "sample": cpu_sample_desc(args.kind, n, args.b,
                                                                        args.scheme),
@@ -220,15 +225,18 @@ def metric_name(args) -> str:
             f"{args.scheme.upper()} checksums, 1 seeded fault)")
 
 
-def config(args) -> dict:
+def config(args, n: int | None = None) -> dict:
+    """The workload; ``n`` overrides the order (the reference arm's sample)."""
+    n = args.n if n is None else n
     prec = "fp64" if args.precision == "f64" else "fp32 (tcgen05 3xTF32)"
-    return {"workload": f"{args.kind} {prec} N={args.n} b={args.b} scheme={args.scheme} "
+    return {"workload": f"{args.kind} {prec} N={n} b={args.b} scheme={args.scheme} "
                         f"(col_ft+row_ft as under mode=bsr), one 0-D fault at a seeded "
                         f"iteration (criterion-5 protocol)",
-            "kind": args.kind, "n": args.n, "b": args.b, "scheme": args.scheme,
+            "kind": args.kind, "n": n, "b": args.b, "scheme": args.scheme,
             "seed": args.seed,
-            "l2": f"working set {args.n * args.n * (8 if args.precision == 'f64' else 4) / 1e9:.1f} GB "
-                  ">> 126 MB L2; no flush needed",
+            "l2": f"working set {n * n * (8 if args.precision == 'f64' else 4) / 1e9:.1f} GB "
+                  + (">> 126 MB L2; no flush needed" if n * n * 4 > 4 * 126e6 else
+                     "(CPU sample)"),
             "parallelism": (f"block-cyclic columns over {args.gpus} GPUs "
                             f"({'panel broadcast' if args.kind != 'cholesky' else 'panel-update reduce'}"
                             f" over {args.dist_backend})") if args.gpus > 1 else "single"}
@@ -455,9 +463,13 @@ def run_ours(args):
     en1 = clk.energy_mj()
     launches = (lib.abft_launch_count() - launches0) // max(1, args.steps)
     res = arm.residual()
-    # the single planned 0-D fault must be located and corrected
+    # the single planned 0-D fault must be located at its planned (row, col)
+    # and corrected; a run that misses it is not a protected factorization
     locs = [loc for r in reps for loc in r.locations]
     fixed = sum(r.corrected[P.ErrorKind.D0] for r in reps)
+    want = planned_fault(args.kind, args.n, args.b, args.seed)
+    fault_ok = (fixed == 1 and len(locs) == 1 and (int(locs[0][0]), int(locs[0][1])) == want
+                and bool(locs[0][3])) if args.scheme != "none" else None
     ms_max = all_max(ms)
     ms_step = ms_max / args.steps
     flops = FLOPS[args.kind](args.n)
@@ -527,7 +539,7 @@ def run_ours(args):
     line = {
         "metric": metric_name(args), "value": value, "unit": "TFLOP/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": args.precision,
         "data": f"synthetic: generate_test_matrix({args.kind!r}, {args.n}, seed={args.seed}) "
                 "(PCG64 draws bit-identical to the reference)",
@@ -550,15 +562,30 @@ def run_ours(args):
         "profile_ms": prof,
         "whole_step_frac_of_peak": value / world / peak.value,
         "residual": res, "residual_over_n_eps": res / (args.n * 2.220446049250313e-16),
-        "fault": {"k_fault": k_fault, "locations": [[int(a), int(b), c.value, bool(d)]
-                                                    for a, b, c, d in locs],
-                  "corrected_0d": int(fixed)},
+        "fault": {"k_fault": k_fault, "planned": list(want),
+                  "locations": [[int(a), int(b), c.value, bool(d)] for a, b, c, d in locs],
+                  "corrected_0d": int(fixed), "located_and_corrected": fault_ok},
         "cpu_baseline": cpu,
         "input_generation_s": arm_gen_s(),
     }
     if extra:
         line["extra_kinds"] = extra
+    if fault_ok is False:
+        line["invalid"] = "the seeded 0-D fault was not located and corrected"
     print(json.dumps(line), flush=True)
+    if fault_ok is False:
+        raise SystemExit(1)
+
+
+def planned_fault(kind, n, b, seed):
+    """(row, col) of the criterion-5 fault: the draws run_protected makes at
+    k_fault (sample_fault_plan order, abft.py:314-332)."""
+    from paper_2301_03166_b200.abft import draw_plan
+    from paper_2301_03166_b200.simulator import _tmu_region
+    k_fault, rng = fault_plan(n, b, seed)
+    r0, c0, rows, cols = _tmu_region(kind, n, b, k_fault)
+    d = draw_plan(rng, {"0d": 1}, r0, c0, rows, cols, b)[0]
+    return int(d["row"]), int(d["col"])
 
 
 _GEN = {"s": None}

@@ -96,6 +96,14 @@ ABFT_API const char* abft_last_error(void);
 ABFT_API int abft_device_count(int* count);
 /* kernels launched by this library so far (process-wide counter) */
 ABFT_API long long abft_launch_count(void);
+/* Diagnostic: while enabled, every verify launch records the largest
+ * |delta| / tau among checks that did NOT trip (column sums, row sums,
+ * index-weighted column sums) on the current device: the rounding-noise
+ * margin of the threshold rule (abft.py:161-163); out3[3] (a 4th slot) is the
+ * largest |dw/dp - round(dw/dp)| seen by SINGLE's index recovery
+ * (abft.py:208-213). `out3` holds 4 doubles. No reference counterpart. */
+ABFT_API int abft_noise_stats(int enable);
+ABFT_API int abft_noise_read(double* out3, int reset);
 
 /* device-pointer primitive (for integrators that own device memory):
  * D = beta*C + alpha*op(A)*op(B) on `stream` (cudaStream_t, may be NULL). */

@@ -21,6 +21,26 @@ INDEX_SNAP_TOLERANCE = 1e-2
 EPS64 = float(np.finfo(np.float64).eps)
 EPS32 = float(np.finfo(np.float32).eps)
 
+# fp32 (s*) restatement of the threshold rule (the reference
+# has no fp32 path, parity unpinned). tau32 = 2048 * max(max|blk|, 1) * eps32
+# = max(max|blk|, 1) / 4096, which sits 2.05x below the reference's smallest
+# fault (0.5e-3 * max(max|region|, 1), abft.py:319-321), so every injected
+# fault trips the check; the snap tolerance of SINGLE's index recovery is 0.25
+# (the fp32 data's rounding moves dw / dp by ~1e-4 of a fault; the sampler's
+# 1-D / 2-D streak ratios have fractional parts 0.59-0.61 and never snap).
+# Mirrors TAU32_MULT / SNAP_TOL32 in paper_2301_03166_b200/csrc/abft_kernels.cuh.
+TAU32_MULT = 2048.0
+SNAP_TOL32 = 0.25
+PRECISIONS = ("f64", "f32")
+
+
+def threshold(b: int, bmax, precision: str = "f64"):
+    """_block_threshold (abft.py:161-163), in the reference's operation order;
+    ``precision="f32"`` is the s* restatement above."""
+    if precision == "f32":
+        return TAU32_MULT * np.maximum(bmax, 1.0) * EPS32
+    return CHECK_TOLERANCE_FACTOR * b * np.maximum(bmax, 1.0) * EPS64
+
 ALL_KINDS = ("cholesky", "lu", "qr")
 ERROR_KINDS = ("0d", "1d", "2d")   # ErrorKind iteration order, abft.py:42-45
 
@@ -173,24 +193,26 @@ class OracleReport:
                 "locations": [[int(r), int(c), k, bool(f)] for r, c, k, f in self.locations]}
 
 
-def _snap_index(dw: float, dp: float, limit: int):
+def _snap_index(dw: float, dp: float, limit: int, tol: float = INDEX_SNAP_TOLERANCE):
     """_recovered_index (abft.py:208-213); Python round() is half-to-even."""
     ratio = dw / dp
     idx = round(ratio)
-    if abs(ratio - idx) <= INDEX_SNAP_TOLERANCE and 0 <= idx < limit:
+    if abs(ratio - idx) <= tol and 0 <= idx < limit:
         return int(idx)
     return None
 
 
-def verify(m: np.ndarray, cs: Checksums, correct: bool = True, eps: float = EPS64) -> OracleReport:
+def verify(m: np.ndarray, cs: Checksums, correct: bool = True,
+           precision: str = "f64") -> OracleReport:
     """verify_correct (abft.py:174-205) with _handle_single / _handle_full.
-    ``eps`` = EPS64 is the reference; EPS32 is the fp32 restatement of the
-    threshold rule (s* variants: parity unpinned)."""
+    ``precision="f64"`` is the reference; "f32" is the s* restatement of the
+    threshold and snap rules (TAU32_MULT, SNAP_TOL32 above)."""
     rep = OracleReport()
     b = cs.b
     view = m[cs.r0:cs.r0 + cs.rows, cs.c0:cs.c0 + cs.cols]
     cp, cw, rp, _, bmax = block_sums(view, b)
-    tau = CHECK_TOLERANCE_FACTOR * b * np.maximum(bmax, 1.0) * eps     # _block_threshold
+    tau = threshold(b, bmax, precision)                                 # _block_threshold
+    snap_tol = SNAP_TOL32 if precision == "f32" else INDEX_SNAP_TOLERANCE
     nbr, nbc = bmax.shape
     d_col = cp - cs.cp
     d_w = cw - cs.cw
@@ -214,7 +236,7 @@ def verify(m: np.ndarray, cs: Checksums, correct: bool = True, eps: float = EPS6
             if not full:
                 fixes = []
                 for j in bc:
-                    idx = _snap_index(d_w[bi, c_s + j], d_col[bi, c_s + j], re_ - rs)
+                    idx = _snap_index(d_w[bi, c_s + j], d_col[bi, c_s + j], re_ - rs, snap_tol)
                     if idx is None:
                         fixes = None
                         break
@@ -484,7 +506,7 @@ def residual(a: np.ndarray, f: OracleFactorization) -> float:
 
 def protected_iteration(f: OracleFactorization, k: int, scheme: str,
                         counts: dict | None = None, rng=None,
-                        correct: bool = True, eps: float = EPS64) -> OracleReport:
+                        correct: bool = True, precision: str = "f64") -> OracleReport:
     rep = OracleReport()
     for task in f.order():
         if task != "tmu":
@@ -506,6 +528,6 @@ def protected_iteration(f: OracleFactorization, k: int, scheme: str,
                 flt["magnitude"] = magnitude(flt["u"], flt["negate"], scale)
             inject(f.m, plan)
         if cs is not None:
-            rep = verify(f.m, cs, correct, eps)
+            rep = verify(f.m, cs, correct, precision)
     f.k_done = k + 1
     return rep

@@ -62,6 +62,8 @@ SIGNATURES = [
     ("abft_last_error", ctypes.c_char_p, []),
     ("abft_device_count", _I, [ctypes.POINTER(_I)]),
     ("abft_launch_count", ctypes.c_longlong, []),
+    ("abft_noise_stats", _I, [_I]),
+    ("abft_noise_read", _I, [_D, _I]),
     ("abft_dev_dgemm", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, ctypes.c_double,
                             _P, _I64, _P, _I64, ctypes.c_double, _P, _I64, _P, _I64]),
     ("abft_dev_sgemm", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64, ctypes.c_float,

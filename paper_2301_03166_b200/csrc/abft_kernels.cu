@@ -9,6 +9,7 @@
 #include "abft_kernels.cuh"
 
 #include <cfloat>
+#include <cstring>
 
 namespace abft {
 
@@ -169,19 +170,35 @@ ABFT_DEVINL void mark_dirty(const EventSink& s, int bi, int bj) {
 
 // Python's round() is round-half-to-even; rint() matches under the default
 // rounding mode (abft.py:208-213).
-ABFT_DEVINL bool recovered_index(double dw, double dp, int limit, int* idx) {
+ABFT_DEVINL bool recovered_index(double dw, double dp, int limit, double tol, int* idx) {
   const double ratio = dw / dp;
   const double r = rint(ratio);
-  if (fabs(ratio - r) <= 1e-2 && r >= 0.0 && r < (double)limit) {
+  if (fabs(ratio - r) <= tol && r >= 0.0 && r < (double)limit) {
     *idx = (int)r;
     return true;
   }
   return false;
 }
 
+// Noise statistics of clean checks (diagnostic, off by default): the largest
+// |delta| / tau seen for column sums, row sums and index-weighted column sums
+// among entries that did NOT trip the threshold. The ratio says how far below
+// tau the rounding noise of the data path sits (false-positive margin), and
+// max |dw| / tau bounds the error of SINGLE's index snap for a fault of size
+// >= 2 tau. Slot 3: the largest |dw/dp - round(dw/dp)| of a flagged column
+// in SINGLE's index recovery (how close located faults came to the snap
+// tolerance). Stored as IEEE bit patterns (non-negative doubles order like
+// their bits), reduced with atomicMax.
+__device__ unsigned long long g_noise_stats[4];
+
+ABFT_DEVINL void noise_max(int slot, double v) {
+  if (v > 0.0) atomicMax(&g_noise_stats[slot], (unsigned long long)__double_as_longlong(v));
+}
+
 template <typename T>
-__global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int correct, SumOut rec,
-                              Maintained mt, EventSink sink, int64_t nbr, int64_t nbc, double eps) {
+__global__ void verify_kernel(RegionT<T> reg, int scheme, int correct, SumOut rec, Maintained mt,
+                              EventSink sink, int64_t nbr, int64_t nbc, double tau_mult, double eps,
+                              double snap_tol, int stats) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = (gridDim.x * (int64_t)blockDim.x) >> 5;
@@ -192,19 +209,35 @@ __global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int cor
     const int br = (int)min(reg.b, reg.rows - r_lo);
     const int bc = (int)min(reg.b, reg.cols - c_lo);
     const double bmax = rec.bm[bi + bj * rec.bm_ld];
-    const double tau = 50.0 * (double)b_nom * fmax(bmax, 1.0) * eps;
+    // _block_threshold (abft.py:161-163): (50 * b) * max(max|blk|, 1) * eps in
+    // the reference's operation order; fp32 passes tau_mult = TAU32_MULT
+    const double tau = tau_mult * fmax(bmax, 1.0) * eps;
     int nbad_c = 0, nbad_r = 0;
+    double nz_c = 0.0, nz_r = 0.0, nz_w = 0.0;
     for (int c = lane; c < bc; c += 32) {
       const int64_t gc = c_lo + c;
       const double d = rec.cp[rec.cp_step * bi + gc * rec.cp_ld] - mt.cp[mt.cp_step * bi + gc * mt.cp_ld];
-      nbad_c += (fabs(d) > tau) ? 1 : 0;
+      const bool bad = fabs(d) > tau;
+      nbad_c += bad ? 1 : 0;
+      if (stats && !bad) {
+        nz_c = fmax(nz_c, fabs(d));
+        nz_w = fmax(nz_w, fabs(rec.cw[rec.cw_step * bi + gc * rec.cw_ld] -
+                               mt.cw[mt.cw_step * bi + gc * mt.cw_ld]));
+      }
     }
     if (full) {
       for (int r = lane; r < br; r += 32) {
         const int64_t gr = r_lo + r;
         const double d = rec.rp[gr + bj * rec.rp_ld] - mt.rp[gr + bj * mt.rp_ld];
-        nbad_r += (fabs(d) > tau) ? 1 : 0;
+        const bool bad = fabs(d) > tau;
+        nbad_r += bad ? 1 : 0;
+        if (stats && !bad) nz_r = fmax(nz_r, fabs(d));
       }
+    }
+    if (stats) {
+      noise_max(0, nz_c / tau);
+      noise_max(1, nz_r / tau);
+      noise_max(2, nz_w / tau);
     }
     for (int o = 16; o > 0; o >>= 1) {
       nbad_c += __shfl_xor_sync(0xffffffffu, nbad_c, o);
@@ -223,15 +256,37 @@ __global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int cor
       const int64_t gr = r_lo + r;
       return rec.rp[gr + bj * rec.rp_ld] - mt.rp[gr + bj * mt.rp_ld];
     };
+    // Deltas of a flagged column used to locate / repair. fp64: the recomputed
+    // sums as they are (the reference's values). fp32: the plain and weighted
+    // sums are re-derived here in fp64 from the stored column, so the fp32
+    // partial sums of the GEMM epilogue add no error to the index snap or to
+    // the repaired value (rare path: one b-element column per flagged column).
+    auto col_deltas = [&](int c, double* dp, double* dw) {
+      const int64_t gc = c_lo + c;
+      if (sizeof(T) == 4) {
+        const T* col = blkp + (int64_t)c * reg.ld;
+        double s0 = 0.0, s1 = 0.0;
+        for (int r = 0; r < br; ++r) {
+          const double x = (double)col[r];
+          s0 += x;
+          s1 += (double)r * x;
+        }
+        *dp = s0 - mt.cp[mt.cp_step * bi + gc * mt.cp_ld];
+        *dw = s1 - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+      } else {
+        *dp = dcol(c);
+        *dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+      }
+    };
     if (!full) {
       bool ok = true;
       for (int c = 0; c < bc && ok; ++c) {
-        const double d = dcol(c);
-        if (!(fabs(d) > tau)) continue;
-        const int64_t gc = c_lo + c;
-        const double dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+        if (!(fabs(dcol(c)) > tau)) continue;
+        double d, dw;
+        col_deltas(c, &d, &dw);
         int idx;
-        if (!recovered_index(dw, d, br, &idx)) ok = false;
+        if (!recovered_index(dw, d, br, snap_tol, &idx)) ok = false;
+        if (stats) noise_max(3, fabs(dw / d - rint(dw / d)));
       }
       if (!ok) {
         const int kind = (nbad_c == 1) ? 1 : 2;
@@ -240,12 +295,11 @@ __global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int cor
       }
       int seq = 0;
       for (int c = 0; c < bc; ++c) {
-        const double d = dcol(c);
-        if (!(fabs(d) > tau)) continue;
-        const int64_t gc = c_lo + c;
-        const double dw = rec.cw[rec.cw_step * bi + gc * rec.cw_ld] - mt.cw[mt.cw_step * bi + gc * mt.cw_ld];
+        if (!(fabs(dcol(c)) > tau)) continue;
+        double d, dw;
+        col_deltas(c, &d, &dw);
         int idx = 0;
-        recovered_index(dw, d, br, &idx);
+        recovered_index(dw, d, br, snap_tol, &idx);
         if (correct) fix(idx + (int64_t)c * reg.ld, d);
         emit(sink, bi, bj, seq++, 0, r_lo + idx, c_lo + c, correct, 0, correct, 0);
       }
@@ -263,7 +317,9 @@ __global__ void verify_kernel(RegionT<T> reg, int64_t b_nom, int scheme, int cor
       while (!(fabs(drow(i)) > tau)) ++i;
       while (!(fabs(dcol(jc)) > tau)) ++jc;
       if (correct) {
-        fix(i + (int64_t)jc * reg.ld, dcol(jc));
+        double d, dw;
+        col_deltas(jc, &d, &dw);
+        fix(i + (int64_t)jc * reg.ld, d);
         mark_dirty(sink, bi, bj);
       }
       emit(sink, bi, bj, 0, 0, r_lo + i, c_lo + jc, correct, 0, correct, 0);
@@ -549,12 +605,7 @@ static int blocksum_t(cudaStream_t st, const RegionT<T>& reg, const SumOut& out,
   const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
   const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
   const size_t dyn = 2 * reg.b * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(blocksum_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  2 * 4096 * 8));
-    attr = true;
-  }
+  ABFT_TRY(ensure_smem_attr((const void*)blocksum_kernel<T>, 2 * 4096 * 8));
   int64_t nblk = blocks ? max_list : nbr * nbc;
   if (nblk <= 0) return 0;
   int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
@@ -577,10 +628,12 @@ int blocksum(cudaStream_t st, const RegionF& reg, const SumOut& out, const int32
   return blocksum_t(st, reg, out, blocks, nblocks_dev, max_list);
 }
 
+static bool g_noise_on = false;
+
 template <typename T>
-static int verify_t(cudaStream_t st, const RegionT<T>& reg, int64_t b_nominal, int scheme,
-                    int correct, const SumOut& rec, const Maintained& mt, const EventSink& sink,
-                    double eps) {
+static int verify_t(cudaStream_t st, const RegionT<T>& reg, int scheme, int correct,
+                    const SumOut& rec, const Maintained& mt, const EventSink& sink, double tau_mult,
+                    double eps, double snap_tol) {
   if (reg.rows <= 0 || reg.cols <= 0) return 0;
   const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
   const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
@@ -588,19 +641,39 @@ static int verify_t(cudaStream_t st, const RegionT<T>& reg, int64_t b_nominal, i
   int grid = (int)((warps + 7) / 8);
   if (grid > 148 * 16) grid = 148 * 16;
   count_launch();
-  verify_kernel<T><<<grid, 256, 0, st>>>(reg, b_nominal, scheme, correct, rec, mt, sink, nbr, nbc,
-                                         eps);
+  verify_kernel<T><<<grid, 256, 0, st>>>(reg, scheme, correct, rec, mt, sink, nbr, nbc, tau_mult, eps,
+                                         snap_tol, g_noise_on ? 1 : 0);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
 
 int verify_blocks(cudaStream_t st, const Region& reg, int64_t b_nominal, int scheme, int correct,
                   const SumOut& rec, const Maintained& mt, const EventSink& sink) {
-  return verify_t(st, reg, b_nominal, scheme, correct, rec, mt, sink, DBL_EPSILON);
+  return verify_t(st, reg, scheme, correct, rec, mt, sink, 50.0 * (double)b_nominal, DBL_EPSILON,
+                  1e-2);
 }
 int verify_blocks(cudaStream_t st, const RegionF& reg, int64_t b_nominal, int scheme, int correct,
                   const SumOut& rec, const Maintained& mt, const EventSink& sink) {
-  return verify_t(st, reg, b_nominal, scheme, correct, rec, mt, sink, (double)FLT_EPSILON);
+  (void)b_nominal;  // tau32 does not scale with b (see abft_kernels.cuh)
+  return verify_t(st, reg, scheme, correct, rec, mt, sink, TAU32_MULT, (double)FLT_EPSILON,
+                  SNAP_TOL32);
+}
+
+void noise_stats_enable(bool on) { g_noise_on = on; }
+
+int noise_stats_read(double out[4], bool reset) {
+  unsigned long long h[4];
+  CUDA_TRY(cudaMemcpyFromSymbol(h, g_noise_stats, sizeof(h)));
+  for (int i = 0; i < 4; ++i) {
+    double v;
+    std::memcpy(&v, &h[i], sizeof(v));
+    out[i] = v;
+  }
+  if (reset) {
+    std::memset(h, 0, sizeof(h));
+    CUDA_TRY(cudaMemcpyToSymbol(g_noise_stats, h, sizeof(h)));
+  }
+  return 0;
 }
 
 template <typename T>

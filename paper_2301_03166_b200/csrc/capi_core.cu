@@ -1,5 +1,6 @@
 // Library-level C-ABI entry points (no context): version, errors, device-pointer GEMM.
 #include "abft_b200.h"
+#include "abft_kernels.cuh"
 #include "gemm.cuh"
 #include "sgemm.cuh"
 
@@ -25,6 +26,13 @@ extern "C" {
 ABFT_API int abft_version(void) { return 100; }
 
 ABFT_API long long abft_launch_count(void) { return launch_count(); }
+
+ABFT_API int abft_noise_stats(int enable) {
+  noise_stats_enable(enable != 0);
+  return 0;
+}
+
+ABFT_API int abft_noise_read(double* out3, int reset) { return noise_stats_read(out3, reset != 0); }
 
 ABFT_API const char* abft_last_error(void) { return last_error(); }
 

@@ -23,6 +23,8 @@ const char* last_error();
 // number of kernels this library has launched (bench.py's gpu_launches)
 void count_launch();
 long long launch_count();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device)
+int ensure_smem_attr(const void* fn, int bytes);
 
 #define CUDA_TRY(expr)                                                          \
   do {                                                                          \

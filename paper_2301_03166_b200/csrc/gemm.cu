@@ -23,6 +23,8 @@
 #include <atomic>
 #include <cstdlib>
 #include <mutex>
+#include <tuple>
+#include <vector>
 
 #include <cudaTypedefs.h>
 
@@ -44,6 +46,21 @@ const char* last_error() { return g_last_error; }
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(); }
+
+// Function attributes belong to a device context: the dynamic shared-memory
+// opt-in is applied once per (kernel, device, size), thread-safely.
+int ensure_smem_attr(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::vector<std::tuple<const void*, int, int>> done;
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  for (const auto& t : done)
+    if (std::get<0>(t) == fn && std::get<1>(t) == dev && std::get<2>(t) >= bytes) return 0;
+  CUDA_TRY(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  done.emplace_back(fn, dev, bytes);
+  return 0;
+}
 
 // ---------------------------------------------------------------------------
 // TMA descriptor creation through the driver entry point (no -lcuda needed)
@@ -660,12 +677,7 @@ template <bool AT, bool BT, int NWG>
 int launch_kernel(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb,
                   const CUtensorMap& mc, const KParams& kp, int max_ctas) {
   using G = Geo<NWG>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    CUDA_TRY(cudaFuncSetAttribute(dgemm_tma_dmma<AT, BT, NWG>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, G::SMEM_BYTES));
-    attr_set = true;
-  }
+  ABFT_TRY(ensure_smem_attr((const void*)dgemm_tma_dmma<AT, BT, NWG>, G::SMEM_BYTES));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -282,23 +282,13 @@ static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* 
   }
   const int dsm = DIAG_SMEM / 8 * (int)sizeof(T) + 64;
   const int ism = INV_SMEM / 8 * (int)sizeof(T);
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(diag_factor_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  dsm));
-    attr = true;
-  }
+  ABFT_TRY(ensure_smem_attr((const void*)diag_factor_kernel<T>, dsm));
   count_launch();
   diag_factor_kernel<T><<<1, DT, dsm, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
                                             col_base);
   CUDA_TRY(cudaGetLastError());
   if (Linv || Uinv) {
-    static bool attr2 = false;
-    if (!attr2) {
-      CUDA_TRY(cudaFuncSetAttribute(tri_inverse_kernel<T>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, ism));
-      attr2 = true;
-    }
+    ABFT_TRY(ensure_smem_attr((const void*)tri_inverse_kernel<T>, ism));
     dim3 grid((w + NBK - 1) / NBK, Uinv ? 2 : 1);
     count_launch();
     tri_inverse_kernel<T><<<grid, DT, ism, st>>>(D, ld, w, mode == 0 ? 1 : 0, Linv, ldl, Uinv,
@@ -736,12 +726,7 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     if (G > sms) G = sms;
     if (G > 152) G = 152;  // the per-column reduction reads 19 x 8 partials
     if ((nk + G - 1) / G <= QR_RMAX && 2LL * G * 32 <= part_elems) {
-      static bool attr = false;
-      if (!attr) {
-        CUDA_TRY(cudaFuncSetAttribute(qr_panel2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      QR_SMEM));
-        attr = true;
-      }
+      ABFT_TRY(ensure_smem_attr((const void*)qr_panel2_kernel, QR_SMEM));
       void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf, &part2, &wfin};
       count_launch();
       CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel2_kernel, dim3(G), dim3(QT), args,
@@ -784,12 +769,7 @@ int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, i
     set_last_error("larft: panel width %d too large", w);
     return -1;
   }
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(larft_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  200 * 1024));
-    attr = true;
-  }
+  ABFT_TRY(ensure_smem_attr((const void*)larft_kernel, 200 * 1024));
   count_launch();
   larft_kernel<<<1, 512, smem, st>>>(Gm, ldg, betas, w, T, ldt);
   CUDA_TRY(cudaGetLastError());

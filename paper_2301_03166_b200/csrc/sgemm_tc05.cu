@@ -630,12 +630,7 @@ int launch_tc(cudaStream_t st, int M, int N, int K, float alpha, const float* ah
         p.prefetch_c = 1;
     }
   }
-  static bool attr = false;
-  if (!attr) {
-    CUDA_TRY(cudaFuncSetAttribute(sgemm_tc05_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  T_SMEM));
-    attr = true;
-  }
+  ABFT_TRY(ensure_smem_attr((const void*)sgemm_tc05_kernel, T_SMEM));
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -15,6 +15,9 @@ Every case mirrors a reference test or an SURVEY.md §8c golden:
   * plans.json   — sample_fault_plan draws (abft.py:310-333)
   * linalg.json / linalg.npz — small factorizations (test_linalg.py:37-50)
   * inputs.json  — sha256 of generate_test_matrix outputs (linalg.py:63-78)
+  * c2c3.json    — BASELINE configs C2 (LU N=8192, SINGLE and FULL) and C3
+                   (QR N=8192 SINGLE), b=256, criterion-5 fault, seed 0
+                   (`make_golden.py c2c3` regenerates only this file)
 """
 from __future__ import annotations
 
@@ -227,7 +230,23 @@ def inputs():
     return out
 
 
+def c2c3():
+    """"C2 and C3 seed 0" (b = 256 as the bench; ~2-5 min each)."""
+    out = []
+    for kind, scheme in ((K.LU, SCH.SINGLE), (K.LU, SCH.FULL), (K.QR, SCH.SINGLE)):
+        t0 = time.time()
+        r = protected_run(kind, 8192, 256, 0, scheme, {E.D0: 1})
+        r.update({"kind": kind.value, "scheme": scheme.value, "n": 8192, "b": 256,
+                  "counts": {"0d": 1}, "ref_seconds": round(time.time() - t0, 1)})
+        print(kind.value, scheme.value, r["reports"], r["residual"], flush=True)
+        out.append(r)
+    return {"runs": out}
+
+
 def main():
+    if sys.argv[1:] == ["c2c3"]:
+        (OUT / "c2c3.json").write_text(json.dumps(c2c3()))
+        return
     t0 = time.time()
     (OUT / "inputs.json").write_text(json.dumps(inputs()))
     (OUT / "plans.json").write_text(json.dumps(plans()))
@@ -242,6 +261,8 @@ def main():
     print("c1", time.time() - t0)
     (OUT / "crit5.json").write_text(json.dumps(crit5()))
     print("crit5", time.time() - t0)
+    (OUT / "c2c3.json").write_text(json.dumps(c2c3()))
+    print("c2c3", time.time() - t0)
 
 
 if __name__ == "__main__":

@@ -1,60 +1,118 @@
 """GPU: the fp32 (s*) factorizations on the tcgen05 path.
 
-The reference is fp64-only (parity unpinned); the fp32 run
+The reference is fp64-only (parity unpinned). The fp32 rule
+(oracle precision "f32", csrc/abft_kernels.cuh): tau32 = max(max|blk|, 1) /
+4096, 2.05x below the reference's smallest fault (0.5e-3 * max|region|,
+abft.py:319-321), and a 0.25 index-snap tolerance for SINGLE. The fp32 run
 must (a) reconstruct A to fp32 accuracy (residual <= 64 * n * eps32 stated
-bound; typically ~1e-7), and (b) report exactly the fault locations of the
-oracle restated for fp32 (same algorithm, tau on eps32). The reference's
-fault magnitude (u * 1e-3 * max|region|) can sit within 2x of tau32 in the
-dominant diagonal blocks, where fp32 rounding decides detection; the test
-uses the first seed whose oracle outcome is identical for tau32 / 2 and
-2 * tau32, so every compared decision has a margin of 2x.
+bound; typically ~1e-7), (b) report exactly the fault locations of the
+oracle under that rule on every seed (no seed selection), and (c) locate
+and correct every injected 0-D fault (detection-rate test below).
 """
+import copy
+
 import numpy as np
 import pytest
 
 import oracle as O
 import paper_2301_03166_b200 as P
+from paper_2301_03166_b200.abft import draw_plan
+from paper_2301_03166_b200.simulator import _tmu_region
 
 pytestmark = pytest.mark.gpu
 EPS32 = float(np.finfo(np.float32).eps)
+
+
+def _oracle32(kind, a, b, scheme, sched, seed):
+    fo = O.OracleFactorization(kind, a, b)
+    rng = np.random.default_rng(seed)
+    return [O.protected_iteration(fo, k, scheme, sched.get(k), rng, precision="f32").locations
+            for k in range(fo.nb)]
+
+
+def _block_corner(r0, c0, b, row, col):
+    return r0 + (row - r0) // b * b, c0 + (col - c0) // b * b
+
+
+def _same_outcome(kind, scheme, got, ref, regions, b):
+    """Exact equality, except the one documented fp32 precision limit:
+    QR under SINGLE may report a 0-D fault the fp64-data oracle corrects as
+    an uncorrectable 1-D event of the SAME block (the index snap of
+    abft.py:208-213 misses; see test_fp32_every_seeded_fault_...)."""
+    if got == ref:
+        return True
+    if not (kind == "qr" and scheme == "single"):
+        return False
+    for k, (g, r) in enumerate(zip(got, ref)):
+        if g == r:
+            continue
+        if len(g) != len(r):
+            return False
+        for eg, er in zip(g, r):
+            if eg == er:
+                continue
+            r0, c0 = regions[k][:2]
+            if not (er[2] == "0d" and er[3] and eg == (*_block_corner(r0, c0, b, er[0], er[1]),
+                                                        "1d", False)):
+                return False
+    return True
 
 
 @pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
 @pytest.mark.parametrize("n,b", [(512, 128), (1000, 128), (768, 64), (700, 50)])
 @pytest.mark.parametrize("scheme", ["full", "single"])
 def test_fp32_fault_locations_match_fp32_oracle(kind, n, b, scheme):
-    if kind == "qr" and scheme == "single":
-        # SINGLE locates a 0-D fault by snapping dw/dp to an index within 1e-2
-        # (abft.py:208-213); with QR's O(sqrt(n)) entries the fp32 rounding of
-        # the data moves that ratio by more than 1e-2 for the smaller sampled
-        # faults, so the fp32 outcome is not a function of the fp64 one.
-        pytest.skip("fp32 SINGLE index recovery is below the snap precision for QR")
     nb = -(-n // b)
     sched = {1: {"0d": 1}, 2: {"0d": 2}, nb - 2: {"1d": 1}}
-
-    def oracle(seed, eps):
+    regions = [_tmu_region(kind, n, b, k) for k in range(nb)]
+    for seed in (5, 6, 7):
         a = O.generate_test_matrix(kind, n, seed)
-        fo = O.OracleFactorization(kind, a, b)
-        rng = np.random.default_rng(seed)
-        return [O.protected_iteration(fo, k, scheme, sched.get(k), rng, eps=eps).locations
-                for k in range(nb)], fo, a
+        ref = _oracle32(kind, a, b, scheme, sched, seed)
+        assert sum(len(x) for x in ref) > 0
+        f = P.SFactorization(kind, a, b)
+        reps = f.run_protected(scheme, sched, np.random.default_rng(seed))
+        got = [[(r, c, kk.value, fl) for r, c, kk, fl in rep.locations] for rep in reps]
+        assert _same_outcome(kind, scheme, got, ref, regions, b), (seed, got, ref)
+        res = f.residual(a)
+        if got == ref:
+            assert res <= 64 * n * EPS32, res
 
-    for seed in range(5, 40):
-        lo, _, _ = oracle(seed, EPS32 / 2)
-        hi, _, _ = oracle(seed, EPS32 * 2)
-        ref, fo, a = oracle(seed, EPS32)
-        if lo == ref == hi:
-            break
-    else:
-        pytest.skip("no seed with a 2x detection margin")
-    assert sum(len(x) for x in ref) > 0
-    f = P.SFactorization(kind, a, b)
-    reps = f.run_protected(scheme, sched, np.random.default_rng(seed))
-    for k in range(nb):
-        got = [(r, c, kk.value, fl) for r, c, kk, fl in reps[k].locations]
-        assert got == ref[k], (seed, k, got, ref[k])
-    res = f.residual(a)
-    assert res <= 64 * n * EPS32, res
+
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
+@pytest.mark.parametrize("scheme", ["full", "single"])
+def test_fp32_every_seeded_fault_located_and_corrected(kind, scheme):
+    """Criterion-5 protocol (pkg/tests/test_acceptance.py:221-224) in fp32:
+    80 seeds, one 0-D fault of the reference's magnitude at a seeded
+    iteration. Every fault is detected (the round-1 rule on eps32 missed the
+    smaller ones). FULL locates by the bad row x bad column and corrects
+    100%; SINGLE locates by snapping dw/dp to an integer within 0.25 — fp32
+    data moves that ratio by (sum_i (i - idx) e_i) / fault, and for QR's
+    O(1) trailing entries the tensor cores' truncating fp32 accumulation
+    pushes it past 0.25 for ~1.7% of faults (profiles/noise_r02.md: 295/300,
+    misses at 0.25-0.34; 1-D streak ratios sit >= 0.39 from an integer, so
+    the tolerance cannot grow). Such a fault is reported as an uncorrectable
+    1-D event of its own block (the recovery policy recomputes) — never as
+    a repair of the wrong element."""
+    n, b = 1536, 128
+    nb = -(-n // b)
+    misses = []
+    runs = 0
+    for seed in range(80):
+        a = P.generate_test_matrix(kind, n, seed)
+        rng = np.random.default_rng(seed)
+        k_fault = int(rng.integers(0, nb - 1))
+        r0, c0, rows, cols = _tmu_region(kind, n, b, k_fault)
+        d = draw_plan(copy.deepcopy(rng), {"0d": 1}, r0, c0, rows, cols, b)[0]
+        f = P.SFactorization(kind, a, b)
+        reps = f.run_protected(scheme, {k_fault: {"0d": 1}}, rng)
+        locs = [(r, c, kk.value, fl) for rep in reps for r, c, kk, fl in rep.locations]
+        runs += 1
+        if locs != [(d["row"], d["col"], "0d", True)]:
+            misses.append((seed, k_fault, (d["row"], d["col"]), locs[:3]))
+            assert kind == "qr" and scheme == "single", misses
+            # detected, in its own block, flagged (not mis-corrected)
+            assert locs == [(*_block_corner(r0, c0, b, d["row"], d["col"]), "1d", False)], misses
+    assert len(misses) <= 0.05 * runs, misses
 
 
 @pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
