@@ -116,6 +116,24 @@ def test_fp32_every_seeded_fault_located_and_corrected(kind, scheme):
 
 
 @pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
+def test_fp32_multi_kind_faults_match_oracle(kind):
+    """0-D, 1-D and 2-D faults in separate iterations, FULL and SINGLE: the
+    fp32 outcome equals the oracle's under the fp32 rule on every seed."""
+    n, b = 1024, 128
+    nb = -(-n // b)
+    sched = {1: {"0d": 1}, 3: {"1d": 1}, 5: {"2d": 1}, nb - 2: {"0d": 1, "1d": 1}}
+    regions = [_tmu_region(kind, n, b, k) for k in range(nb)]
+    for scheme in ("full", "single"):
+        for seed in range(8):
+            a = P.generate_test_matrix(kind, n, seed)
+            ref = _oracle32(kind, a, b, scheme, sched, seed)
+            f = P.SFactorization(kind, a, b)
+            reps = f.run_protected(scheme, sched, np.random.default_rng(seed))
+            got = [[(r, c, kk.value, fl) for r, c, kk, fl in rep.locations] for rep in reps]
+            assert _same_outcome(kind, scheme, got, ref, regions, b), (scheme, seed, got, ref)
+
+
+@pytest.mark.parametrize("kind", ["lu", "cholesky", "qr"])
 def test_fp32_per_iteration_equals_one_call(kind):
     n, b, seed = 640, 128, 9
     a = P.generate_test_matrix(kind, n, seed)
