@@ -542,6 +542,94 @@ def compare_modes(kind, a0: np.ndarray, b: int, r: float = 0.5, seed: int = 0, *
 
 
 # ---------------------------------------------------------------------------
+# derived tables of the reference's sweep / compare / campaign commands
+# (simulator.py:620-710, cli.py:233-277) over measured B200 runs: time =
+# device time of the factorization, energy = NVML joules (None without NVML)
+# ---------------------------------------------------------------------------
+@dataclass(frozen=True)
+class SweepPoint:
+    r: float
+    time_s: float
+    energy_j: float | None
+    ed2p: float | None
+    pareto: bool
+
+
+def _ed2p(energy_j, time_s):
+    """power.py ed2p: energy x delay^2."""
+    return None if energy_j is None else energy_j * time_s * time_s
+
+
+def sweep_points(summaries: list) -> list:
+    """simulator.py:636-647: flag the Pareto-efficient (time, energy) points
+    (without energy readings, time alone orders them)."""
+    pts = []
+    for s in summaries:
+        t, e = s.device_ms * 1e-3, s.energy_j
+        dominated = False
+        for o in summaries:
+            to, eo = o.device_ms * 1e-3, o.energy_j
+            if e is None or eo is None:
+                dominated |= to < t
+            else:
+                dominated |= to <= t and eo <= e and (to < t or eo < e)
+        pts.append(SweepPoint(float(s.r), t, e, _ed2p(e, t), not dominated))
+    return pts
+
+
+def mode_table(summaries: dict) -> dict:
+    """simulator.py:650-669: savings / speedup relative to 'original'."""
+    base = summaries["original"]
+    bt, be = base.device_ms * 1e-3, base.energy_j
+    out = {}
+    for mode, s in summaries.items():
+        t, e = s.device_ms * 1e-3, s.energy_j
+        ok = e is not None and be
+        out[mode] = {
+            "summary": s,
+            "energy_saving_pct": 100.0 * (1.0 - e / be) if ok else None,
+            "ed2p_reduction_pct": 100.0 * (1.0 - _ed2p(e, t) / _ed2p(be, bt)) if ok else None,
+            "speedup": bt / t,
+            # the reference's floor is its modeled peak-efficiency energy
+            # (power.py theoretical_min_energy); no measured counterpart
+            "energy_gap_fraction": None,
+        }
+    return out
+
+
+CAMPAIGN_SCHEMES = ("none", "single", "full", "adaptive")
+
+
+@dataclass(frozen=True)
+class CampaignRow:
+    scheme: str
+    trials: int
+    correct_fraction: float
+    overhead_fraction: float
+
+
+def fault_campaign(kind, a0: np.ndarray, b: int, trials: int, seed: int = 0,
+                   schemes=CAMPAIGN_SCHEMES, **kw) -> list:
+    """simulator.py:683-710 on the B200: bsr mode, recovery 'continue', each
+    forced scheme (and the adaptive governor) over seeds seed..seed+trials-1;
+    correct_fraction = runs whose final residual passes, overhead_fraction =
+    mean measured ABFT share of the device time."""
+    if trials < 1:
+        raise ValueError("need at least one trial")
+    rows = []
+    for scheme in schemes:
+        forced = None if scheme == "adaptive" else scheme
+        rest = {k: v for k, v in kw.items() if k != "r"}
+        sums = [run_mode(kind, a0, b, "bsr", kw.get("r", 0.5), seed + t, recovery="continue",
+                         forced_scheme=forced, **rest)[0]
+                for t in range(trials)]
+        rows.append(CampaignRow(scheme, trials, sum(1 for s in sums if s.correct) / trials,
+                                float(np.mean([s.abft_ms / s.device_ms if s.device_ms else 0.0
+                                               for s in sums]))))
+    return rows
+
+
+# ---------------------------------------------------------------------------
 # output formats (cli.py:33-122): the reference's trace CSV and summary JSON
 # ---------------------------------------------------------------------------
 TRACE_HEADER = ("iter,task,pred_time_s,actual_time_s,slack_pred_s,"
@@ -606,3 +694,41 @@ def write_summary(path: str, summary: RunSummary) -> None:
     import dataclasses
     import json
     _write_atomic(path, json.dumps(dataclasses.asdict(summary), sort_keys=True, indent=2) + "\n")
+
+
+def _fmt_opt(x) -> str:
+    return "" if x is None else repr(float(x))
+
+
+def write_sweep(path: str, points: list) -> None:
+    """cli.py:233-245: r,time_s,energy_j,ed2p,pareto."""
+    lines = ["r,time_s,energy_j,ed2p,pareto"]
+    for p in points:
+        lines.append(",".join([repr(float(p.r)), repr(float(p.time_s)), _fmt_opt(p.energy_j),
+                               _fmt_opt(p.ed2p), "1" if p.pareto else "0"]))
+    _write_atomic(path, "\n".join(lines) + "\n")
+
+
+def write_compare(path: str, table: dict) -> None:
+    """cli.py:248-266 (sorted keys, indent 2)."""
+    import json
+    doc = {}
+    for mode, row in table.items():
+        s = row["summary"]
+        t = s.device_ms * 1e-3
+        doc[mode] = {"energy_saving_pct": row["energy_saving_pct"],
+                     "ed2p_reduction_pct": row["ed2p_reduction_pct"],
+                     "speedup": row["speedup"],
+                     "energy_gap_fraction": row["energy_gap_fraction"],
+                     "total_time_s": t, "total_energy_j": s.energy_j,
+                     "ed2p": _ed2p(s.energy_j, t)}
+    _write_atomic(path, json.dumps(doc, sort_keys=True, indent=2) + "\n")
+
+
+def write_campaign(path: str, rows: list) -> None:
+    """cli.py:269-277: scheme,correct_fraction,overhead_fraction."""
+    lines = ["scheme,correct_fraction,overhead_fraction"]
+    for row in rows:
+        lines.append(",".join([row.scheme, repr(float(row.correct_fraction)),
+                               repr(float(row.overhead_fraction))]))
+    _write_atomic(path, "\n".join(lines) + "\n")

@@ -187,3 +187,33 @@ def test_fp32_run_modes_and_campaign(kind):
     s2, _ = G.run_mode(kind, a, 128, "bsr", r=1.0, seed=4, rates=table, forced_scheme="full",
                        recovery="recompute", precision="f32")
     assert sum(s2.faults_injected.values()) > 0 and s2.faults_detected > 0
+
+
+def _summary(mode, r, ms, j, abft=1.0, correct=True):
+    return G.RunSummary(mode, r, "lu", 512, 128, ms, abft, j, 1e-16, correct,
+                        {"0d": 0, "1d": 0, "2d": 0}, 0, 0, False, 0, {})
+
+
+def test_sweep_pareto_and_output_formats(tmp_path):
+    """sweep / compare / campaign tables and files (simulator.py:636-710,
+    cli.py:233-277): headers, column order, Pareto rule."""
+    sums = [_summary("bsr", 0.0, 10.0, 5.0), _summary("bsr", 0.5, 9.0, 6.0),
+            _summary("bsr", 1.0, 11.0, 7.0)]
+    pts = G.sweep_points(sums)
+    assert [p.pareto for p in pts] == [True, True, False]   # r=1 dominated by r=0
+    assert pts[0].ed2p == pytest.approx(5.0 * 0.01 * 0.01)
+    G.write_sweep(str(tmp_path / "s.csv"), pts)
+    lines = (tmp_path / "s.csv").read_text().splitlines()
+    assert lines[0] == "r,time_s,energy_j,ed2p,pareto" and lines[1].endswith(",1")
+    table = G.mode_table({"original": _summary("original", 0.0, 10.0, 8.0),
+                          "bsr": _summary("bsr", 0.5, 8.0, 6.0)})
+    assert table["bsr"]["speedup"] == pytest.approx(1.25)
+    assert table["bsr"]["energy_saving_pct"] == pytest.approx(25.0)
+    G.write_compare(str(tmp_path / "c.json"), table)
+    doc = json.loads((tmp_path / "c.json").read_text())
+    assert sorted(doc["bsr"]) == ["ed2p", "ed2p_reduction_pct", "energy_gap_fraction",
+                                  "energy_saving_pct", "speedup", "total_energy_j",
+                                  "total_time_s"]
+    G.write_campaign(str(tmp_path / "k.csv"), [G.CampaignRow("full", 4, 1.0, 0.08)])
+    assert (tmp_path / "k.csv").read_text() == (
+        "scheme,correct_fraction,overhead_fraction\nfull,1.0,0.08\n")
