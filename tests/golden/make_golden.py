@@ -15,6 +15,11 @@ Every case mirrors a reference test or an SURVEY.md §8c golden:
   * plans.json   — sample_fault_plan draws (abft.py:310-333)
   * linalg.json / linalg.npz — small factorizations (test_linalg.py:37-50)
   * inputs.json  — sha256 of generate_test_matrix outputs (linalg.py:63-78)
+  * simrun.json  — simulate_run(engine="numeric") summaries (the mode-flag
+                   path: modeled timing, Poisson fault streams, recovery;
+                   simulator.py:314-335, :408-418) under campaign-scale
+                   throughput, every kind x forced scheme, seeds 0..5
+                   (`make_golden.py simrun` regenerates only this file)
   * c2c3.json    — BASELINE configs C2 (LU N=8192, SINGLE and FULL) and C3
                    (QR N=8192 SINGLE), b=256, criterion-5 fault, seed 0
                    (`make_golden.py c2c3` regenerates only this file)
@@ -243,7 +248,43 @@ def c2c3():
     return {"runs": out}
 
 
+def simrun():
+    import dataclasses
+
+    from slackwise.config import SimConfig
+    from slackwise.power import default_cpu_model, default_gpu_model
+    from slackwise.simulator import simulate_run
+    cpu = dataclasses.replace(default_cpu_model(), base_flops_per_second=5e7)
+    gpu = dataclasses.replace(default_gpu_model(), base_flops_per_second=2e7, f_max_mhz=2100.0)
+    out = []
+    for kind in (K.CHOLESKY, K.LU, K.QR):
+        for mode, r in (("bsr", 1.0), ("bsr", 0.5), ("sr", 0.0), ("original", 0.0)):
+            for forced in (None, SCH.NONE, SCH.SINGLE, SCH.FULL):
+                if mode != "bsr" and forced is not None:
+                    continue
+                for seed in range(6):
+                    c = SimConfig(kind=kind, n=256, b=32, seed=seed, cpu=cpu, gpu=gpu, mode=mode,
+                                  r=r, engine="numeric", recovery="recompute")
+                    sm, recs = simulate_run(c, forced_scheme=forced)
+                    out.append({
+                        "kind": kind.value, "mode": mode, "r": r, "seed": seed,
+                        "forced": None if forced is None else forced.value,
+                        "total_time_s": sm.total_time_s, "total_energy_j": sm.total_energy_j,
+                        "correct": sm.correct, "residual": sm.residual,
+                        "unrecoverable": sm.unrecoverable, "breakdown": sm.breakdown,
+                        "faults_injected": {k.value if hasattr(k, "value") else k: int(v)
+                                            for k, v in sm.faults_injected.items()},
+                        "faults_detected": sm.faults_detected,
+                        "faults_corrected": sm.faults_corrected,
+                        "iterations_completed": sm.iterations_completed,
+                        "abft_modes": [getattr(rc, "abft_mode", None) for rc in recs]})
+    return {"runs": out}
+
+
 def main():
+    if sys.argv[1:] == ["simrun"]:
+        (OUT / "simrun.json").write_text(json.dumps(simrun()))
+        return
     if sys.argv[1:] == ["c2c3"]:
         (OUT / "c2c3.json").write_text(json.dumps(c2c3()))
         return
