@@ -306,11 +306,19 @@ int upload_touched(abft_dist* d, const abft_fault* plan, int nplan, const LocalR
 
 // maintain_gemm (abft.py:138-158) for `region -= L @ R` from the operands:
 // L is rows x w (ldl), R is w x cols (ldr), both on the device.
-int maintain_lr(abft_dist* d, const LocalRegion& R, int scheme, const double* L, int64_t ldl,
-                const double* Rm, int64_t ldr, int64_t w) {
-  const int64_t nbr = (R.rows + d->b - 1) / d->b, nbc = (R.cols + d->b - 1) / d->b;
-  SumOut enc = sums_local(d, R.r0, R.lb0, scheme == ABFT_FULL);
-  {
+// Restricted to the region's local block columns [j0, j0 + ncb) (Rm points at
+// the first of them): the maintained sums land at the matching offsets of the
+// region-local csm / rsm, so an update split by block columns (look-ahead)
+// maintains piece by piece. E_L (the block sums of L) is reused when el_ready.
+int maintain_lr_sub(abft_dist* d, const LocalRegion& R, int scheme, const double* L, int64_t ldl,
+                    const double* Rm, int64_t ldr, int64_t w, int64_t j0, int64_t ncb,
+                    bool el_ready) {
+  const int64_t cbeg = j0 * d->b;
+  const int64_t cols = std::min(R.cols - cbeg, ncb * d->b);
+  if (cols <= 0 || R.rows <= 0) return 0;
+  const int64_t nbr = (R.rows + d->b - 1) / d->b, nbc = (cols + d->b - 1) / d->b;
+  SumOut enc = sums_local(d, R.r0, R.lb0 + j0, scheme == ABFT_FULL);
+  if (!el_ready) {
     Region rl{const_cast<double*>(L), ldl, R.rows, w, d->b};
     SumOut o;
     o.cp = d->el;
@@ -321,18 +329,23 @@ int maintain_lr(abft_dist* d, const LocalRegion& R, int scheme, const double* L,
     o.cw_step = 2;
     ABFT_TRY(blocksum(d->st, rl, o));
   }
-  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(2 * nbr), (int)R.cols, (int)w, -1.0, d->el, d->ld_cs, Rm, ldr,
-                1.0, enc.cp, d->ld_cs, d->csm, d->ld_cs, &d->gws));
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(2 * nbr), (int)cols, (int)w, -1.0, d->el, d->ld_cs, Rm, ldr,
+                1.0, enc.cp, d->ld_cs, d->csm + cbeg * d->ld_cs, d->ld_cs, &d->gws));
   if (scheme == ABFT_FULL) {
-    Region rr{const_cast<double*>(Rm), ldr, w, R.cols, d->b};
+    Region rr{const_cast<double*>(Rm), ldr, w, cols, d->b};
     SumOut o;
     o.rp = d->er;
     o.rp_ld = d->ld_t;
     ABFT_TRY(blocksum(d->st, rr, o));
     ABFT_TRY(gemm(d->st, 'N', 'N', (int)R.rows, (int)nbc, (int)w, -1.0, L, ldl, d->er, d->ld_t, 1.0,
-                  enc.rp, d->ld, d->rsm, d->ld, &d->gws));
+                  enc.rp, d->ld, d->rsm + j0 * d->ld, d->ld, &d->gws));
   }
   return 0;
+}
+
+int maintain_lr(abft_dist* d, const LocalRegion& R, int scheme, const double* L, int64_t ldl,
+                const double* Rm, int64_t ldr, int64_t w) {
+  return maintain_lr_sub(d, R, scheme, L, ldl, Rm, ldr, w, 0, (R.cols + d->b - 1) / d->b, false);
 }
 
 // ---------------------------------------------------------------------------
@@ -473,6 +486,70 @@ int update_lu_lookahead(abft_dist* d, int64_t k, int scheme, const double* xb, c
   return 0;
 }
 
+// QR update of iteration k on the owner of panel k+1 (fault-free k): the
+// first local block column (global block k+1) gets V^T C, T^T W, its
+// maintained sums, C -= V mid, and is verified; panel k+1 (Householder +
+// V^T V + larft) is then factored and packed into the look-ahead buffer
+// (ev_pack releases the comm stream), and only then do the remaining local
+// columns run their three GEMMs (the fused one on all but reserve_sms SMs).
+int update_qr_lookahead(abft_dist* d, int64_t k, int scheme, const double* xb,
+                        const LocalRegion& R, int64_t w) {
+  const int64_t n = d->n, p = k * d->b, ldp = panel_ld(d, k);
+  const bool prot = scheme != ABFT_NONE;
+  const double* V = xb;
+  const double* T = xb + ldp * w;
+  double* C = d->m + p + R.lc0 * d->ld;
+  const int64_t wa = std::min<int64_t>(d->b, R.cols);
+  ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)wa, (int)(n - p), 1.0, V, ldp, C, d->ld, 0.0, nullptr,
+                0, d->ww, d->ld_t, &d->gws));
+  ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)wa, (int)w, 1.0, T, d->ld_t, d->ww, d->ld_t, 0.0,
+                nullptr, 0, d->mid, d->ld_t, &d->gws));
+  if (prot) ABFT_TRY(maintain_lr_sub(d, R, scheme, V, ldp, d->mid, d->ld_t, w, 0, 1, false));
+  ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - p), (int)wa, (int)w, -1.0, V, ldp, d->mid, d->ld_t, 1.0,
+                C, d->ld, C, d->ld, &d->gws));
+  if (prot) {
+    Region ra{C, d->ld, R.rows, wa, d->b};
+    ABFT_TRY(blocksum(d->st, ra, sums_local(d, R.r0, R.lb0, true)));
+    ABFT_TRY(verify_sub_local(d, k, scheme, 1, R, 0, 1));
+  }
+  // panel k+1 (global block k+1 = local block R.lb0 on this rank)
+  ABFT_TRY(begin_qr(d, k + 1, d->la_buf));
+  CUDA_TRY(cudaEventRecord(d->ev_pack, d->st));
+  CUDA_TRY(cudaStreamWaitEvent(d->st2, d->ev_pack, 0));
+  d->panel_ready = k + 1;
+  if (R.cols > wa) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+    const int cap = std::max(1, sms - d->reserve_sms);
+    const int64_t cr = R.cols - wa;
+    double* Cr = C + wa * d->ld;
+    ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)cr, (int)(n - p), 1.0, V, ldp, Cr, d->ld, 0.0,
+                  nullptr, 0, d->ww + wa * d->ld_t, d->ld_t, &d->gws));
+    ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)cr, (int)w, 1.0, T, d->ld_t, d->ww + wa * d->ld_t,
+                  d->ld_t, 0.0, nullptr, 0, d->mid + wa * d->ld_t, d->ld_t, &d->gws));
+    const int64_t nbc = (R.cols + d->b - 1) / d->b;
+    if (prot)
+      ABFT_TRY(maintain_lr_sub(d, R, scheme, V, ldp, d->mid + wa * d->ld_t, d->ld_t, w, 1, nbc - 1,
+                               true));
+    if (prot && d->fuse_enabled && gemm_can_fuse((int)d->b)) {
+      ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)(n - p), (int)cr, (int)w, -1.0, V, ldp,
+                               d->mid + wa * d->ld_t, d->ld_t, 1.0, Cr, d->ld, Cr, d->ld, (int)d->b,
+                               fused_local(d, R.r0, R.lb0 + 1), cap));
+    } else {
+      ABFT_TRY(gemm_reserved(d->st, 'N', 'N', (int)(n - p), (int)cr, (int)w, -1.0, V, ldp,
+                             d->mid + wa * d->ld_t, d->ld_t, 1.0, Cr, d->ld, Cr, d->ld, cap));
+      if (prot) {
+        Region rb{Cr, d->ld, R.rows, cr, d->b};
+        ABFT_TRY(blocksum(d->st, rb, sums_local(d, R.r0, R.lb0 + 1, true)));
+      }
+    }
+    if (prot) ABFT_TRY(verify_sub_local(d, k, scheme, 1, R, 1, nbc));
+  }
+  d->verified_in_update = true;
+  d->sums_valid = prot;
+  return 0;
+}
+
 int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int nplan,
                  double* max_out) {
   const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
@@ -525,6 +602,14 @@ int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int npla
       const double* T = xb + ldp * w;
       double* C = d->m + p + R.lc0 * d->ld;
       if (prot && !d->sums_valid) ABFT_TRY(blocksum(d->st, reg, sums_local(d, R.r0, R.lb0, true)));
+      const bool la = d->la_buf != nullptr && nplan == 0;
+      if (la && owner(d, k + 1) == d->rank) return update_qr_lookahead(d, k, scheme, xb, R, w);
+      int cap = 0;  // leave SMs to the collective receiving panel k+1 meanwhile
+      if (la) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, d->device);
+        cap = std::max(1, sms - d->reserve_sms);
+      }
       ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)R.cols, (int)(n - p), 1.0, V, ldp, C, d->ld, 0.0,
                     nullptr, 0, d->ww, d->ld_t, &d->gws));
       ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)R.cols, (int)w, 1.0, T, d->ld_t, d->ww, d->ld_t, 0.0,
@@ -534,8 +619,11 @@ int update_lu_qr(abft_dist* d, int64_t k, int scheme, const double* xb, int npla
       if (fuse) {
         ABFT_TRY(gemm_fused_sums(d->st, 'N', 'N', (int)(n - p), (int)R.cols, (int)w, -1.0, V, ldp,
                                  d->mid, d->ld_t, 1.0, C, d->ld, C, d->ld, (int)d->b,
-                                 fused_local(d, R.r0, R.lb0)));
+                                 fused_local(d, R.r0, R.lb0), cap));
         fused = true;
+      } else if (cap > 0) {
+        ABFT_TRY(gemm_reserved(d->st, 'N', 'N', (int)(n - p), (int)R.cols, (int)w, -1.0, V, ldp,
+                               d->mid, d->ld_t, 1.0, C, d->ld, C, d->ld, cap));
       } else {
         ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - p), (int)R.cols, (int)w, -1.0, V, ldp, d->mid,
                       d->ld_t, 1.0, C, d->ld, C, d->ld, &d->gws));
@@ -947,7 +1035,7 @@ ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) 
     CUDA_TRY(cudaStreamWaitEvent(d->st, d->ev_comm, 0));
     d->comm_pending = false;
   }
-  if (d->kind == ABFT_LU && d->panel_ready == k) {  // factored + packed by the look-ahead
+  if (d->kind != ABFT_CHOLESKY && d->panel_ready == k) {  // factored + packed by the look-ahead
     d->panel_ready = -1;
     return 0;
   }
@@ -989,13 +1077,13 @@ ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double*
   return rc;
 }
 
-// LU look-ahead for the next abft_dist_update(k): the owner of panel k+1
+// LU / QR look-ahead for the next abft_dist_update(k): the owner of panel k+1
 // factors it mid-update into `xnext` (abft_dist_xbuf_elems(k+1) doubles);
 // the caller then broadcasts `xnext` from rank (k+1) mod G on the comm stream
 // (abft_dist_comm_stream) and calls abft_dist_comm_done; begin(k+1) makes the
 // main stream wait for that broadcast.
 ABFT_API int abft_dist_lookahead(abft_dist* d, int64_t k, double* xnext) {
-  if (d->kind != ABFT_LU || k + 1 >= d->nb || abft_dist_xbuf_elems(d, k + 1) == 0) {
+  if (d->kind == ABFT_CHOLESKY || k + 1 >= d->nb || abft_dist_xbuf_elems(d, k + 1) == 0) {
     set_last_error("no look-ahead panel after iteration %lld", (long long)k);
     return ABFT_E_INVALID;
   }

@@ -253,12 +253,13 @@ class DistributedFactorization:
                 self._tx.broadcast(view, owner_of(k, self.world))
         self._prefetched.discard(k)
         nplan = len(plan)
-        # LU look-ahead: panel k+1 is factored mid-update by its owner and
-        # broadcast on the comm stream while the trailing update of k runs
+        # LU / QR look-ahead: panel k+1 is factored mid-update by its owner
+        # and broadcast on the comm stream while the trailing update of k runs
         nb = self.layout.n_blocks
         xe1 = int(lib.abft_dist_xbuf_elems(ctx, k + 1)) if k + 1 < nb else 0
         la = (self.lookahead and (self.world > 1 or self.force_lookahead)
-              and self.kind == DecompositionKind.LU and nplan == 0 and xe1 > 0)
+              and self.kind in (DecompositionKind.LU, DecompositionKind.QR) and nplan == 0
+              and xe1 > 0)
         nxt = self._bufs[(k + 1) % 2]
         if la:
             check(lib.abft_dist_lookahead(ctx, k, ctypes.c_void_p(nxt.data_ptr())))

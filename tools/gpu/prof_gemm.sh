@@ -1,11 +1,12 @@
 #!/bin/bash
-# ncu --set full of the LU N=32768 trailing-update GEMM, fused (FULL) and plain (scheme none)
+# ncu --set full of the first LU N=32768 iterations' DMMA GEMM launches (the
+# trailing update is the longest one), fused (FULL) and plain (scheme none)
 set -u
 TAG=${1:-r02}
 mkdir -p gpurun_out
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_$TAG.log 2>&1
 NCU="ncu --set full --clock-control none --import-source on"
-timeout 900 $NCU -k regex:dgemm_tma_dmma -s 40 -c 1 -o gpurun_out/prof_gemm_full_$TAG \
+timeout 1200 $NCU -k regex:dgemm_tma_dmma -c 10 -o gpurun_out/prof_gemm_full_$TAG \
   python bench.py --profile-only > gpurun_out/prof_gemm_full_$TAG.log 2>&1; echo "gemm fused rc=$?"
-timeout 900 $NCU -k regex:dgemm_tma_dmma -s 40 -c 1 -o gpurun_out/prof_gemm_none_$TAG \
+timeout 1200 $NCU -k regex:dgemm_tma_dmma -c 10 -o gpurun_out/prof_gemm_none_$TAG \
   python bench.py --profile-only --scheme none > gpurun_out/prof_gemm_none_$TAG.log 2>&1; echo "gemm none rc=$?"
