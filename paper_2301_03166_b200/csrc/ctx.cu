@@ -81,6 +81,8 @@ struct abft_ctx {
   double* qr_part2 = nullptr;  // 148 x 32 x b block-update partials
   double* qr_wfin = nullptr;   // 32 x b
   double* gram = nullptr;    // b x b
+  double* qr_small = nullptr;  // QR_SMALL_BUFS x (ld_t x b): panel fast path
+  QrPanelWork qrw;             // qr_panel_factor workspace (Q1 = lw)
   double* ww = nullptr;      // b x n
   double* mid = nullptr;     // b x n
   double* scratch = nullptr; // 4096 doubles
@@ -115,6 +117,8 @@ struct abft_ctx {
   bool chol_enc_ahead = false;    // ... and whose encode ran with it
   int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
   GemmWorkspace gws2;             // split-K workspace of the side stream
+  int qr_la_sms = 16;             // QR look-ahead: SMs left to the side-stream panel
+                                  // (ABFT_QR_LA_SMS)
   // streamed result (abft_stream_out): finished column blocks are copied to
   // this host buffer on a copy stream while the factorization continues
   double* out_host = nullptr;
@@ -332,12 +336,8 @@ int task_pd(abft_ctx* c, int64_t k) {
     ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
     double* V = c->vstore + p + p * c->ld;
-    ABFT_TRY(qr_panel(c->st, D, c->ld, n - p, (int)w, V, c->ld, c->betas, c->qr_part,
-                      c->qr_part_elems, c->qr_rowbuf, c->qr_part2, c->qr_wfin));
-    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)w, (int)(n - p), 1.0, V, c->ld, V, c->ld, 0.0,
-                  nullptr, 0, c->gram, c->ld_t, &c->gws));
-    ABFT_TRY(larft(c->st, c->gram, c->ld_t, c->betas, (int)w, c->tstore + k * c->b * c->ld_t,
-                   c->ld_t));
+    ABFT_TRY(qr_panel_factor(c->st, D, c->ld, n - p, (int)w, V, c->ld,
+                             c->tstore + k * c->b * c->ld_t, c->ld_t, c->betas, c->qrw));
     c->qr_count = (int)(k + 1);
   }
   return 0;
@@ -812,6 +812,102 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   return 0;
 }
 
+// QR protected trailing update with look-ahead (fault-free iterations of the
+// one-call path), the LU scheme restated for Householder updates: W = V^T C
+// and mid = T^T W over the whole region and the maintained sums first; then
+// the next panel's block column C[:, 0:b] -= V mid[:, 0:b] (plain GEMM over
+// all SMs) + checksum pass + verify; panel k+1 (qr_panel_factor, every GEMM
+// capped at qr_la_sms CTAs) is then factored on the side stream while the
+// rest of the region takes C -= V mid with fused sums on the other SMs.
+// Same operations and ordering constraints as _protected_tmu
+// (simulator.py:124-167) and PD(k+1) (linalg.py:260-300); only independent
+// work overlaps.
+int protected_tmu_qr_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  Region reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  const bool prot = scheme != ABFT_NONE;
+  const double* V = c->vstore + p + p * c->ld;
+  const double* T = c->tstore + k * c->b * c->ld_t;
+  double* C = c->m + p + pe * c->ld;
+  if (prot && !c->sums_valid) {
+    prof_mark(c, PROF_ABFT, true);
+    ABFT_TRY(blocksum(c->st, reg, sums_for(c, r0, c0, true)));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  prof_mark(c, PROF_TMU, true);
+  ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)cols, (int)rows, 1.0, V, c->ld, C, c->ld, 0.0,
+                nullptr, 0, c->ww, c->ld_t, &c->gws));
+  ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)cols, (int)w, 1.0, T, c->ld_t, c->ww, c->ld_t, 0.0,
+                nullptr, 0, c->mid, c->ld_t, &c->gws));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    ABFT_TRY(maintain(c, k, scheme, r0, c0, rows, cols));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  const int64_t wa = std::min<int64_t>(c->b, cols);
+  // (a) the next panel's block column
+  prof_mark(c, PROF_TMU, true);
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, V, c->ld, c->mid, c->ld_t, 1.0,
+                C, c->ld, C, c->ld, &c->gws));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    Region ra{C, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, c0, true)));
+    ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  // side stream: panel k+1 on qr_la_sms SMs
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int res = std::max(1, std::min(c->qr_la_sms, sms / 2));
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  {
+    const int64_t p1 = pe, pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
+    QrPanelWork q = c->qrw;
+    q.gws = &c->gws2;
+    ABFT_TRY(qr_panel_factor(c->st2, c->m + p1 + p1 * c->ld, c->ld, n - p1, (int)w1,
+                             c->vstore + p1 + p1 * c->ld, c->ld,
+                             c->tstore + (k + 1) * c->b * c->ld_t, c->ld_t, c->betas, q, res));
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  // (b) the rest of the region
+  if (cols > wa) {
+    prof_mark(c, PROF_TMU, true);
+    const double* midb = c->mid + wa * c->ld_t;
+    double* Cb = C + wa * c->ld;
+    if (prot && c->fuse_enabled && gemm_can_fuse((int)c->b)) {
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, V,
+                               c->ld, midb, c->ld_t, 1.0, Cb, c->ld, Cb, c->ld, (int)c->b,
+                               fused_for(c, r0, c0 + wa), sms - res));
+      prof_mark(c, PROF_TMU, false);
+    } else {
+      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, V, c->ld,
+                             midb, c->ld_t, 1.0, Cb, c->ld, Cb, c->ld, sms - res));
+      prof_mark(c, PROF_TMU, false);
+      if (prot) {
+        Region rb{Cb, c->ld, rows, cols - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, sums_for(c, r0, c0 + wa, true)));
+      }
+    }
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 1, (cols + c->b - 1) / c->b));
+      prof_mark(c, PROF_ABFT, false);
+    }
+  }
+  c->sums_valid = prot;
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  c->qr_count = (int)(k + 2);
+  ABFT_TRY(emit_column(c, k + 1));
+  c->pd_ready = k + 1;
+  return 0;
+}
+
 // Per-task device timers (CUDA events on the context stream), enabled by
 // abft_profile(ctx, 1): PD, PU, TMU GEMM(s) and the ABFT work around them.
 
@@ -858,7 +954,13 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
       ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
   } else {
     ABFT_TRY(pd());
-    ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
+    const int64_t pe = std::min((k + 1) * c->b, c->n);
+    const bool la = lookahead && c->lookahead_enabled && nplan == 0 && pe < c->n &&
+                    k < c->qr_count && c->qr_la_sms > 0;
+    if (la)
+      ABFT_TRY(protected_tmu_qr_lookahead(c, k, scheme, correct));
+    else
+      ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
   }
   return 0;
 }
@@ -964,6 +1066,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     c->fuse_enabled = !(e && e[0] == '1');
     const char* e2 = getenv("ABFT_NO_LOOKAHEAD");
     c->lookahead_enabled = !(e2 && e2[0] == '1');
+    const char* e3 = getenv("ABFT_QR_LA_SMS");
+    if (e3) c->qr_la_sms = atoi(e3);  // 0 disables the QR look-ahead
   }
   int rc = 0;
   auto fail = [&](int r) {
@@ -1003,13 +1107,14 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     if ((rc = dalloc(&c->qr_part2, 160LL * 32 * b))) return fail(rc);
     if ((rc = dalloc(&c->qr_wfin, 32LL * b))) return fail(rc);
     if ((rc = dalloc(&c->gram, c->ld_t * b))) return fail(rc);
+    if ((rc = dalloc(&c->qr_small, QR_SMALL_BUFS * c->ld_t * b))) return fail(rc);
     if ((rc = dalloc(&c->ww, c->ld_t * n_))) return fail(rc);
     if ((rc = dalloc(&c->mid, c->ld_t * n_))) return fail(rc);
   }
   // split-K workspace: bounded (falls back to fewer splits when short)
   c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
   if ((rc = dalloc(&c->gws.ptr, c->gws.elems))) return fail(rc);
-  if (kind == ABFT_CHOLESKY) {
+  if (kind == ABFT_CHOLESKY || kind == ABFT_QR) {
     c->gws2.elems = c->gws.elems;
     if ((rc = dalloc(&c->gws2.ptr, c->gws2.elems))) return fail(rc);
   }
@@ -1019,8 +1124,24 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   cudaMemset(c->counters, 0, 4 * sizeof(int32_t));
   c->dirty_cap = 1 << 16;
   if (cudaMalloc(&c->dirty, 2 * c->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
-  if (cudaMalloc(&c->info, sizeof(int)) != cudaSuccess) return fail(-1000);
-  cudaMemset(c->info, 0, sizeof(int));
+  if (cudaMalloc(&c->info, 2 * sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemset(c->info, 0, 2 * sizeof(int));
+  if (kind == ABFT_QR) {
+    QrPanelWork& q = c->qrw;
+    q.q1 = c->lw;
+    q.ldq = ld;
+    q.small = c->qr_small;
+    q.lds = c->ld_t;
+    q.info = c->info + 1;
+    q.gws = &c->gws;
+    q.part = c->qr_part;
+    q.part_elems = c->qr_part_elems;
+    q.rowbuf = c->qr_rowbuf;
+    q.part2 = c->qr_part2;
+    q.wfin = c->qr_wfin;
+    q.gram = c->gram;
+    q.ldg = c->ld_t;
+  }
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
@@ -1042,7 +1163,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
                     c->chol_rs,
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
-                    c->qr_part2, c->qr_wfin,
+                    c->qr_part2, c->qr_wfin, c->qr_small,
                     c->scratch, c->gws.ptr, c->gws2.ptr};
   for (double* p : bufs)
     if (p) cudaFree(p);

@@ -87,6 +87,9 @@ struct abft_sctx {
   double* v64 = nullptr;     // n x b (ld)
   double* t64 = nullptr;     // b x b (ld_t)
   double* gram = nullptr;    // b x b
+  double* qr_q1 = nullptr;     // fp64 n x b: CholeskyQR2 Q of the widened panel
+  double* qr_small = nullptr;  // QR_SMALL_BUFS x (ld_t x b)
+  QrPanelWork qrw;
   double* betas = nullptr;
   double* qr_part = nullptr;
   int64_t qr_part_elems = 0;
@@ -412,11 +415,8 @@ int s_pd(abft_sctx* c, int64_t k) {
     const int64_t nk = n - p;
     ABFT_TRY(widen_matrix(c->st, D, c->ld, c->pan64, c->ld, nk, w));
     ABFT_TRY(fill_matrix(c->st, c->v64, c->ld, nk, w, 0.0));
-    ABFT_TRY(qr_panel(c->st, c->pan64, c->ld, nk, (int)w, c->v64, c->ld, c->betas, c->qr_part,
-                      c->qr_part_elems, c->qr_rowbuf, c->qr_part2, c->qr_wfin));
-    ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)w, (int)nk, 1.0, c->v64, c->ld, c->v64, c->ld, 0.0,
-                  nullptr, 0, c->gram, c->ld_t, &c->gws));
-    ABFT_TRY(larft(c->st, c->gram, c->ld_t, c->betas, (int)w, c->t64, c->ld_t));
+    ABFT_TRY(qr_panel_factor(c->st, c->pan64, c->ld, nk, (int)w, c->v64, c->ld, c->t64, c->ld_t,
+                             c->betas, c->qrw));
     ABFT_TRY(narrow_matrix(c->st, c->pan64, c->ld, D, c->ld, nk, w));
     ABFT_TRY(narrow_matrix(c->st, c->v64, c->ld, c->vstore + p + p * c->ld, c->ld, nk, w));
     ABFT_TRY(narrow_matrix(c->st, c->t64, c->ld_t, c->tstore + k * c->b * c->ld_t, c->ld_t, w, w));
@@ -1016,6 +1016,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     if ((rc = salloc(&c->v64, ld * b, c->st))) return fail(rc);
     if ((rc = salloc(&c->t64, c->ld_t * b, c->st))) return fail(rc);
     if ((rc = salloc(&c->gram, c->ld_t * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->qr_q1, ld * b, c->st))) return fail(rc);
+    if ((rc = salloc(&c->qr_small, QR_SMALL_BUFS * c->ld_t * b, c->st))) return fail(rc);
     if ((rc = salloc(&c->betas, b, c->st))) return fail(rc);
     c->qr_part_elems = 2 * 160 * (b + 1);
     if ((rc = salloc(&c->qr_part, c->qr_part_elems, c->st))) return fail(rc);
@@ -1062,8 +1064,24 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   cudaMemsetAsync(c->counters, 0, 4 * sizeof(int32_t), c->st);
   c->dirty_cap = 1 << 16;
   if (cudaMalloc(&c->dirty, 2 * c->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
-  if (cudaMalloc(&c->info, sizeof(int)) != cudaSuccess) return fail(-1000);
-  cudaMemsetAsync(c->info, 0, sizeof(int), c->st);
+  if (cudaMalloc(&c->info, 2 * sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemsetAsync(c->info, 0, 2 * sizeof(int), c->st);
+  if (kind == ABFT_QR) {
+    QrPanelWork& q = c->qrw;
+    q.q1 = c->qr_q1;
+    q.ldq = ld;
+    q.small = c->qr_small;
+    q.lds = c->ld_t;
+    q.info = c->info + 1;
+    q.gws = &c->gws;
+    q.part = c->qr_part;
+    q.part_elems = c->qr_part_elems;
+    q.rowbuf = c->qr_rowbuf;
+    q.part2 = c->qr_part2;
+    q.wfin = c->qr_wfin;
+    q.gram = c->gram;
+    q.ldg = c->ld_t;
+  }
   cudaEventCreate(&c->e0);
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
@@ -1084,7 +1102,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
   if (!c) return 0;
   SGuard g(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
-  void* bufs[] = {c->snap_m, c->snap_rs, c->vstore, c->tstore, c->ww, c->mid, c->pan64, c->v64, c->t64, c->gram,
+  void* bufs[] = {c->snap_m, c->snap_rs, c->vstore, c->tstore, c->ww, c->mid, c->pan64, c->v64, c->t64, c->gram, c->qr_q1, c->qr_small,
                   c->betas, c->qr_part, c->qr_rowbuf, c->qr_part2, c->qr_wfin,
                   c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,

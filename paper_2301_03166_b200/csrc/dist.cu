@@ -102,6 +102,9 @@ struct abft_dist {
   double* qr_part2 = nullptr;
   double* qr_wfin = nullptr;
   double* gram = nullptr;
+  double* qr_q1 = nullptr;     // n x b: CholeskyQR2 Q of the owner's panel
+  double* qr_small = nullptr;  // QR_SMALL_BUFS x (ld_t x b)
+  QrPanelWork qrw;
   double* ww = nullptr;     // b x ncl
   double* mid = nullptr;    // b x ncl
   double* dmax = nullptr;   // local max scratch
@@ -374,11 +377,8 @@ int begin_qr(abft_dist* d, int64_t k, double* xb) {
   const int64_t lc = (k / d->world) * d->b, ldp = panel_ld(d, k);
   double* D = d->m + p + lc * d->ld;
   ABFT_TRY(fill_matrix(d->st, xb, ldp, n - p, w, 0.0));
-  ABFT_TRY(qr_panel(d->st, D, d->ld, n - p, (int)w, xb, ldp, d->betas, d->qr_part,
-                    d->qr_part_elems, d->qr_rowbuf, d->qr_part2, d->qr_wfin));
-  ABFT_TRY(gemm(d->st, 'T', 'N', (int)w, (int)w, (int)(n - p), 1.0, xb, ldp, xb, ldp, 0.0, nullptr,
-                0, d->gram, d->ld_t, &d->gws));
-  ABFT_TRY(larft(d->st, d->gram, d->ld_t, d->betas, (int)w, xb + ldp * w, d->ld_t));
+  ABFT_TRY(qr_panel_factor(d->st, D, d->ld, n - p, (int)w, xb, ldp, xb + ldp * w, d->ld_t,
+                           d->betas, d->qrw));
   return 0;
 }
 
@@ -857,6 +857,8 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
     if ((rc = dalloc0(&d->qr_part2, 160LL * 32 * b, d->st))) return fail(rc);
     if ((rc = dalloc0(&d->qr_wfin, 32LL * b, d->st))) return fail(rc);
     if ((rc = dalloc0(&d->gram, d->ld_t * b, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_q1, ld * b, d->st))) return fail(rc);
+    if ((rc = dalloc0(&d->qr_small, QR_SMALL_BUFS * d->ld_t * b, d->st))) return fail(rc);
     if ((rc = dalloc0(&d->ww, d->ld_t * ncl, d->st))) return fail(rc);
     if ((rc = dalloc0(&d->mid, d->ld_t * ncl, d->st))) return fail(rc);
   }
@@ -868,8 +870,24 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
   cudaMemset(d->counters, 0, 4 * sizeof(int32_t));
   d->dirty_cap = 1 << 16;
   if (cudaMalloc(&d->dirty, 2 * d->dirty_cap * sizeof(int32_t)) != cudaSuccess) return fail(-1000);
-  if (cudaMalloc(&d->info, sizeof(int)) != cudaSuccess) return fail(-1000);
-  cudaMemset(d->info, 0, sizeof(int));
+  if (cudaMalloc(&d->info, 2 * sizeof(int)) != cudaSuccess) return fail(-1000);
+  cudaMemset(d->info, 0, 2 * sizeof(int));
+  if (kind == ABFT_QR) {
+    QrPanelWork& q = d->qrw;
+    q.q1 = d->qr_q1;
+    q.ldq = ld;
+    q.small = d->qr_small;
+    q.lds = d->ld_t;
+    q.info = d->info + 1;
+    q.gws = &d->gws;
+    q.part = d->qr_part;
+    q.part_elems = d->qr_part_elems;
+    q.rowbuf = d->qr_rowbuf;
+    q.part2 = d->qr_part2;
+    q.wfin = d->qr_wfin;
+    q.gram = d->gram;
+    q.ldg = d->ld_t;
+  }
   cudaEventCreate(&d->e0);
   cudaEventCreate(&d->e1);
   cudaStreamCreateWithFlags(&d->st2, cudaStreamNonBlocking);
@@ -893,7 +911,7 @@ ABFT_API int abft_dist_destroy(abft_dist* d) {
                     d->m,      d->a0,     d->gcsw,   d->csm,    d->grs,       d->rsm,      d->gmax,
                     d->el,     d->er,     d->uw,     d->lw,        d->linv,     d->uinv,
                     d->bext,   d->vstore, d->tstore, d->betas,     d->qr_part,  d->qr_rowbuf,
-                    d->qr_part2, d->qr_wfin, d->gram, d->ww,       d->mid,      d->dmax,
+                    d->qr_part2, d->qr_wfin, d->gram, d->qr_q1, d->qr_small, d->ww,       d->mid,      d->dmax,
                     d->gws.ptr};
   for (double* p : bufs)
     if (p) cudaFree(p);

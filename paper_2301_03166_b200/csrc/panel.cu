@@ -40,6 +40,9 @@ struct Acc {
 // mode 0: LU without pivoting (L unit lower \ U upper in place),
 //         Linv = L^{-1}, Uinv = U^{-1} (formed by tri_inverse_kernel).
 // mode 1: Cholesky, L lower in place with the strict upper part zeroed.
+// mode 2: LU of D - S with S = diag(s), s_c = -sign(pivot candidate) chosen
+//         column by column (|pivot| >= 1, no breakdown): the modified LU of
+//         the Householder reconstruction (qr_panel.cu); s written to sgn.
 // info: 1 + global column of the first breakdown (atomicCAS, first wins).
 // 512 threads viewed as 16 warps x 32 lanes: lanes walk rows, warps walk
 // columns (no integer division in the inner loops); the trailing update of
@@ -47,7 +50,7 @@ struct Acc {
 template <typename T>
 __global__ void __launch_bounds__(DT, 1)
     diag_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
-                       T* Uinv, int64_t ldu, int* info, int64_t col_base) {
+                       T* Uinv, int64_t ldu, int* info, int64_t col_base, T* sgn) {
   extern __shared__ __align__(16) unsigned char sm_raw[];
   T* sm = reinterpret_cast<T*>(sm_raw);
   T* Ps = sm;                 // [NBK][PLD]  Ps[c*PLD + r]
@@ -63,7 +66,7 @@ __global__ void __launch_bounds__(DT, 1)
     for (int c = ty; c < jw; c += DT / 32)
       for (int r = tx; r < rem; r += 32) Ps[c * PLD + r] = D[(jb + r) + (int64_t)(jb + c) * ld];
     __syncthreads();
-    if (mode == 0) {
+    if (mode != 1) {
       // LU: the sub-panel lives in registers, one row per thread; per pivot
       // the owner of row c publishes it (double-buffered) and ONE barrier
       // separates the pivots (the shared-memory form needed three)
@@ -82,7 +85,14 @@ __global__ void __launch_bounds__(DT, 1)
             for (int cc = c; cc < NBK; ++cc) pr[cc] = a[cc];
           }
           __syncthreads();
-          const T piv = pr[c];
+          T piv = pr[c];
+          if (mode == 2) {
+            // s = -sign(x) (x = -0.0 counts as +, as copysign(., x0 or 1) in linalg.py:278)
+            const T sv = (piv < T(0)) ? T(1) : T(-1);
+            piv -= sv;
+            if (tid == c) a[c] = piv;
+            if (tid == 0 && sgn) sgn[jb + c] = sv;
+          }
           if (piv == T(0) || !isfinite(piv)) {
             badf = true;
             if (tid == 0) {
@@ -103,7 +113,7 @@ __global__ void __launch_bounds__(DT, 1)
           if (c < jw) Ps[c * PLD + tid] = a[c];
       }
     }
-    for (int c = 0; c < jw && mode != 0; ++c) {
+    for (int c = 0; c < jw && mode == 1; ++c) {
       const T piv = Ps[c * PLD + c];
       const bool bad = (mode == 0) ? (piv == 0.0 || !isfinite(piv)) : (!(piv > 0.0) || !isfinite(piv));
       if (bad) {
@@ -136,13 +146,13 @@ __global__ void __launch_bounds__(DT, 1)
     if (s_bad) return;
     for (int c = ty; c < jw; c += DT / 32)
       for (int r = tx; r < rem; r += 32)
-        if (mode == 0 || r >= c) D[(jb + r) + (int64_t)(jb + c) * ld] = Ps[c * PLD + r];
+        if (mode != 1 || r >= c) D[(jb + r) + (int64_t)(jb + c) * ld] = Ps[c * PLD + r];
     __syncthreads();
     const int ncols = w - jb - jw;
     if (ncols <= 0) continue;
     const T* Rop;  // right operand of the trailing update: R[l][c] = Rop[c*ldr + l]
     int ldr;
-    if (mode == 0) {
+    if (mode != 1) {
       // U row block: R = L11^{-1} D[jb:jb+jw, jb+jw:w] (unit lower), one column per thread
       for (int c = ty; c < ncols; c += DT / 32)
         for (int i = tx; i < jw; i += 32) Rs[c * 33 + i] = D[(jb + i) + (int64_t)(jb + jw + c) * ld];
@@ -189,8 +199,8 @@ __global__ void __launch_bounds__(DT, 1)
       for (int i = 0; i < 7; ++i) {
         const int r = tx + 32 * i;
         if (r >= nr) continue;
-        if (mode == 0 || r >= c0) D[(jb + jw + r) + (int64_t)(jb + jw + c0) * ld] -= acc[i][0];
-        if (c1ok && (mode == 0 || r >= c0 + 1))
+        if (mode != 1 || r >= c0) D[(jb + jw + r) + (int64_t)(jb + jw + c0) * ld] -= acc[i][0];
+        if (c1ok && (mode != 1 || r >= c0 + 1))
           D[(jb + jw + r) + (int64_t)(jb + jw + c0 + 1) * ld] -= acc[i][1];
       }
     }
@@ -274,7 +284,7 @@ __global__ void __launch_bounds__(DT)
 
 template <typename T>
 static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
-                         T* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
+                         T* Uinv, int64_t ldu, int* info_dev, int64_t col_base, T* sgn) {
   if (w <= 0) return 0;
   if (w > 256) {
     set_last_error("diag_factor: block width %d > 256 (host-level blocking required)", w);
@@ -285,13 +295,13 @@ static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* 
   ABFT_TRY(ensure_smem_attr((const void*)diag_factor_kernel<T>, dsm));
   count_launch();
   diag_factor_kernel<T><<<1, DT, dsm, st>>>(D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev,
-                                            col_base);
+                                            col_base, sgn);
   CUDA_TRY(cudaGetLastError());
   if (Linv || Uinv) {
     ABFT_TRY(ensure_smem_attr((const void*)tri_inverse_kernel<T>, ism));
     dim3 grid((w + NBK - 1) / NBK, Uinv ? 2 : 1);
     count_launch();
-    tri_inverse_kernel<T><<<grid, DT, ism, st>>>(D, ld, w, mode == 0 ? 1 : 0, Linv, ldl, Uinv,
+    tri_inverse_kernel<T><<<grid, DT, ism, st>>>(D, ld, w, mode != 1 ? 1 : 0, Linv, ldl, Uinv,
                                                  ldu, info_dev);
     CUDA_TRY(cudaGetLastError());
   }
@@ -299,12 +309,12 @@ static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* 
 }
 
 int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
-                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
-  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base);
+                double* Uinv, int64_t ldu, int* info_dev, int64_t col_base, double* sgn) {
+  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
 int diag_factor(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv, int64_t ldl,
-                float* Uinv, int64_t ldu, int* info_dev, int64_t col_base) {
-  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base);
+                float* Uinv, int64_t ldu, int* info_dev, int64_t col_base, float* sgn) {
+  return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
 
 // ===========================================================================
@@ -329,7 +339,8 @@ constexpr int QT = 256;
 
 __global__ void __launch_bounds__(QT)
     qr_panel_kernel(double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
-                    double* betas, double* part, double* rowbuf) {
+                    double* betas, double* part, double* rowbuf, const int* gate) {
+  if (gate && *gate == 0) return;  // uniform over the grid: before any grid.sync
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double qsm[];
@@ -421,7 +432,8 @@ __global__ void __launch_bounds__(QT)
 //   T[0:j0, jb] = -T[0:j0, 0:j0] * (Gm[0:j0, jb] * T[jb, jb]).
 __global__ void __launch_bounds__(512)
     larft_kernel(const double* Gm, int64_t ldg, const double* betas, int w, double* T,
-                 int64_t ldt) {
+                 int64_t ldt, const int* gate) {
+  if (gate && *gate == 0) return;
   extern __shared__ double lsm[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (w + 31) / 32;
@@ -489,7 +501,9 @@ constexpr int QR_SMEM = (3 * 32 * QR_RS + 32 * 33 + 4 * 32) * 8;
 
 __global__ void __launch_bounds__(QT, 1)
     qr_panel2_kernel(double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
-                     double* betas, double* part, double* rowbuf, double* part2, double* wfin) {
+                     double* betas, double* part, double* rowbuf, double* part2, double* wfin,
+                     const int* gate) {
+  if (gate && *gate == 0) return;  // uniform over the grid: before any grid.sync
   namespace cg = cooperative_groups;
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double qs[];
@@ -709,7 +723,7 @@ __global__ void __launch_bounds__(QT, 1)
 
 int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* V, int64_t ldv,
              double* betas, double* part, int64_t part_elems, double* rowbuf, double* part2,
-             double* wfin) {
+             double* wfin, const int* gate) {
   if (w <= 0 || nk <= 0) return 0;
   if (part2 && wfin) {
     int dev = 0, sms = 148;
@@ -727,7 +741,7 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     if (G > 152) G = 152;  // the per-column reduction reads 19 x 8 partials
     if ((nk + G - 1) / G <= QR_RMAX && 2LL * G * 32 <= part_elems) {
       ABFT_TRY(ensure_smem_attr((const void*)qr_panel2_kernel, QR_SMEM));
-      void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf, &part2, &wfin};
+      void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf, &part2, &wfin, &gate};
       count_launch();
       CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel2_kernel, dim3(G), dim3(QT), args,
                                            (size_t)QR_SMEM, st));
@@ -754,14 +768,14 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
     set_last_error("qr_panel: kernel cannot be resident");
     return -1;
   }
-  void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf};
+  void* args[] = {&P, &ld, &nk, &w, &V, &ldv, &betas, &part, &rowbuf, &gate};
   count_launch();
   CUDA_TRY(cudaLaunchCooperativeKernel((void*)qr_panel_kernel, dim3(G), dim3(QT), args, smem, st));
   return 0;
 }
 
 int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, int w, double* T,
-          int64_t ldt) {
+          int64_t ldt, const int* gate) {
   if (w <= 0) return 0;
   const size_t nblk = (size_t)(w + 31) / 32;
   size_t smem = std::max((size_t)w * 32, nblk * 2 * 32 * 33) * sizeof(double);
@@ -771,7 +785,7 @@ int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, i
   }
   ABFT_TRY(ensure_smem_attr((const void*)larft_kernel, 200 * 1024));
   count_launch();
-  larft_kernel<<<1, 512, smem, st>>>(Gm, ldg, betas, w, T, ldt);
+  larft_kernel<<<1, 512, smem, st>>>(Gm, ldg, betas, w, T, ldt, gate);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }

@@ -86,6 +86,48 @@ def test_qr_side_data_matches_oracle():
         np.testing.assert_allclose(f._qr_vs[k], o.qr_vs[k], rtol=1e-9, atol=1e-12)
 
 
+@pytest.mark.parametrize("n,b", [(1024, 256), (700, 128), (256, 256), (300, 64)])
+def test_qr_tensor_core_panel_matches_oracle(n, b):
+    """The CholeskyQR2 + Householder-reconstruction panel (qr_panel.cu) gives
+    the reference's V, T and R (linalg.py:260-300) to rounding, including the
+    square last panel (the reference reflects its last column too: tau = 2)."""
+    a = P.generate_test_matrix("qr", n, 5)
+    f = P.Factorization("qr", a, b).run_all()
+    o = O.OracleFactorization("qr", a, b).run_all()
+    for k in range(len(o.qr_t)):
+        np.testing.assert_allclose(f.qr_t[k], o.qr_t[k], rtol=0, atol=1e-12)
+        np.testing.assert_allclose(f._qr_vs[k], o.qr_vs[k], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(f.m, o.m, rtol=0, atol=1e-10 * np.abs(o.m).max())
+    assert P.residual(a, f) <= O.residual(a, o) + 16 * n * 2.220446049250313e-16
+
+
+@pytest.mark.parametrize("case", ["zero_col", "rank_deficient", "ill_conditioned"])
+def test_qr_degenerate_panel_takes_exact_fallback(case):
+    """Panels whose Gram matrix is not safely positive definite (zero or
+    dependent columns: the reference's normx == 0 branches, linalg.py:273-276)
+    or too ill-conditioned for CholeskyQR2 run the per-column panel instead,
+    and still match the reference's V / T / R."""
+    n, b = 384, 64
+    a = P.generate_test_matrix("qr", n, 11).copy()
+    if case == "zero_col":
+        a[:, 5] = 0.0
+    elif case == "rank_deficient":
+        a[:, 70] = 2.0 * a[:, 66] - a[:, 67]
+    else:
+        a[:, 130] = a[:, 129] + 1e-9 * a[:, 131]
+    a = np.asfortranarray(a)
+    f = P.Factorization("qr", a, b).run_all()
+    o = O.OracleFactorization("qr", a, b).run_all()
+    # from the dependent column on, the reflectors of a rank-deficient panel
+    # are rounding noise (not comparable); an exactly zero column is exact
+    k_cmp = {"zero_col": 1, "rank_deficient": 1, "ill_conditioned": 2}[case]
+    for k in range(k_cmp):
+        np.testing.assert_allclose(f.qr_t[k], o.qr_t[k], rtol=0, atol=1e-9)
+        np.testing.assert_allclose(f._qr_vs[k], o.qr_vs[k], rtol=0, atol=1e-9)
+    assert np.all(np.isfinite(f.m))
+    assert P.residual(a, f) < 1e-12
+
+
 def _protocol(kind, n, b, seed, scheme, counts, stop_after_fault=False):
     rng = np.random.default_rng(seed)
     nb = -(-n // b)

@@ -77,12 +77,13 @@ def test_clean_large_run_has_no_false_positives(kind):
     assert P.residual(a, f) < 64 * n * 2.220446049250313e-16
 
 
+@pytest.mark.parametrize("kind", ["lu", "qr"])
 @pytest.mark.parametrize("n,b", [(2048, 256), (1408, 128), (1300, 256)])
-def test_lookahead_fast_path_equals_per_iteration(n, b):
-    """abft_factorize's LU look-ahead (next panel factored on a side stream
-    while the rest of the trailing matrix updates) gives the same reports as
-    run_numeric_iteration, faults at two iterations (those run serialised)."""
-    kind = "lu"
+def test_lookahead_fast_path_equals_per_iteration(kind, n, b):
+    """abft_factorize's look-ahead (LU: next diagonal block, QR: next
+    Householder panel, factored on a side stream while the rest of the
+    trailing matrix updates) gives the same reports as run_numeric_iteration,
+    faults at two iterations (those run serialised)."""
     nb = -(-n // b)
     sched = {1: {P.ErrorKind.D0: 2, P.ErrorKind.D1: 1}, nb - 2: {P.ErrorKind.D0: 1}}
     a = P.generate_test_matrix(kind, n, 9)
