@@ -127,6 +127,20 @@ ABFT_API int abft_dev_sgemm_splitk(void* stream, char transa, char transb, int64
                                    const float* B, int64_t ldb, float beta, const float* C,
                                    int64_t ldc, float* D, int64_t ldd, int splits);
 
+/* diagonal-block factorization on device pointers: the PD kernel of
+ * linalg.py:219-238 (mode 0 LU unpivoted, 1 Cholesky) and mode 2, the
+ * sign-shifted LU of the QR panel's Householder reconstruction (linalg.py:
+ * 260-300). D (w x w, w <= 256) in place; Linv = L^{-1}, Uinv = U^{-1} (LU
+ * modes; may be NULL); sgn: the mode-2 signs. variant 0 = one CTA, 1 = the
+ * thread-block-cluster kernel. info_dev: device int set to 1 + the column of
+ * the first breakdown (LU pivot 0 / non-finite, Cholesky pivot <= 0). */
+ABFT_API int abft_dev_diag_factor(void* stream, int variant, int mode, int64_t w, double* D,
+                                  int64_t ld, double* Linv, int64_t ldl, double* Uinv,
+                                  int64_t ldu, int* info_dev, double* sgn);
+ABFT_API int abft_dev_sdiag_factor(void* stream, int variant, int mode, int64_t w, float* D,
+                                   int64_t ld, float* Linv, int64_t ldl, float* Uinv, int64_t ldu,
+                                   int* info_dev, float* sgn);
+
 /* factorization context: replaces Factorization (linalg.py:159-359) -------- */
 typedef struct abft_ctx abft_ctx;
 

@@ -71,6 +71,8 @@ SIGNATURES = [
     ("abft_dev_sgemm_splitk", _I, [_P, ctypes.c_char, ctypes.c_char, _I64, _I64, _I64,
                                    ctypes.c_float, _P, _I64, _P, _I64, ctypes.c_float, _P, _I64,
                                    _P, _I64, _I]),
+    ("abft_dev_diag_factor", _I, [_P, _I, _I, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
+    ("abft_dev_sdiag_factor", _I, [_P, _I, _I, _I64, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
     ("abft_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
     ("abft_destroy", _I, [_P]),
     ("abft_set_matrix", _I, [_P, _D, _I64]),

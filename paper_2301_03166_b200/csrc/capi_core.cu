@@ -2,6 +2,7 @@
 #include "abft_b200.h"
 #include "abft_kernels.cuh"
 #include "gemm.cuh"
+#include "panel.cuh"
 #include "sgemm.cuh"
 
 using namespace abft;
@@ -118,6 +119,34 @@ ABFT_API int abft_dev_sgemm(void* stream, char transa, char transb, int64_t m, i
                             float beta, const float* C, int64_t ldc, float* D, int64_t ldd) {
   return abft_dev_sgemm_splitk(stream, transa, transb, m, n, k, alpha, A, lda, B, ldb, beta, C, ldc,
                                D, ldd, 1);
+}
+
+// Diagonal-block factorization on device pointers (the PD kernel of
+// linalg.py:219-238; mode 2 = the sign-shifted LU of the QR reconstruction).
+// variant 0: one-CTA diag_factor + tri_inverse; 1: the cluster kernel.
+// info_dev: device int, 1 + column of the first breakdown (0 if none).
+ABFT_API int abft_dev_diag_factor(void* stream, int variant, int mode, int64_t w, double* D,
+                                  int64_t ld, double* Linv, int64_t ldl, double* Uinv,
+                                  int64_t ldu, int* info_dev, double* sgn) {
+  if (w < 1 || w > 256 || mode < 0 || mode > 2 || variant < 0 || variant > 1) {
+    set_last_error("abft_dev_diag_factor: bad arguments");
+    return ABFT_E_INVALID;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return variant ? diag_factor_fast(st, D, ld, (int)w, mode, Linv, ldl, Uinv, ldu, info_dev, 0, sgn)
+                 : diag_factor(st, D, ld, (int)w, mode, Linv, ldl, Uinv, ldu, info_dev, 0, sgn);
+}
+
+ABFT_API int abft_dev_sdiag_factor(void* stream, int variant, int mode, int64_t w, float* D,
+                                   int64_t ld, float* Linv, int64_t ldl, float* Uinv, int64_t ldu,
+                                   int* info_dev, float* sgn) {
+  if (w < 1 || w > 256 || mode < 0 || mode > 2 || variant < 0 || variant > 1) {
+    set_last_error("abft_dev_sdiag_factor: bad arguments");
+    return ABFT_E_INVALID;
+  }
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  return variant ? diag_factor_fast(st, D, ld, (int)w, mode, Linv, ldl, Uinv, ldu, info_dev, 0, sgn)
+                 : diag_factor(st, D, ld, (int)w, mode, Linv, ldl, Uinv, ldu, info_dev, 0, sgn);
 }
 
 }  // extern "C"

@@ -29,6 +29,17 @@ int qr_panel(cudaStream_t st, double* P, int64_t ld, int64_t nk, int w, double* 
 int larft(cudaStream_t st, const double* Gm, int64_t ldg, const double* betas, int w, double* T,
           int64_t ldt, const int* gate = nullptr);
 
+// diag_factor on a thread-block cluster of ceil(w/32) CTAs (small_factor.cu):
+// same contract, the inverses from the same launch; needs that many free SMs
+// at once (side streams next to a persistent GEMM keep diag_factor).
+// ABFT_NO_CLUSTER_FACTOR=1 routes it to diag_factor.
+int diag_factor_fast(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv,
+                     int64_t ldl, double* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
+                     double* sgn = nullptr);
+int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv,
+                     int64_t ldl, float* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
+                     float* sgn = nullptr);
+
 struct GemmWorkspace;
 
 // Workspace of qr_panel_factor.

@@ -164,10 +164,17 @@ int qr_panel_factor(cudaStream_t st, double* P, int64_t ld, int64_t m, int w, do
   GemmWorkspace* g = ws.gws;
   const int mi = (int)m;
   CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), st));
+  // the cluster diagonal-block kernel needs ceil(w/32) co-resident SMs: only
+  // when the panel owns the GPU (beside the look-ahead's persistent GEMM the
+  // cluster cannot be placed until that GEMM drains)
+  auto dfac = [&](double* D, int mode, double* Li, double* Ui, double* sg) {
+    return max_ctas > 0 ? diag_factor(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg)
+                        : diag_factor_fast(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg);
+  };
   // CholeskyQR, pass 1
   ABFT_TRY(gemm_capped(st, 'T', 'N', w, w, mi, 1.0, P, ld, P, ld, 0.0, nullptr, 0, G1, s, g,
                        max_ctas));
-  ABFT_TRY(diag_factor(st, G1, s, w, 1, L1i, s, nullptr, 0, ws.info, 0));
+  ABFT_TRY(dfac(G1, 1, L1i, nullptr, nullptr));
   ABFT_TRY(gemm_capped(st, 'N', 'T', mi, w, w, 1.0, P, ld, L1i, s, 0.0, nullptr, 0, Q1, lq, g,
                        max_ctas));
   // pass 2
@@ -176,14 +183,14 @@ int qr_panel_factor(cudaStream_t st, double* P, int64_t ld, int64_t m, int w, do
   count_launch();
   ortho_check_kernel<<<(w * w + 255) / 256, 256, 0, st>>>(G2, s, w, ws.info);
   CUDA_TRY(cudaGetLastError());
-  ABFT_TRY(diag_factor(st, G2, s, w, 1, L2i, s, nullptr, 0, ws.info, 0));
+  ABFT_TRY(dfac(G2, 1, L2i, nullptr, nullptr));
   // R = R2 R1 = L2^T L1^T
   ABFT_TRY(gemm_capped(st, 'T', 'T', w, w, w, 1.0, G2, s, G1, s, 0.0, nullptr, 0, R, s, g,
                        max_ctas));
   // reconstruction: X = Q_top = Q1[0:w] R2^{-1}; Q_top - S = Y U
   ABFT_TRY(gemm_capped(st, 'N', 'T', w, w, w, 1.0, Q1, lq, L2i, s, 0.0, nullptr, 0, X, s, g,
                        max_ctas));
-  ABFT_TRY(diag_factor(st, X, s, w, 2, Yi, s, Ui, s, ws.info, 0, sg));
+  ABFT_TRY(dfac(X, 2, Yi, Ui, sg));
   // V[w:m] = Q1[w:m] R2^{-1} U^{-1}
   ABFT_TRY(gemm_capped(st, 'T', 'N', w, w, w, 1.0, L2i, s, Ui, s, 0.0, nullptr, 0, Mt, s, g,
                        max_ctas));

@@ -1,0 +1,498 @@
+// Diagonal-block factorization on a thread-block cluster (K5 PD, fast path).
+//
+// Same contract as diag_factor (panel.cuh): the w x w block D is factored in
+// place -- LU unpivoted (linalg.py:230-238, mode 0), Cholesky (linalg.py:
+// 219-229, mode 1) or the sign-shifted LU of the Householder reconstruction
+// (mode 2, qr_panel.cu) -- and the triangular inverses L^{-1} (and U^{-1})
+// come out of the same launch. diag_factor runs all of it on one CTA (a
+// 32-column sub-panel loop, ~0.35 ms + 0.14 ms for the inverses at w = 256);
+// here CTA r of a cluster of nb = ceil(w/32) CTAs owns block column r in its
+// shared memory and the blocked right-looking algorithm runs across the
+// cluster over distributed shared memory:
+//
+//   step j:  CTA j factors block column j (rows >= 32j, one row per thread,
+//            register resident, one barrier per pivot) and inverts its
+//            diagonal block (L_jj^{-1}, and U_jj^{-1} for LU);
+//            cluster barrier;
+//            CTA r > j updates its block column from CTA j's panel, read in
+//            place through DSMEM (LU: U_jr = L_jj^{-1} A_jr, then
+//            A_ir -= L_ij U_jr; Cholesky: A_ir -= L_ij L_rj^T);
+//            CTA r <= j advances block column r of X = L^{-1} by the same
+//            elimination applied to the identity (X_jr = L_jj^{-1} X_jr,
+//            X_ir -= L_ij X_jr), so the inverse costs no extra phase.
+//   LU then forms U^{-1} by block back substitution over the final U columns
+//   (no barriers: the factor is read-only by then).
+//
+// w is padded to 32 nb with the identity (a block-diagonal extension that
+// changes no pivot of the real block). Breakdown follows the reference: LU
+// pivot == 0 or non-finite, Cholesky pivot <= 0 or non-finite; info gets
+// 1 + (col_base + column) of the first one and nothing else is written.
+#include <cooperative_groups.h>
+
+#include "panel.cuh"
+
+namespace abft {
+
+namespace {
+
+namespace cg = cooperative_groups;
+
+#ifdef CF_TRACE
+__device__ long long g_cf_trace[8][64];
+__device__ long long g_cf_clk[4];
+#define CF_MARK(slot)                                                         \
+  do {                                                                        \
+    if (threadIdx.x == 0 && (slot) < 64) {                                    \
+      long long t_;                                                           \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
+      g_cf_trace[cluster.block_rank()][(slot)] = t_;                          \
+    }                                                                         \
+  } while (0)
+#else
+#define CF_MARK(slot) \
+  do {                \
+  } while (0)
+#endif
+
+constexpr int CF_T = 256;    // threads per CTA (8 warps)
+constexpr int CF_MAXB = 8;   // cluster size limit (portable): w <= 256
+constexpr int TS = 33;       // stride of the 32 x 32 tiles
+
+// Out[i, c] -= sum_l A[i + l*lda] * B[l*TS + c] for rows i in [r0, r1)
+// (r1 - r0 <= 224), c < 32. A may live in another CTA's shared memory.
+template <typename T>
+ABFT_DEVINL void tile_update(T* Out, int ldo, int r0, int r1, const T* A, int lda, const T* B) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  T acc[7][4];
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = T(0);
+#pragma unroll 4
+  for (int l = 0; l < 32; ++l) {
+    T b[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) b[e] = B[l * TS + ty * 4 + e];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const int i = r0 + tx + 32 * q;
+      const T a = (i < r1) ? A[i + l * lda] : T(0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[q][e] = fma(a, b[e], acc[q][e]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const int i = r0 + tx + 32 * q;
+    if (i < r1) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Out[i + (ty * 4 + e) * ldo] -= acc[q][e];
+    }
+  }
+}
+
+// Dst[r0:r1, 0:32] = Src[r0:r1, 0:32] (column stride ld, r0/r1 even), Src
+// possibly in another CTA of the cluster: 16-byte loads, all issued before
+// any store so one DSMEM round trip covers the whole panel.
+template <typename T>
+ABFT_DEVINL void panel_copy(T* Dst, const T* Src, int src_rank, int ld, int r0, int r1) {
+  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
+  const int per_col = (r1 - r0) / V;
+  const int total = 32 * per_col;
+  constexpr int U = 8;
+  uint32_t rbase;  // Src in CTA src_rank's shared window (ld.shared::cluster)
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
+               : "=r"(rbase)
+               : "r"(smem_u32(Src)), "r"(src_rank));
+  for (int base = threadIdx.x; base < total; base += U * CF_T) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * CF_T;
+      if (idx < total) {
+        const int c = idx / per_col, e = r0 + (idx - c * per_col) * V;
+        const uint32_t a = rbase + (uint32_t)((e + c * ld) * sizeof(T));
+        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                     : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
+                     : "r"(a));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int idx = base + u * CF_T;
+      if (idx < total) {
+        const int c = idx / per_col, e = r0 + (idx - c * per_col) * V;
+        *reinterpret_cast<float4*>(Dst + e + c * ld) = v[u];
+      }
+    }
+  }
+}
+
+// Y[32j : 32j+32, :] = Tm (col-major, stride TS) * Y[32j : 32j+32, :]; the
+// result also lands in B (row-major tile B[l*TS + c]) for the following
+// rank-32 update. Ends with a barrier.
+template <typename T>
+ABFT_DEVINL void tile_tri_apply(T* Y, int ldy, int j, const T* Tm, T* B) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  T o[4] = {T(0), T(0), T(0), T(0)};
+#pragma unroll 8
+  for (int l = 0; l < 32; ++l) {
+    const T t = Tm[tx + l * TS];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = fma(t, Y[(32 * j + l) + (ty * 4 + e) * ldy], o[e]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    Y[(32 * j + tx) + (ty * 4 + e) * ldy] = o[e];
+    B[tx * TS + ty * 4 + e] = o[e];
+  }
+  __syncthreads();
+}
+
+// Inverse of the 32 x 32 diagonal block of a column block (rows 32j..): lane
+// = result column. lower: L^{-1} (unit: LU's L), else U^{-1} (upper, non-unit).
+template <typename T>
+__device__ __noinline__ void tile_inverse(const T* C, int ldc, int j, bool lower, bool unit, T* Out) {
+  const int lane = threadIdx.x & 31;
+  const T* Dg = C + 32 * j;
+  T x[32];
+  if (lower) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      T s = (i == lane) ? T(1) : T(0);
+#pragma unroll
+      for (int k = 0; k < i; ++k) s = fma(-Dg[i + k * ldc], x[k], s);
+      x[i] = unit ? s : s / Dg[i + i * ldc];
+    }
+  } else {
+#pragma unroll
+    for (int i = 31; i >= 0; --i) {
+      T s = (i == lane) ? T(1) : T(0);
+#pragma unroll
+      for (int k = i + 1; k < 32; ++k) s = fma(-Dg[i + k * ldc], x[k], s);
+      x[i] = s / Dg[i + i * ldc];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) Out[i + lane * TS] = x[i];
+}
+
+// Factor the 32 x 32 diagonal block at rows c0.. of the block column (Cs,
+// column stride Wp) in place, by ONE warp: lane t holds row t in registers,
+// the pivot row goes through shared memory (pr) with warp-level syncs only.
+// LU (mode 0), sign-shifted LU (mode 2; s -> sgn) or Cholesky (mode 1, lower
+// part meaningful). Returns the local column of the first breakdown or -1
+// (uniform over the warp).
+template <typename T>
+__device__ __noinline__ int diag_block_factor(T* Cs, int Wp, int c0, int mode, T* pr, T* sgn,
+                                              int w) {
+  const int t = threadIdx.x & 31;
+  const bool lu = mode != 1;
+  T* D = Cs + c0;
+  T a[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c) a[c] = D[t + c * Wp];
+  int badc = -1;
+#ifdef CF_TRACE
+  long long tk[5];
+#endif
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+#ifdef CF_TRACE
+    if ((c & 7) == 0) tk[c >> 3] = clock64();
+#endif
+    if (badc < 0) {
+      T* p = pr + (c & 1) * 32;
+      if (lu) {
+        if (t == c) {
+#pragma unroll
+          for (int cc = c; cc < 32; ++cc) p[cc] = a[cc];
+        }
+      } else if (t >= c) {
+        p[t] = a[c];  // column c (the symmetric pivot row)
+      }
+      __syncwarp();
+      T piv = p[c];
+      if (mode == 2) {
+        // s = -sign(x), x = -0.0 counted as + (copysign(., x0 or 1), linalg.py:278)
+        const T sv = (piv < T(0)) ? T(1) : T(-1);
+        piv -= sv;
+        if (t == c) a[c] = piv;
+        if (t == 0 && sgn && c0 + c < w) sgn[c0 + c] = sv;
+      }
+      const bool brk = lu ? (piv == T(0) || !isfinite(piv)) : (!(piv > T(0)) || !isfinite(piv));
+      if (brk) {
+        badc = c;
+      } else if (lu) {
+        if (t > c) {
+          const T l = a[c] / piv;
+          a[c] = l;
+#pragma unroll
+          for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc], a[cc]);
+        }
+      } else {
+        const T d = sqrt(piv);
+        if (t == c) {
+          a[c] = d;
+        } else if (t > c) {
+          const T rd = T(1) / d;
+          const T l = a[c] / d;
+          a[c] = l;
+#pragma unroll
+          for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc] * rd, a[cc]);
+        }
+      }
+    }
+  }
+#ifdef CF_TRACE
+  tk[4] = clock64();
+  if (t == 0 && c0 == 0)
+    for (int q = 0; q < 4; ++q) g_cf_clk[q] = tk[q + 1] - tk[q];
+#endif
+  if (badc < 0) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c) D[t + c * Wp] = a[c];
+  }
+  __syncwarp();
+  return badc;
+}
+
+// Out[i, c] = sum_l Out[i, l] * B(l, c), B(l, c) = B[l*bl + c*bc], rows
+// [r0, r1) (r1 - r0 <= 224): the panel solve L21 = A21 U11^{-1} (LU) or
+// A21 L11^{-T} (Cholesky) against the inverted diagonal block.
+template <typename T>
+ABFT_DEVINL void tile_mul_inplace(T* Out, int ldo, int r0, int r1, const T* B, int bl, int bc) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  T acc[7][4];
+#pragma unroll
+  for (int q = 0; q < 7; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[q][e] = T(0);
+#pragma unroll 4
+  for (int l = 0; l < 32; ++l) {
+    T b[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) b[e] = B[l * bl + (ty * 4 + e) * bc];
+#pragma unroll
+    for (int q = 0; q < 7; ++q) {
+      const int i = r0 + tx + 32 * q;
+      const T a = (i < r1) ? Out[i + l * ldo] : T(0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[q][e] = fma(a, b[e], acc[q][e]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 7; ++q) {
+    const int i = r0 + tx + 32 * q;
+    if (i < r1) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) Out[i + (ty * 4 + e) * ldo] = acc[q][e];
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CF_T, 1)
+    cluster_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl, T* Uinv,
+                          int64_t ldu, int* info, int64_t col_base, T* sgn) {
+  cg::cluster_group cluster = cg::this_cluster();
+  extern __shared__ __align__(16) unsigned char cf_raw[];
+  const int nb = (int)cluster.num_blocks();
+  const int r = (int)cluster.block_rank();
+  const int Wp = 32 * nb;  // padded order = column stride of Cs / Xs
+  T* Cs = reinterpret_cast<T*>(cf_raw);  // block column r of the matrix
+  T* Xs = Cs + 32 * Wp;                  // block column r of L^{-1}, then of U^{-1}
+  T* Ps = Xs + 32 * Wp;                  // local copy of the step's panel
+  T* Li = Ps + 32 * Wp;                  // L_rr^{-1} (col-major, stride TS)
+  T* Ui = Li + 32 * TS;                  // U_rr^{-1}
+  T* Lj = Ui + 32 * TS;                  // copy of the step's L_jj^{-1}
+  T* Bt = Lj + 32 * TS;                  // right operand of the rank-32 update
+  T* pr = Bt + 32 * TS;                  // [2][32] pivot rows
+  int* s_bad = reinterpret_cast<int*>(pr + 64);
+  const int tid = threadIdx.x, ty = tid >> 5;
+  const bool lu = mode != 1;
+  const int c0 = 32 * r;
+
+  // load the block column (identity padding), X = I on block r
+  for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
+    const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
+    Cs[idx] = (i < w && gc < w) ? D[i + (int64_t)gc * ld] : (i == gc ? T(1) : T(0));
+    Xs[idx] = (i == gc) ? T(1) : T(0);
+  }
+  if (tid == 0) *s_bad = 0;
+  __syncthreads();
+
+  bool bad = false;
+  CF_MARK(0);
+  for (int j = 0; j < nb && !bad; ++j) {
+    if (r == j) {
+      // ---- factor block column j: the diagonal block by one warp, its
+      //      inverses by two, then the rows below against the inverse ----
+      if (ty == 0) {
+        const int badc = diag_block_factor(Cs, Wp, c0, mode, pr, sgn, w);
+        if (badc >= 0 && (tid & 31) == 0) {
+          *s_bad = 1;
+          if (c0 + badc < w) atomicCAS(info, 0, (int)(col_base + c0 + badc + 1));
+        }
+      }
+      __syncthreads();
+      CF_MARK(44 + 2 * j);
+      if (*s_bad == 0) {
+        if (ty == 0) tile_inverse(Cs, Wp, j, true, lu, Li);
+        if (ty == 1 && lu) tile_inverse(Cs, Wp, j, false, false, Ui);
+        __syncthreads();
+        CF_MARK(45 + 2 * j);
+        if (c0 + 32 < Wp) {
+          if (lu)
+            tile_mul_inplace(Cs, Wp, c0 + 32, Wp, Ui, 1, TS);   // L21 = A21 U11^{-1}
+          else
+            tile_mul_inplace(Cs, Wp, c0 + 32, Wp, Li, TS, 1);   // L21 = A21 L11^{-T}
+        }
+      }
+      __syncthreads();
+      CF_MARK(1 + 4 * j);
+    }
+    cluster.sync();  // panel j, its inverses and its flag are visible
+    CF_MARK(2 + 4 * j);
+    const int* badj = cluster.map_shared_rank(s_bad, j);
+    if (*badj) {
+      bad = true;
+      break;
+    }
+    const T* Pj = Cs;
+    if (r != j) {
+      panel_copy(Ps, Cs, j, Wp, 32 * j, Wp);
+      Pj = Ps;
+    }
+    const T* Lsrc = (r == j) ? Li : cluster.map_shared_rank(Li, j);
+    for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Lsrc[idx];
+    __syncthreads();
+    CF_MARK(3 + 4 * j);
+    if (r > j) {
+      if (lu) {
+        tile_tri_apply(Cs, Wp, j, Lj, Bt);  // U_jr
+        tile_update(Cs, Wp, 32 * j + 32, Wp, Pj, Wp, Bt);
+      } else {
+        for (int idx = tid; idx < 32 * 32; idx += CF_T) {
+          const int l = idx >> 5, cc = idx & 31;
+          Bt[l * TS + cc] = Pj[(c0 + cc) + l * Wp];  // L_rj^T
+        }
+        __syncthreads();
+        tile_update(Cs, Wp, c0, Wp, Pj, Wp, Bt);
+      }
+    } else {
+      tile_tri_apply(Xs, Wp, j, Lj, Bt);
+      if (32 * j + 32 < Wp) tile_update(Xs, Wp, 32 * j + 32, Wp, Pj, Wp, Bt);
+    }
+    __syncthreads();
+    CF_MARK(4 + 4 * j);
+  }
+  CF_MARK(40);
+  cluster.sync();  // every block column final; nobody reads a panel any more
+  CF_MARK(41);
+  if (!bad) {
+    // factor out (Cholesky: lower part, zeros above)
+    for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
+      const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
+      if (i < w && gc < w) D[i + (int64_t)gc * ld] = (lu || i >= gc) ? Cs[idx] : T(0);
+    }
+    if (Linv) {
+      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
+        const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
+        if (i < w && gc < w) Linv[i + (int64_t)gc * ldl] = (i >= c0) ? Xs[idx] : T(0);
+      }
+    }
+    if (lu && Uinv) {
+      // U^{-1}, block column r: Y = E_r, then for j = r..0:
+      //   Y_jr = U_jj^{-1} Y_jr,  Y_ir -= U_ij Y_jr (i < j)  (U_ij in CTA j)
+      __syncthreads();
+      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
+        const int i = idx % Wp, c = idx / Wp;
+        Xs[idx] = (i == c0 + c) ? T(1) : T(0);
+      }
+      __syncthreads();
+      for (int j = r; j >= 0; --j) {
+        const T* Usrc = (r == j) ? Ui : cluster.map_shared_rank(Ui, j);
+        for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Usrc[idx];
+        const T* Uj = Cs;
+        if (j != r && j > 0) {
+          panel_copy(Ps, Cs, j, Wp, 0, 32 * j);
+          Uj = Ps;
+        }
+        __syncthreads();
+        tile_tri_apply(Xs, Wp, j, Lj, Bt);
+        if (j > 0) tile_update(Xs, Wp, 0, 32 * j, Uj, Wp, Bt);
+        __syncthreads();
+      }
+      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
+        const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
+        if (i < w && gc < w) Uinv[i + (int64_t)gc * ldu] = (i < c0 + 32) ? Xs[idx] : T(0);
+      }
+    }
+  }
+  CF_MARK(42);
+  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
+  CF_MARK(43);
+}
+
+template <typename T>
+size_t cf_smem_bytes(int nb) {
+  return (size_t)(3 * 32 * 32 * nb + 4 * 32 * TS + 64) * sizeof(T) + 16;
+}
+
+template <typename T>
+int cluster_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
+                     T* Uinv, int64_t ldu, int* info_dev, int64_t col_base, T* sgn) {
+  const int nb = (w + 31) / 32;
+  const size_t smem = cf_smem_bytes<T>(nb);
+  ABFT_TRY(ensure_smem_attr((const void*)cluster_factor_kernel<T>, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(CF_T);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = nb;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  count_launch();
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, cluster_factor_kernel<T>, D, ld, w, mode, Linv, ldl, Uinv,
+                              ldu, info_dev, col_base, sgn));
+  return 0;
+}
+
+bool cluster_disabled() {
+  static const int v = [] {
+    const char* e = getenv("ABFT_NO_CLUSTER_FACTOR");  // A/B knob: 1 = one-CTA diag_factor
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  return v == 1;
+}
+
+}  // namespace
+
+int diag_factor_fast(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv,
+                     int64_t ldl, double* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
+                     double* sgn) {
+  if (w <= 0) return 0;
+  if (w > 32 * CF_MAXB || cluster_disabled())
+    return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+  return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+}
+
+int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv,
+                     int64_t ldl, float* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
+                     float* sgn) {
+  if (w <= 0) return 0;
+  if (w > 32 * CF_MAXB || cluster_disabled())
+    return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+  return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+}
+
+}  // namespace abft

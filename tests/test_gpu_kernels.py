@@ -121,3 +121,90 @@ def test_inject_out_of_range_raises():
     m = _rm(8, 1)
     with pytest.raises(IndexError):
         P.inject_faults(m, [P.InjectedFault(P.ErrorKind.D0, 8, 0, 1.0)])
+
+
+def _np_lu_nopiv(a, shift):
+    """Unpivoted LU of a (mode 0) or of a - diag(s), s_c = -sign(pivot) (mode 2)."""
+    a = a.copy()
+    w = a.shape[0]
+    s = np.zeros(w)
+    for c in range(w):
+        if shift:
+            s[c] = 1.0 if a[c, c] < 0 else -1.0
+            a[c, c] -= s[c]
+        a[c + 1:, c] /= a[c, c]
+        a[c + 1:, c + 1:] -= np.outer(a[c + 1:, c], a[c, c + 1:])
+    return a, s
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("w", [256, 200, 128, 64, 33, 1])
+@pytest.mark.parametrize("prec", ["f64", "f32"])
+def test_diag_factor_variants(variant, mode, w, prec):
+    """The diagonal-block factorization (one-CTA diag_factor and the cluster
+    kernel): factors and triangular inverses against numpy in fp64
+    (linalg.py:219-238; mode 2 = the sign-shifted LU of qr_panel.cu)."""
+    torch = _torch()
+    lib = _lib.load()
+    rng = np.random.default_rng(w * 10 + mode)
+    a = rng.uniform(-1, 1, (w, w))
+    if mode == 0:
+        a += np.diag(np.abs(a).sum(axis=1) + 1.0)
+    elif mode == 1:
+        a = a @ a.T + w * np.eye(w)
+    else:
+        a = np.linalg.qr(rng.standard_normal((w, w)))[0]  # the reconstruction's input: orthogonal
+    dt = torch.float64 if prec == "f64" else torch.float32
+    ld = w + 3
+    buf = torch.zeros((w, ld), dtype=dt, device="cuda")
+    buf[:, :w] = torch.from_numpy(a.T.copy()).to(dt)  # column-major: column j = row j of buf
+    D = buf
+    Li = torch.zeros((w, ld), dtype=dt, device="cuda")
+    Ui = torch.zeros((w, ld), dtype=dt, device="cuda")
+    sg = torch.zeros(w, dtype=dt, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fn = lib.abft_dev_diag_factor if prec == "f64" else lib.abft_dev_sdiag_factor
+    rc = fn(None, variant, mode, w, D.data_ptr(), ld, Li.data_ptr(), ld,
+            Ui.data_ptr() if mode != 1 else None, ld, info.data_ptr(), sg.data_ptr())
+    assert rc == 0, _lib.last_error()
+    torch.cuda.synchronize()
+    assert int(info.item()) == 0
+    got = D[:, :w].double().cpu().numpy().T
+    linv = Li[:, :w].double().cpu().numpy().T
+    tol = 1e-11 if prec == "f64" else 5e-4
+    if mode == 1:
+        ref = np.linalg.cholesky(a)
+        np.testing.assert_allclose(got, ref, atol=tol * np.abs(ref).max(), rtol=0)
+        np.testing.assert_allclose(linv, np.linalg.inv(ref), atol=tol * 10, rtol=0)
+    else:
+        ref, s = _np_lu_nopiv(a, mode == 2)
+        np.testing.assert_allclose(got, ref, atol=tol * np.abs(ref).max(), rtol=0)
+        L = np.tril(ref, -1) + np.eye(w)
+        U = np.triu(ref)
+        np.testing.assert_allclose(linv, np.linalg.inv(L), atol=tol * 10 * max(1, np.abs(np.linalg.inv(L)).max()), rtol=0)
+        uinv = Ui[:, :w].double().cpu().numpy().T
+        np.testing.assert_allclose(uinv, np.linalg.inv(U), atol=tol * 10 * max(1, np.abs(np.linalg.inv(U)).max()), rtol=0)
+        if mode == 2:
+            np.testing.assert_array_equal(sg.double().cpu().numpy(), s)
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("mode,col", [(1, 77), (0, 150)])
+def test_diag_factor_breakdown_column(variant, mode, col):
+    """Breakdown reports the reference's column (Cholesky pivot <= 0, LU zero
+    pivot: linalg.py:223-224, :234-235) from both kernels."""
+    torch = _torch()
+    lib = _lib.load()
+    w = 256
+    a = np.eye(w) * 4.0
+    a[col, col] = -1.0 if mode == 1 else 0.0
+    D = torch.from_numpy(a.T.copy()).cuda()
+    Li = torch.zeros_like(D)
+    Ui = torch.zeros_like(D)
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rc = lib.abft_dev_diag_factor(None, variant, mode, w, D.data_ptr(), w, Li.data_ptr(), w,
+                                  Ui.data_ptr() if mode == 0 else None, w, info.data_ptr(), None)
+    assert rc == 0
+    torch.cuda.synchronize()
+    assert int(info.item()) == col + 1
