@@ -91,40 +91,41 @@ ABFT_DEVINL void tile_update(T* Out, int ldo, int r0, int r1, const T* A, int ld
   }
 }
 
-// Dst[r0:r1, 0:32] = Src[r0:r1, 0:32] (column stride ld, r0/r1 even), Src
-// possibly in another CTA of the cluster: 16-byte loads, all issued before
-// any store so one DSMEM round trip covers the whole panel.
+// Dst[r0:r1, 0:32] (column stride ldd) = block column starting at global
+// column c0 of the w x w matrix G (ld), rows r0..r1 (r1 - r0 <= 256), with
+// the identity padding beyond w. Warp = 4 columns, lane = rows; all loads
+// are issued before the stores (one L2 round trip).
 template <typename T>
-ABFT_DEVINL void panel_copy(T* Dst, const T* Src, int src_rank, int ld, int r0, int r1) {
-  constexpr int V = 16 / sizeof(T);  // elements per 16-byte vector
-  const int per_col = (r1 - r0) / V;
-  const int total = 32 * per_col;
-  constexpr int U = 8;
-  uint32_t rbase;  // Src in CTA src_rank's shared window (ld.shared::cluster)
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n"
-               : "=r"(rbase)
-               : "r"(smem_u32(Src)), "r"(src_rank));
-  for (int base = threadIdx.x; base < total; base += U * CF_T) {
-    float4 v[U];
+ABFT_DEVINL void global_block_column(T* Dst, int ldd, const T* G, int64_t ld, int w, int c0, int r0,
+                                     int r1) {
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  T v[4][8];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = base + u * CF_T;
-      if (idx < total) {
-        const int c = idx / per_col, e = r0 + (idx - c * per_col) * V;
-        const uint32_t a = rbase + (uint32_t)((e + c * ld) * sizeof(T));
-        asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
-                     : "=f"(v[u].x), "=f"(v[u].y), "=f"(v[u].z), "=f"(v[u].w)
-                     : "r"(a));
-      }
-    }
+  for (int q = 0; q < 4; ++q) {
+    const int gc = c0 + ty + 8 * q;
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int idx = base + u * CF_T;
-      if (idx < total) {
-        const int c = idx / per_col, e = r0 + (idx - c * per_col) * V;
-        *reinterpret_cast<float4*>(Dst + e + c * ld) = v[u];
-      }
+    for (int e = 0; e < 8; ++e) {
+      const int i = r0 + tx + 32 * e;
+      v[q][e] = (i < r1 && i < w && gc < w) ? G[i + (int64_t)gc * ld] : (i == gc ? T(1) : T(0));
     }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int i = r0 + tx + 32 * e;
+      if (i < r1) Dst[i + (ty + 8 * q) * ldd] = v[q][e];
+    }
+}
+
+// Tile (col-major, stride TS) = the 32 x 32 diagonal block at (c0, c0) of G
+// (identity padding beyond w).
+template <typename T>
+ABFT_DEVINL void global_tile(T* Tile, const T* G, int64_t ld, int w, int c0) {
+  for (int idx = threadIdx.x; idx < 32 * 32; idx += CF_T) {
+    const int i = idx & 31, c = idx >> 5;
+    Tile[i + c * TS] = (c0 + i < w && c0 + c < w) ? G[(c0 + i) + (int64_t)(c0 + c) * ld]
+                                                  : (i == c ? T(1) : T(0));
   }
 }
 
@@ -150,28 +151,35 @@ ABFT_DEVINL void tile_tri_apply(T* Y, int ldy, int j, const T* Tm, T* B) {
   __syncthreads();
 }
 
-// Inverse of the 32 x 32 diagonal block of a column block (rows 32j..): lane
-// = result column. lower: L^{-1} (unit: LU's L), else U^{-1} (upper, non-unit).
+// Inverse of the 32 x 32 diagonal block of a column block (rows 32j..), one
+// warp, lane = result column. Right-looking substitution: as soon as x_k is
+// final every pending partial sum takes its term (independent FMAs), so the
+// dependent chain per step is one multiply + one FMA; the diagonal's
+// reciprocals are formed up front (one division per lane, in parallel).
+// lower: L^{-1} (unit: LU's L), else U^{-1} (upper, non-unit).
 template <typename T>
 __device__ __noinline__ void tile_inverse(const T* C, int ldc, int j, bool lower, bool unit, T* Out) {
   const int lane = threadIdx.x & 31;
   const T* Dg = C + 32 * j;
+  const T rd_own = unit ? T(1) : T(1) / Dg[lane + lane * ldc];
   T x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = (i == lane) ? T(1) : T(0);
   if (lower) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      T s = (i == lane) ? T(1) : T(0);
+    for (int k = 0; k < 32; ++k) {
+      const T rk = __shfl_sync(0xffffffffu, rd_own, k);
+      x[k] *= rk;
 #pragma unroll
-      for (int k = 0; k < i; ++k) s = fma(-Dg[i + k * ldc], x[k], s);
-      x[i] = unit ? s : s / Dg[i + i * ldc];
+      for (int i = k + 1; i < 32; ++i) x[i] = fma(-Dg[i + k * ldc], x[k], x[i]);
     }
   } else {
 #pragma unroll
-    for (int i = 31; i >= 0; --i) {
-      T s = (i == lane) ? T(1) : T(0);
+    for (int k = 31; k >= 0; --k) {
+      const T rk = __shfl_sync(0xffffffffu, rd_own, k);
+      x[k] *= rk;
 #pragma unroll
-      for (int k = i + 1; k < 32; ++k) s = fma(-Dg[i + k * ldc], x[k], s);
-      x[i] = s / Dg[i + i * ldc];
+      for (int i = 0; i < k; ++i) x[i] = fma(-Dg[i + k * ldc], x[k], x[i]);
     }
   }
 #pragma unroll
@@ -179,77 +187,60 @@ __device__ __noinline__ void tile_inverse(const T* C, int ldc, int j, bool lower
 }
 
 // Factor the 32 x 32 diagonal block at rows c0.. of the block column (Cs,
-// column stride Wp) in place, by ONE warp: lane t holds row t in registers,
-// the pivot row goes through shared memory (pr) with warp-level syncs only.
-// LU (mode 0), sign-shifted LU (mode 2; s -> sgn) or Cholesky (mode 1, lower
-// part meaningful). Returns the local column of the first breakdown or -1
-// (uniform over the warp).
-template <typename T>
-__device__ __noinline__ int diag_block_factor(T* Cs, int Wp, int c0, int mode, T* pr, T* sgn,
-                                              int w) {
+// column stride Wp) in place, by ONE warp: lane t holds row t in registers.
+// Per pivot: the pivot row (LU) or pivot column (Cholesky) goes through
+// shared memory (pr, double-buffered: one __syncwarp per pivot), every lane
+// forms one reciprocal, and rows above the pivot get a zero multiplier so
+// the rank-1 update is unconditional (no selects); the breakdown test is
+// tracked without branches (nothing is written back after a breakdown).
+// MODE 0 LU, 2 sign-shifted LU (s -> sgn), 1 Cholesky (lower part
+// meaningful). Returns the local column of the first breakdown or -1.
+template <int MODE, typename T>
+__device__ __noinline__ int diag_block_factor(T* Cs, int Wp, int c0, T* pr, T* sgn, int w) {
   const int t = threadIdx.x & 31;
-  const bool lu = mode != 1;
   T* D = Cs + c0;
   T a[32];
 #pragma unroll
   for (int c = 0; c < 32; ++c) a[c] = D[t + c * Wp];
   int badc = -1;
-#ifdef CF_TRACE
-  long long tk[5];
-#endif
 #pragma unroll
   for (int c = 0; c < 32; ++c) {
-#ifdef CF_TRACE
-    if ((c & 7) == 0) tk[c >> 3] = clock64();
-#endif
-    if (badc < 0) {
-      T* p = pr + (c & 1) * 32;
-      if (lu) {
-        if (t == c) {
+    T* p = pr + (c & 1) * 32;
+    if (MODE == 1) {
+      if (t >= c) p[t] = a[c];  // column c of the diagonal block
+      __syncwarp();
+      const T piv = p[c];
+      const bool brk = !(piv > T(0)) || !isfinite(piv);
+      badc = (badc < 0 && brk) ? c : badc;
+      const T d = sqrt(piv);
+      const T rd = T(1) / d;
+      const T l = (t > c) ? a[c] * rd : T(0);  // l_{t,c}
+      a[c] = (t > c) ? l : (t == c ? d : a[c]);
 #pragma unroll
-          for (int cc = c; cc < 32; ++cc) p[cc] = a[cc];
-        }
-      } else if (t >= c) {
-        p[t] = a[c];  // column c (the symmetric pivot row)
+      for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc] * rd, a[cc]);  // l_{cc,c} = p[cc]/d
+    } else {
+      if (t == c) {
+#pragma unroll
+        for (int cc = c; cc < 32; ++cc) p[cc] = a[cc];  // pivot row
       }
       __syncwarp();
       T piv = p[c];
-      if (mode == 2) {
+      if (MODE == 2) {
         // s = -sign(x), x = -0.0 counted as + (copysign(., x0 or 1), linalg.py:278)
         const T sv = (piv < T(0)) ? T(1) : T(-1);
         piv -= sv;
         if (t == c) a[c] = piv;
         if (t == 0 && sgn && c0 + c < w) sgn[c0 + c] = sv;
       }
-      const bool brk = lu ? (piv == T(0) || !isfinite(piv)) : (!(piv > T(0)) || !isfinite(piv));
-      if (brk) {
-        badc = c;
-      } else if (lu) {
-        if (t > c) {
-          const T l = a[c] / piv;
-          a[c] = l;
+      const bool brk = (piv == T(0)) || !isfinite(piv);
+      badc = (badc < 0 && brk) ? c : badc;
+      const T rp = T(1) / piv;
+      const T l = (t > c) ? a[c] * rp : T(0);
+      if (t > c) a[c] = l;
 #pragma unroll
-          for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc], a[cc]);
-        }
-      } else {
-        const T d = sqrt(piv);
-        if (t == c) {
-          a[c] = d;
-        } else if (t > c) {
-          const T rd = T(1) / d;
-          const T l = a[c] / d;
-          a[c] = l;
-#pragma unroll
-          for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc] * rd, a[cc]);
-        }
-      }
+      for (int cc = c + 1; cc < 32; ++cc) a[cc] = fma(-l, p[cc], a[cc]);
     }
   }
-#ifdef CF_TRACE
-  tk[4] = clock64();
-  if (t == 0 && c0 == 0)
-    for (int q = 0; q < 4; ++q) g_cf_clk[q] = tk[q + 1] - tk[q];
-#endif
   if (badc < 0) {
 #pragma unroll
     for (int c = 0; c < 32; ++c) D[t + c * Wp] = a[c];
@@ -317,11 +308,13 @@ __global__ void __launch_bounds__(CF_T, 1)
   const int c0 = 32 * r;
 
   // load the block column (identity padding), X = I on block r
-  for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
-    const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
-    Cs[idx] = (i < w && gc < w) ? D[i + (int64_t)gc * ld] : (i == gc ? T(1) : T(0));
-    Xs[idx] = (i == gc) ? T(1) : T(0);
-  }
+  // (warp per column, lane over rows: no integer division in these loops)
+  for (int c = ty; c < 32; c += CF_T / 32)
+    for (int i = tid & 31; i < Wp; i += 32) {
+      const int gc = c0 + c;
+      Cs[i + c * Wp] = (i < w && gc < w) ? D[i + (int64_t)gc * ld] : (i == gc ? T(1) : T(0));
+      Xs[i + c * Wp] = (i == gc) ? T(1) : T(0);
+    }
   if (tid == 0) *s_bad = 0;
   __syncthreads();
 
@@ -332,7 +325,9 @@ __global__ void __launch_bounds__(CF_T, 1)
       // ---- factor block column j: the diagonal block by one warp, its
       //      inverses by two, then the rows below against the inverse ----
       if (ty == 0) {
-        const int badc = diag_block_factor(Cs, Wp, c0, mode, pr, sgn, w);
+        const int badc = mode == 0   ? diag_block_factor<0>(Cs, Wp, c0, pr, sgn, w)
+                         : mode == 1 ? diag_block_factor<1>(Cs, Wp, c0, pr, sgn, w)
+                                     : diag_block_factor<2>(Cs, Wp, c0, pr, sgn, w);
         if (badc >= 0 && (tid & 31) == 0) {
           *s_bad = 1;
           if (c0 + badc < w) atomicCAS(info, 0, (int)(col_base + c0 + badc + 1));
@@ -351,6 +346,20 @@ __global__ void __launch_bounds__(CF_T, 1)
           else
             tile_mul_inplace(Cs, Wp, c0 + 32, Wp, Li, TS, 1);   // L21 = A21 L11^{-T}
         }
+        // publish the final block column (rows >= 32j) and the diagonal
+        // block's inverses through global memory (L2): the other CTAs read
+        // them from there after the cluster barrier (a DSMEM pull would put
+        // seven readers on this CTA's shared-memory port)
+        for (int c = ty; c < 32; c += CF_T / 32)
+          for (int i = c0 + (tid & 31); i < Wp; i += 32)
+            if (i < w && c0 + c < w) D[i + (int64_t)(c0 + c) * ld] = Cs[i + c * Wp];
+        for (int idx = tid; idx < 32 * 32; idx += CF_T) {
+          const int i = idx & 31, c = idx >> 5;
+          if (c0 + i < w && c0 + c < w) {
+            Linv[(c0 + i) + (int64_t)(c0 + c) * ldl] = Li[i + c * TS];
+            if (lu) Uinv[(c0 + i) + (int64_t)(c0 + c) * ldu] = Ui[i + c * TS];
+          }
+        }
       }
       __syncthreads();
       CF_MARK(1 + 4 * j);
@@ -364,11 +373,12 @@ __global__ void __launch_bounds__(CF_T, 1)
     }
     const T* Pj = Cs;
     if (r != j) {
-      panel_copy(Ps, Cs, j, Wp, 32 * j, Wp);
+      global_block_column(Ps, Wp, D, ld, w, 32 * j, 32 * j, Wp);
+      global_tile(Lj, Linv, ldl, w, 32 * j);
       Pj = Ps;
+    } else {
+      for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Li[idx];
     }
-    const T* Lsrc = (r == j) ? Li : cluster.map_shared_rank(Li, j);
-    for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Lsrc[idx];
     __syncthreads();
     CF_MARK(3 + 4 * j);
     if (r > j) {
@@ -395,42 +405,37 @@ __global__ void __launch_bounds__(CF_T, 1)
   CF_MARK(41);
   if (!bad) {
     // factor out (Cholesky: lower part, zeros above)
-    for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
-      const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
-      if (i < w && gc < w) D[i + (int64_t)gc * ld] = (lu || i >= gc) ? Cs[idx] : T(0);
-    }
-    if (Linv) {
-      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
-        const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
-        if (i < w && gc < w) Linv[i + (int64_t)gc * ldl] = (i >= c0) ? Xs[idx] : T(0);
+    for (int c = ty; c < 32 && c0 + c < w; c += CF_T / 32)
+      for (int i = tid & 31; i < w; i += 32) {
+        const int gc = c0 + c;
+        D[i + (int64_t)gc * ld] = (lu || i >= gc) ? Cs[i + c * Wp] : T(0);
+        Linv[i + (int64_t)gc * ldl] = (i >= c0) ? Xs[i + c * Wp] : T(0);
       }
-    }
     if (lu && Uinv) {
       // U^{-1}, block column r: Y = E_r, then for j = r..0:
-      //   Y_jr = U_jj^{-1} Y_jr,  Y_ir -= U_ij Y_jr (i < j)  (U_ij in CTA j)
-      __syncthreads();
-      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
-        const int i = idx % Wp, c = idx / Wp;
-        Xs[idx] = (i == c0 + c) ? T(1) : T(0);
-      }
+      //   Y_jr = U_jj^{-1} Y_jr,  Y_ir -= U_ij Y_jr (i < j)  (U_ij: block
+      //   column j of the final factor, read back from D)
+      cluster.sync();  // every CTA's block column is in D
+      for (int c = ty; c < 32; c += CF_T / 32)
+        for (int i = tid & 31; i < Wp; i += 32) Xs[i + c * Wp] = (i == c0 + c) ? T(1) : T(0);
       __syncthreads();
       for (int j = r; j >= 0; --j) {
-        const T* Usrc = (r == j) ? Ui : cluster.map_shared_rank(Ui, j);
-        for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Usrc[idx];
         const T* Uj = Cs;
-        if (j != r && j > 0) {
-          panel_copy(Ps, Cs, j, Wp, 0, 32 * j);
+        if (j != r) {
+          global_tile(Lj, Uinv, ldu, w, 32 * j);
+          if (j > 0) global_block_column(Ps, Wp, D, ld, w, 32 * j, 0, 32 * j);
           Uj = Ps;
+        } else {
+          for (int idx = tid; idx < 32 * TS; idx += CF_T) Lj[idx] = Ui[idx];
         }
         __syncthreads();
         tile_tri_apply(Xs, Wp, j, Lj, Bt);
         if (j > 0) tile_update(Xs, Wp, 0, 32 * j, Uj, Wp, Bt);
         __syncthreads();
       }
-      for (int idx = tid; idx < 32 * Wp; idx += CF_T) {
-        const int i = idx % Wp, c = idx / Wp, gc = c0 + c;
-        if (i < w && gc < w) Uinv[i + (int64_t)gc * ldu] = (i < c0 + 32) ? Xs[idx] : T(0);
-      }
+      for (int c = ty; c < 32 && c0 + c < w; c += CF_T / 32)
+        for (int i = tid & 31; i < w; i += 32)
+          Uinv[i + (int64_t)(c0 + c) * ldu] = (i < c0 + 32) ? Xs[i + c * Wp] : T(0);
     }
   }
   CF_MARK(42);
@@ -481,7 +486,8 @@ int diag_factor_fast(cudaStream_t st, double* D, int64_t ld, int w, int mode, do
                      int64_t ldl, double* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
                      double* sgn) {
   if (w <= 0) return 0;
-  if (w > 32 * CF_MAXB || cluster_disabled())
+  // the cluster kernel exchanges panels / inverse blocks through D, Linv, Uinv
+  if (w > 32 * CF_MAXB || cluster_disabled() || !Linv || (mode != 1 && !Uinv))
     return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
   return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
@@ -490,7 +496,7 @@ int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, flo
                      int64_t ldl, float* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
                      float* sgn) {
   if (w <= 0) return 0;
-  if (w > 32 * CF_MAXB || cluster_disabled())
+  if (w > 32 * CF_MAXB || cluster_disabled() || !Linv || (mode != 1 && !Uinv))
     return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
   return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
