@@ -119,6 +119,10 @@ struct abft_ctx {
   GemmWorkspace gws2;             // split-K workspace of the side stream
   int qr_la_sms = 16;             // QR look-ahead: SMs left to the side-stream panel
                                   // (ABFT_QR_LA_SMS)
+  bool chol_cluster = false;      // Cholesky PD on the cluster kernel, submitted ahead of
+                                  // the look-ahead update (ABFT_CHOL_CLUSTER=1). Off for
+                                  // fp64: PD is hidden behind the K = p update, whose
+                                  // 8-SM cap then costs more (dpotrf 27.9 -> 27.0 TF/s)
   // streamed result (abft_stream_out): finished column blocks are copied to
   // this host buffer on a copy stream while the factorization continues
   double* out_host = nullptr;
@@ -333,7 +337,10 @@ int task_pd(abft_ctx* c, int64_t k) {
     ABFT_TRY(lu_diag(c, c->st, k));
     ABFT_TRY(lu_l21(c, k));
   } else if (c->kind == ABFT_CHOLESKY) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+    if (c->chol_cluster)
+      ABFT_TRY(diag_factor_fast(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+    else
+      ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
     double* V = c->vstore + p + p * c->ld;
     ABFT_TRY(qr_panel_factor(c->st, D, c->ld, n - p, (int)w, V, c->ld,
@@ -692,10 +699,15 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
 // PD(k) runs on the main stream; the panel-(k+1) encode goes with it. PU(k)
 // waits for the side stream (it needs the whole GPU), TMU(k+1) then only
 // applies panel k (K = b). Same operations as simulator.py:135-167, split.
-int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next) {
+// With chol_cluster the caller records ev_a (after TMU(k)), submits PD(k)
+// -- the cluster diagonal factorization, ceil(b/32) SMs -- and only then this
+// update, capped to leave those SMs: both become ready together and the
+// cluster, first in submission order, is placed before the persistent GEMM
+// fills the GPU.
+int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next, bool ev_recorded = false) {
   const int64_t n = c->n, pk = k * c->b, p1 = (k + 1) * c->b;
   const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
-  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  if (!ev_recorded) CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
   c->chol_enc_ahead = false;
   if (scheme_next != ABFT_NONE) {
@@ -706,8 +718,9 @@ int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next) {
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   double* P1 = c->m + p1 + p1 * c->ld;
+  const int keep = c->chol_cluster ? (int)((c->b + 31) / 32) : 1;
   ABFT_TRY(gemm_capped(c->st2, 'N', 'T', (int)(n - p1), (int)w1, (int)pk, -1.0, c->m + p1, c->ld,
-                       c->m + p1, c->ld, 1.0, P1, c->ld, P1, c->ld, &c->gws2, sms - 1));
+                       c->m + p1, c->ld, 1.0, P1, c->ld, P1, c->ld, &c->gws2, sms - keep));
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   c->chol_part = k + 1;
   return 0;
@@ -938,8 +951,14 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
   if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
     const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb;
-    if (la) ABFT_TRY(chol_lookahead(c, k, c->next_scheme));
-    ABFT_TRY(pd());
+    if (la && c->chol_cluster) {
+      CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+      ABFT_TRY(pd());
+      ABFT_TRY(chol_lookahead(c, k, c->next_scheme, true));
+    } else {
+      if (la) ABFT_TRY(chol_lookahead(c, k, c->next_scheme));
+      ABFT_TRY(pd());
+    }
     if (la) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
     ABFT_TRY(pu());
   } else if (c->kind == ABFT_LU) {
@@ -1066,6 +1085,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     c->fuse_enabled = !(e && e[0] == '1');
     const char* e2 = getenv("ABFT_NO_LOOKAHEAD");
     c->lookahead_enabled = !(e2 && e2[0] == '1');
+    const char* e4 = getenv("ABFT_CHOL_CLUSTER");
+    if (e4) c->chol_cluster = e4[0] == '1';
     const char* e3 = getenv("ABFT_QR_LA_SMS");
     if (e3) c->qr_la_sms = atoi(e3);  // 0 disables the QR look-ahead
   }

@@ -87,6 +87,9 @@ struct abft_sctx {
   double* v64 = nullptr;     // n x b (ld)
   double* t64 = nullptr;     // b x b (ld_t)
   double* gram = nullptr;    // b x b
+  bool chol_cluster = true;     // Cholesky PD on the cluster kernel (ABFT_CHOL_CLUSTER=0: off);
+                                // spotrf N=16384 32.4 -> 35.4 TF/s (the fp32 update is short,
+                                // so the diagonal chain was on the critical path)
   double* qr_q1 = nullptr;     // fp64 n x b: CholeskyQR2 Q of the widened panel
   double* qr_small = nullptr;  // QR_SMALL_BUFS x (ld_t x b)
   QrPanelWork qrw;
@@ -335,10 +338,12 @@ int s_chol_update(abft_sctx* c, cudaStream_t st, int64_t k, int64_t K0, int64_t 
 // k+1 by panels 0..k-1 -- final since their PU -- runs on the side stream
 // (encode of panel k+1 first, when its iteration is protected) while the
 // main stream factors panel k; TMU(k+1) then applies panel k alone.
-int s_chol_lookahead(abft_sctx* c, int64_t k, int scheme_next) {
+// (chol_cluster: the caller records ev_a after TMU(k) and submits the cluster
+// PD(k) first, as ctx.cu's chol_lookahead)
+int s_chol_lookahead(abft_sctx* c, int64_t k, int scheme_next, bool ev_recorded = false) {
   const int64_t n = c->n, pk = k * c->b, p1 = (k + 1) * c->b;
   const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
-  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  if (!ev_recorded) CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
   c->chol_enc_ahead = false;
   if (scheme_next != ABFT_NONE) {
@@ -346,7 +351,8 @@ int s_chol_lookahead(abft_sctx* c, int64_t k, int scheme_next) {
     ABFT_TRY(blocksum(c->st2, reg1, s_sums(c, p1, p1, true)));
     c->chol_enc_ahead = true;
   }
-  ABFT_TRY(s_chol_update(c, c->st2, k + 1, 0, pk, c->sms - 1));
+  const int keep = c->chol_cluster ? (int)((c->b + 31) / 32) : 1;
+  ABFT_TRY(s_chol_update(c, c->st2, k + 1, 0, pk, c->sms - keep));
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   c->chol_part = k + 1;
   return 0;
@@ -409,7 +415,10 @@ int s_pd(abft_sctx* c, int64_t k) {
     ABFT_TRY(s_lu_diag(c, c->st, k));
     ABFT_TRY(s_lu_l21(c, k));
   } else if (c->kind == ABFT_CHOLESKY) {
-    ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+    if (c->chol_cluster)
+      ABFT_TRY(diag_factor_fast(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
+    else
+      ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
     // mixed-precision Householder panel: widen, factor in fp64, narrow back
     const int64_t nk = n - p;
@@ -874,8 +883,14 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
     // (b % 4: the newest panel's K offset must keep the pre-split rows TMA-aligned)
     const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb && c->b % 4 == 0;
-    if (la) ABFT_TRY(s_chol_lookahead(c, k, c->next_scheme));
-    ABFT_TRY(pd());
+    if (la && c->chol_cluster) {
+      CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+      ABFT_TRY(pd());
+      ABFT_TRY(s_chol_lookahead(c, k, c->next_scheme, true));
+    } else {
+      if (la) ABFT_TRY(s_chol_lookahead(c, k, c->next_scheme));
+      ABFT_TRY(pd());
+    }
     if (la) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
     ABFT_TRY(pu());
   } else if (c->kind == ABFT_QR) {
@@ -985,6 +1000,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   {
     const char* e = getenv("ABFT_NO_FUSE");
     c->fuse_enabled = !(e && e[0] == '1');
+    const char* e4 = getenv("ABFT_CHOL_CLUSTER");
+    if (e4 && e4[0] == '0') c->chol_cluster = false;
   }
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
     set_last_error("cudaStreamCreate failed");
@@ -1043,7 +1060,7 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     int64_t need = 0;
     if (kind == ABFT_CHOLESKY && k > 0) {  // pre-split operands: partials only
       // main-stream updates (all SMs) and the look-ahead's (one SM fewer)
-      for (int cap : {c->sms, c->sms - 1}) {
+      for (int cap : {c->sms, c->sms - 1, c->sms - (int)((b + 31) / 32)}) {
         int64_t unused;
         s_gemm_plan(cap, n - p, pe - p, p, S_KCHUNK_CHOL, false, &sp, &unused);
         need = std::max(need, sgemm_partial_elems((int)(n - p), (int)(pe - p), sp) + 128);
