@@ -359,7 +359,7 @@ int begin_lu(abft_dist* d, int64_t k, double* xb) {
   const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
   const int64_t lc = (k / d->world) * d->b, ldp = panel_ld(d, k);
   double* D = d->m + p + lc * d->ld;
-  ABFT_TRY(diag_factor(d->st, D, d->ld, (int)w, 0, d->linv, d->ld_t, d->uinv, d->ld_t, d->info, p));
+  ABFT_TRY(diag_factor_fast(d->st, D, d->ld, (int)w, 0, d->linv, d->ld_t, d->uinv, d->ld_t, d->info, p));
   if (pe < n) {
     // L21 = A21 U11^{-1} straight into the exchange buffer, then back into m
     ABFT_TRY(gemm(d->st, 'N', 'N', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->uinv, d->ld_t,
@@ -371,6 +371,9 @@ int begin_lu(abft_dist* d, int64_t k, double* xb) {
   return 0;
 }
 
+// (the owner's diagonal factorizations run on the cluster kernel: on 8 GPUs
+// this chain -- not the trailing update -- bounds the per-iteration time,
+// tools/projection.py)
 int begin_qr(abft_dist* d, int64_t k, double* xb) {
   if (owner(d, k) != d->rank) return 0;
   const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
@@ -726,7 +729,7 @@ int chol_pd_pu(abft_dist* d, int64_t k) {
   if (owner(d, k) == d->rank) {
     const int64_t lc = (k / d->world) * d->b;
     double* D = d->m + p + lc * d->ld;
-    ABFT_TRY(diag_factor(d->st, D, d->ld, (int)w, 1, d->linv, d->ld_t, nullptr, 0, d->info, p));
+    ABFT_TRY(diag_factor_fast(d->st, D, d->ld, (int)w, 1, d->linv, d->ld_t, nullptr, 0, d->info, p));
     if (pe < n) {
       ABFT_TRY(gemm(d->st, 'N', 'T', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->linv,
                     d->ld_t, 0.0, nullptr, 0, d->lw, d->ld, &d->gws));
@@ -1063,7 +1066,7 @@ ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) 
     if (pe >= d->n) {
       if (owner(d, k) == d->rank) {
         const int64_t lc = (k / d->world) * d->b;
-        ABFT_TRY(diag_factor(d->st, d->m + p + lc * d->ld, d->ld, (int)(pe - p), 0, d->linv,
+        ABFT_TRY(diag_factor_fast(d->st, d->m + p + lc * d->ld, d->ld, (int)(pe - p), 0, d->linv,
                              d->ld_t, d->uinv, d->ld_t, d->info, p));
       }
       return 0;

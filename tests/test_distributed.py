@@ -152,10 +152,12 @@ def test_nccl_transport_and_lookahead_on_one_rank(tmp_path):
     res = json.loads((tmp_path / "nccl.json").read_text())
     for kind, r in res.items():
         assert r["same_reports"], kind
-        # LU: identical kernels, identical results; QR's look-ahead splits
-        # V^T C by block columns (other split-K factors) and Cholesky's
-        # distributed form sums its panel products in another order
-        assert r["max_diff"] <= (0.0 if kind == "lu" else 1e-10), (kind, r)
+        # the distributed owner factors diagonal blocks on the cluster kernel
+        # (small_factor.cu; the one-GPU LU look-ahead keeps the one-CTA
+        # kernel), QR's look-ahead splits V^T C by block columns (other
+        # split-K factors) and Cholesky's distributed form sums its panel
+        # products in another order: rounding-level differences only
+        assert r["max_diff"] <= (1e-12 if kind == "lu" else 1e-10), (kind, r)
         assert r["residual"] < 1e-12 and r["residual1"] < 1e-12, (kind, r)
 
 
