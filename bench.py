@@ -238,7 +238,7 @@ def config(args, n: int | None = None) -> dict:
                   + (">> 126 MB L2; no flush needed" if n * n * 4 > 4 * 126e6 else
                      "(CPU sample)"),
             "parallelism": (f"block-cyclic columns over {args.gpus} GPUs "
-                            f"({'panel broadcast' if args.kind != 'cholesky' else 'panel-update reduce'}"
+                            f"({'panel-update reduce' if args.kind == 'cholesky' and os.environ.get('ABFT_DIST_CHOL', '').startswith('l') else 'panel broadcast + cross-rank look-ahead'}"
                             f" over {args.dist_backend})") if args.gpus > 1 else "single"}
 
 

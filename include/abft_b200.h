@@ -240,6 +240,13 @@ ABFT_API int abft_dist_set_local(abft_dist* d, const double* local, int64_t ldl)
 /* local columns (n x local_cols) -> host */
 ABFT_API int abft_dist_get_matrix(abft_dist* d, double* out, int64_t ldo);
 ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf);
+
+/* The exchange step of iteration k (between abft_dist_begin and
+ * abft_dist_update): returns 0 none, 1 broadcast from *root, 2 sum-reduce
+ * to *root (left-looking Cholesky, ABFT_DIST_CHOL=left), over
+ * abft_dist_xbuf_elems(k) doubles. Right-looking Cholesky (default)
+ * broadcasts panel k-1 from its owner at iteration k. */
+ABFT_API int abft_dist_exchange(abft_dist* d, int64_t k, int* root);
 ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double* xbuf, int nplan,
                               double* local_max);
 /* scale: device pointer to the all-reduced max|region| (NULL if nplan == 0) */

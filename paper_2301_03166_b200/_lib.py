@@ -114,6 +114,7 @@ SIGNATURES = [
     ("abft_dist_keep_input", _I, [_P, _I]),
     ("abft_dist_reset", _I, [_P]),
     ("abft_dist_begin", _I, [_P, _I64, _I, _P]),
+    ("abft_dist_exchange", _I, [_P, _I64, ctypes.POINTER(_I)]),
     ("abft_dist_update", _I, [_P, _I64, _I, _P, _I, _P]),
     ("abft_dist_finish", _I, [_P, _I64, _I, ctypes.POINTER(Fault), _I, _I, _P]),
     ("abft_dist_events", _I, [_P, ctypes.POINTER(Location), ctypes.POINTER(_I64), _I,

@@ -138,6 +138,11 @@ struct abft_dist {
   bool comm_pending = false;     // main stream must wait on ev_comm before the next begin
   bool verified_in_update = false;
   int reserve_sms = 8;           // SMs left to the collective kernels during the big GEMM
+  // Cholesky right-looking (default; ABFT_DIST_CHOL=left keeps the reference's
+  // left-looking form with its per-iteration sum-reduce)
+  bool chol_right = true;
+  double* rv = nullptr;          // b x nbl: row-block sums of L over each local block
+  int64_t chol_pd_done = -1;     // panel verified + factored by the look-ahead in update(k)
 };
 
 namespace {
@@ -407,6 +412,150 @@ int begin_chol(abft_dist* d, int64_t k, double* xb) {
                 d->ld_b, 0.0, nullptr, 0, X, ldp, &d->gws));
   ABFT_TRY(gemm(d->st, 'N', 'N', (int)(2 * nbr), (int)w, (int)pl, 1.0, d->gcsw + 2 * k, d->ld_cs,
                 d->bext, d->ld_b, 0.0, nullptr, 0, CS, ldc, &d->gws));
+  return 0;
+}
+
+int local_max(abft_dist* d, const LocalRegion& R, double* out);
+
+// ---------------------------------------------------------------------------
+// right-looking Cholesky: panel k is complete when iteration k
+// starts (every earlier panel's rank-b update went to all columns as soon as
+// that panel was factored), so the protected region of iteration k -- panel
+// column k (simulator.py:90-91) -- is verified, factored and broadcast by its
+// owner, and every rank applies it to its own trailing columns. The column /
+// row checksums of every future panel are encoded once (k = 0) and maintained
+// through each rank-b update from the operands (abft.py:138-158 applied one
+// panel at a time), so at iteration k they are exactly the reference's
+// maintained checksums of the region, summed in another order.
+// Exchange of iteration k >= 1: broadcast from owner(k-1) of
+//   [L_{k-1} rows p'..n (ldp x w) | block-row checksums of L_{k-1} (ldc x w)].
+int64_t chol_right_xe(const abft_dist* d, int64_t k) {
+  if (k == 0) return 0;
+  const int64_t k1 = k - 1, p1 = k1 * d->b, w = width(d, k1);
+  const int64_t nbr = (d->n - p1 + d->b - 1) / d->b;
+  return panel_ld(d, k1) * w + round_even(2 * nbr) * w;
+}
+
+// RV[q, t] = sum_{c < w_j} L[(j_t b - p1) + c, q] for the rank's blocks j_t >= k
+__global__ void rowblock_sums_kernel(const double* L, int64_t ldp, int64_t p1, int w, int64_t n,
+                                     int64_t b, int rank, int world, int64_t l0, int nt,
+                                     double* RV, int64_t ldrv) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < nt * w;
+       idx += gridDim.x * blockDim.x) {
+    const int q = idx % w, t = idx / w;
+    const int64_t jb = ((l0 + t) * world + rank) * b;
+    const int64_t wj = (n - jb < b) ? n - jb : b;
+    double s = 0.0;
+    for (int64_t c = 0; c < wj; ++c) s += L[(jb - p1) + c + (int64_t)q * ldp];
+    RV[q + (int64_t)t * ldrv] = s;
+  }
+}
+
+int begin_chol_right(abft_dist* d, int64_t k, double* xb) {
+  const int64_t n = d->n;
+  if (k == 0) {
+    // encode every local column once: column sums on the global block grid,
+    // row sums per local block column, block maxima
+    if (d->ncl > 0) {
+      Region all{d->m, d->ld, n, d->ncl, d->b};
+      ABFT_TRY(blocksum(d->st, all, sums_local(d, 0, 0, true)));
+    }
+    return 0;
+  }
+  const int64_t k1 = k - 1;
+  if (owner(d, k1) != d->rank) return 0;
+  const int64_t p1 = k1 * d->b, w = width(d, k1), ldp = panel_ld(d, k1);
+  const int64_t nbr = (n - p1 + d->b - 1) / d->b, ldc = round_even(2 * nbr);
+  const int64_t lc = (k1 / d->world) * d->b;
+  ABFT_TRY(copy_matrix(d->st, d->m + p1 + lc * d->ld, d->ld, xb, ldp, n - p1, w));
+  // block-row checksums of L_{k-1} (chol_pd_pu wrote them on the global grid)
+  ABFT_TRY(copy_matrix(d->st, d->gcsw + 2 * k1 + lc * d->ld_cs, d->ld_cs, xb + ldp * w, ldc,
+                       2 * nbr, w));
+  return 0;
+}
+
+// Apply panel k-1 (L = xb) to the rank's local blocks [la, lb) (all global
+// indices >= k): the lower-triangular rank-b update of each block column and
+// the maintenance of its column / row checksums.
+int chol_right_apply(abft_dist* d, int64_t k, const double* xb, int64_t la, int64_t lb) {
+  const int64_t n = d->n, b = d->b;
+  const int64_t k1 = k - 1, p1 = k1 * b, w = width(d, k1), ldp = panel_ld(d, k1);
+  const int64_t nbr = (n - p1 + b - 1) / b, ldc = round_even(2 * nbr);
+  const double* L = xb;
+  const double* CS = xb + ldp * w;
+  if (lb <= la) return 0;
+  for (int64_t l = la; l < lb; ++l) {
+    const int64_t j = l * d->world + d->rank, jb = j * b, wj = width(d, j), lc = l * b;
+    // A[jb:n, j] -= L[jb:n, :] L[jb:jb+wj, :]^T   (rows >= jb: the panel-j region)
+    ABFT_TRY(gemm(d->st, 'N', 'T', (int)(n - jb), (int)wj, (int)w, -1.0, L + (jb - p1), ldp,
+                  L + (jb - p1), ldp, 1.0, d->m + jb + lc * d->ld, d->ld, d->m + jb + lc * d->ld,
+                  d->ld, &d->gws));
+    // column sums of panel j's blocks: CS_j -= CS(L) L[jb:jb+wj, :]^T
+    const int64_t nbj = d->nb - j;
+    ABFT_TRY(gemm(d->st, 'N', 'T', (int)(2 * nbj), (int)wj, (int)w, -1.0, CS + 2 * (j - k1), ldc,
+                  L + (jb - p1), ldp, 1.0, d->gcsw + 2 * j + lc * d->ld_cs, d->ld_cs,
+                  d->gcsw + 2 * j + lc * d->ld_cs, d->ld_cs, &d->gws));
+  }
+  // row sums of the future panels: RS[i, l] -= L[i, :] RV[:, l]
+  const int nt = (int)(lb - la);
+  int blocks = (int)std::min<int64_t>((nt * w + 255) / 256, 1024);
+  count_launch();
+  rowblock_sums_kernel<<<std::max(blocks, 1), 256, 0, d->st>>>(L, ldp, p1, (int)w, n, b, d->rank,
+                                                               d->world, la, nt, d->rv, d->ld_t);
+  CUDA_TRY(cudaGetLastError());
+  const int64_t r0 = k * b;
+  return gemm(d->st, 'N', 'N', (int)(n - r0), nt, (int)w, -1.0, L + (r0 - p1), ldp, d->rv, d->ld_t,
+              1.0, d->grs + r0 + la * d->ld, d->ld, d->grs + r0 + la * d->ld, d->ld, &d->gws);
+}
+
+// Panel k on its owner, once every update reached it: maintained sums =
+// the running ones, recomputed sums (+ block maxima) from one pass.
+int chol_right_region(abft_dist* d, int64_t k, int scheme, int nplan) {
+  const LocalRegion R = local_region(d, k);
+  if (R.rows <= 0 || R.cols <= 0) return 0;
+  const bool prot = scheme != ABFT_NONE;
+  const int64_t nbr = (R.rows + d->b - 1) / d->b;
+  Region reg{d->m + R.r0 + R.lc0 * d->ld, d->ld, R.rows, R.cols, d->b};
+  SumOut run = sums_local(d, R.r0, R.lb0, true);
+  if (prot) {
+    ABFT_TRY(copy_matrix(d->st, run.cp, d->ld_cs, d->csm, d->ld_cs, 2 * nbr, R.cols));
+    if (scheme == ABFT_FULL) ABFT_TRY(copy_matrix(d->st, run.rp, d->ld, d->rsm, d->ld, R.rows, 1));
+    ABFT_TRY(blocksum(d->st, reg, run));
+  } else if (nplan > 0) {
+    SumOut o;
+    o.bm = run.bm;
+    o.bm_ld = run.bm_ld;
+    ABFT_TRY(blocksum(d->st, reg, o));
+  }
+  return 0;
+}
+
+int chol_pd_pu_owner(abft_dist* d, int64_t k);
+int inject_verify(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, int nplan,
+                  int correct, const double* scale);
+
+int update_chol_right(abft_dist* d, int64_t k, int scheme, const double* xb, int nplan,
+                      double* max_out) {
+  const int64_t l0 = owned_upto(d, k - 1);  // first local block with global index >= k
+  if (d->la_buf && owner(d, k) == d->rank && nplan == 0 && k + 1 < d->nb) {
+    // cross-rank look-ahead: panel k first, then verified, factored and
+    // packed for the broadcast (comm stream) before the rest of the update
+    if (k >= 1) ABFT_TRY(chol_right_apply(d, k, xb, l0, l0 + 1));
+    ABFT_TRY(chol_right_region(d, k, scheme, 0));
+    ABFT_TRY(inject_verify(d, k, scheme, nullptr, 0, 1, nullptr));
+    ABFT_TRY(chol_pd_pu_owner(d, k));
+    ABFT_TRY(begin_chol_right(d, k + 1, d->la_buf));
+    CUDA_TRY(cudaEventRecord(d->ev_pack, d->st));
+    CUDA_TRY(cudaStreamWaitEvent(d->st2, d->ev_pack, 0));
+    d->panel_ready = k + 1;
+    d->chol_pd_done = k;
+    d->verified_in_update = true;
+    if (k >= 1) ABFT_TRY(chol_right_apply(d, k, xb, l0 + 1, d->nbl));
+    return 0;
+  }
+  if (k >= 1) ABFT_TRY(chol_right_apply(d, k, xb, l0, d->nbl));
+  ABFT_TRY(chol_right_region(d, k, scheme, nplan));
+  if (nplan > 0 && max_out) ABFT_TRY(local_max(d, local_region(d, k), max_out));
   return 0;
 }
 
@@ -724,22 +873,30 @@ int inject_verify(abft_dist* d, int64_t k, int scheme, const abft_fault* plan, i
 
 // Cholesky PD + PU of panel k (owner) after verification; every rank zeroes
 // its columns of the row block m[p:pe, pe:n] (linalg.py:228-229, :251-252).
+int chol_pd_pu_owner(abft_dist* d, int64_t k) {
+  const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
+  if (owner(d, k) != d->rank) return 0;
+  const int64_t lc = (k / d->world) * d->b;
+  double* D = d->m + p + lc * d->ld;
+  ABFT_TRY(diag_factor_fast(d->st, D, d->ld, (int)w, 1, d->linv, d->ld_t, nullptr, 0, d->info, p));
+  if (pe < n) {
+    ABFT_TRY(gemm(d->st, 'N', 'T', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->linv,
+                  d->ld_t, 0.0, nullptr, 0, d->lw, d->ld, &d->gws));
+    ABFT_TRY(copy_matrix(d->st, d->lw, d->ld, D + w, d->ld, n - pe, w));
+  }
+  // block-row checksums of the finished L panel (operand sums of later maintenance)
+  Region reg{D, d->ld, n - p, w, d->b};
+  SumOut o = sums_local(d, p, k / d->world, false);
+  o.bm = nullptr;
+  return blocksum(d->st, reg, o);
+}
+
 int chol_pd_pu(abft_dist* d, int64_t k) {
   const int64_t n = d->n, p = k * d->b, pe = std::min(p + d->b, n), w = pe - p;
-  if (owner(d, k) == d->rank) {
-    const int64_t lc = (k / d->world) * d->b;
-    double* D = d->m + p + lc * d->ld;
-    ABFT_TRY(diag_factor_fast(d->st, D, d->ld, (int)w, 1, d->linv, d->ld_t, nullptr, 0, d->info, p));
-    if (pe < n) {
-      ABFT_TRY(gemm(d->st, 'N', 'T', (int)(n - pe), (int)w, (int)w, 1.0, D + w, d->ld, d->linv,
-                    d->ld_t, 0.0, nullptr, 0, d->lw, d->ld, &d->gws));
-      ABFT_TRY(copy_matrix(d->st, d->lw, d->ld, D + w, d->ld, n - pe, w));
-    }
-    // block-row checksums of the finished L panel (operand sums of later maintenance)
-    Region reg{D, d->ld, n - p, w, d->b};
-    SumOut o = sums_local(d, p, k / d->world, false);
-    o.bm = nullptr;
-    ABFT_TRY(blocksum(d->st, reg, o));
+  if (d->chol_pd_done == k) {
+    d->chol_pd_done = -1;  // factored by the look-ahead in update(k)
+  } else {
+    ABFT_TRY(chol_pd_pu_owner(d, k));
   }
   const int64_t tc0 = owned_upto(d, k) * d->b;
   if (pe < n && d->ncl > tc0) ABFT_TRY(fill_matrix(d->st, d->m + p + tc0 * d->ld, d->ld, w, d->ncl - tc0, 0.0));
@@ -850,6 +1007,7 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
   if ((rc = dalloc0(&d->uinv, d->ld_t * b, d->st))) return fail(rc);
   if ((rc = dalloc0(&d->dmax, 2, d->st))) return fail(rc);
   if (kind == ABFT_CHOLESKY && (rc = dalloc0(&d->bext, d->ld_b * (b + 1), d->st))) return fail(rc);
+  if (kind == ABFT_CHOLESKY && (rc = dalloc0(&d->rv, d->ld_t * nbl, d->st))) return fail(rc);
   if (kind == ABFT_QR) {
     if ((rc = dalloc0(&d->vstore, ld * n, d->st))) return fail(rc);
     if ((rc = dalloc0(&d->tstore, d->nb * b * d->ld_t, d->st))) return fail(rc);
@@ -898,6 +1056,10 @@ ABFT_API int abft_dist_create(abft_dist** out, int kind, int64_t n, int64_t b, i
   cudaEventCreateWithFlags(&d->ev_pack, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&d->ev_comm, cudaEventDisableTiming);
   {
+    const char* ec = getenv("ABFT_DIST_CHOL");
+    d->chol_right = !(ec && (ec[0] == 'l' || ec[0] == 'L'));
+  }
+  {
     const char* e = getenv("ABFT_DIST_RESERVE_SMS");
     if (e) d->reserve_sms = std::max(0, atoi(e));
   }
@@ -913,7 +1075,7 @@ ABFT_API int abft_dist_destroy(abft_dist* d) {
   double* bufs[] = {d->fpart,  d->fmaxp,
                     d->m,      d->a0,     d->gcsw,   d->csm,    d->grs,       d->rsm,      d->gmax,
                     d->el,     d->er,     d->uw,     d->lw,        d->linv,     d->uinv,
-                    d->bext,   d->vstore, d->tstore, d->betas,     d->qr_part,  d->qr_rowbuf,
+                    d->bext,   d->rv,     d->vstore, d->tstore, d->betas,     d->qr_part,  d->qr_rowbuf,
                     d->qr_part2, d->qr_wfin, d->gram, d->qr_q1, d->qr_small, d->ww,       d->mid,      d->dmax,
                     d->gws.ptr};
   for (double* p : bufs)
@@ -945,6 +1107,7 @@ ABFT_API int64_t abft_dist_xbuf_elems(abft_dist* d, int64_t k) {
   if (k < 0 || k >= d->nb) return 0;
   const int64_t p = k * d->b, w = width(d, k), ldp = panel_ld(d, k);
   if (d->kind == ABFT_CHOLESKY) {
+    if (d->chol_right) return chol_right_xe(d, k);
     if (k == 0) return 0;
     const int64_t nbr = (d->n - p + d->b - 1) / d->b;
     return ldp * (w + 1) + round_even(2 * nbr) * w;
@@ -977,6 +1140,7 @@ ABFT_API int abft_dist_set_matrix(abft_dist* d, const double* a, int64_t lda) {
   d->comm_pending = false;
   d->la_buf = nullptr;
   d->verified_in_update = false;
+  d->chol_pd_done = -1;
   return 0;
 }
 
@@ -1002,6 +1166,7 @@ ABFT_API int abft_dist_reset(abft_dist* d) {
   d->comm_pending = false;
   d->la_buf = nullptr;
   d->verified_in_update = false;
+  d->chol_pd_done = -1;
   return 0;
 }
 
@@ -1028,6 +1193,7 @@ ABFT_API int abft_dist_set_local(abft_dist* d, const double* local, int64_t ldl)
   d->comm_pending = false;
   d->la_buf = nullptr;
   d->verified_in_update = false;
+  d->chol_pd_done = -1;
   return 0;
 }
 
@@ -1056,7 +1222,7 @@ ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) 
     CUDA_TRY(cudaStreamWaitEvent(d->st, d->ev_comm, 0));
     d->comm_pending = false;
   }
-  if (d->kind != ABFT_CHOLESKY && d->panel_ready == k) {  // factored + packed by the look-ahead
+  if ((d->kind != ABFT_CHOLESKY || d->chol_right) && d->panel_ready == k) {  // packed by the look-ahead
     d->panel_ready = -1;
     return 0;
   }
@@ -1074,14 +1240,42 @@ ABFT_API int abft_dist_begin(abft_dist* d, int64_t k, int scheme, double* xbuf) 
     return begin_lu(d, k, xbuf);
   }
   if (d->kind == ABFT_QR) return begin_qr(d, k, xbuf);
+  if (d->chol_right) return begin_chol_right(d, k, xbuf);
   return begin_chol(d, k, xbuf);
+}
+
+// The exchange step of iteration k, between abft_dist_begin and
+// abft_dist_update: 0 none, 1 broadcast from *root, 2 sum-reduce to *root
+// (left-looking Cholesky); abft_dist_xbuf_elems(k) doubles of the buffer.
+ABFT_API int abft_dist_exchange(abft_dist* d, int64_t k, int* root) {
+  *root = 0;
+  if (k < 0 || k >= d->nb || abft_dist_xbuf_elems(d, k) == 0) return 0;
+  if (d->kind == ABFT_CHOLESKY) {
+    if (d->chol_right) {
+      *root = owner(d, k - 1);
+      return 1;
+    }
+    *root = owner(d, k);
+    return 2;
+  }
+  *root = owner(d, k);
+  return 1;
 }
 
 ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double* xbuf, int nplan,
                               double* local_max) {
   DevGuardD g(d->device);
   ABFT_TRY(check_k(d, k, scheme));
-  if (d->kind == ABFT_CHOLESKY) return update_chol(d, k, scheme, xbuf, nplan, local_max);
+  if (d->kind == ABFT_CHOLESKY && !d->chol_right) return update_chol(d, k, scheme, xbuf, nplan, local_max);
+  if (d->kind == ABFT_CHOLESKY) {
+    if (d->la_buf) {
+      CUDA_TRY(cudaEventRecord(d->ev_free, d->st));
+      CUDA_TRY(cudaStreamWaitEvent(d->st2, d->ev_free, 0));
+    }
+    const int rc = update_chol_right(d, k, scheme, xbuf, nplan, local_max);
+    d->la_buf = nullptr;
+    return rc;
+  }
   if (d->kind == ABFT_LU && std::min((k + 1) * d->b, d->n) >= d->n) {
     d->la_buf = nullptr;
     if (nplan > 0 && local_max) CUDA_TRY(cudaMemsetAsync(local_max, 0, sizeof(double), d->st));
@@ -1104,7 +1298,8 @@ ABFT_API int abft_dist_update(abft_dist* d, int64_t k, int scheme, const double*
 // (abft_dist_comm_stream) and calls abft_dist_comm_done; begin(k+1) makes the
 // main stream wait for that broadcast.
 ABFT_API int abft_dist_lookahead(abft_dist* d, int64_t k, double* xnext) {
-  if (d->kind == ABFT_CHOLESKY || k + 1 >= d->nb || abft_dist_xbuf_elems(d, k + 1) == 0) {
+  if ((d->kind == ABFT_CHOLESKY && !d->chol_right) || k + 1 >= d->nb ||
+      abft_dist_xbuf_elems(d, k + 1) == 0) {
     set_last_error("no look-ahead panel after iteration %lld", (long long)k);
     return ABFT_E_INVALID;
   }

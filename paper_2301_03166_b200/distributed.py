@@ -10,10 +10,13 @@ simulator; its protected iteration (simulator.py:97-167) and factorization
 * LU / QR: the owner of panel k factors it and the panel (plus L11^{-1} or
   T) is **broadcast** from k mod G; every rank then updates its own trailing
   columns with the fused-checksum trailing-update GEMM;
-* Cholesky stays left-looking like the reference (linalg.py:192-200): every
-  rank forms the partial update of panel k from its own finished panels and
-  the partials are **sum-reduced** to the owner, together with the partial
-  checksum-maintenance products (abft.py:138-158);
+* Cholesky is right-looking (default): the owner of panel k verifies,
+  factors and **broadcasts** it (with its block-row checksums), every rank
+  applies the rank-b update to its own trailing column blocks and maintains
+  their checksums from the operands (abft.py:138-158 one panel at a time);
+  with the cross-rank look-ahead the owner of panel k does that mid-update.
+  ABFT_DIST_CHOL=left keeps the reference's left-looking form (linalg.py:
+  192-200: partial panel products **sum-reduced** to the owner);
 * the fault plan is drawn on every rank from the same seeded Generator in
   sample_fault_plan's order (abft.py:310-333); the magnitude scale
   max|region| (simulator.py:159-160) is an all-reduce MAX over ranks;
@@ -245,21 +248,25 @@ class DistributedFactorization:
         buf = self._bufs[k % 2]
         xptr = buf.data_ptr()
         check(lib.abft_dist_begin(ctx, k, code, ctypes.c_void_p(xptr)))
-        if xe > 0 and k not in self._prefetched:
+        root = ctypes.c_int(0)
+        op = int(lib.abft_dist_exchange(ctx, k, ctypes.byref(root)))
+        if xe > 0 and op and k not in self._prefetched:
             view = buf[:xe]
-            if self.kind == DecompositionKind.CHOLESKY:
-                self._tx.reduce_sum(view, owner_of(k, self.world))
-            else:
-                self._tx.broadcast(view, owner_of(k, self.world))
+            if op == 2:  # left-looking Cholesky: partial panel products
+                self._tx.reduce_sum(view, root.value)
+            else:        # the panel (LU / QR: k; right-looking Cholesky: k-1)
+                self._tx.broadcast(view, root.value)
         self._prefetched.discard(k)
         nplan = len(plan)
-        # LU / QR look-ahead: panel k+1 is factored mid-update by its owner
-        # and broadcast on the comm stream while the trailing update of k runs
+        # look-ahead: the next exchanged panel (LU / QR: panel k+1; right-looking
+        # Cholesky: panel k) is factored mid-update by its owner and broadcast
+        # on the comm stream while the trailing update of k runs
         nb = self.layout.n_blocks
         xe1 = int(lib.abft_dist_xbuf_elems(ctx, k + 1)) if k + 1 < nb else 0
+        root1 = ctypes.c_int(0)
+        op1 = int(lib.abft_dist_exchange(ctx, k + 1, ctypes.byref(root1))) if k + 1 < nb else 0
         la = (self.lookahead and (self.world > 1 or self.force_lookahead)
-              and self.kind in (DecompositionKind.LU, DecompositionKind.QR) and nplan == 0
-              and xe1 > 0)
+              and op1 == 1 and nplan == 0 and xe1 > 0)
         nxt = self._bufs[(k + 1) % 2]
         if la:
             check(lib.abft_dist_lookahead(ctx, k, ctypes.c_void_p(nxt.data_ptr())))
@@ -267,7 +274,7 @@ class DistributedFactorization:
         check(lib.abft_dist_update(ctx, k, code, ctypes.c_void_p(xptr), nplan,
                                    sptr if nplan else None))
         if la:
-            self._tx.broadcast(nxt[:xe1], owner_of(k + 1, self.world), comm=True)
+            self._tx.broadcast(nxt[:xe1], root1.value, comm=True)
             check(lib.abft_dist_comm_done(ctx))
             self._prefetched.add(k + 1)
         if nplan:

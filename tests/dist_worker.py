@@ -35,7 +35,10 @@ def gpu_cases(rank: int, world: int, init_file: str, cases: list, out: str) -> N
     results = []
     for c in cases:
         a = P.generate_test_matrix(c["kind"], c["n"], c["seed"])
+        if c.get("chol_left"):  # the reference's left-looking form (sum-reduce exchange)
+            os.environ["ABFT_DIST_CHOL"] = "left"
         f = DistributedFactorization(c["kind"], a, c["b"], keep_input=bool(c.get("reset")))
+        os.environ.pop("ABFT_DIST_CHOL", None)
         f.lookahead = not c.get("no_lookahead", False)
         if c.get("reset"):  # a throw-away factorization, then restore the kept input
             f.run_protected("none", {}, None)

@@ -100,6 +100,14 @@ CASES = [
      "schedule": {"4": {"0d": 1}}, "world": 3},
     {"name": "qr_w2_la_single", "kind": "qr", "n": 1000, "b": 128, "scheme": "single", "seed": 16,
      "schedule": {"5": {"0d": 1}}, "world": 2},
+    # Cholesky: right-looking broadcast (default) vs the reference's left-looking
+    # form (per-iteration sum-reduce of partial panel products)
+    {"name": "chol_left", "kind": "cholesky", "n": 640, "b": 128, "scheme": "full", "seed": 5,
+     "schedule": {"0": {"0d": 1}, "2": {"1d": 1}, "3": {"0d": 1}}, "world": 2, "chol_left": True},
+    {"name": "chol_w3_left", "kind": "cholesky", "n": 400, "b": 64, "scheme": "single", "seed": 8,
+     "schedule": {"2": {"2d": 1}, "5": {"0d": 1}}, "world": 3, "chol_left": True},
+    {"name": "chol_w3_clean", "kind": "cholesky", "n": 768, "b": 128, "scheme": "full", "seed": 17,
+     "schedule": {}, "world": 3},
     # clean runs, no checksums
     {"name": "lu_none", "kind": "lu", "n": 512, "b": 128, "scheme": "none", "seed": 9,
      "schedule": {}, "world": 2},
