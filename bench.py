@@ -310,31 +310,36 @@ class Arm:
 
 
 class DistArm:
-    """Block-cyclic factorization over all ranks: every rank
-    holds its column blocks of the same global input, kept on the device."""
+    """Block-cyclic factorization over all ranks: rank 0 alone
+    generates the global input and scatters every rank its column blocks
+    (scatter_input); each rank keeps its local input on the device."""
 
     def __init__(self, kind, n, b, seed, device):
         import paper_2301_03166_b200 as P
         from paper_2301_03166_b200 import _lib
         from paper_2301_03166_b200.distributed import DistributedFactorization
+        import torch.distributed as dist
         self.P, self.L = P, _lib
         self.lib = _lib.load()
         self.kind, self.n, self.b, self.seed = kind, n, b, seed
         t0 = time.perf_counter()
-        if kind == "cholesky":
-            # uniform draws on the host, SPD product on this rank's GPU
-            host = np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n)))
-            tmp = P.Factorization(kind, host, b, device=device)
-            P.linalg.check(self.lib.abft_make_spd(tmp._ctx))
-            tmp._dirty()
-            host = tmp.m
-            del tmp
-        else:
-            host = P.generate_test_matrix(kind, n, seed)
+        host = None
+        if dist.get_rank() == 0:
+            if kind == "cholesky":
+                # uniform draws on the host, SPD product on rank 0's GPU
+                host = np.asfortranarray(np.random.default_rng(seed).uniform(-1.0, 1.0, size=(n, n)))
+                tmp = P.Factorization(kind, host, b, device=device)
+                P.linalg.check(self.lib.abft_make_spd(tmp._ctx))
+                tmp._dirty()
+                host = tmp.m
+                del tmp
+            else:
+                host = P.generate_test_matrix(kind, n, seed)
         self.gen_s = time.perf_counter() - t0
         _GEN["s"] = self.gen_s
-        self.host = host
-        self.f = DistributedFactorization(kind, host, b, device=device, keep_input=True)
+        self.host = host  # rank 0 only
+        self.f = DistributedFactorization(kind, host, b, device=device, keep_input=True, root=0,
+                                          n=n)
         import torch
         self.torch = torch
         self.stream = torch.cuda.ExternalStream(self.f.stream_ptr())
@@ -669,10 +674,8 @@ def run_e2e_dist(arm, args):
     local columns: 1/N of the matrix per rank) in, runs the distributed
     factorization and copies its columns out; time = max over ranks."""
     import torch
-    from paper_2301_03166_b200.distributed import scatter_columns
     f, n = arm.f, args.n
-    rank = torch.distributed.get_rank()
-    local = scatter_columns(arm.host, args.b, rank, f.world)
+    local = f.local_input  # this rank's column blocks (scattered from rank 0)
     pinned_in = torch.empty((max(f.ncl, 1), n), dtype=torch.float64, pin_memory=True).numpy()
     pinned_in[:f.ncl] = local.T
     src = pinned_in.T

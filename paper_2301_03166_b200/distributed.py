@@ -85,6 +85,35 @@ def assemble_columns(parts: list, n: int, b: int) -> np.ndarray:
     return out
 
 
+def scatter_input(a0, n: int, b: int, group=None, root: int = 0, device: int = 0) -> np.ndarray:
+    """The rank's own column blocks of a global matrix that only `root`
+    holds (the others pass None): root cuts every rank's blocks and sends
+    them point to point (NCCL: device buffers; other backends: host), so no
+    rank but root ever materialises the n x n input (8.6 GB at N = 32768)."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    native = dist.get_backend(group) == "nccl"
+    dev = torch.device("cuda", device) if native else torch.device("cpu")
+    gr = (lambda r: r) if group is None else (lambda r: dist.get_global_rank(group, r))
+    if rank == root:
+        a = np.asarray(a0)
+        if a.shape != (n, n):
+            raise ERRORS["dim"]("square input of order n required on the root rank")
+        for r in range(world):
+            if r == root:
+                continue
+            part = scatter_columns(a, b, r, world)
+            # row-major (ncl x n) storage of the Fortran (n x ncl) block
+            t = torch.from_numpy(np.ascontiguousarray(part.T)).to(dev)
+            dist.send(t, gr(r), group=group)
+        return scatter_columns(a, b, root, world)
+    ncl = local_columns(n, b, rank, world)
+    t = torch.empty((ncl, n), dtype=torch.float64, device=dev)
+    dist.recv(t, gr(root), group=group)
+    return np.asfortranarray(t.cpu().numpy().T)
+
+
 def merge_events(per_rank: list) -> list:
     """Events of all ranks (dicts with EVENT_FIELDS) in the reference's
     location order: iteration, block row, block column, column
@@ -172,14 +201,21 @@ class DistributedFactorization:
     column blocks on its GPU.
     """
 
-    def __init__(self, kind, a0: np.ndarray, b: int, group=None, device: int | None = None,
-                 keep_input: bool = False):
+    def __init__(self, kind, a0: np.ndarray | None, b: int, group=None, device: int | None = None,
+                 keep_input: bool = False, root: int | None = None, n: int | None = None):
+        """``root``: only that rank passes the global ``a0`` (the others pass
+        None and the order ``n``); it is scattered by column blocks
+        (scatter_input). Otherwise every rank passes the same ``a0``."""
         import torch
         import torch.distributed as dist
         self.kind = DecompositionKind(_value(kind))
-        n = a0.shape[0]
-        if a0.ndim != 2 or a0.shape != (n, n):
-            raise ERRORS["dim"]("square input required")
+        if root is not None and a0 is None:
+            if n is None:
+                raise ERRORS["dim"]("the order n is required on non-root ranks")
+        else:
+            n = a0.shape[0]
+            if a0.ndim != 2 or a0.shape != (n, n):
+                raise ERRORS["dim"]("square input required")
         self.n, self.b = n, int(b)
         self.layout = BlockLayout(n, self.b)
         self.group = group
@@ -194,8 +230,13 @@ class DistributedFactorization:
         self._ctx = ctx
         if keep_input:  # device copy of the local input for reset()
             check(lib.abft_dist_keep_input(ctx, 1))
-        host = np.asfortranarray(np.asarray(a0, dtype=np.float64))
-        check(lib.abft_dist_set_matrix(ctx, _lib.dptr(host), n))
+        if root is not None:
+            self.local_input = scatter_input(a0, n, self.b, group, root, self.device)
+            check(lib.abft_dist_set_local(ctx, _lib.dptr(self.local_input), n))
+        else:
+            host = np.asfortranarray(np.asarray(a0, dtype=np.float64))
+            check(lib.abft_dist_set_matrix(ctx, _lib.dptr(host), n))
+            self.local_input = None
         self.ncl = int(lib.abft_dist_local_cols(ctx))
         dev = torch.device("cuda", self.device)
         cap = max(int(lib.abft_dist_xbuf_elems(ctx, k)) for k in range(self.layout.n_blocks))

@@ -35,9 +35,14 @@ def gpu_cases(rank: int, world: int, init_file: str, cases: list, out: str) -> N
     results = []
     for c in cases:
         a = P.generate_test_matrix(c["kind"], c["n"], c["seed"])
+        root = c.get("root")  # input only on this rank, scattered by column blocks
         if c.get("chol_left"):  # the reference's left-looking form (sum-reduce exchange)
             os.environ["ABFT_DIST_CHOL"] = "left"
-        f = DistributedFactorization(c["kind"], a, c["b"], keep_input=bool(c.get("reset")))
+        if root is not None:
+            f = DistributedFactorization(c["kind"], a if rank == root else None, c["b"],
+                                         keep_input=bool(c.get("reset")), root=root, n=c["n"])
+        else:
+            f = DistributedFactorization(c["kind"], a, c["b"], keep_input=bool(c.get("reset")))
         os.environ.pop("ABFT_DIST_CHOL", None)
         f.lookahead = not c.get("no_lookahead", False)
         if c.get("reset"):  # a throw-away factorization, then restore the kept input
@@ -83,6 +88,23 @@ def cpu_merge(rank: int, world: int, init_file: str, out: str) -> None:
         json.dump({"order": [(e["iter"], e["block_row"], e["block_col"], e["seq"]) for e in merged],
                    "counts": [sum(r.detected.values()) for r in reps],
                    "locations": [r.locations for r in reps]}, fh, default=str)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def cpu_scatter(rank: int, world: int, init_file: str, out: str) -> None:
+    """scatter_input over gloo: only the root holds the global matrix."""
+    import numpy as np
+    dist = _init(rank, world, init_file)
+    from paper_2301_03166_b200.distributed import scatter_columns, scatter_input
+    n, b, root = 70, 16, world - 1
+    a = np.asfortranarray(np.arange(n * n, dtype=np.float64).reshape(n, n)) if rank == root else None
+    local = scatter_input(a, n, b, None, root)
+    ref = scatter_columns(np.asfortranarray(np.arange(n * n, dtype=np.float64).reshape(n, n)), b,
+                          rank, world)
+    with open(os.path.join(out, f"rank{rank}.json"), "w") as fh:
+        json.dump({"ok": bool(local.shape == ref.shape and np.array_equal(local, ref)),
+                   "fortran": bool(local.flags.f_contiguous)}, fh)
     dist.barrier()
     dist.destroy_process_group()
 

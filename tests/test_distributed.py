@@ -35,6 +35,17 @@ def _spawn(target, world, *args, timeout=600):
 # ---------------------------------------------------------------------------
 # CPU
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("world", [2, 3])
+def test_scatter_input_from_root_over_gloo(tmp_path, world):
+    """Only the root rank holds the global input; every rank receives exactly
+    its block-cyclic column blocks (Fortran order, ready for set_local)."""
+    from dist_worker import cpu_scatter
+    _spawn(cpu_scatter, world, str(tmp_path / "init"), str(tmp_path))
+    for r in range(world):
+        res = json.loads((tmp_path / f"rank{r}.json").read_text())
+        assert res["ok"] and res["fortran"], (r, res)
+
+
 @pytest.mark.parametrize("n,b,world", [(100, 16, 2), (96, 32, 3), (64, 64, 2), (130, 32, 4)])
 def test_scatter_assemble_roundtrip(n, b, world):
     a = np.asfortranarray(np.random.default_rng(0).standard_normal((n, n)))
@@ -107,7 +118,9 @@ CASES = [
     {"name": "chol_w3_left", "kind": "cholesky", "n": 400, "b": 64, "scheme": "single", "seed": 8,
      "schedule": {"2": {"2d": 1}, "5": {"0d": 1}}, "world": 3, "chol_left": True},
     {"name": "chol_w3_clean", "kind": "cholesky", "n": 768, "b": 128, "scheme": "full", "seed": 17,
-     "schedule": {}, "world": 3},
+     "schedule": {}, "world": 3, "root": 1},
+    {"name": "lu_w2_root", "kind": "lu", "n": 640, "b": 128, "scheme": "full", "seed": 18,
+     "schedule": {"1": {"0d": 1}}, "world": 2, "root": 0},
     # clean runs, no checksums
     {"name": "lu_none", "kind": "lu", "n": 512, "b": 128, "scheme": "none", "seed": 9,
      "schedule": {}, "world": 2},
