@@ -164,12 +164,13 @@ int qr_panel_factor(cudaStream_t st, double* P, int64_t ld, int64_t m, int w, do
   GemmWorkspace* g = ws.gws;
   const int mi = (int)m;
   CUDA_TRY(cudaMemsetAsync(ws.info, 0, sizeof(int), st));
-  // the cluster diagonal-block kernel needs ceil(w/32) co-resident SMs: only
-  // when the panel owns the GPU (beside the look-ahead's persistent GEMM the
-  // cluster cannot be placed until that GEMM drains)
+  // the multi-CTA diagonal-block kernel needs ceil(w/32) co-resident SMs
+  // (cooperative launch, anywhere on the chip): beside the look-ahead's
+  // persistent GEMM it runs on the panel's reserved SMs
   auto dfac = [&](double* D, int mode, double* Li, double* Ui, double* sg) {
-    return max_ctas > 0 ? diag_factor(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg)
-                        : diag_factor_fast(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg);
+    return (max_ctas > 0 && max_ctas < (w + 31) / 32)
+               ? diag_factor(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg)
+               : diag_factor_fast(st, D, s, w, mode, Li, s, Ui, s, ws.info, 0, sg);
   };
   // CholeskyQR, pass 1
   ABFT_TRY(gemm_capped(st, 'T', 'N', w, w, mi, 1.0, P, ld, P, ld, 0.0, nullptr, 0, G1, s, g,

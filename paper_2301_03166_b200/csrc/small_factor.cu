@@ -27,7 +27,8 @@
 // changes no pivot of the real block). Breakdown follows the reference: LU
 // pivot == 0 or non-finite, Cholesky pivot <= 0 or non-finite; info gets
 // 1 + (col_base + column) of the first one and nothing else is written.
-#include <cooperative_groups.h>
+#include <atomic>
+#include <mutex>
 
 #include "panel.cuh"
 
@@ -35,7 +36,6 @@ namespace abft {
 
 namespace {
 
-namespace cg = cooperative_groups;
 
 #ifdef CF_TRACE
 __device__ long long g_cf_trace[8][64];
@@ -45,7 +45,7 @@ __device__ long long g_cf_clk[4];
     if (threadIdx.x == 0 && (slot) < 64) {                                    \
       long long t_;                                                           \
       asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                  \
-      g_cf_trace[cluster.block_rank()][(slot)] = t_;                          \
+      g_cf_trace[blockIdx.x][(slot)] = t_;                            \
     }                                                                         \
   } while (0)
 #else
@@ -57,6 +57,29 @@ __device__ long long g_cf_clk[4];
 constexpr int CF_T = 256;    // threads per CTA (8 warps)
 constexpr int CF_MAXB = 8;   // cluster size limit (portable): w <= 256
 constexpr int TS = 33;       // stride of the 32 x 32 tiles
+
+// Grid barrier of the nb co-resident CTAs (cooperative launch): sync[0]
+// counts arrivals (monotonic; the host zeroes the slot before the launch),
+// sync[1] carries the breakdown flag. Release/acquire through the L2.
+ABFT_DEVINL void grid_barrier(int* sync, int target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(sync, 1);
+    int v;
+    do {
+      asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(sync) : "memory");
+    } while (v < target);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+ABFT_DEVINL int read_flag(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 
 // Out[i, c] -= sum_l A[i + l*lda] * B[l*TS + c] for rows i in [r0, r1)
 // (r1 - r0 <= 224), c < 32. A may live in another CTA's shared memory.
@@ -106,7 +129,7 @@ ABFT_DEVINL void global_block_column(T* Dst, int ldd, const T* G, int64_t ld, in
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       const int i = r0 + tx + 32 * e;
-      v[q][e] = (i < r1 && i < w && gc < w) ? G[i + (int64_t)gc * ld] : (i == gc ? T(1) : T(0));
+      v[q][e] = (i < r1 && i < w && gc < w) ? __ldcg(G + i + (int64_t)gc * ld) : (i == gc ? T(1) : T(0));
     }
   }
 #pragma unroll
@@ -124,7 +147,7 @@ template <typename T>
 ABFT_DEVINL void global_tile(T* Tile, const T* G, int64_t ld, int w, int c0) {
   for (int idx = threadIdx.x; idx < 32 * 32; idx += CF_T) {
     const int i = idx & 31, c = idx >> 5;
-    Tile[i + c * TS] = (c0 + i < w && c0 + c < w) ? G[(c0 + i) + (int64_t)(c0 + c) * ld]
+    Tile[i + c * TS] = (c0 + i < w && c0 + c < w) ? __ldcg(G + (c0 + i) + (int64_t)(c0 + c) * ld)
                                                   : (i == c ? T(1) : T(0));
   }
 }
@@ -288,11 +311,11 @@ ABFT_DEVINL void tile_mul_inplace(T* Out, int ldo, int r0, int r1, const T* B, i
 template <typename T>
 __global__ void __launch_bounds__(CF_T, 1)
     cluster_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl, T* Uinv,
-                          int64_t ldu, int* info, int64_t col_base, T* sgn) {
-  cg::cluster_group cluster = cg::this_cluster();
+                          int64_t ldu, int* info, int64_t col_base, T* sgn, int* sync) {
   extern __shared__ __align__(16) unsigned char cf_raw[];
-  const int nb = (int)cluster.num_blocks();
-  const int r = (int)cluster.block_rank();
+  const int nb = (int)gridDim.x;
+  const int r = (int)blockIdx.x;
+  int gen = 0;
   const int Wp = 32 * nb;  // padded order = column stride of Cs / Xs
   T* Cs = reinterpret_cast<T*>(cf_raw);  // block column r of the matrix
   T* Xs = Cs + 32 * Wp;                  // block column r of L^{-1}, then of U^{-1}
@@ -364,10 +387,10 @@ __global__ void __launch_bounds__(CF_T, 1)
       __syncthreads();
       CF_MARK(1 + 4 * j);
     }
-    cluster.sync();  // panel j, its inverses and its flag are visible
+    if (r == j && *s_bad && tid == 0) atomicExch(sync + 1, 1);
+    grid_barrier(sync, ++gen * nb);  // panel j, its inverses and its flag are visible
     CF_MARK(2 + 4 * j);
-    const int* badj = cluster.map_shared_rank(s_bad, j);
-    if (*badj) {
+    if (read_flag(sync + 1)) {
       bad = true;
       break;
     }
@@ -401,7 +424,7 @@ __global__ void __launch_bounds__(CF_T, 1)
     CF_MARK(4 + 4 * j);
   }
   CF_MARK(40);
-  cluster.sync();  // every block column final; nobody reads a panel any more
+  grid_barrier(sync, ++gen * nb);  // every block column final
   CF_MARK(41);
   if (!bad) {
     // factor out (Cholesky: lower part, zeros above)
@@ -415,7 +438,7 @@ __global__ void __launch_bounds__(CF_T, 1)
       // U^{-1}, block column r: Y = E_r, then for j = r..0:
       //   Y_jr = U_jj^{-1} Y_jr,  Y_ir -= U_ij Y_jr (i < j)  (U_ij: block
       //   column j of the final factor, read back from D)
-      cluster.sync();  // every CTA's block column is in D
+      grid_barrier(sync, ++gen * nb);  // every CTA's block column is in D
       for (int c = ty; c < 32; c += CF_T / 32)
         for (int i = tid & 31; i < Wp; i += 32) Xs[i + c * Wp] = (i == c0 + c) ? T(1) : T(0);
       __syncthreads();
@@ -439,13 +462,30 @@ __global__ void __launch_bounds__(CF_T, 1)
     }
   }
   CF_MARK(42);
-  cluster.sync();  // keep every CTA's shared memory alive until all remote reads are done
-  CF_MARK(43);
 }
 
 template <typename T>
 size_t cf_smem_bytes(int nb) {
   return (size_t)(3 * 32 * 32 * nb + 4 * 32 * TS + 64) * sizeof(T) + 16;
+}
+
+// One barrier slot per launch (arrival counter + breakdown flag), zeroed on
+// the launch's stream; 4096 slots in rotation.
+__device__ int g_cf_sync[4096 * 2];
+
+int* next_sync_slot() {
+  static std::atomic<unsigned> ticket{0};
+  static int* base = nullptr;
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!base) {
+      void* p = nullptr;
+      if (cudaGetSymbolAddress(&p, g_cf_sync) != cudaSuccess) return nullptr;
+      base = static_cast<int*>(p);
+    }
+  }
+  return base + 2 * (ticket.fetch_add(1) % 4096u);
 }
 
 template <typename T>
@@ -454,21 +494,19 @@ int cluster_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv
   const int nb = (w + 31) / 32;
   const size_t smem = cf_smem_bytes<T>(nb);
   ABFT_TRY(ensure_smem_attr((const void*)cluster_factor_kernel<T>, (int)smem));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nb);
-  cfg.blockDim = dim3(CF_T);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = nb;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  int* sync = next_sync_slot();
+  if (!sync) {
+    set_last_error("cluster_factor: barrier slots unavailable");
+    return -1;
+  }
+  CUDA_TRY(cudaMemsetAsync(sync, 0, 2 * sizeof(int), st));
+  // cooperative launch: the nb CTAs are co-resident (anywhere on the chip --
+  // no GPC co-location as a thread-block cluster would need, so it also runs
+  // beside a persistent GEMM that leaves a few SMs free)
+  void* args[] = {&D, &ld, &w, &mode, &Linv, &ldl, &Uinv, &ldu, &info_dev, &col_base, &sgn, &sync};
   count_launch();
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, cluster_factor_kernel<T>, D, ld, w, mode, Linv, ldl, Uinv,
-                              ldu, info_dev, col_base, sgn));
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cluster_factor_kernel<T>, dim3(nb), dim3(CF_T),
+                                       args, smem, st));
   return 0;
 }
 
