@@ -87,6 +87,8 @@ struct abft_sctx {
   double* v64 = nullptr;     // n x b (ld)
   double* t64 = nullptr;     // b x b (ld_t)
   double* gram = nullptr;    // b x b
+  bool lu_coop = true;          // LU look-ahead diagonal factor on the multi-CTA kernel
+                                // beside the update capped at sms - b/32 (ABFT_LU_COOP=0: off)
   bool chol_cluster = true;     // Cholesky PD on the cluster kernel (ABFT_CHOL_CLUSTER=0: off);
                                 // spotrf N=16384 32.4 -> 35.4 TF/s (the fp32 update is short,
                                 // so the diagonal chain was on the critical path)
@@ -376,6 +378,9 @@ int s_check_info(abft_sctx* c) {
 // ---- tasks -------------------------------------------------------------------
 int s_lu_diag(abft_sctx* c, cudaStream_t st, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (c->lu_coop)
+    return diag_factor_fast(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv,
+                            c->ld_t, c->info, p);
   return diag_factor(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv, c->ld_t,
                      c->info, p);
 }
@@ -836,7 +841,8 @@ int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
     if (fuse) fs = s_fused(c, r0, c0 + wa);
     smark(c, SP_TMU, true);
     ABFT_TRY(s_gemm(c, 'N', 'N', rows, cols - wa, w, -1.0f, L21, c->ld, U12 + wa * c->ld, c->ld, 1.0f,
-                    A22 + wa * c->ld, c->ld, A22 + wa * c->ld, c->ld, fuse ? &fs : nullptr, sms - 2));
+                    A22 + wa * c->ld, c->ld, A22 + wa * c->ld, c->ld, fuse ? &fs : nullptr,
+                    sms - (c->lu_coop ? (int)((c->b + 31) / 32) : 2)));
     smark(c, SP_TMU, false);
     if (prot) {
       smark(c, SP_ABFT, true);
@@ -1002,6 +1008,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     c->fuse_enabled = !(e && e[0] == '1');
     const char* e4 = getenv("ABFT_CHOL_CLUSTER");
     if (e4 && e4[0] == '0') c->chol_cluster = false;
+    const char* e5 = getenv("ABFT_LU_COOP");
+    if (e5) c->lu_coop = e5[0] == '1';
   }
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
     set_last_error("cudaStreamCreate failed");
