@@ -118,7 +118,9 @@ struct abft_ctx {
   int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
   GemmWorkspace gws2;             // split-K workspace of the side stream
   int qr_la_sms = 16;             // QR look-ahead: SMs left to the side-stream panel
-                                  // (ABFT_QR_LA_SMS)
+  bool qr_la_sms_fixed = false;   // ABFT_QR_LA_SMS=R fixes it; else qr_panel_sms's model
+  bool lu_coop = true;            // late LU look-ahead iterations: multi-CTA diagonal factor
+                                  // (ABFT_LU_COOP=0: always the one-CTA kernel)
   bool chol_cluster = false;      // Cholesky PD on the cluster kernel, submitted ahead of
                                   // the look-ahead update (ABFT_CHOL_CLUSTER=1). Off for
                                   // fp64: PD is hidden behind the K = p update, whose
@@ -315,8 +317,11 @@ int chol_rs_update(abft_ctx* c, int64_t k) {
 }
 
 // LU panel, part 1: factor the diagonal block and form L11^{-1}, U11^{-1}.
-int lu_diag(abft_ctx* c, cudaStream_t st, int64_t k) {
+int lu_diag(abft_ctx* c, cudaStream_t st, int64_t k, bool fast = false) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  if (fast)
+    return diag_factor_fast(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv,
+                            c->ld_t, c->info, p);
   return diag_factor(st, c->m + p + p * c->ld, c->ld, (int)w, 0, c->linv, c->ld_t, c->uinv,
                      c->ld_t, c->info, p);
 }
@@ -787,25 +792,30 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
     ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
     prof_mark(c, PROF_ABFT, false);
   }
-  // side stream: diagonal block of panel k+1
+  // side stream: diagonal block of panel k+1. A long update hides the one-CTA
+  // factor on 2 free SMs; once the update gets short (late iterations) the
+  // multi-CTA factor (b/32 SMs, ~2x faster) is worth the SMs it takes.
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const double upd_s = 2.0 * (double)rows * (double)(cols - wa) * (double)w / (30.0e12 * (sms - 2) / 148.0);
+  const bool fast_diag = c->lu_coop && upd_s < 1.0e-3;
+  const int keep = fast_diag ? (int)((c->b + 31) / 32) : 2;
   CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
-  ABFT_TRY(lu_diag(c, c->st2, k + 1));
+  ABFT_TRY(lu_diag(c, c->st2, k + 1, fast_diag));
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   // (b) the rest of the trailing matrix with fused checksums
   if (cols > wa) {
-    int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
     prof_mark(c, PROF_TMU, true);
     if (prot) {
       FusedSums fs = fused_for(c, r0, c0 + wa);
       ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
                                c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
-                               A22 + wa * c->ld, c->ld, (int)c->b, fs, sms - 2));
+                               A22 + wa * c->ld, c->ld, (int)c->b, fs, sms - keep));
     } else {
       ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
                              c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
-                             A22 + wa * c->ld, c->ld, sms - 2));
+                             A22 + wa * c->ld, c->ld, sms - keep));
     }
     prof_mark(c, PROF_TMU, false);
     if (prot) {
@@ -823,6 +833,33 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   ABFT_TRY(emit_column(c, k + 1));
   c->pd_ready = k + 1;
   return 0;
+}
+
+// SMs for the look-ahead's side-stream QR panel of iteration k (the B200
+// form of the reference's slack reclamation, scheduler.py:84-146: the stream
+// with slack gets fewer resources). A per-iteration model at the measured
+// per-SM DMMA rate: panel(R) = four tall GEMM passes (8 m b^2 flops) on R
+// SMs + the latency of its small factorizations; update(R) = C -= V mid on
+// the other SMs; R minimises max(panel, update). ABFT_QR_LA_SMS > 0 fixes R.
+int qr_panel_sms(const abft_ctx* c, int64_t k, int sms) {
+  if (c->qr_la_sms_fixed) return std::max(1, std::min(c->qr_la_sms, sms / 2));
+  const double rate = 30.0e12 / 148.0;  // fused trailing-update rate per SM (bench_lu32k_r02)
+  const double lat = 0.8e-3;            // three multi-CTA diagonal factors + small GEMMs
+  const double n = (double)c->n, b = (double)c->b, p = (double)(k * c->b);
+  const double m1 = n - p - b;          // rows of panel k+1
+  const double cols = n - p - 2 * b;    // columns left to part (b) of the update
+  int best = 16;
+  double best_t = 1e30;
+  for (int R = 8; R <= 48 && R < sms / 2; R += 4) {
+    const double tp = 8.0 * m1 * b * b / (R * rate) + lat;
+    const double tu = cols > 0 ? 2.0 * (n - p) * cols * b / ((sms - R) * rate) : 0.0;
+    const double t = std::max(tp, tu);
+    if (t < 0.995 * best_t) {
+      best_t = t;
+      best = R;
+    }
+  }
+  return best;
 }
 
 // QR protected trailing update with look-ahead (fault-free iterations of the
@@ -876,7 +913,7 @@ int protected_tmu_qr_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   // side stream: panel k+1 on qr_la_sms SMs
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  const int res = std::max(1, std::min(c->qr_la_sms, sms / 2));
+  const int res = qr_panel_sms(c, k, sms);
   CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
   {
@@ -1085,10 +1122,15 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     c->fuse_enabled = !(e && e[0] == '1');
     const char* e2 = getenv("ABFT_NO_LOOKAHEAD");
     c->lookahead_enabled = !(e2 && e2[0] == '1');
+    const char* e5 = getenv("ABFT_LU_COOP");
+    if (e5) c->lu_coop = e5[0] == '1';
     const char* e4 = getenv("ABFT_CHOL_CLUSTER");
     if (e4) c->chol_cluster = e4[0] == '1';
     const char* e3 = getenv("ABFT_QR_LA_SMS");
-    if (e3) c->qr_la_sms = atoi(e3);  // 0 disables the QR look-ahead
+    if (e3) {
+      c->qr_la_sms = atoi(e3);  // 0 disables the QR look-ahead
+      c->qr_la_sms_fixed = true;
+    }
   }
   int rc = 0;
   auto fail = [&](int r) {
