@@ -192,6 +192,14 @@ ABFT_API int abft_get_qr_panel(abft_ctx* ctx, int64_t k, double* V, int64_t ldv,
  * ms[0]=PD, ms[1]=PU, ms[2]=TMU GEMMs, ms[3]=ABFT encode/maintain/verify/inject */
 ABFT_API int abft_profile(abft_ctx* ctx, int enable);
 ABFT_API int abft_profile_read(abft_ctx* ctx, double* ms);
+/* per-iteration device times since abft_profile(ctx, 1): out[4k + t], t = PD
+ * (a look-ahead's side-stream panel included), PU, TMU GEMMs, ABFT work */
+ABFT_API int abft_profile_read_iters(abft_ctx* ctx, double* out, int64_t nb);
+/* per-iteration SMs left to the panel work beside a look-ahead update (QR:
+ * the side-stream panel; LU: >= ceil(b/32) selects the multi-CTA diagonal
+ * factor); NULL / 0 = built-in choice. The run modes' slack-reclamation lever
+ * (replaces the reference's DVFS decisions, scheduler.py:84-146). */
+ABFT_API int abft_set_side_sms(abft_ctx* ctx, const int32_t* sms, int64_t nb);
 /* FP64 DMMA issue-rate probe (TFLOP/s) over all SMs: the roofline denominator */
 ABFT_API int abft_probe_dmma_peak(int iters, double* tflops);
 /* in-device snapshot slots replacing _Run._snapshot/_restore (simulator.py:420-436) */

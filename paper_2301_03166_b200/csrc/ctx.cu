@@ -12,6 +12,7 @@
 // GLOBAL b-grid so the verify pass of iteration k is the encode of k+1 for LU
 // and QR (their next region is a block-aligned sub-grid untouched by PD/PU).
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -136,8 +137,14 @@ struct abft_ctx {
   // profiling
   struct ProfPair {
     int cat;
+    int32_t iter;
     cudaEvent_t e0, e1;
   };
+  std::vector<std::array<double, 4>> prof_iter;  // per-iteration PD/PU/TMU/ABFT ms
+  cudaEvent_t prof_open2 = nullptr;              // side-stream (look-ahead) PD bracket
+  // per-iteration SMs left to the panel work beside a look-ahead update
+  // (abft_set_side_sms; empty = the built-in choice): the run modes' lever
+  std::vector<int32_t> side_sms;
   bool prof_on = false;
   double prof_ms[4] = {0, 0, 0, 0};
   std::vector<ProfPair> prof_pending;
@@ -167,8 +174,22 @@ void prof_mark(abft_ctx* c, int cat, bool begin) {
   if (begin) {
     c->prof_open[cat] = e;
   } else {
-    c->prof_pending.push_back({cat, c->prof_open[cat], e});
+    c->prof_pending.push_back({cat, c->cur_iter, c->prof_open[cat], e});
     c->prof_open[cat] = nullptr;
+  }
+}
+
+// PD bracket on the side stream (the look-ahead's panel k+1, credited to
+// iteration k+1)
+void prof_mark_side(abft_ctx* c, bool begin, int32_t iter) {
+  if (!c->prof_on) return;
+  cudaEvent_t e = prof_event(c);
+  cudaEventRecord(e, c->st2);
+  if (begin) {
+    c->prof_open2 = e;
+  } else {
+    c->prof_pending.push_back({PROF_PD, iter, c->prof_open2, e});
+    c->prof_open2 = nullptr;
   }
 }
 
@@ -342,7 +363,8 @@ int task_pd(abft_ctx* c, int64_t k) {
     ABFT_TRY(lu_diag(c, c->st, k));
     ABFT_TRY(lu_l21(c, k));
   } else if (c->kind == ABFT_CHOLESKY) {
-    if (c->chol_cluster)
+    const bool side_set = (int64_t)c->side_sms.size() > k && c->side_sms[k] > 0;
+    if (side_set ? c->side_sms[k] >= (int)((c->b + 31) / 32) : c->chol_cluster)
       ABFT_TRY(diag_factor_fast(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
     else
       ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
@@ -723,7 +745,9 @@ int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next, bool ev_recorded = f
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   double* P1 = c->m + p1 + p1 * c->ld;
-  const int keep = c->chol_cluster ? (int)((c->b + 31) / 32) : 1;
+  int keep = c->chol_cluster ? (int)((c->b + 31) / 32) : 1;
+  if ((int64_t)c->side_sms.size() > k && c->side_sms[k] > 0)
+    keep = std::max(1, std::min((int)c->side_sms[k], sms / 2));
   ABFT_TRY(gemm_capped(c->st2, 'N', 'T', (int)(n - p1), (int)w1, (int)pk, -1.0, c->m + p1, c->ld,
                        c->m + p1, c->ld, 1.0, P1, c->ld, P1, c->ld, &c->gws2, sms - keep));
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
@@ -798,11 +822,18 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   const double upd_s = 2.0 * (double)rows * (double)(cols - wa) * (double)w / (30.0e12 * (sms - 2) / 148.0);
-  const bool fast_diag = c->lu_coop && upd_s < 1.0e-3;
-  const int keep = fast_diag ? (int)((c->b + 31) / 32) : 2;
+  const int nbd = (int)((c->b + 31) / 32);
+  bool fast_diag = c->lu_coop && upd_s < 1.0e-3;
+  int keep = fast_diag ? nbd : 2;
+  if ((int64_t)c->side_sms.size() > k + 1 && c->side_sms[k + 1] > 0) {
+    keep = std::max(1, std::min((int)c->side_sms[k + 1], sms / 2));
+    fast_diag = keep >= nbd;
+  }
   CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  prof_mark_side(c, true, (int32_t)(k + 1));
   ABFT_TRY(lu_diag(c, c->st2, k + 1, fast_diag));
+  prof_mark_side(c, false, (int32_t)(k + 1));
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   // (b) the rest of the trailing matrix with fused checksums
   if (cols > wa) {
@@ -842,6 +873,8 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
 // SMs + the latency of its small factorizations; update(R) = C -= V mid on
 // the other SMs; R minimises max(panel, update). ABFT_QR_LA_SMS > 0 fixes R.
 int qr_panel_sms(const abft_ctx* c, int64_t k, int sms) {
+  if ((int64_t)c->side_sms.size() > k + 1 && c->side_sms[k + 1] > 0)
+    return std::max(1, std::min((int)c->side_sms[k + 1], sms / 2));
   if (c->qr_la_sms_fixed) return std::max(1, std::min(c->qr_la_sms, sms / 2));
   const double rate = 30.0e12 / 148.0;  // fused trailing-update rate per SM (bench_lu32k_r02)
   const double lat = 0.8e-3;            // three multi-CTA diagonal factors + small GEMMs
@@ -920,9 +953,11 @@ int protected_tmu_qr_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
     const int64_t p1 = pe, pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
     QrPanelWork q = c->qrw;
     q.gws = &c->gws2;
+    prof_mark_side(c, true, (int32_t)(k + 1));
     ABFT_TRY(qr_panel_factor(c->st2, c->m + p1 + p1 * c->ld, c->ld, n - p1, (int)w1,
                              c->vstore + p1 + p1 * c->ld, c->ld,
                              c->tstore + (k + 1) * c->b * c->ld_t, c->ld_t, c->betas, q, res));
+    prof_mark_side(c, false, (int32_t)(k + 1));
   }
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   // (b) the rest of the region
@@ -988,7 +1023,9 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
   if (c->kind == ABFT_CHOLESKY) {
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
     const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb;
-    if (la && c->chol_cluster) {
+    const bool side_set = (int64_t)c->side_sms.size() > k && c->side_sms[k] > 0;
+    const bool fast_pd = side_set ? c->side_sms[k] >= (int)((c->b + 31) / 32) : c->chol_cluster;
+    if (la && fast_pd) {
       CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
       ABFT_TRY(pd());
       ABFT_TRY(chol_lookahead(c, k, c->next_scheme, true));
@@ -1499,6 +1536,31 @@ ABFT_API int abft_profile(abft_ctx* c, int enable) {
   c->prof_on = enable != 0;
   for (int i = 0; i < PROF_N; ++i) c->prof_ms[i] = 0.0;
   c->prof_pending.clear();
+  c->prof_iter.assign(c->nb, {0.0, 0.0, 0.0, 0.0});
+  return 0;
+}
+
+// Per-iteration device times since abft_profile(ctx, 1): out[4k + t] for
+// t = PD (incl. a look-ahead's side-stream panel), PU, TMU, ABFT.
+ABFT_API int abft_profile_read_iters(abft_ctx* c, double* out, int64_t nb) {
+  double tot[4];
+  ABFT_TRY(abft_profile_read(c, tot));
+  for (int64_t k = 0; k < nb && k < (int64_t)c->prof_iter.size(); ++k)
+    for (int t = 0; t < 4; ++t) out[4 * k + t] = c->prof_iter[k][t];
+  return 0;
+}
+
+// Per-iteration SMs left to the panel work when iteration k's panel is
+// factored beside a look-ahead update (QR: the side-stream panel's GEMMs;
+// LU: >= ceil(b/32) selects the multi-CTA diagonal factor). 0 or a null
+// array: the built-in choice. The B200 form of the reference's slack
+// reclamation (scheduler.py:84-146): the stream with slack gets fewer SMs.
+ABFT_API int abft_set_side_sms(abft_ctx* c, const int32_t* sms, int64_t nb) {
+  if (!sms || nb <= 0) {
+    c->side_sms.clear();
+    return 0;
+  }
+  c->side_sms.assign(sms, sms + nb);
   return 0;
 }
 
@@ -1507,10 +1569,13 @@ ABFT_API int abft_profile(abft_ctx* c, int enable) {
 ABFT_API int abft_profile_read(abft_ctx* c, double* ms) {
   DevGuard g(c->device);
   CUDA_TRY(cudaStreamSynchronize(c->st));
+  if ((int64_t)c->prof_iter.size() < c->nb) c->prof_iter.resize(c->nb, {0.0, 0.0, 0.0, 0.0});
+  CUDA_TRY(cudaStreamSynchronize(c->st2));
   for (auto& pe : c->prof_pending) {
     float f = 0.f;
     CUDA_TRY(cudaEventElapsedTime(&f, pe.e0, pe.e1));
     c->prof_ms[pe.cat] += f;
+    if (pe.iter >= 0 && pe.iter < c->nb) c->prof_iter[pe.iter][pe.cat] += f;
     c->prof_free.push_back(pe.e0);
     c->prof_free.push_back(pe.e1);
   }

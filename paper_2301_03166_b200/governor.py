@@ -27,6 +27,18 @@ Here the same loop runs over the B200 path with MEASURED task times:
 The mode flags are the reference's (config.py:30-39): ``original`` and
 ``r2h`` run unprotected at base clocks, ``sr`` reclaims slack downward only,
 ``bsr`` overclocks the critical side under adaptive SINGLE/FULL checksums.
+
+Two engines. ``engine="iteration"`` (default) is the reference's loop one
+iteration at a time (snapshots + recompute recovery, a host synchronisation
+per iteration, no look-ahead). ``engine="stream"`` (run_mode_streamed) runs
+the modes on the one-call look-ahead path with a PHYSICAL lever: the panel
+work of iteration k+1 runs on a side stream beside the update of k, and the
+decision's reclaimed slack becomes the number of SMs left to that side stream
+(abft_set_side_sms) -- the stream with slack gets fewer SMs, the critical one
+more -- so the modes change measured time and NVML energy. Its decisions use
+the history predictor over the per-iteration times of a calibration pass;
+fault counts are drawn up front from the predicted update times; an
+uncorrectable event falls back to the iteration engine (recompute recovery).
 """
 from __future__ import annotations
 
@@ -346,6 +358,7 @@ class IterationRecord:
     retries: int = 0
     pred_time_s: dict = field(default_factory=dict)    # task -> predicted seconds
     actual_time_s: dict = field(default_factory=dict)  # task -> measured seconds
+    side_sms: int = 0          # stream engine: SMs left to the panel (0 = built-in split)
 
 
 @dataclass
@@ -407,10 +420,18 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
              rates: ErrorRateTable | None = None, recovery: str = "recompute",
              fc_desired: float = 0.999999, forced_scheme=None, device: int | None = None,
              cpu: ClockDomain | None = None, gpu: ClockDomain | None = None,
-             precision: str = "f64"):
+             precision: str = "f64", engine: str = "iteration"):
     """One factorization under a run mode (simulate_run(engine="numeric"),
     simulator.py:440-492) with measured B200 task times. Returns
-    (RunSummary, [IterationRecord])."""
+    (RunSummary, [IterationRecord]). engine="stream": run_mode_streamed."""
+    if engine == "stream":
+        if precision != "f64":
+            raise ValueError("engine='stream' drives the fp64 context")
+        return run_mode_streamed(kind, a0, b, mode, r, seed, rates=rates, recovery=recovery,
+                                 fc_desired=fc_desired, forced_scheme=forced_scheme,
+                                 device=device, cpu=cpu, gpu=gpu)
+    if engine != "iteration":
+        raise ValueError("engine must be 'iteration' or 'stream'")
     if mode not in MODES:
         raise ValueError(f"mode must be one of {MODES}")
     if recovery not in RECOVERY_POLICIES:
@@ -527,6 +548,187 @@ def run_mode(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5, se
                          (e1 - e0) / 1e3 if e0 is not None and e1 is not None else None,
                          res, res <= tol and not unrecoverable, injected, detected, corrected,
                          unrecoverable, total_retries, schemes)
+    return summary, records
+
+
+SIDE_BASE = {DecompositionKind.QR: (16, 8, 48), DecompositionKind.LU: (2, 2, 8),
+             DecompositionKind.CHOLESKY: (1, 1, 8)}
+# panel-side latency that more SMs do not shorten (three multi-CTA diagonal
+# factors + small GEMMs per QR panel, tools/prof/diag_probe.py)
+SIDE_FIXED_S = {DecompositionKind.QR: 0.75e-3}
+
+
+def _side_time(kind, t_panel, R, base):
+    """Panel-side time on R SMs from its time at the fixed split `base`."""
+    if kind == DecompositionKind.QR:
+        fix = min(t_panel, SIDE_FIXED_S[kind])
+        return fix + (t_panel - fix) * base / R
+    # LU / Cholesky: one-CTA diagonal factor below ceil(b/32) SMs, the
+    # multi-CTA kernel (~2.2x faster, tools/prof/diag_probe.py) from there on
+    return t_panel if R < 4 else t_panel / 2.2
+
+
+def _qr_side_model(n, b, k):
+    """ctx.cu qr_panel_sms: the QR panel's split from flop counts at the
+    measured per-SM DMMA rate (panel: four tall GEMM passes + its fixed
+    latency; update: C -= V mid on the other SMs)."""
+    rate = 30.0e12 / 148.0
+    p = (k - 1) * b  # panel k is factored beside the update of k - 1
+    m1, cols = n - p - b, n - p - 2 * b
+    best, best_t = 16, None
+    for R in range(8, 49, 4):
+        tp = 8.0 * m1 * b * b / (R * rate) + 0.8e-3
+        tu = 2.0 * (n - p) * cols * b / ((148 - R) * rate) if cols > 0 else 0.0
+        t = max(tp, tu)
+        if best_t is None or t < 0.995 * best_t:
+            best, best_t = R, t
+    return best
+
+
+def _side_sms_choice(kind, t_panel, t_update, r, reclaim, n=0, b=0, k=0):
+    """SMs left to iteration k's panel work beside the look-ahead update: the
+    fixed split without slack reclamation; with it, the split at which the
+    predicted panel and update times meet (the side with slack gets fewer
+    SMs, the critical side more), reached by the reclamation ratio r
+    (scheduler.py:84-146 restated on SMs instead of clocks). QR uses the
+    library's flop model (its panel time is part latency, part SM-bound)."""
+    kind = DecompositionKind(_value(kind))
+    base, lo, hi = SIDE_BASE[kind]
+    if not reclaim or t_update <= 0.0 or t_panel <= 0.0:
+        return base
+    if kind == DecompositionKind.QR and n > 0 and k >= 1:
+        return int(round(base + r * (_qr_side_model(n, b, k) - base)))
+    best, best_t = base, None
+    for R in range(lo, hi + 1):
+        tp = _side_time(kind, t_panel, R, base)
+        tu = t_update * (148.0 - base) / (148.0 - R)
+        t = max(tp, tu)
+        if best_t is None or t < best_t * 0.995 or (abs(t - best_t) <= best_t * 0.005 and R < best):
+            best, best_t = R, t
+    return int(round(base + r * (best - base)))
+
+
+def run_mode_streamed(kind, a0: np.ndarray, b: int, mode: str = "bsr", r: float = 0.5,
+                      seed: int = 0, rates: ErrorRateTable | None = None,
+                      recovery: str = "recompute", fc_desired: float = 0.999999,
+                      forced_scheme=None, device: int | None = None,
+                      cpu: ClockDomain | None = None, gpu: ClockDomain | None = None):
+    """run_mode on the one-call look-ahead path (engine="stream", module doc).
+    Returns (RunSummary, [IterationRecord])."""
+    from .simulator import run_protected
+    if mode not in MODES:
+        raise ValueError(f"mode must be one of {MODES}")
+    if recovery not in RECOVERY_POLICIES:
+        raise ValueError(f"recovery must be one of {RECOVERY_POLICIES}")
+    kind = DecompositionKind(_value(kind))
+    flags = MODE_FLAGS[mode]
+    cpu = cpu or panel_domain()
+    gpu = gpu or update_domain()
+    table = rates or default_gpu_rate_table()
+    n = a0.shape[0]
+    f = Factorization(kind, a0, b, device=device, keep_input=True)
+    lib, ctx = f._lib, f._ctx
+    nb = f.layout.n_blocks
+    buf = (ctypes.c_double * (4 * nb))()
+    # calibration pass at the fixed split: per-iteration device times
+    base = SIDE_BASE[kind][0]
+    check(lib.abft_set_side_sms(ctx, (ctypes.c_int32 * nb)(*([base] * nb)), nb))
+    check(lib.abft_profile(ctx, 1))
+    run_protected(f, "full", {}, None)
+    check(lib.abft_profile_read_iters(ctx, buf, nb))
+    check(lib.abft_profile(ctx, 0))
+    cal = [[buf[4 * k + t] * 1e-3 for t in range(4)] for k in range(nb)]
+    check(lib.abft_reset(ctx))
+    f.k_done = 0
+    # decisions from the history predictor over the calibration times
+    coverage = CoverageParams.for_matrix(n, b, fc_desired)
+    _, fault_seed = np.random.SeedSequence(seed).spawn(2)   # simulator.py:212-215
+    rng_fault = np.random.default_rng(fault_seed)
+    hist = {t: _History(kind, t, n, b) for t in ("pd", "pu", "tmu")}
+    forced = ChecksumScheme(_value(forced_scheme)) if forced_scheme is not None else None
+    decisions, schemes, schedule, side, preds = [], [], {}, [], []
+    prev = None
+    for k in range(nb):
+        t_cpu = hist["pd"].predict(k) + hist["pu"].predict(k)
+        t_gpu = hist["tmu"].predict(k)
+        if mode == "original":
+            dec = ScheduleDecision(cpu.f_base_mhz, gpu.f_base_mhz, 1.0, 1.0, False, False, False, False)
+        elif mode == "r2h" or k == 0:
+            a_c = cpu.alpha_default if mode == "bsr" else 1.0
+            a_g = gpu.alpha_default if mode == "bsr" else 1.0
+            dec = ScheduleDecision(cpu.f_base_mhz, gpu.f_base_mhz, a_c, a_g, False, False, False, True)
+        elif mode == "sr":
+            dec = decide_sr(cpu, gpu, t_cpu, t_gpu, 0.0)
+        else:
+            ft_on = flags["col_ft"] and forced is None
+            dec = decide_bsr(cpu, gpu, t_cpu, t_gpu, 0.0, r, coverage if ft_on else None,
+                             table if ft_on else None, prev)
+        prev = dec
+        sch = forced if forced is not None else scheme_of(dec)
+        decisions.append(dec)
+        schemes.append(sch.value)
+        side.append(_side_sms_choice(kind, t_cpu, t_gpu, r if mode == "bsr" else 1.0,
+                                     flags["reclaim_slack"], n, b, k))
+        preds.append((t_cpu, t_gpu))
+        t_tmu = (t_gpu if t_gpu > 0 else 0.0) * gpu.f_base_mhz / dec.f_gpu_mhz
+        lam = table.rates(dec.f_gpu_mhz)
+        counts = {kk: int(rng_fault.poisson(l * t_tmu)) for kk, l in zip(ErrorKind, lam)}
+        if any(counts.values()):
+            schedule[k] = counts
+        pd_, pu_, tmu_, abft_ = cal[k]
+        hist["pd"].observe(k, pd_, 1.0, 1.0)
+        hist["pu"].observe(k, pu_, 1.0, 1.0)
+        hist["tmu"].observe(k, tmu_ + abft_, 1.0, 1.0)
+    # the run: per-iteration schemes, side-stream SM shares and fault plans
+    sarr = (ctypes.c_int32 * nb)(*side)
+    check(lib.abft_set_side_sms(ctx, sarr, nb))
+    energy = _Energy(f.device)
+    check(lib.abft_profile(ctx, 1))
+    e0 = energy.mj()
+    reps = run_protected(f, "none", schedule, rng_fault, schemes=schemes)
+    e1 = energy.mj()
+    check(lib.abft_profile_read_iters(ctx, buf, nb))
+    check(lib.abft_profile(ctx, 0))
+    check(lib.abft_set_side_sms(ctx, None, 0))
+    total_ms = ctypes.c_double(0.0)
+    check(lib.abft_last_elapsed_ms(ctx, ctypes.byref(total_ms)))
+    if recovery == "recompute" and any(rep.uncorrectable for rep in reps):
+        # exact reference semantics (snapshot + recompute) on the iteration engine
+        return run_mode(kind, a0, b, mode, r, seed, rates=rates, recovery=recovery,
+                        fc_desired=fc_desired, forced_scheme=forced_scheme, device=device,
+                        cpu=cpu, gpu=gpu)
+    records = []
+    injected = {kk.value: 0 for kk in ErrorKind}
+    detected = corrected = 0
+    abft_ms = 0.0
+    for k in range(nb):
+        dec, rep = decisions[k], reps[k]
+        t = [buf[4 * k + i] for i in range(4)]
+        rec = IterationRecord(k, dec.f_cpu_mhz, dec.f_gpu_mhz, schemes[k], dec.skipped,
+                              slack_pred_s=preds[k][1] - preds[k][0])
+        for kk, v in schedule.get(k, {}).items():
+            rec.faults[kk.value] += v
+            injected[kk.value] += v
+        rec.detected, rec.corrected = rep.total_detected, rep.total_corrected
+        detected += rep.total_detected
+        corrected += rep.total_corrected
+        rec.pred_time_s = {"pd": preds[k][0], "pu": 0.0, "tmu": preds[k][1], "transfer": 0.0}
+        rec.actual_time_s = {"pd": t[0] * 1e-3, "pu": t[1] * 1e-3, "tmu": (t[2] + t[3]) * 1e-3,
+                             "transfer": 0.0}
+        rec.t_panel_ms, rec.t_update_ms, rec.t_abft_ms = t[0] + t[1], t[2] + t[3], t[3]
+        rec.slack_actual_s = (rec.t_update_ms - rec.t_panel_ms) * 1e-3
+        rec.side_sms = side[k]
+        abft_ms += t[3]
+        records.append(rec)
+    res = residual(a0, f)
+    sch_count = {}
+    for sname in schemes:
+        sch_count[sname] = sch_count.get(sname, 0) + 1
+    unrec = any(rep.uncorrectable for rep in reps)
+    summary = RunSummary(mode, r, kind.value, n, b, float(total_ms.value), abft_ms,
+                         (e1 - e0) / 1e3 if e0 is not None and e1 is not None else None,
+                         res, res <= 1e-8 and not unrec, injected, detected, corrected, unrec, 0,
+                         sch_count)
     return summary, records
 
 

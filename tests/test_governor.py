@@ -102,6 +102,30 @@ def test_run_modes_on_b200(kind):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kind", ["lu", "qr", "cholesky"])
+def test_stream_engine_modes(kind):
+    """engine="stream": the modes run on the one-call look-ahead path; the
+    slack-reclaiming modes move the panel / update SM split away from the
+    fixed one (the physical lever), results stay correct and every injected
+    fault is accounted for."""
+    import paper_2301_03166_b200 as P
+    n, b = 2048, 256 if kind != "lu" else 128
+    a = P.generate_test_matrix(kind, n, 3)
+    out = {}
+    for mode in ("original", "sr", "bsr"):
+        s, recs = G.run_mode(kind, a, b, mode, r=1.0, seed=3, engine="stream")
+        assert s.correct and s.residual < 1e-12, (mode, s)
+        assert len(recs) == -(-n // b)
+        assert s.faults_detected >= sum(s.faults_injected.values())
+        out[mode] = (s, [rc.side_sms for rc in recs])
+    base = G.SIDE_BASE[P.DecompositionKind(kind)][0]
+    assert set(out["original"][1]) == {base}
+    if kind == "qr":
+        assert any(x != base for x in out["sr"][1])
+    assert out["original"][0].schemes == {"none": -(-n // b)}
+
+
+@pytest.mark.gpu
 def test_forced_full_scheme_overhead_is_measured():
     import paper_2301_03166_b200 as P
     a = P.generate_test_matrix("lu", 1024, 0)

@@ -21,11 +21,14 @@ ap.add_argument("--rate-scale", type=float, default=2e3,
                 help="fault-rate scale of the forced-scheme campaign runs")
 ap.add_argument("--sweep", action="store_true")
 ap.add_argument("--precision", default="f64", choices=["f64", "f32"])
+ap.add_argument("--engine", default="iteration", choices=["iteration", "stream"],
+                help="stream: the modes on the look-ahead path with the SM-split lever")
 ap.add_argument("--repeat", type=int, default=10,
                 help="factorizations per configuration (NVML energy counter resolution)")
 args = ap.parse_args()
 a = P.generate_test_matrix(args.kind, args.n, args.seed)
-G.run_mode(args.kind, a, args.b, "original", seed=args.seed, precision=args.precision)  # warm-up
+G.run_mode(args.kind, a, args.b, "original", seed=args.seed, precision=args.precision,
+           engine=args.engine)  # warm-up
 # (mode, r, forced scheme, rate scale): the reference's rates for the mode
 # comparison and the r sweep; forced-scheme campaign runs with scaled rates
 runs = [(m, 0.5, None, 1.0) for m in G.MODES]
@@ -41,7 +44,7 @@ for mode, r, forced, scale in runs:
         s, recs = G.run_mode(args.kind, a, args.b, mode, r=r, seed=args.seed,
                              rates=G.scaled_rate_table(scale), forced_scheme=forced,
                              recovery="continue" if forced == "none" else "recompute",
-                             precision=args.precision)
+                             precision=args.precision, engine=args.engine)
     e1 = nv.mj()
     d = dataclasses.asdict(s)
     d["energy_j"] = (e1 - e0) / 1e3 / args.repeat if e0 is not None and e1 is not None else None
@@ -51,4 +54,6 @@ for mode, r, forced, scale in runs:
     d["precision"] = args.precision
     d["f_gpu_mhz"] = [rc.f_gpu_mhz for rc in recs]
     d["abft_modes"] = "".join(rc.abft_mode[0] for rc in recs)
+    d["engine"] = args.engine
+    d["side_sms"] = [rc.side_sms for rc in recs]
     print(json.dumps(d), flush=True)
