@@ -179,16 +179,16 @@ void prof_mark(abft_ctx* c, int cat, bool begin) {
   }
 }
 
-// PD bracket on the side stream (the look-ahead's panel k+1, credited to
-// iteration k+1)
-void prof_mark_side(abft_ctx* c, bool begin, int32_t iter) {
+// Bracket on the side stream (the look-ahead's panel k+1, or Cholesky's
+// early update of panel k+1, credited to iteration k+1)
+void prof_mark_side(abft_ctx* c, bool begin, int32_t iter, int cat = PROF_PD) {
   if (!c->prof_on) return;
   cudaEvent_t e = prof_event(c);
   cudaEventRecord(e, c->st2);
   if (begin) {
     c->prof_open2 = e;
   } else {
-    c->prof_pending.push_back({PROF_PD, iter, c->prof_open2, e});
+    c->prof_pending.push_back({cat, iter, c->prof_open2, e});
     c->prof_open2 = nullptr;
   }
 }
@@ -748,8 +748,10 @@ int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next, bool ev_recorded = f
   int keep = c->chol_cluster ? (int)((c->b + 31) / 32) : 1;
   if ((int64_t)c->side_sms.size() > k && c->side_sms[k] > 0)
     keep = std::max(1, std::min((int)c->side_sms[k], sms / 2));
+  prof_mark_side(c, true, (int32_t)(k + 1), PROF_TMU);
   ABFT_TRY(gemm_capped(c->st2, 'N', 'T', (int)(n - p1), (int)w1, (int)pk, -1.0, c->m + p1, c->ld,
                        c->m + p1, c->ld, 1.0, P1, c->ld, P1, c->ld, &c->gws2, sms - keep));
+  prof_mark_side(c, false, (int32_t)(k + 1), PROF_TMU);
   CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
   c->chol_part = k + 1;
   return 0;

@@ -1,27 +1,34 @@
-// Diagonal-block factorization on a thread-block cluster (K5 PD, fast path).
+// Multi-CTA diagonal-block factorization (K5 PD, fast path).
 //
 // Same contract as diag_factor (panel.cuh): the w x w block D is factored in
 // place -- LU unpivoted (linalg.py:230-238, mode 0), Cholesky (linalg.py:
 // 219-229, mode 1) or the sign-shifted LU of the Householder reconstruction
 // (mode 2, qr_panel.cu) -- and the triangular inverses L^{-1} (and U^{-1})
 // come out of the same launch. diag_factor runs all of it on one CTA (a
-// 32-column sub-panel loop, ~0.35 ms + 0.14 ms for the inverses at w = 256);
-// here CTA r of a cluster of nb = ceil(w/32) CTAs owns block column r in its
-// shared memory and the blocked right-looking algorithm runs across the
-// cluster over distributed shared memory:
+// 32-column sub-panel loop: ~0.47 ms at w = 256 with its inverses); here CTA
+// r of nb = ceil(w/32) co-resident CTAs (cooperative launch) owns block
+// column r in its shared memory and the blocked right-looking algorithm runs
+// across them:
 //
-//   step j:  CTA j factors block column j (rows >= 32j, one row per thread,
-//            register resident, one barrier per pivot) and inverts its
-//            diagonal block (L_jj^{-1}, and U_jj^{-1} for LU);
-//            cluster barrier;
-//            CTA r > j updates its block column from CTA j's panel, read in
-//            place through DSMEM (LU: U_jr = L_jj^{-1} A_jr, then
-//            A_ir -= L_ij U_jr; Cholesky: A_ir -= L_ij L_rj^T);
-//            CTA r <= j advances block column r of X = L^{-1} by the same
-//            elimination applied to the identity (X_jr = L_jj^{-1} X_jr,
-//            X_ir -= L_ij X_jr), so the inverse costs no extra phase.
-//   LU then forms U^{-1} by block back substitution over the final U columns
-//   (no barriers: the factor is read-only by then).
+//   step j:  CTA j factors its 32 x 32 diagonal block with one warp (rows in
+//            registers, pivot row through shared memory, warp-level syncs),
+//            inverts it (right-looking substitution), solves the rows below
+//            against the inverse and publishes the block column and the
+//            inverse blocks through global memory (L2);
+//            grid barrier (an L2 counter);
+//            CTA r > j pulls the panel from L2 and updates its block column
+//            (LU: U_jr = L_jj^{-1} A_jr, A_ir -= L_ij U_jr; Cholesky:
+//            A_ir -= L_ij L_rj^T); CTA r <= j advances block column r of
+//            X = L^{-1} by the same elimination applied to the identity, so
+//            the inverse costs no extra phase.
+//   LU then forms U^{-1} by block back substitution over the final U columns.
+//
+// Round-2 history: the first version was a thread-block cluster pulling the
+// panel over DSMEM (seven readers on one CTA's shared-memory port, ~21 B/cycle)
+// with a register-resident 256-row pivot loop (~1000 cycles per pivot); the
+// warp-level diagonal block, the L2 exchange and the cooperative launch (no
+// GPC co-location, so it also runs beside a persistent GEMM that leaves a few
+// SMs free) took w = 256 LU from 590 to 214 us (tools/probe/cf_trace.cu).
 //
 // w is padded to 32 nb with the identity (a block-diagonal extension that
 // changes no pivot of the real block). Breakdown follows the reference: LU
@@ -55,7 +62,7 @@ __device__ long long g_cf_clk[4];
 #endif
 
 constexpr int CF_T = 256;    // threads per CTA (8 warps)
-constexpr int CF_MAXB = 8;   // cluster size limit (portable): w <= 256
+constexpr int CF_MAXB = 8;   // CTAs (block columns) per launch: w <= 256
 constexpr int TS = 33;       // stride of the 32 x 32 tiles
 
 // Grid barrier of the nb co-resident CTAs (cooperative launch): sync[0]
@@ -310,7 +317,7 @@ ABFT_DEVINL void tile_mul_inplace(T* Out, int ldo, int r0, int r1, const T* B, i
 
 template <typename T>
 __global__ void __launch_bounds__(CF_T, 1)
-    cluster_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl, T* Uinv,
+    coop_factor_kernel(T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl, T* Uinv,
                           int64_t ldu, int* info, int64_t col_base, T* sgn, int* sync) {
   extern __shared__ __align__(16) unsigned char cf_raw[];
   const int nb = (int)gridDim.x;
@@ -371,7 +378,7 @@ __global__ void __launch_bounds__(CF_T, 1)
         }
         // publish the final block column (rows >= 32j) and the diagonal
         // block's inverses through global memory (L2): the other CTAs read
-        // them from there after the cluster barrier (a DSMEM pull would put
+        // them from there after the grid barrier (a DSMEM pull would put
         // seven readers on this CTA's shared-memory port)
         for (int c = ty; c < 32; c += CF_T / 32)
           for (int i = c0 + (tid & 31); i < Wp; i += 32)
@@ -489,14 +496,14 @@ int* next_sync_slot() {
 }
 
 template <typename T>
-int cluster_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
+int coop_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv, int64_t ldl,
                      T* Uinv, int64_t ldu, int* info_dev, int64_t col_base, T* sgn) {
   const int nb = (w + 31) / 32;
   const size_t smem = cf_smem_bytes<T>(nb);
-  ABFT_TRY(ensure_smem_attr((const void*)cluster_factor_kernel<T>, (int)smem));
+  ABFT_TRY(ensure_smem_attr((const void*)coop_factor_kernel<T>, (int)smem));
   int* sync = next_sync_slot();
   if (!sync) {
-    set_last_error("cluster_factor: barrier slots unavailable");
+    set_last_error("coop_factor: barrier slots unavailable");
     return -1;
   }
   CUDA_TRY(cudaMemsetAsync(sync, 0, 2 * sizeof(int), st));
@@ -505,7 +512,7 @@ int cluster_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* Linv
   // beside a persistent GEMM that leaves a few SMs free)
   void* args[] = {&D, &ld, &w, &mode, &Linv, &ldl, &Uinv, &ldu, &info_dev, &col_base, &sgn, &sync};
   count_launch();
-  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)cluster_factor_kernel<T>, dim3(nb), dim3(CF_T),
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)coop_factor_kernel<T>, dim3(nb), dim3(CF_T),
                                        args, smem, st));
   return 0;
 }
@@ -524,10 +531,10 @@ int diag_factor_fast(cudaStream_t st, double* D, int64_t ld, int w, int mode, do
                      int64_t ldl, double* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
                      double* sgn) {
   if (w <= 0) return 0;
-  // the cluster kernel exchanges panels / inverse blocks through D, Linv, Uinv
+  // the multi-CTA kernel exchanges panels / inverse blocks through D, Linv, Uinv
   if (w > 32 * CF_MAXB || cluster_disabled() || !Linv || (mode != 1 && !Uinv))
     return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
-  return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+  return coop_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
 
 int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, float* Linv,
@@ -536,7 +543,7 @@ int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, flo
   if (w <= 0) return 0;
   if (w > 32 * CF_MAXB || cluster_disabled() || !Linv || (mode != 1 && !Uinv))
     return diag_factor(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
-  return cluster_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
+  return coop_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);
 }
 
 }  // namespace abft
