@@ -87,6 +87,8 @@ struct abft_sctx {
   double* v64 = nullptr;     // n x b (ld)
   double* t64 = nullptr;     // b x b (ld_t)
   double* gram = nullptr;    // b x b
+  int qr_la_sms = 16;           // QR look-ahead: SMs left to the side-stream panel
+                                // (ABFT_QR_LA_SMS; 0 disables the QR look-ahead)
   bool lu_coop = true;          // LU look-ahead diagonal factor on the multi-CTA kernel
                                 // beside the update capped at sms - b/32 (ABFT_LU_COOP=0: off)
   bool chol_cluster = true;     // Cholesky PD on the cluster kernel (ABFT_CHOL_CLUSTER=0: off);
@@ -122,6 +124,7 @@ struct abft_sctx {
   int64_t ldk = 0;
   double* scratch = nullptr;
   GemmWorkspace gws;
+  GemmWorkspace gws2;           // fp64 split-K workspace of the side-stream QR panel
   Event* ev = nullptr;
   int32_t* counters = nullptr;
   int ev_cap = 0;
@@ -413,6 +416,24 @@ int s_lu_l21(abft_sctx* c, int64_t k) {
   return 0;
 }
 
+// Mixed-precision Householder panel k on stream st: widen, factor in fp64
+// (qr_panel_factor: tensor-core path + exact fallback; GEMMs capped at
+// max_ctas), narrow back into the fp32 matrix / V / T stores.
+int s_qr_panel(abft_sctx* c, cudaStream_t st, int64_t k, int max_ctas, GemmWorkspace* gws) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  float* D = c->m + p + p * c->ld;
+  const int64_t nk = n - p;
+  ABFT_TRY(widen_matrix(st, D, c->ld, c->pan64, c->ld, nk, w));
+  ABFT_TRY(fill_matrix(st, c->v64, c->ld, nk, w, 0.0));
+  QrPanelWork q = c->qrw;
+  q.gws = gws;
+  ABFT_TRY(qr_panel_factor(st, c->pan64, c->ld, nk, (int)w, c->v64, c->ld, c->t64, c->ld_t,
+                           c->betas, q, max_ctas));
+  ABFT_TRY(narrow_matrix(st, c->pan64, c->ld, D, c->ld, nk, w));
+  ABFT_TRY(narrow_matrix(st, c->v64, c->ld, c->vstore + p + p * c->ld, c->ld, nk, w));
+  return narrow_matrix(st, c->t64, c->ld_t, c->tstore + k * c->b * c->ld_t, c->ld_t, w, w);
+}
+
 int s_pd(abft_sctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   float* D = c->m + p + p * c->ld;
@@ -425,15 +446,7 @@ int s_pd(abft_sctx* c, int64_t k) {
     else
       ABFT_TRY(diag_factor(c->st, D, c->ld, (int)w, 1, c->linv, c->ld_t, nullptr, 0, c->info, p));
   } else {
-    // mixed-precision Householder panel: widen, factor in fp64, narrow back
-    const int64_t nk = n - p;
-    ABFT_TRY(widen_matrix(c->st, D, c->ld, c->pan64, c->ld, nk, w));
-    ABFT_TRY(fill_matrix(c->st, c->v64, c->ld, nk, w, 0.0));
-    ABFT_TRY(qr_panel_factor(c->st, c->pan64, c->ld, nk, (int)w, c->v64, c->ld, c->t64, c->ld_t,
-                             c->betas, c->qrw));
-    ABFT_TRY(narrow_matrix(c->st, c->pan64, c->ld, D, c->ld, nk, w));
-    ABFT_TRY(narrow_matrix(c->st, c->v64, c->ld, c->vstore + p + p * c->ld, c->ld, nk, w));
-    ABFT_TRY(narrow_matrix(c->st, c->t64, c->ld_t, c->tstore + k * c->b * c->ld_t, c->ld_t, w, w));
+    ABFT_TRY(s_qr_panel(c, c->st, k, 0, &c->gws));
     c->qr_count = (int)(k + 1);
   }
   return 0;
@@ -797,6 +810,82 @@ int s_verify_sub(abft_sctx* c, int64_t k, int scheme, int correct, int64_t r0, i
 // path, as ctx.cu): the next panel's block column is updated and verified
 // first, its diagonal block is factored on a side stream while the rest of
 // the trailing matrix updates on the remaining SMs.
+// fp32 QR look-ahead (fault-free iterations of the one-call path), ctx.cu's
+// protected_tmu_qr_lookahead restated: W = V^T C, mid = T^T W and the
+// maintained sums over the whole region; the next panel's block column
+// first (plain GEMM + checksum pass + verify); panel k+1 (widen, tensor-core
+// fp64 panel on qr_la_sms SMs, narrow) on the side stream; the rest of the
+// region with fused sums on the other SMs.
+int s_tmu_qr_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  s_region(c, k, &r0, &c0, &rows, &cols);
+  RegionF reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
+  const bool prot = scheme != ABFT_NONE;
+  const float* V = c->vstore + p + p * c->ld;
+  const float* T = c->tstore + k * c->b * c->ld_t;
+  float* C = c->m + p + pe * c->ld;
+  if (prot && !c->sums_valid) {
+    smark(c, SP_ABFT, true);
+    ABFT_TRY(blocksum(c->st, reg, s_sums(c, r0, c0, true)));
+    smark(c, SP_ABFT, false);
+  }
+  smark(c, SP_TMU, true);
+  ABFT_TRY(s_gemm(c, 'T', 'N', w, cols, rows, 1.0f, V, c->ld, C, c->ld, 0.0f, nullptr, 0, c->ww,
+                  c->ld_t));
+  ABFT_TRY(s_gemm(c, 'T', 'N', w, cols, w, 1.0f, T, c->ld_t, c->ww, c->ld_t, 0.0f, nullptr, 0, c->mid,
+                  c->ld_t));
+  smark(c, SP_TMU, false);
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    ABFT_TRY(s_maintain(c, k, scheme, r0, c0, rows, cols));
+    smark(c, SP_ABFT, false);
+  }
+  const int64_t wa = std::min<int64_t>(c->b, cols);
+  smark(c, SP_TMU, true);
+  ABFT_TRY(s_gemm(c, 'N', 'N', rows, wa, w, -1.0f, V, c->ld, c->mid, c->ld_t, 1.0f, C, c->ld, C,
+                  c->ld));
+  smark(c, SP_TMU, false);
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    RegionF ra{C, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, c0, true)));
+    ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 0, 1));
+    smark(c, SP_ABFT, false);
+  }
+  const int res = std::max(8, std::min(c->qr_la_sms, c->sms / 2));
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  ABFT_TRY(s_qr_panel(c, c->st2, k + 1, res, &c->gws2));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  if (cols > wa) {
+    const float* midb = c->mid + wa * c->ld_t;
+    float* Cb = C + wa * c->ld;
+    const bool fuse = prot && c->fuse_enabled && c->b == 128;
+    FusedSums fs;
+    if (fuse) fs = s_fused(c, r0, c0 + wa);
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, cols - wa, w, -1.0f, V, c->ld, midb, c->ld_t, 1.0f, Cb, c->ld,
+                    Cb, c->ld, fuse ? &fs : nullptr, c->sms - res));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      if (!fuse) {
+        RegionF rb{Cb, c->ld, rows, cols - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, s_sums(c, r0, c0 + wa, true)));
+      }
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 1, (cols + c->b - 1) / c->b));
+      smark(c, SP_ABFT, false);
+    }
+  }
+  c->sums_valid = prot;
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  c->qr_count = (int)(k + 2);
+  ABFT_TRY(s_emit_column(c, k + 1));
+  c->pd_ready = k + 1;
+  return 0;
+}
+
 int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   int64_t r0, c0, rows, cols;
@@ -901,7 +990,13 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     ABFT_TRY(pu());
   } else if (c->kind == ABFT_QR) {
     ABFT_TRY(pd());
-    ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
+    const int64_t pe = std::min((k + 1) * c->b, c->n);
+    const bool la = lookahead && c->lookahead_enabled && nplan == 0 && pe < c->n &&
+                    k < c->qr_count && c->qr_la_sms > 0;
+    if (la)
+      ABFT_TRY(s_tmu_qr_lookahead(c, k, scheme, correct));
+    else
+      ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
   } else {
     ABFT_TRY(pd());
     ABFT_TRY(pu());
@@ -1010,6 +1105,8 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     if (e4 && e4[0] == '0') c->chol_cluster = false;
     const char* e5 = getenv("ABFT_LU_COOP");
     if (e5) c->lu_coop = e5[0] == '1';
+    const char* e6 = getenv("ABFT_QR_LA_SMS");
+    if (e6) c->qr_la_sms = atoi(e6);
   }
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) {
     set_last_error("cudaStreamCreate failed");
@@ -1058,6 +1155,10 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   if ((rc = salloc(&c->scratch, 4096, c->st))) return fail(rc);
   c->gws.elems = std::min<int64_t>(std::max<int64_t>(8 * ld * b, 1 << 20), int64_t(64) << 20);
   if ((rc = salloc(&c->gws.ptr, c->gws.elems, c->st))) return fail(rc);
+  if (kind == ABFT_QR) {
+    c->gws2.elems = c->gws.elems;
+    if ((rc = salloc(&c->gws2.ptr, c->gws2.elems, c->st))) return fail(rc);
+  }
   // split-operand workspace sized once for the deepest s_gemm of the kind
   // (regrowing inside the per-iteration path costs allocator round trips)
   cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
@@ -1131,7 +1232,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
                   c->betas, c->qr_part, c->qr_rowbuf, c->qr_part2, c->qr_wfin,
                   c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
-                  c->uinv, c->sws, c->lsh, c->lsl, c->scratch, c->gws.ptr, c->ev, c->counters, c->dirty,
+                  c->uinv, c->sws, c->lsh, c->lsl, c->scratch, c->gws.ptr, c->gws2.ptr, c->ev, c->counters, c->dirty,
                   c->dplan, c->dlist, c->info};
   for (void* p : bufs)
     if (p) cudaFree(p);
