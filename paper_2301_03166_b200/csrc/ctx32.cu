@@ -87,8 +87,11 @@ struct abft_sctx {
   double* v64 = nullptr;     // n x b (ld)
   double* t64 = nullptr;     // b x b (ld_t)
   double* gram = nullptr;    // b x b
-  int qr_la_sms = 16;           // QR look-ahead: SMs left to the side-stream panel
-                                // (ABFT_QR_LA_SMS; 0 disables the QR look-ahead)
+  int qr_la_sms = 0;            // QR look-ahead: SMs left to the side-stream panel
+                                // (ABFT_QR_LA_SMS=R enables it). Off: the fp32 update is
+                                // short, the fp64 panel is the critical path, and taking
+                                // SMs from it measured slower (sgeqrf 41.0 -> 35.0 / 37.9
+                                // TF/s at R = 16 / 24)
   bool lu_coop = true;          // LU look-ahead diagonal factor on the multi-CTA kernel
                                 // beside the update capped at sms - b/32 (ABFT_LU_COOP=0: off)
   bool chol_cluster = true;     // Cholesky PD on the cluster kernel (ABFT_CHOL_CLUSTER=0: off);
