@@ -155,6 +155,24 @@ def test_fp32_per_iteration_equals_one_call(kind):
         np.testing.assert_array_equal(f1.m, f2.m)
 
 
+def test_fp32_qr_lookahead_equals_per_iteration(monkeypatch):
+    """The fp32 QR look-ahead (off by default, ABFT_QR_LA_SMS=R): panel k+1
+    factored on a side stream gives the per-iteration path's reports."""
+    n, b, seed = 768, 128, 5
+    a = P.generate_test_matrix("qr", n, seed)
+    sched = {1: {"0d": 1}, 3: {"1d": 1}}
+    monkeypatch.setenv("ABFT_QR_LA_SMS", "16")
+    f1 = P.SFactorization("qr", a, b)
+    r1 = f1.run_protected("full", sched, np.random.default_rng(seed))
+    monkeypatch.delenv("ABFT_QR_LA_SMS")
+    f2 = P.SFactorization("qr", a, b)
+    rng = np.random.default_rng(seed)
+    r2 = [f2.run_numeric_iteration(k, "full", sched.get(k), rng) for k in range(f2.layout.n_blocks)]
+    assert [r.locations for r in r1] == [r.locations for r in r2]
+    scale = float(np.abs(f2.m).max())
+    np.testing.assert_allclose(f1.m, f2.m, rtol=0, atol=1e-5 * scale)
+
+
 def test_fp32_clean_run_reports_nothing_and_breakdown_raises():
     a = P.generate_test_matrix("lu", 512, 1)
     f = P.SFactorization("lu", a, 128)
