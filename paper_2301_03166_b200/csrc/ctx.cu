@@ -879,7 +879,10 @@ int qr_panel_sms(const abft_ctx* c, int64_t k, int sms) {
     return std::max(1, std::min((int)c->side_sms[k + 1], sms / 2));
   if (c->qr_la_sms_fixed) return std::max(1, std::min(c->qr_la_sms, sms / 2));
   const double rate = 30.0e12 / 148.0;  // fused trailing-update rate per SM (bench_lu32k_r02)
-  const double lat = 0.8e-3;            // three multi-CTA diagonal factors + small GEMMs
+  static const double lat = [] {        // three multi-CTA diagonal factors + small GEMMs
+    const char* e = getenv("ABFT_QR_LA_LAT_US");  // A/B knob
+    return (e ? atof(e) : 800.0) * 1e-6;
+  }();
   const double n = (double)c->n, b = (double)c->b, p = (double)(k * c->b);
   const double m1 = n - p - b;          // rows of panel k+1
   const double cols = n - p - 2 * b;    // columns left to part (b) of the update
