@@ -365,18 +365,20 @@ __global__ void __launch_bounds__(T_THREADS, 1)
 #pragma unroll
             for (int j = 0; j < 16; ++j) tr[lane * T_TP + j] = v[hh * 16 + j];
             __syncwarp();
-            if (lane < 16) {
-              float a0 = 0.0f, a1 = 0.0f;
+            {
+              // all 32 lanes: lane l < 16 forms column l's plain sum, lane
+              // l + 16 its index-weighted sum (one FADD / FFMA per element)
+              const int cl = lane & 15;
+              const bool wtd = lane >= 16;
+              float a = 0.0f;
 #pragma unroll 8
               for (int r = 0; r < 32; ++r) {
-                const float x = tr[r * T_TP + lane];
-                a0 += x;
-                a1 = fmaf((float)(quarter * 32 + r), x, a1);
+                const float x = tr[r * T_TP + cl];
+                a = fmaf(wtd ? (float)(quarter * 32 + r) : 1.0f, x, a);
               }
-              const int col = half * HN + cc * 32 + hh * 16 + lane;
+              const int col = half * HN + cc * 32 + hh * 16 + cl;
               float* cq = parts + acc * T_PART_FLOATS + quarter * TBN * 2;
-              cq[col * 2 + 0] = a0;
-              cq[col * 2 + 1] = a1;
+              cq[col * 2 + (wtd ? 1 : 0)] = a;
             }
             __syncwarp();
           }
