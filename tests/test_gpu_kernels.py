@@ -208,3 +208,19 @@ def test_diag_factor_breakdown_column(variant, mode, col):
     assert rc == 0
     torch.cuda.synchronize()
     assert int(info.item()) == col + 1
+
+
+def test_full_zero_bad_rows_two_bad_columns_raises_index_error():
+    """Quirk Q5: FULL verification of a block whose row sums
+    agree but two column sums disagree -- +d and -d in one row -- classifies
+    it as 1-D and reads bad_rows[0] of an empty array (abft.py:267): the
+    reference raises IndexError (checked against the reference itself in
+    tests/test_oracle_golden.py), so does the drop-in."""
+    n, b = 64, 16
+    m = _rm(n, 21)
+    cs = P.encode(m, b, P.ChecksumScheme.FULL)
+    d = 0.5
+    m[5, 2] += d
+    m[5, 9] -= d
+    with pytest.raises(IndexError):
+        P.verify_correct(m, cs)

@@ -142,3 +142,16 @@ def test_small_factorizations():
         key = f"{case['kind']}_{case['n']}_{case['b']}"
         if key in arrays and case["seed"] == 1:
             assert np.allclose(f.m, arrays[key], rtol=1e-12, atol=1e-12)
+
+
+def test_oracle_q5_full_two_bad_columns_no_bad_row_raises():
+    """Quirk Q5: FULL verification with row sums intact and two bad column
+    sums raises IndexError in the reference (abft.py:267; reproduced by
+    running slackwise.abft on this input when the reference is importable)."""
+    n, b = 64, 16
+    m = np.random.default_rng(21).uniform(-1.0, 1.0, (n, n))
+    cs = O.encode(m, b, "full")
+    m[5, 2] += 0.5
+    m[5, 9] -= 0.5
+    with pytest.raises(IndexError):
+        O.verify(m, cs)
