@@ -121,6 +121,15 @@ CASES = [
      "schedule": {}, "world": 3, "root": 1},
     {"name": "lu_w2_root", "kind": "lu", "n": 640, "b": 128, "scheme": "full", "seed": 18,
      "schedule": {"1": {"0d": 1}}, "world": 2, "root": 0},
+    # four ranks: every rank owns a block or two, look-ahead owners rotate fast
+    {"name": "lu_w4", "kind": "lu", "n": 1024, "b": 128, "scheme": "full", "seed": 19,
+     "schedule": {"2": {"0d": 1}, "5": {"1d": 1}}, "world": 4, "root": 3},
+    {"name": "qr_w4", "kind": "qr", "n": 1024, "b": 128, "scheme": "full", "seed": 20,
+     "schedule": {"3": {"0d": 1}}, "world": 4},
+    {"name": "chol_w4", "kind": "cholesky", "n": 1024, "b": 128, "scheme": "full", "seed": 21,
+     "schedule": {"1": {"0d": 1}, "4": {"2d": 1}}, "world": 4, "root": 0},
+    {"name": "chol_w4_single", "kind": "cholesky", "n": 900, "b": 128, "scheme": "single",
+     "seed": 22, "schedule": {"6": {"0d": 1}}, "world": 4},
     # clean runs, no checksums
     {"name": "lu_none", "kind": "lu", "n": 512, "b": 128, "scheme": "none", "seed": 9,
      "schedule": {}, "world": 2},
@@ -140,7 +149,7 @@ def _oracle(case):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 4])
 def test_distributed_matches_oracle(tmp_path, world):
     from dist_worker import gpu_cases
     import paper_2301_03166_b200 as P
