@@ -192,6 +192,12 @@ ABFT_API int abft_get_qr_panel(abft_ctx* ctx, int64_t k, double* V, int64_t ldv,
  * ms[0]=PD, ms[1]=PU, ms[2]=TMU GEMMs, ms[3]=ABFT encode/maintain/verify/inject */
 ABFT_API int abft_profile(abft_ctx* ctx, int enable);
 ABFT_API int abft_profile_read(abft_ctx* ctx, double* ms);
+/* LU with partial pivoting (LAPACK dgetrf semantics, P A = L U), an option:
+ * the reference factors LU unpivoted (linalg.py:230-238); set before
+ * iteration 0. abft_get_pivots: n global 0-based rows (row i interchanged
+ * with piv[i], in order; LAPACK ipiv - 1), identity when off. */
+ABFT_API int abft_set_pivoting(abft_ctx* ctx, int enable);
+ABFT_API int abft_get_pivots(abft_ctx* ctx, int32_t* piv);
 /* per-iteration device times since abft_profile(ctx, 1): out[4k + t], t = PD
  * (a look-ahead's side-stream panel included), PU, TMU GEMMs, ABFT work */
 ABFT_API int abft_profile_read_iters(abft_ctx* ctx, double* out, int64_t nb);

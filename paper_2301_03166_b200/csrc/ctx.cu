@@ -120,6 +120,10 @@ struct abft_ctx {
   GemmWorkspace gws2;             // split-K workspace of the side stream
   int qr_la_sms = 16;             // QR look-ahead: SMs left to the side-stream panel
   bool qr_la_sms_fixed = false;   // ABFT_QR_LA_SMS=R fixes it; else qr_panel_sms's model
+  bool pivot = false;             // LU with partial pivoting (abft_set_pivoting)
+  int32_t* ipiv = nullptr;        // n: panel-local pivot rows of each panel
+  double* piv_part = nullptr;     // lu_panel_pivot partials
+  int64_t piv_part_elems = 0;
   bool lu_coop = true;            // late LU look-ahead iterations: multi-CTA diagonal factor
                                   // (ABFT_LU_COOP=0: always the one-CTA kernel)
   bool chol_cluster = false;      // Cholesky PD on the cluster kernel, submitted ahead of
@@ -359,7 +363,17 @@ int lu_l21(abft_ctx* c, int64_t k) {
 int task_pd(abft_ctx* c, int64_t k) {
   const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
   double* D = c->m + p + p * c->ld;
-  if (c->kind == ABFT_LU) {
+  if (c->kind == ABFT_LU && c->pivot) {
+    // partial pivoting (LAPACK dgetf2 on the tall panel), the interchanges on
+    // every other column (dlaswp), L11^{-1} for PU; the region's rows moved:
+    // its checksums are re-encoded by the protected update
+    ABFT_TRY(lu_panel_pivot(c->st, D, c->ld, n - p, (int)w, c->ipiv + p, c->piv_part,
+                            c->piv_part_elems, c->info, p));
+    ABFT_TRY(laswp(c->st, c->m, c->ld, 0, p, p, (int)w, c->ipiv + p));
+    ABFT_TRY(laswp(c->st, c->m, c->ld, pe, n - pe, p, (int)w, c->ipiv + p));
+    ABFT_TRY(tri_inverse_lower(c->st, D, c->ld, (int)w, true, c->linv, c->ld_t, c->info));
+    c->sums_valid = false;
+  } else if (c->kind == ABFT_LU) {
     ABFT_TRY(lu_diag(c, c->st, k));
     ABFT_TRY(lu_l21(c, k));
   } else if (c->kind == ABFT_CHOLESKY) {
@@ -1045,7 +1059,7 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
     ABFT_TRY(pu());
     const int64_t pe = std::min((k + 1) * c->b, c->n);
     const bool la = lookahead && nplan == 0 && pe < c->n && c->fuse_enabled &&
-                    gemm_can_fuse((int)c->b);
+                    gemm_can_fuse((int)c->b) && !c->pivot;
     if (la)
       ABFT_TRY(protected_tmu_lu_lookahead(c, k, scheme, correct));
     else
@@ -1278,6 +1292,8 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   if (c->dplan) cudaFree(c->dplan);
   if (c->dlist) cudaFree(c->dlist);
   if (c->info) cudaFree(c->info);
+  if (c->ipiv) cudaFree(c->ipiv);
+  if (c->piv_part) cudaFree(c->piv_part);
   for (auto& s : c->snaps) {
     if (s.m) cudaFree(s.m);
     if (s.chol_rs) cudaFree(s.chol_rs);
@@ -1545,6 +1561,47 @@ ABFT_API int abft_profile(abft_ctx* c, int enable) {
   return 0;
 }
 
+// LU with partial pivoting (LAPACK dgetrf semantics; the reference factors
+// unpivoted, linalg.py:230-238). Set before iteration 0.
+ABFT_API int abft_set_pivoting(abft_ctx* c, int enable) {
+  DevGuard g(c->device);
+  if (c->kind != ABFT_LU && enable) {
+    set_last_error("partial pivoting is an LU option");
+    return ABFT_E_INVALID;
+  }
+  if (c->k_done != 0) {
+    set_last_error("abft_set_pivoting before the first iteration");
+    return ABFT_E_INVALID;
+  }
+  c->pivot = enable != 0;
+  if (c->pivot && !c->ipiv) {
+    CUDA_TRY(cudaMalloc(&c->ipiv, c->n * sizeof(int32_t)));
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    c->piv_part_elems = 2LL * (sms + 1) * (c->b + 2);
+    ABFT_TRY(dalloc(&c->piv_part, c->piv_part_elems));
+  }
+  c->sums_valid = false;
+  return 0;
+}
+
+// The pivots (global 0-based: row i was interchanged with row piv[i], in
+// order; LAPACK ipiv - 1). Valid for the completed panels.
+ABFT_API int abft_get_pivots(abft_ctx* c, int32_t* piv) {
+  DevGuard g(c->device);
+  if (!c->pivot) {
+    for (int64_t i = 0; i < c->n; ++i) piv[i] = (int32_t)i;
+    return 0;
+  }
+  CUDA_TRY(cudaMemcpyAsync(piv, c->ipiv, c->n * sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+  CUDA_TRY(cudaStreamSynchronize(c->st));
+  for (int64_t k = 0; k < c->nb; ++k) {
+    const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
+    for (int64_t j = 0; j < w; ++j) piv[p + j] = (int32_t)(p + piv[p + j]);
+  }
+  return 0;
+}
+
 // Per-iteration device times since abft_profile(ctx, 1): out[4k + t] for
 // t = PD (incl. a look-ahead's side-stream panel), PU, TMU, ABFT.
 ABFT_API int abft_profile_read_iters(abft_ctx* c, double* out, int64_t nb) {
@@ -1706,6 +1763,11 @@ static int reconstruct_device(abft_ctx* c, double* out, double* tmp) {
     if (!rc)
       rc = gemm(c->st, 'N', 'N', (int)n, (int)n, (int)n, 1.0, tmp, ld, U, ld, 0.0, nullptr, 0, out,
                 ld, &c->gws);
+    // pivoted: A = P^T L U -- undo the interchanges, last panel first
+    for (int64_t k = c->nb - 1; c->pivot && !rc && k >= 0; --k) {
+      const int64_t p = k * c->b, w = std::min(c->b, n - p);
+      rc = laswp(c->st, out, ld, 0, n, p, (int)w, c->ipiv + p, true);
+    }
     cudaStreamSynchronize(c->st);
     cudaFree(U);
     return rc;

@@ -308,6 +308,18 @@ static int diag_factor_t(cudaStream_t st, T* D, int64_t ld, int w, int mode, T* 
   return 0;
 }
 
+int tri_inverse_lower(cudaStream_t st, const double* D, int64_t ld, int w, bool unit, double* Linv,
+                      int64_t ldl, const int* info_dev) {
+  if (w <= 0) return 0;
+  const int ism = INV_SMEM;
+  ABFT_TRY(ensure_smem_attr((const void*)tri_inverse_kernel<double>, ism));
+  count_launch();
+  tri_inverse_kernel<double><<<dim3((w + NBK - 1) / NBK, 1), DT, ism, st>>>(
+      D, ld, w, unit ? 1 : 0, Linv, ldl, nullptr, 0, info_dev);
+  CUDA_TRY(cudaGetLastError());
+  return 0;
+}
+
 int diag_factor(cudaStream_t st, double* D, int64_t ld, int w, int mode, double* Linv, int64_t ldl,
                 double* Uinv, int64_t ldu, int* info_dev, int64_t col_base, double* sgn) {
   return diag_factor_t(st, D, ld, w, mode, Linv, ldl, Uinv, ldu, info_dev, col_base, sgn);

@@ -40,6 +40,23 @@ int diag_factor_fast(cudaStream_t st, float* D, int64_t ld, int w, int mode, flo
                      int64_t ldl, float* Uinv, int64_t ldu, int* info_dev, int64_t col_base,
                      float* sgn = nullptr);
 
+// L^{-1} of the lower triangle of the w x w block D (unit: unit diagonal);
+// skipped if *info_dev != 0.
+int tri_inverse_lower(cudaStream_t st, const double* D, int64_t ld, int w, bool unit, double* Linv,
+                      int64_t ldl, const int* info_dev);
+
+// LU with partial pivoting of the m x w panel P in place (LAPACK dgetf2
+// semantics: ipiv[j] = panel-local row swapped with row j; L unit lower
+// below, U on/above the diagonal), lu_pivot.cu. part: >= 2 (G+1)(w+2)
+// doubles (G <= #SMs). info: 1 + col_base + column of an exactly singular
+// (or non-finite) pivot.
+int lu_panel_pivot(cudaStream_t st, double* P, int64_t ld, int64_t m, int w, int32_t* ipiv,
+                   double* part, int64_t part_elems, int* info, int64_t col_base);
+// Row interchanges ipiv[0..w) at rows k0.. applied to columns [c0, c0+ncols)
+// (LAPACK dlaswp, in order; reverse: last first, i.e. P^T).
+int laswp(cudaStream_t st, double* A, int64_t ld, int64_t c0, int64_t ncols, int64_t k0, int w,
+          const int32_t* ipiv, bool reverse = false);
+
 struct GemmWorkspace;
 
 // Workspace of qr_panel_factor.

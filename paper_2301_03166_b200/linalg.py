@@ -214,7 +214,10 @@ class Factorization:
     """
 
     def __init__(self, kind, a0: np.ndarray, b: int, device: int | None = None,
-                 keep_input: bool = False):
+                 keep_input: bool = False, pivoting: bool = False):
+        """``pivoting`` (LU only): partial pivoting with LAPACK dgetrf
+        semantics (P a0 = L U; ``piv``) -- an option of the drop-in, the
+        reference factors unpivoted (linalg.py:230-238)."""
         self.kind = DecompositionKind(_value(kind))
         self.a0 = a0
         self.b = int(b)
@@ -233,9 +236,20 @@ class Factorization:
             check(lib.abft_keep_input(ctx, 1))
         host = np.asfortranarray(np.asarray(a0, dtype=np.float64))
         check(lib.abft_set_matrix(ctx, _lib.dptr(host), n))
+        self.pivoting = bool(pivoting)
+        if self.pivoting:
+            check(lib.abft_set_pivoting(ctx, 1))
         self._m_cache: np.ndarray | None = None
         self.qr_t = _QRFactors(self, "t")
         self._qr_vs = _QRFactors(self, "v")
+
+    @property
+    def piv(self) -> np.ndarray:
+        """Row interchanges of the pivoted LU (0-based, LAPACK ipiv - 1: row i
+        was swapped with piv[i], in order); the identity when unpivoted."""
+        out = np.empty(self.n, dtype=np.int32)
+        check(self._lib.abft_get_pivots(self._ctx, out.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))))
+        return out
 
     def __del__(self):
         ctx = getattr(self, "_ctx", None)
