@@ -410,6 +410,18 @@ def tf32x3_peak() -> tuple:
         return 1590.0 / 6.0, "fallback bf16 1.59 PF / 2 / 3 (B200_PROFILING.md), of fallback"
 
 
+def hbm_peak() -> tuple:
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json), else the fallback."""
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        for key in ("hbm_gbs", "hbm_copy_gbs", "hbm_GBs"):
+            if key in d:
+                return float(d[key]), f"MEASURED_PEAKS.json {key}"
+    except Exception:
+        pass
+    return 6533.5, "fallback (SURVEY §8d MEASURED_PEAKS hbm_gbs)"
+
+
 def tmu_flops(kind, n, b) -> float:
     from paper_2301_03166_b200.linalg import compute_flops
     return sum(compute_flops(kind, "tmu", n, b, k) for k in range(-(-n // b)))
@@ -524,6 +536,16 @@ def run_ours(args):
                     "achieved": achieved, "peak": p32, "unit": "TFLOP/s",
                     "frac": (achieved / p32) if achieved else None, "traffic": None,
                     "peak_source": src32}
+        if args.kind == "lu" and prof["tmu_gemm"]:
+            # the K = b trailing update reads C and writes D once (8 B per element in
+            # fp32): at b = 128 it is HBM-bound before it is tensor-bound
+            elems = sum((args.n - min((k + 1) * args.b, args.n)) ** 2
+                        for k in range(-(-args.n // args.b)))
+            gbs = 8.0 * elems / (prof["tmu_gemm"] * 1e-3) / 1e9
+            hbm = hbm_peak()
+            roofline["hbm_view"] = {"achieved": gbs, "peak": hbm[0], "unit": "GB/s",
+                                    "frac": gbs / hbm[0], "bytes_per_factorization": 8.0 * elems,
+                                    "peak_source": hbm[1]}
     e2e = None
     if not args.no_e2e and args.precision == "f32":
         e2e = run_e2e_s(arm, args)
