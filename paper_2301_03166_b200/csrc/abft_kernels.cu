@@ -16,14 +16,18 @@ namespace abft {
 namespace {
 
 constexpr int BS_THREADS = 256;  // 8 warps
-constexpr int BS_ROWS = 256;     // rows per chunk (8 per lane)
 
-// One CTA per block (grid-stride). Warp w takes columns w, w+8, ...; lane l
-// takes rows l + 32*i of the current 256-row chunk.
-template <typename T>
+// One CTA per block (grid-stride). Warp w takes column groups of C4 adjacent
+// columns (w*C4, w*C4 + 8*C4, ...); lane l takes rows l + 32*i (i < RPL) of
+// the current 32*RPL-row chunk. RPL = 4 for blocks of <= 128 rows (fp32
+// b = 128: no masked half-chunk), else 8. Per element: one conversion, two
+// fp64 adds and one fp64 FMA against a per-chunk row weight; the block max is
+// tracked in T (|x| max is exact in any precision).
+template <typename T, int RPL, int C4>
 __global__ void __launch_bounds__(BS_THREADS)
     blocksum_kernel(RegionT<T> reg, SumOut out, int64_t nbr, int64_t nbc, const int32_t* blocks,
                     const int32_t* nblocks_dev, int64_t nlist_static) {
+  constexpr int BS_ROWS = 32 * RPL;
   extern __shared__ double dsm[];
   double* colacc_p = dsm;             // [b]
   double* colacc_w = dsm + reg.b;     // [b]
@@ -49,31 +53,32 @@ __global__ void __launch_bounds__(BS_THREADS)
     const int br = (int)min(reg.b, reg.rows - r_lo);
     const int bc = (int)min(reg.b, reg.cols - c_lo);
     const T* base = reg.ptr + r_lo + c_lo * reg.ld;
-    double mx = 0.0;
+    T mx = T(0);
     for (int c = threadIdx.x; c < bc; c += BS_THREADS) {
       colacc_p[c] = 0.0;
       colacc_w[c] = 0.0;
     }
     __syncthreads();
     for (int r0 = 0; r0 < br; r0 += BS_ROWS) {
-      double racc[8], rwacc[8];
+      double racc[RPL], rwacc[RPL], wgt[RPL];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) racc[i] = rwacc[i] = 0.0;
-      // each warp takes 4 adjacent columns per step and issues all 32 of its
-      // loads per lane before reducing: 4x the memory-level parallelism of a
-      // column-at-a-time loop (panel-shaped regions have few blocks, so
-      // per-CTA bandwidth is what bounds this pass)
-      constexpr int C4 = 4;
+      for (int i = 0; i < RPL; ++i) {
+        racc[i] = rwacc[i] = 0.0;
+        wgt[i] = (double)(r0 + lane + 32 * i);  // row index inside the block
+      }
+      // each warp takes C4 adjacent columns per step and issues all its loads
+      // per lane before reducing (panel-shaped regions have few blocks, so
+      // per-CTA memory-level parallelism is what bounds this pass)
       for (int cb = warp * C4; cb < bc; cb += 8 * C4) {
-        double x[C4][8];
+        T xr[C4][RPL];
 #pragma unroll
         for (int q = 0; q < C4; ++q) {
           const int c = cb + q;
           const T* col = base + (int64_t)c * reg.ld + r0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
+          for (int i = 0; i < RPL; ++i) {
             const int r = lane + 32 * i;
-            x[q][i] = (c < bc && r0 + r < br) ? (double)col[r] : 0.0;
+            xr[q][i] = (c < bc && r0 + r < br) ? col[r] : T(0);
           }
         }
 #pragma unroll
@@ -81,13 +86,13 @@ __global__ void __launch_bounds__(BS_THREADS)
           const int c = cb + q;
           double cs = 0.0, cw = 0.0;
 #pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            const int r = lane + 32 * i;
-            cs += x[q][i];
-            cw += (double)(r0 + r) * x[q][i];
-            racc[i] += x[q][i];
-            if (want_rw) rwacc[i] += (double)c * x[q][i];
-            mx = fmax(mx, fabs(x[q][i]));
+          for (int i = 0; i < RPL; ++i) {
+            const double xv = (double)xr[q][i];
+            cs += xv;
+            cw += wgt[i] * xv;
+            racc[i] += xv;
+            if (want_rw) rwacc[i] += (double)c * xv;
+            mx = fmax(mx, fabs(xr[q][i]));
           }
           cs = warp_sum(cs);
           cw = warp_sum(cw);
@@ -99,13 +104,13 @@ __global__ void __launch_bounds__(BS_THREADS)
       }
       if (want_rp || want_rw) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < RPL; ++i) {
           srow[warp][lane + 32 * i] = racc[i];
           srw[warp][lane + 32 * i] = rwacc[i];
         }
         __syncthreads();
         const int r = threadIdx.x;
-        if (r0 + r < br) {
+        if (r < BS_ROWS && r0 + r < br) {
           double s = 0.0, sw = 0.0;
 #pragma unroll
           for (int w = 0; w < 8; ++w) {
@@ -123,8 +128,8 @@ __global__ void __launch_bounds__(BS_THREADS)
       if (out.cp) out.cp[out.cp_step * bi + (c_lo + c) * out.cp_ld] = colacc_p[c];
       if (out.cw) out.cw[out.cw_step * bi + (c_lo + c) * out.cw_ld] = colacc_w[c];
     }
-    mx = warp_max(mx);
-    if (lane == 0) smax[warp] = mx;
+    const double mxd = warp_max((double)mx);
+    if (lane == 0) smax[warp] = mxd;
     __syncthreads();
     if (threadIdx.x == 0 && out.bm) {
       double m = smax[0];
@@ -605,7 +610,11 @@ static int blocksum_t(cudaStream_t st, const RegionT<T>& reg, const SumOut& out,
   const int64_t nbr = (reg.rows + reg.b - 1) / reg.b;
   const int64_t nbc = (reg.cols + reg.b - 1) / reg.b;
   const size_t dyn = 2 * reg.b * sizeof(double);
-  ABFT_TRY(ensure_smem_attr((const void*)blocksum_kernel<T>, 2 * 4096 * 8));
+  // fp32 blocks of <= 128 rows: 4 rows per lane, 8 columns per warp step;
+  // otherwise (fp64 b = 256, the bit-exact goldens) 8 rows per lane, 4 columns
+  const bool small = sizeof(T) == 4 && reg.b <= 128;
+  const void* fn = small ? (const void*)blocksum_kernel<T, 4, 8> : (const void*)blocksum_kernel<T, 8, 4>;
+  ABFT_TRY(ensure_smem_attr(fn, 2 * 4096 * 8));
   int64_t nblk = blocks ? max_list : nbr * nbc;
   if (nblk <= 0) return 0;
   int grid = (int)(nblk < 148 * 8 ? nblk : 148 * 8);
@@ -613,8 +622,12 @@ static int blocksum_t(cudaStream_t st, const RegionT<T>& reg, const SumOut& out,
   // empty: a one-wave grid keeps the no-op launch cheap
   if (nblocks_dev && grid > 148) grid = 148;
   count_launch();
-  blocksum_kernel<T><<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
-                                                     (int64_t)max_list);
+  if (small)
+    blocksum_kernel<T, 4, 8><<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
+                                                            (int64_t)max_list);
+  else
+    blocksum_kernel<T, 8, 4><<<grid, BS_THREADS, dyn, st>>>(reg, out, nbr, nbc, blocks, nblocks_dev,
+                                                            (int64_t)max_list);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
