@@ -22,3 +22,7 @@ for k in lu qr; do
 done
 NCU="ncu --set full --clock-control none --import-source on"
 timeout 900 $NCU -k regex:coop_factor -c 3 -o gpurun_out/prof_cf_$TAG python bench.py --kind qr --profile-only > gpurun_out/prof_cf_$TAG.log 2>&1; echo "ncu cf rc=$?"
+for k in lu cholesky qr; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 6000 --csv \
+    --log-file gpurun_out/launches_s${k}_$TAG.csv python bench.py --kind $k --precision f32 --n 16384 --b 128 --profile-only > gpurun_out/launches_s${k}_$TAG.log 2>&1; echo "launches s$k rc=$?"
+done
