@@ -149,6 +149,14 @@ ABFT_API int abft_create(abft_ctx** ctx, int kind, int64_t n, int64_t b, int dev
 ABFT_API int abft_destroy(abft_ctx* ctx);
 /* copy the host input (column-major, leading dim lda) into the device working matrix */
 ABFT_API int abft_set_matrix(abft_ctx* ctx, const double* a, int64_t lda);
+/* like abft_set_matrix, but the copy happens inside the next abft_factorize
+ * call, column block by column block on a copy stream, overlapped with the
+ * factorization (Cholesky copies only rows >= j*b of block column j, the lower
+ * block triangle it reads, and waits per block; LU / QR wait for the whole
+ * matrix). `a` (pinned for an asynchronous copy) must stay valid until that
+ * call returns; other entries that touch the matrix copy it first. Replaces
+ * the host-to-device half of the e2e round trip (bench.py run_e2e). */
+ABFT_API int abft_set_matrix_streamed(abft_ctx* ctx, const double* a, int64_t lda);
 /* keep a device copy of the input for abft_residual(ctx, NULL, ...) */
 ABFT_API int abft_keep_input(abft_ctx* ctx, int keep);
 /* restore the working matrix from the kept input (needs abft_keep_input) */

@@ -76,6 +76,7 @@ SIGNATURES = [
     ("abft_create", _I, [ctypes.POINTER(_P), _I, _I64, _I64, _I]),
     ("abft_destroy", _I, [_P]),
     ("abft_set_matrix", _I, [_P, _D, _I64]),
+    ("abft_set_matrix_streamed", _I, [_P, _D, _I64]),
     ("abft_keep_input", _I, [_P, _I]),
     ("abft_reset", _I, [_P]),
     ("abft_stream", _P, [_P]),

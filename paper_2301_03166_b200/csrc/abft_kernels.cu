@@ -562,12 +562,15 @@ __global__ void copy_kernel(const T* s, int64_t lds, U* d, int64_t ldd, int64_t 
 
 template <typename T>
 __global__ void sub_kernel(const T* x, int64_t ldx, T* d, int64_t ldd, int64_t rows,
-                           int64_t cols) {
+                           int64_t cols, int add) {
   const int64_t total = rows * cols;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i % rows, c = i / rows;
-    d[r + c * ldd] -= x[r + c * ldx];
+    if (add)
+      d[r + c * ldd] += x[r + c * ldx];
+    else
+      d[r + c * ldd] -= x[r + c * ldx];
   }
 }
 
@@ -812,10 +815,10 @@ int widen_matrix(cudaStream_t st, const float* src, int64_t lds, double* dst, in
 
 template <typename T>
 static int sub_t(cudaStream_t st, const T* x, int64_t ldx, T* d, int64_t ldd, int64_t rows,
-                 int64_t cols) {
+                 int64_t cols, int add = 0) {
   if (rows <= 0 || cols <= 0) return 0;
   count_launch();
-  sub_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols);
+  sub_kernel<T><<<grid_for(rows * cols, 256), 256, 0, st>>>(x, ldx, d, ldd, rows, cols, add);
   CUDA_TRY(cudaGetLastError());
   return 0;
 }
@@ -826,6 +829,10 @@ int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t
 int sub_matrix(cudaStream_t st, const float* x, int64_t ldx, float* d, int64_t ldd, int64_t rows,
                int64_t cols) {
   return sub_t(st, x, ldx, d, ldd, rows, cols);
+}
+int add_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols) {
+  return sub_t(st, x, ldx, d, ldd, rows, cols, 1);
 }
 
 int gather_transpose(cudaStream_t st, const double* src, int64_t row_step, int64_t lds,

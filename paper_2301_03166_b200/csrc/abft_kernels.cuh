@@ -161,5 +161,8 @@ int sub_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t
                int64_t cols);
 int sub_matrix(cudaStream_t st, const float* x, int64_t ldx, float* d, int64_t ldd, int64_t rows,
                int64_t cols);
+// d += x
+int add_matrix(cudaStream_t st, const double* x, int64_t ldx, double* d, int64_t ldd, int64_t rows,
+               int64_t cols);
 
 }  // namespace abft

@@ -138,6 +138,17 @@ struct abft_ctx {
   cudaEvent_t ev_out = nullptr;
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
   cudaEvent_t ev_a = nullptr, ev_p = nullptr;
+  // streamed input (abft_set_matrix_streamed): the next abft_factorize call
+  // copies the column blocks on st_in (Cholesky: only rows >= j b of block j,
+  // the lower block triangle the algorithm reads) and each iteration waits
+  // for the block it is about to touch, so the H2D overlaps the factorization
+  const double* in_host = nullptr;
+  int64_t in_ld = 0;
+  bool in_stream = false;         // the running abft_factorize consumes streamed blocks
+  cudaStream_t st_in = nullptr;
+  std::vector<cudaEvent_t> ev_in;
+  std::vector<char> rs_enc;       // streamed Cholesky FULL: block column's row sums added
+  double* rs_tmp = nullptr;       // n: fresh row sums of one block column
   // profiling
   struct ProfPair {
     int cat;
@@ -339,6 +350,31 @@ int chol_rs_update(abft_ctx* c, int64_t k) {
   return gemm(c->st, 'N', 'N', (int)(n - pe), (int)nj, (int)w, -1.0, c->m + pe + p * c->ld, c->ld,
               c->er, c->ld_t, 1.0, c->chol_rs + pe + (k + 1) * c->ld, c->ld,
               c->chol_rs + pe + (k + 1) * c->ld, c->ld, &c->gws);
+}
+
+// Streamed input: the stream waits until column block j has arrived.
+int wait_in(abft_ctx* c, cudaStream_t st, int64_t j) {
+  if (!c->in_stream || j < 0 || j >= c->nb) return 0;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in[j], 0));
+  return 0;
+}
+
+// Streamed Cholesky FULL: chol_rs starts at zero and takes the panel updates
+// as they come (chol_rs_update); block column j's own row sums are added once
+// it has arrived, before anything modifies its rows >= j b (the look-ahead
+// update of panel j on st2, else TMU(j)). Same quantity as chol_rs_encode +
+// the updates, summed in another order.
+int chol_rs_encode_col(abft_ctx* c, cudaStream_t st, int64_t j) {
+  if (!c->in_stream || !c->chol_rs_valid || j >= c->nb || c->rs_enc[j]) return 0;
+  const int64_t n = c->n, p = j * c->b, w = std::min(c->b, n - p);
+  Region reg{c->m + p + p * c->ld, c->ld, n - p, w, c->b};
+  SumOut o;
+  o.rp = c->rs_tmp;
+  o.rp_ld = c->ld;
+  ABFT_TRY(blocksum(st, reg, o));
+  ABFT_TRY(add_matrix(st, c->rs_tmp, c->ld, c->chol_rs + p + j * c->ld, c->ld, n - p, 1));
+  c->rs_enc[j] = 1;
+  return 0;
 }
 
 // LU panel, part 1: factor the diagonal block and form L11^{-1}, U11^{-1}.
@@ -604,9 +640,15 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
   bool fused_done = false;
   if (c->kind == ABFT_CHOLESKY && k == 0 && (scheme == ABFT_FULL || c->want_chol_rs)) {
     prof_mark(c, PROF_ABFT, true);
-    ABFT_TRY(chol_rs_encode(c));
+    if (c->in_stream) {  // block columns add their row sums as they arrive
+      CUDA_TRY(cudaMemsetAsync(c->chol_rs, 0, (size_t)c->ld * c->nb * sizeof(double), c->st));
+      c->chol_rs_valid = true;
+    } else {
+      ABFT_TRY(chol_rs_encode(c));
+    }
     prof_mark(c, PROF_ABFT, false);
   }
+  if (c->kind == ABFT_CHOLESKY) ABFT_TRY(chol_rs_encode_col(c, c->st, k));
   if (prot) {
     // encode (abft.py:118-135): reuse the previous verify's sums when the
     // region is a sub-grid of the last verified region (LU/QR), else a pass
@@ -750,6 +792,8 @@ int chol_lookahead(abft_ctx* c, int64_t k, int scheme_next, bool ev_recorded = f
   const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
   if (!ev_recorded) CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  ABFT_TRY(wait_in(c, c->st2, k + 1));
+  ABFT_TRY(chol_rs_encode_col(c, c->st2, k + 1));
   c->chol_enc_ahead = false;
   if (scheme_next != ABFT_NONE) {
     Region reg1{c->m + p1 + p1 * c->ld, c->ld, n - p1, w1, c->b};
@@ -1040,6 +1084,7 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(wait_in(c, c->st, k));
     ABFT_TRY(protected_tmu(c, k, scheme, plan, nplan, correct));
     const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb;
     const bool side_set = (int64_t)c->side_sms.size() > k && c->side_sms[k] > 0;
@@ -1138,6 +1183,17 @@ int collect_events(abft_ctx* c, const std::vector<int64_t>& r0s, const std::vect
 // C-ABI
 // ===========================================================================
 extern "C" {
+
+// A streamed input not yet consumed by abft_factorize: entries that touch
+// the matrix otherwise copy it now (the whole matrix, synchronously).
+static int flush_pending_input(abft_ctx* c) {
+  if (!c->in_host) return 0;
+  const double* a = c->in_host;
+  c->in_host = nullptr;
+  CUDA_TRY(cudaMemcpy2DAsync(c->m, c->ld * 8, a, c->in_ld * 8, c->n * 8, c->n,
+                             cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
 
 ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int device) {
   *out = nullptr;
@@ -1265,6 +1321,7 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
@@ -1311,6 +1368,12 @@ ABFT_API int abft_destroy(abft_ctx* c) {
     cudaStreamSynchronize(c->st_out);
     cudaStreamDestroy(c->st_out);
   }
+  if (c->st_in) {
+    cudaStreamSynchronize(c->st_in);
+    cudaStreamDestroy(c->st_in);
+  }
+  for (auto e : c->ev_in) cudaEventDestroy(e);
+  if (c->rs_tmp) cudaFree(c->rs_tmp);
   if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
@@ -1323,6 +1386,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
 
 ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   DevGuard g(c->device);
+  c->in_host = nullptr;
   if (lda < c->n) {
     set_last_error("lda < n");
     return ABFT_E_INVALID;
@@ -1335,6 +1399,34 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
                                cudaMemcpyDeviceToDevice, c->st));
   }
   CUDA_TRY(cudaStreamSynchronize(c->st));
+  c->k_done = 0;
+  c->sums_valid = false;
+  c->qr_count = 0;
+  c->breakdown_col = -1;
+  c->pd_ready = -1;
+  c->chol_part = -1;
+  c->chol_enc_ahead = false;
+  c->chol_rs_valid = false;
+  return 0;
+}
+
+// Like abft_set_matrix, but the copy is deferred into the next
+// abft_factorize call, column block by column block on a copy stream, and
+// overlaps the factorization (Cholesky reads only the lower block triangle:
+// rows >= j b of block column j are copied, the rest of the device matrix is
+// zeroed by the factorization itself). `a` must stay valid (and should be
+// pinned) until that call returns. With keep_input (abft_reset) this is a
+// plain abft_set_matrix.
+ABFT_API int abft_set_matrix_streamed(abft_ctx* c, const double* a, int64_t lda) {
+  if (c->keep_input) return abft_set_matrix(c, a, lda);
+  DevGuard g(c->device);
+  if (lda < c->n) {
+    set_last_error("lda < n");
+    return ABFT_E_INVALID;
+  }
+  if (c->kind == ABFT_CHOLESKY && !c->rs_tmp) ABFT_TRY(dalloc(&c->rs_tmp, c->ld));
+  c->in_host = a;
+  c->in_ld = lda;
   c->k_done = 0;
   c->sums_valid = false;
   c->qr_count = 0;
@@ -1374,6 +1466,7 @@ ABFT_API void* abft_stream(abft_ctx* c) { return reinterpret_cast<void*>(c->st);
 // the kept input copy (if any) is refreshed.
 ABFT_API int abft_make_spd(abft_ctx* c) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   double* T = nullptr;
   ABFT_TRY(dalloc(&T, c->ld * c->n));
   int rc = gemm(c->st, 'N', 'T', (int)c->n, (int)c->n, (int)c->n, 1.0, c->m, c->ld, c->m, c->ld,
@@ -1393,6 +1486,7 @@ ABFT_API int abft_keep_input(abft_ctx* c, int keep) {
 
 ABFT_API int abft_get_matrix(abft_ctx* c, double* mh, int64_t ldm) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   CUDA_TRY(cudaMemcpy2DAsync(mh, ldm * 8, c->m, c->ld * 8, c->n * 8, c->n, cudaMemcpyDeviceToHost,
                              c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
@@ -1408,6 +1502,7 @@ ABFT_API int abft_set_k_done(abft_ctx* c, int64_t k) {
 
 ABFT_API int abft_task(abft_ctx* c, int64_t k, int task) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   if (k < 0 || k >= c->nb) {
     set_last_error("iteration %lld out of range", (long long)k);
     return ABFT_E_DIM;
@@ -1431,6 +1526,7 @@ ABFT_API int abft_task(abft_ctx* c, int64_t k, int task) {
 ABFT_API int abft_iteration(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
                             int correct, abft_report* rep, abft_location* locs, int max_locs) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   if (k < 0 || k >= c->nb) {
     set_last_error("iteration %lld out of range for %lld blocks", (long long)k, (long long)c->nb);
     return ABFT_E_DIM;
@@ -1465,6 +1561,35 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
     if ((schemes ? schemes[k] : scheme) == ABFT_FULL) c->want_chol_rs = true;
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
+  c->in_stream = false;
+  if (c->in_host) {
+    // streamed input: every column block goes out now on st_in (in order);
+    // Cholesky iterations wait for their own block, LU / QR for all of them
+    const bool chol = c->kind == ABFT_CHOLESKY;
+    if ((int64_t)c->ev_in.size() < c->nb) {
+      for (int64_t j = (int64_t)c->ev_in.size(); j < c->nb; ++j) {
+        cudaEvent_t e = nullptr;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_in.push_back(e);
+      }
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_a, c->st));  // the previous use of the matrix is over
+    CUDA_TRY(cudaStreamWaitEvent(c->st_in, c->ev_a, 0));
+    for (int64_t j = 0; j < c->nb; ++j) {
+      const int64_t p = j * c->b, w = std::min(c->b, c->n - p);
+      const int64_t r0 = chol ? p : 0;
+      CUDA_TRY(cudaMemcpy2DAsync(c->m + r0 + p * c->ld, c->ld * 8, c->in_host + r0 + p * c->in_ld,
+                                 c->in_ld * 8, (c->n - r0) * 8, w, cudaMemcpyHostToDevice, c->st_in));
+      CUDA_TRY(cudaEventRecord(c->ev_in[j], c->st_in));
+    }
+    c->in_host = nullptr;
+    if (chol) {
+      c->in_stream = true;
+      c->rs_enc.assign(c->nb, 0);
+    } else {
+      CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
+    }
+  }
   for (int64_t k = k0; k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
     int f0 = 0, f1 = 0;
@@ -1479,9 +1604,11 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
                                   c->lookahead_enabled);
     if (rc != 0) {
       cudaEventRecord(c->e1, c->st);
+      c->in_stream = false;
       return rc;
     }
   }
+  c->in_stream = false;
   if (c->out_host) {  // the streamed result is part of the call
     CUDA_TRY(cudaEventRecord(c->ev_out, c->st_out));
     CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_out, 0));
@@ -1681,6 +1808,7 @@ ABFT_API int abft_get_qr_panel(abft_ctx* c, int64_t k, double* V, int64_t ldv, d
 
 ABFT_API int abft_snapshot(abft_ctx* c, int slot) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   if (slot < 0 || slot > 64) {
     set_last_error("bad snapshot slot");
     return ABFT_E_INVALID;
@@ -1730,6 +1858,7 @@ ABFT_API int64_t abft_breakdown_column(abft_ctx* c) { return c->breakdown_col; }
 // 4 gmax (nb x nb). Copies the full array into `out` (column-major).
 ABFT_API int abft_debug_array(abft_ctx* c, int which, double* out, int64_t* rows, int64_t* cols) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   const double* src;
   int64_t r, cl, ld;
   switch (which) {
@@ -1796,6 +1925,7 @@ static int reconstruct_device(abft_ctx* c, double* out, double* tmp) {
 
 ABFT_API int abft_reconstruct(abft_ctx* c, double* outh, int64_t ldo) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   if (c->k_done < c->nb) {
     set_last_error("factorization incomplete");
     return ABFT_E_INCOMPLETE;
@@ -1842,6 +1972,7 @@ ABFT_API int abft_set_qr_panels(abft_ctx* c, int count) {
 
 ABFT_API int abft_residual(abft_ctx* c, const double* a0h, int64_t lda, double* out) {
   DevGuard g(c->device);
+  ABFT_TRY(flush_pending_input(c));
   if (c->k_done < c->nb) {
     set_last_error("factorization incomplete");
     return ABFT_E_INCOMPLETE;

@@ -98,3 +98,34 @@ def test_lookahead_fast_path_equals_per_iteration(kind, n, b):
     assert r2 == pytest.approx(r1, rel=1e-6, abs=1e-15)
     if not any(r["uncorrectable"] for r in per):
         assert r2 < 1e-14
+
+
+@pytest.mark.parametrize("kind", ["cholesky", "lu", "qr"])
+@pytest.mark.parametrize("n,b", [(2048, 256), (1300, 256), (1408, 128)])
+def test_streamed_input_equals_set_matrix(kind, n, b):
+    """abft_set_matrix_streamed: the input arrives block column by block
+    column inside abft_factorize (Cholesky: only the lower block triangle,
+    each iteration waiting for its block; its FULL row checksums start at
+    zero and take each block's row sums on arrival). Same reports and the
+    same factor as abft_set_matrix, with faults at two iterations; the device
+    matrix is overwritten with junk first so nothing stale can pass."""
+    import ctypes
+    nb = -(-n // b)
+    sched = {1: {P.ErrorKind.D0: 2, P.ErrorKind.D1: 1}, nb - 2: {P.ErrorKind.D0: 1}}
+    a = P.generate_test_matrix(kind, n, 5)
+    f1 = P.Factorization(kind, a, b)
+    ref = [report_json(r) for r in P.run_protected(f1, "full", sched, np.random.default_rng(5))]
+    f2 = P.Factorization(kind, a, b)
+    lib = f2._lib
+    junk = np.asfortranarray(np.random.default_rng(1).standard_normal((n, n)) * 1e3)
+    assert lib.abft_set_matrix(f2._ctx, junk.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n) == 0
+    af = np.asfortranarray(a, dtype=np.float64)
+    assert lib.abft_set_matrix_streamed(f2._ctx, af.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        n) == 0
+    got = [report_json(r) for r in P.run_protected(f2, "full", sched, np.random.default_rng(5))]
+    assert got == ref
+    m1, m2 = f1.m, f2.m
+    if kind == "cholesky":  # the factorization zeroes what it does not copy in
+        m1, m2 = np.tril(m1), np.tril(m2)
+        assert not np.any(np.triu(f2.m, 1))
+    np.testing.assert_allclose(m2, m1, rtol=0, atol=1e-12 * max(1.0, np.abs(m1).max()))
