@@ -306,6 +306,8 @@ ABFT_API void* abft_s_stream(abft_sctx* ctx);
 ABFT_API int64_t abft_s_k_done(abft_sctx* ctx);
 ABFT_API int abft_s_keep_input(abft_sctx* ctx, int keep);
 ABFT_API int abft_s_set_matrix(abft_sctx* ctx, const float* a, int64_t lda);
+/* fp32 twin of abft_set_matrix_streamed */
+ABFT_API int abft_s_set_matrix_streamed(abft_sctx* ctx, const float* a, int64_t lda);
 ABFT_API int abft_s_reset(abft_sctx* ctx);
 ABFT_API int abft_s_make_spd(abft_sctx* ctx);
 ABFT_API int abft_s_get_matrix(abft_sctx* ctx, float* m, int64_t ldm);

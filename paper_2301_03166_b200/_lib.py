@@ -137,6 +137,7 @@ SIGNATURES = [
     ("abft_s_k_done", _I64, [_P]),
     ("abft_s_keep_input", _I, [_P, _I]),
     ("abft_s_set_matrix", _I, [_P, _F, _I64]),
+    ("abft_s_set_matrix_streamed", _I, [_P, _F, _I64]),
     ("abft_s_reset", _I, [_P]),
     ("abft_s_make_spd", _I, [_P]),
     ("abft_s_get_matrix", _I, [_P, _F, _I64]),

@@ -142,6 +142,15 @@ struct abft_sctx {
   int64_t out_ld = 0;
   cudaStream_t st_out = nullptr;
   cudaEvent_t ev_out = nullptr;
+  // streamed input (abft_s_set_matrix_streamed, as ctx.cu): block columns
+  // copied on st_in inside the next abft_s_factorize call
+  const float* in_host = nullptr;
+  int64_t in_ld = 0;
+  bool in_stream = false;
+  cudaStream_t st_in = nullptr;
+  std::vector<cudaEvent_t> ev_in;
+  std::vector<char> rs_enc;
+  double* rs_tmp = nullptr;
   // device snapshot slot (replaces _Run._snapshot/_restore, simulator.py:420-436)
   float* snap_m = nullptr;
   double* snap_rs = nullptr;
@@ -342,6 +351,29 @@ int s_chol_update(abft_sctx* c, cudaStream_t st, int64_t k, int64_t K0, int64_t 
   return 0;
 }
 
+// Streamed input: the stream waits until column block j has arrived.
+int s_wait_in(abft_sctx* c, cudaStream_t st, int64_t j) {
+  if (!c->in_stream || j < 0 || j >= c->nb) return 0;
+  CUDA_TRY(cudaStreamWaitEvent(st, c->ev_in[j], 0));
+  return 0;
+}
+
+// Streamed Cholesky FULL (as ctx.cu chol_rs_encode_col): block column j's
+// row sums join chol_rs (zeroed at k = 0, panel updates already applied)
+// before anything modifies its rows >= j b.
+int s_chol_rs_encode_col(abft_sctx* c, cudaStream_t st, int64_t j) {
+  if (!c->in_stream || !c->chol_rs_valid || j >= c->nb || c->rs_enc[j]) return 0;
+  const int64_t n = c->n, p = j * c->b, w = std::min(c->b, n - p);
+  RegionF reg{c->m + p + p * c->ld, c->ld, n - p, w, c->b};
+  SumOut o;
+  o.rp = c->rs_tmp;
+  o.rp_ld = c->ld;
+  ABFT_TRY(blocksum(st, reg, o));
+  ABFT_TRY(add_matrix(st, c->rs_tmp, c->ld, c->chol_rs + p + j * c->ld, c->ld, n - p, 1));
+  c->rs_enc[j] = 1;
+  return 0;
+}
+
 // Cholesky look-ahead (as ctx.cu): right after TMU(k) the update of panel
 // k+1 by panels 0..k-1 -- final since their PU -- runs on the side stream
 // (encode of panel k+1 first, when its iteration is protected) while the
@@ -353,6 +385,8 @@ int s_chol_lookahead(abft_sctx* c, int64_t k, int scheme_next, bool ev_recorded 
   const int64_t pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
   if (!ev_recorded) CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  ABFT_TRY(s_wait_in(c, c->st2, k + 1));
+  ABFT_TRY(s_chol_rs_encode_col(c, c->st2, k + 1));
   c->chol_enc_ahead = false;
   if (scheme_next != ABFT_NONE) {
     RegionF reg1{c->m + p1 + p1 * c->ld, c->ld, n - p1, w1, c->b};
@@ -652,13 +686,18 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
   RegionF reg{c->m + r0 + c0 * c->ld, c->ld, rows, cols, c->b};
   bool fused = false;
   if (c->kind == ABFT_CHOLESKY && k == 0 && (scheme == ABFT_FULL || c->want_chol_rs)) {
-    RegionF all{c->m, c->ld, n, n, c->b};
-    SumOut o;
-    o.rp = c->chol_rs;
-    o.rp_ld = c->ld;
-    ABFT_TRY(blocksum(c->st, all, o));
+    if (c->in_stream) {  // block columns add their row sums as they arrive
+      CUDA_TRY(cudaMemsetAsync(c->chol_rs, 0, (size_t)c->ld * c->nb * sizeof(double), c->st));
+    } else {
+      RegionF all{c->m, c->ld, n, n, c->b};
+      SumOut o;
+      o.rp = c->chol_rs;
+      o.rp_ld = c->ld;
+      ABFT_TRY(blocksum(c->st, all, o));
+    }
     c->chol_rs_valid = true;
   }
+  if (c->kind == ABFT_CHOLESKY) ABFT_TRY(s_chol_rs_encode_col(c, c->st, k));
   const bool qr_live = c->kind == ABFT_QR && pe < n && k < c->qr_count;
   if (prot) {
     smark(c, SP_ABFT, true);
@@ -978,6 +1017,7 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
+    ABFT_TRY(s_wait_in(c, c->st, k));
     ABFT_TRY(s_protected_tmu(c, k, scheme, plan, nplan, correct));
     // (b % 4: the newest panel's K offset must keep the pre-split rows TMA-aligned)
     const bool la = lookahead && c->lookahead_enabled && k >= 1 && k + 1 < c->nb && c->b % 4 == 0;
@@ -1075,6 +1115,17 @@ void s_fill(abft_sctx* c, const std::vector<Event>& evs, int64_t k0, abft_report
 extern "C" {
 
 ABFT_API int abft_s_destroy(abft_sctx* c);
+
+// A streamed input not yet consumed by abft_s_factorize: entries that touch
+// the matrix otherwise copy it now.
+static int s_flush_pending_input(abft_sctx* c) {
+  if (!c->in_host) return 0;
+  const float* a = c->in_host;
+  c->in_host = nullptr;
+  CUDA_TRY(cudaMemcpy2DAsync(c->m, c->ld * 4, a, c->in_ld * 4, c->n * 4, c->n,
+                             cudaMemcpyHostToDevice, c->st));
+  return 0;
+}
 
 ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int device) {
   *out = nullptr;
@@ -1215,6 +1266,7 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
   cudaEventCreate(&c->e1);
   cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking);
   cudaStreamCreateWithFlags(&c->st_out, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->st_in, cudaStreamNonBlocking);
   cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
@@ -1251,6 +1303,12 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
     cudaStreamSynchronize(c->st_out);
     cudaStreamDestroy(c->st_out);
   }
+  if (c->st_in) {
+    cudaStreamSynchronize(c->st_in);
+    cudaStreamDestroy(c->st_in);
+  }
+  for (auto e : c->ev_in) cudaEventDestroy(e);
+  if (c->rs_tmp) cudaFree(c->rs_tmp);
   if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
@@ -1284,6 +1342,7 @@ static void s_reset_state(abft_sctx* c) {
 
 ABFT_API int abft_s_set_matrix(abft_sctx* c, const float* a, int64_t lda) {
   SGuard g(c->device);
+  c->in_host = nullptr;
   if (lda < c->n) {
     set_last_error("lda < n");
     return ABFT_E_INVALID;
@@ -1294,6 +1353,21 @@ ABFT_API int abft_s_set_matrix(abft_sctx* c, const float* a, int64_t lda) {
     CUDA_TRY(cudaMemcpyAsync(c->a0, c->m, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
   }
   CUDA_TRY(cudaStreamSynchronize(c->st));
+  s_reset_state(c);
+  return 0;
+}
+
+// abft_set_matrix_streamed for the fp32 context.
+ABFT_API int abft_s_set_matrix_streamed(abft_sctx* c, const float* a, int64_t lda) {
+  if (c->keep_input) return abft_s_set_matrix(c, a, lda);
+  SGuard g(c->device);
+  if (lda < c->n) {
+    set_last_error("lda < n");
+    return ABFT_E_INVALID;
+  }
+  if (c->kind == ABFT_CHOLESKY && !c->rs_tmp) CUDA_TRY(cudaMalloc(&c->rs_tmp, c->ld * sizeof(double)));
+  c->in_host = a;
+  c->in_ld = lda;
   s_reset_state(c);
   return 0;
 }
@@ -1312,6 +1386,7 @@ ABFT_API int abft_s_reset(abft_sctx* c) {
 // m <- m m^T + n I (generate_test_matrix's SPD construction, linalg.py:74-75)
 ABFT_API int abft_s_make_spd(abft_sctx* c) {
   SGuard g(c->device);
+  ABFT_TRY(s_flush_pending_input(c));
   float* T = nullptr;
   ABFT_TRY(salloc(&T, c->ld * c->n, c->st));
   int rc = s_gemm(c, 'N', 'T', c->n, c->n, c->n, 1.0f, c->m, c->ld, c->m, c->ld, 0.0f, nullptr, 0, T,
@@ -1326,6 +1401,7 @@ ABFT_API int abft_s_make_spd(abft_sctx* c) {
 
 ABFT_API int abft_s_get_matrix(abft_sctx* c, float* mh, int64_t ldm) {
   SGuard g(c->device);
+  ABFT_TRY(s_flush_pending_input(c));
   CUDA_TRY(cudaMemcpy2DAsync(mh, ldm * 4, c->m, c->ld * 4, c->n * 4, c->n, cudaMemcpyDeviceToHost, c->st));
   CUDA_TRY(cudaStreamSynchronize(c->st));
   return 0;
@@ -1334,6 +1410,7 @@ ABFT_API int abft_s_get_matrix(abft_sctx* c, float* mh, int64_t ldm) {
 ABFT_API int abft_s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan,
                               int correct, abft_report* rep, abft_location* locs, int max_locs) {
   SGuard g(c->device);
+  ABFT_TRY(s_flush_pending_input(c));
   if (k != c->k_done || k < 0 || k >= c->nb) {
     set_last_error("expected iteration %lld, got %lld", (long long)c->k_done, (long long)k);
     return ABFT_E_DIM;
@@ -1371,6 +1448,33 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
     if ((schemes ? schemes[k] : scheme) == ABFT_FULL) c->want_chol_rs = true;
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
+  c->in_stream = false;
+  if (c->in_host) {
+    // streamed input (as abft_factorize): every block column goes out now on
+    // st_in; Cholesky iterations wait for their own block, LU / QR for all
+    const bool chol = c->kind == ABFT_CHOLESKY;
+    for (int64_t j = (int64_t)c->ev_in.size(); j < c->nb; ++j) {
+      cudaEvent_t e = nullptr;
+      CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      c->ev_in.push_back(e);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+    CUDA_TRY(cudaStreamWaitEvent(c->st_in, c->ev_a, 0));
+    for (int64_t j = 0; j < c->nb; ++j) {
+      const int64_t p = j * c->b, w = std::min(c->b, c->n - p);
+      const int64_t r0 = chol ? p : 0;
+      CUDA_TRY(cudaMemcpy2DAsync(c->m + r0 + p * c->ld, c->ld * 4, c->in_host + r0 + p * c->in_ld,
+                                 c->in_ld * 4, (c->n - r0) * 4, w, cudaMemcpyHostToDevice, c->st_in));
+      CUDA_TRY(cudaEventRecord(c->ev_in[j], c->st_in));
+    }
+    c->in_host = nullptr;
+    if (chol) {
+      c->in_stream = true;
+      c->rs_enc.assign(c->nb, 0);
+    } else {
+      CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
+    }
+  }
   for (int64_t k = k0; k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
     c->next_scheme = (k + 1 < c->nb) ? (schemes ? schemes[k + 1] : scheme) : ABFT_NONE;
@@ -1383,9 +1487,11 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
     int rc = s_iteration(c, k, sch, plan ? plan + f0 : nullptr, f1 - f0, correct, false, true);
     if (rc) {
       cudaEventRecord(c->e1, c->st);
+      c->in_stream = false;
       return rc;
     }
   }
+  c->in_stream = false;
   if (c->out_host) {
     CUDA_TRY(cudaEventRecord(c->ev_out, c->st_out));
     CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_out, 0));
@@ -1449,6 +1555,7 @@ ABFT_API int abft_s_profile_read(abft_sctx* c, double* ms) {
 // tcgen05 GEMM (fp32 accuracy) and fp64 Frobenius sums. a0 == NULL: kept input.
 ABFT_API int abft_s_residual(abft_sctx* c, const float* a0h, int64_t lda, double* out) {
   SGuard g(c->device);
+  ABFT_TRY(s_flush_pending_input(c));
   if (c->k_done < c->nb) {
     set_last_error("factorization incomplete");
     return ABFT_E_INCOMPLETE;
@@ -1519,6 +1626,7 @@ ABFT_API int64_t abft_s_breakdown_column(abft_sctx* c) { return c->breakdown_col
 // row checksums) for the recompute recovery policy.
 ABFT_API int abft_s_snapshot(abft_sctx* c) {
   SGuard g(c->device);
+  ABFT_TRY(s_flush_pending_input(c));
   if (!c->snap_m) ABFT_TRY(salloc(&c->snap_m, c->ld * c->n, c->st));
   CUDA_TRY(cudaMemcpyAsync(c->snap_m, c->m, c->ld * c->n * 4, cudaMemcpyDeviceToDevice, c->st));
   if (c->chol_rs) {

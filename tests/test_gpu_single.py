@@ -207,3 +207,32 @@ def test_fp32_large_residual_bound(kind, bound):
     f.run_protected("none")
     res = f.residual(a)
     assert res <= bound, res
+
+
+@pytest.mark.parametrize("kind", ["cholesky", "lu"])
+def test_fp32_streamed_input_equals_set_matrix(kind):
+    """abft_s_set_matrix_streamed (block columns copied inside the call;
+    Cholesky: lower block triangle, per-iteration waits, FULL row checksums
+    built on arrival): same locations and factor as abft_s_set_matrix, with
+    the device matrix overwritten by junk first."""
+    import ctypes
+    n, b, seed = 1280, 128, 4
+    sched = {1: {"0d": 1}, 7: {"0d": 1}}
+    a = P.generate_test_matrix(kind, n, seed)
+    f1 = P.SFactorization(kind, a, b)
+    r1 = f1.run_protected("full", sched, np.random.default_rng(seed))
+    f2 = P.SFactorization(kind, a, b)
+    lib = f2._lib
+    fp = ctypes.POINTER(ctypes.c_float)
+    junk = np.asfortranarray(np.random.default_rng(2).standard_normal((n, n)), dtype=np.float32)
+    assert lib.abft_s_set_matrix(f2._ctx, junk.ctypes.data_as(fp), n) == 0
+    af = np.asfortranarray(a, dtype=np.float32)
+    assert lib.abft_s_set_matrix_streamed(f2._ctx, af.ctypes.data_as(fp), n) == 0
+    r2 = f2.run_protected("full", sched, np.random.default_rng(seed))
+    assert [r.locations for r in r1] == [r.locations for r in r2]
+    assert sum(len(r.locations) for r in r2) == 2
+    m1, m2 = f1.m, f2.m
+    if kind == "cholesky":
+        m1, m2 = np.tril(m1), np.tril(m2)
+        assert not np.any(np.triu(f2.m, 1))
+    np.testing.assert_allclose(m2, m1, rtol=0, atol=1e-6 * float(np.abs(m1).max()))
