@@ -149,6 +149,15 @@ struct abft_ctx {
   std::vector<cudaEvent_t> ev_in;
   std::vector<char> rs_enc;       // streamed Cholesky FULL: block column's row sums added
   double* rs_tmp = nullptr;       // n: fresh row sums of one block column
+  // streamed LU input: block columns [0, lu_split b) are factored left-looking
+  // in chunks of lu_chunk block columns as they arrive (lu_stream_chunks);
+  // L11^{-1} of every panel is kept for the late PU of the next chunks
+  int lu_chunk = -1;              // ABFT_LU_STREAM_CHUNK (0: wait for the whole input; -1: nb / 8)
+  int64_t lu_split = -1;          // ABFT_LU_STREAM_SPLIT (block columns; -1: 3 nb / 8)
+  int lu_rchunk = 0;              // right part's catch-up chunks (0: all of it at once)
+  double* linv_store = nullptr;   // nb x (ld_t x b)
+  double* el_store = nullptr;     // nb x (ld_cs x b): block-row sums of each L panel
+  std::vector<char> el_ok;
   // profiling
   struct ProfPair {
     int cat;
@@ -842,6 +851,27 @@ int verify_sub(abft_ctx* c, int scheme, int correct, int64_t r0, int64_t c0, int
   return 0;
 }
 
+// Diagonal-factor kernel of PD(k+1) under the LU look-ahead of iteration k
+// (and the SMs kept from the update for it). A long update hides the
+// one-CTA factor on 2 free SMs; once the update gets short (late iterations)
+// the multi-CTA factor (b/32 SMs, ~2x faster) is worth the SMs it takes.
+bool lu_la_fast_diag(const abft_ctx* c, int64_t k, int* keep_out) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t rows = n - pe, cols = n - pe, wa = std::min<int64_t>(c->b, cols);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const double upd_s = 2.0 * (double)rows * (double)(cols - wa) * (double)w / (30.0e12 * (sms - 2) / 148.0);
+  const int nbd = (int)((c->b + 31) / 32);
+  bool fast_diag = c->lu_coop && upd_s < 1.0e-3;
+  int keep = fast_diag ? nbd : 2;
+  if ((int64_t)c->side_sms.size() > k + 1 && c->side_sms[k + 1] > 0) {
+    keep = std::max(1, std::min((int)c->side_sms[k + 1], sms / 2));
+    fast_diag = keep >= nbd;
+  }
+  if (keep_out) *keep_out = keep;
+  return fast_diag;
+}
+
 // LU protected trailing update with look-ahead (fault-free iterations of the
 // one-call path): the next panel's block column is updated and verified
 // first, then its diagonal block is factored on a side stream (2 SMs left
@@ -876,19 +906,11 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
     ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
     prof_mark(c, PROF_ABFT, false);
   }
-  // side stream: diagonal block of panel k+1. A long update hides the one-CTA
-  // factor on 2 free SMs; once the update gets short (late iterations) the
-  // multi-CTA factor (b/32 SMs, ~2x faster) is worth the SMs it takes.
+  // side stream: diagonal block of panel k+1 (lu_la_fast_diag)
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
-  const double upd_s = 2.0 * (double)rows * (double)(cols - wa) * (double)w / (30.0e12 * (sms - 2) / 148.0);
-  const int nbd = (int)((c->b + 31) / 32);
-  bool fast_diag = c->lu_coop && upd_s < 1.0e-3;
-  int keep = fast_diag ? nbd : 2;
-  if ((int64_t)c->side_sms.size() > k + 1 && c->side_sms[k + 1] > 0) {
-    keep = std::max(1, std::min((int)c->side_sms[k + 1], sms / 2));
-    fast_diag = keep >= nbd;
-  }
+  int keep = 2;
+  const bool fast_diag = lu_la_fast_diag(c, k, &keep);
   CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
   prof_mark_side(c, true, (int32_t)(k + 1));
@@ -923,6 +945,239 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   prof_mark(c, PROF_PD, false);
   ABFT_TRY(emit_column(c, k + 1));
   c->pd_ready = k + 1;
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Streamed LU input. Right-looking LU touches every column in iteration 0, so
+// the input cannot be consumed block column by block column in iteration
+// order. Instead the left part [0, split b) is processed chunk by chunk as it
+// arrives: a chunk first receives the updates of every earlier panel (PU(k)
+// and the protected TMU(k) restricted to its columns, k in increasing order),
+// then its own panels are factored with the updates restricted to it. Every
+// block sees the same sequence of K = b updates, encodes, maintenances and
+// verifies as in the iteration-ordered schedule (_protected_tmu,
+// simulator.py:124-167, restricted to a block-column window -- checksums,
+// maintenance and verify are per b x b block), so factor and reports are the
+// same. The right part [split b, n) catches up once the whole input is in;
+// iterations split.. then run the ordinary (look-ahead) schedule. Used only
+// while no fault is planned before iteration `split` (a fault's magnitude
+// depends on max|region| over all columns of that iteration).
+
+// PU(k) restricted to columns [cs, ce): U12 = L11^{-1} A12 with the kept L11^{-1}.
+int lu_pu_win(abft_ctx* c, int64_t k, int64_t cs, int64_t ce) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  cs = std::max(cs, pe);
+  if (cs >= ce) return 0;
+  const double* linv = c->linv_store + k * c->ld_t * c->b;
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(ce - cs), (int)w, 1.0, linv, c->ld_t,
+                c->m + p + cs * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, &c->gws));
+  return copy_matrix(c->st, c->uw, c->ld_t, c->m + p + cs * c->ld, c->ld, w, ce - cs);
+}
+
+// maintain() of LU iteration k for the region columns [cs, ce): writes the
+// window's part of the region-local maintained sums (csm, rsm).
+int lu_maintain_win(abft_ctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t rows,
+                    int64_t cs, int64_t ce) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t cw = ce - cs, cbeg = cs - c0, j0 = cbeg / c->b;
+  const int64_t nbr = (rows + c->b - 1) / c->b, nbw = (cw + c->b - 1) / c->b;
+  SumOut enc = sums_for(c, r0, cs, scheme == ABFT_FULL);
+  const double* L = c->m + pe + p * c->ld;
+  const double* R = c->m + p + cs * c->ld;
+  // E_L of panel k: one pass per panel, kept for every window of iteration k
+  double* el = c->el_store + k * c->ld_cs * c->b;
+  if (!c->el_ok[k]) {
+    Region rl{const_cast<double*>(L), c->ld, rows, w, c->b};
+    SumOut o;
+    o.cp = el;
+    o.cp_ld = c->ld_cs;
+    o.cp_step = 2;
+    o.cw = el + 1;
+    o.cw_ld = c->ld_cs;
+    o.cw_step = 2;
+    ABFT_TRY(blocksum(c->st, rl, o));
+    c->el_ok[k] = 1;
+  }
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cw, (int)w, -1.0, el, c->ld_cs, R, c->ld,
+                1.0, enc.cp, c->ld_cs, c->csm + cbeg * c->ld_cs, c->ld_cs, &c->gws));
+  if (scheme == ABFT_FULL) {
+    Region rr{const_cast<double*>(R), c->ld, w, cw, c->b};
+    SumOut o;
+    o.rp = c->er;
+    o.rp_ld = c->ld_t;
+    ABFT_TRY(blocksum(c->st, rr, o));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbw, (int)w, -1.0, L, c->ld, c->er, c->ld_t,
+                  1.0, enc.rp, c->ld, c->rsm + j0 * c->ld, c->ld, &c->gws));
+  }
+  return 0;
+}
+
+// Does the iteration-ordered schedule run iteration k (fault-free) with the
+// LU look-ahead (run_iteration_device)?
+bool lu_la_applies(const abft_ctx* c, int64_t k) {
+  const int64_t pe = std::min((k + 1) * c->b, c->n);
+  return c->lookahead_enabled && pe < c->n && c->fuse_enabled && gemm_can_fuse((int)c->b) &&
+         !c->pivot;
+}
+
+// The protected TMU(k) of LU restricted to region columns [cs, ce). `encode`:
+// the window's blocks were not verified by iteration k-1 (first update of the
+// window, or an unprotected k-1), so their checksums come from a pass.
+int lu_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int64_t ce,
+               bool encode) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  cs = std::max(cs, c0);
+  ce = std::min(ce, c0 + cols);
+  if (cs >= ce || rows <= 0) return 0;
+  const int64_t cw = ce - cs, j0 = (cs - c0) / c->b, ncb = (cw + c->b - 1) / c->b;
+  const bool prot = scheme != ABFT_NONE;
+  Region wreg{c->m + r0 + cs * c->ld, c->ld, rows, cw, c->b};
+  const double* L21 = c->m + pe + p * c->ld;
+  const double* U12 = c->m + p + cs * c->ld;
+  double* A22 = c->m + r0 + cs * c->ld;
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    if (encode) ABFT_TRY(blocksum(c->st, wreg, sums_for(c, r0, cs, true)));
+    ABFT_TRY(lu_maintain_win(c, k, scheme, r0, c0, rows, cs, ce));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  // the iteration-ordered schedule's kernels per block column: its look-ahead
+  // (lu_la_applies) updates block column k+1 with the plain GEMM + a pass and
+  // verifies it first, factors the diagonal block of panel k+1 on the side
+  // stream (lu_la_fast_diag) beside the rest of the update, then L21
+  const bool fuse = prot && c->fuse_enabled && gemm_can_fuse((int)c->b);
+  const bool la = lu_la_applies(c, k) && cs == c0;
+  if (!la) {
+    prof_mark(c, PROF_TMU, true);
+    if (fuse)
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)cw, (int)w, -1.0, L21, c->ld, U12,
+                               c->ld, 1.0, A22, c->ld, A22, c->ld, (int)c->b, fused_for(c, r0, cs)));
+    else
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)cw, (int)w, -1.0, L21, c->ld, U12, c->ld,
+                    1.0, A22, c->ld, A22, c->ld, &c->gws));
+    prof_mark(c, PROF_TMU, false);
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      if (!fuse) ABFT_TRY(blocksum(c->st, wreg, sums_for(c, r0, cs, true)));
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, j0, ncb));
+      prof_mark(c, PROF_ABFT, false);
+    }
+    return 0;
+  }
+  const int64_t wa = std::min<int64_t>(c->b, cw);
+  prof_mark(c, PROF_TMU, true);
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, L21, c->ld, U12, c->ld, 1.0,
+                A22, c->ld, A22, c->ld, &c->gws));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    Region ra{A22, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, cs, true)));
+    ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  int keep = 2;
+  const bool fast_diag = lu_la_fast_diag(c, k, &keep);
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  prof_mark_side(c, true, (int32_t)(k + 1));
+  ABFT_TRY(lu_diag(c, c->st2, k + 1, fast_diag));
+  prof_mark_side(c, false, (int32_t)(k + 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  if (cw > wa) {
+    prof_mark(c, PROF_TMU, true);
+    if (prot)
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cw - wa), (int)w, -1.0, L21,
+                               c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
+                               A22 + wa * c->ld, c->ld, (int)c->b, fused_for(c, r0, cs + wa),
+                               sms - keep));
+    else
+      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cw - wa), (int)w, -1.0, L21,
+                             c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
+                             A22 + wa * c->ld, c->ld, sms - keep));
+    prof_mark(c, PROF_TMU, false);
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 1, ncb - 1));
+      prof_mark(c, PROF_ABFT, false);
+    }
+  }
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  c->cur_iter = (int32_t)(k + 1);
+  prof_mark(c, PROF_PD, true);
+  ABFT_TRY(lu_l21(c, k + 1));
+  prof_mark(c, PROF_PD, false);
+  ABFT_TRY(emit_column(c, k + 1));
+  c->pd_ready = k + 1;
+  return 0;
+}
+
+// Block columns of the streamed LU's left part (0: not used for this call).
+// Defaults measured on dgetrf N = 32768 b = 256 (nb = 128; e2e ms, H2D of
+// 8.6 GB at ~50 GB/s): wait-for-all 1022, chunk 16 / split 48 902, split 32
+// 946, split 64 914, chunk 8 906, chunk 32 922 (profiles/lu_stream_r02.txt).
+int lu_stream_chunk(const abft_ctx* c) {
+  return c->lu_chunk >= 0 ? c->lu_chunk : (int)std::max<int64_t>(1, c->nb / 8);
+}
+
+int64_t lu_stream_split(const abft_ctx* c) {
+  if (c->kind != ABFT_LU || c->pivot || lu_stream_chunk(c) <= 0 || c->nb < 4) return 0;
+  int64_t s = c->lu_split >= 0 ? c->lu_split : 3 * c->nb / 8;
+  return std::max<int64_t>(1, std::min(s, c->nb - 1));
+}
+
+// Iterations 0..split-1 of a streamed LU (see above); returns with the
+// matrix in the state of the iteration-ordered schedule after TMU(split-1).
+int lu_stream_chunks(abft_ctx* c, int64_t split, int scheme, const int32_t* schemes, int correct) {
+  const int64_t b = c->b, n = c->n;
+  auto sch = [&](int64_t k) { return schemes ? schemes[k] : scheme; };
+  if (!c->linv_store) ABFT_TRY(dalloc(&c->linv_store, c->ld_t * b * c->nb));
+  if (!c->el_store) ABFT_TRY(dalloc(&c->el_store, c->ld_cs * b * c->nb));
+  c->el_ok.assign(c->nb, 0);
+  c->pd_ready = -1;
+  auto run = [&](int64_t k, int64_t cs, int64_t ce) -> int {
+    c->cur_iter = (int32_t)k;
+    prof_mark(c, PROF_PU, true);
+    ABFT_TRY(lu_pu_win(c, k, cs, ce));
+    prof_mark(c, PROF_PU, false);
+    const bool enc = k == 0 || sch(k - 1) == ABFT_NONE;
+    return lu_tmu_win(c, k, sch(k), correct, cs, ce, enc);
+  };
+  // the first chunk is a quarter of the others: the GPU starts early
+  const int64_t chunk = lu_stream_chunk(c), first = std::max<int64_t>(1, chunk / 4);
+  for (int64_t q0 = 0, q1 = 0; q0 < split; q0 = q1) {
+    q1 = std::min<int64_t>(q0 + (q0 == 0 ? first : chunk), split);
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));
+    for (int64_t k = 0; k < q1; ++k) {
+      if (k >= q0) {
+        c->cur_iter = (int32_t)k;
+        if (c->pd_ready != k) {  // else formed by the look-ahead of TMU(k-1)
+          prof_mark(c, PROF_PD, true);
+          ABFT_TRY(task_pd(c, k));
+          prof_mark(c, PROF_PD, false);
+          ABFT_TRY(emit_column(c, k));
+        }
+        c->pd_ready = -1;
+        ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t,
+                             b, b));
+      }
+      ABFT_TRY(run(k, q0 * b, q1 * b));
+    }
+  }
+  // the right part: every earlier panel's update, chunk by chunk as it arrives
+  const int64_t rch = c->lu_rchunk > 0 ? c->lu_rchunk : c->nb;
+  for (int64_t q0 = split; q0 < c->nb; q0 += rch) {
+    const int64_t q1 = std::min<int64_t>(q0 + rch, c->nb);
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));
+    for (int64_t k = 0; k < split; ++k) ABFT_TRY(run(k, q0 * b, std::min(q1 * b, n)));
+  }
+  c->sums_valid = sch(split - 1) != ABFT_NONE;
+  // pd_ready == split when the look-ahead of TMU(split-1) formed PD(split)
   return 0;
 }
 
@@ -1238,6 +1493,10 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     if (e5) c->lu_coop = e5[0] == '1';
     const char* e4 = getenv("ABFT_CHOL_CLUSTER");
     if (e4) c->chol_cluster = e4[0] == '1';
+    const char* e6 = getenv("ABFT_LU_STREAM_CHUNK");
+    if (e6) c->lu_chunk = atoi(e6);
+    const char* e7 = getenv("ABFT_LU_STREAM_SPLIT");
+    if (e7) c->lu_split = atoll(e7);
     const char* e3 = getenv("ABFT_QR_LA_SMS");
     if (e3) {
       c->qr_la_sms = atoi(e3);  // 0 disables the QR look-ahead
@@ -1340,7 +1599,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
                     c->el,    c->er,     c->lw,     c->uw,      c->linv,  c->uinv, c->vstore,
                     c->tstore, c->betas, c->qr_part, c->qr_rowbuf, c->gram, c->ww,  c->mid,
                     c->qr_part2, c->qr_wfin, c->qr_small,
-                    c->scratch, c->gws.ptr, c->gws2.ptr};
+                    c->scratch, c->gws.ptr, c->gws2.ptr, c->linv_store, c->el_store};
   for (double* p : bufs)
     if (p) cudaFree(p);
   if (c->ev) cudaFree(c->ev);
@@ -1562,6 +1821,7 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
   c->in_stream = false;
+  int64_t lu_split = 0;  // streamed LU: iterations [0, lu_split) ran chunk by chunk
   if (c->in_host) {
     // streamed input: every column block goes out now on st_in (in order);
     // Cholesky iterations wait for their own block, LU / QR for all of them
@@ -1587,10 +1847,22 @@ ABFT_API int abft_factorize(abft_ctx* c, int scheme, const int32_t* schemes, con
       c->in_stream = true;
       c->rs_enc.assign(c->nb, 0);
     } else {
-      CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
+      // LU: chunked left part while the input arrives, if no fault is planned there
+      lu_split = k0 == 0 ? lu_stream_split(c) : 0;
+      if (plan && plan_iter)
+        for (int f = 0; f < nplan; ++f)
+          if (plan_iter[f] < lu_split) lu_split = 0;
+      if (lu_split == 0) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
     }
   }
-  for (int64_t k = k0; k < c->nb; ++k) {
+  if (lu_split > 0) {
+    int rc = lu_stream_chunks(c, lu_split, scheme, schemes, correct);
+    if (rc != 0) {
+      cudaEventRecord(c->e1, c->st);
+      return rc;
+    }
+  }
+  for (int64_t k = std::max(k0, lu_split); k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
     int f0 = 0, f1 = 0;
     if (plan && plan_iter) {
@@ -1744,6 +2016,17 @@ ABFT_API int abft_profile_read_iters(abft_ctx* c, double* out, int64_t nb) {
 // LU: >= ceil(b/32) selects the multi-CTA diagonal factor). 0 or a null
 // array: the built-in choice. The B200 form of the reference's slack
 // reclamation (scheduler.py:84-146): the stream with slack gets fewer SMs.
+ABFT_API int abft_set_lu_stream(abft_ctx* c, int chunk, int64_t split, int right_chunk) {
+  if (chunk < -1 || split < -1 || right_chunk < 0) {
+    set_last_error("abft_set_lu_stream: chunk >= -1, split >= -1, right_chunk >= 0");
+    return ABFT_E_INVALID;
+  }
+  c->lu_chunk = chunk;
+  c->lu_split = split;
+  c->lu_rchunk = right_chunk;
+  return 0;
+}
+
 ABFT_API int abft_set_side_sms(abft_ctx* c, const int32_t* sms, int64_t nb) {
   if (!sms || nb <= 0) {
     c->side_sms.clear();
