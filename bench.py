@@ -651,20 +651,17 @@ def run_e2e(arm, args):
     pinned_out = torch.empty((n, n), dtype=torch.float64, pin_memory=True).numpy().T
     torch.cuda.synchronize()
     # Cholesky streams the input in by block columns inside the factorization
-    # call (the lower block triangle it reads); LU streams all of it and
-    # factors its left half chunk by chunk as it arrives; QR needs all of it
-    # at k = 0
+    # call (the lower block triangle it reads); LU / QR stream all of it and
+    # factor the left 3/8 chunk by chunk as it arrives
     chol = args.kind == "cholesky"
-    streamed = args.kind in ("cholesky", "lu")
-    set_in = lib.abft_set_matrix_streamed if streamed else lib.abft_set_matrix
+    set_in = lib.abft_set_matrix_streamed
     h2d = 8 * n * n
     if chol:
         h2d = sum(8 * (n - j * args.b) * min(args.b, n - j * args.b) for j in range(-(-n // args.b)))
     times = []
     # the kept device copy of the input (residual / abft_reset) already holds
     # this matrix: the streamed set does not refresh it
-    if streamed:
-        P.linalg.check(lib.abft_keep_input(f._ctx, 0))
+    P.linalg.check(lib.abft_keep_input(f._ctx, 0))
     try:
         for i in range(1 + args.steps):
             t0 = time.perf_counter()
@@ -676,8 +673,7 @@ def run_e2e(arm, args):
             if i:
                 times.append(dt)
     finally:
-        if streamed:
-            P.linalg.check(lib.abft_keep_input(f._ctx, 1))
+        P.linalg.check(lib.abft_keep_input(f._ctx, 1))
     sec = statistics.median(times)
     return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 8 * n * n,
@@ -685,7 +681,7 @@ def run_e2e(arm, args):
             "api": ("abft_set_matrix_streamed (block columns H2D inside the call, lower block "
                     "triangle)" if chol else
                     "abft_set_matrix_streamed (block columns H2D inside the call; the left 3/8 "
-                    "factored chunk by chunk as it arrives)" if streamed else "abft_set_matrix") +
+                    "factored chunk by chunk as it arrives)") +
                    " + run_protected(out=pinned host; finished column blocks stream D2H on a "
                    "copy stream during the factorization)"}
 

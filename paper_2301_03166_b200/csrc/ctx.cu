@@ -152,8 +152,9 @@ struct abft_ctx {
   // streamed LU input: block columns [0, lu_split b) are factored left-looking
   // in chunks of lu_chunk block columns as they arrive (lu_stream_chunks);
   // L11^{-1} of every panel is kept for the late PU of the next chunks
-  int lu_chunk = -1;              // ABFT_LU_STREAM_CHUNK (0: wait for the whole input; -1: nb / 8)
-  int64_t lu_split = -1;          // ABFT_LU_STREAM_SPLIT (block columns; -1: 3 nb / 8)
+  int lu_chunk = -1;              // ABFT_STREAM_CHUNK (0: wait for the whole input; -1: LU nb / 8,
+                                  // QR 0 -- measured slower, see lu_stream_chunk)
+  int64_t lu_split = -1;          // ABFT_STREAM_SPLIT (block columns; -1: 3 nb / 8)
   int lu_rchunk = 0;              // right part's catch-up chunks (0: all of it at once)
   double* linv_store = nullptr;   // nb x (ld_t x b)
   double* el_store = nullptr;     // nb x (ld_cs x b): block-row sums of each L panel
@@ -1117,16 +1118,174 @@ int lu_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int6
   return 0;
 }
 
-// Block columns of the streamed LU's left part (0: not used for this call).
+// Block columns of the streamed LU / QR left part (0: not used for this call).
+int qr_panel_sms(const abft_ctx* c, int64_t k, int sms);
+
+// Does the iteration-ordered schedule run QR iteration k (fault-free) with
+// the QR look-ahead (run_iteration_device)?
+bool qr_la_applies(const abft_ctx* c, int64_t k) {
+  const int64_t pe = std::min((k + 1) * c->b, c->n);
+  return c->lookahead_enabled && pe < c->n && c->qr_la_sms > 0;
+}
+
+// The protected TMU(k) of QR restricted to region columns [cs, ce):
+// W = V^T C (with the full product's split-K partition), mid = T^T W,
+// maintenance from mid, C -= V mid with the look-ahead's kernels mirrored
+// (protected_tmu_qr_lookahead) when the window holds block column k+1.
+int qr_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int64_t ce,
+               bool encode) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  region_of(c, k, &r0, &c0, &rows, &cols);
+  cs = std::max(cs, c0);
+  ce = std::min(ce, c0 + cols);
+  if (cs >= ce || rows <= 0) return 0;
+  const int64_t cw = ce - cs, cbeg = cs - c0, j0 = cbeg / c->b, ncb = (cw + c->b - 1) / c->b;
+  const bool prot = scheme != ABFT_NONE;
+  Region wreg{c->m + r0 + cs * c->ld, c->ld, rows, cw, c->b};
+  const double* V = c->vstore + p + p * c->ld;
+  const double* T = c->tstore + k * c->b * c->ld_t;
+  double* C = c->m + p + cs * c->ld;
+  if (prot && encode) {
+    prof_mark(c, PROF_ABFT, true);
+    ABFT_TRY(blocksum(c->st, wreg, sums_for(c, r0, cs, true)));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  prof_mark(c, PROF_TMU, true);
+  const int spl = gemm_effective_splits((int)w, (int)cols, (int)rows, &c->gws);
+  ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)cw, (int)rows, 1.0, V, c->ld, C, c->ld, 0.0,
+                nullptr, 0, c->ww, c->ld_t, &c->gws, spl));
+  const int spl2 = gemm_effective_splits((int)w, (int)cols, (int)w, &c->gws);
+  ABFT_TRY(gemm(c->st, 'T', 'N', (int)w, (int)cw, (int)w, 1.0, T, c->ld_t, c->ww, c->ld_t, 0.0,
+                nullptr, 0, c->mid, c->ld_t, &c->gws, spl2));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    // maintain() for the window: E_L of V kept per panel, R = mid
+    prof_mark(c, PROF_ABFT, true);
+    const int64_t nbr = (rows + c->b - 1) / c->b;
+    SumOut enc = sums_for(c, r0, cs, scheme == ABFT_FULL);
+    double* el = c->el_store + k * c->ld_cs * c->b;
+    if (!c->el_ok[k]) {
+      Region rl{const_cast<double*>(V), c->ld, rows, w, c->b};
+      SumOut o;
+      o.cp = el;
+      o.cp_ld = c->ld_cs;
+      o.cp_step = 2;
+      o.cw = el + 1;
+      o.cw_ld = c->ld_cs;
+      o.cw_step = 2;
+      ABFT_TRY(blocksum(c->st, rl, o));
+      c->el_ok[k] = 1;
+    }
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cw, (int)w, -1.0, el, c->ld_cs, c->mid,
+                  c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm + cbeg * c->ld_cs, c->ld_cs, &c->gws,
+                  gemm_effective_splits((int)(2 * nbr), (int)cols, (int)w, &c->gws)));
+    if (scheme == ABFT_FULL) {
+      Region rr{c->mid, c->ld_t, w, cw, c->b};
+      SumOut o;
+      o.rp = c->er;
+      o.rp_ld = c->ld_t;
+      ABFT_TRY(blocksum(c->st, rr, o));
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)ncb, (int)w, -1.0, V, c->ld, c->er, c->ld_t,
+                    1.0, enc.rp, c->ld, c->rsm + j0 * c->ld, c->ld, &c->gws,
+                    gemm_effective_splits((int)rows, (int)((cols + c->b - 1) / c->b), (int)w,
+                                          &c->gws)));
+    }
+    prof_mark(c, PROF_ABFT, false);
+  }
+  const bool fuse = prot && c->fuse_enabled && gemm_can_fuse((int)c->b);
+  if (!(qr_la_applies(c, k) && cs == c0)) {
+    prof_mark(c, PROF_TMU, true);
+    if (fuse)
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)cw, (int)w, -1.0, V, c->ld,
+                               c->mid, c->ld_t, 1.0, C, c->ld, C, c->ld, (int)c->b,
+                               fused_for(c, r0, cs)));
+    else
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)cw, (int)w, -1.0, V, c->ld, c->mid, c->ld_t,
+                    1.0, C, c->ld, C, c->ld, &c->gws));
+    prof_mark(c, PROF_TMU, false);
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      if (!fuse) ABFT_TRY(blocksum(c->st, wreg, sums_for(c, r0, cs, true)));
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, j0, ncb));
+      prof_mark(c, PROF_ABFT, false);
+    }
+    return 0;
+  }
+  const int64_t wa = std::min<int64_t>(c->b, cw);
+  prof_mark(c, PROF_TMU, true);
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)wa, (int)w, -1.0, V, c->ld, c->mid, c->ld_t, 1.0,
+                C, c->ld, C, c->ld, &c->gws));
+  prof_mark(c, PROF_TMU, false);
+  if (prot) {
+    prof_mark(c, PROF_ABFT, true);
+    Region ra{C, c->ld, rows, wa, c->b};
+    ABFT_TRY(blocksum(c->st, ra, sums_for(c, r0, cs, true)));
+    ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 0, 1));
+    prof_mark(c, PROF_ABFT, false);
+  }
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+  const int res = qr_panel_sms(c, k, sms);
+  CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+  {
+    const int64_t p1 = pe, pe1 = std::min(p1 + c->b, n), w1 = pe1 - p1;
+    QrPanelWork q = c->qrw;
+    q.gws = &c->gws2;
+    prof_mark_side(c, true, (int32_t)(k + 1));
+    ABFT_TRY(qr_panel_factor(c->st2, c->m + p1 + p1 * c->ld, c->ld, n - p1, (int)w1,
+                             c->vstore + p1 + p1 * c->ld, c->ld,
+                             c->tstore + (k + 1) * c->b * c->ld_t, c->ld_t, c->betas, q, res));
+    prof_mark_side(c, false, (int32_t)(k + 1));
+  }
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  if (cw > wa) {
+    prof_mark(c, PROF_TMU, true);
+    const double* midb = c->mid + wa * c->ld_t;
+    double* Cb = C + wa * c->ld;
+    if (fuse) {
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cw - wa), (int)w, -1.0, V, c->ld,
+                               midb, c->ld_t, 1.0, Cb, c->ld, Cb, c->ld, (int)c->b,
+                               fused_for(c, r0, cs + wa), sms - res));
+      prof_mark(c, PROF_TMU, false);
+    } else {
+      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cw - wa), (int)w, -1.0, V, c->ld,
+                             midb, c->ld_t, 1.0, Cb, c->ld, Cb, c->ld, sms - res));
+      prof_mark(c, PROF_TMU, false);
+      if (prot) {
+        Region rb{Cb, c->ld, rows, cw - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, sums_for(c, r0, cs + wa, true)));
+      }
+    }
+    if (prot) {
+      prof_mark(c, PROF_ABFT, true);
+      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 1, ncb - 1));
+      prof_mark(c, PROF_ABFT, false);
+    }
+  }
+  CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+  c->qr_count = (int)(k + 2);
+  ABFT_TRY(emit_column(c, k + 1));
+  c->pd_ready = k + 1;
+  return 0;
+}
+
 // Defaults measured on dgetrf N = 32768 b = 256 (nb = 128; e2e ms, H2D of
 // 8.6 GB at ~50 GB/s): wait-for-all 1022, chunk 16 / split 48 902, split 32
 // 946, split 64 914, chunk 8 906, chunk 32 922 (profiles/lu_stream_r02.txt).
+// QR (same windows, qr_tmu_win; bit-identical too) is off unless a chunk is
+// set: each in-chunk panel runs beside only a window's update on the SMs the
+// look-ahead's model leaves it, so the panels serialise -- dgeqrf N = 32768
+// e2e 1742 ms waiting for the whole input, 1923 / 2058 / 2168 ms chunked with
+// split 32 / 48 / 64 (profiles/lu_stream_r02.txt).
 int lu_stream_chunk(const abft_ctx* c) {
-  return c->lu_chunk >= 0 ? c->lu_chunk : (int)std::max<int64_t>(1, c->nb / 8);
+  if (c->lu_chunk >= 0) return c->lu_chunk;
+  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 8) : 0;
 }
 
 int64_t lu_stream_split(const abft_ctx* c) {
-  if (c->kind != ABFT_LU || c->pivot || lu_stream_chunk(c) <= 0 || c->nb < 4) return 0;
+  if (c->kind == ABFT_CHOLESKY || c->pivot || lu_stream_chunk(c) <= 0 || c->nb < 4) return 0;
   int64_t s = c->lu_split >= 0 ? c->lu_split : 3 * c->nb / 8;
   return std::max<int64_t>(1, std::min(s, c->nb - 1));
 }
@@ -1136,16 +1295,18 @@ int64_t lu_stream_split(const abft_ctx* c) {
 int lu_stream_chunks(abft_ctx* c, int64_t split, int scheme, const int32_t* schemes, int correct) {
   const int64_t b = c->b, n = c->n;
   auto sch = [&](int64_t k) { return schemes ? schemes[k] : scheme; };
-  if (!c->linv_store) ABFT_TRY(dalloc(&c->linv_store, c->ld_t * b * c->nb));
+  if (c->kind == ABFT_LU && !c->linv_store) ABFT_TRY(dalloc(&c->linv_store, c->ld_t * b * c->nb));
   if (!c->el_store) ABFT_TRY(dalloc(&c->el_store, c->ld_cs * b * c->nb));
   c->el_ok.assign(c->nb, 0);
   c->pd_ready = -1;
+  const bool lu = c->kind == ABFT_LU;
   auto run = [&](int64_t k, int64_t cs, int64_t ce) -> int {
     c->cur_iter = (int32_t)k;
+    const bool enc = k == 0 || sch(k - 1) == ABFT_NONE;
+    if (!lu) return qr_tmu_win(c, k, sch(k), correct, cs, ce, enc);
     prof_mark(c, PROF_PU, true);
     ABFT_TRY(lu_pu_win(c, k, cs, ce));
     prof_mark(c, PROF_PU, false);
-    const bool enc = k == 0 || sch(k - 1) == ABFT_NONE;
     return lu_tmu_win(c, k, sch(k), correct, cs, ce, enc);
   };
   // the first chunk is a quarter of the others: the GPU starts early
@@ -1163,8 +1324,9 @@ int lu_stream_chunks(abft_ctx* c, int64_t split, int scheme, const int32_t* sche
           ABFT_TRY(emit_column(c, k));
         }
         c->pd_ready = -1;
-        ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t,
-                             b, b));
+        if (lu)
+          ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t,
+                               b, b));
       }
       ABFT_TRY(run(k, q0 * b, q1 * b));
     }
@@ -1493,9 +1655,9 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     if (e5) c->lu_coop = e5[0] == '1';
     const char* e4 = getenv("ABFT_CHOL_CLUSTER");
     if (e4) c->chol_cluster = e4[0] == '1';
-    const char* e6 = getenv("ABFT_LU_STREAM_CHUNK");
+    const char* e6 = getenv("ABFT_STREAM_CHUNK");
     if (e6) c->lu_chunk = atoi(e6);
-    const char* e7 = getenv("ABFT_LU_STREAM_SPLIT");
+    const char* e7 = getenv("ABFT_STREAM_SPLIT");
     if (e7) c->lu_split = atoll(e7);
     const char* e3 = getenv("ABFT_QR_LA_SMS");
     if (e3) {
@@ -2016,9 +2178,9 @@ ABFT_API int abft_profile_read_iters(abft_ctx* c, double* out, int64_t nb) {
 // LU: >= ceil(b/32) selects the multi-CTA diagonal factor). 0 or a null
 // array: the built-in choice. The B200 form of the reference's slack
 // reclamation (scheduler.py:84-146): the stream with slack gets fewer SMs.
-ABFT_API int abft_set_lu_stream(abft_ctx* c, int chunk, int64_t split, int right_chunk) {
+ABFT_API int abft_set_input_chunks(abft_ctx* c, int chunk, int64_t split, int right_chunk) {
   if (chunk < -1 || split < -1 || right_chunk < 0) {
-    set_last_error("abft_set_lu_stream: chunk >= -1, split >= -1, right_chunk >= 0");
+    set_last_error("abft_set_input_chunks: chunk >= -1, split >= -1, right_chunk >= 0");
     return ABFT_E_INVALID;
   }
   c->lu_chunk = chunk;

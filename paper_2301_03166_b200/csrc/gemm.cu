@@ -729,6 +729,34 @@ int gemm_splits_for(int M, int N, int K, int num_sms) {
   return best;
 }
 
+// The split-K factor gemm() uses for this shape (requested `splits` <= 0:
+// the wave model; then capped by the workspace), so a product computed in
+// column windows can reproduce the full product's K partition bit for bit.
+int gemm_effective_splits(int M, int N, int K, const GemmWorkspace* ws, int splits, int max_ctas) {
+  if (splits <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    // a capped launch (look-ahead side streams) deals its units over fewer CTAs
+    if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
+    splits = gemm_splits_for(M, N, K, sms);
+  }
+  int kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+  splits = (K + kps - 1) / kps;
+  const int64_t slice = (int64_t)M * N;
+  if (splits > 1 && (!ws || ws->ptr == nullptr || ws->elems < slice * splits)) {
+    const int64_t cap = (ws && ws->ptr) ? ws->elems / slice : 0;
+    if (cap >= 2) {
+      splits = static_cast<int>(cap < splits ? cap : splits);
+      kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
+      splits = (K + kps - 1) / kps;
+    } else {
+      splits = 1;
+    }
+  }
+  return splits;
+}
+
 static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,
                      const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
                      const double* C, int64_t ldc, double* D, int64_t ldd, GemmWorkspace* ws,
@@ -745,33 +773,10 @@ static int gemm_impl(cudaStream_t st, char ta, char tb, int M, int N, int K, dou
   const bool AT = (ta == 'T' || ta == 't');
   const bool BT = (tb == 'T' || tb == 't');
   if (fs) splits = 1;
-  if (splits <= 0) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    // a capped launch (look-ahead side streams) deals its units over fewer CTAs
-    if (max_ctas > 0 && max_ctas < sms) sms = max_ctas;
-    splits = gemm_splits_for(M, N, K, sms);
-  }
-  int kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
-  splits = (K + kps - 1) / kps;
+  splits = gemm_effective_splits(M, N, K, ws, splits, max_ctas);
+  const int kps = splits > 1 ? ((K + splits - 1) / splits + BK - 1) / BK * BK : K;
   const int64_t ldw = M;
   const int64_t slice = ldw * N;
-  if (splits > 1) {
-    if (!ws || ws->ptr == nullptr || ws->elems < slice * splits) {
-      const int64_t cap = (ws && ws->ptr) ? ws->elems / slice : 0;
-      if (cap >= 2) {
-        splits = static_cast<int>(cap < splits ? cap : splits);
-        kps = ((K + splits - 1) / splits + BK - 1) / BK * BK;
-        splits = (K + kps - 1) / kps;
-      } else {
-        splits = 1;
-        kps = K;
-      }
-    }
-  } else {
-    kps = K;
-  }
 
   // three warpgroups (64x64 tiles) for short-K products such as the rank-b
   // trailing updates, two (128x64 tiles) for long K

@@ -47,6 +47,9 @@ int gemm_fused_sums(cudaStream_t st, char ta, char tb, int M, int N, int K, doub
                     const double* C, int64_t ldc, double* D, int64_t ldd, int fb,
                     const FusedSums& sums, int max_ctas = 0);
 bool gemm_can_fuse(int fb);
+// split-K factor gemm() would use for this shape and workspace
+int gemm_effective_splits(int M, int N, int K, const GemmWorkspace* ws, int splits = 0,
+                          int max_ctas = 0);
 
 // gemm() (split-K allowed) on at most max_ctas SMs per launch
 int gemm_capped(cudaStream_t st, char ta, char tb, int M, int N, int K, double alpha,

@@ -133,10 +133,11 @@ def test_streamed_input_equals_set_matrix(kind, n, b):
 
 @pytest.mark.parametrize("n,b,chunk,split", [(2048, 128, 3, 8), (2048, 128, 2, -1), (1300, 256, 1, 3),
                                              (1408, 128, 4, 10), (2048, 256, 8, -1),
-                                             (4096, 128, -1, -1)])
+                                             (4096, 128, -1, -1), (2048, 128, 0, -1)])
 @pytest.mark.parametrize("schemes", ["full", "single", "mixed"])
-def test_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, b, chunk, split, schemes):
-    """Streamed LU input: block columns [0, split b) are factored chunk by
+@pytest.mark.parametrize("kind", ["lu", "qr"])
+def test_streamed_chunked_equals_set_matrix(monkeypatch, kind, n, b, chunk, split, schemes):
+    """Streamed LU / QR input: block columns [0, split b) are factored chunk by
     chunk (left-looking over chunks) while the input arrives, the rest after
     a catch-up. Every block sees the same update / checksum sequence as the
     iteration-ordered schedule, so the factor is bit-identical and the
@@ -145,19 +146,19 @@ def test_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, b, chunk, split, 
     schemes put unprotected iterations inside the chunked part (their
     successors re-encode)."""
     import ctypes
-    monkeypatch.setenv("ABFT_LU_STREAM_CHUNK", str(chunk))
-    monkeypatch.setenv("ABFT_LU_STREAM_SPLIT", str(split))
+    monkeypatch.setenv("ABFT_STREAM_CHUNK", str(chunk))
+    monkeypatch.setenv("ABFT_STREAM_SPLIT", str(split))
     nb = -(-n // b)
     sp = 3 * nb // 8 if split < 0 else min(split, nb - 1)
     sched = {sp: {P.ErrorKind.D0: 1}, nb - 2: {P.ErrorKind.D0: 1, P.ErrorKind.D1: 1}}
     cyc = ["full", "none", "single", "full", "none", "none", "single"]
     sch_list = ([cyc[k % len(cyc)] for k in range(nb)] if schemes == "mixed" else None)
     scheme = "full" if schemes == "mixed" else schemes
-    a = P.generate_test_matrix("lu", n, 7)
-    f1 = P.Factorization("lu", a, b)
+    a = P.generate_test_matrix(kind, n, 7)
+    f1 = P.Factorization(kind, a, b)
     ref = [report_json(r) for r in P.run_protected(f1, scheme, sched, np.random.default_rng(7),
                                                    schemes=sch_list)]
-    f2 = P.Factorization("lu", a, b)
+    f2 = P.Factorization(kind, a, b)
     lib = f2._lib
     junk = np.asfortranarray(np.random.default_rng(1).standard_normal((n, n)) * 1e3)
     assert lib.abft_set_matrix(f2._ctx, junk.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n) == 0
@@ -172,3 +173,8 @@ def test_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, b, chunk, split, 
         assert sum(len(r["locations"]) for r in got) >= 1
     assert np.array_equal(f2.m, f1.m)
     assert np.array_equal(out, f1.m)
+    if kind == "qr":  # the compact-WY panels too
+        assert len(f2.qr_t) == len(f1.qr_t) == nb
+        for k in range(nb):
+            assert np.array_equal(f2.qr_t[k], f1.qr_t[k])
+            assert np.array_equal(f2._qr_vs[k], f1._qr_vs[k])

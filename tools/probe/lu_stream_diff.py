@@ -3,13 +3,15 @@ import ctypes, os, sys
 import numpy as np
 import paper_2301_03166_b200 as P
 
+KIND = sys.argv[1] if len(sys.argv) > 1 else "lu"
+
 n, b = 2048, 128
 nb = n // b
 
 
 def run(streamed, sched, scheme="full"):
-    a = P.generate_test_matrix("lu", n, 7)
-    f = P.Factorization("lu", a, b)
+    a = P.generate_test_matrix(KIND, n, 7)
+    f = P.Factorization(KIND, a, b)
     if streamed:
         af = np.asfortranarray(a)
         assert f._lib.abft_set_matrix_streamed(f._ctx, af.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), n) == 0
