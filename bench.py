@@ -695,12 +695,13 @@ def run_e2e_s(arm, args):
     src = pinned_in.T
     pinned_out = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy().T
     chol = args.kind == "cholesky"  # streamed input, as run_e2e
-    set_in = arm.lib.abft_s_set_matrix_streamed if chol else arm.lib.abft_s_set_matrix
+    streamed = args.kind in ("cholesky", "lu")
+    set_in = arm.lib.abft_s_set_matrix_streamed if streamed else arm.lib.abft_s_set_matrix
     h2d = 4 * n * n
     if chol:
         h2d = sum(4 * (n - j * args.b) * min(args.b, n - j * args.b) for j in range(-(-n // args.b)))
     times = []
-    if chol:
+    if streamed:
         arm.P.linalg.check(arm.lib.abft_s_keep_input(f._ctx, 0))
     try:
         for i in range(1 + args.steps):
@@ -711,14 +712,16 @@ def run_e2e_s(arm, args):
             if i:
                 times.append(time.perf_counter() - t0)
     finally:
-        if chol:
+        if streamed:
             arm.P.linalg.check(arm.lib.abft_s_keep_input(f._ctx, 1))
     sec = statistics.median(times)
     return {"value": FLOPS[args.kind](n) / sec / 1e12, "unit": "TFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4 * n * n,
             "ms_per_step": sec * 1e3,
             "api": ("abft_s_set_matrix_streamed (block columns H2D inside the call, lower block "
-                    "triangle)" if chol else "abft_s_set_matrix") +
+                    "triangle)" if chol else
+                    "abft_s_set_matrix_streamed (block columns H2D inside the call; the left 1/4 "
+                    "factored chunk by chunk as it arrives)" if streamed else "abft_s_set_matrix") +
                    " + SFactorization.run_protected(out=pinned host; column blocks stream D2H "
                    "during the factorization)"}
 

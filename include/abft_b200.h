@@ -310,6 +310,9 @@ ABFT_API int abft_set_qr_panel(abft_ctx* ctx, int64_t k, const double* V, int64_
  * The reference has no fp32 path (parity unpinned). */
 typedef struct abft_sctx abft_sctx;
 ABFT_API int abft_s_create(abft_sctx** ctx, int kind, int64_t n, int64_t b, int device);
+/* streamed fp32 input: as abft_set_input_chunks (sgetrf; built-in chunk and split
+ * n_blocks / 4; QR is not chunked in fp32) */
+ABFT_API int abft_s_set_input_chunks(abft_sctx* ctx, int chunk, int64_t split, int right_chunk);
 ABFT_API int abft_s_destroy(abft_sctx* ctx);
 ABFT_API void* abft_s_stream(abft_sctx* ctx);
 ABFT_API int64_t abft_s_k_done(abft_sctx* ctx);

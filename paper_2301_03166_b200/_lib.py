@@ -99,6 +99,7 @@ SIGNATURES = [
     ("abft_profile_read_iters", _I, [_P, _D, _I64]),
     ("abft_set_side_sms", _I, [_P, ctypes.POINTER(ctypes.c_int32), _I64]),
     ("abft_set_input_chunks", _I, [_P, _I, _I64, _I]),
+    ("abft_s_set_input_chunks", _I, [_P, _I, _I64, _I]),
     ("abft_set_pivoting", _I, [_P, _I]),
     ("abft_get_pivots", _I, [_P, ctypes.POINTER(ctypes.c_int32)]),
     ("abft_probe_dmma_peak", _I, [_I, _D]),

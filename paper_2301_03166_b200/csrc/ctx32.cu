@@ -165,6 +165,13 @@ struct abft_sctx {
   bool fuse_enabled = true;
   bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
   int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  // streamed LU input (as ctx.cu's lu_stream_chunks): the left `lu_split`
+  // block columns are factored chunk by chunk as they arrive
+  int lu_chunk = -1;              // ABFT_STREAM_CHUNK (0: wait for all; -1: nb / 4)
+  int64_t lu_split = -1;          // ABFT_STREAM_SPLIT (-1: nb / 4)
+  int lu_rchunk = 0;
+  float* linv_store = nullptr;    // nb x (ld_t x b): L11^{-1} of every panel
+  double* el_store = nullptr;     // nb x (ld_cs x b): E_L of every panel
   int64_t chol_part = -1;         // Cholesky: panel already updated by panels 0..k-2
   bool chol_enc_ahead = false;    // ... and encoded before that update
   int next_scheme = 0;            // scheme of the next iteration (abft_s_factorize)
@@ -995,6 +1002,219 @@ int s_tmu_lu_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Streamed LU input, fp32 context: ctx.cu's lu_stream_chunks restated over
+// s_pu / s_maintain / s_tmu_lu_lookahead restricted to block-column windows.
+// Every block gets the same updates, operand sums (E_L from the L21
+// epilogue, R E_R from the PU epilogue) and kernels as in the
+// iteration-ordered schedule: factor and reports are bit-identical.
+
+// PU(k) for region columns [cs, ce) with the kept L11^{-1}; R E_R from the epilogue.
+int s_pu_win(abft_sctx* c, int64_t k, int64_t cs, int64_t ce) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  cs = std::max(cs, pe);
+  if (cs >= ce) return 0;
+  float* U12 = c->m + p + cs * c->ld;
+  FusedSums fs;
+  const bool fuse = c->fuse_enabled && c->b == 128 && w == 128;
+  if (fuse) {
+    fs.cp = c->uwd;  // column sums are not needed: scratch
+    fs.cp_ld = c->ld_t;
+    fs.cp_step = 1;
+    fs.cw = c->uwd + 1;
+    fs.cw_ld = c->ld_t;
+    fs.cw_step = 1;
+    fs.rp = c->er;
+    fs.rp_ld = c->ld_t;
+    fs.bm = c->scratch + 2048;
+    fs.bm_ld = 1;
+  }
+  ABFT_TRY(s_gemm(c, 'N', 'N', w, ce - cs, w, 1.0f, c->linv_store + k * c->ld_t * c->b, c->ld_t,
+                  U12, c->ld, 0.0f, nullptr, 0, c->uw, c->ld_t, fuse ? &fs : nullptr));
+  c->er_for = fuse ? k : -1;
+  return copy_matrix(c->st, c->uw, c->ld_t, U12, c->ld, w, ce - cs);
+}
+
+// s_maintain of LU iteration k for region columns [cs, ce) (E_L kept per panel).
+int s_maintain_win(abft_sctx* c, int64_t k, int scheme, int64_t r0, int64_t c0, int64_t rows,
+                   int64_t cs, int64_t ce) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  const int64_t cw = ce - cs, cbeg = cs - c0, j0 = cbeg / c->b;
+  const int64_t nbr = (rows + c->b - 1) / c->b, nbw = (cw + c->b - 1) / c->b;
+  SumOut enc = s_sums(c, r0, cs, scheme == ABFT_FULL);
+  const float* L = c->m + pe + p * c->ld;
+  const float* R = c->m + p + cs * c->ld;
+  const double* el = c->el_store + k * c->ld_cs * c->b;
+  ABFT_TRY(widen_matrix(c->st, R, c->ld, c->uwd, c->ld_t, w, cw));
+  ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cw, (int)w, -1.0, el, c->ld_cs, c->uwd,
+                c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm + cbeg * c->ld_cs, c->ld_cs, &c->gws));
+  if (scheme == ABFT_FULL) {
+    if (c->er_for != k) {
+      RegionF rr{const_cast<float*>(R), c->ld, w, cw, c->b};
+      SumOut o;
+      o.rp = c->er;
+      o.rp_ld = c->ld_t;
+      ABFT_TRY(blocksum(c->st, rr, o));
+    }
+    ABFT_TRY(widen_matrix(c->st, L, c->ld, c->lwd, c->ld, rows, w));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)nbw, (int)w, -1.0, c->lwd, c->ld, c->er, c->ld_t,
+                  1.0, enc.rp, c->ld, c->rsm + j0 * c->ld, c->ld, &c->gws));
+  }
+  return 0;
+}
+
+// Protected TMU(k) of LU for region columns [cs, ce); the look-ahead's
+// kernels (s_tmu_lu_lookahead) when the window holds block column k+1.
+int s_lu_tmu_win(abft_sctx* c, int64_t k, int scheme, int correct, int64_t cs, int64_t ce,
+                 bool encode) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  s_region(c, k, &r0, &c0, &rows, &cols);
+  cs = std::max(cs, c0);
+  ce = std::min(ce, c0 + cols);
+  if (cs >= ce || rows <= 0) return 0;
+  const int64_t cw = ce - cs, j0 = (cs - c0) / c->b, ncb = (cw + c->b - 1) / c->b;
+  const bool prot = scheme != ABFT_NONE;
+  RegionF wreg{c->m + r0 + cs * c->ld, c->ld, rows, cw, c->b};
+  const float* L21 = c->m + pe + p * c->ld;
+  const float* U12 = c->m + p + cs * c->ld;
+  float* A22 = c->m + r0 + cs * c->ld;
+  if (prot) {
+    smark(c, SP_ABFT, true);
+    if (encode) ABFT_TRY(blocksum(c->st, wreg, s_sums(c, r0, cs, true)));
+    ABFT_TRY(s_maintain_win(c, k, scheme, r0, c0, rows, cs, ce));
+    smark(c, SP_ABFT, false);
+  }
+  const bool fuse = prot && c->fuse_enabled && c->b == 128;
+  const bool la = c->lookahead_enabled && pe < n && cs == c0;
+  const int64_t wa = la ? std::min<int64_t>(c->b, cw) : 0;
+  if (la) {
+    FusedSums fsa;
+    if (fuse) fsa = s_fused(c, r0, cs);
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, wa, w, -1.0f, L21, c->ld, U12, c->ld, 1.0f, A22, c->ld, A22,
+                    c->ld, fuse ? &fsa : nullptr));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      if (!fuse) {
+        RegionF ra{A22, c->ld, rows, wa, c->b};
+        ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, cs, true)));
+      }
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 0, 1));
+      smark(c, SP_ABFT, false);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+    CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+    ABFT_TRY(s_lu_diag(c, c->st2, k + 1));
+    CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  }
+  if (cw > wa) {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
+    FusedSums fs;
+    if (fuse) fs = s_fused(c, r0, cs + wa);
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, cw - wa, w, -1.0f, L21, c->ld, U12 + wa * c->ld, c->ld,
+                    1.0f, A22 + wa * c->ld, c->ld, A22 + wa * c->ld, c->ld, fuse ? &fs : nullptr,
+                    la ? sms - (c->lu_coop ? (int)((c->b + 31) / 32) : 2) : 0));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      if (!fuse) {
+        RegionF rb{A22 + wa * c->ld, c->ld, rows, cw - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, s_sums(c, r0, cs + wa, true)));
+      }
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, j0 + (wa ? 1 : 0),
+                            ncb - (wa ? 1 : 0)));
+      smark(c, SP_ABFT, false);
+    }
+  }
+  if (la) {
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+    smark(c, SP_PD, true);
+    ABFT_TRY(s_lu_l21(c, k + 1));
+    smark(c, SP_PD, false);
+    ABFT_TRY(s_emit_column(c, k + 1));
+    c->pd_ready = k + 1;
+  }
+  return 0;
+}
+
+// Defaults nb / 4 and nb / 4 (sgetrf N = 16384 b = 128 e2e: wait-for-all 82.5 ms,
+// 32/32 77.9, 16/32 78.1, 12/24 79.6, 16/48 80.3, 16/16 81.1): the fp32
+// iterations are launch-latency bound, so every extra window costs more
+// than in fp64 and a short left part with few chunks wins.
+int s_stream_chunk(const abft_sctx* c) {
+  if (c->lu_chunk >= 0) return c->lu_chunk;
+  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 4) : 0;
+}
+
+int64_t s_stream_split(const abft_sctx* c) {
+  if (c->kind != ABFT_LU || s_stream_chunk(c) <= 0 || c->nb < 4) return 0;
+  const int64_t s = c->lu_split >= 0 ? c->lu_split : c->nb / 4;
+  return std::max<int64_t>(1, std::min(s, c->nb - 1));
+}
+
+int s_lu_stream_chunks(abft_sctx* c, int64_t split, int scheme, const int32_t* schemes,
+                       int correct) {
+  const int64_t b = c->b, n = c->n;
+  auto sch = [&](int64_t k) { return schemes ? schemes[k] : scheme; };
+  if (!c->linv_store) ABFT_TRY(salloc(&c->linv_store, c->ld_t * b * c->nb, c->st));
+  if (!c->el_store) ABFT_TRY(salloc(&c->el_store, c->ld_cs * b * c->nb, c->st));
+  c->pd_ready = -1;
+  auto run = [&](int64_t k, int64_t cs, int64_t ce) -> int {
+    const bool enc = k == 0 || sch(k - 1) == ABFT_NONE;
+    smark(c, SP_PU, true);
+    ABFT_TRY(s_pu_win(c, k, cs, ce));
+    smark(c, SP_PU, false);
+    return s_lu_tmu_win(c, k, sch(k), correct, cs, ce, enc);
+  };
+  const int64_t chunk = s_stream_chunk(c), first = std::max<int64_t>(1, chunk / 4);
+  for (int64_t q0 = 0, q1 = 0; q0 < split; q0 = q1) {
+    q1 = std::min<int64_t>(q0 + (q0 == 0 ? first : chunk), split);
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));
+    for (int64_t k = 0; k < q1; ++k) {
+      if (k >= q0) {
+        if (c->pd_ready != k) {  // else formed by the look-ahead of TMU(k-1)
+          smark(c, SP_PD, true);
+          ABFT_TRY(s_pd(c, k));
+          smark(c, SP_PD, false);
+          ABFT_TRY(s_emit_column(c, k));
+        }
+        c->pd_ready = -1;
+        const int64_t pe = std::min((k + 1) * b, n);
+        ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t, b, b));
+        // E_L of panel k as s_maintain would take it: the L21 epilogue's, else a pass
+        double* el = c->el_store + k * c->ld_cs * b;
+        const int64_t nbr = (n - pe + b - 1) / b;
+        if (c->el_for == k) {
+          ABFT_TRY(copy_matrix(c->st, c->el, c->ld_cs, el, c->ld_cs, 2 * nbr, b));
+        } else if (pe < n) {
+          RegionF rl{c->m + pe + k * b * c->ld, c->ld, n - pe, b, b};
+          SumOut o;
+          o.cp = el;
+          o.cp_ld = c->ld_cs;
+          o.cp_step = 2;
+          o.cw = el + 1;
+          o.cw_ld = c->ld_cs;
+          o.cw_step = 2;
+          ABFT_TRY(blocksum(c->st, rl, o));
+        }
+      }
+      ABFT_TRY(run(k, q0 * b, q1 * b));
+    }
+  }
+  const int64_t rch = c->lu_rchunk > 0 ? c->lu_rchunk : c->nb;
+  for (int64_t q0 = split; q0 < c->nb; q0 += rch) {
+    const int64_t q1 = std::min<int64_t>(q0 + rch, c->nb);
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));
+    for (int64_t k = 0; k < split; ++k) ABFT_TRY(run(k, q0 * b, std::min(q1 * b, n)));
+  }
+  c->sums_valid = sch(split - 1) != ABFT_NONE;
+  return 0;
+}
+
 int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int nplan, int correct,
                 bool sync_checks, bool lookahead = false) {
   auto pd = [&]() -> int {
@@ -1159,6 +1379,10 @@ ABFT_API int abft_s_create(abft_sctx** out, int kind, int64_t n, int64_t b, int 
     if (e4 && e4[0] == '0') c->chol_cluster = false;
     const char* e5 = getenv("ABFT_LU_COOP");
     if (e5) c->lu_coop = e5[0] == '1';
+    const char* e8 = getenv("ABFT_STREAM_CHUNK");
+    if (e8) c->lu_chunk = atoi(e8);
+    const char* e9 = getenv("ABFT_STREAM_SPLIT");
+    if (e9) c->lu_split = atoll(e9);
     const char* e6 = getenv("ABFT_QR_LA_SMS");
     if (e6) c->qr_la_sms = atoi(e6);
   }
@@ -1288,7 +1512,7 @@ ABFT_API int abft_s_destroy(abft_sctx* c) {
                   c->chol_rs, c->m,   c->a0,  c->gcsw, c->csm,  c->grs,     c->rsm,   c->gmax,
                   c->el,  c->er,  c->lwd,  c->uwd,  c->lw,      c->uw,    c->linv,
                   c->uinv, c->sws, c->lsh, c->lsl, c->scratch, c->gws.ptr, c->gws2.ptr, c->ev, c->counters, c->dirty,
-                  c->dplan, c->dlist, c->info};
+                  c->dplan, c->dlist, c->info, c->linv_store, c->el_store};
   for (void* p : bufs)
     if (p) cudaFree(p);
   for (auto& pe : c->prof_pending) {
@@ -1449,6 +1673,7 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
   CUDA_TRY(cudaEventRecord(c->e0, c->st));
   c->timed = true;
   c->in_stream = false;
+  int64_t lu_split = 0;  // streamed LU: iterations [0, lu_split) ran chunk by chunk
   if (c->in_host) {
     // streamed input (as abft_factorize): every block column goes out now on
     // st_in; Cholesky iterations wait for their own block, LU / QR for all
@@ -1472,10 +1697,21 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
       c->in_stream = true;
       c->rs_enc.assign(c->nb, 0);
     } else {
-      CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
+      lu_split = k0 == 0 ? s_stream_split(c) : 0;
+      if (plan && plan_iter)
+        for (int f = 0; f < nplan; ++f)
+          if (plan_iter[f] < lu_split) lu_split = 0;
+      if (lu_split == 0) CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[c->nb - 1], 0));
     }
   }
-  for (int64_t k = k0; k < c->nb; ++k) {
+  if (lu_split > 0) {
+    int rc = s_lu_stream_chunks(c, lu_split, scheme, schemes, correct);
+    if (rc) {
+      cudaEventRecord(c->e1, c->st);
+      return rc;
+    }
+  }
+  for (int64_t k = std::max(k0, lu_split); k < c->nb; ++k) {
     const int sch = schemes ? schemes[k] : scheme;
     c->next_scheme = (k + 1 < c->nb) ? (schemes ? schemes[k + 1] : scheme) : ABFT_NONE;
     int f0 = 0, f1 = 0;
@@ -1506,6 +1742,17 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
   ABFT_TRY(s_collect(c, &evs));
   s_fill(c, evs, k0, reports, locs, max_locs, n_locs);
   c->k_done = c->nb;
+  return 0;
+}
+
+ABFT_API int abft_s_set_input_chunks(abft_sctx* c, int chunk, int64_t split, int right_chunk) {
+  if (chunk < -1 || split < -1 || right_chunk < 0) {
+    set_last_error("abft_s_set_input_chunks: chunk >= -1, split >= -1, right_chunk >= 0");
+    return ABFT_E_INVALID;
+  }
+  c->lu_chunk = chunk;
+  c->lu_split = split;
+  c->lu_rchunk = right_chunk;
   return 0;
 }
 

@@ -236,3 +236,38 @@ def test_fp32_streamed_input_equals_set_matrix(kind):
         m1, m2 = np.tril(m1), np.tril(m2)
         assert not np.any(np.triu(f2.m, 1))
     np.testing.assert_allclose(m2, m1, rtol=0, atol=1e-6 * float(np.abs(m1).max()))
+
+
+@pytest.mark.parametrize("n,chunk,split", [(2048, 3, 7), (2048, -1, -1), (1280, 1, 3), (2048, 4, 15)])
+@pytest.mark.parametrize("schemes", ["full", "single", "mixed"])
+def test_fp32_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, chunk, split, schemes):
+    """Streamed sgetrf input: the left `split` block columns are factored
+    chunk by chunk (left-looking over chunks: PU + maintenance + fused update +
+    verify per window, the look-ahead's kernels mirrored) while the input
+    arrives. Factor bit-identical to abft_s_set_matrix and the same
+    locations; faults after `split`."""
+    import ctypes
+    monkeypatch.setenv("ABFT_STREAM_CHUNK", str(chunk))
+    monkeypatch.setenv("ABFT_STREAM_SPLIT", str(split))
+    b, seed = 128, 6
+    nb = n // b
+    sp = nb // 4 if split < 0 else min(split, nb - 2)
+    sched = {sp: {"0d": 1}, nb - 2: {"0d": 1}}
+    cyc = ["full", "none", "single", "full", "none", "none", "single"]
+    sch_list = [cyc[k % len(cyc)] for k in range(nb)] if schemes == "mixed" else None
+    scheme = "full" if schemes == "mixed" else schemes
+    a = P.generate_test_matrix("lu", n, seed)
+    f1 = P.SFactorization("lu", a, b)
+    r1 = f1.run_protected(scheme, sched, np.random.default_rng(seed), schemes=sch_list)
+    f2 = P.SFactorization("lu", a, b)
+    lib = f2._lib
+    fp = ctypes.POINTER(ctypes.c_float)
+    junk = np.asfortranarray(np.random.default_rng(2).standard_normal((n, n)), dtype=np.float32)
+    assert lib.abft_s_set_matrix(f2._ctx, junk.ctypes.data_as(fp), n) == 0
+    af = np.asfortranarray(a, dtype=np.float32)
+    assert lib.abft_s_set_matrix_streamed(f2._ctx, af.ctypes.data_as(fp), n) == 0
+    r2 = f2.run_protected(scheme, sched, np.random.default_rng(seed), schemes=sch_list)
+    assert [r.locations for r in r1] == [r.locations for r in r2]
+    if schemes != "mixed":
+        assert sum(len(r.locations) for r in r2) == len(sched)
+    assert np.array_equal(f2.m, f1.m)
