@@ -148,11 +148,11 @@ ABFT_DEVINL void emit(const EventSink& s, int bi, int bj, int seq, int kind, int
   const int slot = atomicAdd(s.count, 1);
   if (slot < s.capacity) {
     Event e;
-    e.bi = bi;
+    e.bi = bi + s.bi_base;
     e.bj = bj + s.bj_base;
     e.seq = seq;
     e.kind = kind;
-    e.row = row;
+    e.row = row + (int64_t)s.bi_base * s.b;
     e.col = col + (int64_t)s.bj_base * s.b;
     e.flag = flag;
     e.detected_kind = det;

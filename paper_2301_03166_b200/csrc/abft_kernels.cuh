@@ -71,6 +71,7 @@ struct EventSink {
   int32_t iter;
   int32_t bj_base = 0;  // block-column offset of a sub-region (event coordinates only)
   int64_t b = 0;        // block size, for the column offset bj_base * b
+  int32_t bi_base = 0;  // block-row offset of a sub-region (event coordinates only)
 };
 
 // K2: threshold, classify and repair (verify_correct + _handle_single/_full,

@@ -114,6 +114,11 @@ struct abft_ctx {
   bool want_chol_rs = false;      // abft_factorize: a later iteration uses FULL
   bool lookahead_enabled = true;  // ABFT_NO_LOOKAHEAD=1 disables
   int64_t pd_ready = -1;          // panel already factored by the look-ahead
+  int64_t pu_ready = -1;          // PU already applied by the LU look-ahead (depth 2)
+  bool lu_la2 = false;            // LU look-ahead also forms PU(k+1), L21(k+1) on the side
+                                  // stream beside the update (ABFT_LU_LA2=1). Off: measured
+                                  // slower (dgetrf N = 32768 845 -> 850 ms: the side chain's
+                                  // SMs cost the update more than the serial PU / L21 did)
   int64_t chol_part = -1;         // Cholesky: panel whose update from panels 0..k-2 is done
   bool chol_enc_ahead = false;    // ... and whose encode ran with it
   int next_scheme = 0;            // scheme of the next iteration (abft_factorize)
@@ -137,7 +142,7 @@ struct abft_ctx {
   cudaStream_t st_out = nullptr;
   cudaEvent_t ev_out = nullptr;
   cudaStream_t st2 = nullptr;     // side stream for look-ahead panels
-  cudaEvent_t ev_a = nullptr, ev_p = nullptr;
+  cudaEvent_t ev_a = nullptr, ev_p = nullptr, ev_r = nullptr;
   // streamed input (abft_set_matrix_streamed): the next abft_factorize call
   // copies the column blocks on st_in (Cholesky: only rows >= j b of block j,
   // the lower block triangle the algorithm reads) and each iteration waits
@@ -873,6 +878,32 @@ bool lu_la_fast_diag(const abft_ctx* c, int64_t k, int* keep_out) {
   return fast_diag;
 }
 
+// verify_sub restricted to block rows [i0, i0 + nrb) of the region.
+int verify_rows(abft_ctx* c, int scheme, int correct, int64_t r0, int64_t c0, int64_t rows,
+                int64_t cols, int64_t i0, int64_t nrb, int64_t j0, int64_t ncb) {
+  const int64_t rbeg = i0 * c->b, cbeg = j0 * c->b;
+  const int64_t rsub = std::min(rows - rbeg, nrb * c->b);
+  const int64_t csub = std::min(cols - cbeg, ncb * c->b);
+  if (csub <= 0 || rsub <= 0) return 0;
+  Region sub{c->m + r0 + rbeg + (c0 + cbeg) * c->ld, c->ld, rsub, csub, c->b};
+  SumOut rec = sums_for(c, r0 + rbeg, c0 + cbeg, true);
+  Maintained mt;
+  mt.cp = c->csm + 2 * i0 + cbeg * c->ld_cs;
+  mt.cp_ld = c->ld_cs;
+  mt.cp_step = 2;
+  mt.cw = mt.cp + 1;
+  mt.cw_ld = c->ld_cs;
+  mt.cw_step = 2;
+  mt.rp = c->rsm + rbeg + j0 * c->ld;
+  mt.rp_ld = c->ld;
+  EventSink sink{c->ev,          c->counters,    c->ev_cap,  c->dirty,
+                 c->counters + 1, c->dirty_cap,  c->cur_iter, (int32_t)j0, c->b, (int32_t)i0};
+  ABFT_TRY(verify_blocks(c->st, sub, c->b, scheme, correct, rec, mt, sink));
+  ABFT_TRY(blocksum(c->st, sub, rec, c->dirty, c->counters + 1, c->dirty_cap));
+  CUDA_TRY(cudaMemsetAsync(c->counters + 1, 0, sizeof(int32_t), c->st));
+  return 0;
+}
+
 // LU protected trailing update with look-ahead (fault-free iterations of the
 // one-call path): the next panel's block column is updated and verified
 // first, then its diagonal block is factored on a side stream (2 SMs left
@@ -912,40 +943,83 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device);
   int keep = 2;
   const bool fast_diag = lu_la_fast_diag(c, k, &keep);
+  const int64_t pe1 = std::min(pe + c->b, n), w1 = pe1 - pe;
+  // depth 2 (lu_la2): the side stream also forms L21(k+1) and, once block row
+  // k+1 is updated and verified, PU(k+1) -- both only read blocks the rest of
+  // the update does not touch -- on SMs sized from the flop ratio
+  const bool la2 = c->lu_la2 && cols > wa && rows > c->b && pe1 < n;
+  if (la2) {
+    const double side = 4.0 * (double)(n - pe1) * (double)w1 * (double)w1;
+    const double upd = 2.0 * (double)(rows - c->b) * (double)(cols - wa) * (double)w;
+    const int ks = (int)std::ceil((double)sms * side / (side + upd)) + 1;
+    keep = std::max(keep, std::min(ks, sms / 2));
+  }
   CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
   prof_mark_side(c, true, (int32_t)(k + 1));
   ABFT_TRY(lu_diag(c, c->st2, k + 1, fast_diag));
-  prof_mark_side(c, false, (int32_t)(k + 1));
-  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
-  // (b) the rest of the trailing matrix with fused checksums
-  if (cols > wa) {
+  if (la2) {
+    // L21(k+1) = A21 U11^{-1} (lu_l21 on the side stream)
+    ABFT_TRY(gemm_reserved(c->st2, 'N', 'N', (int)(n - pe1), (int)w1, (int)w1, 1.0,
+                           c->m + pe1 + pe * c->ld, c->ld, c->uinv, c->ld_t, 0.0, nullptr, 0,
+                           c->lw, c->ld, keep));
+    ABFT_TRY(copy_matrix(c->st2, c->lw, c->ld, c->m + pe1 + pe * c->ld, c->ld, n - pe1, w1));
+  }
+  if (!la2) prof_mark_side(c, false, (int32_t)(k + 1));
+  if (!la2) CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  auto rest = [&](int64_t rb, int64_t nr) -> int {  // rows [rb, rb + nr) x columns [wa, cols)
+    const int64_t rr = std::min(rows - rb, nr);
+    if (rr <= 0 || cols <= wa) return 0;
     prof_mark(c, PROF_TMU, true);
     if (prot) {
-      FusedSums fs = fused_for(c, r0, c0 + wa);
-      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
-                               c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
-                               A22 + wa * c->ld, c->ld, (int)c->b, fs, sms - keep));
+      FusedSums fs = fused_for(c, r0 + rb, c0 + wa);
+      ABFT_TRY(gemm_fused_sums(c->st, 'N', 'N', (int)rr, (int)(cols - wa), (int)w, -1.0,
+                               L21 + rb, c->ld, U12 + wa * c->ld, c->ld, 1.0,
+                               A22 + rb + wa * c->ld, c->ld, A22 + rb + wa * c->ld, c->ld,
+                               (int)c->b, fs, sms - keep));
     } else {
-      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rows, (int)(cols - wa), (int)w, -1.0, L21,
-                             c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + wa * c->ld, c->ld,
-                             A22 + wa * c->ld, c->ld, sms - keep));
+      ABFT_TRY(gemm_reserved(c->st, 'N', 'N', (int)rr, (int)(cols - wa), (int)w, -1.0, L21 + rb,
+                             c->ld, U12 + wa * c->ld, c->ld, 1.0, A22 + rb + wa * c->ld, c->ld,
+                             A22 + rb + wa * c->ld, c->ld, sms - keep));
     }
     prof_mark(c, PROF_TMU, false);
     if (prot) {
       prof_mark(c, PROF_ABFT, true);
-      ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, 1, (cols + c->b - 1) / c->b));
+      ABFT_TRY(verify_rows(c, scheme, correct, r0, c0, rows, cols, rb / c->b,
+                           (rr + c->b - 1) / c->b, 1, (cols + c->b - 1) / c->b));
       prof_mark(c, PROF_ABFT, false);
     }
+    return 0;
+  };
+  if (!la2) {
+    // (b) the rest of the trailing matrix with fused checksums
+    ABFT_TRY(rest(0, rows));
+    c->sums_valid = prot;
+    // join, then L21 of panel k+1 on the main stream
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+    prof_mark(c, PROF_PD, true);
+    ABFT_TRY(lu_l21(c, k + 1));
+    prof_mark(c, PROF_PD, false);
+    ABFT_TRY(emit_column(c, k + 1));
+    c->pd_ready = k + 1;
+    return 0;
   }
+  // (b1) block row k+1 of the rest, verified; then PU(k+1) on the side stream
+  ABFT_TRY(rest(0, c->b));
+  CUDA_TRY(cudaEventRecord(c->ev_r, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_r, 0));
+  ABFT_TRY(gemm_reserved(c->st2, 'N', 'N', (int)w1, (int)(n - pe1), (int)w1, 1.0, c->linv, c->ld_t,
+                         c->m + pe + pe1 * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, keep));
+  ABFT_TRY(copy_matrix(c->st2, c->uw, c->ld_t, c->m + pe + pe1 * c->ld, c->ld, w1, n - pe1));
+  prof_mark_side(c, false, (int32_t)(k + 1));
+  CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  // (b2) the rows below
+  ABFT_TRY(rest(c->b, rows));
   c->sums_valid = prot;
-  // join, then L21 of panel k+1 on the main stream
   CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
-  prof_mark(c, PROF_PD, true);
-  ABFT_TRY(lu_l21(c, k + 1));
-  prof_mark(c, PROF_PD, false);
   ABFT_TRY(emit_column(c, k + 1));
   c->pd_ready = k + 1;
+  c->pu_ready = k + 1;
   return 0;
 }
 
@@ -1299,6 +1373,7 @@ int lu_stream_chunks(abft_ctx* c, int64_t split, int scheme, const int32_t* sche
   if (!c->el_store) ABFT_TRY(dalloc(&c->el_store, c->ld_cs * b * c->nb));
   c->el_ok.assign(c->nb, 0);
   c->pd_ready = -1;
+  c->pu_ready = -1;
   const bool lu = c->kind == ABFT_LU;
   auto run = [&](int64_t k, int64_t cs, int64_t ce) -> int {
     c->cur_iter = (int32_t)k;
@@ -1494,6 +1569,10 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
     return 0;
   };
   auto pu = [&]() -> int {
+    if (c->pu_ready == k) {  // applied by the previous iteration's look-ahead
+      c->pu_ready = -1;
+      return 0;
+    }
     prof_mark(c, PROF_PU, true);
     ABFT_TRY(task_pu(c, k));
     prof_mark(c, PROF_PU, false);
@@ -1653,6 +1732,8 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
     c->lookahead_enabled = !(e2 && e2[0] == '1');
     const char* e5 = getenv("ABFT_LU_COOP");
     if (e5) c->lu_coop = e5[0] == '1';
+    const char* e10 = getenv("ABFT_LU_LA2");
+    if (e10) c->lu_la2 = e10[0] == '1';
     const char* e4 = getenv("ABFT_CHOL_CLUSTER");
     if (e4) c->chol_cluster = e4[0] == '1';
     const char* e6 = getenv("ABFT_STREAM_CHUNK");
@@ -1746,6 +1827,7 @@ ABFT_API int abft_create(abft_ctx** out, int kind, int64_t n, int64_t b, int dev
   cudaEventCreateWithFlags(&c->ev_out, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_p, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_r, cudaEventDisableTiming);
   if (cudaDeviceSynchronize() != cudaSuccess) return fail(-1000);
   *out = c;
   return 0;
@@ -1798,6 +1880,7 @@ ABFT_API int abft_destroy(abft_ctx* c) {
   if (c->ev_out) cudaEventDestroy(c->ev_out);
   if (c->ev_a) cudaEventDestroy(c->ev_a);
   if (c->ev_p) cudaEventDestroy(c->ev_p);
+  if (c->ev_r) cudaEventDestroy(c->ev_r);
   if (c->e0) cudaEventDestroy(c->e0);
   if (c->e1) cudaEventDestroy(c->e1);
   if (c->st) cudaStreamDestroy(c->st);
@@ -1825,6 +1908,7 @@ ABFT_API int abft_set_matrix(abft_ctx* c, const double* a, int64_t lda) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->pu_ready = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
@@ -1853,6 +1937,7 @@ ABFT_API int abft_set_matrix_streamed(abft_ctx* c, const double* a, int64_t lda)
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->pu_ready = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
@@ -1874,6 +1959,7 @@ ABFT_API int abft_reset(abft_ctx* c) {
   c->qr_count = 0;
   c->breakdown_col = -1;
   c->pd_ready = -1;
+  c->pu_ready = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   c->chol_rs_valid = false;
@@ -2290,6 +2376,7 @@ ABFT_API int abft_restore(abft_ctx* c, int slot) {
   c->qr_count = s.qr_count;
   c->sums_valid = false;
   c->pd_ready = -1;
+  c->pu_ready = -1;
   c->chol_part = -1;
   c->chol_enc_ahead = false;
   CUDA_TRY(cudaStreamSynchronize(c->st));

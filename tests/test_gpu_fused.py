@@ -100,6 +100,29 @@ def test_lookahead_fast_path_equals_per_iteration(kind, n, b):
         assert r2 < 1e-14
 
 
+@pytest.mark.parametrize("n,b", [(2048, 256), (1408, 128), (1300, 256)])
+@pytest.mark.parametrize("scheme", ["full", "single", "none"])
+def test_lu_lookahead_depth2_equals_depth1(monkeypatch, n, b, scheme):
+    """ABFT_LU_LA2=1 (off by default, measured slower): the look-ahead also
+    forms L21(k+1) and -- after block row k+1 of the update is verified --
+    PU(k+1) on the side stream, the rest of the update split into that block
+    row and the rows below (events with a block-row offset). Same reports,
+    bit-identical factor."""
+    nb = -(-n // b)
+    sched = {2: {P.ErrorKind.D0: 1}, nb - 3: {P.ErrorKind.D0: 1, P.ErrorKind.D1: 1}}
+    a = P.generate_test_matrix("lu", n, 11)
+    out = []
+    for la2 in ("0", "1"):
+        monkeypatch.setenv("ABFT_LU_LA2", la2)
+        f = P.Factorization("lu", a, b)
+        reps = [report_json(r) for r in P.run_protected(f, scheme, sched, np.random.default_rng(11))]
+        out.append((reps, f.m))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+    if scheme != "none":
+        assert sum(len(r["locations"]) for r in out[1][0]) >= 2
+
+
 @pytest.mark.parametrize("kind", ["cholesky", "lu", "qr"])
 @pytest.mark.parametrize("n,b", [(2048, 256), (1300, 256), (1408, 128)])
 def test_streamed_input_equals_set_matrix(kind, n, b):
