@@ -680,8 +680,10 @@ def run_e2e(arm, args):
             "ms_per_step": sec * 1e3,
             "api": ("abft_set_matrix_streamed (block columns H2D inside the call, lower block "
                     "triangle)" if chol else
-                    "abft_set_matrix_streamed (block columns H2D inside the call; the left 3/8 "
-                    "factored chunk by chunk as it arrives)") +
+                    "abft_set_matrix_streamed (block columns H2D inside the call; " +
+                    ("the left 3/8 factored chunk by chunk as it arrives)" if args.kind == "lu" else
+                     "panels 0-2 factored as their block columns arrive, the rest updated in "
+                     "n/8-wide pieces as they arrive)")) +
                    " + run_protected(out=pinned host; finished column blocks stream D2H on a "
                    "copy stream during the factorization)"}
 

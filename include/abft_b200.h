@@ -217,11 +217,12 @@ ABFT_API int abft_set_side_sms(abft_ctx* ctx, const int32_t* sms, int64_t nb);
 /* streamed input of LU / QR (abft_set_matrix_streamed): block columns
  * [0, split b) are factored chunk by chunk (`chunk` block columns each,
  * left-looking over the chunks) while the input arrives; the rest receives
- * their updates once it is in (in `right_chunk` block-column pieces as they
- * arrive; 0 = all at once). chunk = 0 waits for the whole input; chunk = -1
- * is the built-in n_blocks / 8 for LU and 0 for QR (measured slower), split
- * = -1 is 3 n_blocks / 8. Same factor and reports either way. Used only when
- * no fault is planned before iteration `split`. */
+ * their updates as it arrives, in `right_chunk` block-column pieces (0: all
+ * at once). chunk = 0 waits for the whole input. -1 = built-in: LU chunk
+ * n_blocks / 8, split 3 n_blocks / 8, right part at once; QR chunk 1, split
+ * 3, right_chunk n_blocks / 8 (its panels serialise inside chunks). Same
+ * factor and reports either way. Used only when no fault is planned before
+ * iteration `split`. */
 ABFT_API int abft_set_input_chunks(abft_ctx* ctx, int chunk, int64_t split, int right_chunk);
 /* FP64 DMMA issue-rate probe (TFLOP/s) over all SMs: the roofline denominator */
 ABFT_API int abft_probe_dmma_peak(int iters, double* tflops);

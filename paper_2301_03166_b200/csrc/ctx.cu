@@ -160,7 +160,8 @@ struct abft_ctx {
   int lu_chunk = -1;              // ABFT_STREAM_CHUNK (0: wait for the whole input; -1: LU nb / 8,
                                   // QR 0 -- measured slower, see lu_stream_chunk)
   int64_t lu_split = -1;          // ABFT_STREAM_SPLIT (block columns; -1: 3 nb / 8)
-  int lu_rchunk = 0;              // right part's catch-up chunks (0: all of it at once)
+  int lu_rchunk = -1;             // right part's catch-up chunks (0: all of it at once;
+                                  // -1: LU 0, QR nb / 8)
   double* linv_store = nullptr;   // nb x (ld_t x b)
   double* el_store = nullptr;     // nb x (ld_cs x b): block-row sums of each L panel
   std::vector<char> el_ok;
@@ -1348,20 +1349,28 @@ int qr_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int6
 // Defaults measured on dgetrf N = 32768 b = 256 (nb = 128; e2e ms, H2D of
 // 8.6 GB at ~50 GB/s): wait-for-all 1022, chunk 16 / split 48 902, split 32
 // 946, split 64 914, chunk 8 906, chunk 32 922 (profiles/lu_stream_r02.txt).
-// QR (same windows, qr_tmu_win; bit-identical too) is off unless a chunk is
-// set: each in-chunk panel runs beside only a window's update on the SMs the
-// look-ahead's model leaves it, so the panels serialise -- dgeqrf N = 32768
-// e2e 1742 ms waiting for the whole input, 1923 / 2058 / 2168 ms chunked with
-// split 32 / 48 / 64 (profiles/lu_stream_r02.txt).
+// QR (same windows, qr_tmu_win; bit-identical too) keeps the chunked part
+// short: each in-chunk panel runs beside only a window's update on the SMs
+// the look-ahead's model leaves it, so the panels serialise. dgeqrf N = 32768
+// e2e: wait-for-all 1748 ms; split 32 / 48 / 64 (chunk 16) 1923 / 2058 /
+// 2168 ms; split 3 with 1-block chunks and the right part in nb/8 pieces as
+// it arrives 1653 ms (split 1 / 2 / 4 / 6 / 8: 1713 / 1684 / 1669 / 1723 /
+// 1777; profiles/lu_stream_r02.txt).
 int lu_stream_chunk(const abft_ctx* c) {
   if (c->lu_chunk >= 0) return c->lu_chunk;
-  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 8) : 0;
+  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 8) : 1;
 }
 
 int64_t lu_stream_split(const abft_ctx* c) {
   if (c->kind == ABFT_CHOLESKY || c->pivot || lu_stream_chunk(c) <= 0 || c->nb < 4) return 0;
-  int64_t s = c->lu_split >= 0 ? c->lu_split : 3 * c->nb / 8;
+  int64_t s = c->lu_split >= 0 ? c->lu_split : (c->kind == ABFT_LU ? 3 * c->nb / 8 : 3);
   return std::max<int64_t>(1, std::min(s, c->nb - 1));
+}
+
+int64_t lu_stream_rchunk(const abft_ctx* c) {
+  if (c->lu_rchunk > 0) return c->lu_rchunk;
+  if (c->lu_rchunk == 0 || c->kind == ABFT_LU) return c->nb;
+  return std::max<int64_t>(1, c->nb / 8);
 }
 
 // Iterations 0..split-1 of a streamed LU (see above); returns with the
@@ -1407,7 +1416,7 @@ int lu_stream_chunks(abft_ctx* c, int64_t split, int scheme, const int32_t* sche
     }
   }
   // the right part: every earlier panel's update, chunk by chunk as it arrives
-  const int64_t rch = c->lu_rchunk > 0 ? c->lu_rchunk : c->nb;
+  const int64_t rch = lu_stream_rchunk(c);
   for (int64_t q0 = split; q0 < c->nb; q0 += rch) {
     const int64_t q1 = std::min<int64_t>(q0 + rch, c->nb);
     CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));
@@ -2265,8 +2274,8 @@ ABFT_API int abft_profile_read_iters(abft_ctx* c, double* out, int64_t nb) {
 // array: the built-in choice. The B200 form of the reference's slack
 // reclamation (scheduler.py:84-146): the stream with slack gets fewer SMs.
 ABFT_API int abft_set_input_chunks(abft_ctx* c, int chunk, int64_t split, int right_chunk) {
-  if (chunk < -1 || split < -1 || right_chunk < 0) {
-    set_last_error("abft_set_input_chunks: chunk >= -1, split >= -1, right_chunk >= 0");
+  if (chunk < -1 || split < -1 || right_chunk < -1) {
+    set_last_error("abft_set_input_chunks: chunk, split, right_chunk >= -1");
     return ABFT_E_INVALID;
   }
   c->lu_chunk = chunk;

@@ -1746,8 +1746,8 @@ ABFT_API int abft_s_factorize(abft_sctx* c, int scheme, const int32_t* schemes, 
 }
 
 ABFT_API int abft_s_set_input_chunks(abft_sctx* c, int chunk, int64_t split, int right_chunk) {
-  if (chunk < -1 || split < -1 || right_chunk < 0) {
-    set_last_error("abft_s_set_input_chunks: chunk >= -1, split >= -1, right_chunk >= 0");
+  if (chunk < -1 || split < -1 || right_chunk < -1) {
+    set_last_error("abft_s_set_input_chunks: chunk, split, right_chunk >= -1");
     return ABFT_E_INVALID;
   }
   c->lu_chunk = chunk;
