@@ -697,8 +697,8 @@ def run_e2e_s(arm, args):
     src = pinned_in.T
     pinned_out = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy().T
     chol = args.kind == "cholesky"  # streamed input, as run_e2e
-    streamed = args.kind in ("cholesky", "lu")
-    set_in = arm.lib.abft_s_set_matrix_streamed if streamed else arm.lib.abft_s_set_matrix
+    streamed = True
+    set_in = arm.lib.abft_s_set_matrix_streamed
     h2d = 4 * n * n
     if chol:
         h2d = sum(4 * (n - j * args.b) * min(args.b, n - j * args.b) for j in range(-(-n // args.b)))
@@ -722,8 +722,10 @@ def run_e2e_s(arm, args):
             "ms_per_step": sec * 1e3,
             "api": ("abft_s_set_matrix_streamed (block columns H2D inside the call, lower block "
                     "triangle)" if chol else
-                    "abft_s_set_matrix_streamed (block columns H2D inside the call; the left 1/4 "
-                    "factored chunk by chunk as it arrives)" if streamed else "abft_s_set_matrix") +
+                    "abft_s_set_matrix_streamed (block columns H2D inside the call; " +
+                    ("the left 1/4 factored chunk by chunk as it arrives)" if args.kind == "lu" else
+                     "panels 0-2 factored as their block columns arrive, the rest updated in "
+                     "n/8-wide pieces as they arrive)")) +
                    " + SFactorization.run_protected(out=pinned host; column blocks stream D2H "
                    "during the factorization)"}
 

@@ -169,9 +169,10 @@ struct abft_sctx {
   // block columns are factored chunk by chunk as they arrive
   int lu_chunk = -1;              // ABFT_STREAM_CHUNK (0: wait for all; -1: nb / 4)
   int64_t lu_split = -1;          // ABFT_STREAM_SPLIT (-1: nb / 4)
-  int lu_rchunk = 0;
+  int lu_rchunk = -1;             // right part's pieces (0: at once; -1: LU 0, QR nb / 8)
   float* linv_store = nullptr;    // nb x (ld_t x b): L11^{-1} of every panel
   double* el_store = nullptr;     // nb x (ld_cs x b): E_L of every panel
+  std::vector<char> el_ok;        // QR windows: E_L of panel k already in el_store
   int64_t chol_part = -1;         // Cholesky: panel already updated by panels 0..k-2
   bool chol_enc_ahead = false;    // ... and encoded before that update
   int next_scheme = 0;            // scheme of the next iteration (abft_s_factorize)
@@ -292,12 +293,16 @@ void s_gemm_plan(int sms, int64_t M, int64_t N, int64_t K, int64_t kchunk, bool 
 int s_gemm(abft_sctx* c, char ta, char tb, int64_t M, int64_t N, int64_t K, float alpha,
            const float* A, int64_t lda, const float* B, int64_t ldb, float beta, const float* C,
            int64_t ldc, float* D, int64_t ldd, const FusedSums* fs = nullptr, int max_ctas = 0,
-           int64_t kchunk = S_KCHUNK) {
+           int64_t kchunk = S_KCHUNK, int force_splits = 0) {
   if (M <= 0 || N <= 0 || K <= 0) return 0;
   int splits;
   int64_t need;
   s_gemm_plan(max_ctas > 0 ? std::min(max_ctas, c->sms) : c->sms, M, N, K, kchunk, fs != nullptr,
               &splits, &need);
+  if (force_splits > 0 && !fs) {  // a column window of a wider product: its K partition
+    splits = force_splits;
+    need = sgemm_workspace_elems((int)M, (int)N, (int)(splits > 1 ? K : std::min(K, kchunk)), splits);
+  }
   if (need > c->sws_elems) {
     CUDA_TRY(cudaStreamSynchronize(c->st));
     if (c->sws) cudaFree(c->sws);
@@ -1145,14 +1150,130 @@ int s_lu_tmu_win(abft_sctx* c, int64_t k, int scheme, int correct, int64_t cs, i
 // 32/32 77.9, 16/32 78.1, 12/24 79.6, 16/48 80.3, 16/16 81.1): the fp32
 // iterations are launch-latency bound, so every extra window costs more
 // than in fp64 and a short left part with few chunks wins.
+// Protected TMU(k) of QR for region columns [cs, ce) (ctx.cu's qr_tmu_win in
+// fp32): W = V^T C with the full product's K partition, mid = T^T W, the
+// window's maintenance, C -= V mid with s_tmu_qr_lookahead's kernels when the
+// window holds block column k+1.
+int s_qr_tmu_win(abft_sctx* c, int64_t k, int scheme, int correct, int64_t cs, int64_t ce,
+                 bool encode) {
+  const int64_t n = c->n, p = k * c->b, pe = std::min(p + c->b, n), w = pe - p;
+  int64_t r0, c0, rows, cols;
+  s_region(c, k, &r0, &c0, &rows, &cols);
+  cs = std::max(cs, c0);
+  ce = std::min(ce, c0 + cols);
+  if (cs >= ce || rows <= 0) return 0;
+  const int64_t cw = ce - cs, cbeg = cs - c0, j0 = cbeg / c->b, ncb = (cw + c->b - 1) / c->b;
+  const bool prot = scheme != ABFT_NONE;
+  RegionF wreg{c->m + r0 + cs * c->ld, c->ld, rows, cw, c->b};
+  const float* V = c->vstore + p + p * c->ld;
+  const float* T = c->tstore + k * c->b * c->ld_t;
+  float* C = c->m + p + cs * c->ld;
+  if (prot && encode) {
+    smark(c, SP_ABFT, true);
+    ABFT_TRY(blocksum(c->st, wreg, s_sums(c, r0, cs, true)));
+    smark(c, SP_ABFT, false);
+  }
+  int spl = 1, spl2 = 1;
+  int64_t need = 0;
+  s_gemm_plan(c->sms, w, cols, rows, S_KCHUNK, false, &spl, &need);
+  s_gemm_plan(c->sms, w, cols, w, S_KCHUNK, false, &spl2, &need);
+  smark(c, SP_TMU, true);
+  ABFT_TRY(s_gemm(c, 'T', 'N', w, cw, rows, 1.0f, V, c->ld, C, c->ld, 0.0f, nullptr, 0, c->ww,
+                  c->ld_t, nullptr, 0, S_KCHUNK, spl));
+  ABFT_TRY(s_gemm(c, 'T', 'N', w, cw, w, 1.0f, T, c->ld_t, c->ww, c->ld_t, 0.0f, nullptr, 0, c->mid,
+                  c->ld_t, nullptr, 0, S_KCHUNK, spl2));
+  smark(c, SP_TMU, false);
+  if (prot) {
+    // s_maintain for the window (E_L of V kept per panel, R = mid)
+    smark(c, SP_ABFT, true);
+    const int64_t nbr = (rows + c->b - 1) / c->b;
+    SumOut enc = s_sums(c, r0, cs, scheme == ABFT_FULL);
+    double* el = c->el_store + k * c->ld_cs * c->b;
+    if (!c->el_ok[k]) {
+      RegionF rl{const_cast<float*>(V), c->ld, rows, w, c->b};
+      SumOut o;
+      o.cp = el;
+      o.cp_ld = c->ld_cs;
+      o.cp_step = 2;
+      o.cw = el + 1;
+      o.cw_ld = c->ld_cs;
+      o.cw_step = 2;
+      ABFT_TRY(blocksum(c->st, rl, o));
+      c->el_ok[k] = 1;
+    }
+    ABFT_TRY(widen_matrix(c->st, c->mid, c->ld_t, c->uwd, c->ld_t, w, cw));
+    ABFT_TRY(gemm(c->st, 'N', 'N', (int)(2 * nbr), (int)cw, (int)w, -1.0, el, c->ld_cs, c->uwd,
+                  c->ld_t, 1.0, enc.cp, c->ld_cs, c->csm + cbeg * c->ld_cs, c->ld_cs, &c->gws));
+    if (scheme == ABFT_FULL) {
+      RegionF rr{c->mid, c->ld_t, w, cw, c->b};
+      SumOut o;
+      o.rp = c->er;
+      o.rp_ld = c->ld_t;
+      ABFT_TRY(blocksum(c->st, rr, o));
+      ABFT_TRY(widen_matrix(c->st, V, c->ld, c->lwd, c->ld, rows, w));
+      ABFT_TRY(gemm(c->st, 'N', 'N', (int)rows, (int)ncb, (int)w, -1.0, c->lwd, c->ld, c->er,
+                    c->ld_t, 1.0, enc.rp, c->ld, c->rsm + j0 * c->ld, c->ld, &c->gws));
+    }
+    smark(c, SP_ABFT, false);
+  }
+  const bool fuse = prot && c->fuse_enabled && c->b == 128;
+  const bool la = c->lookahead_enabled && pe < n && c->qr_la_sms > 0 && cs == c0;
+  const int64_t wa = la ? std::min<int64_t>(c->b, cw) : 0;
+  const int res = std::max(8, std::min(c->qr_la_sms, c->sms / 2));
+  if (la) {
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, wa, w, -1.0f, V, c->ld, c->mid, c->ld_t, 1.0f, C, c->ld, C,
+                    c->ld));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      RegionF ra{C, c->ld, rows, wa, c->b};
+      ABFT_TRY(blocksum(c->st, ra, s_sums(c, r0, cs, true)));
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, 0, 1));
+      smark(c, SP_ABFT, false);
+    }
+    CUDA_TRY(cudaEventRecord(c->ev_a, c->st));
+    CUDA_TRY(cudaStreamWaitEvent(c->st2, c->ev_a, 0));
+    ABFT_TRY(s_qr_panel(c, c->st2, k + 1, res, &c->gws2));
+    CUDA_TRY(cudaEventRecord(c->ev_p, c->st2));
+  }
+  if (cw > wa) {
+    const float* midb = c->mid + wa * c->ld_t;
+    float* Cb = C + wa * c->ld;
+    FusedSums fs;
+    if (fuse) fs = s_fused(c, r0, cs + wa);
+    smark(c, SP_TMU, true);
+    ABFT_TRY(s_gemm(c, 'N', 'N', rows, cw - wa, w, -1.0f, V, c->ld, midb, c->ld_t, 1.0f, Cb, c->ld,
+                    Cb, c->ld, fuse ? &fs : nullptr, la ? c->sms - res : 0));
+    smark(c, SP_TMU, false);
+    if (prot) {
+      smark(c, SP_ABFT, true);
+      if (!fuse) {
+        RegionF rb{Cb, c->ld, rows, cw - wa, c->b};
+        ABFT_TRY(blocksum(c->st, rb, s_sums(c, r0, cs + wa, true)));
+      }
+      ABFT_TRY(s_verify_sub(c, k, scheme, correct, r0, c0, rows, cols, j0 + (wa ? 1 : 0),
+                            ncb - (wa ? 1 : 0)));
+      smark(c, SP_ABFT, false);
+    }
+  }
+  if (la) {
+    CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
+    c->qr_count = (int)(k + 2);
+    ABFT_TRY(s_emit_column(c, k + 1));
+    c->pd_ready = k + 1;
+  }
+  return 0;
+}
+
 int s_stream_chunk(const abft_sctx* c) {
   if (c->lu_chunk >= 0) return c->lu_chunk;
-  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 4) : 0;
+  return c->kind == ABFT_LU ? (int)std::max<int64_t>(1, c->nb / 4) : 1;
 }
 
 int64_t s_stream_split(const abft_sctx* c) {
-  if (c->kind != ABFT_LU || s_stream_chunk(c) <= 0 || c->nb < 4) return 0;
-  const int64_t s = c->lu_split >= 0 ? c->lu_split : c->nb / 4;
+  if (c->kind == ABFT_CHOLESKY || s_stream_chunk(c) <= 0 || c->nb < 4) return 0;
+  const int64_t s = c->lu_split >= 0 ? c->lu_split : (c->kind == ABFT_LU ? c->nb / 4 : 3);
   return std::max<int64_t>(1, std::min(s, c->nb - 1));
 }
 
@@ -1160,11 +1281,15 @@ int s_lu_stream_chunks(abft_sctx* c, int64_t split, int scheme, const int32_t* s
                        int correct) {
   const int64_t b = c->b, n = c->n;
   auto sch = [&](int64_t k) { return schemes ? schemes[k] : scheme; };
-  if (!c->linv_store) ABFT_TRY(salloc(&c->linv_store, c->ld_t * b * c->nb, c->st));
+  if (c->kind == ABFT_LU && !c->linv_store)
+    ABFT_TRY(salloc(&c->linv_store, c->ld_t * b * c->nb, c->st));
   if (!c->el_store) ABFT_TRY(salloc(&c->el_store, c->ld_cs * b * c->nb, c->st));
   c->pd_ready = -1;
+  const bool lu = c->kind == ABFT_LU;
+  c->el_ok.assign(c->nb, 0);
   auto run = [&](int64_t k, int64_t cs, int64_t ce) -> int {
     const bool enc = k == 0 || sch(k - 1) == ABFT_NONE;
+    if (!lu) return s_qr_tmu_win(c, k, sch(k), correct, cs, ce, enc);
     smark(c, SP_PU, true);
     ABFT_TRY(s_pu_win(c, k, cs, ce));
     smark(c, SP_PU, false);
@@ -1183,29 +1308,34 @@ int s_lu_stream_chunks(abft_sctx* c, int64_t split, int scheme, const int32_t* s
           ABFT_TRY(s_emit_column(c, k));
         }
         c->pd_ready = -1;
-        const int64_t pe = std::min((k + 1) * b, n);
-        ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t, b, b));
-        // E_L of panel k as s_maintain would take it: the L21 epilogue's, else a pass
-        double* el = c->el_store + k * c->ld_cs * b;
-        const int64_t nbr = (n - pe + b - 1) / b;
-        if (c->el_for == k) {
-          ABFT_TRY(copy_matrix(c->st, c->el, c->ld_cs, el, c->ld_cs, 2 * nbr, b));
-        } else if (pe < n) {
-          RegionF rl{c->m + pe + k * b * c->ld, c->ld, n - pe, b, b};
-          SumOut o;
-          o.cp = el;
-          o.cp_ld = c->ld_cs;
-          o.cp_step = 2;
-          o.cw = el + 1;
-          o.cw_ld = c->ld_cs;
-          o.cw_step = 2;
-          ABFT_TRY(blocksum(c->st, rl, o));
+        if (lu) {
+          const int64_t pe = std::min((k + 1) * b, n);
+          ABFT_TRY(copy_matrix(c->st, c->linv, c->ld_t, c->linv_store + k * c->ld_t * b, c->ld_t,
+                               b, b));
+          // E_L of panel k as s_maintain would take it: the L21 epilogue's, else a pass
+          double* el = c->el_store + k * c->ld_cs * b;
+          const int64_t nbr = (n - pe + b - 1) / b;
+          if (c->el_for == k) {
+            ABFT_TRY(copy_matrix(c->st, c->el, c->ld_cs, el, c->ld_cs, 2 * nbr, b));
+          } else if (pe < n) {
+            RegionF rl{c->m + pe + k * b * c->ld, c->ld, n - pe, b, b};
+            SumOut o;
+            o.cp = el;
+            o.cp_ld = c->ld_cs;
+            o.cp_step = 2;
+            o.cw = el + 1;
+            o.cw_ld = c->ld_cs;
+            o.cw_step = 2;
+            ABFT_TRY(blocksum(c->st, rl, o));
+          }
         }
       }
       ABFT_TRY(run(k, q0 * b, q1 * b));
     }
   }
-  const int64_t rch = c->lu_rchunk > 0 ? c->lu_rchunk : c->nb;
+  const int64_t rch = c->lu_rchunk > 0 ? c->lu_rchunk
+                      : (c->lu_rchunk == 0 || lu) ? c->nb
+                                                  : std::max<int64_t>(1, c->nb / 8);
   for (int64_t q0 = split; q0 < c->nb; q0 += rch) {
     const int64_t q1 = std::min<int64_t>(q0 + rch, c->nb);
     CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_in[q1 - 1], 0));

@@ -240,7 +240,8 @@ def test_fp32_streamed_input_equals_set_matrix(kind):
 
 @pytest.mark.parametrize("n,chunk,split", [(2048, 3, 7), (2048, -1, -1), (1280, 1, 3), (2048, 4, 15)])
 @pytest.mark.parametrize("schemes", ["full", "single", "mixed"])
-def test_fp32_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, chunk, split, schemes):
+@pytest.mark.parametrize("kind", ["lu", "qr"])
+def test_fp32_streamed_chunked_equals_set_matrix(monkeypatch, kind, n, chunk, split, schemes):
     """Streamed sgetrf input: the left `split` block columns are factored
     chunk by chunk (left-looking over chunks: PU + maintenance + fused update +
     verify per window, the look-ahead's kernels mirrored) while the input
@@ -256,10 +257,10 @@ def test_fp32_streamed_lu_chunked_equals_set_matrix(monkeypatch, n, chunk, split
     cyc = ["full", "none", "single", "full", "none", "none", "single"]
     sch_list = [cyc[k % len(cyc)] for k in range(nb)] if schemes == "mixed" else None
     scheme = "full" if schemes == "mixed" else schemes
-    a = P.generate_test_matrix("lu", n, seed)
-    f1 = P.SFactorization("lu", a, b)
+    a = P.generate_test_matrix(kind, n, seed)
+    f1 = P.SFactorization(kind, a, b)
     r1 = f1.run_protected(scheme, sched, np.random.default_rng(seed), schemes=sch_list)
-    f2 = P.SFactorization("lu", a, b)
+    f2 = P.SFactorization(kind, a, b)
     lib = f2._lib
     fp = ctypes.POINTER(ctypes.c_float)
     junk = np.asfortranarray(np.random.default_rng(2).standard_normal((n, n)), dtype=np.float32)
