@@ -300,6 +300,22 @@ class Factorization:
     def _dirty(self) -> None:
         self._m_cache = None
 
+    def stream_input(self, a: np.ndarray) -> None:
+        """abft_set_matrix_streamed: the host matrix (n x n float64, Fortran
+        order; pinned for asynchronous copies) moves to the device block column
+        by block column inside the next run_protected call, overlapped with
+        the factorization (LU / QR factor their first panels as they arrive).
+        The array is held until that call returns."""
+        if a.shape != (self.n, self.n) or a.dtype != np.float64 or not a.flags.f_contiguous:
+            raise ValueError("a must be an n x n float64 Fortran-ordered array")
+        check(self._lib.abft_set_matrix_streamed(self._ctx, _lib.dptr(a), self.n))
+        self._streamed_in = a
+        self._m_cache = None
+
+    def set_input_chunks(self, chunk: int = -1, split: int = -1, right_chunk: int = -1) -> None:
+        """abft_set_input_chunks (-1: built-in; chunk 0: wait for all input)."""
+        check(self._lib.abft_set_input_chunks(self._ctx, int(chunk), int(split), int(right_chunk)))
+
     def _set_qr_count(self, q: int) -> None:
         # panels beyond q are re-produced by the next PD(k) (del qr_t[n:])
         check(self._lib.abft_set_qr_panels(self._ctx, int(q)))

@@ -112,6 +112,7 @@ def run_protected(factors: Factorization, scheme, fault_schedule: dict | None = 
     finally:
         if out is not None:
             factors._lib.abft_stream_out(factors._ctx, None, 0)
+        factors._streamed_in = None  # the streamed input was consumed by this call
     out, pos = [], 0
     for k in range(k0, nb):
         r = reports[k]

@@ -60,6 +60,20 @@ class SFactorization:
         host = np.asfortranarray(np.asarray(a, dtype=np.float32))
         check(self._lib.abft_s_set_matrix(self._ctx, _lib.fptr(host), self.n))
 
+    def stream_input(self, a: np.ndarray) -> None:
+        """abft_s_set_matrix_streamed: the host matrix (n x n float32, Fortran
+        order; pinned for asynchronous copies) moves to the device block column
+        by block column inside the next run_protected call, overlapped with
+        the factorization. The array is held until that call returns."""
+        if a.shape != (self.n, self.n) or a.dtype != np.float32 or not a.flags.f_contiguous:
+            raise ValueError("a must be an n x n float32 Fortran-ordered array")
+        check(self._lib.abft_s_set_matrix_streamed(self._ctx, _lib.fptr(a), self.n))
+        self._streamed_in = a
+
+    def set_input_chunks(self, chunk: int = -1, split: int = -1, right_chunk: int = -1) -> None:
+        """abft_s_set_input_chunks (-1: built-in; chunk 0: wait for all input)."""
+        check(self._lib.abft_s_set_input_chunks(self._ctx, int(chunk), int(split), int(right_chunk)))
+
     def reset(self) -> None:
         check(self._lib.abft_s_reset(self._ctx))
 
@@ -139,6 +153,7 @@ class SFactorization:
         finally:
             if out is not None:
                 self._lib.abft_s_stream_out(self._ctx, None, 0)
+            self._streamed_in = None  # the streamed input was consumed by this call
         out, pos = [], 0
         for k in range(k0, nb):
             r = reports[k]

@@ -201,3 +201,35 @@ def test_streamed_chunked_equals_set_matrix(monkeypatch, kind, n, b, chunk, spli
         for k in range(nb):
             assert np.array_equal(f2.qr_t[k], f1.qr_t[k])
             assert np.array_equal(f2._qr_vs[k], f1._qr_vs[k])
+
+
+@pytest.mark.parametrize("kind", ["lu", "qr", "cholesky"])
+def test_stream_input_python_api(kind):
+    """Factorization.stream_input + run_protected(out=...): the public-API
+    form of the streamed input (built-in chunking) gives the reports and the
+    factor of the ordinary input path; fp32 likewise (SFactorization)."""
+    n, b = 2048, 128
+    nb = n // b
+    sched = {nb // 2 + 1: {P.ErrorKind.D0: 1}}
+    a = P.generate_test_matrix(kind, n, 13)
+    f1 = P.Factorization(kind, a, b)
+    ref = [report_json(r) for r in P.run_protected(f1, "full", sched, np.random.default_rng(13))]
+    f2 = P.Factorization(kind, np.zeros((n, n)), b)
+    f2.stream_input(np.asfortranarray(a))
+    out = np.empty((n, n), order="F")
+    got = [report_json(r) for r in P.run_protected(f2, "full", sched, np.random.default_rng(13),
+                                                   out=out)]
+    assert got == ref and sum(len(r["locations"]) for r in got) == 1
+    m1 = f1.m if kind != "cholesky" else np.tril(f1.m)
+    m2 = out if kind != "cholesky" else np.tril(out)
+    np.testing.assert_allclose(m2, m1, rtol=0, atol=1e-12 * max(1.0, np.abs(m1).max()))
+    if kind != "cholesky":
+        assert np.array_equal(out, f1.m)
+    s1 = P.SFactorization(kind, a, b)
+    r1 = s1.run_protected("full", sched, np.random.default_rng(13))
+    s2 = P.SFactorization(kind, np.zeros((n, n), dtype=np.float32), b)
+    s2.stream_input(np.asfortranarray(a, dtype=np.float32))
+    r2 = s2.run_protected("full", sched, np.random.default_rng(13))
+    assert [r.locations for r in r1] == [r.locations for r in r2]
+    if kind != "cholesky":
+        assert np.array_equal(s2.m, s1.m)
