@@ -271,13 +271,33 @@ void region_of(const abft_ctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 
 // Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
 // its device-to-host copy on the copy stream behind the main stream's work.
+// Unpivoted LU emits its U rows earlier (emit_rowblock, after each PU), so a
+// column block here carries only rows >= k b: the D2H of the late, tall U
+// columns no longer piles up behind the last iterations (dgetrf N = 32768:
+// the streamed output added 23 ms to the call before).
 int emit_column(abft_ctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
+  const int64_t r0 = (c->kind == ABFT_LU && !c->pivot) ? p : 0;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
-  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p * c->out_ld, c->out_ld * 8, c->m + p * c->ld, c->ld * 8,
-                             c->n * 8, w, cudaMemcpyDeviceToHost, c->st_out));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 8, c->m + r0 + p * c->ld,
+                             c->ld * 8, (c->n - r0) * 8, w, cudaMemcpyDeviceToHost, c->st_out));
+  return 0;
+}
+
+// Unpivoted LU: row block k of U over columns [cs, ce) is final after PU(k)
+// (nothing updates it again): queue its D2H.
+int emit_rowblock(abft_ctx* c, int64_t k, int64_t cs, int64_t ce) {
+  if (!c->out_host || c->kind != ABFT_LU || c->pivot) return 0;
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
+  cs = std::max(cs, pe);
+  ce = std::min(ce, c->n);
+  if (cs >= ce) return 0;
+  CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p + cs * c->out_ld, c->out_ld * 8, c->m + p + cs * c->ld,
+                             c->ld * 8, w * 8, ce - cs, cudaMemcpyDeviceToHost, c->st_out));
   return 0;
 }
 
@@ -1019,6 +1039,7 @@ int protected_tmu_lu_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
   c->sums_valid = prot;
   CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
   ABFT_TRY(emit_column(c, k + 1));
+  ABFT_TRY(emit_rowblock(c, k + 1, 0, n));
   c->pd_ready = k + 1;
   c->pu_ready = k + 1;
   return 0;
@@ -1048,7 +1069,8 @@ int lu_pu_win(abft_ctx* c, int64_t k, int64_t cs, int64_t ce) {
   const double* linv = c->linv_store + k * c->ld_t * c->b;
   ABFT_TRY(gemm(c->st, 'N', 'N', (int)w, (int)(ce - cs), (int)w, 1.0, linv, c->ld_t,
                 c->m + p + cs * c->ld, c->ld, 0.0, nullptr, 0, c->uw, c->ld_t, &c->gws));
-  return copy_matrix(c->st, c->uw, c->ld_t, c->m + p + cs * c->ld, c->ld, w, ce - cs);
+  ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, c->m + p + cs * c->ld, c->ld, w, ce - cs));
+  return emit_rowblock(c, k, cs, ce);
 }
 
 // maintain() of LU iteration k for the region columns [cs, ce): writes the
@@ -1586,6 +1608,7 @@ int run_iteration_device(abft_ctx* c, int64_t k, int scheme, const abft_fault* p
     ABFT_TRY(task_pu(c, k));
     prof_mark(c, PROF_PU, false);
     if (c->kind == ABFT_CHOLESKY) ABFT_TRY(emit_column(c, k));
+    ABFT_TRY(emit_rowblock(c, k, 0, c->n));
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {

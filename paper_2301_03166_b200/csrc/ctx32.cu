@@ -214,13 +214,30 @@ void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 
 // Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
 // its device-to-host copy on the copy stream (as ctx.cu).
+// LU emits its U rows after each PU (s_emit_rowblock, as ctx.cu), so a
+// column block carries only rows >= k b.
 int s_emit_column(abft_sctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
+  const int64_t r0 = c->kind == ABFT_LU ? p : 0;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
-  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p * c->out_ld, c->out_ld * 4, c->m + p * c->ld, c->ld * 4,
-                             c->n * 4, w, cudaMemcpyDeviceToHost, c->st_out));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 4, c->m + r0 + p * c->ld,
+                             c->ld * 4, (c->n - r0) * 4, w, cudaMemcpyDeviceToHost, c->st_out));
+  return 0;
+}
+
+// LU: row block k of U over columns [cs, ce) is final after PU(k).
+int s_emit_rowblock(abft_sctx* c, int64_t k, int64_t cs, int64_t ce) {
+  if (!c->out_host || c->kind != ABFT_LU) return 0;
+  const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
+  cs = std::max(cs, pe);
+  ce = std::min(ce, c->n);
+  if (cs >= ce) return 0;
+  CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
+  CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
+  CUDA_TRY(cudaMemcpy2DAsync(c->out_host + p + cs * c->out_ld, c->out_ld * 4, c->m + p + cs * c->ld,
+                             c->ld * 4, w * 4, ce - cs, cudaMemcpyDeviceToHost, c->st_out));
   return 0;
 }
 
@@ -1037,7 +1054,8 @@ int s_pu_win(abft_sctx* c, int64_t k, int64_t cs, int64_t ce) {
   ABFT_TRY(s_gemm(c, 'N', 'N', w, ce - cs, w, 1.0f, c->linv_store + k * c->ld_t * c->b, c->ld_t,
                   U12, c->ld, 0.0f, nullptr, 0, c->uw, c->ld_t, fuse ? &fs : nullptr));
   c->er_for = fuse ? k : -1;
-  return copy_matrix(c->st, c->uw, c->ld_t, U12, c->ld, w, ce - cs);
+  ABFT_TRY(copy_matrix(c->st, c->uw, c->ld_t, U12, c->ld, w, ce - cs));
+  return s_emit_rowblock(c, k, cs, ce);
 }
 
 // s_maintain of LU iteration k for region columns [cs, ce) (E_L kept per panel).
@@ -1364,6 +1382,7 @@ int s_iteration(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan, int
     ABFT_TRY(s_pu(c, k));
     smark(c, SP_PU, false);
     if (c->kind == ABFT_CHOLESKY) ABFT_TRY(s_emit_column(c, k));
+    ABFT_TRY(s_emit_rowblock(c, k, 0, c->n));
     return 0;
   };
   if (c->kind == ABFT_CHOLESKY) {
