@@ -278,7 +278,7 @@ void region_of(const abft_ctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 int emit_column(abft_ctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
-  const int64_t r0 = (c->kind == ABFT_LU && !c->pivot) ? p : 0;
+  const int64_t r0 = ((c->kind == ABFT_LU && !c->pivot) || c->kind == ABFT_CHOLESKY) ? p : 0;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
   CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 8, c->m + r0 + p * c->ld,
@@ -287,9 +287,10 @@ int emit_column(abft_ctx* c, int64_t k) {
 }
 
 // Unpivoted LU: row block k of U over columns [cs, ce) is final after PU(k)
-// (nothing updates it again): queue its D2H.
+// (nothing updates it again): queue its D2H. Cholesky: the same row block is
+// zeroed by PU(k) (linalg.py:251-252) and final too.
 int emit_rowblock(abft_ctx* c, int64_t k, int64_t cs, int64_t ce) {
-  if (!c->out_host || c->kind != ABFT_LU || c->pivot) return 0;
+  if (!c->out_host || c->kind == ABFT_QR || c->pivot) return 0;
   const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
   cs = std::max(cs, pe);
   ce = std::min(ce, c->n);

@@ -214,12 +214,12 @@ void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 
 // Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
 // its device-to-host copy on the copy stream (as ctx.cu).
-// LU emits its U rows after each PU (s_emit_rowblock, as ctx.cu), so a
-// column block carries only rows >= k b.
+// LU / Cholesky emit row block k after PU(k) (s_emit_rowblock, as ctx.cu), so
+// a column block carries only rows >= k b.
 int s_emit_column(abft_sctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
-  const int64_t r0 = c->kind == ABFT_LU ? p : 0;
+  const int64_t r0 = c->kind != ABFT_QR ? p : 0;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
   CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 4, c->m + r0 + p * c->ld,
@@ -229,7 +229,7 @@ int s_emit_column(abft_sctx* c, int64_t k) {
 
 // LU: row block k of U over columns [cs, ce) is final after PU(k).
 int s_emit_rowblock(abft_sctx* c, int64_t k, int64_t cs, int64_t ce) {
-  if (!c->out_host || c->kind != ABFT_LU) return 0;
+  if (!c->out_host || c->kind == ABFT_QR) return 0;  // LU: U rows; Cholesky: zeroed rows
   const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
   cs = std::max(cs, pe);
   ce = std::min(ce, c->n);

@@ -216,10 +216,15 @@ def test_stream_input_python_api(kind):
     ref = [report_json(r) for r in P.run_protected(f1, "full", sched, np.random.default_rng(13))]
     f2 = P.Factorization(kind, np.zeros((n, n)), b)
     f2.stream_input(np.asfortranarray(a))
-    out = np.empty((n, n), order="F")
+    out = np.full((n, n), np.nan, order="F")  # every entry must arrive
     got = [report_json(r) for r in P.run_protected(f2, "full", sched, np.random.default_rng(13),
                                                    out=out)]
     assert got == ref and sum(len(r["locations"]) for r in got) == 1
+    assert not np.isnan(out).any()
+    assert np.array_equal(out, f2.m)
+    if kind == "cholesky":  # the row blocks right of the diagonal arrive zeroed
+        for k in range(nb - 1):
+            assert not np.any(out[k * b:(k + 1) * b, (k + 1) * b:])
     m1 = f1.m if kind != "cholesky" else np.tril(f1.m)
     m2 = out if kind != "cholesky" else np.tril(out)
     np.testing.assert_allclose(m2, m1, rtol=0, atol=1e-12 * max(1.0, np.abs(m1).max()))
