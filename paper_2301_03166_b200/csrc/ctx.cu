@@ -278,7 +278,7 @@ void region_of(const abft_ctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 int emit_column(abft_ctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
-  const int64_t r0 = ((c->kind == ABFT_LU && !c->pivot) || c->kind == ABFT_CHOLESKY) ? p : 0;
+  const int64_t r0 = (c->kind == ABFT_LU && c->pivot) ? 0 : p;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
   CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 8, c->m + r0 + p * c->ld,
@@ -288,9 +288,10 @@ int emit_column(abft_ctx* c, int64_t k) {
 
 // Unpivoted LU: row block k of U over columns [cs, ce) is final after PU(k)
 // (nothing updates it again): queue its D2H. Cholesky: the same row block is
-// zeroed by PU(k) (linalg.py:251-252) and final too.
+// zeroed by PU(k) (linalg.py:251-252) and final too. QR: row block k of R is
+// final after the verified TMU(k).
 int emit_rowblock(abft_ctx* c, int64_t k, int64_t cs, int64_t ce) {
-  if (!c->out_host || c->kind == ABFT_QR || c->pivot) return 0;
+  if (!c->out_host || c->pivot) return 0;
   const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
   cs = std::max(cs, pe);
   ce = std::min(ce, c->n);
@@ -810,6 +811,7 @@ int protected_tmu(abft_ctx* c, int64_t k, int scheme, const abft_fault* plan, in
     c->chol_part = -1;
     c->chol_enc_ahead = false;
   }
+  if (c->kind == ABFT_QR) ABFT_TRY(emit_rowblock(c, k, 0, c->n));
   return 0;
 }
 
@@ -1308,7 +1310,7 @@ int qr_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int6
       ABFT_TRY(verify_sub(c, scheme, correct, r0, c0, rows, cols, j0, ncb));
       prof_mark(c, PROF_ABFT, false);
     }
-    return 0;
+    return emit_rowblock(c, k, cs, ce);
   }
   const int64_t wa = std::min<int64_t>(c->b, cw);
   prof_mark(c, PROF_TMU, true);
@@ -1362,6 +1364,7 @@ int qr_tmu_win(abft_ctx* c, int64_t k, int scheme, int correct, int64_t cs, int6
       prof_mark(c, PROF_ABFT, false);
     }
   }
+  ABFT_TRY(emit_rowblock(c, k, cs, ce));
   CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
   c->qr_count = (int)(k + 2);
   ABFT_TRY(emit_column(c, k + 1));
@@ -1573,6 +1576,7 @@ int protected_tmu_qr_lookahead(abft_ctx* c, int64_t k, int scheme, int correct) 
     }
   }
   c->sums_valid = prot;
+  ABFT_TRY(emit_rowblock(c, k, 0, n));
   CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
   c->qr_count = (int)(k + 2);
   ABFT_TRY(emit_column(c, k + 1));

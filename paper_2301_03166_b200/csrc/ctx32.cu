@@ -214,12 +214,12 @@ void s_region(const abft_sctx* c, int64_t k, int64_t* r0, int64_t* c0, int64_t* 
 
 // Column block k is final (LU/QR after PD(k), Cholesky after PU(k)): queue
 // its device-to-host copy on the copy stream (as ctx.cu).
-// LU / Cholesky emit row block k after PU(k) (s_emit_rowblock, as ctx.cu), so
-// a column block carries only rows >= k b.
+// LU / Cholesky emit row block k after PU(k), QR after TMU(k) (s_emit_rowblock,
+// as ctx.cu), so a column block carries only rows >= k b.
 int s_emit_column(abft_sctx* c, int64_t k) {
   if (!c->out_host) return 0;
   const int64_t p = k * c->b, w = std::min(c->b, c->n - p);
-  const int64_t r0 = c->kind != ABFT_QR ? p : 0;
+  const int64_t r0 = p;
   CUDA_TRY(cudaEventRecord(c->ev_out, c->st));
   CUDA_TRY(cudaStreamWaitEvent(c->st_out, c->ev_out, 0));
   CUDA_TRY(cudaMemcpy2DAsync(c->out_host + r0 + p * c->out_ld, c->out_ld * 4, c->m + r0 + p * c->ld,
@@ -229,7 +229,7 @@ int s_emit_column(abft_sctx* c, int64_t k) {
 
 // LU: row block k of U over columns [cs, ce) is final after PU(k).
 int s_emit_rowblock(abft_sctx* c, int64_t k, int64_t cs, int64_t ce) {
-  if (!c->out_host || c->kind == ABFT_QR) return 0;  // LU: U rows; Cholesky: zeroed rows
+  if (!c->out_host) return 0;  // LU: U rows; Cholesky: zeroed rows; QR: R rows after TMU(k)
   const int64_t p = k * c->b, pe = std::min(p + c->b, c->n), w = pe - p;
   cs = std::max(cs, pe);
   ce = std::min(ce, c->n);
@@ -847,6 +847,7 @@ int s_protected_tmu(abft_sctx* c, int64_t k, int scheme, const abft_fault* plan,
     c->chol_part = -1;
     c->chol_enc_ahead = false;
   }
+  if (c->kind == ABFT_QR) ABFT_TRY(s_emit_rowblock(c, k, 0, n));
   return 0;
 }
 
@@ -950,6 +951,7 @@ int s_tmu_qr_lookahead(abft_sctx* c, int64_t k, int scheme, int correct) {
     }
   }
   c->sums_valid = prot;
+  ABFT_TRY(s_emit_rowblock(c, k, 0, n));
   CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
   c->qr_count = (int)(k + 2);
   ABFT_TRY(s_emit_column(c, k + 1));
@@ -1275,6 +1277,7 @@ int s_qr_tmu_win(abft_sctx* c, int64_t k, int scheme, int correct, int64_t cs, i
       smark(c, SP_ABFT, false);
     }
   }
+  ABFT_TRY(s_emit_rowblock(c, k, cs, ce));
   if (la) {
     CUDA_TRY(cudaStreamWaitEvent(c->st, c->ev_p, 0));
     c->qr_count = (int)(k + 2);

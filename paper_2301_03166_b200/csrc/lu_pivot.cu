@@ -154,7 +154,12 @@ __global__ void __launch_bounds__(PT)
         const double piv = s_u[j];
         if (!(piv != 0.0) || !isfinite(piv)) {
           s_bad = 1;
-          if (gi == 0) atomicCAS(info, 0, (int)(col_base + j + 1));
+          if (gi == 0) {
+            atomicCAS(info, 0, (int)(col_base + j + 1));
+            // the columns after the breakdown are not factored: no interchanges
+            // (laswp still runs on them; stale ipiv entries sent it out of bounds)
+            for (int jj = j + 1; jj < w; ++jj) ipiv[jj] = (int32_t)jj;
+          }
         }
         if (gi == 0) ipiv[j] = (int32_t)s_piv;
       }
