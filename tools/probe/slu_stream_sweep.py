@@ -13,11 +13,12 @@ pin_in[...] = arm.host.T
 src = pin_in.T
 pin_out = torch.empty((n, n), dtype=torch.float32, pin_memory=True).numpy().T
 P.linalg.check(lib.abft_s_keep_input(f._ctx, 0))
-cfgs = [(0, -1), (-1, -1), (8, 32), (16, 64), (4, 24)]
+cfgs = [(0, -1, 0), (-1, -1, 0), (8, 32, 0), (16, 64, 0), (4, 24, 0)]
 if len(sys.argv) > 1:
-    cfgs = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:]]
-for chunk, split in cfgs:
-    lib.abft_s_set_input_chunks(f._ctx, chunk, split, 0)
+    cfgs = [tuple(int(x) for x in a.split(",")) + ((0,) if a.count(",") == 1 else ())
+            for a in sys.argv[1:]]
+for chunk, split, rch in cfgs:
+    lib.abft_s_set_input_chunks(f._ctx, chunk, split, rch)
     ts, dev = [], []
     for i in range(4):
         t0 = time.perf_counter()
@@ -31,6 +32,6 @@ for chunk, split in cfgs:
         if i:
             ts.append((t2 - t0, t2 - t1))
             dev.append(el.value)
-    print(f"chunk={chunk} split={split} wall {statistics.median(t[0] for t in ts)*1e3:.1f} ms "
+    print(f"chunk={chunk} split={split} rch={rch} wall {statistics.median(t[0] for t in ts)*1e3:.1f} ms "
           f"(run_protected {statistics.median(t[1] for t in ts)*1e3:.1f}) device call "
           f"{statistics.median(dev):.1f} ms", flush=True)
